@@ -1,0 +1,4 @@
+// Forwarding header: keeps `#include "traincap/net_model.hpp"` source-compatible with the
+// reference layout; the declarations live in api.hpp.
+#pragma once
+#include "traincap/api.hpp"
