@@ -1,0 +1,165 @@
+/*
+ * tcb.h — C-ABI of the B200 training-step library (libtcb.so).
+ *
+ * The reference (arXiv 1709.06622 `traincap`, /root/reference/proj) has no
+ * device code and no FFI: its hot path enters through the C++ planner's
+ * measurement boundary — per-layer conv cost rows (`CostEntry`,
+ * /root/reference/proj/include/traincap/catalog.hpp:19-27), the step trace
+ * (`StepTrace`, /root/reference/proj/include/traincap/io.hpp:23-26) and the
+ * parameter-server sizing inputs (`ClusterSpec`,
+ * /root/reference/proj/include/traincap/scale_plan.hpp:39-44). Every entry
+ * point below produces or consumes one of those quantities; the comment on
+ * each names the reference interface it feeds. INTEGRATION.md shows the
+ * bindings a maintainer adds on the reference side.
+ *
+ * Conventions
+ *   - plain pointers + sizes; device pointers are caller-owned CUDA device
+ *     memory; `stream` is a cudaStream_t passed as void*.
+ *   - every call returns TCB_OK (0) or a negative status; the message of the
+ *     last failure on the calling thread is tcb_last_error().
+ *   - handles are not thread-safe: one host thread per GPU.
+ *   - tensors are NHWC; conv weights are KRSC ([out][fh][fw][in]).
+ *   - dtype of activations/weights follows the plan precision:
+ *       TCB_PREC_FFMA_FP32 -> float,  TCB_PREC_BF16 -> bf16 (uint16_t bits).
+ *     Weight gradients are always fp32 (they land in the PS flat buffer).
+ */
+#ifndef TCB_H_
+#define TCB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    TCB_OK = 0,
+    TCB_ERR_INVALID = -1,     /* bad argument (maps to traincap::DomainError)   */
+    TCB_ERR_UNSUPPORTED = -2, /* algorithm/precision not applicable to geometry */
+    TCB_ERR_CUDA = -3,        /* CUDA runtime failure                           */
+    TCB_ERR_NCCL = -4,        /* NCCL failure                                   */
+    TCB_ERR_OOM = -5,         /* workspace does not fit: infeasible CostEntry   */
+    TCB_ERR_INTERNAL = -6
+};
+
+typedef enum { TCB_ALGO_GEMM = 0, TCB_ALGO_WINOGRAD = 1, TCB_ALGO_FFT = 2 } tcb_algo;
+typedef enum { TCB_PREC_FFMA_FP32 = 0, TCB_PREC_TF32 = 1, TCB_PREC_BF16 = 2 } tcb_prec;
+typedef enum { TCB_DT_F32 = 0, TCB_DT_BF16 = 1 } tcb_dtype;
+
+/* One convolution (geometry of Eq 1, generalised to rectangular filters). */
+typedef struct tcb_conv_geom {
+    int n, h, w, c;         /* input  N x H x W x C                      */
+    int k, r, s;            /* K filters of R x S                        */
+    int pad_h, pad_w;       /* symmetric zero padding                    */
+    int stride_h, stride_w; /* strides                                   */
+} tcb_conv_geom;
+
+typedef struct tcb_conv_plan tcb_conv_plan;
+
+/* ---------------------------------------------------------------- status -- */
+const char* tcb_last_error(void);
+const char* tcb_version(void);
+int tcb_device_count(int* count);
+int tcb_device_init(int device);
+
+/* Output spatial size, Eq 1: floor((in - f + 2p)/s) + 1
+ * (traincap::propagate_shapes, /root/reference/proj/src/net_model.cpp:80-99). */
+int tcb_conv_out_hw(const tcb_conv_geom* g, int* ho, int* wo);
+
+/* ------------------------------------------------------------ conv plans -- */
+/* Builds a plan for (geometry, algorithm, precision). Returns
+ * TCB_ERR_UNSUPPORTED when the algorithm does not apply (e.g. Winograd on a
+ * non-3x3/stride-1 layer) so the profiler omits that CostEntry, matching the
+ * catalog's "absent algorithm is a value" rule
+ * (/root/reference/proj/include/traincap/catalog.hpp:60-62).
+ * *workspace_bytes receives the plan's scratch need; the profiler records it
+ * as CostEntry::memory_bits = 8 * workspace_bytes. */
+int tcb_conv_plan_create(const tcb_conv_geom* g, int algo, int prec, tcb_conv_plan** plan,
+                         size_t* workspace_bytes);
+int tcb_conv_plan_destroy(tcb_conv_plan* plan);
+
+/* y = act(conv(x, w) + bias + residual); bias (fp32, K) and residual (same
+ * dtype/shape as y) may be NULL; relu != 0 applies max(0, .). */
+int tcb_conv_fwd(const tcb_conv_plan* plan, const void* x, const void* w, const float* bias,
+                 const void* residual, int relu, void* y, void* workspace, void* stream);
+
+/* dx = (conv^T(dy, w) + residual_grad) * [mask_act > 0]; residual_grad and
+ * mask_act (activation whose ReLU is undone) may be NULL. */
+int tcb_conv_dgrad(const tcb_conv_plan* plan, const void* dy, const void* w,
+                   const void* residual_grad, const void* mask_act, void* dx, void* workspace,
+                   void* stream);
+
+/* dw = sum_{n,ho,wo} dy (x) x  (fp32, KRSC) and db = sum dy (fp32, K; may be
+ * NULL). Deterministic (fixed-order split reduction, no float atomics). */
+int tcb_conv_wgrad(const tcb_conv_plan* plan, const void* dy, const void* x, float* dw,
+                   float* db, void* workspace, void* stream);
+
+/* --------------------------------------------------------- other layers -- */
+/* max pool (pooling layers of the chain: depth preserved, Eq 1 geometry). */
+int tcb_maxpool_fwd(int dtype, const void* x, void* y, uint8_t* argmax, int n, int h, int w,
+                    int c, int f, int stride, int pad, void* stream);
+int tcb_maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, void* dx, int n, int h,
+                    int w, int c, int f, int stride, int pad, void* stream);
+int tcb_avgpool_global_fwd(int dtype, const void* x, void* y, int n, int hw, int c, void* stream);
+int tcb_avgpool_global_bwd(int dtype, const void* dy, void* dx, int n, int hw, int c,
+                           void* stream);
+/* mean softmax cross-entropy over n rows of `classes` logits; writes
+ * dlogits = (softmax - onehot)/n and the mean loss (device float). */
+int tcb_softmax_xent(int dtype, const void* logits, const int32_t* labels, void* dlogits,
+                     float* loss, int n, int classes, void* stream);
+
+/* ------------------------------------------------------ synthetic inputs -- */
+/* Counter-based uniform fill, identical stream on CPU (oracle) and GPU:
+ * u = splitmix64(seed ^ tag*0x9E3779B97F4A7C15 ^ i) -> 24-bit -> [lo, hi). */
+int tcb_fill_uniform(int dtype, void* p, size_t n, uint64_t seed, uint64_t tag, float lo,
+                     float hi, void* stream);
+int tcb_fill_labels(int32_t* labels, int n, int classes, uint64_t seed, void* stream);
+int tcb_cast(int src_dtype, const void* src, int dst_dtype, void* dst, size_t n, void* stream);
+
+/* ----------------------------------------------------- parameter update -- */
+/* Fused momentum SGD on one PS shard (paper step 6):
+ *   g' = grad*grad_scale + weight_decay*w;  v = momentum*v + g';  w -= lr*v
+ * and refreshes the compute-dtype copy (w_compute, may be NULL). */
+int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_dtype, void* w_compute,
+                     size_t n, float lr, float momentum, float weight_decay, float grad_scale,
+                     void* stream);
+
+/* ------------------------------------------------------------- trainer -- */
+/* A whole data-parallel training step on one GPU: fwd chain -> loss ->
+ * bwd (dgrad + wgrad into the flat PS gradient buffer) -> PS aggregation
+ * (reduce-scatter over NCCL when world > 1) -> fused momentum SGD on the
+ * owned shard -> all-gather of updated weights. Model and options are a JSON
+ * document (see paper_1709_06622_b200/models.py). */
+typedef struct tcb_trainer tcb_trainer;
+
+int tcb_trainer_create(const char* config_json, tcb_trainer** out);
+int tcb_trainer_destroy(tcb_trainer* t);
+/* NCCL unique id for rank 0 to broadcast (128 bytes). */
+int tcb_nccl_unique_id(uint8_t* id128);
+/* Join a world of `world` ranks (one process per GPU). world == 1 needs no id. */
+int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t* id128);
+/* Loads a mini-batch from HOST memory (NHWC fp32 images, int32 labels). NULL
+ * images = keep the device-resident synthetic batch. */
+int tcb_trainer_set_batch(tcb_trainer* t, const float* host_images, const int32_t* host_labels,
+                          void* stream);
+int tcb_trainer_step(tcb_trainer* t, void* stream);
+int tcb_trainer_loss(tcb_trainer* t, float* loss_host, void* stream);
+/* Per-phase device times of the last timed step (ms): fwd, bwd, reduce-scatter,
+ * sgd, all-gather — the StepTrace the Lemma-1 estimate consumes. */
+int tcb_trainer_phase_times(tcb_trainer* t, float* ms5);
+int tcb_trainer_enable_timing(tcb_trainer* t, int on);
+/* Introspection for tests: JSON description of the layer table, flat-buffer
+ * layout (per-layer offsets) and shard table; caller frees with tcb_free. */
+int tcb_trainer_describe(tcb_trainer* t, char** json_out);
+/* Device pointers of named tensors ("param", "grad", "momentum", "act:<i>",
+ * "dact:<i>", "input", "labels", "logits", "wcompute"). */
+int tcb_trainer_tensor(tcb_trainer* t, const char* name, void** ptr, size_t* bytes);
+/* Count of kernels launched by the last step (for the bench's gpu_launches). */
+int tcb_trainer_launch_count(tcb_trainer* t, int* count);
+void tcb_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCB_H_ */

@@ -1,0 +1,534 @@
+// Tensor-core implicit-GEMM convolution for sm_100a (tcgen05 + TMEM).
+//
+// One warp-specialised, persistent kernel serves all three passes of a conv
+// layer (the GEMM views are in common.cuh::ConvShape):
+//
+//   warps 0-3  producers: gather 16-byte chunks of the implicit im2col
+//              operands straight from NHWC activations with cp.async
+//              (zero-fill handles padding, strides and ragged tiles) into
+//              128B-swizzled shared memory, K-major for fwd/dgrad and
+//              MN-major for wgrad; signal a per-stage mbarrier
+//   warp  8    MMA issuer: one elected thread issues tcgen05.mma
+//              (kind::f16, bf16 x bf16 -> fp32, M=128, N=BN, K=16) into a
+//              double-buffered TMEM accumulator and tcgen05.commit's the
+//              smem stage / accumulator barriers
+//   warps 4-7  epilogue: tcgen05.ld TMEM -> registers, fused bias +
+//              residual + ReLU (fwd) or residual-grad + ReLU-mask (dgrad),
+//              bf16 store; wgrad writes fp32 split-K partials that a fixed-
+//              order reduction folds into the PS gradient buffer.
+//
+// Tiles: BM=128 rows x BN (64/128/256) cols x BK=64 per stage; the grid is
+// min(tiles, #SMs) CTAs, each walking tiles with stride gridDim.x so the
+// epilogue of tile i overlaps the MMAs of tile i+1.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace tcb {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;               // bf16 elements per stage along the reduction
+constexpr int kProducerThreads = 128;
+constexpr int kEpilogueThreads = 128;
+constexpr int kMmaWarp = 8;
+constexpr int kThreads = kProducerThreads + kEpilogueThreads + 32;
+constexpr int kLag = 2;              // cp.async groups a producer keeps in flight
+
+template <int BN>
+struct Cfg {
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+    static constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
+    static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 + 256;
+    static_assert(kStages > kLag, "pipeline depth");
+};
+
+struct Params {
+    ConvShape s;
+    const __nv_bfloat16* a;  // fwd: x   dgrad: dy   wgrad: dy
+    const __nv_bfloat16* b;  // fwd: w   dgrad: wT   wgrad: x
+    void* out;               // bf16 (fwd/dgrad) or fp32 partials [split][M][Ncol] (wgrad)
+    const float* bias;
+    const __nv_bfloat16* residual;
+    const __nv_bfloat16* mask;
+    int relu;
+    int m_tiles, n_tiles, splits, kb_total, kb_per_split, num_tiles;
+};
+
+struct TileCoord {
+    int split, mt, nt, kb_begin, kb_end;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const Params& p, int t) {
+    TileCoord c;
+    c.nt = t % p.n_tiles;
+    const int rest = t / p.n_tiles;
+    c.mt = rest % p.m_tiles;
+    c.split = rest / p.m_tiles;
+    c.kb_begin = c.split * p.kb_per_split;
+    c.kb_end = min(p.kb_total, c.kb_begin + p.kb_per_split);
+    return c;
+}
+
+// 128B swizzle: 16-byte chunk j of a 128-byte row r lands at chunk j ^ (r & 7).
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
+    return row * 128u + ((chunk ^ (row & 7u)) << 4);
+}
+
+// ------------------------------------------------------------ producers ----
+template <ConvMode MODE, int BN>
+__device__ __forceinline__ void load_stage(const Params& p, const TileCoord& tc, int kb,
+                                           uint32_t a_smem, uint32_t b_smem, int tid,
+                                           int row_n, int row_hb, int row_wb, bool row_ok) {
+    const ConvShape& s = p.s;
+    if constexpr (MODE == ConvMode::Fwd || MODE == ConvMode::Dgrad) {
+        // A: one row (pixel) per thread, 8 chunks of 8 channels.
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int kk0 = kb * BK + j * 8;
+            const void* src = p.a;
+            uint32_t bytes = 0;
+            if (row_ok && kk0 < s.Kdim) {
+                uint32_t rs, c0, r, sx;
+                if constexpr (MODE == ConvMode::Fwd) {
+                    s.d_c.divmod(static_cast<uint32_t>(kk0), rs, c0);
+                    s.d_s.divmod(rs, r, sx);
+                    const int hi = row_hb + static_cast<int>(r);
+                    const int wi = row_wb + static_cast<int>(sx);
+                    if (hi >= 0 && hi < s.H && wi >= 0 && wi < s.W) {
+                        src = p.a + ((static_cast<size_t>(row_n) * s.H + hi) * s.W + wi) * s.C + c0;
+                        bytes = 16;
+                    }
+                } else {
+                    s.d_k.divmod(static_cast<uint32_t>(kk0), rs, c0);  // c0 is the k offset here
+                    s.d_s.divmod(rs, r, sx);
+                    int ho = row_hb - static_cast<int>(r);  // row_hb = h + pad_h
+                    int wo = row_wb - static_cast<int>(sx);
+                    bool ok = ho >= 0 && wo >= 0;
+                    if (s.sh > 1) { ok = ok && (ho % s.sh) == 0; ho /= s.sh; }
+                    if (s.sw > 1) { ok = ok && (wo % s.sw) == 0; wo /= s.sw; }
+                    if (ok && ho < s.Ho && wo < s.Wo) {
+                        src = p.a + ((static_cast<size_t>(row_n) * s.Ho + ho) * s.Wo + wo) * s.K + c0;
+                        bytes = 16;
+                    }
+                }
+            }
+            ptx::cp_async_16(a_smem + swz(tid, j), src, bytes);
+        }
+        // B: BN rows of the (transposed) weight matrix, Kdim-contiguous.
+#pragma unroll
+        for (int i = 0; i < BN / 16; ++i) {
+            const int idx = tid + i * kProducerThreads;
+            const int brow = idx >> 3, j = idx & 7;
+            const int col = tc.nt * BN + brow;
+            const int kk0 = kb * BK + j * 8;
+            const bool ok = col < s.Ncol && kk0 < s.Kdim;
+            const void* src = ok ? static_cast<const void*>(p.b + static_cast<size_t>(col) * s.Kdim + kk0)
+                                 : static_cast<const void*>(p.b);
+            ptx::cp_async_16(b_smem + swz(brow, j), src, ok ? 16u : 0u);
+        }
+    } else {
+        // Wgrad, both operands MN-major: smem row = pixel (reduction index),
+        // 128 B = 64 consecutive M (or N) elements, 64-element blocks 8 KB apart.
+        const int P = s.Kdim;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // A = dy: 64 pixels x 128 out-channels
+            const int idx = tid + i * kProducerThreads;
+            const int pl = idx >> 4, ck = idx & 15;
+            const int pix = kb * BK + pl;
+            const int k0 = tc.mt * BM + ck * 8;
+            const bool ok = pix < P && k0 < s.K;
+            const void* src = ok ? static_cast<const void*>(p.a + static_cast<size_t>(pix) * s.K + k0)
+                                 : static_cast<const void*>(p.a);
+            ptx::cp_async_16(a_smem + (ck >> 3) * 8192u + swz(pl, ck & 7), src, ok ? 16u : 0u);
+        }
+        constexpr int kChunksPerRow = BN / 8;
+#pragma unroll 4
+        for (int i = 0; i < BN / 16; ++i) {  // B = im2col(x): 64 pixels x BN (r,s,c) columns
+            const int idx = tid + i * kProducerThreads;
+            const int pl = idx / kChunksPerRow, cn = idx % kChunksPerRow;
+            const int pix = kb * BK + pl;
+            const int col0 = tc.nt * BN + cn * 8;
+            const void* src = p.b;
+            uint32_t bytes = 0;
+            if (pix < P && col0 < s.Ncol) {
+                uint32_t n, rem, ho, wo, rs, c0, r, sx;
+                s.d_howo.divmod(static_cast<uint32_t>(pix), n, rem);
+                s.d_wo.divmod(rem, ho, wo);
+                s.d_c.divmod(static_cast<uint32_t>(col0), rs, c0);
+                s.d_s.divmod(rs, r, sx);
+                const int hi = static_cast<int>(ho) * s.sh - s.ph + static_cast<int>(r);
+                const int wi = static_cast<int>(wo) * s.sw - s.pw + static_cast<int>(sx);
+                if (hi >= 0 && hi < s.H && wi >= 0 && wi < s.W) {
+                    src = p.b + ((static_cast<size_t>(n) * s.H + hi) * s.W + wi) * s.C + c0;
+                    bytes = 16;
+                }
+            }
+            ptx::cp_async_16(b_smem + (cn >> 3) * 8192u + swz(pl, cn & 7), src, bytes);
+        }
+    }
+}
+
+// ------------------------------------------------------------- epilogue ----
+__device__ __forceinline__ void unpack8(uint4 v, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 x = __bfloat1622float2(h[i]);
+        f[2 * i] = x.x;
+        f[2 * i + 1] = x.y;
+    }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+    uint4 v;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return v;
+}
+
+template <ConvMode MODE>
+__device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord& tc, int m,
+                                               int col0, const uint32_t (&acc)[32]) {
+    const ConvShape& s = p.s;
+    if (m >= s.M || col0 >= s.Ncol) return;
+    if constexpr (MODE == ConvMode::Wgrad) {
+        float* out = static_cast<float*>(p.out) +
+                     (static_cast<size_t>(tc.split) * s.M + m) * s.Ncol + col0;
+        if (col0 + 32 <= s.Ncol) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                reinterpret_cast<float4*>(out)[i] =
+                    make_float4(__uint_as_float(acc[4 * i]), __uint_as_float(acc[4 * i + 1]),
+                                __uint_as_float(acc[4 * i + 2]), __uint_as_float(acc[4 * i + 3]));
+        } else {
+            for (int i = 0; i < 32 && col0 + i < s.Ncol; ++i) out[i] = __uint_as_float(acc[i]);
+        }
+    } else {
+        const size_t base = static_cast<size_t>(m) * s.Ncol + col0;
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + base;
+        const bool full = col0 + 32 <= s.Ncol;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(acc[8 * g + i]);
+            const int c = col0 + 8 * g;
+            if (full) {
+                if (p.bias) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] += __ldg(p.bias + c + i);
+                }
+                if (p.residual) {
+                    float r[8];
+                    unpack8(__ldg(reinterpret_cast<const uint4*>(p.residual + base + 8 * g)), r);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] += r[i];
+                }
+                if (p.relu) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+                }
+                if (p.mask) {
+                    float mk[8];
+                    unpack8(__ldg(reinterpret_cast<const uint4*>(p.mask + base + 8 * g)), mk);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = mk[i] > 0.f ? v[i] : 0.f;
+                }
+                reinterpret_cast<uint4*>(out)[g] = pack8(v);
+            } else {
+                for (int i = 0; i < 8 && c + i < s.Ncol; ++i) {
+                    float x = v[i];
+                    if (p.bias) x += p.bias[c + i];
+                    if (p.residual) x += __bfloat162float(p.residual[base + 8 * g + i]);
+                    if (p.relu) x = fmaxf(x, 0.f);
+                    if (p.mask && !(__bfloat162float(p.mask[base + 8 * g + i]) > 0.f)) x = 0.f;
+                    out[8 * g + i] = __float2bfloat16_rn(x);
+                }
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------- kernel ----
+template <ConvMode MODE, int BN>
+__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ Params p) {
+    using C = Cfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tfull = empty + C::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+
+    if (tid == 0) {
+        for (int i = 0; i < C::kStages; ++i) {
+            ptx::mbar_init(&full[i], kProducerThreads);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], kEpilogueThreads);
+        }
+        ptx::fence_mbarrier_init();
+    }
+    if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t smem_base = ptx::smem_addr(smem);
+
+    if (warp < 4) {
+        // ================================================ producers ======
+        int stage = 0;
+        uint32_t phase = 0;
+        int pending = 0, arrive_stage = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            const TileCoord tc = tile_coord(p, t);
+            int row_n = 0, row_hb = 0, row_wb = 0;
+            bool row_ok = false;
+            if constexpr (MODE != ConvMode::Wgrad) {
+                const int m = tc.mt * BM + tid;
+                row_ok = m < p.s.M;
+                if (row_ok) {
+                    uint32_t n, rem, a, b;
+                    if constexpr (MODE == ConvMode::Fwd) {
+                        p.s.d_howo.divmod(static_cast<uint32_t>(m), n, rem);
+                        p.s.d_wo.divmod(rem, a, b);
+                        row_hb = static_cast<int>(a) * p.s.sh - p.s.ph;
+                        row_wb = static_cast<int>(b) * p.s.sw - p.s.pw;
+                    } else {
+                        p.s.d_hw.divmod(static_cast<uint32_t>(m), n, rem);
+                        p.s.d_w.divmod(rem, a, b);
+                        row_hb = static_cast<int>(a) + p.s.ph;
+                        row_wb = static_cast<int>(b) + p.s.pw;
+                    }
+                    row_n = static_cast<int>(n);
+                }
+            }
+            for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t a_smem = smem_base + stage * C::kStageBytes;
+                load_stage<MODE, BN>(p, tc, kb, a_smem, a_smem + C::kABytes, tid, row_n, row_hb,
+                                     row_wb, row_ok);
+                ptx::cp_async_commit();
+                if (++pending > kLag) {
+                    ptx::cp_async_wait<kLag>();
+                    ptx::fence_proxy_async_smem();
+                    ptx::mbar_arrive(&full[arrive_stage]);
+                    arrive_stage = arrive_stage + 1 == C::kStages ? 0 : arrive_stage + 1;
+                    --pending;
+                }
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        ptx::cp_async_wait<0>();
+        ptx::fence_proxy_async_smem();
+        for (; pending > 0; --pending) {
+            ptx::mbar_arrive(&full[arrive_stage]);
+            arrive_stage = arrive_stage + 1 == C::kStages ? 0 : arrive_stage + 1;
+        }
+    } else if (warp == kMmaWarp) {
+        // =============================================== MMA issuer ======
+        constexpr uint32_t kMN = MODE == ConvMode::Wgrad ? 1u : 0u;
+        constexpr uint32_t idesc = ptx::make_idesc(1, BM, BN, kMN, kMN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+            const TileCoord tc = tile_coord(p, t);
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
+                ptx::mbar_wait(&full[stage], phase);
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+                    const uint32_t a_addr = smem_base + stage * C::kStageBytes;
+                    const uint32_t b_addr = a_addr + C::kABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        uint64_t ad, bd;
+                        if constexpr (MODE == ConvMode::Wgrad) {
+                            ad = ptx::sw128_desc(a_addr + k * 2048, 8192, 1024);
+                            bd = ptx::sw128_desc(b_addr + k * 2048, 8192, 1024);
+                        } else {
+                            ad = ptx::sw128_desc(a_addr + k * 32, 16, 1024);
+                            bd = ptx::sw128_desc(b_addr + k * 32, 16, 1024);
+                        }
+                        ptx::umma_f16(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
+                    }
+                    ptx::umma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == Cfg<BN>::kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
+            __syncwarp();
+        }
+    } else {
+        // ================================================= epilogue ======
+        const int ew = warp - 4;  // TMEM lane quarter
+        const int row = ew * 32 + (tid & 31);
+        int it = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+            const TileCoord tc = tile_coord(p, t);
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const int m = tc.mt * BM + row;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
+                                            acc * BN + c * 32,
+                                        v);
+                ptx::tmem_ld_wait();
+                epilogue_chunk<MODE>(p, tc, m, tc.nt * BN + c * 32, v);
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------- host ----
+int pick_bn(int ncol) { return ncol >= 256 ? 256 : (ncol > 64 ? 128 : 64); }
+
+struct SplitPlan {
+    int splits, kb_per_split;
+};
+
+SplitPlan plan_splits(const ConvShape& s, int bn) {
+    const int kb_total = (s.Kdim + BK - 1) / BK;
+    const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + bn - 1) / bn);
+    int want = std::max(1, (2 * num_sms() + tiles - 1) / tiles);
+    want = std::min(want, std::max(1, kb_total / 4));  // keep >= 4 k-blocks per split
+    want = std::min(want, 64);
+    const int per = (kb_total + want - 1) / want;
+    return {(kb_total + per - 1) / per, per};
+}
+
+template <ConvMode MODE, int BN>
+cudaError_t launch(Params p, cudaStream_t st) {
+    using C = Cfg<BN>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(C::kSmem));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    p.m_tiles = (p.s.M + BM - 1) / BM;
+    p.n_tiles = (p.s.Ncol + BN - 1) / BN;
+    p.kb_total = (p.s.Kdim + BK - 1) / BK;
+    if (MODE != ConvMode::Wgrad) {
+        p.splits = 1;
+        p.kb_per_split = p.kb_total;
+    }
+    p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
+    const int grid = std::min(p.num_tiles, num_sms());
+    conv_tc_kernel<MODE, BN><<<grid, kThreads, C::kSmem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <ConvMode MODE>
+cudaError_t dispatch(Params p, cudaStream_t st) {
+    switch (pick_bn(p.s.Ncol)) {
+        case 256: return launch<MODE, 256>(p, st);
+        case 128: return launch<MODE, 128>(p, st);
+        default: return launch<MODE, 64>(p, st);
+    }
+}
+
+}  // namespace
+
+bool conv_tc_supported(const ConvGeom& g, ConvMode mode) {
+    if (g.n < 1 || g.h < 1 || g.w < 1 || g.c < 1 || g.k < 1) return false;
+    if (mode == ConvMode::Fwd) return g.c % 8 == 0;
+    if (mode == ConvMode::Dgrad) return g.k % 8 == 0 && g.c % 8 == 0;
+    return g.c % 8 == 0 && g.k % 8 == 0;
+}
+
+size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
+    if (mode != ConvMode::Wgrad) return 0;
+    const ConvShape s = make_shape(g, mode);
+    const SplitPlan sp = plan_splits(s, pick_bn(s.Ncol));
+    return sp.splits > 1 ? size_t(sp.splits) * s.M * s.Ncol * sizeof(float) : 0;
+}
+
+cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
+                        void* y, cudaStream_t st) {
+    Params p{};
+    p.s = make_shape(g, ConvMode::Fwd);
+    p.a = static_cast<const __nv_bfloat16*>(x);
+    p.b = static_cast<const __nv_bfloat16*>(w);
+    p.out = y;
+    p.bias = ep.bias;
+    p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
+    p.mask = nullptr;
+    p.relu = ep.relu ? 1 : 0;
+    return dispatch<ConvMode::Fwd>(p, st);
+}
+
+cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wT, const Epilogue& ep,
+                          void* dx, cudaStream_t st) {
+    Params p{};
+    p.s = make_shape(g, ConvMode::Dgrad);
+    p.a = static_cast<const __nv_bfloat16*>(dy);
+    p.b = static_cast<const __nv_bfloat16*>(wT);
+    p.out = dx;
+    p.bias = nullptr;
+    p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
+    p.mask = static_cast<const __nv_bfloat16*>(ep.mask);
+    p.relu = 0;
+    return dispatch<ConvMode::Dgrad>(p, st);
+}
+
+cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
+                          void* workspace, cudaStream_t st) {
+    Params p{};
+    p.s = make_shape(g, ConvMode::Wgrad);
+    const SplitPlan sp = plan_splits(p.s, pick_bn(p.s.Ncol));
+    p.a = static_cast<const __nv_bfloat16*>(dy);
+    p.b = static_cast<const __nv_bfloat16*>(x);
+    p.splits = sp.splits;
+    p.kb_per_split = sp.kb_per_split;
+    p.out = sp.splits > 1 ? workspace : static_cast<void*>(dw);
+    if (sp.splits > 1 && workspace == nullptr) return cudaErrorInvalidValue;
+    cudaError_t e = dispatch<ConvMode::Wgrad>(p, st);
+    if (e != cudaSuccess || sp.splits == 1) return e;
+    return split_reduce(static_cast<const float*>(workspace), sp.splits,
+                        size_t(p.s.M) * p.s.Ncol, dw, st);
+}
+
+}  // namespace tcb

@@ -1,0 +1,455 @@
+// HBM-bound kernels of the step: synthetic fills, casts, the weight
+// transpose dgrad needs, deterministic reductions (bias grads, split-K),
+// pools, softmax cross-entropy and the fused momentum-SGD shard update.
+//
+// Arithmetic that the CPU oracle must reproduce bit-exactly (RNG fill,
+// labels, SGD) uses explicitly rounded intrinsics (__fmul_rn/__fadd_rn) so
+// nvcc cannot contract it into FMAs; oracle/numerics.c is compiled with
+// -ffp-contract=off to match.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace tcb {
+namespace {
+
+constexpr int kBlock = 256;
+
+inline int grid_for(size_t n, int per_thread = 1) {
+    size_t blocks = (n + size_t(kBlock) * per_thread - 1) / (size_t(kBlock) * per_thread);
+    const size_t cap = size_t(num_sms()) * 16;
+    return static_cast<int>(std::max<size_t>(1, std::min(blocks, cap)));
+}
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t stream_base(uint64_t seed, uint64_t tag) {
+    return splitmix64(seed ^ splitmix64(tag));
+}
+
+template <typename T>
+__global__ void fill_uniform_kernel(T* p, size_t n, uint64_t base, float lo, float span) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const uint64_t bits = splitmix64(base + i);
+        const float u = static_cast<float>(bits >> 40) * (1.0f / 16777216.0f);
+        p[i] = from_f32<T>(__fadd_rn(lo, __fmul_rn(span, u)));
+    }
+}
+
+__global__ void fill_labels_kernel(int32_t* labels, int n, int classes, uint64_t base) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) labels[i] = static_cast<int32_t>(splitmix64(base + i) % uint64_t(classes));
+}
+
+template <typename S, typename D>
+__global__ void cast_kernel(const S* src, D* dst, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        dst[i] = from_f32<D>(to_f32<S>(src[i]));
+}
+
+// [K][RS][C] -> [C][RS][K], 32x32 tiles through shared memory.
+template <typename T>
+__global__ void transpose_krsc_kernel(const T* __restrict__ w, T* __restrict__ wT, int K, int RS,
+                                      int C) {
+    __shared__ T tile[32][33];
+    const int rs = blockIdx.z;
+    const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int k = k0 + i, c = c0 + threadIdx.x;
+        if (k < K && c < C) tile[i][threadIdx.x] = w[(size_t(k) * RS + rs) * C + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, k = k0 + threadIdx.x;
+        if (k < K && c < C) wT[(size_t(c) * RS + rs) * K + k] = tile[threadIdx.x][i];
+    }
+}
+
+template <typename T>
+__global__ void column_partial_kernel(const T* __restrict__ in, float* __restrict__ part,
+                                      int rows, int cols, int rows_per_chunk) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= cols) return;
+    const int r0 = blockIdx.y * rows_per_chunk;
+    const int r1 = min(rows, r0 + rows_per_chunk);
+    float acc = 0.f;
+    for (int r = r0; r < r1; ++r) acc += to_f32<T>(in[size_t(r) * cols + col]);
+    part[size_t(blockIdx.y) * cols + col] = acc;
+}
+
+__global__ void split_reduce_kernel(const float* __restrict__ parts, int splits, size_t n,
+                                    float* __restrict__ out) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int s = 0; s < splits; ++s) acc += parts[size_t(s) * n + i];
+        out[i] = acc;
+    }
+}
+
+__global__ void split_reduce4_kernel(const float4* __restrict__ parts, int splits, size_t n4,
+                                     float4* __restrict__ out) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
+         i += size_t(gridDim.x) * blockDim.x) {
+        float4 acc = parts[i];
+        for (int s = 1; s < splits; ++s) {
+            const float4 v = parts[size_t(s) * n4 + i];
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        out[i] = acc;
+    }
+}
+
+// One PS shard: g' = g*scale + wd*w ; v = mom*v + g' ; w = w - lr*v ; wc = compute copy.
+template <typename CT>
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g,
+                           float* __restrict__ v, CT* __restrict__ wc, size_t n, float lr,
+                           float mom, float wd, float gscale) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const float wi = w[i];
+        const float gi = __fadd_rn(__fmul_rn(g[i], gscale), __fmul_rn(wd, wi));
+        const float vi = __fadd_rn(__fmul_rn(mom, v[i]), gi);
+        const float wn = __fsub_rn(wi, __fmul_rn(lr, vi));
+        v[i] = vi;
+        w[i] = wn;
+        if (wc) wc[i] = from_f32<CT>(wn);
+    }
+}
+
+// Vectorised variant: 4 params per thread-iteration (n % 4 == 0, 16B-aligned).
+template <typename CT>
+__global__ void sgd4_kernel(float4* __restrict__ w, const float4* __restrict__ g,
+                            float4* __restrict__ v, CT* __restrict__ wc, size_t n4, float lr,
+                            float mom, float wd, float gscale) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
+         i += size_t(gridDim.x) * blockDim.x) {
+        float4 wi = w[i], gi = g[i], vi = v[i];
+        float* wp = &wi.x;
+        float* gp = &gi.x;
+        float* vp = &vi.x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float gg = __fadd_rn(__fmul_rn(gp[j], gscale), __fmul_rn(wd, wp[j]));
+            vp[j] = __fadd_rn(__fmul_rn(mom, vp[j]), gg);
+            wp[j] = __fsub_rn(wp[j], __fmul_rn(lr, vp[j]));
+        }
+        v[i] = vi;
+        w[i] = wi;
+        if (wc) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wc[4 * i + j] = from_f32<CT>(wp[j]);
+        }
+    }
+}
+
+template <typename T>
+__global__ void add_kernel(T* y, const T* x, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        y[i] = from_f32<T>(to_f32<T>(y[i]) + to_f32<T>(x[i]));
+}
+
+template <typename T>
+__global__ void relu_mask_kernel(T* g, const T* act, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        if (!(to_f32<T>(act[i]) > 0.f)) g[i] = from_f32<T>(0.f);
+}
+
+// Max pool, NHWC; padded positions never win; ties keep the first (r, s) in scan order.
+template <typename T>
+__global__ void maxpool_fwd_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                   uint8_t* __restrict__ arg, int N, int H, int W, int C, int F,
+                                   int S, int P, int Ho, int Wo) {
+    const size_t total = size_t(N) * Ho * Wo * C;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % C);
+        size_t t = i / C;
+        const int wo = int(t % Wo);
+        t /= Wo;
+        const int ho = int(t % Ho);
+        const int n = int(t / Ho);
+        float best = -INFINITY;
+        int best_idx = 0;
+        for (int r = 0; r < F; ++r) {
+            const int h = ho * S - P + r;
+            if (h < 0 || h >= H) continue;
+            for (int s = 0; s < F; ++s) {
+                const int w = wo * S - P + s;
+                if (w < 0 || w >= W) continue;
+                const float v = to_f32<T>(x[((size_t(n) * H + h) * W + w) * C + c]);
+                if (v > best) {
+                    best = v;
+                    best_idx = r * F + s;
+                }
+            }
+        }
+        y[i] = from_f32<T>(best);
+        if (arg) arg[i] = static_cast<uint8_t>(best_idx);
+    }
+}
+
+template <typename T>
+__global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ arg,
+                                   T* __restrict__ dx, int N, int H, int W, int C, int F, int S,
+                                   int P, int Ho, int Wo) {
+    const size_t total = size_t(N) * H * W * C;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % C);
+        size_t t = i / C;
+        const int w = int(t % W);
+        t /= W;
+        const int h = int(t % H);
+        const int n = int(t / H);
+        // windows (ho, wo) with ho*S - P <= h <= ho*S - P + F - 1
+        const int ho0 = max(0, (h + P - F + S) / S), ho1 = min(Ho - 1, (h + P) / S);
+        const int wo0 = max(0, (w + P - F + S) / S), wo1 = min(Wo - 1, (w + P) / S);
+        float acc = 0.f;
+        for (int ho = ho0; ho <= ho1; ++ho) {
+            const int r = h - (ho * S - P);
+            if (r < 0 || r >= F) continue;
+            for (int wo = wo0; wo <= wo1; ++wo) {
+                const int s = w - (wo * S - P);
+                if (s < 0 || s >= F) continue;
+                const size_t o = ((size_t(n) * Ho + ho) * Wo + wo) * C + c;
+                if (arg[o] == r * F + s) acc += to_f32<T>(dy[o]);
+            }
+        }
+        dx[i] = from_f32<T>(acc);
+    }
+}
+
+template <typename T>
+__global__ void avgpool_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, int N, int HW,
+                                   int C) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * C) return;
+    const int n = i / C, c = i % C;
+    float acc = 0.f;
+    for (int p = 0; p < HW; ++p) acc += to_f32<T>(x[(size_t(n) * HW + p) * C + c]);
+    y[i] = from_f32<T>(acc / float(HW));
+}
+
+template <typename T>
+__global__ void avgpool_bwd_kernel(const T* __restrict__ dy, T* __restrict__ dx, int N, int HW,
+                                   int C) {
+    const size_t total = size_t(N) * HW * C;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % C);
+        const int n = int(i / (size_t(HW) * C));
+        dx[i] = from_f32<T>(to_f32<T>(dy[size_t(n) * C + c]) / float(HW));
+    }
+}
+
+// One block per row: softmax, per-row loss, gradient (p - onehot) / N.
+template <typename T>
+__global__ void softmax_xent_kernel(const T* __restrict__ logits, const int32_t* __restrict__ lab,
+                                    T* __restrict__ dl, float* __restrict__ row_loss, int N,
+                                    int K) {
+    __shared__ float red[32];
+    const int n = blockIdx.x;
+    const T* z = logits + size_t(n) * K;
+    float m = -INFINITY;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) m = fmaxf(m, to_f32<T>(z[k]));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+        for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    m = red[0];
+    __syncthreads();
+    float s = 0.f;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) s += expf(to_f32<T>(z[k]) - m);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    s = red[0];
+    const int y = lab[n];
+    const float inv_n = 1.0f / float(N);
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        const float pk = expf(to_f32<T>(z[k]) - m) / s;
+        dl[size_t(n) * K + k] = from_f32<T>((pk - (k == y ? 1.f : 0.f)) * inv_n);
+    }
+    if (threadIdx.x == 0) row_loss[n] = logf(s) + m - to_f32<T>(z[y]);
+}
+
+__global__ void mean_kernel(float* loss, const float* row_loss, int N) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < N; ++i) acc += row_loss[i];
+        loss[0] = static_cast<float>(acc / N);
+    }
+}
+
+}  // namespace
+
+#define TCB_DT_SWITCH(dt, T, ...)                   \
+    do {                                            \
+        if ((dt) == DType::F32) {                   \
+            using T = float;                        \
+            __VA_ARGS__;                            \
+        } else {                                    \
+            using T = __nv_bfloat16;                \
+            __VA_ARGS__;                            \
+        }                                           \
+    } while (0)
+
+cudaError_t fill_uniform(DType dt, void* p, size_t n, uint64_t seed, uint64_t tag, float lo,
+                         float hi, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t base = stream_base(seed, tag);
+    const float span = hi - lo;
+    TCB_DT_SWITCH(dt, T, (fill_uniform_kernel<T><<<grid_for(n, 4), kBlock, 0, st>>>(
+                              static_cast<T*>(p), n, base, lo, span)));
+    return cudaGetLastError();
+}
+
+cudaError_t fill_labels(int32_t* labels, int n, int classes, uint64_t seed, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const uint64_t base = stream_base(seed, 0x4C4142454C53ull);
+    fill_labels_kernel<<<(n + kBlock - 1) / kBlock, kBlock, 0, st>>>(labels, n, classes, base);
+    return cudaGetLastError();
+}
+
+cudaError_t cast(DType src_t, const void* src, DType dst_t, void* dst, size_t n,
+                 cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    TCB_DT_SWITCH(src_t, S, TCB_DT_SWITCH(dst_t, D, (cast_kernel<S, D><<<grid_for(n, 4), kBlock, 0, st>>>(
+                                                        static_cast<const S*>(src), static_cast<D*>(dst), n))));
+    return cudaGetLastError();
+}
+
+cudaError_t transpose_krsc(DType dt, const void* w, void* wT, int K, int R, int S, int C,
+                           cudaStream_t st) {
+    dim3 grid((C + 31) / 32, (K + 31) / 32, R * S), block(32, 8);
+    TCB_DT_SWITCH(dt, T, (transpose_krsc_kernel<T><<<grid, block, 0, st>>>(
+                              static_cast<const T*>(w), static_cast<T*>(wT), K, R * S, C)));
+    return cudaGetLastError();
+}
+
+size_t column_sum_workspace(int rows, int cols) {
+    const int chunks = std::min(rows, 512);
+    return size_t(chunks) * cols * sizeof(float);
+}
+
+cudaError_t column_sum(DType dt, const void* in, float* out, int rows, int cols, float* ws,
+                       cudaStream_t st) {
+    const int chunks = std::min(rows, 512);
+    const int per = (rows + chunks - 1) / chunks;
+    const int used = (rows + per - 1) / per;
+    const int tpb = cols >= 128 ? 128 : 32 * ((cols + 31) / 32);
+    dim3 grid((cols + tpb - 1) / tpb, used);
+    TCB_DT_SWITCH(dt, T, (column_partial_kernel<T><<<grid, tpb, 0, st>>>(
+                              static_cast<const T*>(in), ws, rows, cols, per)));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return split_reduce(ws, used, size_t(cols), out, st);
+}
+
+cudaError_t split_reduce(const float* parts, int splits, size_t n, float* out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(parts) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    if (vec)
+        split_reduce4_kernel<<<grid_for(n / 4), kBlock, 0, st>>>(
+            reinterpret_cast<const float4*>(parts), splits, n / 4, reinterpret_cast<float4*>(out));
+    else
+        split_reduce_kernel<<<grid_for(n), kBlock, 0, st>>>(parts, splits, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t sgd_momentum(float* w, const float* g, float* v, DType cdt, void* wc, size_t n,
+                         float lr, float mom, float wd, float gscale, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const bool vec = n % 4 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(g) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(v) % 16 == 0;
+    TCB_DT_SWITCH(cdt, CT, {
+        if (vec)
+            sgd4_kernel<CT><<<grid_for(n / 4, 2), kBlock, 0, st>>>(
+                reinterpret_cast<float4*>(w), reinterpret_cast<const float4*>(g),
+                reinterpret_cast<float4*>(v), static_cast<CT*>(wc), n / 4, lr, mom, wd, gscale);
+        else
+            sgd_kernel<CT><<<grid_for(n, 4), kBlock, 0, st>>>(w, g, v, static_cast<CT*>(wc), n, lr,
+                                                              mom, wd, gscale);
+    });
+    return cudaGetLastError();
+}
+
+cudaError_t add_inplace(DType dt, void* y, const void* x, size_t n, cudaStream_t st) {
+    TCB_DT_SWITCH(dt, T, (add_kernel<T><<<grid_for(n, 4), kBlock, 0, st>>>(
+                              static_cast<T*>(y), static_cast<const T*>(x), n)));
+    return cudaGetLastError();
+}
+
+cudaError_t relu_mask_inplace(DType dt, void* g, const void* act, size_t n, cudaStream_t st) {
+    TCB_DT_SWITCH(dt, T, (relu_mask_kernel<T><<<grid_for(n, 4), kBlock, 0, st>>>(
+                              static_cast<T*>(g), static_cast<const T*>(act), n)));
+    return cudaGetLastError();
+}
+
+cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, int h, int w,
+                        int c, int f, int s, int p, cudaStream_t st) {
+    const int ho = (h + 2 * p - f) / s + 1, wo = (w + 2 * p - f) / s + 1;
+    const size_t total = size_t(n) * ho * wo * c;
+    TCB_DT_SWITCH(dt, T, (maxpool_fwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
+                              static_cast<const T*>(x), static_cast<T*>(y), arg, n, h, w, c, f, s,
+                              p, ho, wo)));
+    return cudaGetLastError();
+}
+
+cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, int n, int h,
+                        int w, int c, int f, int s, int p, cudaStream_t st) {
+    const int ho = (h + 2 * p - f) / s + 1, wo = (w + 2 * p - f) / s + 1;
+    const size_t total = size_t(n) * h * w * c;
+    TCB_DT_SWITCH(dt, T, (maxpool_bwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
+                              static_cast<const T*>(dy), arg, static_cast<T*>(dx), n, h, w, c, f,
+                              s, p, ho, wo)));
+    return cudaGetLastError();
+}
+
+cudaError_t avgpool_global_fwd(DType dt, const void* x, void* y, int n, int hw, int c,
+                               cudaStream_t st) {
+    TCB_DT_SWITCH(dt, T, (avgpool_fwd_kernel<T><<<(n * c + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+                              static_cast<const T*>(x), static_cast<T*>(y), n, hw, c)));
+    return cudaGetLastError();
+}
+
+cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw, int c,
+                               cudaStream_t st) {
+    TCB_DT_SWITCH(dt, T, (avgpool_bwd_kernel<T><<<grid_for(size_t(n) * hw * c, 2), kBlock, 0, st>>>(
+                              static_cast<const T*>(dy), static_cast<T*>(dx), n, hw, c)));
+    return cudaGetLastError();
+}
+
+cudaError_t softmax_xent(DType dt, const void* logits, const int32_t* labels, void* dlogits,
+                         float* loss, int n, int classes, cudaStream_t st) {
+    TCB_DT_SWITCH(dt, T, (softmax_xent_kernel<T><<<n, kBlock, 0, st>>>(
+                              static_cast<const T*>(logits), labels, static_cast<T*>(dlogits),
+                              loss + 1, n, classes)));
+    mean_kernel<<<1, 32, 0, st>>>(loss, loss + 1, n);
+    return cudaGetLastError();
+}
+
+}  // namespace tcb

@@ -1,0 +1,102 @@
+// Host-side declarations of every kernel launcher in csrc/cuda/*.cu. The
+// runtime (csrc/runtime) calls only these; all take a cudaStream_t and return
+// cudaError_t from the launch (asynchronous errors surface at the next sync).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tcb {
+
+struct ConvGeom {
+    int n, h, w, c, k, r, s, pad_h, pad_w, stride_h, stride_w;
+    int ho() const { return (h + 2 * pad_h - r) / stride_h + 1; }
+    int wo() const { return (w + 2 * pad_w - s) / stride_w + 1; }
+};
+
+enum class ConvMode { Fwd = 0, Dgrad = 1, Wgrad = 2 };
+enum class DType { F32 = 0, BF16 = 1 };
+
+inline size_t dtype_size(DType t) { return t == DType::F32 ? 4 : 2; }
+
+// Epilogue options shared by fwd / dgrad.
+struct Epilogue {
+    const float* bias = nullptr;     // [Ncol] fp32, fwd only
+    const void* residual = nullptr;  // same dtype/shape as the output, added before act
+    const void* mask = nullptr;      // dgrad: multiply by [mask > 0]
+    bool relu = false;               // fwd: max(0, .)
+};
+
+// ---- tensor-core implicit GEMM (tcgen05 / TMEM), bf16 in, fp32 accumulate ----
+// Requirements: C % 8 == 0 (fwd/wgrad), K % 8 == 0 (dgrad/wgrad).
+// wT (dgrad) is the [C][R][S][K] transpose of w produced by transpose_krsc.
+size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode);
+cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
+                        void* y, cudaStream_t st);
+cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wT, const Epilogue& ep,
+                          void* dx, cudaStream_t st);
+cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
+                          void* workspace, cudaStream_t st);
+bool conv_tc_supported(const ConvGeom& g, ConvMode mode);
+
+// ---- FP32 FFMA implicit GEMM (parity mode) ----
+size_t conv_ffma_workspace(const ConvGeom& g, ConvMode mode);
+cudaError_t conv_ffma_fwd(const ConvGeom& g, const float* x, const float* w, const Epilogue& ep,
+                          float* y, cudaStream_t st);
+cudaError_t conv_ffma_dgrad(const ConvGeom& g, const float* dy, const float* w,
+                            const Epilogue& ep, float* dx, cudaStream_t st);
+cudaError_t conv_ffma_wgrad(const ConvGeom& g, const float* dy, const float* x, float* dw,
+                            void* workspace, cudaStream_t st);
+
+// ---- Winograd F(2x2,3x3) (3x3, stride 1) ----
+size_t winograd_workspace(const ConvGeom& g, ConvMode mode, DType dt);
+bool winograd_supported(const ConvGeom& g);
+cudaError_t winograd_fwd(const ConvGeom& g, DType dt, const void* x, const void* w,
+                         const Epilogue& ep, void* y, void* ws, cudaStream_t st);
+cudaError_t winograd_dgrad(const ConvGeom& g, DType dt, const void* dy, const void* w,
+                           const Epilogue& ep, void* dx, void* ws, cudaStream_t st);
+cudaError_t winograd_wgrad(const ConvGeom& g, DType dt, const void* dy, const void* x, float* dw,
+                           void* ws, cudaStream_t st);
+
+// ---- FFT convolution (stride 1) ----
+size_t fft_workspace(const ConvGeom& g, ConvMode mode);
+bool fft_supported(const ConvGeom& g);
+cudaError_t fft_fwd(const ConvGeom& g, DType dt, const void* x, const void* w, const Epilogue& ep,
+                    void* y, void* ws, cudaStream_t st);
+cudaError_t fft_dgrad(const ConvGeom& g, DType dt, const void* dy, const void* w,
+                      const Epilogue& ep, void* dx, void* ws, cudaStream_t st);
+cudaError_t fft_wgrad(const ConvGeom& g, DType dt, const void* dy, const void* x, float* dw,
+                      void* ws, cudaStream_t st);
+
+// ---- elementwise / layout / reductions ----
+cudaError_t fill_uniform(DType dt, void* p, size_t n, uint64_t seed, uint64_t tag, float lo,
+                         float hi, cudaStream_t st);
+cudaError_t fill_labels(int32_t* labels, int n, int classes, uint64_t seed, cudaStream_t st);
+cudaError_t cast(DType src_t, const void* src, DType dst_t, void* dst, size_t n, cudaStream_t st);
+// [K][R][S][C] -> [C][R][S][K]
+cudaError_t transpose_krsc(DType dt, const void* w, void* wT, int K, int R, int S, int C,
+                           cudaStream_t st);
+// out[j] = sum_i in[i][j] (rows x cols, fp32 result), deterministic.
+cudaError_t column_sum(DType dt, const void* in, float* out, int rows, int cols, float* ws,
+                       cudaStream_t st);
+size_t column_sum_workspace(int rows, int cols);
+// out[i] = sum_s parts[s][i] (fixed order)
+cudaError_t split_reduce(const float* parts, int splits, size_t n, float* out, cudaStream_t st);
+cudaError_t sgd_momentum(float* w, const float* g, float* v, DType cdt, void* wc, size_t n,
+                         float lr, float mom, float wd, float gscale, cudaStream_t st);
+cudaError_t add_inplace(DType dt, void* y, const void* x, size_t n, cudaStream_t st);
+cudaError_t relu_mask_inplace(DType dt, void* g, const void* act, size_t n, cudaStream_t st);
+
+cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, int h, int w,
+                        int c, int f, int s, int p, cudaStream_t st);
+cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, int n, int h,
+                        int w, int c, int f, int s, int p, cudaStream_t st);
+cudaError_t avgpool_global_fwd(DType dt, const void* x, void* y, int n, int hw, int c,
+                               cudaStream_t st);
+cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw, int c,
+                               cudaStream_t st);
+cudaError_t softmax_xent(DType dt, const void* logits, const int32_t* labels, void* dlogits,
+                         float* loss, int n, int classes, cudaStream_t st);
+
+}  // namespace tcb

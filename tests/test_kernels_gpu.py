@@ -1,0 +1,178 @@
+"""Numeric-half parity: every sm_100a kernel vs the CPU oracle (oracle/numerics.c)
+on identical seeded inputs, through the C-ABI (libtcb.so).
+
+Tolerances (north_star): normwise relative error <= 1e-5 in fp32-FFMA mode,
+<= 2e-2 in the bf16 tensor-core mode (the oracle is fed the same
+bf16-rounded inputs; outputs are bf16). Integer/byte work (RNG, labels,
+argmax) and the SGD update are bit-exact.
+SURVEY §8 rows: a14 (conv fwd/dgrad/wgrad), a16 (SGD), a17 (pools, loss), d1 (RNG).
+"""
+import numpy as np
+import pytest
+
+from oracle_binding import elem_err, rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {"ffma": 1e-5, "bf16": 2e-2}
+SEED = 20260810
+
+# (name, n, h, w, c, k, r, pad, stride) — drawn from the BASELINE configs' layer shapes,
+# shrunk in N so the fp64 oracle finishes in seconds; ragged M/N/K tails on purpose.
+GEOMS = [
+    ("lenet_conv2", 4, 12, 12, 24, 56, 5, 0, 1),
+    ("alex_conv2", 2, 27, 27, 96, 256, 5, 2, 1),
+    ("alex_conv3", 2, 13, 13, 256, 384, 3, 1, 1),
+    ("rn50_3x3_s1", 2, 14, 14, 64, 64, 3, 1, 1),
+    ("rn50_3x3_s2", 2, 28, 28, 128, 128, 3, 1, 2),
+    ("rn50_1x1", 4, 14, 14, 256, 64, 1, 0, 1),
+    ("rn50_1x1_s2", 2, 28, 28, 256, 512, 1, 0, 2),
+    ("rn50_stem_7x7_s2", 2, 32, 32, 8, 64, 7, 3, 2),
+    ("vgg_fc_as_conv", 3, 7, 7, 64, 136, 7, 0, 1),
+    ("ragged", 3, 9, 11, 40, 72, 3, 1, 1),
+]
+FFMA_ONLY = [
+    ("lenet_conv1_c1", 4, 28, 28, 1, 20, 5, 0, 1),
+    ("odd_channels", 2, 10, 10, 3, 7, 3, 1, 2),
+]
+
+
+def _dev():
+    from paper_1709_06622_b200 import device
+    return device
+
+
+def _rand(oracle, shape, tag, scale=1.0, bf16=False):
+    n = int(np.prod(shape))
+    a = oracle.uniform(n, SEED, tag, -scale, scale)
+    if bf16:
+        a = oracle.round_bf16(a)
+    return a.reshape(shape)
+
+
+def _to_dev(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to("cuda").to(dtype)
+
+
+def _host(t):
+    return t.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+@pytest.mark.parametrize("spec", GEOMS + FFMA_ONLY, ids=lambda s: s[0])
+def test_conv_gemm_parity(oracle, prec, spec):
+    if prec == "bf16" and spec in FFMA_ONLY:
+        pytest.skip("tensor-core path needs C, K multiples of 8")
+    dev = _dev()
+    name, n, h, w, c, k, r, pad, stride = spec
+    g = dev.geom(n, h, w, c, k, r, pad=pad, stride=stride)
+    gd = g.as_dict()
+    plan = dev.ConvPlan(g, "gemm", prec)
+    bf = prec == "bf16"
+    dt = plan.dtype
+    fan_in = c * r * r
+    x = _rand(oracle, (n, h, w, c), 1, 1.0, bf)
+    wt = _rand(oracle, (k, r, r, c), 2, (6.0 / fan_in) ** 0.5, bf)
+    bias = _rand(oracle, (k,), 3, 0.1)
+    res = _rand(oracle, (n, g.ho, g.wo, k), 4, 0.5, bf)
+    dy = _rand(oracle, (n, g.ho, g.wo, k), 5, 1.0, bf)
+    mask = _rand(oracle, (n, h, w, c), 6, 1.0, bf)
+    rgrad = _rand(oracle, (n, h, w, c), 7, 0.5, bf)
+    tol = TOL[prec]
+
+    # forward with every epilogue feature
+    y = plan.fwd(_to_dev(x, dt), _to_dev(wt, dt), bias=_to_dev(bias, torch.float32),
+                 residual=_to_dev(res, dt), relu=True)
+    ref = oracle.conv_fwd(gd, x, wt, bias=bias, residual=res, relu=True)
+    assert rel_err(_host(y), ref) <= tol, (name, "fwd", rel_err(_host(y), ref))
+    y0 = plan.fwd(_to_dev(x, dt), _to_dev(wt, dt))
+    ref0 = oracle.conv_fwd(gd, x, wt)
+    assert rel_err(_host(y0), ref0) <= tol
+
+    # data gradient (+ residual gradient, ReLU mask of the layer input)
+    dx = plan.dgrad(_to_dev(dy, dt), _to_dev(wt, dt), residual=_to_dev(rgrad, dt),
+                    mask=_to_dev(mask, dt))
+    refd = oracle.conv_dgrad(gd, dy, wt, residual=rgrad, mask=mask)
+    assert rel_err(_host(dx), refd) <= tol, (name, "dgrad", rel_err(_host(dx), refd))
+    dx0 = plan.dgrad(_to_dev(dy, dt), _to_dev(wt, dt))
+    assert rel_err(_host(dx0), oracle.conv_dgrad(gd, dy, wt)) <= tol
+
+    # weight + bias gradient (fp32, deterministic)
+    dw, db = plan.wgrad(_to_dev(dy, dt), _to_dev(x, dt), want_db=True)
+    refw, refb = oracle.conv_wgrad(gd, dy, x, want_db=True)
+    assert rel_err(_host(dw), refw) <= tol, (name, "wgrad", rel_err(_host(dw), refw))
+    assert rel_err(_host(db), refb) <= tol
+    dw2 = plan.wgrad(_to_dev(dy, dt), _to_dev(x, dt))
+    assert torch.equal(dw, dw2), "wgrad must be bitwise deterministic"
+    if prec == "ffma":
+        assert elem_err(_host(y), ref, 1e-2) <= 1e-4
+
+
+def test_fill_and_labels_bit_exact(oracle):
+    dev = _dev()
+    for tag, lo, hi in ((1, -1.0, 1.0), (99, -0.05, 0.05), (7, 0.0, 3.0)):
+        t = torch.empty(100_003, dtype=torch.float32, device="cuda")
+        dev.fill_uniform(t, SEED, tag, lo, hi)
+        assert np.array_equal(t.cpu().numpy(), oracle.uniform(t.numel(), SEED, tag, lo, hi))
+        tb = torch.empty(100_003, dtype=torch.bfloat16, device="cuda")
+        dev.fill_uniform(tb, SEED, tag, lo, hi)
+        assert np.array_equal(tb.float().cpu().numpy(),
+                              oracle.round_bf16(oracle.uniform(tb.numel(), SEED, tag, lo, hi)))
+    lab = torch.empty(4097, dtype=torch.int32, device="cuda")
+    dev.fill_labels(lab, 1000, SEED)
+    assert np.array_equal(lab.cpu().numpy(), oracle.labels(4097, 1000, SEED))
+
+
+@pytest.mark.parametrize("n", [1, 7, 4096, 1_000_003])
+def test_sgd_bit_exact(oracle, n):
+    dev = _dev()
+    w = oracle.uniform(n, SEED, 11, -0.1, 0.1)
+    g = oracle.uniform(n, SEED, 12, -1.0, 1.0)
+    v = oracle.uniform(n, SEED, 13, -0.01, 0.01)
+    wd, vd, gd = (torch.from_numpy(a.copy()).cuda() for a in (w, v, g))
+    wc = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    dev.sgd_momentum(wd, gd, vd, 0.01, 0.9, 5e-4, 0.25, w_compute=wc)
+    w_ref, v_ref = oracle.sgd(w, g, v, 0.01, 0.9, 5e-4, 0.25)
+    assert np.array_equal(wd.cpu().numpy(), w_ref)
+    assert np.array_equal(vd.cpu().numpy(), v_ref)
+    assert np.array_equal(wc.float().cpu().numpy(), oracle.round_bf16(w_ref))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("pool", [(3, 2, 0), (2, 2, 0), (3, 2, 1), (3, 1, 1)])
+def test_maxpool_parity(oracle, dtype, pool):
+    dev = _dev()
+    f, s, p = pool
+    n, h, w, c = 2, 13, 15, 24
+    bf = dtype == "bf16"
+    dt = torch.bfloat16 if bf else torch.float32
+    x = _rand(oracle, (n, h, w, c), 21, 1.0, bf)
+    y, arg = dev.maxpool_fwd(_to_dev(x, dt), f, s, p)
+    ry, rarg = oracle.maxpool_fwd(x, n, h, w, c, f, s, p)
+    assert np.array_equal(arg.cpu().numpy().ravel(), rarg)
+    assert np.array_equal(_host(y).ravel(), ry.astype(np.float32))
+    dy = _rand(oracle, tuple(y.shape), 22, 1.0, bf)
+    dx = dev.maxpool_bwd(_to_dev(dy, dt), arg, (n, h, w, c), f, s, p)
+    rdx = oracle.maxpool_bwd(dy, rarg, n, h, w, c, f, s, p)
+    assert rel_err(_host(dx), rdx) <= TOL["bf16" if bf else "ffma"]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_avgpool_and_softmax_parity(oracle, dtype):
+    dev = _dev()
+    bf = dtype == "bf16"
+    dt = torch.bfloat16 if bf else torch.float32
+    tol = TOL["bf16" if bf else "ffma"]
+    x = _rand(oracle, (3, 7, 7, 64), 31, 1.0, bf)
+    y = dev.avgpool_fwd(_to_dev(x, dt))
+    assert rel_err(_host(y), oracle.avgpool_fwd(x, 3, 49, 64)) <= tol
+    dy = _rand(oracle, (3, 64), 32, 1.0, bf)
+    dx = dev.avgpool_bwd(_to_dev(dy, dt), 7, 7)
+    assert rel_err(_host(dx), oracle.avgpool_bwd(dy, 3, 49, 64)) <= tol
+    z = _rand(oracle, (17, 1000), 33, 4.0, bf)
+    lab = oracle.labels(17, 1000, SEED)
+    loss, dl = dev.softmax_xent(_to_dev(z, dt), torch.from_numpy(lab).cuda())
+    rl, rdl = oracle.softmax_xent(z, lab, 17, 1000)
+    assert abs(float(loss) - rl) <= 1e-5 * abs(rl)
+    assert rel_err(_host(dl), rdl) <= tol
