@@ -1,0 +1,372 @@
+#!/usr/bin/env python3
+"""Headline benchmark: data-parallel training images/sec on B200.
+
+Workload (BASELINE.json configs[2], the config the metric's 1/2/4/8-GPU
+scaling is quoted on): ResNet-50-shaped synthetic step, 224x224x3, 256 images
+per GPU, bf16 tensor-core convolutions with fp32 accumulate, PS shards = GPUs
+(NCCL reduce-scatter -> fused momentum SGD -> all-gather). One process per
+GPU; for N > 1 launch with torchrun (see the contract in the task README).
+
+Prints ONE JSON line (rank 0). `value` = images/sec over all ranks with the
+batch resident in HBM; `e2e` = the same step through the public C-ABI
+(tcb_trainer_set_batch from pinned host memory + tcb_trainer_step +
+tcb_trainer_loss readback). `roofline` = the tcgen05 implicit-GEMM conv kernel
+(all conv passes of one step, timed alone per layer with CUDA events) against
+the measured bf16 peak. `cpu_baseline` = the CPU oracle's training step on
+this box's host cores (bounded sample). `--impl reference` times that CPU
+path instead (the reference has no training step of its own).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "training images/sec at 1/2/4/8 B200 + conv %TC peak, PS-sync NVLink GB/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        d["source"] = "measured"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["source"] = "fallback"
+    return d
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--batch", type=int, default=256, help="images per GPU")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "ffma"])
+    ap.add_argument("--n-ps", type=int, default=0, help="PS shards (0 = one per GPU)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks ---
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------ CPU oracle ---
+def cpu_oracle_step(model, precision, steps=1, batch=1):
+    """Time the CPU oracle training step (tests/oracle_step.py over oracle/liboracle.so)."""
+    import ctypes
+
+    import oracle_binding
+    import oracle_step
+    from paper_1709_06622_b200 import device, models, trainer
+
+    orc = oracle_binding.Oracle(os.path.join(ROOT, "oracle", "liboracle.so"))
+    cfg = models.build(model, batch=batch, precision=precision)
+    L = trainer._lib()
+    h = ctypes.c_void_p()
+    device.check(L.tcb_trainer_create(json.dumps(cfg).encode(), ctypes.byref(h)))
+    out = ctypes.c_char_p()
+    device.check(L.tcb_trainer_describe(h, ctypes.byref(out)))
+    layout = json.loads(out.value.decode())
+    L.tcb_trainer_destroy(h)
+    st = oracle_step.OracleStep(orc, cfg, layout)
+    x, lab = st.inputs()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        st.run(x, lab)
+        g = st.flat_grad().astype("float32")
+        st.sgd(g)
+        times.append(time.perf_counter() - t0)
+    return {"seconds_per_step": statistics.median(times), "batch": batch,
+            "images_per_sec": batch / statistics.median(times), "cores": orc.threads()}
+
+
+# ----------------------------------------------------------- conv roofline ---
+def conv_roofline(cfg, pk, reps=5):
+    """Time every conv pass of one step alone (tcgen05 kernels via the C-ABI
+    conv plans) and return aggregate algorithmic TFLOP/s over all of them."""
+    import torch
+
+    from paper_1709_06622_b200 import device, models
+
+    bf = cfg["precision"] == "bf16"
+    dt = torch.bfloat16 if bf else torch.float32
+    total_flop, total_ms = 0.0, 0.0
+    per_layer = []
+    launches = 0
+    for name, g in models.conv_layers(cfg):
+        c = g["c"] if not bf else -(-g["c"] // 8) * 8
+        geo = device.geom(g["n"], g["h"], g["w"], c, g["k"], g["r"], g["s"], pad=g["pad_h"],
+                          stride=g["stride_h"], pad_w=g["pad_w"], stride_w=g["stride_w"])
+        plan = device.ConvPlan(geo, "gemm", cfg["precision"])
+        x = torch.randn(geo.n, geo.h, geo.w, geo.c, device="cuda").to(dt)
+        w = (torch.randn(geo.k, geo.r, geo.s, geo.c, device="cuda") * 0.05).to(dt)
+        dy = torch.randn(geo.n, geo.ho, geo.wo, geo.k, device="cuda").to(dt)
+        flop = 2.0 * geo.n * geo.ho * geo.wo * geo.k * g["c"] * geo.r * geo.s
+        first = name == "stem" or name.endswith("conv1") and g["c"] == 3
+        passes = [("fwd", lambda: plan.fwd(x, w)), ("wgrad", lambda: plan.wgrad(dy, x))]
+        if not first:
+            passes.insert(1, ("dgrad", lambda: plan.dgrad(dy, w)))
+        row = {"layer": name, "geom": g}
+        for pname, fn in passes:
+            fn()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s.record()
+            for _ in range(reps):
+                fn()
+            e.record()
+            e.synchronize()
+            ms = s.elapsed_time(e) / reps
+            total_ms += ms
+            total_flop += flop
+            launches += 1
+            row[pname + "_ms"] = ms
+            row[pname + "_tflops"] = flop / ms / 1e9
+        per_layer.append(row)
+        del plan, x, w, dy
+    achieved = total_flop / total_ms / 1e9
+    peak = pk["bf16_tflops"] if bf else pk.get("fp32_tflops", 75.0)
+    return {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "conv_tc_kernel (tcgen05 implicit GEMM, fwd+dgrad+wgrad of every conv)",
+            "flop_per_step": total_flop, "conv_ms_per_step": round(total_ms, 3),
+            "peak_kind": f"bf16 dense burst ({pk['source']})"}, per_layer
+
+
+# ------------------------------------------------------------------ main ---
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "RANK" in os.environ:
+        args.gpus = world
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_06622_b200 import models
+    from paper_1709_06622_b200.trainer import Trainer, nccl_unique_id
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
+        nid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        nid = nid[0]
+    else:
+        nid = None
+
+    cfg = models.build(args.model, batch=args.batch, precision=args.precision)
+    cfg["n_ps"] = args.n_ps
+    tr = Trainer(cfg, rank, world, nid)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also materialises the arena and the synthetic batch)
+    for _ in range(max(args.warmup, 3)):
+        tr.step()
+    barrier()
+
+    # phase breakdown of one extra step (StepTrace for Lemma 1)
+    tr.enable_timing(True)
+    tr.step()
+    phases = tr.phase_times()
+    tr.enable_timing(False)
+    launches_per_step = tr.launch_count()
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record(stream)
+    for _ in range(args.steps):
+        tr.step()
+    end.record(stream)
+    barrier()
+    ms_local = start.elapsed_time(end)
+    clk = clocks.stop()
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    loss = tr.loss()
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        inp = tr.describe()["layers"][0]
+        n, h, w = args.batch, inp["shape"][1], inp["shape"][2]
+        cl = inp["c_logical"]
+        images = torch.empty(n, h, w, cl, dtype=torch.float32).pin_memory()
+        images.copy_(tr.tensor("input_f32").view(n, h, w, cl).cpu())
+        labels = tr.tensor("labels").cpu().pin_memory()
+        lossbuf = torch.empty(1, dtype=torch.float32).pin_memory()
+        barrier()
+        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_start.record(stream)
+        for _ in range(args.steps):
+            tr.set_batch(images, labels)
+            tr.step()
+            lossbuf.copy_(tr.tensor("loss")[:1], non_blocking=True)
+        e_end.record(stream)
+        barrier()
+        ems = e_start.elapsed_time(e_end)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": round(world * args.batch * args.steps / (ems / 1e3), 2), "unit": "images/s",
+               "h2d_bytes_per_step": images.numel() * 4 + labels.numel() * 4, "d2h_bytes_per_step": 4,
+               "ms_per_step": round(ems / args.steps, 3)}
+
+    pk = peaks()
+    roof, per_layer = None, None
+    if rank == 0 and not args.no_roofline:
+        roof, per_layer = conv_roofline(cfg, pk)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", f"conv_layers_{args.model}_{args.precision}.json"), "w") as f:
+            json.dump(per_layer, f, indent=1)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_oracle_step(args.model, args.precision, steps=1, batch=1)
+        cpu = {"value": round(r["images_per_sec"], 4), "unit": "images/s", "cores": r["cores"],
+               "kind": "port",
+               "sample": f"1 training step of {args.model} at batch 1 (fwd+bwd+SGD, fp64 accumulate) "
+                         f"= {r['seconds_per_step']:.2f} s"}
+
+    if rank == 0:
+        layout = tr.describe()
+        param_bytes = layout["param_padded"] * 4
+        rs_ag_bytes = 2 * param_bytes * (world - 1) / world if world > 1 else 0
+        line = {
+            "metric": METRIC,
+            "value": round(world * args.batch * args.steps / (ms / 1e3), 2),
+            "unit": "images/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16" if args.precision == "bf16" else "f32",
+            "data": "synthetic (counter-based RNG images/labels, random-init weights)",
+            "config": {"workload": f"{args.model}_synthetic_224" if args.model == "resnet50" else args.model,
+                       "per_gpu_batch": args.batch, "global_batch": args.batch * world,
+                       "ps_shards": args.n_ps or world, "precision": args.precision,
+                       "parallelism": f"dp{world}",
+                       "l2": "inputs larger than L2 (per-step activations >> 126 MB); no flush"},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "phases_ms": {k: round(v, 3) for k, v in phases.items()},
+            "loss": loss,
+            "ps": {"param_bytes": param_bytes, "rs_ag_bytes_per_gpu_step": rs_ag_bytes},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference arm: the reference (traincap) has no executable training step;
+    its hot path is the CPU oracle port of the step (tests/oracle_step.py over
+    oracle/liboracle.so) on this box's host cores, same model and precision."""
+    samples = []
+    r = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_step(args.model, args.precision, steps=1, batch=1)
+        if i >= args.warmup:
+            samples.append(r["seconds_per_step"])
+    sec = statistics.median(samples)
+    v = round(1.0 / sec, 5)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64-accumulate", "data": "synthetic",
+        "config": {"workload": f"{args.model}_synthetic_224", "per_gpu_batch": 1,
+                   "precision": args.precision},
+        "cpu_baseline": {"kind": "port", "cores": r["cores"], "value": v, "unit": "images/s",
+                         "sample": f"{args.model} training step at batch 1 per timed step"},
+        "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,17 +1,779 @@
-// Placeholder; the executor lands in the next commit.
+// The data-parallel training step on one B200 (one process per GPU):
+//
+//   paper step 5  GPU processing : fwd chain -> softmax-xent -> bwd (dgrad +
+//                                  wgrad straight into the flat PS gradient buffer)
+//   paper step 7  distributed update : PS aggregation — ncclReduceScatter of
+//                                  the flat fp32 gradient (N_ps = G) or grouped
+//                                  ncclReduce to N_ps < G shard owners
+//   paper step 6  parameter update : fused momentum-SGD on the owned shard,
+//                                  refreshing the compute-dtype copy
+//   paper step 1  parameter refresh : ncclAllGather (or per-owner broadcast)
+//                                  of the updated compute-dtype weights
+// (/root/reference/PAPER.md:229-238). Per-phase CUDA-event times form the
+// StepTrace the reference's Lemma 1 consumes
+// (/root/reference/proj/include/traincap/io.hpp:23-26).
+//
+// Memory: one cudaMalloc'ed HBM arena holds activations, gradients, flat
+// parameter/gradient/momentum buffers and workspaces (bump-allocated,
+// 256-byte aligned). The layer-to-PS-shard assignment: the
+// parameters of conv layers 1..q (fc layers are convs spanning the whole
+// spatial map) are flattened in layer order, [K][R][S][C] weights then bias,
+// each segment 64-element aligned; the buffer is padded to G*64 elements and
+// rank r owns [r*P/G, (r+1)*P/G).
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <json.hpp>
+#include <nccl.h>
+
 #include "runtime.h"
 #include "tcb.h"
-#define TCB_API extern "C" __attribute__((visibility("default")))
+#include "tcb/kernels.h"
+
+namespace tcb {
+namespace {
+
+using json = nlohmann::json;
+
+constexpr size_t kAlign = 256;
+constexpr size_t kParamAlign = 64;  // elements
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+enum class Op { Input, Conv, MaxPool, AvgPool, Loss };
+
+struct Node {
+    Op op = Op::Input;
+    std::string name;
+    int in = -1, residual = -1;
+    // output tensor NHWC (c = allocated channels, c_logical = semantic channels)
+    int n = 0, h = 0, w = 0, c = 0, c_logical = 0;
+    // conv
+    ConvGeom g{};
+    bool bias = false, relu = false, need_dgrad = true;
+    int conv_index = 0;
+    size_t woff = 0, boff = 0, wcount = 0;  // flat param offsets (elements)
+    float init_scale = 0.f;
+    std::string algo = "gemm";
+    // pool
+    int f = 0, s = 0, p = 0;
+    // arena offsets (bytes)
+    size_t act = 0, grad = 0, argmax = 0, wT = 0;
+    // backward plan for this node's OUTPUT tensor
+    int final_writer = -1;              // consumer node that writes G[this] last
+    std::vector<int> compute_from;      // consumers with a computed contribution
+    std::vector<int> alias_from;        // consumers whose G[out] adds via the residual path
+    std::map<int, size_t> tmp;          // consumer -> temp buffer offset (non-final computed)
+};
+
+struct Phase {
+    cudaEvent_t e[6]{};
+};
+
+}  // namespace
+}  // namespace tcb
+
 using namespace tcb;
-TCB_API int tcb_trainer_create(const char*, tcb_trainer**) { return fail(TCB_ERR_UNSUPPORTED, "trainer not built"); }
-TCB_API int tcb_trainer_destroy(tcb_trainer*) { return TCB_OK; }
-TCB_API int tcb_nccl_unique_id(uint8_t*) { return fail(TCB_ERR_UNSUPPORTED, "trainer not built"); }
-TCB_API int tcb_trainer_join(tcb_trainer*, int, int, const uint8_t*) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
-TCB_API int tcb_trainer_set_batch(tcb_trainer*, const float*, const int32_t*, void*) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
-TCB_API int tcb_trainer_step(tcb_trainer*, void*) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
-TCB_API int tcb_trainer_loss(tcb_trainer*, float*, void*) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
-TCB_API int tcb_trainer_phase_times(tcb_trainer*, float*) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
-TCB_API int tcb_trainer_enable_timing(tcb_trainer*, int) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
-TCB_API int tcb_trainer_describe(tcb_trainer*, char**) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
-TCB_API int tcb_trainer_tensor(tcb_trainer*, const char*, void**, size_t*) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
-TCB_API int tcb_trainer_launch_count(tcb_trainer*, int*) { return fail(TCB_ERR_UNSUPPORTED, "x"); }
+
+struct tcb_trainer {
+    json cfg;
+    DType dt = DType::BF16;
+    bool bf16 = true;
+    int batch = 0, classes = 0;
+    uint64_t seed = 20260810;
+    float lr = 0.01f, momentum = 0.9f, weight_decay = 0.f;
+    std::vector<Node> nodes;
+    int logits = -1;
+
+    // distributed
+    int rank = 0, world = 1, n_ps = 0;
+    ncclComm_t comm = nullptr;
+    size_t param_count = 0;   // logical (unpadded) parameter elements
+    size_t param_padded = 0;  // padded to world * kParamAlign
+    size_t shard = 0;
+
+    // arena
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    size_t off_param = 0, off_grad = 0, off_mom = 0, off_wc = 0, off_ws = 0, off_colsum = 0;
+    size_t off_labels = 0, off_loss = 0, off_input_f32 = 0;
+    size_t ws_bytes = 0, colsum_bytes = 0;
+
+    cudaStream_t stream = nullptr;  // stream of the last step call
+    bool timing = false;
+    Phase ph;
+    float phase_ms[5] = {0, 0, 0, 0, 0};
+    int launches = 0;
+    bool initialized = false;
+
+    template <typename T = void>
+    T* at(size_t off) const {
+        return reinterpret_cast<T*>(static_cast<char*>(arena) + off);
+    }
+};
+
+namespace tcb {
+namespace {
+
+#define TRY_CUDA(expr)                                           \
+    do {                                                         \
+        cudaError_t e__ = (expr);                                \
+        if (e__ != cudaSuccess) return check_cuda(e__, #expr);   \
+    } while (0)
+#define TRY_NCCL(expr)                                                                    \
+    do {                                                                                  \
+        ncclResult_t r__ = (expr);                                                        \
+        if (r__ != ncclSuccess)                                                           \
+            return fail(TCB_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r__)); \
+    } while (0)
+#define TRY(expr)                     \
+    do {                              \
+        int rc__ = (expr);            \
+        if (rc__ != TCB_OK) return rc__; \
+    } while (0)
+
+// --------------------------------------------------------------- build ----
+int build_graph(tcb_trainer* t) {
+    const json& cfg = t->cfg;
+    t->bf16 = cfg.value("precision", std::string("bf16")) == "bf16";
+    t->dt = t->bf16 ? DType::BF16 : DType::F32;
+    t->batch = cfg.at("batch").get<int>();
+    t->classes = cfg.at("classes").get<int>();
+    t->seed = cfg.value("seed", uint64_t(20260810));
+    t->lr = cfg.value("lr", 0.01f);
+    t->momentum = cfg.value("momentum", 0.9f);
+    t->weight_decay = cfg.value("weight_decay", 0.f);
+    t->n_ps = cfg.value("n_ps", 0);
+    t->world = cfg.value("world", 1);  // layout planning before join (join overrides)
+
+    std::map<std::string, int> by_name;
+    int conv_idx = 0;
+    for (const json& L : cfg.at("layers")) {
+        Node nd;
+        nd.name = L.at("name").get<std::string>();
+        const std::string op = L.at("op").get<std::string>();
+        auto src = [&](const char* key) -> int {
+            if (!L.contains(key) || L.at(key).is_null()) return -1;
+            auto it = by_name.find(L.at(key).get<std::string>());
+            if (it == by_name.end()) throw std::runtime_error("unknown tensor " + L.at(key).dump());
+            return it->second;
+        };
+        if (op == "input") {
+            nd.op = Op::Input;
+            nd.n = t->batch;
+            nd.h = L.at("h").get<int>();
+            nd.w = L.at("w").get<int>();
+            nd.c_logical = L.at("c").get<int>();
+            nd.c = t->bf16 ? static_cast<int>(round_up(nd.c_logical, 8)) : nd.c_logical;
+        } else if (op == "conv") {
+            nd.op = Op::Conv;
+            nd.in = src("in");
+            nd.residual = src("residual");
+            const Node& x = t->nodes.at(nd.in);
+            nd.g = ConvGeom{x.n, x.h, x.w, x.c, L.at("k").get<int>(), L.at("r").get<int>(),
+                            L.value("s", L.at("r").get<int>()), L.value("pad_h", L.value("pad", 0)),
+                            L.value("pad_w", L.value("pad", 0)), L.value("stride_h", L.value("stride", 1)),
+                            L.value("stride_w", L.value("stride", 1))};
+            nd.bias = L.value("bias", false);
+            nd.relu = L.value("relu", false);
+            nd.algo = L.value("algo", std::string("gemm"));
+            nd.n = x.n;
+            nd.h = nd.g.ho();
+            nd.w = nd.g.wo();
+            nd.c = nd.c_logical = nd.g.k;
+            nd.conv_index = ++conv_idx;
+            nd.need_dgrad = t->nodes.at(nd.in).op != Op::Input;
+            const int fan_in = x.c_logical * nd.g.r * nd.g.s;
+            // He-uniform bound sqrt(6 / fan_in) times an optional gain (residual branches
+            // of the BN-free ResNet use a small gain on their last conv, Fixup-style).
+            nd.init_scale = L.value("init_gain", 1.0f) * std::sqrt(6.0f / static_cast<float>(fan_in));
+            std::string why;
+            if (nd.h < 1 || nd.w < 1 || !geom_valid(nd.g, &why))
+                throw std::runtime_error("layer " + nd.name + ": bad geometry " + why);
+            if (t->bf16 && !conv_tc_supported(nd.g, ConvMode::Fwd))
+                throw std::runtime_error("layer " + nd.name + ": bf16 path needs C % 8 == 0");
+            if (nd.residual >= 0) {
+                const Node& r = t->nodes.at(nd.residual);
+                if (r.h != nd.h || r.w != nd.w || r.c != nd.c)
+                    throw std::runtime_error("layer " + nd.name + ": residual shape mismatch");
+            }
+        } else if (op == "maxpool" || op == "avgpool") {
+            nd.op = op == "maxpool" ? Op::MaxPool : Op::AvgPool;
+            nd.in = src("in");
+            const Node& x = t->nodes.at(nd.in);
+            nd.n = x.n;
+            nd.c = x.c;
+            nd.c_logical = x.c_logical;
+            if (nd.op == Op::MaxPool) {
+                nd.f = L.at("f").get<int>();
+                nd.s = L.value("stride", nd.f);
+                nd.p = L.value("pad", 0);
+                nd.h = (x.h + 2 * nd.p - nd.f) / nd.s + 1;
+                nd.w = (x.w + 2 * nd.p - nd.f) / nd.s + 1;
+                if (nd.f > 15 || nd.h < 1 || nd.w < 1)
+                    throw std::runtime_error("layer " + nd.name + ": bad pool window");
+            } else {
+                nd.h = nd.w = 1;
+            }
+        } else if (op == "loss") {
+            nd.op = Op::Loss;
+            nd.in = src("in");
+            const Node& x = t->nodes.at(nd.in);
+            if (x.h != 1 || x.w != 1 || x.c != t->classes)
+                throw std::runtime_error("loss input must be N x 1 x 1 x classes");
+            t->logits = nd.in;
+        } else {
+            throw std::runtime_error("unknown op " + op);
+        }
+        by_name[nd.name] = static_cast<int>(t->nodes.size());
+        t->nodes.push_back(std::move(nd));
+    }
+    if (t->logits < 0) throw std::runtime_error("model has no loss layer");
+
+    // Backward plan: who contributes to each tensor's gradient.
+    const int count = static_cast<int>(t->nodes.size());
+    for (int i = 0; i < count; ++i) {
+        const Node& nd = t->nodes[i];
+        if (nd.op == Op::Conv) {
+            if (nd.need_dgrad) t->nodes[nd.in].compute_from.push_back(i);
+            if (nd.residual >= 0 && t->nodes[nd.residual].op != Op::Input)
+                t->nodes[nd.residual].alias_from.push_back(i);
+        } else if (nd.op == Op::MaxPool || nd.op == Op::AvgPool) {
+            if (t->nodes[nd.in].op != Op::Input) t->nodes[nd.in].compute_from.push_back(i);
+        }
+    }
+    for (Node& nd : t->nodes) {
+        if (!nd.compute_from.empty())
+            nd.final_writer = *std::min_element(nd.compute_from.begin(), nd.compute_from.end());
+    }
+    return TCB_OK;
+}
+
+// ---------------------------------------------------------------- arena ---
+struct Bump {
+    size_t top = 0;
+    size_t take(size_t bytes) {
+        const size_t off = top;
+        top += round_up(std::max<size_t>(bytes, 1), kAlign);
+        return off;
+    }
+};
+
+void plan_params(tcb_trainer* t) {
+    size_t off = 0, logical = 0;
+    for (Node& nd : t->nodes) {
+        if (nd.op != Op::Conv) continue;
+        nd.wcount = size_t(nd.g.k) * nd.g.r * nd.g.s * nd.g.c;
+        nd.woff = off;
+        off = round_up(off + nd.wcount, kParamAlign);
+        logical += size_t(nd.g.k) * nd.g.r * nd.g.s * t->nodes[nd.in].c_logical;
+        if (nd.bias) {
+            nd.boff = off;
+            off = round_up(off + nd.g.k, kParamAlign);
+            logical += nd.g.k;
+        }
+    }
+    t->param_count = logical;
+    const size_t unit = size_t(t->world) * kParamAlign;
+    t->param_padded = round_up(std::max<size_t>(off, 1), unit);
+    t->shard = t->param_padded / t->world;
+}
+
+int allocate(tcb_trainer* t) {
+    const size_t es = dtype_size(t->dt);
+    Bump b;
+    plan_params(t);
+    t->off_param = b.take(t->param_padded * 4);
+    t->off_grad = b.take(t->param_padded * 4);
+    t->off_mom = b.take(t->param_padded * 4);  // only the owned shard is used
+    t->off_wc = t->bf16 ? b.take(t->param_padded * 2) : t->off_param;
+    size_t ws = 0, colsum = 0;
+    for (Node& nd : t->nodes) {
+        const size_t elems = size_t(nd.n) * nd.h * nd.w * nd.c;
+        if (nd.op == Op::Loss) continue;
+        nd.act = b.take(elems * es);
+        if (nd.op != Op::Input) nd.grad = b.take(elems * es);
+        if (nd.op == Op::MaxPool) nd.argmax = b.take(elems);
+        if (nd.op == Op::Conv) {
+            ws = std::max(ws, t->bf16 ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
+                                      : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
+            if (nd.bias) colsum = std::max(colsum, column_sum_workspace(nd.n * nd.h * nd.w, nd.g.k));
+            if (t->bf16 && nd.need_dgrad) nd.wT = b.take(nd.wcount * 2);
+        }
+    }
+    for (Node& nd : t->nodes)
+        for (int c : nd.compute_from)
+            if (c != nd.final_writer) nd.tmp[c] = b.take(size_t(nd.n) * nd.h * nd.w * nd.c * es);
+    t->ws_bytes = ws;
+    t->colsum_bytes = colsum;
+    t->off_ws = b.take(ws);
+    t->off_colsum = b.take(colsum);
+    t->off_labels = b.take(size_t(t->batch) * 4);
+    t->off_loss = b.take(size_t(t->batch + 1) * 4);
+    const Node& in = t->nodes[0];
+    t->off_input_f32 = b.take(size_t(in.n) * in.h * in.w * in.c_logical * 4);
+    t->arena_bytes = b.top;
+    cudaError_t e = cudaMalloc(&t->arena, t->arena_bytes);
+    if (e != cudaSuccess)
+        return fail(TCB_ERR_OOM, "arena of " + std::to_string(t->arena_bytes) + " bytes: " +
+                                     cudaGetErrorString(e));
+    return TCB_OK;
+}
+
+int pack_input(tcb_trainer* t, cudaStream_t st) {
+    const Node& in = t->nodes[0];
+    const size_t px = size_t(in.n) * in.h * in.w;
+    const float* src = t->at<float>(t->off_input_f32);
+    t->launches++;
+    return check_cuda(pack_channels(t->dt, src, t->at(in.act), px, in.c_logical, in.c, st),
+                      "pack_input");
+}
+
+int initialize(tcb_trainer* t, cudaStream_t st) {
+    // parameters: deterministic per-layer streams, tag = 1000 + conv index
+    float* param = t->at<float>(t->off_param);
+    TRY_CUDA(cudaMemsetAsync(param, 0, t->param_padded * 4, st));
+    TRY_CUDA(cudaMemsetAsync(t->at(t->off_mom), 0, t->param_padded * 4, st));
+    TRY_CUDA(cudaMemsetAsync(t->at(t->off_grad), 0, t->param_padded * 4, st));
+    for (const Node& nd : t->nodes) {
+        if (nd.op != Op::Conv) continue;
+        const int cl = t->nodes[nd.in].c_logical, cp = nd.g.c;
+        const size_t outer = size_t(nd.g.k) * nd.g.r * nd.g.s;
+        if (cl == cp) {
+            TRY_CUDA(fill_uniform(DType::F32, param + nd.woff, outer * cl, t->seed,
+                                  1000 + nd.conv_index, -nd.init_scale, nd.init_scale, st));
+        } else {
+            // generate the logical stream in the grad buffer, scatter into padded channels
+            float* scratch = t->at<float>(t->off_grad);
+            TRY_CUDA(fill_uniform(DType::F32, scratch, outer * cl, t->seed, 1000 + nd.conv_index,
+                                  -nd.init_scale, nd.init_scale, st));
+            TRY_CUDA(pack_channels(DType::F32, scratch, param + nd.woff, outer, cl, cp, st));
+        }
+    }
+    if (t->bf16)
+        TRY_CUDA(cast(DType::F32, param, DType::BF16, t->at(t->off_wc), t->param_padded, st));
+    // synthetic mini-batch: worker r uses seed + r (distinct mini-batches)
+    const Node& in = t->nodes[0];
+    TRY_CUDA(fill_uniform(DType::F32, t->at(t->off_input_f32), size_t(in.n) * in.h * in.w * in.c_logical,
+                          t->seed + t->rank, 1, -1.f, 1.f, st));
+    TRY_CUDA(fill_labels(t->at<int32_t>(t->off_labels), t->batch, t->classes, t->seed + t->rank, st));
+    TRY(pack_input(t, st));
+    TRY_CUDA(cudaMemsetAsync(t->at(t->off_grad), 0, t->param_padded * 4, st));
+    TRY_CUDA(cudaStreamSynchronize(st));
+    t->initialized = true;
+    return TCB_OK;
+}
+
+// ------------------------------------------------------------------ step ---
+int refresh_transposes(tcb_trainer* t, cudaStream_t st) {
+    if (!t->bf16) return TCB_OK;
+    for (const Node& nd : t->nodes) {
+        if (nd.op != Op::Conv || !nd.need_dgrad) continue;
+        TRY_CUDA(transpose_krsc(DType::BF16, t->at<__nv_bfloat16>(t->off_wc) + nd.woff, t->at(nd.wT),
+                                nd.g.k, nd.g.r, nd.g.s, nd.g.c, st));
+        t->launches++;
+    }
+    return TCB_OK;
+}
+
+int forward(tcb_trainer* t, cudaStream_t st) {
+    for (const Node& nd : t->nodes) {
+        const Node* x = nd.in >= 0 ? &t->nodes[nd.in] : nullptr;
+        switch (nd.op) {
+            case Op::Input: break;
+            case Op::Conv: {
+                Epilogue ep;
+                ep.bias = nd.bias ? t->at<float>(t->off_param) + nd.boff : nullptr;
+                ep.residual = nd.residual >= 0 ? t->at(t->nodes[nd.residual].act) : nullptr;
+                ep.relu = nd.relu;
+                if (t->bf16)
+                    TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
+                                         ep, t->at(nd.act), st));
+                else
+                    TRY_CUDA(conv_ffma_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
+                                           ep, t->at<float>(nd.act), st));
+                t->launches++;
+                break;
+            }
+            case Op::MaxPool:
+                TRY_CUDA(maxpool_fwd(t->dt, t->at(x->act), t->at(nd.act), t->at<uint8_t>(nd.argmax), x->n,
+                                     x->h, x->w, x->c, nd.f, nd.s, nd.p, st));
+                t->launches++;
+                break;
+            case Op::AvgPool:
+                TRY_CUDA(avgpool_global_fwd(t->dt, t->at(x->act), t->at(nd.act), x->n, x->h * x->w, x->c, st));
+                t->launches++;
+                break;
+            case Op::Loss: {
+                const Node& z = t->nodes[t->logits];
+                TRY_CUDA(softmax_xent(t->dt, t->at(z.act), t->at<int32_t>(t->off_labels), t->at(z.grad),
+                                      t->at<float>(t->off_loss), t->batch, t->classes, st));
+                t->launches += 2;
+                break;
+            }
+        }
+    }
+    return TCB_OK;
+}
+
+// Gradient contribution of consumer `ci` to tensor `ti`: either the final
+// G[ti] (with every other contribution fused in) or a temp buffer.
+int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
+    Node& tgt = t->nodes[ti];
+    const Node& con = t->nodes[ci];
+    const bool final = tgt.final_writer == ci;
+    const size_t elems = size_t(tgt.n) * tgt.h * tgt.w * tgt.c;
+    void* out = final ? t->at(tgt.grad) : t->at(tgt.tmp.at(ci));
+    const Node* producer = &tgt;
+    const bool mask_needed = final && producer->op == Op::Conv && producer->relu;
+
+    // extra contributions to fold in (only at the final writer)
+    std::vector<const void*> extras;
+    if (final) {
+        for (int c : tgt.compute_from)
+            if (c != ci) extras.push_back(t->at(tgt.tmp.at(c)));
+        for (int a : tgt.alias_from) extras.push_back(t->at(t->nodes[a].grad));
+    }
+    if (con.op == Op::Conv) {
+        // combine extras into one residual operand for the dgrad epilogue
+        const void* residual = nullptr;
+        if (extras.size() == 1) {
+            residual = extras[0];
+        } else if (extras.size() > 1) {
+            void* acc = const_cast<void*>(extras[0]);
+            for (size_t i = 1; i < extras.size(); ++i) {
+                TRY_CUDA(add_inplace(t->dt, acc, extras[i], elems, st));
+                t->launches++;
+            }
+            residual = acc;
+        }
+        Epilogue ep;
+        ep.residual = residual;
+        ep.mask = mask_needed ? t->at(tgt.act) : nullptr;
+        if (t->bf16)
+            TRY_CUDA(conv_tc_dgrad(con.g, t->at(con.grad), t->at(con.wT), ep, out, st));
+        else
+            TRY_CUDA(conv_ffma_dgrad(con.g, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
+                                     ep, static_cast<float*>(out), st));
+        t->launches++;
+        return TCB_OK;
+    }
+    if (con.op == Op::MaxPool)
+        TRY_CUDA(maxpool_bwd(t->dt, t->at(con.grad), t->at<uint8_t>(con.argmax), out, tgt.n, tgt.h, tgt.w,
+                             tgt.c, con.f, con.s, con.p, st));
+    else
+        TRY_CUDA(avgpool_global_bwd(t->dt, t->at(con.grad), out, tgt.n, tgt.h * tgt.w, tgt.c, st));
+    t->launches++;
+    for (const void* e : extras) {
+        TRY_CUDA(add_inplace(t->dt, out, e, elems, st));
+        t->launches++;
+    }
+    if (mask_needed) {
+        TRY_CUDA(relu_mask_inplace(t->dt, out, t->at(tgt.act), elems, st));
+        t->launches++;
+    }
+    return TCB_OK;
+}
+
+int backward(tcb_trainer* t, cudaStream_t st) {
+    TRY(refresh_transposes(t, st));
+    float* grad = t->at<float>(t->off_grad);
+    for (int i = static_cast<int>(t->nodes.size()) - 1; i >= 0; --i) {
+        const Node& nd = t->nodes[i];
+        if (nd.op == Op::Conv) {
+            const Node& x = t->nodes[nd.in];
+            // weight (and bias) gradient straight into the flat PS buffer
+            if (t->bf16)
+                TRY_CUDA(conv_tc_wgrad(nd.g, t->at(nd.grad), t->at(x.act), grad + nd.woff, t->at(t->off_ws), st));
+            else
+                TRY_CUDA(conv_ffma_wgrad(nd.g, t->at<float>(nd.grad), t->at<float>(x.act), grad + nd.woff,
+                                         t->at(t->off_ws), st));
+            t->launches += 2;
+            if (nd.bias) {
+                TRY_CUDA(column_sum(t->dt, t->at(nd.grad), grad + nd.boff, nd.n * nd.h * nd.w, nd.g.k,
+                                    t->at<float>(t->off_colsum), st));
+                t->launches += 2;
+            }
+            if (nd.need_dgrad) TRY(backward_contribution(t, i, nd.in, st));
+        } else if (nd.op == Op::MaxPool || nd.op == Op::AvgPool) {
+            if (t->nodes[nd.in].op != Op::Input) TRY(backward_contribution(t, i, nd.in, st));
+        }
+    }
+    return TCB_OK;
+}
+
+int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, cudaEvent_t after_sgd) {
+    float* grad = t->at<float>(t->off_grad);
+    float* param = t->at<float>(t->off_param);
+    float* mom = t->at<float>(t->off_mom);
+    const float gscale = 1.0f / static_cast<float>(t->world);
+    const ncclDataType_t wdt = t->bf16 ? ncclBfloat16 : ncclFloat32;
+    const size_t wes = t->bf16 ? 2 : 4;
+    char* wc = t->at<char>(t->off_wc);
+    const int owners = (t->n_ps > 0 && t->n_ps < t->world) ? t->n_ps : t->world;
+
+    if (t->world > 1 && owners == t->world) {
+        // PS shards = GPUs: reduce-scatter (in place) -> SGD on own shard -> all-gather
+        TRY_NCCL(ncclReduceScatter(grad, grad + t->rank * t->shard, t->shard, ncclFloat32, ncclSum,
+                                   t->comm, st));
+        t->launches++;
+        if (after_rs) TRY_CUDA(cudaEventRecord(after_rs, st));
+        const size_t o = t->rank * t->shard;
+        TRY_CUDA(sgd_momentum(param + o, grad + o, mom + o, t->dt, t->bf16 ? wc + o * 2 : nullptr, t->shard,
+                              t->lr, t->momentum, t->weight_decay, gscale, st));
+        t->launches++;
+        if (after_sgd) TRY_CUDA(cudaEventRecord(after_sgd, st));
+        TRY_NCCL(ncclAllGather(wc + o * wes, wc, t->shard, wdt, t->comm, st));
+        t->launches++;
+    } else if (t->world > 1) {
+        // N_ps < G: shard j (of N_ps) is owned by rank j; every worker pushes its
+        // full gradient to the owners (Lemma 2's N_w * S_p / N_ps ingress).
+        const size_t per = round_up((t->param_padded + owners - 1) / owners, kParamAlign);
+        TRY_NCCL(ncclGroupStart());
+        for (int j = 0; j < owners; ++j) {
+            const size_t o = j * per;
+            if (o >= t->param_padded) break;
+            const size_t cnt = std::min(per, t->param_padded - o);
+            TRY_NCCL(ncclReduce(grad + o, grad + o, cnt, ncclFloat32, ncclSum, j, t->comm, st));
+        }
+        TRY_NCCL(ncclGroupEnd());
+        t->launches++;
+        if (after_rs) TRY_CUDA(cudaEventRecord(after_rs, st));
+        if (t->rank < owners) {
+            const size_t o = t->rank * per;
+            if (o < t->param_padded) {
+                const size_t cnt = std::min(per, t->param_padded - o);
+                TRY_CUDA(sgd_momentum(param + o, grad + o, mom + o, t->dt, t->bf16 ? wc + o * 2 : nullptr,
+                                      cnt, t->lr, t->momentum, t->weight_decay, gscale, st));
+                t->launches++;
+            }
+        }
+        if (after_sgd) TRY_CUDA(cudaEventRecord(after_sgd, st));
+        TRY_NCCL(ncclGroupStart());
+        for (int j = 0; j < owners; ++j) {
+            const size_t o = j * per;
+            if (o >= t->param_padded) break;
+            const size_t cnt = std::min(per, t->param_padded - o);
+            TRY_NCCL(ncclBroadcast(wc + o * wes, wc + o * wes, cnt, wdt, j, t->comm, st));
+        }
+        TRY_NCCL(ncclGroupEnd());
+        t->launches++;
+    } else {
+        if (after_rs) TRY_CUDA(cudaEventRecord(after_rs, st));
+        TRY_CUDA(sgd_momentum(param, grad, mom, t->dt, t->bf16 ? wc : nullptr, t->param_padded, t->lr,
+                              t->momentum, t->weight_decay, gscale, st));
+        t->launches++;
+        if (after_sgd) TRY_CUDA(cudaEventRecord(after_sgd, st));
+    }
+    return TCB_OK;
+}
+
+}  // namespace
+}  // namespace tcb
+
+#define TCB_API extern "C" __attribute__((visibility("default")))
+
+TCB_API int tcb_trainer_create(const char* config_json, tcb_trainer** out) {
+    if (!config_json || !out) return fail(TCB_ERR_INVALID, "NULL argument");
+    auto t = std::make_unique<tcb_trainer>();
+    try {
+        t->cfg = json::parse(config_json);
+        TRY(build_graph(t.get()));
+    } catch (const std::exception& e) {
+        return fail(TCB_ERR_INVALID, std::string("model config: ") + e.what());
+    }
+    *out = t.release();
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_destroy(tcb_trainer* t) {
+    if (!t) return TCB_OK;
+    if (t->comm) ncclCommDestroy(t->comm);
+    for (cudaEvent_t& e : t->ph.e)
+        if (e) cudaEventDestroy(e);
+    if (t->arena) cudaFree(t->arena);
+    delete t;
+    return TCB_OK;
+}
+
+TCB_API int tcb_nccl_unique_id(uint8_t* id128) {
+    if (!id128) return fail(TCB_ERR_INVALID, "NULL argument");
+    ncclUniqueId id;
+    TRY_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(id128, &id, sizeof(id));
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t* id128) {
+    if (!t || world < 1 || rank < 0 || rank >= world) return fail(TCB_ERR_INVALID, "bad rank/world");
+    if (t->initialized) return fail(TCB_ERR_INVALID, "join before the first step");
+    t->rank = rank;
+    t->world = world;
+    if (world > 1) {
+        if (!id128) return fail(TCB_ERR_INVALID, "NCCL id required for world > 1");
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        TRY_NCCL(ncclCommInitRank(&t->comm, world, id, rank));
+    }
+    return TCB_OK;
+}
+
+static int ensure_ready(tcb_trainer* t, cudaStream_t st) {
+    if (t->initialized) return TCB_OK;
+    if (!t->arena) TRY(allocate(t));
+    for (cudaEvent_t& e : t->ph.e)
+        if (!e) TRY_CUDA(cudaEventCreate(&e));
+    return initialize(t, st);
+}
+
+TCB_API int tcb_trainer_set_batch(tcb_trainer* t, const float* host_images, const int32_t* host_labels,
+                                  void* stream) {
+    if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
+    auto st = static_cast<cudaStream_t>(stream);
+    TRY(ensure_ready(t, st));
+    const Node& in = t->nodes[0];
+    if (host_images) {
+        TRY_CUDA(cudaMemcpyAsync(t->at(t->off_input_f32), host_images,
+                                 size_t(in.n) * in.h * in.w * in.c_logical * 4, cudaMemcpyHostToDevice, st));
+        TRY(pack_input(t, st));
+    }
+    if (host_labels)
+        TRY_CUDA(cudaMemcpyAsync(t->at(t->off_labels), host_labels, size_t(t->batch) * 4,
+                                 cudaMemcpyHostToDevice, st));
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_step(tcb_trainer* t, void* stream) {
+    if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
+    auto st = static_cast<cudaStream_t>(stream);
+    TRY(ensure_ready(t, st));
+    t->launches = 0;
+    cudaEvent_t* e = t->ph.e;
+    if (t->timing) TRY_CUDA(cudaEventRecord(e[0], st));
+    TRY(forward(t, st));
+    if (t->timing) TRY_CUDA(cudaEventRecord(e[1], st));
+    TRY(backward(t, st));
+    if (t->timing) TRY_CUDA(cudaEventRecord(e[2], st));
+    TRY(aggregate_and_update(t, st, t->timing ? e[3] : nullptr, t->timing ? e[4] : nullptr));
+    if (t->timing) TRY_CUDA(cudaEventRecord(e[5], st));
+    return check_cuda(cudaGetLastError(), "step");
+}
+
+TCB_API int tcb_trainer_loss(tcb_trainer* t, float* loss_host, void* stream) {
+    if (!t || !loss_host) return fail(TCB_ERR_INVALID, "NULL argument");
+    auto st = static_cast<cudaStream_t>(stream);
+    TRY_CUDA(cudaMemcpyAsync(loss_host, t->at(t->off_loss), 4, cudaMemcpyDeviceToHost, st));
+    TRY_CUDA(cudaStreamSynchronize(st));
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_enable_timing(tcb_trainer* t, int on) {
+    if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
+    t->timing = on != 0;
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_phase_times(tcb_trainer* t, float* ms5) {
+    if (!t || !ms5) return fail(TCB_ERR_INVALID, "NULL argument");
+    if (!t->timing) return fail(TCB_ERR_INVALID, "timing not enabled");
+    cudaEvent_t* e = t->ph.e;
+    TRY_CUDA(cudaEventSynchronize(e[5]));
+    for (int i = 0; i < 5; ++i) TRY_CUDA(cudaEventElapsedTime(&ms5[i], e[i], e[i + 1]));
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_launch_count(tcb_trainer* t, int* count) {
+    if (!t || !count) return fail(TCB_ERR_INVALID, "NULL argument");
+    *count = t->launches;
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
+    if (!t || !json_out) return fail(TCB_ERR_INVALID, "NULL argument");
+    if (!t->arena) plan_params(t);
+    json d;
+    d["precision"] = t->bf16 ? "bf16" : "ffma";
+    d["batch"] = t->batch;
+    d["classes"] = t->classes;
+    d["world"] = t->world;
+    d["rank"] = t->rank;
+    d["param_count"] = t->param_count;
+    d["param_padded"] = t->param_padded;
+    d["shard"] = t->shard;
+    d["arena_bytes"] = t->arena_bytes;
+    json layers = json::array();
+    for (size_t i = 0; i < t->nodes.size(); ++i) {
+        const Node& nd = t->nodes[i];
+        json L;
+        L["index"] = i;
+        L["name"] = nd.name;
+        static const char* ops[] = {"input", "conv", "maxpool", "avgpool", "loss"};
+        L["op"] = ops[static_cast<int>(nd.op)];
+        L["in"] = nd.in;
+        L["residual"] = nd.residual;
+        L["shape"] = {nd.n, nd.h, nd.w, nd.c};
+        L["c_logical"] = nd.c_logical;
+        if (nd.op == Op::Conv) {
+            L["conv_index"] = nd.conv_index;
+            L["geom"] = {nd.g.n, nd.g.h, nd.g.w, nd.g.c, nd.g.k, nd.g.r, nd.g.s, nd.g.pad_h, nd.g.pad_w,
+                         nd.g.stride_h, nd.g.stride_w};
+            L["relu"] = nd.relu;
+            L["bias"] = nd.bias;
+            L["woff"] = nd.woff;
+            L["wcount"] = nd.wcount;
+            L["boff"] = nd.bias ? json(nd.boff) : json(nullptr);
+            L["init_scale"] = nd.init_scale;
+            const size_t first = nd.woff / std::max<size_t>(t->shard, 1);
+            const size_t last_el = (nd.bias ? nd.boff + nd.g.k : nd.woff + nd.wcount) - 1;
+            L["shards"] = {first, last_el / std::max<size_t>(t->shard, 1)};
+        }
+        if (nd.op == Op::MaxPool) L["pool"] = {nd.f, nd.s, nd.p};
+        layers.push_back(std::move(L));
+    }
+    d["layers"] = std::move(layers);
+    const std::string s = d.dump();
+    *json_out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*json_out, s.c_str(), s.size() + 1);
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_tensor(tcb_trainer* t, const char* name, void** ptr, size_t* bytes) {
+    if (!t || !name || !ptr) return fail(TCB_ERR_INVALID, "NULL argument");
+    if (!t->arena) return fail(TCB_ERR_INVALID, "trainer not initialised (run a step or set_batch)");
+    const std::string n(name);
+    const size_t es = dtype_size(t->dt);
+    size_t b = 0;
+    void* p = nullptr;
+    auto node_bytes = [&](const Node& nd) { return size_t(nd.n) * nd.h * nd.w * nd.c * es; };
+    if (n == "param") { p = t->at(t->off_param); b = t->param_padded * 4; }
+    else if (n == "grad") { p = t->at(t->off_grad); b = t->param_padded * 4; }
+    else if (n == "momentum") { p = t->at(t->off_mom); b = t->param_padded * 4; }
+    else if (n == "wcompute") { p = t->at(t->off_wc); b = t->param_padded * es; }
+    else if (n == "labels") { p = t->at(t->off_labels); b = size_t(t->batch) * 4; }
+    else if (n == "loss") { p = t->at(t->off_loss); b = size_t(t->batch + 1) * 4; }
+    else if (n == "input") { p = t->at(t->nodes[0].act); b = node_bytes(t->nodes[0]); }
+    else if (n == "input_f32") {
+        const Node& in = t->nodes[0];
+        p = t->at(t->off_input_f32);
+        b = size_t(in.n) * in.h * in.w * in.c_logical * 4;
+    } else if (n.rfind("act:", 0) == 0 || n.rfind("dact:", 0) == 0) {
+        const bool grad = n[0] == 'd';
+        const int i = std::stoi(n.substr(grad ? 5 : 4));
+        if (i < 0 || i >= static_cast<int>(t->nodes.size())) return fail(TCB_ERR_INVALID, "bad node index");
+        const Node& nd = t->nodes[i];
+        if (nd.op == Op::Loss || (grad && nd.op == Op::Input)) return fail(TCB_ERR_INVALID, "no such tensor");
+        p = t->at(grad ? nd.grad : nd.act);
+        b = node_bytes(nd);
+    } else {
+        return fail(TCB_ERR_INVALID, "unknown tensor " + n);
+    }
+    *ptr = p;
+    if (bytes) *bytes = b;
+    return TCB_OK;
+}

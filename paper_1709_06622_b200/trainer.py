@@ -1,0 +1,132 @@
+"""Python handle over the C++ training-step executor (libtcb.so tcb_trainer_*).
+
+One Trainer per GPU process. For world > 1 the NCCL unique id is created on
+rank 0 and broadcast with torch.distributed (plumbing only); the gradient
+aggregation / parameter refresh itself runs inside the C++ step over NCCL.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+
+import torch
+
+from . import device, models
+
+_vp = ctypes.c_void_p
+_bound = False
+
+
+def _lib():
+    global _bound
+    L = device.lib()
+    if not _bound:
+        L.tcb_trainer_create.argtypes = [ctypes.c_char_p, ctypes.POINTER(_vp)]
+        L.tcb_trainer_destroy.argtypes = [_vp]
+        L.tcb_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.tcb_trainer_join.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+        L.tcb_trainer_set_batch.argtypes = [_vp, _vp, _vp, _vp]
+        L.tcb_trainer_step.argtypes = [_vp, _vp]
+        L.tcb_trainer_loss.argtypes = [_vp, ctypes.POINTER(ctypes.c_float), _vp]
+        L.tcb_trainer_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_float)]
+        L.tcb_trainer_enable_timing.argtypes = [_vp, ctypes.c_int]
+        L.tcb_trainer_describe.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p)]
+        L.tcb_trainer_tensor.argtypes = [_vp, ctypes.c_char_p, ctypes.POINTER(_vp),
+                                         ctypes.POINTER(ctypes.c_size_t)]
+        L.tcb_trainer_launch_count.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
+        L.tcb_free.argtypes = [_vp]
+        _bound = True
+    return L
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    device.check(_lib().tcb_nccl_unique_id(buf))
+    return buf.raw
+
+
+class _DevBuf:
+    """Exposes a device pointer to torch via __cuda_array_interface__."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2, "strides": None}
+
+
+def small_config(precision="bf16"):
+    return models.tiny_resnet(precision=precision)
+
+
+class Trainer:
+    PHASES = ("fwd", "bwd", "reduce_scatter", "sgd", "all_gather")
+
+    def __init__(self, cfg: dict, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        self.cfg = cfg
+        self.handle = _vp()
+        device.check(_lib().tcb_trainer_create(json.dumps(cfg).encode(), ctypes.byref(self.handle)))
+        self.rank, self.world = rank, world
+        if world > 1 or nccl_id is not None:
+            device.check(_lib().tcb_trainer_join(self.handle, rank, world, nccl_id))
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib().tcb_trainer_destroy(self.handle)
+            self.handle = None
+
+    @staticmethod
+    def _stream():
+        return _vp(torch.cuda.current_stream().cuda_stream)
+
+    def set_batch(self, images=None, labels=None):
+        """Host (CPU, ideally pinned) fp32 NHWC images / int32 labels -> device."""
+        device.check(_lib().tcb_trainer_set_batch(
+            self.handle, None if images is None else _vp(images.data_ptr()),
+            None if labels is None else _vp(labels.data_ptr()), self._stream()))
+
+    def step(self):
+        device.check(_lib().tcb_trainer_step(self.handle, self._stream()))
+
+    def loss(self) -> float:
+        out = ctypes.c_float()
+        device.check(_lib().tcb_trainer_loss(self.handle, ctypes.byref(out), self._stream()))
+        return out.value
+
+    def enable_timing(self, on=True):
+        device.check(_lib().tcb_trainer_enable_timing(self.handle, int(on)))
+
+    def phase_times(self) -> dict:
+        buf = (ctypes.c_float * 5)()
+        device.check(_lib().tcb_trainer_phase_times(self.handle, buf))
+        return dict(zip(self.PHASES, list(buf)))
+
+    def launch_count(self) -> int:
+        n = ctypes.c_int()
+        device.check(_lib().tcb_trainer_launch_count(self.handle, ctypes.byref(n)))
+        return n.value
+
+    def describe(self) -> dict:
+        out = ctypes.c_char_p()
+        device.check(_lib().tcb_trainer_describe(self.handle, ctypes.byref(out)))
+        d = json.loads(out.value.decode())
+        _lib().tcb_free(ctypes.cast(out, _vp))
+        return d
+
+    def tensor(self, name: str, dtype=None) -> torch.Tensor:
+        ptr, nbytes = _vp(), ctypes.c_size_t()
+        device.check(_lib().tcb_trainer_tensor(self.handle, name.encode(), ctypes.byref(ptr),
+                                               ctypes.byref(nbytes)))
+        if dtype is None:
+            if name in ("param", "grad", "momentum", "loss", "input_f32"):
+                dtype = torch.float32
+            elif name == "labels":
+                dtype = torch.int32
+            else:
+                dtype = torch.bfloat16 if self.cfg.get("precision", "bf16") == "bf16" else torch.float32
+        esz = torch.tensor([], dtype=dtype).element_size()
+        typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.bfloat16: "<f2",
+                   torch.uint8: "|u1"}[dtype]
+        count = nbytes.value // esz
+        if dtype == torch.bfloat16:  # no bf16 typestr in the interface: view int16 bits
+            t = torch.as_tensor(_DevBuf(ptr.value, count, "<i2"), device="cuda")
+            return t.view(torch.bfloat16)
+        return torch.as_tensor(_DevBuf(ptr.value, count, typestr), device="cuda")

@@ -1,0 +1,169 @@
+"""CPU restatement of one data-parallel training step — TEST INFRASTRUCTURE.
+
+Walks the same model graph as the C++ executor (paper_1709_06622_b200/models.py
+config) with the C oracle ops (oracle/numerics.c, fp64 accumulation):
+forward (conv + bias + residual + ReLU, max/avg pools), softmax
+cross-entropy, backward (dgrad with residual-gradient fan-in and ReLU masks,
+wgrad + bias grads in the flat PS layout), then the momentum-SGD update of
+paper step 6. In bf16 mode every stored
+tensor is rounded to bf16 exactly where the device stores bf16, so the two
+paths see the same operands.
+
+Parity of this restatement is unpinned by the reference (no conv/SGD values
+exist in /root/reference — SURVEY.md §8c); it follows the paper's definitions.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class OracleStep:
+    def __init__(self, oracle, cfg: dict, layout: dict, rank: int = 0, world: int = 1):
+        self.o = oracle
+        self.cfg = cfg
+        self.layout = layout
+        self.rank, self.world = rank, world
+        self.bf16 = cfg.get("precision", "bf16") == "bf16"
+        self.seed = cfg.get("seed", 20260810)
+        self.layers = layout["layers"]
+        self.params = {}  # conv index -> (w logical [K,R,S,Cl] float32, bias float32 or None)
+        for L in self.layers:
+            if L["op"] != "conv":
+                continue
+            k, r, s = L["geom"][4], L["geom"][5], L["geom"][6]
+            cl = self.layers[L["in"]]["c_logical"]
+            n = k * r * s * cl
+            a = np.float32(L["init_scale"])
+            w = oracle.uniform(n, self.seed, 1000 + L["conv_index"], -a, a).reshape(k, r, s, cl)
+            b = np.zeros(k, np.float32) if L["bias"] else None
+            self.params[L["index"]] = [w, b]
+
+    # storage rounding of activations / gradients
+    def _st(self, a):
+        a = np.asarray(a, np.float32)
+        return self.o.round_bf16(a) if self.bf16 else a
+
+    def _geom(self, L, logical_in_c):
+        g = L["geom"]
+        return dict(n=g[0], h=g[1], w=g[2], c=logical_in_c, k=g[4], r=g[5], s=g[6],
+                    pad_h=g[7], pad_w=g[8], stride_h=g[9], stride_w=g[10])
+
+    def inputs(self):
+        inp = self.layers[0]
+        n, h, w, _ = inp["shape"]
+        cl = inp["c_logical"]
+        x = self.o.uniform(n * h * w * cl, self.seed + self.rank, 1, -1.0, 1.0).reshape(n, h, w, cl)
+        lab = self.o.labels(n, self.cfg["classes"], self.seed + self.rank)
+        return x, lab
+
+    def run(self, x=None, labels=None):
+        o = self.o
+        if x is None:
+            x, labels = self.inputs()
+        act = {0: self._st(x)}
+        wq = {i: (self._st(w) if self.bf16 else w) for i, (w, _) in self.params.items()}
+        # ---------------------------------------------------------- forward
+        loss = None
+        dlogits = None
+        for L in self.layers[1:]:
+            i = L["index"]
+            if L["op"] == "conv":
+                xin = act[L["in"]]
+                g = self._geom(L, xin.shape[-1])
+                res = act[L["residual"]] if L["residual"] >= 0 else None
+                y = o.conv_fwd(g, xin, wq[i], bias=self.params[i][1], residual=res, relu=L["relu"])
+                act[i] = self._st(y).reshape(g["n"], L["shape"][1], L["shape"][2], g["k"])
+            elif L["op"] == "maxpool":
+                xin = act[L["in"]]
+                n, h, w, c = xin.shape
+                f, s, p = L["pool"]
+                y, arg = o.maxpool_fwd(xin, n, h, w, c, f, s, p)
+                act[i] = self._st(y).reshape(L["shape"][0], L["shape"][1], L["shape"][2], c)
+                L["_arg"] = arg
+            elif L["op"] == "avgpool":
+                xin = act[L["in"]]
+                n, h, w, c = xin.shape
+                act[i] = self._st(o.avgpool_fwd(xin, n, h * w, c)).reshape(n, 1, 1, c)
+            elif L["op"] == "loss":
+                z = act[L["in"]]
+                n = z.shape[0]
+                loss, dl = o.softmax_xent(z.reshape(n, -1), labels, n, z.shape[-1])
+                dlogits = self._st(dl).reshape(z.shape)
+                logits_idx = L["in"]
+        # --------------------------------------------------------- backward
+        contrib = {}  # tensor index -> list of float arrays
+        G = {logits_idx: dlogits}
+        grads = {}
+        for L in reversed(self.layers[1:]):
+            i = L["index"]
+            if L["op"] == "loss":
+                continue
+            if i not in G:  # finalise this tensor's gradient
+                parts = contrib.get(i, [])
+                tot = np.sum(parts, axis=0) if parts else np.zeros_like(act[i], np.float64)
+                if L["op"] == "conv" and L["relu"]:
+                    tot = np.where(act[i] > 0, tot, 0.0)
+                G[i] = self._st(tot).reshape(act[i].shape)
+            gi = G[i]
+            if L["op"] == "conv":
+                xin = act[L["in"]]
+                g = self._geom(L, xin.shape[-1])
+                dw, db = o.conv_wgrad(g, gi, xin, want_db=True)
+                grads[i] = (dw, db if L["bias"] else None)
+                if L["residual"] >= 0 and self.layers[L["residual"]]["op"] != "input":
+                    contrib.setdefault(L["residual"], []).append(gi.astype(np.float64))
+                if self.layers[L["in"]]["op"] != "input":
+                    dx = o.conv_dgrad(g, gi, wq[i]).reshape(xin.shape)
+                    contrib.setdefault(L["in"], []).append(dx)
+            elif L["op"] == "maxpool":
+                xin = act[L["in"]]
+                n, h, w, c = xin.shape
+                f, s, p = L["pool"]
+                dx = o.maxpool_bwd(gi, L["_arg"], n, h, w, c, f, s, p).reshape(xin.shape)
+                if self.layers[L["in"]]["op"] != "input":
+                    contrib.setdefault(L["in"], []).append(dx)
+            elif L["op"] == "avgpool":
+                xin = act[L["in"]]
+                n, h, w, c = xin.shape
+                dx = o.avgpool_bwd(gi.reshape(n, c), n, h * w, c).reshape(xin.shape)
+                contrib.setdefault(L["in"], []).append(dx)
+        self.loss, self.act, self.G, self.grads = loss, act, G, grads
+        return loss
+
+    def flat_grad(self):
+        """Gradients in the executor's flat PS layout (padded channels = 0)."""
+        flat = np.zeros(self.layout["param_padded"], np.float64)
+        for L in self.layers:
+            if L["op"] != "conv":
+                continue
+            dw, db = self.grads[L["index"]]
+            k, r, s, cp = L["geom"][4], L["geom"][5], L["geom"][6], L["geom"][3]
+            cl = self.layers[L["in"]]["c_logical"]
+            w4 = np.zeros((k, r, s, cp), np.float64)
+            w4[..., :cl] = dw.reshape(k, r, s, cl)
+            flat[L["woff"]:L["woff"] + w4.size] = w4.ravel()
+            if db is not None:
+                flat[L["boff"]:L["boff"] + k] = db
+        return flat
+
+    def flat_params(self):
+        flat = np.zeros(self.layout["param_padded"], np.float32)
+        for L in self.layers:
+            if L["op"] != "conv":
+                continue
+            w, b = self.params[L["index"]]
+            k, r, s, cp = L["geom"][4], L["geom"][5], L["geom"][6], L["geom"][3]
+            cl = w.shape[-1]
+            w4 = np.zeros((k, r, s, cp), np.float32)
+            w4[..., :cl] = w
+            flat[L["woff"]:L["woff"] + w4.size] = w4.ravel()
+            if b is not None:
+                flat[L["boff"]:L["boff"] + k] = b
+        return flat
+
+    def sgd(self, flat_grad_f32):
+        c = self.cfg
+        w = self.flat_params()
+        v = np.zeros_like(w)
+        return self.o.sgd(w, flat_grad_f32, v, c.get("lr", 0.01), c.get("momentum", 0.9),
+                          c.get("weight_decay", 0.0), 1.0 / self.world)

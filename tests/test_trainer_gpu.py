@@ -1,0 +1,133 @@
+"""Step-level parity: the C++ executor's full training step (fwd -> loss ->
+bwd -> fused SGD) vs the CPU oracle step on identical seeded inputs/weights.
+Tolerances: normwise 1e-5 (fp32-FFMA mode), 2e-2 (bf16 tensor-core mode).
+SURVEY §8 rows a14-a17 end to end, d1 (synthetic inputs)."""
+import numpy as np
+import pytest
+
+from oracle_binding import rel_err
+from oracle_step import OracleStep
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {"ffma": 1e-5, "bf16": 2e-2}
+
+
+def _models():
+    from paper_1709_06622_b200 import models
+    return models
+
+
+def _run_step(cfg):
+    from paper_1709_06622_b200.trainer import Trainer
+    t = Trainer(cfg)
+    t.step()
+    torch.cuda.synchronize()
+    return t
+
+
+def _check(oracle, cfg, per_layer=True):
+    prec = cfg["precision"]
+    tol = TOL[prec]
+    t = _run_step(cfg)
+    lay = t.describe()
+    ref = OracleStep(oracle, cfg, lay)
+    ref.run()
+    loss = t.loss()
+    assert abs(loss - ref.loss) <= max(tol, 1e-6) * abs(ref.loss), (loss, ref.loss)
+    g_dev = t.tensor("grad").cpu().numpy().astype(np.float64)
+    g_ref = ref.flat_grad()
+    worst = 0.0
+    for L in lay["layers"]:
+        if L["op"] != "conv":
+            continue
+        sl = slice(L["woff"], L["woff"] + L["wcount"])
+        e = rel_err(g_dev[sl], g_ref[sl])
+        worst = max(worst, e)
+        if per_layer:
+            assert e <= tol, (L["name"], e)
+        if L["boff"] is not None:
+            sb = slice(L["boff"], L["boff"] + L["geom"][4])
+            assert rel_err(g_dev[sb], g_ref[sb]) <= tol, (L["name"], "bias")
+    # update: device SGD applied to device grads must equal the oracle SGD bit-exactly
+    w_ref, _ = ref.sgd(g_dev.astype(np.float32))
+    w_dev = t.tensor("param").cpu().numpy()
+    assert np.array_equal(w_dev, w_ref)
+    # and the delta against the oracle's own gradients within tolerance
+    w_ref2, _ = ref.sgd(g_ref.astype(np.float32))
+    w0 = ref.flat_params()
+    assert rel_err(w_dev - w0, w_ref2 - w0) <= tol
+    if prec == "bf16":
+        wc = t.tensor("wcompute").float().cpu().numpy()
+        assert np.array_equal(wc, oracle.round_bf16(w_dev))
+    return t, worst
+
+
+@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+def test_tiny_resnet_step(oracle, prec):
+    _check(oracle, _models().tiny_resnet(batch=4, precision=prec))
+
+
+def test_lenet_step_c1(oracle):
+    """C1: LeNet 28x28x1 batch 64, 1 worker + 1 PS shard, fp32-FFMA mode."""
+    _check(oracle, _models().lenet(batch=64))
+
+
+@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+def test_alexnet_step_small_batch(oracle, prec):
+    """C2 geometry (227x227x3, ungrouped AlexNet + 4096/4096/1000) at N=2."""
+    _check(oracle, _models().alexnet(batch=2, precision=prec))
+
+
+def test_from_net_fixture_chain(oracle):
+    """The reference's own alexnet.net fixture, executed as a chain."""
+    import planner_cases
+    cfg = _models().from_net(planner_cases.fixture("alexnet.net"), batch=2, precision="bf16")
+    _check(oracle, cfg)
+
+
+def test_step_is_deterministic():
+    cfg = _models().tiny_resnet(batch=4, precision="bf16")
+    a, b = _run_step(cfg), _run_step(cfg)
+    assert torch.equal(a.tensor("grad"), b.tensor("grad"))
+    assert torch.equal(a.tensor("param"), b.tensor("param"))
+    a.step()
+    b.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.tensor("param"), b.tensor("param"))
+
+
+def test_host_batch_path_matches_resident_batch(oracle):
+    from paper_1709_06622_b200.trainer import Trainer
+    cfg = _models().tiny_resnet(batch=4, precision="bf16")
+    a = _run_step(cfg)
+    b = Trainer(cfg)
+    ref = OracleStep(oracle, cfg, b.describe())
+    x, lab = ref.inputs()
+    b.set_batch(torch.from_numpy(x.copy()).pin_memory(), torch.from_numpy(lab.copy()).pin_memory())
+    b.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.tensor("grad"), b.tensor("grad"))
+
+
+def test_loss_decreases_over_steps():
+    from paper_1709_06622_b200.trainer import Trainer
+    cfg = _models().tiny_resnet(batch=8, precision="bf16", lr=0.05)
+    t = Trainer(cfg)
+    losses = []
+    for _ in range(15):
+        t.step()
+        losses.append(t.loss())
+    assert losses[-1] < losses[0], losses
+
+
+def test_phase_times_and_launch_count():
+    from paper_1709_06622_b200.trainer import Trainer
+    t = Trainer(_models().tiny_resnet(batch=4, precision="bf16"))
+    t.enable_timing(True)
+    t.step()
+    ph = t.phase_times()
+    assert set(ph) == set(Trainer.PHASES) and all(v >= 0 for v in ph.values())
+    assert ph["fwd"] > 0 and ph["bwd"] > 0
+    assert t.launch_count() > 20
