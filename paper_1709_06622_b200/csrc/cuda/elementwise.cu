@@ -267,10 +267,10 @@ __global__ void avgpool_bwd_kernel(const T* __restrict__ dy, T* __restrict__ dx,
 template <typename T>
 __global__ void softmax_xent_kernel(const T* __restrict__ logits, const int32_t* __restrict__ lab,
                                     T* __restrict__ dl, float* __restrict__ row_loss, int N,
-                                    int K) {
+                                    int K, int ld) {
     __shared__ float red[32];
     const int n = blockIdx.x;
-    const T* z = logits + size_t(n) * K;
+    const T* z = logits + size_t(n) * ld;
     float m = -INFINITY;
     for (int k = threadIdx.x; k < K; k += blockDim.x) m = fmaxf(m, to_f32<T>(z[k]));
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -300,8 +300,9 @@ __global__ void softmax_xent_kernel(const T* __restrict__ logits, const int32_t*
     const float inv_n = 1.0f / float(N);
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
         const float pk = expf(to_f32<T>(z[k]) - m) / s;
-        dl[size_t(n) * K + k] = from_f32<T>((pk - (k == y ? 1.f : 0.f)) * inv_n);
+        dl[size_t(n) * ld + k] = from_f32<T>((pk - (k == y ? 1.f : 0.f)) * inv_n);
     }
+    for (int k = K + threadIdx.x; k < ld; k += blockDim.x) dl[size_t(n) * ld + k] = from_f32<T>(0.f);
     if (threadIdx.x == 0) row_loss[n] = logf(s) + m - to_f32<T>(z[y]);
 }
 
@@ -462,10 +463,10 @@ cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw
 }
 
 cudaError_t softmax_xent(DType dt, const void* logits, const int32_t* labels, void* dlogits,
-                         float* loss, int n, int classes, cudaStream_t st) {
+                         float* loss, int n, int classes, int ld, cudaStream_t st) {
     TCB_DT_SWITCH(dt, T, (softmax_xent_kernel<T><<<n, kBlock, 0, st>>>(
                               static_cast<const T*>(logits), labels, static_cast<T*>(dlogits),
-                              loss + 1, n, classes)));
+                              loss + 1, n, classes, ld)));
     mean_kernel<<<1, 32, 0, st>>>(loss, loss + 1, n);
     return cudaGetLastError();
 }

@@ -99,7 +99,8 @@ cudaError_t avgpool_global_fwd(DType dt, const void* x, void* y, int n, int hw, 
                                cudaStream_t st);
 cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw, int c,
                                cudaStream_t st);
+// logits rows are `ld` apart (ld >= classes; padded columns get zero gradient)
 cudaError_t softmax_xent(DType dt, const void* logits, const int32_t* labels, void* dlogits,
-                         float* loss, int n, int classes, cudaStream_t st);
+                         float* loss, int n, int classes, int ld, cudaStream_t st);
 
 }  // namespace tcb

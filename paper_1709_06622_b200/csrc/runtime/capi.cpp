@@ -262,7 +262,7 @@ TCB_API int tcb_avgpool_global_bwd(int dtype, const void* dy, void* dx, int n, i
 
 TCB_API int tcb_softmax_xent(int dtype, const void* logits, const int32_t* labels, void* dlogits,
                              float* loss, int n, int classes, void* stream) {
-    return check_cuda(softmax_xent(dt_of(dtype), logits, labels, dlogits, loss, n, classes,
+    return check_cuda(softmax_xent(dt_of(dtype), logits, labels, dlogits, loss, n, classes, classes,
                                    static_cast<cudaStream_t>(stream)),
                       "softmax_xent");
 }

@@ -69,6 +69,7 @@ struct Node {
     std::vector<int> compute_from;      // consumers with a computed contribution
     std::vector<int> alias_from;        // consumers whose G[out] adds via the residual path
     std::map<int, size_t> tmp;          // consumer -> temp buffer offset (non-final computed)
+    int grad_alias = -1;                // G[this] is G[grad_alias] (no copy)
 };
 
 struct Phase {
@@ -175,7 +176,11 @@ int build_graph(tcb_trainer* t) {
             nd.in = src("in");
             nd.residual = src("residual");
             const Node& x = t->nodes.at(nd.in);
-            nd.g = ConvGeom{x.n, x.h, x.w, x.c, L.at("k").get<int>(), L.at("r").get<int>(),
+            // bf16 tensor-core path: output channels padded to a multiple of 8 (16-byte
+            // NHWC rows); padded filters are zero, so padded channels stay exactly 0.
+            const int k_logical = L.at("k").get<int>();
+            const int k_alloc = t->bf16 ? static_cast<int>(round_up(k_logical, 8)) : k_logical;
+            nd.g = ConvGeom{x.n, x.h, x.w, x.c, k_alloc, L.at("r").get<int>(),
                             L.value("s", L.at("r").get<int>()), L.value("pad_h", L.value("pad", 0)),
                             L.value("pad_w", L.value("pad", 0)), L.value("stride_h", L.value("stride", 1)),
                             L.value("stride_w", L.value("stride", 1))};
@@ -185,7 +190,8 @@ int build_graph(tcb_trainer* t) {
             nd.n = x.n;
             nd.h = nd.g.ho();
             nd.w = nd.g.wo();
-            nd.c = nd.c_logical = nd.g.k;
+            nd.c = k_alloc;
+            nd.c_logical = k_logical;
             nd.conv_index = ++conv_idx;
             nd.need_dgrad = t->nodes.at(nd.in).op != Op::Input;
             const int fan_in = x.c_logical * nd.g.r * nd.g.s;
@@ -224,7 +230,7 @@ int build_graph(tcb_trainer* t) {
             nd.op = Op::Loss;
             nd.in = src("in");
             const Node& x = t->nodes.at(nd.in);
-            if (x.h != 1 || x.w != 1 || x.c != t->classes)
+            if (x.h != 1 || x.w != 1 || x.c_logical != t->classes)
                 throw std::runtime_error("loss input must be N x 1 x 1 x classes");
             t->logits = nd.in;
         } else {
@@ -250,6 +256,11 @@ int build_graph(tcb_trainer* t) {
     for (Node& nd : t->nodes) {
         if (!nd.compute_from.empty())
             nd.final_writer = *std::min_element(nd.compute_from.begin(), nd.compute_from.end());
+        // A tensor whose gradient arrives only through one residual path and whose
+        // producer has no ReLU (a projection shortcut) shares that gradient buffer.
+        nd.grad_alias = nd.compute_from.empty() && nd.alias_from.size() == 1 && !nd.relu
+                            ? nd.alias_from[0]
+                            : -1;
     }
     return TCB_OK;
 }
@@ -271,11 +282,11 @@ void plan_params(tcb_trainer* t) {
         nd.wcount = size_t(nd.g.k) * nd.g.r * nd.g.s * nd.g.c;
         nd.woff = off;
         off = round_up(off + nd.wcount, kParamAlign);
-        logical += size_t(nd.g.k) * nd.g.r * nd.g.s * t->nodes[nd.in].c_logical;
+        logical += size_t(nd.c_logical) * nd.g.r * nd.g.s * t->nodes[nd.in].c_logical;
         if (nd.bias) {
             nd.boff = off;
             off = round_up(off + nd.g.k, kParamAlign);
-            logical += nd.g.k;
+            logical += nd.c_logical;
         }
     }
     t->param_count = logical;
@@ -297,7 +308,7 @@ int allocate(tcb_trainer* t) {
         const size_t elems = size_t(nd.n) * nd.h * nd.w * nd.c;
         if (nd.op == Op::Loss) continue;
         nd.act = b.take(elems * es);
-        if (nd.op != Op::Input) nd.grad = b.take(elems * es);
+        if (nd.op != Op::Input && nd.grad_alias < 0) nd.grad = b.take(elems * es);
         if (nd.op == Op::MaxPool) nd.argmax = b.take(elems);
         if (nd.op == Op::Conv) {
             ws = std::max(ws, t->bf16 ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
@@ -309,6 +320,8 @@ int allocate(tcb_trainer* t) {
     for (Node& nd : t->nodes)
         for (int c : nd.compute_from)
             if (c != nd.final_writer) nd.tmp[c] = b.take(size_t(nd.n) * nd.h * nd.w * nd.c * es);
+    for (int i = static_cast<int>(t->nodes.size()) - 1; i >= 0; --i)
+        if (t->nodes[i].grad_alias >= 0) t->nodes[i].grad = t->nodes[t->nodes[i].grad_alias].grad;
     t->ws_bytes = ws;
     t->colsum_bytes = colsum;
     t->off_ws = b.take(ws);
@@ -343,7 +356,8 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
     for (const Node& nd : t->nodes) {
         if (nd.op != Op::Conv) continue;
         const int cl = t->nodes[nd.in].c_logical, cp = nd.g.c;
-        const size_t outer = size_t(nd.g.k) * nd.g.r * nd.g.s;
+        // logical filters k < c_logical; padded filters (k >= c_logical) stay zero
+        const size_t outer = size_t(nd.c_logical) * nd.g.r * nd.g.s;
         if (cl == cp) {
             TRY_CUDA(fill_uniform(DType::F32, param + nd.woff, outer * cl, t->seed,
                                   1000 + nd.conv_index, -nd.init_scale, nd.init_scale, st));
@@ -412,7 +426,7 @@ int forward(tcb_trainer* t, cudaStream_t st) {
             case Op::Loss: {
                 const Node& z = t->nodes[t->logits];
                 TRY_CUDA(softmax_xent(t->dt, t->at(z.act), t->at<int32_t>(t->off_labels), t->at(z.grad),
-                                      t->at<float>(t->off_loss), t->batch, t->classes, st));
+                                      t->at<float>(t->off_loss), t->batch, t->classes, z.c, st));
                 t->launches += 2;
                 break;
             }
@@ -485,6 +499,21 @@ int backward(tcb_trainer* t, cudaStream_t st) {
     float* grad = t->at<float>(t->off_grad);
     for (int i = static_cast<int>(t->nodes.size()) - 1; i >= 0; --i) {
         const Node& nd = t->nodes[i];
+        if (nd.op != Op::Input && nd.op != Op::Loss && nd.compute_from.empty() &&
+            !nd.alias_from.empty() && nd.grad_alias < 0) {
+            // gradient only via residual paths (several, or through a ReLU): combine
+            const size_t elems = size_t(nd.n) * nd.h * nd.w * nd.c;
+            TRY_CUDA(cudaMemcpyAsync(t->at(nd.grad), t->at(t->nodes[nd.alias_from[0]].grad),
+                                     elems * dtype_size(t->dt), cudaMemcpyDeviceToDevice, st));
+            for (size_t a = 1; a < nd.alias_from.size(); ++a) {
+                TRY_CUDA(add_inplace(t->dt, t->at(nd.grad), t->at(t->nodes[nd.alias_from[a]].grad), elems, st));
+                t->launches++;
+            }
+            if (nd.op == Op::Conv && nd.relu) {
+                TRY_CUDA(relu_mask_inplace(t->dt, t->at(nd.grad), t->at(nd.act), elems, st));
+                t->launches++;
+            }
+        }
         if (nd.op == Op::Conv) {
             const Node& x = t->nodes[nd.in];
             // weight (and bias) gradient straight into the flat PS buffer

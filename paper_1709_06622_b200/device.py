@@ -119,9 +119,12 @@ class ConvPlan:
         self.workspace = torch.empty(max(ws.value, 1), dtype=torch.uint8, device="cuda")
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            lib().tcb_conv_plan_destroy(self.handle)
-            self.handle = None
+        try:
+            if getattr(self, "handle", None):
+                lib().tcb_conv_plan_destroy(self.handle)
+                self.handle = None
+        except Exception:  # interpreter teardown
+            pass
 
     @property
     def dtype(self):

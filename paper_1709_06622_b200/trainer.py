@@ -69,9 +69,12 @@ class Trainer:
             device.check(_lib().tcb_trainer_join(self.handle, rank, world, nccl_id))
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            _lib().tcb_trainer_destroy(self.handle)
-            self.handle = None
+        try:
+            if getattr(self, "handle", None):
+                _lib().tcb_trainer_destroy(self.handle)
+                self.handle = None
+        except Exception:  # interpreter teardown
+            pass
 
     @staticmethod
     def _stream():

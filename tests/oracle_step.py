@@ -30,7 +30,7 @@ class OracleStep:
         for L in self.layers:
             if L["op"] != "conv":
                 continue
-            k, r, s = L["geom"][4], L["geom"][5], L["geom"][6]
+            k, r, s = L["c_logical"], L["geom"][5], L["geom"][6]
             cl = self.layers[L["in"]]["c_logical"]
             n = k * r * s * cl
             a = np.float32(L["init_scale"])
@@ -45,7 +45,7 @@ class OracleStep:
 
     def _geom(self, L, logical_in_c):
         g = L["geom"]
-        return dict(n=g[0], h=g[1], w=g[2], c=logical_in_c, k=g[4], r=g[5], s=g[6],
+        return dict(n=g[0], h=g[1], w=g[2], c=logical_in_c, k=L["c_logical"], r=g[5], s=g[6],
                     pad_h=g[7], pad_w=g[8], stride_h=g[9], stride_w=g[10])
 
     def inputs(self):
@@ -137,10 +137,10 @@ class OracleStep:
             if L["op"] != "conv":
                 continue
             dw, db = self.grads[L["index"]]
-            k, r, s, cp = L["geom"][4], L["geom"][5], L["geom"][6], L["geom"][3]
-            cl = self.layers[L["in"]]["c_logical"]
-            w4 = np.zeros((k, r, s, cp), np.float64)
-            w4[..., :cl] = dw.reshape(k, r, s, cl)
+            ka, r, s, cp = L["geom"][4], L["geom"][5], L["geom"][6], L["geom"][3]
+            k, cl = L["c_logical"], self.layers[L["in"]]["c_logical"]
+            w4 = np.zeros((ka, r, s, cp), np.float64)
+            w4[:k, ..., :cl] = dw.reshape(k, r, s, cl)
             flat[L["woff"]:L["woff"] + w4.size] = w4.ravel()
             if db is not None:
                 flat[L["boff"]:L["boff"] + k] = db
@@ -152,10 +152,10 @@ class OracleStep:
             if L["op"] != "conv":
                 continue
             w, b = self.params[L["index"]]
-            k, r, s, cp = L["geom"][4], L["geom"][5], L["geom"][6], L["geom"][3]
-            cl = w.shape[-1]
-            w4 = np.zeros((k, r, s, cp), np.float32)
-            w4[..., :cl] = w
+            ka, r, s, cp = L["geom"][4], L["geom"][5], L["geom"][6], L["geom"][3]
+            k, cl = w.shape[0], w.shape[-1]
+            w4 = np.zeros((ka, r, s, cp), np.float32)
+            w4[:k, ..., :cl] = w
             flat[L["woff"]:L["woff"] + w4.size] = w4.ravel()
             if b is not None:
                 flat[L["boff"]:L["boff"] + k] = b
