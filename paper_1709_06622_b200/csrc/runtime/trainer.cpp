@@ -791,6 +791,13 @@ TCB_API int tcb_trainer_tensor(tcb_trainer* t, const char* name, void** ptr, siz
         const Node& in = t->nodes[0];
         p = t->at(t->off_input_f32);
         b = size_t(in.n) * in.h * in.w * in.c_logical * 4;
+    } else if (n.rfind("argmax:", 0) == 0) {
+        const int i = std::stoi(n.substr(7));
+        if (i < 0 || i >= static_cast<int>(t->nodes.size()) || t->nodes[i].op != Op::MaxPool)
+            return fail(TCB_ERR_INVALID, "no such argmax tensor");
+        const Node& nd = t->nodes[i];
+        p = t->at(nd.argmax);
+        b = size_t(nd.n) * nd.h * nd.w * nd.c;
     } else if (n.rfind("act:", 0) == 0 || n.rfind("dact:", 0) == 0) {
         const bool grad = n[0] == 'd';
         const int i = std::stoi(n.substr(grad ? 5 : 4));

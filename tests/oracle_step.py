@@ -17,6 +17,37 @@ from __future__ import annotations
 import numpy as np
 
 
+def _rel(got, ref):
+    got = np.asarray(got, np.float64).ravel()
+    ref = np.asarray(ref, np.float64).ravel()
+    den = np.linalg.norm(ref)
+    return float(np.linalg.norm(got - ref) / (den if den > 0 else 1.0))
+
+
+class DeviceTeacher:
+    """Reads the executor's tensors (logical channels) for teacher-forced parity."""
+
+    def __init__(self, trainer, layout):
+        self.t, self.layers = trainer, layout["layers"]
+
+    def _get(self, name, i):
+        L = self.layers[i]
+        a = self.t.tensor(f"{name}:{i}").float().cpu().numpy().reshape(L["shape"])
+        return a[..., :L["c_logical"]].astype(np.float32)
+
+    def act(self, i):
+        return self._get("act", i)
+
+    def grad(self, i):
+        return self._get("dact", i)
+
+    def argmax(self, i):
+        import torch
+        L = self.layers[i]
+        a = self.t.tensor(f"argmax:{i}", dtype=torch.uint8).cpu().numpy().reshape(L["shape"])
+        return np.ascontiguousarray(a[..., :L["c_logical"]]).ravel()
+
+
 class OracleStep:
     def __init__(self, oracle, cfg: dict, layout: dict, rank: int = 0, world: int = 1):
         self.o = oracle
@@ -56,12 +87,24 @@ class OracleStep:
         lab = self.o.labels(n, self.cfg["classes"], self.seed + self.rank)
         return x, lab
 
-    def run(self, x=None, labels=None):
+    def run(self, x=None, labels=None, teacher=None):
+        """One step. With `teacher` (an object exposing the DEVICE's tensors:
+        act(i), grad(i), argmax(i), in logical channels), every op is
+        recomputed from the device's own inputs — layer-local parity — and the
+        relative error of each device output is recorded in self.local_err."""
         o = self.o
         if x is None:
             x, labels = self.inputs()
         act = {0: self._st(x)}
         wq = {i: (self._st(w) if self.bf16 else w) for i, (w, _) in self.params.items()}
+        self.local_err = {}
+
+        def adopt(kind, i, ref, dev_value):
+            if teacher is None:
+                return ref
+            self.local_err[(kind, self.layers[i]["name"])] = _rel(dev_value, ref)
+            return dev_value.reshape(ref.shape)
+
         # ---------------------------------------------------------- forward
         loss = None
         dlogits = None
@@ -72,24 +115,29 @@ class OracleStep:
                 g = self._geom(L, xin.shape[-1])
                 res = act[L["residual"]] if L["residual"] >= 0 else None
                 y = o.conv_fwd(g, xin, wq[i], bias=self.params[i][1], residual=res, relu=L["relu"])
-                act[i] = self._st(y).reshape(g["n"], L["shape"][1], L["shape"][2], g["k"])
+                y = self._st(y).reshape(g["n"], L["shape"][1], L["shape"][2], g["k"])
+                act[i] = adopt("fwd", i, y, teacher.act(i) if teacher else None)
             elif L["op"] == "maxpool":
                 xin = act[L["in"]]
                 n, h, w, c = xin.shape
                 f, s, p = L["pool"]
                 y, arg = o.maxpool_fwd(xin, n, h, w, c, f, s, p)
-                act[i] = self._st(y).reshape(L["shape"][0], L["shape"][1], L["shape"][2], c)
-                L["_arg"] = arg
+                y = self._st(y).reshape(L["shape"][0], L["shape"][1], L["shape"][2], c)
+                act[i] = adopt("fwd", i, y, teacher.act(i) if teacher else None)
+                L["_arg"] = teacher.argmax(i) if teacher else arg
             elif L["op"] == "avgpool":
                 xin = act[L["in"]]
                 n, h, w, c = xin.shape
-                act[i] = self._st(o.avgpool_fwd(xin, n, h * w, c)).reshape(n, 1, 1, c)
+                y = self._st(o.avgpool_fwd(xin, n, h * w, c)).reshape(n, 1, 1, c)
+                act[i] = adopt("fwd", i, y, teacher.act(i) if teacher else None)
             elif L["op"] == "loss":
                 z = act[L["in"]]
                 n = z.shape[0]
                 loss, dl = o.softmax_xent(z.reshape(n, -1), labels, n, z.shape[-1])
-                dlogits = self._st(dl).reshape(z.shape)
                 logits_idx = L["in"]
+                dlogits = self._st(dl).reshape(z.shape)
+                dlogits = adopt("grad", logits_idx, dlogits,
+                                teacher.grad(logits_idx) if teacher else None)
         # --------------------------------------------------------- backward
         contrib = {}  # tensor index -> list of float arrays
         G = {logits_idx: dlogits}
@@ -103,7 +151,8 @@ class OracleStep:
                 tot = np.sum(parts, axis=0) if parts else np.zeros_like(act[i], np.float64)
                 if L["op"] == "conv" and L["relu"]:
                     tot = np.where(act[i] > 0, tot, 0.0)
-                G[i] = self._st(tot).reshape(act[i].shape)
+                ref = self._st(tot).reshape(act[i].shape)
+                G[i] = adopt("grad", i, ref, teacher.grad(i) if teacher else None)
             gi = G[i]
             if L["op"] == "conv":
                 xin = act[L["in"]]
