@@ -71,6 +71,40 @@ inline ConvShape make_shape(const ConvGeom& g, ConvMode mode) {
     return s;
 }
 
+// Strided dgrad, sub-pixel decomposition: input pixels (h, w) with
+// h % sh == ph, w % sw == pw receive gradient only from filter taps
+// r ≡ (ph + pad_h) (mod sh), s ≡ (pw + pad_w) (mod sw). Each phase is a dense
+// implicit GEMM over its own pixel grid (Hq x Wq) and tap subset (tr x ts),
+// with its weights packed as [C][tr][ts][K] at element offset woff.
+struct DgradPhase {
+    int ph, pw, r0, s0, tr, ts, bh, bw, Hq, Wq;
+    size_t woff;
+};
+
+__host__ __device__ inline DgradPhase dgrad_phase(const ConvGeom& g, int ph, int pw) {
+    DgradPhase d{};
+    d.ph = ph;
+    d.pw = pw;
+    d.r0 = (ph + g.pad_h) % g.stride_h;
+    d.s0 = (pw + g.pad_w) % g.stride_w;
+    d.tr = d.r0 < g.r ? (g.r - 1 - d.r0) / g.stride_h + 1 : 0;
+    d.ts = d.s0 < g.s ? (g.s - 1 - d.s0) / g.stride_w + 1 : 0;
+    d.bh = (ph + g.pad_h - d.r0) / g.stride_h;
+    d.bw = (pw + g.pad_w - d.s0) / g.stride_w;
+    d.Hq = ph < g.h ? (g.h - ph + g.stride_h - 1) / g.stride_h : 0;
+    d.Wq = pw < g.w ? (g.w - pw + g.stride_w - 1) / g.stride_w : 0;
+    size_t off = 0;
+    for (int q = 0; q < ph * g.stride_w + pw; ++q) {
+        const int qh = q / g.stride_w, qw = q % g.stride_w;
+        const int r0 = (qh + g.pad_h) % g.stride_h, s0 = (qw + g.pad_w) % g.stride_w;
+        const int tr = r0 < g.r ? (g.r - 1 - r0) / g.stride_h + 1 : 0;
+        const int ts = s0 < g.s ? (g.s - 1 - s0) / g.stride_w + 1 : 0;
+        off += size_t(g.c) * g.k * tr * ts;
+    }
+    d.woff = off;
+    return d;
+}
+
 template <typename T>
 __device__ __forceinline__ float to_f32(T v);
 template <>

@@ -1,41 +1,44 @@
-// Tensor-core implicit-GEMM convolution for sm_100a (tcgen05 + TMEM).
+// Tensor-core implicit-GEMM convolution for sm_100a (tcgen05 + TMEM + TMA).
 //
 // One warp-specialised, persistent kernel serves all three passes of a conv
-// layer (the GEMM views are in common.cuh::ConvShape):
+// layer (GEMM views in common.cuh::ConvShape):
 //
-//   warps 0-3  producers: gather 16-byte chunks of the implicit im2col
-//              operands straight from NHWC activations with cp.async
-//              (zero-fill handles padding, strides and ragged tiles) into
-//              128B-swizzled shared memory, K-major for fwd/dgrad and
-//              MN-major for wgrad; signal a per-stage mbarrier
-//   warp  8    MMA issuer: one elected thread issues tcgen05.mma
-//              (kind::f16, bf16 x bf16 -> fp32, M=128, N=BN, K=16) into a
-//              double-buffered TMEM accumulator and tcgen05.commit's the
-//              smem stage / accumulator barriers
-//   warps 4-7  epilogue: tcgen05.ld TMEM -> registers, fused bias +
-//              residual + ReLU (fwd) or residual-grad + ReLU-mask (dgrad),
-//              bf16 store; wgrad writes fp32 split-K partials that a fixed-
-//              order reduction folds into the PS gradient buffer.
+//   warps 0-3  producers. The activation operand (implicit im2col of NHWC x
+//              for fwd, of dy for dgrad) is gathered in 16-byte chunks with
+//              cp.async (zero-fill = padding / strides / ragged tiles) into
+//              128B-swizzled K-major shared memory, several stages in flight
+//              per thread. The weight operand is a plain row-major matrix
+//              (w[K][R*S*C] for fwd, the per-phase packed w^T[C][taps*K] for
+//              dgrad) and is fetched by one elected thread with a TMA tiled
+//              load (SWIZZLE_128B, OOB -> 0) that completes on the same
+//              mbarrier via expect_tx. For wgrad both operands are gathered
+//              MN-major (pixels are the reduction axis).
+//   warp  8    MMA issuer: one elected thread issues tcgen05.mma kind::f16
+//              (bf16 x bf16 -> fp32, M=128, N=BN, K=16) into a double-buffered
+//              TMEM accumulator; tcgen05.commit releases smem stages and
+//              hands finished accumulators to the epilogue.
+//   warps 4-7  epilogue: tcgen05.ld -> registers, fused bias + residual + ReLU
+//              (fwd) or residual-grad + ReLU-mask (dgrad), bf16 stores; wgrad
+//              writes fp32 split-K partials reduced in fixed order afterwards.
 //
-// Tiles: BM=128 rows x BN (64/128/256) cols x BK=64 per stage; the grid is
-// min(tiles, #SMs) CTAs, each walking tiles with stride gridDim.x so the
-// epilogue of tile i overlaps the MMAs of tile i+1.
+// Strided dgrad uses the sub-pixel decomposition (common.cuh::DgradPhase):
+// stride^2 dense GEMMs over disjoint pixel phases, no zero-insertion waste.
 #include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "tma.cuh"
 
 namespace tcb {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 64;               // bf16 elements per stage along the reduction
+constexpr int BK = 64;  // bf16 elements per stage along the reduction
 constexpr int kProducerThreads = 128;
 constexpr int kEpilogueThreads = 128;
 constexpr int kMmaWarp = 8;
 constexpr int kThreads = kProducerThreads + kEpilogueThreads + 32;
-constexpr int kLag = 2;              // cp.async groups a producer keeps in flight
 
 template <int BN>
 struct Cfg {
@@ -43,21 +46,25 @@ struct Cfg {
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+    static constexpr int kLag = kStages - 1;  // cp.async groups in flight per producer
     static constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
     static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 + 256;
-    static_assert(kStages > kLag, "pipeline depth");
 };
 
 struct Params {
+    CUtensorMap tmap_b;      // weight operand (fwd / dgrad), 64-byte aligned
     ConvShape s;
     const __nv_bfloat16* a;  // fwd: x   dgrad: dy   wgrad: dy
-    const __nv_bfloat16* b;  // fwd: w   dgrad: wT   wgrad: x
+    const __nv_bfloat16* b;  // wgrad: x (gathered)
     void* out;               // bf16 (fwd/dgrad) or fp32 partials [split][M][Ncol] (wgrad)
     const float* bias;
     const __nv_bfloat16* residual;
     const __nv_bfloat16* mask;
     int relu;
     int m_tiles, n_tiles, splits, kb_total, kb_per_split, num_tiles;
+    // dgrad phase
+    DgradPhase ph;
+    FastDiv d_hwq, d_wq, d_ts;
 };
 
 struct TileCoord {
@@ -80,97 +87,101 @@ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
     return row * 128u + ((chunk ^ (row & 7u)) << 4);
 }
 
-// ------------------------------------------------------------ producers ----
-template <ConvMode MODE, int BN>
-__device__ __forceinline__ void load_stage(const Params& p, const TileCoord& tc, int kb,
-                                           uint32_t a_smem, uint32_t b_smem, int tid,
-                                           int row_n, int row_hb, int row_wb, bool row_ok) {
-    const ConvShape& s = p.s;
-    if constexpr (MODE == ConvMode::Fwd || MODE == ConvMode::Dgrad) {
-        // A: one row (pixel) per thread, 8 chunks of 8 channels.
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int kk0 = kb * BK + j * 8;
-            const void* src = p.a;
-            uint32_t bytes = 0;
-            if (row_ok && kk0 < s.Kdim) {
-                uint32_t rs, c0, r, sx;
-                if constexpr (MODE == ConvMode::Fwd) {
-                    s.d_c.divmod(static_cast<uint32_t>(kk0), rs, c0);
-                    s.d_s.divmod(rs, r, sx);
-                    const int hi = row_hb + static_cast<int>(r);
-                    const int wi = row_wb + static_cast<int>(sx);
-                    if (hi >= 0 && hi < s.H && wi >= 0 && wi < s.W) {
-                        src = p.a + ((static_cast<size_t>(row_n) * s.H + hi) * s.W + wi) * s.C + c0;
-                        bytes = 16;
-                    }
-                } else {
-                    s.d_k.divmod(static_cast<uint32_t>(kk0), rs, c0);  // c0 is the k offset here
-                    s.d_s.divmod(rs, r, sx);
-                    int ho = row_hb - static_cast<int>(r);  // row_hb = h + pad_h
-                    int wo = row_wb - static_cast<int>(sx);
-                    bool ok = ho >= 0 && wo >= 0;
-                    if (s.sh > 1) { ok = ok && (ho % s.sh) == 0; ho /= s.sh; }
-                    if (s.sw > 1) { ok = ok && (wo % s.sw) == 0; wo /= s.sw; }
-                    if (ok && ho < s.Ho && wo < s.Wo) {
-                        src = p.a + ((static_cast<size_t>(row_n) * s.Ho + ho) * s.Wo + wo) * s.K + c0;
-                        bytes = 16;
-                    }
-                }
-            }
-            ptx::cp_async_16(a_smem + swz(tid, j), src, bytes);
-        }
-        // B: BN rows of the (transposed) weight matrix, Kdim-contiguous.
-#pragma unroll
-        for (int i = 0; i < BN / 16; ++i) {
-            const int idx = tid + i * kProducerThreads;
-            const int brow = idx >> 3, j = idx & 7;
-            const int col = tc.nt * BN + brow;
-            const int kk0 = kb * BK + j * 8;
-            const bool ok = col < s.Ncol && kk0 < s.Kdim;
-            const void* src = ok ? static_cast<const void*>(p.b + static_cast<size_t>(col) * s.Kdim + kk0)
-                                 : static_cast<const void*>(p.b);
-            ptx::cp_async_16(b_smem + swz(brow, j), src, ok ? 16u : 0u);
-        }
+// Output / residual / mask row of GEMM row m. Dgrad phases scatter their rows
+// over the stride lattice of dx.
+template <ConvMode MODE>
+__device__ __forceinline__ size_t out_row(const Params& p, int m) {
+    if constexpr (MODE == ConvMode::Dgrad) {
+        uint32_t n, rem, hq, wq;
+        p.d_hwq.divmod(static_cast<uint32_t>(m), n, rem);
+        p.d_wq.divmod(rem, hq, wq);
+        const int h = static_cast<int>(hq) * p.s.sh + p.ph.ph;
+        const int w = static_cast<int>(wq) * p.s.sw + p.ph.pw;
+        return (size_t(n) * p.s.H + h) * p.s.W + w;
     } else {
-        // Wgrad, both operands MN-major: smem row = pixel (reduction index),
-        // 128 B = 64 consecutive M (or N) elements, 64-element blocks 8 KB apart.
-        const int P = s.Kdim;
+        return static_cast<size_t>(m);
+    }
+}
+
+// ------------------------------------------------------------ producers ----
+// Activation operand of fwd / dgrad: one GEMM row (pixel) per thread.
+template <ConvMode MODE>
+__device__ __forceinline__ void gather_a_rows(const Params& p, int kb, uint32_t a_smem, int tid,
+                                              int row_n, int row_hb, int row_wb, bool row_ok) {
+    const ConvShape& s = p.s;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {  // A = dy: 64 pixels x 128 out-channels
-            const int idx = tid + i * kProducerThreads;
-            const int pl = idx >> 4, ck = idx & 15;
-            const int pix = kb * BK + pl;
-            const int k0 = tc.mt * BM + ck * 8;
-            const bool ok = pix < P && k0 < s.K;
-            const void* src = ok ? static_cast<const void*>(p.a + static_cast<size_t>(pix) * s.K + k0)
-                                 : static_cast<const void*>(p.a);
-            ptx::cp_async_16(a_smem + (ck >> 3) * 8192u + swz(pl, ck & 7), src, ok ? 16u : 0u);
-        }
-        constexpr int kChunksPerRow = BN / 8;
-#pragma unroll 4
-        for (int i = 0; i < BN / 16; ++i) {  // B = im2col(x): 64 pixels x BN (r,s,c) columns
-            const int idx = tid + i * kProducerThreads;
-            const int pl = idx / kChunksPerRow, cn = idx % kChunksPerRow;
-            const int pix = kb * BK + pl;
-            const int col0 = tc.nt * BN + cn * 8;
-            const void* src = p.b;
-            uint32_t bytes = 0;
-            if (pix < P && col0 < s.Ncol) {
-                uint32_t n, rem, ho, wo, rs, c0, r, sx;
-                s.d_howo.divmod(static_cast<uint32_t>(pix), n, rem);
-                s.d_wo.divmod(rem, ho, wo);
-                s.d_c.divmod(static_cast<uint32_t>(col0), rs, c0);
+    for (int j = 0; j < 8; ++j) {
+        const int kk0 = kb * BK + j * 8;
+        const void* src = p.a;
+        uint32_t bytes = 0;
+        if (row_ok && kk0 < s.Kdim) {
+            if constexpr (MODE == ConvMode::Fwd) {
+                uint32_t rs, c0, r, sx;
+                s.d_c.divmod(static_cast<uint32_t>(kk0), rs, c0);
                 s.d_s.divmod(rs, r, sx);
-                const int hi = static_cast<int>(ho) * s.sh - s.ph + static_cast<int>(r);
-                const int wi = static_cast<int>(wo) * s.sw - s.pw + static_cast<int>(sx);
+                const int hi = row_hb + static_cast<int>(r);
+                const int wi = row_wb + static_cast<int>(sx);
                 if (hi >= 0 && hi < s.H && wi >= 0 && wi < s.W) {
-                    src = p.b + ((static_cast<size_t>(n) * s.H + hi) * s.W + wi) * s.C + c0;
+                    src = p.a + ((static_cast<size_t>(row_n) * s.H + hi) * s.W + wi) * s.C + c0;
+                    bytes = 16;
+                }
+            } else {
+                uint32_t t, k0, ri, si;
+                s.d_k.divmod(static_cast<uint32_t>(kk0), t, k0);
+                p.d_ts.divmod(t, ri, si);
+                const int ho = row_hb - static_cast<int>(ri);
+                const int wo = row_wb - static_cast<int>(si);
+                if (ho >= 0 && ho < s.Ho && wo >= 0 && wo < s.Wo) {
+                    src = p.a + ((static_cast<size_t>(row_n) * s.Ho + ho) * s.Wo + wo) * s.K + k0;
                     bytes = 16;
                 }
             }
-            ptx::cp_async_16(b_smem + (cn >> 3) * 8192u + swz(pl, cn & 7), src, bytes);
         }
+        ptx::cp_async_16(a_smem + swz(tid, j), src, bytes);
+    }
+}
+
+// Wgrad operands, both MN-major: smem row = pixel (the reduction index),
+// 128 B = 64 consecutive M (or N) elements, 64-element blocks 8 KB apart.
+template <int BN>
+__device__ __forceinline__ void gather_wgrad(const Params& p, const TileCoord& tc, int kb,
+                                             uint32_t a_smem, uint32_t b_smem, int tid) {
+    const ConvShape& s = p.s;
+    const int P = s.Kdim;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // A = dy: 64 pixels x 128 out-channels
+        const int idx = tid + i * kProducerThreads;
+        const int pl = idx >> 4, ck = idx & 15;
+        const int pix = kb * BK + pl;
+        const int k0 = tc.mt * BM + ck * 8;
+        const bool ok = pix < P && k0 < s.K;
+        const void* src = ok ? static_cast<const void*>(p.a + static_cast<size_t>(pix) * s.K + k0)
+                             : static_cast<const void*>(p.a);
+        ptx::cp_async_16(a_smem + (ck >> 3) * 8192u + swz(pl, ck & 7), src, ok ? 16u : 0u);
+    }
+    constexpr int kChunksPerRow = BN / 8;
+#pragma unroll 4
+    for (int i = 0; i < BN / 16; ++i) {  // B = im2col(x): 64 pixels x BN (r,s,c) columns
+        const int idx = tid + i * kProducerThreads;
+        const int pl = idx / kChunksPerRow, cn = idx % kChunksPerRow;
+        const int pix = kb * BK + pl;
+        const int col0 = tc.nt * BN + cn * 8;
+        const void* src = p.b;
+        uint32_t bytes = 0;
+        if (pix < P && col0 < s.Ncol) {
+            uint32_t n, rem, ho, wo, rs, c0, r, sx;
+            s.d_howo.divmod(static_cast<uint32_t>(pix), n, rem);
+            s.d_wo.divmod(rem, ho, wo);
+            s.d_c.divmod(static_cast<uint32_t>(col0), rs, c0);
+            s.d_s.divmod(rs, r, sx);
+            const int hi = static_cast<int>(ho) * s.sh - s.ph + static_cast<int>(r);
+            const int wi = static_cast<int>(wo) * s.sw - s.pw + static_cast<int>(sx);
+            if (hi >= 0 && hi < s.H && wi >= 0 && wi < s.W) {
+                src = p.b + ((static_cast<size_t>(n) * s.H + hi) * s.W + wi) * s.C + c0;
+                bytes = 16;
+            }
+        }
+        ptx::cp_async_16(b_smem + (cn >> 3) * 8192u + swz(pl, cn & 7), src, bytes);
     }
 }
 
@@ -195,7 +206,7 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 
 template <ConvMode MODE>
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord& tc, int m,
-                                               int col0, const uint32_t (&acc)[32]) {
+                                               size_t row, int col0, const uint32_t (&acc)[32]) {
     const ConvShape& s = p.s;
     if (m >= s.M || col0 >= s.Ncol) return;
     if constexpr (MODE == ConvMode::Wgrad) {
@@ -211,7 +222,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
             for (int i = 0; i < 32 && col0 + i < s.Ncol; ++i) out[i] = __uint_as_float(acc[i]);
         }
     } else {
-        const size_t base = static_cast<size_t>(m) * s.Ncol + col0;
+        const size_t base = row * s.Ncol + col0;
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + base;
         const bool full = col0 + 32 <= s.Ncol;
 #pragma unroll
@@ -260,6 +271,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
 template <ConvMode MODE, int BN>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ Params p) {
     using C = Cfg<BN>;
+    constexpr bool kTmaB = MODE != ConvMode::Wgrad;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 
     if (tid == 0) {
         for (int i = 0; i < C::kStages; ++i) {
-            ptx::mbar_init(&full[i], kProducerThreads);
+            ptx::mbar_init(&full[i], kProducerThreads + (kTmaB ? 1 : 0));
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -282,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             ptx::mbar_init(&tempty[i], kEpilogueThreads);
         }
         ptx::fence_mbarrier_init();
+        if (kTmaB) ptx::tma_prefetch_desc(&p.tmap_b);
     }
     if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
@@ -310,10 +323,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                         row_hb = static_cast<int>(a) * p.s.sh - p.s.ph;
                         row_wb = static_cast<int>(b) * p.s.sw - p.s.pw;
                     } else {
-                        p.s.d_hw.divmod(static_cast<uint32_t>(m), n, rem);
-                        p.s.d_w.divmod(rem, a, b);
-                        row_hb = static_cast<int>(a) + p.s.ph;
-                        row_wb = static_cast<int>(b) + p.s.pw;
+                        p.d_hwq.divmod(static_cast<uint32_t>(m), n, rem);
+                        p.d_wq.divmod(rem, a, b);
+                        row_hb = static_cast<int>(a) + p.ph.bh;  // ho = hq + bh - ri
+                        row_wb = static_cast<int>(b) + p.ph.bw;
                     }
                     row_n = static_cast<int>(n);
                 }
@@ -321,11 +334,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 const uint32_t a_smem = smem_base + stage * C::kStageBytes;
-                load_stage<MODE, BN>(p, tc, kb, a_smem, a_smem + C::kABytes, tid, row_n, row_hb,
-                                     row_wb, row_ok);
+                const uint32_t b_smem = a_smem + C::kABytes;
+                if constexpr (kTmaB) {
+                    if (tid == 0) {
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kBBytes);
+                        ptx::tma_load_2d(b_smem, &p.tmap_b, &full[stage], kb * BK, tc.nt * BN);
+                    }
+                    gather_a_rows<MODE>(p, kb, a_smem, tid, row_n, row_hb, row_wb, row_ok);
+                } else {
+                    gather_wgrad<BN>(p, tc, kb, a_smem, b_smem, tid);
+                }
                 ptx::cp_async_commit();
-                if (++pending > kLag) {
-                    ptx::cp_async_wait<kLag>();
+                if (++pending > C::kLag) {
+                    ptx::cp_async_wait<C::kLag>();
                     ptx::fence_proxy_async_smem();
                     ptx::mbar_arrive(&full[arrive_stage]);
                     arrive_stage = arrive_stage + 1 == C::kStages ? 0 : arrive_stage + 1;
@@ -378,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     ptx::umma_commit(&empty[stage]);
                 }
                 __syncwarp();
-                if (++stage == Cfg<BN>::kStages) {
+                if (++stage == C::kStages) {
                     stage = 0;
                     phase ^= 1;
                 }
@@ -395,9 +416,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             const TileCoord tc = tile_coord(p, t);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
+            const int m = tc.mt * BM + row;
+            const size_t orow = m < p.s.M ? out_row<MODE>(p, m) : 0;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
-            const int m = tc.mt * BM + row;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
@@ -405,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                                             acc * BN + c * 32,
                                         v);
                 ptx::tmem_ld_wait();
-                epilogue_chunk<MODE>(p, tc, m, tc.nt * BN + c * 32, v);
+                epilogue_chunk<MODE>(p, tc, m, orow, tc.nt * BN + c * 32, v);
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
@@ -417,6 +439,21 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     if (warp == kMmaWarp) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+// Dgrad phases without any filter tap (e.g. odd pixels of a 1x1 stride-2
+// conv): dx = residual_grad * mask (or 0).
+__global__ void dgrad_empty_phase_kernel(const Params p) {
+    const size_t total = size_t(p.s.M) * p.s.Ncol;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(i / p.s.Ncol);
+        const int c = static_cast<int>(i % p.s.Ncol);
+        const size_t o = out_row<ConvMode::Dgrad>(p, m) * p.s.Ncol + c;
+        float v = p.residual ? __bfloat162float(p.residual[o]) : 0.f;
+        if (p.mask && !(__bfloat162float(p.mask[o]) > 0.f)) v = 0.f;
+        static_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16_rn(v);
     }
 }
 
@@ -438,7 +475,7 @@ SplitPlan plan_splits(const ConvShape& s, int bn) {
 }
 
 template <ConvMode MODE, int BN>
-cudaError_t launch(Params p, cudaStream_t st) {
+cudaError_t launch(Params& p, const void* b_matrix, cudaStream_t st) {
     using C = Cfg<BN>;
     static bool configured = false;
     if (!configured) {
@@ -447,6 +484,11 @@ cudaError_t launch(Params p, cudaStream_t st) {
                                              static_cast<int>(C::kSmem));
         if (e != cudaSuccess) return e;
         configured = true;
+    }
+    if (MODE != ConvMode::Wgrad) {
+        // weight operand: row-major [Ncol][Kdim] bf16, boxes of BN rows x 64
+        if (!make_tmap_bf16_2d(&p.tmap_b, b_matrix, p.s.Ncol, p.s.Kdim, BN))
+            return cudaErrorInvalidValue;
     }
     p.m_tiles = (p.s.M + BM - 1) / BM;
     p.n_tiles = (p.s.Ncol + BN - 1) / BN;
@@ -462,11 +504,11 @@ cudaError_t launch(Params p, cudaStream_t st) {
 }
 
 template <ConvMode MODE>
-cudaError_t dispatch(Params p, cudaStream_t st) {
+cudaError_t dispatch(Params& p, const void* b_matrix, cudaStream_t st) {
     switch (pick_bn(p.s.Ncol)) {
-        case 256: return launch<MODE, 256>(p, st);
-        case 128: return launch<MODE, 128>(p, st);
-        default: return launch<MODE, 64>(p, st);
+        case 256: return launch<MODE, 256>(p, b_matrix, st);
+        case 128: return launch<MODE, 128>(p, b_matrix, st);
+        default: return launch<MODE, 64>(p, b_matrix, st);
     }
 }
 
@@ -491,28 +533,47 @@ cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const E
     Params p{};
     p.s = make_shape(g, ConvMode::Fwd);
     p.a = static_cast<const __nv_bfloat16*>(x);
-    p.b = static_cast<const __nv_bfloat16*>(w);
     p.out = y;
     p.bias = ep.bias;
     p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
-    p.mask = nullptr;
     p.relu = ep.relu ? 1 : 0;
-    return dispatch<ConvMode::Fwd>(p, st);
+    return dispatch<ConvMode::Fwd>(p, w, st);
 }
 
-cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wT, const Epilogue& ep,
+cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, const Epilogue& ep,
                           void* dx, cudaStream_t st) {
-    Params p{};
-    p.s = make_shape(g, ConvMode::Dgrad);
-    p.a = static_cast<const __nv_bfloat16*>(dy);
-    p.b = static_cast<const __nv_bfloat16*>(wT);
-    p.out = dx;
-    p.bias = nullptr;
-    p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
-    p.mask = static_cast<const __nv_bfloat16*>(ep.mask);
-    p.relu = 0;
-    return dispatch<ConvMode::Dgrad>(p, st);
+    for (int ph = 0; ph < g.stride_h; ++ph) {
+        for (int pw = 0; pw < g.stride_w; ++pw) {
+            Params p{};
+            p.ph = dgrad_phase(g, ph, pw);
+            if (p.ph.Hq <= 0 || p.ph.Wq <= 0) continue;
+            p.s = make_shape(g, ConvMode::Dgrad);
+            p.s.M = g.n * p.ph.Hq * p.ph.Wq;
+            p.s.Kdim = p.ph.tr * p.ph.ts * g.k;
+            p.d_hwq = FastDiv(static_cast<uint32_t>(p.ph.Hq * p.ph.Wq));
+            p.d_wq = FastDiv(static_cast<uint32_t>(p.ph.Wq));
+            p.d_ts = FastDiv(static_cast<uint32_t>(std::max(p.ph.ts, 1)));
+            p.a = static_cast<const __nv_bfloat16*>(dy);
+            p.out = dx;
+            p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
+            p.mask = static_cast<const __nv_bfloat16*>(ep.mask);
+            cudaError_t e;
+            if (p.s.Kdim == 0) {
+                const size_t total = size_t(p.s.M) * p.s.Ncol;
+                const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
+                dgrad_empty_phase_kernel<<<blocks, 256, 0, st>>>(p);
+                e = cudaGetLastError();
+            } else {
+                e = dispatch<ConvMode::Dgrad>(
+                    p, static_cast<const __nv_bfloat16*>(wTp) + p.ph.woff, st);
+            }
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
 }
+
+int conv_tc_dgrad_launches(const ConvGeom& g) { return g.stride_h * g.stride_w; }
 
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
                           void* workspace, cudaStream_t st) {
@@ -525,7 +586,7 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
     p.kb_per_split = sp.kb_per_split;
     p.out = sp.splits > 1 ? workspace : static_cast<void*>(dw);
     if (sp.splits > 1 && workspace == nullptr) return cudaErrorInvalidValue;
-    cudaError_t e = dispatch<ConvMode::Wgrad>(p, st);
+    cudaError_t e = dispatch<ConvMode::Wgrad>(p, nullptr, st);
     if (e != cudaSuccess || sp.splits == 1) return e;
     return split_reduce(static_cast<const float*>(workspace), sp.splits,
                         size_t(p.s.M) * p.s.Ncol, dw, st);

@@ -72,6 +72,29 @@ __global__ void transpose_krsc_kernel(const T* __restrict__ w, T* __restrict__ w
     }
 }
 
+// w[K][R][S][C] -> per-phase packed dgrad operand [C][tr][ts][K] (see DgradPhase);
+// one (r, s) tap per blockIdx.z, 32x32 (c, k) tiles through shared memory.
+template <typename T>
+__global__ void pack_dgrad_kernel(const T* __restrict__ w, T* __restrict__ out, ConvGeom g) {
+    __shared__ T tile[32][33];
+    const int r = blockIdx.z / g.s, s = blockIdx.z % g.s;
+    const int ph = ((r - g.pad_h) % g.stride_h + g.stride_h) % g.stride_h;
+    const int pw = ((s - g.pad_w) % g.stride_w + g.stride_w) % g.stride_w;
+    const DgradPhase d = dgrad_phase(g, ph, pw);
+    const int ri = (r - d.r0) / g.stride_h, si = (s - d.s0) / g.stride_w;
+    const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int k = k0 + i, c = c0 + threadIdx.x;
+        if (k < g.k && c < g.c) tile[i][threadIdx.x] = w[((size_t(k) * g.r + r) * g.s + s) * g.c + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, k = k0 + threadIdx.x;
+        if (k < g.k && c < g.c)
+            out[d.woff + ((size_t(c) * d.tr + ri) * d.ts + si) * g.k + k] = tile[threadIdx.x][i];
+    }
+}
+
 template <typename T>
 __global__ void column_partial_kernel(const T* __restrict__ in, float* __restrict__ part,
                                       int rows, int cols, int rows_per_chunk) {
@@ -357,6 +380,14 @@ cudaError_t transpose_krsc(DType dt, const void* w, void* wT, int K, int R, int 
     dim3 grid((C + 31) / 32, (K + 31) / 32, R * S), block(32, 8);
     TCB_DT_SWITCH(dt, T, (transpose_krsc_kernel<T><<<grid, block, 0, st>>>(
                               static_cast<const T*>(w), static_cast<T*>(wT), K, R * S, C)));
+    return cudaGetLastError();
+}
+
+cudaError_t pack_dgrad_weights(DType dt, const void* w, void* packed, const ConvGeom& g,
+                               cudaStream_t st) {
+    dim3 grid((g.c + 31) / 32, (g.k + 31) / 32, g.r * g.s), block(32, 8);
+    TCB_DT_SWITCH(dt, T, (pack_dgrad_kernel<T><<<grid, block, 0, st>>>(
+                              static_cast<const T*>(w), static_cast<T*>(packed), g)));
     return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ struct Epilogue {
 
 // ---- tensor-core implicit GEMM (tcgen05 / TMEM), bf16 in, fp32 accumulate ----
 // Requirements: C % 8 == 0 (fwd/wgrad), K % 8 == 0 (dgrad/wgrad).
-// wT (dgrad) is the [C][R][S][K] transpose of w produced by transpose_krsc.
+// wTp (dgrad) is w packed per stride phase by pack_dgrad_weights.
 size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode);
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
                         void* y, cudaStream_t st);
@@ -77,6 +77,10 @@ cudaError_t cast(DType src_t, const void* src, DType dst_t, void* dst, size_t n,
 // [K][R][S][C] -> [C][R][S][K]
 cudaError_t transpose_krsc(DType dt, const void* w, void* wT, int K, int R, int S, int C,
                            cudaStream_t st);
+// [K][R][S][C] -> per stride-phase packed [C][taps_r][taps_s][K] blocks (the dgrad
+// B operand of conv_tc_dgrad; same total size as w; plain transpose at stride 1).
+cudaError_t pack_dgrad_weights(DType dt, const void* w, void* packed, const ConvGeom& g,
+                               cudaStream_t st);
 // out[j] = sum_i in[i][j] (rows x cols, fp32 result), deterministic.
 cudaError_t column_sum(DType dt, const void* in, float* out, int rows, int cols, float* ws,
                        cudaStream_t st);

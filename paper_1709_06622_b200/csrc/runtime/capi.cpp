@@ -191,7 +191,7 @@ TCB_API int tcb_conv_dgrad(const tcb_conv_plan* plan, const void* dy, const void
             if (plan->prec == TCB_PREC_BF16) {
                 if (!workspace) return fail(TCB_ERR_INVALID, "bf16 dgrad needs the plan workspace");
                 void* wT = static_cast<char*>(workspace) + plan->layout.off_wT;
-                e = transpose_krsc(DType::BF16, w, wT, plan->g.k, plan->g.r, plan->g.s, plan->g.c, st);
+                e = pack_dgrad_weights(DType::BF16, w, wT, plan->g, st);
                 if (e == cudaSuccess) e = conv_tc_dgrad(plan->g, dy, wT, ep, dx, st);
             } else {
                 e = conv_ffma_dgrad(plan->g, static_cast<const float*>(dy),

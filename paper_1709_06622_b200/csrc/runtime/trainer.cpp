@@ -388,8 +388,8 @@ int refresh_transposes(tcb_trainer* t, cudaStream_t st) {
     if (!t->bf16) return TCB_OK;
     for (const Node& nd : t->nodes) {
         if (nd.op != Op::Conv || !nd.need_dgrad) continue;
-        TRY_CUDA(transpose_krsc(DType::BF16, t->at<__nv_bfloat16>(t->off_wc) + nd.woff, t->at(nd.wT),
-                                nd.g.k, nd.g.r, nd.g.s, nd.g.c, st));
+        TRY_CUDA(pack_dgrad_weights(DType::BF16, t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
+                                    t->at(nd.wT), nd.g, st));
         t->launches++;
     }
     return TCB_OK;
