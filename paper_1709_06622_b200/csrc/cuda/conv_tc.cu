@@ -52,7 +52,8 @@ struct Cfg {
 };
 
 struct Params {
-    CUtensorMap tmap_b;      // weight operand (fwd / dgrad), 64-byte aligned
+    CUtensorMap tmap_a;      // activation operand when it is a plain matrix (1x1/s1/p0)
+    CUtensorMap tmap_b;      // weight operand (fwd / dgrad) or x (plain wgrad)
     ConvShape s;
     const __nv_bfloat16* a;  // fwd: x   dgrad: dy   wgrad: dy
     const __nv_bfloat16* b;  // wgrad: x (gathered)
@@ -143,9 +144,28 @@ __device__ __forceinline__ void gather_a_rows(const Params& p, int kb, uint32_t 
 
 // Wgrad operands, both MN-major: smem row = pixel (the reduction index),
 // 128 B = 64 consecutive M (or N) elements, 64-element blocks 8 KB apart.
+// Per-thread constant part of the wgrad im2col column decode: with 128
+// producer threads and BN/8 chunks per pixel row, thread t always loads
+// column chunk t % (BN/8) of the tile.
+struct WgradCol {
+    int r, s, c0;
+    bool ok;
+};
+
+// Pixel table entry of one stage: n*H, ho*sh - pad_h, wo*sw - pad_w (valid if nH >= 0).
+__device__ __forceinline__ int4 wgrad_pixel(const ConvShape& s, int pix) {
+    if (pix >= s.Kdim) return make_int4(-1, 0, 0, 0);
+    uint32_t n, rem, ho, wo;
+    s.d_howo.divmod(static_cast<uint32_t>(pix), n, rem);
+    s.d_wo.divmod(rem, ho, wo);
+    return make_int4(static_cast<int>(n) * s.H, static_cast<int>(ho) * s.sh - s.ph,
+                     static_cast<int>(wo) * s.sw - s.pw, 0);
+}
+
 template <int BN>
 __device__ __forceinline__ void gather_wgrad(const Params& p, const TileCoord& tc, int kb,
-                                             uint32_t a_smem, uint32_t b_smem, int tid) {
+                                             uint32_t a_smem, uint32_t b_smem, int tid,
+                                             const WgradCol& col, const int4* pixtab) {
     const ConvShape& s = p.s;
     const int P = s.Kdim;
 #pragma unroll
@@ -160,26 +180,18 @@ __device__ __forceinline__ void gather_wgrad(const Params& p, const TileCoord& t
         ptx::cp_async_16(a_smem + (ck >> 3) * 8192u + swz(pl, ck & 7), src, ok ? 16u : 0u);
     }
     constexpr int kChunksPerRow = BN / 8;
+    constexpr int kRowsPerPass = kProducerThreads / kChunksPerRow;
+    const int cn = tid % kChunksPerRow;
 #pragma unroll 4
     for (int i = 0; i < BN / 16; ++i) {  // B = im2col(x): 64 pixels x BN (r,s,c) columns
-        const int idx = tid + i * kProducerThreads;
-        const int pl = idx / kChunksPerRow, cn = idx % kChunksPerRow;
-        const int pix = kb * BK + pl;
-        const int col0 = tc.nt * BN + cn * 8;
+        const int pl = tid / kChunksPerRow + i * kRowsPerPass;
+        const int4 px = pixtab[pl];
         const void* src = p.b;
         uint32_t bytes = 0;
-        if (pix < P && col0 < s.Ncol) {
-            uint32_t n, rem, ho, wo, rs, c0, r, sx;
-            s.d_howo.divmod(static_cast<uint32_t>(pix), n, rem);
-            s.d_wo.divmod(rem, ho, wo);
-            s.d_c.divmod(static_cast<uint32_t>(col0), rs, c0);
-            s.d_s.divmod(rs, r, sx);
-            const int hi = static_cast<int>(ho) * s.sh - s.ph + static_cast<int>(r);
-            const int wi = static_cast<int>(wo) * s.sw - s.pw + static_cast<int>(sx);
-            if (hi >= 0 && hi < s.H && wi >= 0 && wi < s.W) {
-                src = p.b + ((static_cast<size_t>(n) * s.H + hi) * s.W + wi) * s.C + c0;
-                bytes = 16;
-            }
+        const int hi = px.y + col.r, wi = px.z + col.s;
+        if (col.ok && px.x >= 0 && hi >= 0 && hi < s.H && wi >= 0 && wi < s.W) {
+            src = p.b + ((static_cast<size_t>(px.x) + hi) * s.W + wi) * s.C + col.c0;
+            bytes = 16;
         }
         ptx::cp_async_16(b_smem + (cn >> 3) * 8192u + swz(pl, cn & 7), src, bytes);
     }
@@ -268,10 +280,13 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
 }
 
 // --------------------------------------------------------------- kernel ----
-template <ConvMode MODE, int BN>
+// PLAIN: the implicit-GEMM operands are plain row-major matrices (1x1 filter,
+// stride 1, no padding) and are fetched entirely by TMA; otherwise the
+// activation operand is gathered with cp.async.
+template <ConvMode MODE, int BN, bool PLAIN>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ Params p) {
     using C = Cfg<BN>;
-    constexpr bool kTmaB = MODE != ConvMode::Wgrad;
+    constexpr bool kTmaB = MODE != ConvMode::Wgrad || PLAIN;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -280,13 +295,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    __shared__ int4 pixtab[2][BK];  // wgrad im2col pixel decode, double-buffered
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
 
     if (tid == 0) {
         for (int i = 0; i < C::kStages; ++i) {
-            ptx::mbar_init(&full[i], kProducerThreads + (kTmaB ? 1 : 0));
+            ptx::mbar_init(&full[i], PLAIN ? 1 : kProducerThreads + (kTmaB ? 1 : 0));
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -295,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
         ptx::fence_mbarrier_init();
         if (kTmaB) ptx::tma_prefetch_desc(&p.tmap_b);
+        if (PLAIN) ptx::tma_prefetch_desc(&p.tmap_a);
     }
     if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
@@ -303,15 +320,58 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t smem_base = ptx::smem_addr(smem);
 
-    if (warp < 4) {
+    if (warp < 4 && PLAIN) {
+        // ======================================= TMA-only producer ======
+        if (tid == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                const TileCoord tc = tile_coord(p, t);
+                for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t a_smem = smem_base + stage * C::kStageBytes;
+                    const uint32_t b_smem = a_smem + C::kABytes;
+                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    if constexpr (MODE == ConvMode::Wgrad) {
+                        // MN-major 64-element x 64-pixel boxes (8 KB each)
+                        ptx::tma_load_2d(a_smem, &p.tmap_a, &full[stage], tc.mt * BM, kb * BK);
+                        ptx::tma_load_2d(a_smem + 8192, &p.tmap_a, &full[stage], tc.mt * BM + 64,
+                                         kb * BK);
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j)
+                            ptx::tma_load_2d(b_smem + j * 8192, &p.tmap_b, &full[stage],
+                                             tc.nt * BN + j * 64, kb * BK);
+                    } else {
+                        ptx::tma_load_2d(a_smem, &p.tmap_a, &full[stage], kb * BK, tc.mt * BM);
+                        ptx::tma_load_2d(b_smem, &p.tmap_b, &full[stage], kb * BK, tc.nt * BN);
+                    }
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp < 4) {
         // ================================================ producers ======
         int stage = 0;
         uint32_t phase = 0;
-        int pending = 0, arrive_stage = 0;
+        int kb_seq = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             const TileCoord tc = tile_coord(p, t);
             int row_n = 0, row_hb = 0, row_wb = 0;
             bool row_ok = false;
+            WgradCol col{0, 0, 0, false};
+            if constexpr (MODE == ConvMode::Wgrad) {
+                const int col0 = tc.nt * BN + (tid % (BN / 8)) * 8;
+                col.ok = col0 < p.s.Ncol;
+                if (col.ok) {
+                    uint32_t rs, c0, r, sx;
+                    p.s.d_c.divmod(static_cast<uint32_t>(col0), rs, c0);
+                    p.s.d_s.divmod(rs, r, sx);
+                    col = WgradCol{static_cast<int>(r), static_cast<int>(sx), static_cast<int>(c0), true};
+                }
+            }
             if constexpr (MODE != ConvMode::Wgrad) {
                 const int m = tc.mt * BM + tid;
                 row_ok = m < p.s.M;
@@ -331,7 +391,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     row_n = static_cast<int>(n);
                 }
             }
-            for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
+            for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb, ++kb_seq) {
+                int4* tab = pixtab[kb_seq & 1];
+                if constexpr (MODE == ConvMode::Wgrad) {
+                    // decode this stage's 64 pixels once, shared by all producers
+                    if (tid < BK) tab[tid] = wgrad_pixel(p.s, kb * BK + tid);
+                    asm volatile("bar.sync 1, %0;" ::"n"(kProducerThreads) : "memory");
+                }
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 const uint32_t a_smem = smem_base + stage * C::kStageBytes;
                 const uint32_t b_smem = a_smem + C::kABytes;
@@ -342,16 +408,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     }
                     gather_a_rows<MODE>(p, kb, a_smem, tid, row_n, row_hb, row_wb, row_ok);
                 } else {
-                    gather_wgrad<BN>(p, tc, kb, a_smem, b_smem, tid);
+                    gather_wgrad<BN>(p, tc, kb, a_smem, b_smem, tid, col, tab);
                 }
-                ptx::cp_async_commit();
-                if (++pending > C::kLag) {
-                    ptx::cp_async_wait<C::kLag>();
-                    ptx::fence_proxy_async_smem();
-                    ptx::mbar_arrive(&full[arrive_stage]);
-                    arrive_stage = arrive_stage + 1 == C::kStages ? 0 : arrive_stage + 1;
-                    --pending;
-                }
+                // arrives once this thread's copies of the stage have landed
+                ptx::cp_async_mbar_arrive_noinc(&full[stage]);
                 if (++stage == C::kStages) {
                     stage = 0;
                     phase ^= 1;
@@ -359,11 +419,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             }
         }
         ptx::cp_async_wait<0>();
-        ptx::fence_proxy_async_smem();
-        for (; pending > 0; --pending) {
-            ptx::mbar_arrive(&full[arrive_stage]);
-            arrive_stage = arrive_stage + 1 == C::kStages ? 0 : arrive_stage + 1;
-        }
     } else if (warp == kMmaWarp) {
         // =============================================== MMA issuer ======
         constexpr uint32_t kMN = MODE == ConvMode::Wgrad ? 1u : 0u;
@@ -474,12 +529,17 @@ SplitPlan plan_splits(const ConvShape& s, int bn) {
     return {(kb_total + per - 1) / per, per};
 }
 
-template <ConvMode MODE, int BN>
-cudaError_t launch(Params& p, const void* b_matrix, cudaStream_t st) {
+// 1x1 filter, stride 1, no padding: every implicit-GEMM operand is a plain matrix.
+bool plain_geometry(const ConvShape& s) {
+    return s.R == 1 && s.S == 1 && s.ph == 0 && s.pw == 0 && s.sh == 1 && s.sw == 1;
+}
+
+template <ConvMode MODE, int BN, bool PLAIN>
+cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
     using C = Cfg<BN>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN>,
+        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, PLAIN>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(C::kSmem));
         if (e != cudaSuccess) return e;
@@ -488,6 +548,14 @@ cudaError_t launch(Params& p, const void* b_matrix, cudaStream_t st) {
     if (MODE != ConvMode::Wgrad) {
         // weight operand: row-major [Ncol][Kdim] bf16, boxes of BN rows x 64
         if (!make_tmap_bf16_2d(&p.tmap_b, b_matrix, p.s.Ncol, p.s.Kdim, BN))
+            return cudaErrorInvalidValue;
+        // activation operand as a plain [M][Kdim] matrix, boxes of 128 rows x 64
+        if (PLAIN && !make_tmap_bf16_2d(&p.tmap_a, a_matrix, p.s.M, p.s.Kdim, BM))
+            return cudaErrorInvalidValue;
+    } else if (PLAIN) {
+        // dy [P][K] and x [P][C], MN-major 64 x 64 boxes
+        if (!make_tmap_bf16_2d(&p.tmap_a, a_matrix, p.s.Kdim, p.s.K, BK, 64) ||
+            !make_tmap_bf16_2d(&p.tmap_b, b_matrix, p.s.Kdim, p.s.C, BK, 64))
             return cudaErrorInvalidValue;
     }
     p.m_tiles = (p.s.M + BM - 1) / BM;
@@ -499,17 +567,23 @@ cudaError_t launch(Params& p, const void* b_matrix, cudaStream_t st) {
     }
     p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
     const int grid = std::min(p.num_tiles, num_sms());
-    conv_tc_kernel<MODE, BN><<<grid, kThreads, C::kSmem, st>>>(p);
+    conv_tc_kernel<MODE, BN, PLAIN><<<grid, kThreads, C::kSmem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <ConvMode MODE>
-cudaError_t dispatch(Params& p, const void* b_matrix, cudaStream_t st) {
+template <ConvMode MODE, bool PLAIN>
+cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
     switch (pick_bn(p.s.Ncol)) {
-        case 256: return launch<MODE, 256>(p, b_matrix, st);
-        case 128: return launch<MODE, 128>(p, b_matrix, st);
-        default: return launch<MODE, 64>(p, b_matrix, st);
+        case 256: return launch<MODE, 256, PLAIN>(p, a_matrix, b_matrix, st);
+        case 128: return launch<MODE, 128, PLAIN>(p, a_matrix, b_matrix, st);
+        default: return launch<MODE, 64, PLAIN>(p, a_matrix, b_matrix, st);
     }
+}
+
+template <ConvMode MODE>
+cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
+    if (plain_geometry(p.s)) return dispatch_bn<MODE, true>(p, a_matrix, b_matrix, st);
+    return dispatch_bn<MODE, false>(p, a_matrix, b_matrix, st);
 }
 
 }  // namespace
@@ -537,7 +611,7 @@ cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const E
     p.bias = ep.bias;
     p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
     p.relu = ep.relu ? 1 : 0;
-    return dispatch<ConvMode::Fwd>(p, w, st);
+    return dispatch<ConvMode::Fwd>(p, x, w, st);
 }
 
 cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, const Epilogue& ep,
@@ -565,7 +639,7 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, co
                 e = cudaGetLastError();
             } else {
                 e = dispatch<ConvMode::Dgrad>(
-                    p, static_cast<const __nv_bfloat16*>(wTp) + p.ph.woff, st);
+                    p, dy, static_cast<const __nv_bfloat16*>(wTp) + p.ph.woff, st);
             }
             if (e != cudaSuccess) return e;
         }
@@ -586,7 +660,7 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
     p.kb_per_split = sp.kb_per_split;
     p.out = sp.splits > 1 ? workspace : static_cast<void*>(dw);
     if (sp.splits > 1 && workspace == nullptr) return cudaErrorInvalidValue;
-    cudaError_t e = dispatch<ConvMode::Wgrad>(p, nullptr, st);
+    cudaError_t e = dispatch<ConvMode::Wgrad>(p, dy, x, st);
     if (e != cudaSuccess || sp.splits == 1) return e;
     return split_reduce(static_cast<const float*>(workspace), sp.splits,
                         size_t(p.s.M) * p.s.Ncol, dw, st);

@@ -75,6 +75,12 @@ __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint3
                  "r"(src_bytes)
                  : "memory");
 }
+// Arrive on `bar` once every cp.async this thread issued so far has landed
+// (.noinc: the arrival counts against the barrier's expected count).
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }

@@ -31,6 +31,10 @@ GEOMS = [
     ("rn50_stem_7x7_s2", 2, 32, 32, 8, 64, 7, 3, 2),
     ("vgg_fc_as_conv", 3, 7, 7, 64, 136, 7, 0, 1),
     ("ragged", 3, 9, 11, 40, 72, 3, 1, 1),
+    ("plain_1x1_ragged", 3, 5, 7, 24, 40, 1, 0, 1),
+    ("plain_1x1_wide", 2, 9, 9, 520, 264, 1, 0, 1),
+    ("dgrad_phase_3x3_s2_odd", 2, 15, 13, 32, 48, 3, 1, 2),
+    ("dgrad_phase_5x5_s3", 2, 17, 16, 16, 24, 5, 2, 3),
 ]
 FFMA_ONLY = [
     ("lenet_conv1_c1", 4, 28, 28, 1, 20, 5, 0, 1),
