@@ -78,6 +78,10 @@ int tcb_conv_out_hw(const tcb_conv_geom* g, int* ho, int* wo);
 int tcb_conv_plan_create(const tcb_conv_geom* g, int algo, int prec, tcb_conv_plan** plan,
                          size_t* workspace_bytes);
 int tcb_conv_plan_destroy(tcb_conv_plan* plan);
+/* Operand-load path of the tensor-core GEMM conv: 0 = automatic (2-D TMA for
+ * 1x1/stride-1 layers, im2col-mode TMA when channels % 64 == 0, cp.async
+ * gather otherwise), 1 = force the cp.async gather path (A/B testing). */
+int tcb_set_conv_operand_path(int mode);
 
 /* y = act(conv(x, w) + bias + residual); bias (fp32, K) and residual (same
  * dtype/shape as y) may be NULL; relu != 0 applies max(0, .). */

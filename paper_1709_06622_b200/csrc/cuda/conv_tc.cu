@@ -127,11 +127,13 @@ __device__ __forceinline__ void gather_a_rows(const Params& p, int kb, uint32_t 
                     bytes = 16;
                 }
             } else {
+                // packed dgrad taps are flipped: tap index t = (ri', si'),
+                // ho = hq + bh - (tr - 1) + ri' = row_hb + ri'
                 uint32_t t, k0, ri, si;
                 s.d_k.divmod(static_cast<uint32_t>(kk0), t, k0);
                 p.d_ts.divmod(t, ri, si);
-                const int ho = row_hb - static_cast<int>(ri);
-                const int wo = row_wb - static_cast<int>(si);
+                const int ho = row_hb + static_cast<int>(ri);
+                const int wo = row_wb + static_cast<int>(si);
                 if (ho >= 0 && ho < s.Ho && wo >= 0 && wo < s.Wo) {
                     src = p.a + ((static_cast<size_t>(row_n) * s.Ho + ho) * s.Wo + wo) * s.K + k0;
                     bytes = 16;
@@ -279,14 +281,23 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
     }
 }
 
+
 // --------------------------------------------------------------- kernel ----
-// PLAIN: the implicit-GEMM operands are plain row-major matrices (1x1 filter,
-// stride 1, no padding) and are fetched entirely by TMA; otherwise the
-// activation operand is gathered with cp.async.
-template <ConvMode MODE, int BN, bool PLAIN>
+// Operand load modes.
+//   kGather: the activation operand is gathered with cp.async by 128 producer
+//            threads (any C % 8 == 0 geometry); weights by TMA (fwd/dgrad).
+//   kPlain : 1x1 / stride 1 / no padding: every operand is a plain row-major
+//            matrix fetched with 2-D TMA tiles by one thread.
+//   kIm2col: the activation operand (x for fwd and wgrad, dy for dgrad) is an
+//            im2col-mode TMA load (one instruction per 64-channel tap slice),
+//            everything else 2-D TMA; one producer thread.
+constexpr int kGather = 0, kPlain = 1, kIm2col = 2;
+
+template <ConvMode MODE, int BN, int LOAD>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ Params p) {
     using C = Cfg<BN>;
-    constexpr bool kTmaB = MODE != ConvMode::Wgrad || PLAIN;
+    constexpr bool kTmaOnly = LOAD != kGather;
+    constexpr bool kTmaB = MODE != ConvMode::Wgrad || kTmaOnly;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -295,14 +306,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    __shared__ int4 pixtab[2][BK];  // wgrad im2col pixel decode, double-buffered
+    __shared__ int4 pixtab[2][BK];  // wgrad im2col pixel decode (gather mode), double-buffered
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
 
     if (tid == 0) {
         for (int i = 0; i < C::kStages; ++i) {
-            ptx::mbar_init(&full[i], PLAIN ? 1 : kProducerThreads + (kTmaB ? 1 : 0));
+            ptx::mbar_init(&full[i], kTmaOnly ? 1 : kProducerThreads + (kTmaB ? 1 : 0));
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -311,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
         ptx::fence_mbarrier_init();
         if (kTmaB) ptx::tma_prefetch_desc(&p.tmap_b);
-        if (PLAIN) ptx::tma_prefetch_desc(&p.tmap_a);
+        if (kTmaOnly) ptx::tma_prefetch_desc(&p.tmap_a);
     }
     if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
@@ -320,29 +331,82 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t smem_base = ptx::smem_addr(smem);
 
-    if (warp < 4 && PLAIN) {
+    if (warp < 4 && kTmaOnly) {
         // ======================================= TMA-only producer ======
         if (tid == 0) {
+            const ConvShape& s = p.s;
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
                 const TileCoord tc = tile_coord(p, t);
+                // im2col base position of the tile's first GEMM row (fwd / dgrad)
+                int bn = 0, bw = 0, bh = 0;
+                if constexpr (LOAD == kIm2col && MODE != ConvMode::Wgrad) {
+                    uint32_t n, rem, a, b;
+                    const uint32_t m0 = static_cast<uint32_t>(tc.mt * BM);
+                    if constexpr (MODE == ConvMode::Fwd) {
+                        s.d_howo.divmod(m0, n, rem);
+                        s.d_wo.divmod(rem, a, b);
+                        bh = static_cast<int>(a) * s.sh - s.ph;
+                        bw = static_cast<int>(b) * s.sw - s.pw;
+                    } else {
+                        p.d_hwq.divmod(m0, n, rem);
+                        p.d_wq.divmod(rem, a, b);
+                        bh = static_cast<int>(a) + p.ph.bh - (p.ph.tr - 1);
+                        bw = static_cast<int>(b) + p.ph.bw - (p.ph.ts - 1);
+                    }
+                    bn = static_cast<int>(n);
+                }
                 for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t a_smem = smem_base + stage * C::kStageBytes;
                     const uint32_t b_smem = a_smem + C::kABytes;
                     ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     if constexpr (MODE == ConvMode::Wgrad) {
-                        // MN-major 64-element x 64-pixel boxes (8 KB each)
+                        // A = dy [P][K]: MN-major 64-channel x 64-pixel boxes (8 KB each)
                         ptx::tma_load_2d(a_smem, &p.tmap_a, &full[stage], tc.mt * BM, kb * BK);
                         ptx::tma_load_2d(a_smem + 8192, &p.tmap_a, &full[stage], tc.mt * BM + 64,
                                          kb * BK);
+                        if constexpr (LOAD == kPlain) {
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j)
-                            ptx::tma_load_2d(b_smem + j * 8192, &p.tmap_b, &full[stage],
-                                             tc.nt * BN + j * 64, kb * BK);
+                            for (int j = 0; j < BN / 64; ++j)
+                                ptx::tma_load_2d(b_smem + j * 8192, &p.tmap_b, &full[stage],
+                                                 tc.nt * BN + j * 64, kb * BK);
+                        } else {
+                            // B = im2col(x): 64 pixels x 64 channels of one tap per box
+                            const int4 px = wgrad_pixel(s, kb * BK);
+                            const int pn = px.x >= 0 ? px.x / s.H : s.N;
+#pragma unroll
+                            for (int j = 0; j < BN / 64; ++j) {
+                                int col0 = tc.nt * BN + j * 64;
+                                if (col0 >= s.Ncol) col0 = 0;  // padding columns: never stored
+                                uint32_t rs, c0, r, sx;
+                                s.d_c.divmod(static_cast<uint32_t>(col0), rs, c0);
+                                s.d_s.divmod(rs, r, sx);
+                                ptx::tma_load_im2col_4d(b_smem + j * 8192, &p.tmap_b, &full[stage],
+                                                        static_cast<int>(c0), px.z, px.y, pn,
+                                                        static_cast<uint16_t>(sx),
+                                                        static_cast<uint16_t>(r));
+                            }
+                        }
                     } else {
-                        ptx::tma_load_2d(a_smem, &p.tmap_a, &full[stage], kb * BK, tc.mt * BM);
+                        if constexpr (LOAD == kPlain) {
+                            ptx::tma_load_2d(a_smem, &p.tmap_a, &full[stage], kb * BK, tc.mt * BM);
+                        } else {
+                            const uint32_t kk0 = static_cast<uint32_t>(kb * BK);
+                            uint32_t tap, c0, r, sx;
+                            if constexpr (MODE == ConvMode::Fwd) {
+                                s.d_c.divmod(kk0, tap, c0);
+                                s.d_s.divmod(tap, r, sx);
+                            } else {
+                                s.d_k.divmod(kk0, tap, c0);
+                                p.d_ts.divmod(tap, r, sx);
+                            }
+                            ptx::tma_load_im2col_4d(a_smem, &p.tmap_a, &full[stage],
+                                                    static_cast<int>(c0), bw, bh, bn,
+                                                    static_cast<uint16_t>(sx),
+                                                    static_cast<uint16_t>(r));
+                        }
                         ptx::tma_load_2d(b_smem, &p.tmap_b, &full[stage], kb * BK, tc.nt * BN);
                     }
                     if (++stage == C::kStages) {
@@ -371,8 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     p.s.d_s.divmod(rs, r, sx);
                     col = WgradCol{static_cast<int>(r), static_cast<int>(sx), static_cast<int>(c0), true};
                 }
-            }
-            if constexpr (MODE != ConvMode::Wgrad) {
+            } else {
                 const int m = tc.mt * BM + tid;
                 row_ok = m < p.s.M;
                 if (row_ok) {
@@ -385,8 +448,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     } else {
                         p.d_hwq.divmod(static_cast<uint32_t>(m), n, rem);
                         p.d_wq.divmod(rem, a, b);
-                        row_hb = static_cast<int>(a) + p.ph.bh;  // ho = hq + bh - ri
-                        row_wb = static_cast<int>(b) + p.ph.bw;
+                        row_hb = static_cast<int>(a) + p.ph.bh - (p.ph.tr - 1);
+                        row_wb = static_cast<int>(b) + p.ph.bw - (p.ph.ts - 1);
                     }
                     row_n = static_cast<int>(n);
                 }
@@ -500,15 +563,27 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 // Dgrad phases without any filter tap (e.g. odd pixels of a 1x1 stride-2
 // conv): dx = residual_grad * mask (or 0).
 __global__ void dgrad_empty_phase_kernel(const Params p) {
-    const size_t total = size_t(p.s.M) * p.s.Ncol;
+    const int groups = p.s.Ncol / 8;  // C % 8 == 0 on the tensor-core path
+    const size_t total = size_t(p.s.M) * groups;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
          i += size_t(gridDim.x) * blockDim.x) {
-        const int m = static_cast<int>(i / p.s.Ncol);
-        const int c = static_cast<int>(i % p.s.Ncol);
+        const int m = static_cast<int>(i / groups);
+        const int c = static_cast<int>(i % groups) * 8;
         const size_t o = out_row<ConvMode::Dgrad>(p, m) * p.s.Ncol + c;
-        float v = p.residual ? __bfloat162float(p.residual[o]) : 0.f;
-        if (p.mask && !(__bfloat162float(p.mask[o]) > 0.f)) v = 0.f;
-        static_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16_rn(v);
+        float v[8];
+        if (p.residual) {
+            unpack8(*reinterpret_cast<const uint4*>(p.residual + o), v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = 0.f;
+        }
+        if (p.mask) {
+            float mk[8];
+            unpack8(*reinterpret_cast<const uint4*>(p.mask + o), mk);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = mk[j] > 0.f ? v[j] : 0.f;
+        }
+        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + o) = pack8(v);
     }
 }
 
@@ -534,30 +609,55 @@ bool plain_geometry(const ConvShape& s) {
     return s.R == 1 && s.S == 1 && s.ph == 0 && s.pw == 0 && s.sh == 1 && s.sw == 1;
 }
 
-template <ConvMode MODE, int BN, bool PLAIN>
+// im2col TMA needs whole 64-channel slices of one tap per k-block and small
+// bounding-box corners / tap offsets.
+template <ConvMode MODE>
+bool im2col_ok(const Params& p) {
+    const ConvShape& s = p.s;
+    const int ch = MODE == ConvMode::Dgrad ? s.K : s.C;
+    if (ch % 64 != 0) return false;
+    if (s.R > 16 || s.S > 16 || s.ph > 15 || s.pw > 15) return false;
+    return true;
+}
+
+template <ConvMode MODE, int LOAD>
+bool build_maps(Params& p, const void* a_matrix, const void* b_matrix, int bn) {
+    const ConvShape& s = p.s;
+    if (MODE == ConvMode::Wgrad) {
+        if (LOAD == kGather) return true;
+        // dy [P][K], MN-major 64 x 64 boxes
+        if (!make_tmap_bf16_2d(&p.tmap_a, a_matrix, s.Kdim, s.K, BK, 64)) return false;
+        if (LOAD == kPlain) return make_tmap_bf16_2d(&p.tmap_b, b_matrix, s.Kdim, s.C, BK, 64);
+        return make_tmap_im2col_bf16(&p.tmap_b, b_matrix, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
+                                     s.pw - (s.S - 1), s.ph - (s.R - 1), s.sw, s.sh, BK);
+    }
+    // weight operand: row-major [Ncol][Kdim] bf16, boxes of BN rows x 64
+    if (!make_tmap_bf16_2d(&p.tmap_b, b_matrix, s.Ncol, s.Kdim, bn)) return false;
+    if (LOAD == kPlain) return make_tmap_bf16_2d(&p.tmap_a, a_matrix, s.M, s.Kdim, BM);
+    if (LOAD == kIm2col) {
+        if (MODE == ConvMode::Fwd)
+            return make_tmap_im2col_bf16(&p.tmap_a, a_matrix, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
+                                         s.pw - (s.S - 1), s.ph - (s.R - 1), s.sw, s.sh, BM);
+        // dgrad phase over dy: base positions lower .. lower + (Wq, Hq) - 1, stride 1
+        const int lw = p.ph.bw - (p.ph.ts - 1), lh = p.ph.bh - (p.ph.tr - 1);
+        return make_tmap_im2col_bf16(&p.tmap_a, a_matrix, s.N, s.Ho, s.Wo, s.K, lw, lh,
+                                     lw + p.ph.Wq - s.Wo, lh + p.ph.Hq - s.Ho, 1, 1, BM);
+    }
+    return true;
+}
+
+template <ConvMode MODE, int BN, int LOAD>
 cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
     using C = Cfg<BN>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, PLAIN>,
+        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, LOAD>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(C::kSmem));
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (MODE != ConvMode::Wgrad) {
-        // weight operand: row-major [Ncol][Kdim] bf16, boxes of BN rows x 64
-        if (!make_tmap_bf16_2d(&p.tmap_b, b_matrix, p.s.Ncol, p.s.Kdim, BN))
-            return cudaErrorInvalidValue;
-        // activation operand as a plain [M][Kdim] matrix, boxes of 128 rows x 64
-        if (PLAIN && !make_tmap_bf16_2d(&p.tmap_a, a_matrix, p.s.M, p.s.Kdim, BM))
-            return cudaErrorInvalidValue;
-    } else if (PLAIN) {
-        // dy [P][K] and x [P][C], MN-major 64 x 64 boxes
-        if (!make_tmap_bf16_2d(&p.tmap_a, a_matrix, p.s.Kdim, p.s.K, BK, 64) ||
-            !make_tmap_bf16_2d(&p.tmap_b, b_matrix, p.s.Kdim, p.s.C, BK, 64))
-            return cudaErrorInvalidValue;
-    }
+    if (!build_maps<MODE, LOAD>(p, a_matrix, b_matrix, BN)) return cudaErrorInvalidValue;
     p.m_tiles = (p.s.M + BM - 1) / BM;
     p.n_tiles = (p.s.Ncol + BN - 1) / BN;
     p.kb_total = (p.s.Kdim + BK - 1) / BK;
@@ -567,26 +667,40 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
     }
     p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
     const int grid = std::min(p.num_tiles, num_sms());
-    conv_tc_kernel<MODE, BN, PLAIN><<<grid, kThreads, C::kSmem, st>>>(p);
+    conv_tc_kernel<MODE, BN, LOAD><<<grid, kThreads, C::kSmem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <ConvMode MODE, bool PLAIN>
+template <ConvMode MODE, int LOAD>
 cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
     switch (pick_bn(p.s.Ncol)) {
-        case 256: return launch<MODE, 256, PLAIN>(p, a_matrix, b_matrix, st);
-        case 128: return launch<MODE, 128, PLAIN>(p, a_matrix, b_matrix, st);
-        default: return launch<MODE, 64, PLAIN>(p, a_matrix, b_matrix, st);
+        case 256: return launch<MODE, 256, LOAD>(p, a_matrix, b_matrix, st);
+        case 128: return launch<MODE, 128, LOAD>(p, a_matrix, b_matrix, st);
+        default: return launch<MODE, 64, LOAD>(p, a_matrix, b_matrix, st);
     }
 }
 
+int g_force_gather = -1;  // test hook: 1 = always use the cp.async gather path
+
 template <ConvMode MODE>
 cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
-    if (plain_geometry(p.s)) return dispatch_bn<MODE, true>(p, a_matrix, b_matrix, st);
-    return dispatch_bn<MODE, false>(p, a_matrix, b_matrix, st);
+    if (g_force_gather < 0) {
+        const char* e = getenv("TCB_CONV_FORCE_GATHER");
+        g_force_gather = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (!g_force_gather) {
+        const bool plain = MODE == ConvMode::Dgrad
+                               ? plain_geometry(p.s) && p.ph.tr == 1 && p.ph.ts == 1
+                               : plain_geometry(p.s);
+        if (plain) return dispatch_bn<MODE, kPlain>(p, a_matrix, b_matrix, st);
+        if (im2col_ok<MODE>(p)) return dispatch_bn<MODE, kIm2col>(p, a_matrix, b_matrix, st);
+    }
+    return dispatch_bn<MODE, kGather>(p, a_matrix, b_matrix, st);
 }
 
 }  // namespace
+
+void conv_tc_set_force_gather(int on) { g_force_gather = on ? 1 : 0; }
 
 bool conv_tc_supported(const ConvGeom& g, ConvMode mode) {
     if (g.n < 1 || g.h < 1 || g.w < 1 || g.c < 1 || g.k < 1) return false;
@@ -633,8 +747,8 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, co
             p.mask = static_cast<const __nv_bfloat16*>(ep.mask);
             cudaError_t e;
             if (p.s.Kdim == 0) {
-                const size_t total = size_t(p.s.M) * p.s.Ncol;
-                const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
+                const size_t total = size_t(p.s.M) * (p.s.Ncol / 8);
+                const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 8192));
                 dgrad_empty_phase_kernel<<<blocks, 256, 0, st>>>(p);
                 e = cudaGetLastError();
             } else {
@@ -646,8 +760,6 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, co
     }
     return cudaSuccess;
 }
-
-int conv_tc_dgrad_launches(const ConvGeom& g) { return g.stride_h * g.stride_w; }
 
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
                           void* workspace, cudaStream_t st) {

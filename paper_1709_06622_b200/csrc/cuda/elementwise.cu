@@ -81,7 +81,8 @@ __global__ void pack_dgrad_kernel(const T* __restrict__ w, T* __restrict__ out, 
     const int ph = ((r - g.pad_h) % g.stride_h + g.stride_h) % g.stride_h;
     const int pw = ((s - g.pad_w) % g.stride_w + g.stride_w) % g.stride_w;
     const DgradPhase d = dgrad_phase(g, ph, pw);
-    const int ri = (r - d.r0) / g.stride_h, si = (s - d.s0) / g.stride_w;
+    // taps are stored flipped (ri' = tr - 1 - ri) so the dy operand walks forward
+    const int ri = d.tr - 1 - (r - d.r0) / g.stride_h, si = d.ts - 1 - (s - d.s0) / g.stride_w;
     const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int k = k0 + i, c = c0 + threadIdx.x;
@@ -459,23 +460,154 @@ cudaError_t relu_mask_inplace(DType dt, void* g, const void* act, size_t n, cuda
     return cudaGetLastError();
 }
 
+namespace {
+
+// 16-byte vector of V elements of T (V = 8 for bf16, 4 for fp32).
+template <typename T, int V>
+struct alignas(16) Vec {
+    T v[V];
+};
+
+// Vectorised NHWC max pool: one thread = V consecutive channels of one output
+// pixel; argmax bytes stored V at a time. Same tie rule as the scalar kernel.
+template <typename T, int V>
+__global__ void maxpool_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                       uint8_t* __restrict__ arg, int N, int H, int W, int C,
+                                       int F, int S, int P, int Ho, int Wo) {
+    const int cg = C / V;
+    const size_t total = size_t(N) * Ho * Wo * cg;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % cg) * V;
+        size_t t = i / cg;
+        const int wo = int(t % Wo);
+        t /= Wo;
+        const int ho = int(t % Ho);
+        const int n = int(t / Ho);
+        float best[V];
+        uint8_t bi[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            best[j] = -INFINITY;
+            bi[j] = 0;
+        }
+        for (int r = 0; r < F; ++r) {
+            const int h = ho * S - P + r;
+            if (h < 0 || h >= H) continue;
+            for (int s = 0; s < F; ++s) {
+                const int w = wo * S - P + s;
+                if (w < 0 || w >= W) continue;
+                const Vec<T, V> in =
+                    *reinterpret_cast<const Vec<T, V>*>(x + ((size_t(n) * H + h) * W + w) * C + c);
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    const float v = to_f32<T>(in.v[j]);
+                    if (v > best[j]) {
+                        best[j] = v;
+                        bi[j] = static_cast<uint8_t>(r * F + s);
+                    }
+                }
+            }
+        }
+        Vec<T, V> out;
+#pragma unroll
+        for (int j = 0; j < V; ++j) out.v[j] = from_f32<T>(best[j]);
+        const size_t o = ((size_t(n) * Ho + ho) * Wo + wo) * C + c;
+        *reinterpret_cast<Vec<T, V>*>(y + o) = out;
+        if (arg) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) arg[o + j] = bi[j];
+        }
+    }
+}
+
+// Gather-form backward, V channels per thread, optional fused ReLU mask of the
+// pool input (dx *= [x > 0]).
+template <typename T, int V>
+__global__ void maxpool_bwd_vec_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ arg,
+                                       T* __restrict__ dx, const T* __restrict__ mask, int N,
+                                       int H, int W, int C, int F, int S, int P, int Ho, int Wo) {
+    const int cg = C / V;
+    const size_t total = size_t(N) * H * W * cg;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % cg) * V;
+        size_t t = i / cg;
+        const int w = int(t % W);
+        t /= W;
+        const int h = int(t % H);
+        const int n = int(t / H);
+        const int ho0 = max(0, (h + P - F + S) / S), ho1 = min(Ho - 1, (h + P) / S);
+        const int wo0 = max(0, (w + P - F + S) / S), wo1 = min(Wo - 1, (w + P) / S);
+        float acc[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = 0.f;
+        for (int ho = ho0; ho <= ho1; ++ho) {
+            const int r = h - (ho * S - P);
+            if (r < 0 || r >= F) continue;
+            for (int wo = wo0; wo <= wo1; ++wo) {
+                const int s = w - (wo * S - P);
+                if (s < 0 || s >= F) continue;
+                const size_t o = ((size_t(n) * Ho + ho) * Wo + wo) * C + c;
+                const Vec<T, V> g = *reinterpret_cast<const Vec<T, V>*>(dy + o);
+                const uint8_t want = static_cast<uint8_t>(r * F + s);
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    if (arg[o + j] == want) acc[j] += to_f32<T>(g.v[j]);
+            }
+        }
+        const size_t io = ((size_t(n) * H + h) * W + w) * C + c;
+        if (mask) {
+            const Vec<T, V> m = *reinterpret_cast<const Vec<T, V>*>(mask + io);
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if (!(to_f32<T>(m.v[j]) > 0.f)) acc[j] = 0.f;
+        }
+        Vec<T, V> out;
+#pragma unroll
+        for (int j = 0; j < V; ++j) out.v[j] = from_f32<T>(acc[j]);
+        *reinterpret_cast<Vec<T, V>*>(dx + io) = out;
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
 cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, int h, int w,
                         int c, int f, int s, int p, cudaStream_t st) {
     const int ho = (h + 2 * p - f) / s + 1, wo = (w + 2 * p - f) / s + 1;
     const size_t total = size_t(n) * ho * wo * c;
-    TCB_DT_SWITCH(dt, T, (maxpool_fwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
-                              static_cast<const T*>(x), static_cast<T*>(y), arg, n, h, w, c, f, s,
-                              p, ho, wo)));
+    TCB_DT_SWITCH(dt, T, {
+        constexpr int V = 16 / sizeof(T);
+        if (c % V == 0 && aligned16(x) && aligned16(y))
+            maxpool_fwd_vec_kernel<T, V><<<grid_for(total / V, 2), kBlock, 0, st>>>(
+                static_cast<const T*>(x), static_cast<T*>(y), arg, n, h, w, c, f, s, p, ho, wo);
+        else
+            maxpool_fwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
+                static_cast<const T*>(x), static_cast<T*>(y), arg, n, h, w, c, f, s, p, ho, wo);
+    });
     return cudaGetLastError();
 }
 
 cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, int n, int h,
-                        int w, int c, int f, int s, int p, cudaStream_t st) {
+                        int w, int c, int f, int s, int p, cudaStream_t st, const void* mask) {
     const int ho = (h + 2 * p - f) / s + 1, wo = (w + 2 * p - f) / s + 1;
     const size_t total = size_t(n) * h * w * c;
-    TCB_DT_SWITCH(dt, T, (maxpool_bwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
-                              static_cast<const T*>(dy), arg, static_cast<T*>(dx), n, h, w, c, f,
-                              s, p, ho, wo)));
+    TCB_DT_SWITCH(dt, T, {
+        constexpr int V = 16 / sizeof(T);
+        if (c % V == 0 && aligned16(dy) && aligned16(dx) && (!mask || aligned16(mask))) {
+            maxpool_bwd_vec_kernel<T, V><<<grid_for(total / V, 2), kBlock, 0, st>>>(
+                static_cast<const T*>(dy), arg, static_cast<T*>(dx), static_cast<const T*>(mask), n,
+                h, w, c, f, s, p, ho, wo);
+        } else {
+            maxpool_bwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
+                static_cast<const T*>(dy), arg, static_cast<T*>(dx), n, h, w, c, f, s, p, ho, wo);
+            if (mask)
+                relu_mask_kernel<T><<<grid_for(total, 4), kBlock, 0, st>>>(
+                    static_cast<T*>(dx), static_cast<const T*>(mask), total);
+        }
+    });
     return cudaGetLastError();
 }
 

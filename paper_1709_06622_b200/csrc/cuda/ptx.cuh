@@ -109,6 +109,18 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* desc, uint
         : "memory");
 }
 
+// im2col-mode tensor load: coordinates {c, w, h, n} of the first filter-base
+// position, im2col offsets {ow, oh} = the filter tap.
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const void* desc, uint64_t* bar,
+                                                   int32_t c, int32_t w, int32_t h, int32_t n,
+                                                   uint16_t ow, uint16_t oh) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(desc), "r"(smem_addr(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+        : "memory");
+}
+
 // --------------------------------------------------------------- tcgen05 ----
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

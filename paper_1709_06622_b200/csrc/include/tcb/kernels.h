@@ -39,6 +39,9 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wT, con
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
                           void* workspace, cudaStream_t st);
 bool conv_tc_supported(const ConvGeom& g, ConvMode mode);
+// 1: always use the cp.async gather operand path (tests / A-B comparisons);
+// 0: pick plain-TMA / im2col-TMA / gather per geometry.
+void conv_tc_set_force_gather(int on);
 
 // ---- FP32 FFMA implicit GEMM (parity mode) ----
 size_t conv_ffma_workspace(const ConvGeom& g, ConvMode mode);
@@ -97,8 +100,10 @@ cudaError_t relu_mask_inplace(DType dt, void* g, const void* act, size_t n, cuda
 
 cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, int h, int w,
                         int c, int f, int s, int p, cudaStream_t st);
+// mask (may be NULL): the pool input; dx *= [mask > 0] (fused ReLU backward)
 cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, int n, int h,
-                        int w, int c, int f, int s, int p, cudaStream_t st);
+                        int w, int c, int f, int s, int p, cudaStream_t st,
+                        const void* mask = nullptr);
 cudaError_t avgpool_global_fwd(DType dt, const void* x, void* y, int n, int hw, int c,
                                cudaStream_t st);
 cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw, int c,

@@ -297,3 +297,9 @@ TCB_API int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_
 }
 
 TCB_API void tcb_free(void* p) { std::free(p); }
+
+TCB_API int tcb_set_conv_operand_path(int mode) {
+    if (mode < 0 || mode > 1) return fail(TCB_ERR_INVALID, "mode must be 0 (auto) or 1 (gather)");
+    conv_tc_set_force_gather(mode);
+    return TCB_OK;
+}

@@ -477,9 +477,11 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         t->launches++;
         return TCB_OK;
     }
+    // the ReLU mask fuses into the pool backward when nothing else must be added first
+    const bool fuse_mask = mask_needed && extras.empty() && con.op == Op::MaxPool;
     if (con.op == Op::MaxPool)
         TRY_CUDA(maxpool_bwd(t->dt, t->at(con.grad), t->at<uint8_t>(con.argmax), out, tgt.n, tgt.h, tgt.w,
-                             tgt.c, con.f, con.s, con.p, st));
+                             tgt.c, con.f, con.s, con.p, st, fuse_mask ? t->at(tgt.act) : nullptr));
     else
         TRY_CUDA(avgpool_global_bwd(t->dt, t->at(con.grad), out, tgt.n, tgt.h * tgt.w, tgt.c, st));
     t->launches++;
@@ -487,7 +489,7 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         TRY_CUDA(add_inplace(t->dt, out, e, elems, st));
         t->launches++;
     }
-    if (mask_needed) {
+    if (mask_needed && !fuse_mask) {
         TRY_CUDA(relu_mask_inplace(t->dt, out, t->at(tgt.act), elems, st));
         t->launches++;
     }

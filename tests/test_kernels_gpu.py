@@ -35,6 +35,10 @@ GEOMS = [
     ("plain_1x1_wide", 2, 9, 9, 520, 264, 1, 0, 1),
     ("dgrad_phase_3x3_s2_odd", 2, 15, 13, 32, 48, 3, 1, 2),
     ("dgrad_phase_5x5_s3", 2, 17, 16, 16, 24, 5, 2, 3),
+    ("im2col_ragged", 3, 9, 11, 64, 72, 3, 1, 1),
+    ("im2col_k128_c64", 2, 10, 9, 64, 128, 3, 1, 1),
+    ("im2col_s2_odd", 2, 11, 13, 64, 64, 3, 1, 2),
+    ("im2col_5x5_pad2", 2, 8, 8, 128, 64, 5, 2, 1),
 ]
 FFMA_ONLY = [
     ("lenet_conv1_c1", 4, 28, 28, 1, 20, 5, 0, 1),
@@ -63,11 +67,25 @@ def _host(t):
     return t.float().cpu().numpy()
 
 
+@pytest.fixture(params=["auto", "gather"])
+def operand_path(request):
+    """auto = 2-D TMA (1x1/s1) or im2col-mode TMA (channels % 64 == 0) where they
+    apply; gather = force the cp.async gather path. Both must agree with the oracle."""
+    import ctypes
+    lib = _dev().lib()
+    lib.tcb_set_conv_operand_path.argtypes = [ctypes.c_int]
+    lib.tcb_set_conv_operand_path(1 if request.param == "gather" else 0)
+    yield request.param
+    lib.tcb_set_conv_operand_path(0)
+
+
 @pytest.mark.parametrize("prec", ["ffma", "bf16"])
 @pytest.mark.parametrize("spec", GEOMS + FFMA_ONLY, ids=lambda s: s[0])
-def test_conv_gemm_parity(oracle, prec, spec):
+def test_conv_gemm_parity(oracle, prec, spec, operand_path):
     if prec == "bf16" and spec in FFMA_ONLY:
         pytest.skip("tensor-core path needs C, K multiples of 8")
+    if prec == "ffma" and operand_path == "gather":
+        pytest.skip("operand path only applies to the tensor-core kernel")
     dev = _dev()
     name, n, h, w, c, k, r, pad, stride = spec
     g = dev.geom(n, h, w, c, k, r, pad=pad, stride=stride)
