@@ -159,6 +159,11 @@ int tcb_trainer_describe(tcb_trainer* t, char** json_out);
 /* Device pointers of named tensors ("param", "grad", "momentum", "act:<i>",
  * "dact:<i>", "input", "labels", "logits", "wcompute"). */
 int tcb_trainer_tensor(tcb_trainer* t, const char* name, void** ptr, size_t* bytes);
+/* Per-conv-pass CUDA events inside a real step (fwd, dgrad, wgrad of every conv
+ * layer) -> per-layer CostEntry times under real cache state; JSON list, free
+ * with tcb_free. */
+int tcb_trainer_enable_layer_timing(tcb_trainer* t, int on);
+int tcb_trainer_layer_times(tcb_trainer* t, char** json_out);
 /* Count of kernels launched by the last step (for the bench's gpu_launches). */
 int tcb_trainer_launch_count(tcb_trainer* t, int* count);
 void tcb_free(void* p);

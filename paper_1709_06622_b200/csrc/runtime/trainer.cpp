@@ -20,6 +20,7 @@
 // spatial map) are flattened in layer order, [K][R][S][C] weights then bias,
 // each segment 64-element aligned; the buffer is padded to G*64 elements and
 // rank r owns [r*P/G, (r+1)*P/G).
+#include <array>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -111,6 +112,14 @@ struct tcb_trainer {
     float phase_ms[5] = {0, 0, 0, 0, 0};
     int launches = 0;
     bool initialized = false;
+    // per-conv-pass CUDA events inside a real step: [node][fwd0,fwd1,dgrad0,dgrad1,wgrad0,wgrad1]
+    bool layer_timing = false;
+    std::vector<std::array<cudaEvent_t, 6>> lev;
+    cudaStream_t lev_stream = nullptr;
+
+    void mark(size_t node, int slot, cudaStream_t st) {
+        if (layer_timing) cudaEventRecord(lev[node][slot], st);
+    }
 
     template <typename T = void>
     T* at(size_t off) const {
@@ -371,11 +380,13 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
     }
     if (t->bf16)
         TRY_CUDA(cast(DType::F32, param, DType::BF16, t->at(t->off_wc), t->param_padded, st));
-    // synthetic mini-batch: worker r uses seed + r (distinct mini-batches)
+    // synthetic mini-batch: worker r uses seed + r (distinct mini-batches);
+    // "data_rank" overrides r (tests replay one rank's batch on a single GPU)
     const Node& in = t->nodes[0];
+    const uint64_t data_seed = t->seed + static_cast<uint64_t>(t->cfg.value("data_rank", t->rank));
     TRY_CUDA(fill_uniform(DType::F32, t->at(t->off_input_f32), size_t(in.n) * in.h * in.w * in.c_logical,
-                          t->seed + t->rank, 1, -1.f, 1.f, st));
-    TRY_CUDA(fill_labels(t->at<int32_t>(t->off_labels), t->batch, t->classes, t->seed + t->rank, st));
+                          data_seed, 1, -1.f, 1.f, st));
+    TRY_CUDA(fill_labels(t->at<int32_t>(t->off_labels), t->batch, t->classes, data_seed, st));
     TRY(pack_input(t, st));
     TRY_CUDA(cudaMemsetAsync(t->at(t->off_grad), 0, t->param_padded * 4, st));
     TRY_CUDA(cudaStreamSynchronize(st));
@@ -405,12 +416,15 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                 ep.bias = nd.bias ? t->at<float>(t->off_param) + nd.boff : nullptr;
                 ep.residual = nd.residual >= 0 ? t->at(t->nodes[nd.residual].act) : nullptr;
                 ep.relu = nd.relu;
+                const size_t idx = static_cast<size_t>(&nd - t->nodes.data());
+                t->mark(idx, 0, st);
                 if (t->bf16)
                     TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
                                          ep, t->at(nd.act), st));
                 else
                     TRY_CUDA(conv_ffma_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
                                            ep, t->at<float>(nd.act), st));
+                t->mark(idx, 1, st);
                 t->launches++;
                 break;
             }
@@ -519,6 +533,7 @@ int backward(tcb_trainer* t, cudaStream_t st) {
         if (nd.op == Op::Conv) {
             const Node& x = t->nodes[nd.in];
             // weight (and bias) gradient straight into the flat PS buffer
+            t->mark(i, 4, st);
             if (t->bf16)
                 TRY_CUDA(conv_tc_wgrad(nd.g, t->at(nd.grad), t->at(x.act), grad + nd.woff, t->at(t->off_ws), st));
             else
@@ -530,7 +545,12 @@ int backward(tcb_trainer* t, cudaStream_t st) {
                                     t->at<float>(t->off_colsum), st));
                 t->launches += 2;
             }
-            if (nd.need_dgrad) TRY(backward_contribution(t, i, nd.in, st));
+            t->mark(i, 5, st);
+            if (nd.need_dgrad) {
+                t->mark(i, 2, st);
+                TRY(backward_contribution(t, i, nd.in, st));
+                t->mark(i, 3, st);
+            }
         } else if (nd.op == Op::MaxPool || nd.op == Op::AvgPool) {
             if (t->nodes[nd.in].op != Op::Input) TRY(backward_contribution(t, i, nd.in, st));
         }
@@ -627,6 +647,9 @@ TCB_API int tcb_trainer_destroy(tcb_trainer* t) {
     if (t->comm) ncclCommDestroy(t->comm);
     for (cudaEvent_t& e : t->ph.e)
         if (e) cudaEventDestroy(e);
+    for (auto& a : t->lev)
+        for (cudaEvent_t e : a)
+            if (e) cudaEventDestroy(e);
     if (t->arena) cudaFree(t->arena);
     delete t;
     return TCB_OK;
@@ -716,6 +739,47 @@ TCB_API int tcb_trainer_phase_times(tcb_trainer* t, float* ms5) {
     cudaEvent_t* e = t->ph.e;
     TRY_CUDA(cudaEventSynchronize(e[5]));
     for (int i = 0; i < 5; ++i) TRY_CUDA(cudaEventElapsedTime(&ms5[i], e[i], e[i + 1]));
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_enable_layer_timing(tcb_trainer* t, int on) {
+    if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
+    if (on && t->lev.empty()) {
+        t->lev.resize(t->nodes.size());
+        for (auto& a : t->lev)
+            for (cudaEvent_t& e : a) TRY_CUDA(cudaEventCreate(&e));
+    }
+    t->layer_timing = on != 0;
+    return TCB_OK;
+}
+
+// JSON [{name, conv_index, flop, fwd_ms, dgrad_ms|null, wgrad_ms}] of the last step
+// (flop = 2*N*Ho*Wo*K*C*R*S with logical channel counts).
+TCB_API int tcb_trainer_layer_times(tcb_trainer* t, char** json_out) {
+    if (!t || !json_out) return fail(TCB_ERR_INVALID, "NULL argument");
+    if (t->lev.empty()) return fail(TCB_ERR_INVALID, "layer timing never enabled");
+    json out = json::array();
+    for (size_t i = 0; i < t->nodes.size(); ++i) {
+        const Node& nd = t->nodes[i];
+        if (nd.op != Op::Conv) continue;
+        auto& e = t->lev[i];
+        TRY_CUDA(cudaEventSynchronize(e[5]));
+        float f = 0, w = 0, d = 0;
+        TRY_CUDA(cudaEventElapsedTime(&f, e[0], e[1]));
+        TRY_CUDA(cudaEventElapsedTime(&w, e[4], e[5]));
+        if (nd.need_dgrad) TRY_CUDA(cudaEventElapsedTime(&d, e[2], e[3]));
+        json r;
+        r["name"] = nd.name;
+        r["conv_index"] = nd.conv_index;
+        r["flop"] = 2.0 * nd.n * nd.h * nd.w * nd.c_logical * t->nodes[nd.in].c_logical * nd.g.r * nd.g.s;
+        r["fwd_ms"] = f;
+        r["dgrad_ms"] = nd.need_dgrad ? json(d) : json(nullptr);
+        r["wgrad_ms"] = w;
+        out.push_back(std::move(r));
+    }
+    const std::string s = out.dump();
+    *json_out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*json_out, s.c_str(), s.size() + 1);
     return TCB_OK;
 }
 

@@ -34,6 +34,8 @@ def _lib():
         L.tcb_trainer_tensor.argtypes = [_vp, ctypes.c_char_p, ctypes.POINTER(_vp),
                                          ctypes.POINTER(ctypes.c_size_t)]
         L.tcb_trainer_launch_count.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
+        L.tcb_trainer_enable_layer_timing.argtypes = [_vp, ctypes.c_int]
+        L.tcb_trainer_layer_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p)]
         L.tcb_free.argtypes = [_vp]
         _bound = True
     return L
@@ -101,6 +103,17 @@ class Trainer:
         buf = (ctypes.c_float * 5)()
         device.check(_lib().tcb_trainer_phase_times(self.handle, buf))
         return dict(zip(self.PHASES, list(buf)))
+
+    def enable_layer_timing(self, on=True):
+        device.check(_lib().tcb_trainer_enable_layer_timing(self.handle, int(on)))
+
+    def layer_times(self) -> list:
+        """Per-conv [fwd, dgrad, wgrad] ms measured inside the last step."""
+        out = ctypes.c_char_p()
+        device.check(_lib().tcb_trainer_layer_times(self.handle, ctypes.byref(out)))
+        d = json.loads(out.value.decode())
+        _lib().tcb_free(ctypes.cast(out, _vp))
+        return d
 
     def launch_count(self) -> int:
         n = ctypes.c_int()

@@ -1,0 +1,26 @@
+"""Summarise an ncu --csv launch list (gpu__time_duration.sum) by kernel name."""
+import collections
+import csv
+import re
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hdr, data = None, []
+for r in rows:
+    if r and r[0] == "ID":
+        hdr = r
+        continue
+    if hdr and len(r) == len(hdr):
+        data.append(dict(zip(hdr, r)))
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+agg = collections.defaultdict(lambda: [0, 0.0])
+tot = 0.0
+for d in data:
+    key = re.sub(r"\(.*", "", d["Kernel Name"]).replace("void ", "")[:70]
+    us = float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1.0)
+    agg[key][0] += 1
+    agg[key][1] += us
+    tot += us
+print(f"{len(data)} launches, {tot / 1000:.3f} ms of kernel time")
+for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"{us / 1000:8.3f} ms {us / tot * 100:5.1f}%  n={n:4d}  {k}")
