@@ -87,9 +87,12 @@ def test_two_gpu_ps_step_bit_exact(oracle, n_ps):
     w_exp, _ = oracle.sgd(w0, s, np.zeros_like(w0), cfg["lr"], cfg["momentum"],
                           cfg["weight_decay"], 0.5)
     res = _run_world(cfg, 2)
+    # the world-2 flat buffer is padded to 2*64 elements; the padding stays zero
+    padded = res[0][1].size
+    w_exp = np.concatenate([w_exp, np.zeros(padded - w_exp.size, np.float32)])
     wc_exp = oracle.round_bf16(w_exp)
     owners = 2 if n_ps == 0 else 1
-    per = res[0][0] if n_ps == 0 else w0.size
+    per = res[0][0] if n_ps == 0 else padded
     for r in range(owners):
         shard, param, _ = res[r]
         sl = slice(r * per, (r + 1) * per)
