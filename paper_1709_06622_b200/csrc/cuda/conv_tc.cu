@@ -36,8 +36,8 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;  // bf16 elements per stage along the reduction
 constexpr int kProducerThreads = 128;
-constexpr int kEpilogueThreads = 128;
-constexpr int kMmaWarp = 8;
+constexpr int kEpilogueThreads = 256;  // warps 4-11
+constexpr int kMmaWarp = 12;
 constexpr int kThreads = kProducerThreads + kEpilogueThreads + 32;
 
 template <int BN>
@@ -218,9 +218,32 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
     return v;
 }
 
+// Side inputs of one 32-column epilogue chunk (residual / ReLU-mask rows),
+// loaded one chunk ahead so their HBM latency overlaps the TMEM load and math
+// of the previous chunk.
+struct SideIn {
+    uint4 r[4];
+    uint4 k[4];
+};
+
+__device__ __forceinline__ void load_side(const Params& p, size_t row, int col0, bool valid,
+                                          SideIn& f) {
+    if (!valid || col0 + 32 > p.s.Ncol) return;  // tail chunks take the scalar path
+    const size_t base = row * p.s.Ncol + col0;
+    if (p.residual) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) f.r[g] = __ldg(reinterpret_cast<const uint4*>(p.residual + base) + g);
+    }
+    if (p.mask) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) f.k[g] = __ldg(reinterpret_cast<const uint4*>(p.mask + base) + g);
+    }
+}
+
 template <ConvMode MODE>
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord& tc, int m,
-                                               size_t row, int col0, const uint32_t (&acc)[32]) {
+                                               size_t row, int col0, const uint32_t (&acc)[32],
+                                               const SideIn& side) {
     const ConvShape& s = p.s;
     if (m >= s.M || col0 >= s.Ncol) return;
     if constexpr (MODE == ConvMode::Wgrad) {
@@ -252,7 +275,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
                 }
                 if (p.residual) {
                     float r[8];
-                    unpack8(__ldg(reinterpret_cast<const uint4*>(p.residual + base + 8 * g)), r);
+                    unpack8(side.r[g], r);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) v[i] += r[i];
                 }
@@ -262,7 +285,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
                 }
                 if (p.mask) {
                     float mk[8];
-                    unpack8(__ldg(reinterpret_cast<const uint4*>(p.mask + base + 8 * g)), mk);
+                    unpack8(side.k[g], mk);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) v[i] = mk[i] > 0.f ? v[i] : 0.f;
                 }
@@ -527,25 +550,39 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
     } else {
         // ================================================= epilogue ======
-        const int ew = warp - 4;  // TMEM lane quarter
-        const int row = ew * 32 + (tid & 31);
+        // Two warps per TMEM lane quarter (a warp may only touch lanes
+        // 32*(warp%4)..+31); each takes half of the tile's 32-column chunks.
+        const int quarter = warp & 3;
+        const int half = (warp - 4) >> 2;
+        constexpr int kChunks = BN / 32, kHalfChunks = kChunks / 2;
+        const int c_begin = half * kHalfChunks, c_end = c_begin + kHalfChunks;
+        const int row = quarter * 32 + (tid & 31);
         int it = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
             const TileCoord tc = tile_coord(p, t);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int m = tc.mt * BM + row;
-            const size_t orow = m < p.s.M ? out_row<MODE>(p, m) : 0;
+            const bool mvalid = m < p.s.M;
+            const size_t orow = mvalid ? out_row<MODE>(p, m) : 0;
+            // first chunk's residual / mask loads are in flight while the MMAs finish
+            SideIn cur{}, nxt{};
+            if constexpr (MODE != ConvMode::Wgrad)
+                load_side(p, orow, tc.nt * BN + c_begin * 32, mvalid, cur);
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = c_begin; c < c_end; ++c) {
+                if constexpr (MODE != ConvMode::Wgrad) {
+                    if (c + 1 < c_end) load_side(p, orow, tc.nt * BN + (c + 1) * 32, mvalid, nxt);
+                }
                 uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                             acc * BN + c * 32,
                                         v);
                 ptx::tmem_ld_wait();
-                epilogue_chunk<MODE>(p, tc, m, orow, tc.nt * BN + c * 32, v);
+                epilogue_chunk<MODE>(p, tc, m, orow, tc.nt * BN + c * 32, v, cur);
+                cur = nxt;
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
