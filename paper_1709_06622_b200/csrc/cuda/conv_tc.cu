@@ -314,7 +314,10 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
 //   kIm2col: the activation operand (x for fwd and wgrad, dy for dgrad) is an
 //            im2col-mode TMA load (one instruction per 64-channel tap slice),
 //            everything else 2-D TMA; one producer thread.
-constexpr int kGather = 0, kPlain = 1, kIm2col = 2;
+//   kIm2colC8: fwd with C == 8 (the padded RGB stem): eight 8-channel im2col
+//            boxes per k-block (one per filter tap), each 128 pixels x 16 B,
+//            landing as no-swizzle 8x16B core matrices (LBO 2 KB, SBO 128 B).
+constexpr int kGather = 0, kPlain = 1, kIm2col = 2, kIm2colC8 = 3;
 
 template <ConvMode MODE, int BN, int LOAD>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ Params p) {
@@ -364,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 const TileCoord tc = tile_coord(p, t);
                 // im2col base position of the tile's first GEMM row (fwd / dgrad)
                 int bn = 0, bw = 0, bh = 0;
-                if constexpr (LOAD == kIm2col && MODE != ConvMode::Wgrad) {
+                if constexpr ((LOAD == kIm2col || LOAD == kIm2colC8) && MODE != ConvMode::Wgrad) {
                     uint32_t n, rem, a, b;
                     const uint32_t m0 = static_cast<uint32_t>(tc.mt * BM);
                     if constexpr (MODE == ConvMode::Fwd) {
@@ -415,6 +418,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     } else {
                         if constexpr (LOAD == kPlain) {
                             ptx::tma_load_2d(a_smem, &p.tmap_a, &full[stage], kb * BK, tc.mt * BM);
+                        } else if constexpr (LOAD == kIm2colC8) {
+                            const int taps = s.R * s.S;
+#pragma unroll
+                            for (int jj = 0; jj < 8; ++jj) {
+                                int tap = kb * 8 + jj;
+                                if (tap >= taps) tap = 0;  // K tail: B rows are zero there
+                                uint32_t r, sx;
+                                s.d_s.divmod(static_cast<uint32_t>(tap), r, sx);
+                                ptx::tma_load_im2col_4d(a_smem + jj * 2048, &p.tmap_a, &full[stage], 0,
+                                                        bw, bh, bn, static_cast<uint16_t>(sx),
+                                                        static_cast<uint16_t>(r));
+                            }
                         } else {
                             const uint32_t kk0 = static_cast<uint32_t>(kb * BK);
                             uint32_t tap, c0, r, sx;
@@ -531,6 +546,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                         if constexpr (MODE == ConvMode::Wgrad) {
                             ad = ptx::sw128_desc(a_addr + k * 2048, 8192, 1024);
                             bd = ptx::sw128_desc(b_addr + k * 2048, 8192, 1024);
+                        } else if constexpr (LOAD == kIm2colC8) {
+                            ad = ptx::interleave_desc(a_addr + k * 4096, 2048, 128);
+                            bd = ptx::sw128_desc(b_addr + k * 32, 16, 1024);
                         } else {
                             ad = ptx::sw128_desc(a_addr + k * 32, 16, 1024);
                             bd = ptx::sw128_desc(b_addr + k * 32, 16, 1024);
@@ -671,6 +689,9 @@ bool build_maps(Params& p, const void* a_matrix, const void* b_matrix, int bn) {
     // weight operand: row-major [Ncol][Kdim] bf16, boxes of BN rows x 64
     if (!make_tmap_bf16_2d(&p.tmap_b, b_matrix, s.Ncol, s.Kdim, bn)) return false;
     if (LOAD == kPlain) return make_tmap_bf16_2d(&p.tmap_a, a_matrix, s.M, s.Kdim, BM);
+    if (LOAD == kIm2colC8)
+        return make_tmap_im2col_bf16(&p.tmap_a, a_matrix, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
+                                     s.pw - (s.S - 1), s.ph - (s.R - 1), s.sw, s.sh, BM, 8);
     if (LOAD == kIm2col) {
         if (MODE == ConvMode::Fwd)
             return make_tmap_im2col_bf16(&p.tmap_a, a_matrix, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
@@ -731,6 +752,10 @@ cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cuda
                                : plain_geometry(p.s);
         if (plain) return dispatch_bn<MODE, kPlain>(p, a_matrix, b_matrix, st);
         if (im2col_ok<MODE>(p)) return dispatch_bn<MODE, kIm2col>(p, a_matrix, b_matrix, st);
+        if constexpr (MODE == ConvMode::Fwd) {
+            if (p.s.C == 8 && p.s.R <= 16 && p.s.S <= 16 && p.s.ph <= 15 && p.s.pw <= 15)
+                return dispatch_bn<MODE, kIm2colC8>(p, a_matrix, b_matrix, st);
+        }
     }
     return dispatch_bn<MODE, kGather>(p, a_matrix, b_matrix, st);
 }

@@ -211,6 +211,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_byte
     return d;
 }
 
+// No-swizzle ("interleaved") descriptor: 8-row x 16-byte core matrices,
+// K-direction core matrices LBO apart, 8-row groups SBO apart.
+__device__ __forceinline__ uint64_t interleave_desc(uint32_t saddr, uint32_t lbo_bytes,
+                                                    uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // version; layout type 0 = SWIZZLE_NONE
+    return d;
+}
+
 // Instruction descriptor, dense kind::f16 / kind::tf32 with fp32 accumulate.
 //   fmt: 0 = f16, 1 = bf16, 2 = tf32;  major: 0 = K-major, 1 = MN-major.
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t fmt, uint32_t m, uint32_t n,

@@ -39,6 +39,8 @@ GEOMS = [
     ("im2col_k128_c64", 2, 10, 9, 64, 128, 3, 1, 1),
     ("im2col_s2_odd", 2, 11, 13, 64, 64, 3, 1, 2),
     ("im2col_5x5_pad2", 2, 8, 8, 128, 64, 5, 2, 1),
+    ("c8_3x3", 2, 12, 10, 8, 24, 3, 1, 1),
+    ("c8_11x11_s4", 2, 35, 35, 8, 96, 11, 2, 4),
 ]
 FFMA_ONLY = [
     ("lenet_conv1_c1", 4, 28, 28, 1, 20, 5, 0, 1),
