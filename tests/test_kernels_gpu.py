@@ -200,3 +200,49 @@ def test_avgpool_and_softmax_parity(oracle, dtype):
     rl, rdl = oracle.softmax_xent(z, lab, 17, 1000)
     assert abs(float(loss) - rl) <= 1e-5 * abs(rl)
     assert rel_err(_host(dl), rdl) <= tol
+
+
+# 3x3 stride-1 layers of the BASELINE configs for the Winograd / FFT families
+FAMILY_GEOMS = [
+    ("alex_conv3", 2, 13, 13, 256, 384, 3, 1, 1),
+    ("rn50_3x3", 2, 14, 14, 64, 64, 3, 1, 1),
+    ("vgg_3x3_odd", 2, 15, 9, 32, 48, 3, 1, 1),
+    ("pad0_3x3", 2, 10, 11, 16, 24, 3, 0, 1),
+]
+
+
+@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+@pytest.mark.parametrize("spec", FAMILY_GEOMS, ids=lambda s: s[0])
+def test_conv_winograd_parity(oracle, prec, spec):
+    """Winograd F(2x2,3x3): fwd / dgrad / wgrad vs the direct-conv oracle."""
+    dev = _dev()
+    name, n, h, w, c, k, r, pad, stride = spec
+    g = dev.geom(n, h, w, c, k, r, pad=pad, stride=stride)
+    gd = g.as_dict()
+    plan = dev.ConvPlan(g, "winograd", prec)
+    bf = prec == "bf16"
+    dt = plan.dtype
+    x = _rand(oracle, (n, h, w, c), 1, 1.0, bf)
+    wt = _rand(oracle, (k, r, r, c), 2, (6.0 / (c * 9)) ** 0.5, bf)
+    bias = _rand(oracle, (k,), 3, 0.1)
+    res = _rand(oracle, (n, g.ho, g.wo, k), 4, 0.5, bf)
+    dy = _rand(oracle, (n, g.ho, g.wo, k), 5, 1.0, bf)
+    mask = _rand(oracle, (n, h, w, c), 6, 1.0, bf)
+    tol = TOL[prec]
+    y = plan.fwd(_to_dev(x, dt), _to_dev(wt, dt), bias=_to_dev(bias, torch.float32),
+                 residual=_to_dev(res, dt), relu=True)
+    assert rel_err(_host(y), oracle.conv_fwd(gd, x, wt, bias=bias, residual=res, relu=True)) <= tol
+    dx = plan.dgrad(_to_dev(dy, dt), _to_dev(wt, dt), mask=_to_dev(mask, dt))
+    assert rel_err(_host(dx), oracle.conv_dgrad(gd, dy, wt, mask=mask)) <= tol
+    dw, db = plan.wgrad(_to_dev(dy, dt), _to_dev(x, dt), want_db=True)
+    refw, refb = oracle.conv_wgrad(gd, dy, x, want_db=True)
+    assert rel_err(_host(dw), refw) <= tol, (name, rel_err(_host(dw), refw))
+    assert rel_err(_host(db), refb) <= tol
+
+
+def test_winograd_rejects_inapplicable_geometry():
+    dev = _dev()
+    with pytest.raises(dev.Unsupported):
+        dev.ConvPlan(dev.geom(2, 14, 14, 64, 64, 3, pad=1, stride=2), "winograd", "bf16")
+    with pytest.raises(dev.Unsupported):
+        dev.ConvPlan(dev.geom(2, 14, 14, 64, 64, 5, pad=2), "winograd", "bf16")
