@@ -240,6 +240,53 @@ def test_conv_winograd_parity(oracle, prec, spec):
     assert rel_err(_host(db), refb) <= tol
 
 
+FFT_GEOMS = FAMILY_GEOMS + [
+    ("alex_conv2_5x5", 2, 27, 27, 96, 256, 5, 2, 1),
+    ("incep_1x7", 2, 17, 17, 32, 48, (1, 7), (0, 3), 1),
+    ("incep_7x1", 2, 17, 17, 32, 48, (7, 1), (3, 0), 1),
+]
+
+
+@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+@pytest.mark.parametrize("spec", FFT_GEOMS, ids=lambda s: s[0])
+def test_conv_fft_parity(oracle, prec, spec):
+    """Tiled FFT convolution (overlap-save 8x8): fwd / dgrad / wgrad vs the oracle."""
+    dev = _dev()
+    name, n, h, w, c, k, r, pad, stride = spec
+    rr, ss = (r, r) if isinstance(r, int) else r
+    ph, pw = (pad, pad) if isinstance(pad, int) else pad
+    g = dev.geom(n, h, w, c, k, rr, ss, pad=ph, pad_w=pw, stride=stride)
+    gd = g.as_dict()
+    plan = dev.ConvPlan(g, "fft", prec)
+    bf = prec == "bf16"
+    dt = plan.dtype
+    x = _rand(oracle, (n, h, w, c), 1, 1.0, bf)
+    wt = _rand(oracle, (k, rr, ss, c), 2, (6.0 / (c * rr * ss)) ** 0.5, bf)
+    bias = _rand(oracle, (k,), 3, 0.1)
+    res = _rand(oracle, (n, g.ho, g.wo, k), 4, 0.5, bf)
+    dy = _rand(oracle, (n, g.ho, g.wo, k), 5, 1.0, bf)
+    mask = _rand(oracle, (n, h, w, c), 6, 1.0, bf)
+    tol = TOL[prec]
+    y = plan.fwd(_to_dev(x, dt), _to_dev(wt, dt), bias=_to_dev(bias, torch.float32),
+                 residual=_to_dev(res, dt), relu=True)
+    e = rel_err(_host(y), oracle.conv_fwd(gd, x, wt, bias=bias, residual=res, relu=True))
+    assert e <= tol, (name, "fwd", e)
+    dx = plan.dgrad(_to_dev(dy, dt), _to_dev(wt, dt), mask=_to_dev(mask, dt))
+    e = rel_err(_host(dx), oracle.conv_dgrad(gd, dy, wt, mask=mask))
+    assert e <= tol, (name, "dgrad", e)
+    dw, db = plan.wgrad(_to_dev(dy, dt), _to_dev(x, dt), want_db=True)
+    refw, refb = oracle.conv_wgrad(gd, dy, x, want_db=True)
+    e = rel_err(_host(dw), refw)
+    assert e <= tol, (name, "wgrad", e)
+    assert rel_err(_host(db), refb) <= tol
+
+
+def test_fft_rejects_strided_geometry():
+    dev = _dev()
+    with pytest.raises(dev.Unsupported):
+        dev.ConvPlan(dev.geom(2, 27, 27, 96, 256, 11, pad=2, stride=4), "fft", "bf16")
+
+
 def test_winograd_rejects_inapplicable_geometry():
     dev = _dev()
     with pytest.raises(dev.Unsupported):
