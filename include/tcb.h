@@ -129,6 +129,15 @@ int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_dtype, v
                      size_t n, float lr, float momentum, float weight_decay, float grad_scale,
                      void* stream);
 
+/* ------------------------------------------------------------ profiler -- */
+/* Measures every (conv layer, algorithm, mini-batch) on this GPU and returns
+ * the reference's cost catalog: rows of traincap::CostEntry
+ * (/root/reference/proj/include/traincap/catalog.hpp:19-27) as CSV in the
+ * reference's format (time_seconds = median fwd+dgrad+wgrad, memory_bits =
+ * 8 * workspace bytes; inapplicable algorithms produce no row). Request and
+ * reply are JSON (see csrc/runtime/profiler.cpp); free the reply with tcb_free. */
+int tcb_profile_catalog(const char* request_json, char** reply_out);
+
 /* ------------------------------------------------------------- trainer -- */
 /* A whole data-parallel training step on one GPU: fwd chain -> loss ->
  * bwd (dgrad + wgrad into the flat PS gradient buffer) -> PS aggregation
