@@ -4,12 +4,16 @@ Runs every request in tests/planner_cases.py through oracle/_ref/
 libtraincap_ref.so (the unmodified reference sources, built by
 oracle/Makefile) and stores request/reply pairs, so the parity suite can
 check this build's planner on machines without /root/reference (the GPU box).
+B200-catalog cases run in a child process with a time limit: the reference's
+branch-and-bound is exponential under binding bounds, and a case
+it cannot finish is recorded as such instead of stalling the generator.
 
     make -C oracle ref && python tests/golden/make_planner_golden.py
 """
 import ctypes
 import gzip
 import json
+import multiprocessing as mp
 import os
 import sys
 
@@ -22,11 +26,33 @@ from paper_1709_06622_b200.planner import Planner  # noqa: E402
 import planner_cases  # noqa: E402
 
 FIXTURE_TOKEN = "@FIXTURES@"
+REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libtraincap_ref.so")
+TIME_LIMIT_S = 60
+
+
+def _ref():
+    return Planner(ctypes.CDLL(REF_LIB), prefix="tcref_")
+
+
+def _child(req, q):
+    q.put(_ref().raw(**req))
+
+
+def ref_with_limit(req):
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    p = ctx.Process(target=_child, args=(req, q))
+    p.start()
+    p.join(TIME_LIMIT_S)
+    if p.is_alive():
+        p.kill()
+        p.join()
+        return None
+    return q.get()
 
 
 def main():
-    ref = Planner(ctypes.CDLL(os.path.join(ROOT, "oracle", "_ref", "libtraincap_ref.so")),
-                  prefix="tcref_")
+    ref = _ref()
     fixture_dir = planner_cases.FIXTURES
     records = []
     for req in planner_cases.build_cases():
@@ -35,11 +61,19 @@ def main():
         reply = ref.raw(**req)
         text = json.dumps({"request": req, "reply": reply}).replace(fixture_dir, FIXTURE_TOKEN)
         records.append(json.loads(text))
+    b200, slow = [], 0
+    for req in planner_cases.build_b200_cases():
+        reply = ref_with_limit(req)
+        if reply is None:
+            slow += 1
+            b200.append({"request": req, "reply": None, "reference": f"did not finish in {TIME_LIMIT_S} s"})
+        else:
+            b200.append({"request": req, "reply": reply})
     out = os.path.join(HERE, "planner_golden.json.gz")
     with gzip.open(out, "wt") as f:
         json.dump({"generator": "oracle/_ref/libtraincap_ref.so (reference planner)",
-                   "records": records}, f)
-    print(f"wrote {len(records)} records to {out}")
+                   "records": records, "b200_records": b200}, f)
+    print(f"wrote {len(records)} + {len(b200)} B200 records ({slow} beyond the reference's time limit)")
 
 
 if __name__ == "__main__":

@@ -304,6 +304,41 @@ def build_cases() -> list[dict]:
     return cases
 
 
+B200_DIR = os.path.join(HERE, "golden", "b200")
+
+
+def b200(name: str) -> str:
+    with open(os.path.join(B200_DIR, name)) as f:
+        return f.read()
+
+
+def build_b200_cases() -> list[dict]:
+    """Decisions re-driven by catalogs MEASURED on B200 (scripts/b200_plan.py):
+    the mini-batch sweep at several GPU memory sizes (from 180 GB down to sizes
+    where feature maps no longer fit) and Eq 6 selection on the 94-layer
+    Inception-v3 catalog under loose and binding workspace bounds."""
+    cases = []
+    for tag in ("alexnet", "vgg16"):
+        net, cat = b200(f"b200_{tag}.net"), b200(f"b200_catalog_{tag}.csv")
+        for gbits in (180 * 10**9 * 8, 12 * 2**30 * 8, 4 * 2**30 * 8, 2 * 2**30 * 8, 2**30 * 8,
+                      3 * 10**8 * 8):
+            cases.append({"op": "plan_batch_size", "network": net, "catalog": cat,
+                          "gpu_bits": gbits, "dataset": 1_281_167})
+    inc = b200("b200_catalog_inception_v3.csv")
+    lo = None
+    import csv as _csv
+    import io as _io
+    rows = list(_csv.DictReader(_io.StringIO(inc)))
+    per = {}
+    for r in rows:
+        per.setdefault(int(r["layer_id"]), []).append(int(r["memory_bits"]))
+    lo = sum(min(v) for v in per.values())
+    hi = sum(max(v) for v in per.values())
+    for bound in (lo - 1, lo, lo + (hi - lo) // 100, lo + (hi - lo) // 10, lo + (hi - lo) // 2, hi):
+        cases.append({"op": "solve_catalog", "catalog": inc, "batch": 128, "bound": bound})
+    return cases
+
+
 def build_plan_cases(fixture_dir: str) -> list[dict]:
     """Full run_plan / renderer cases (file-path based)."""
     net = os.path.join(fixture_dir, "alexnet.net")

@@ -43,6 +43,25 @@ def test_golden_replay(planner_lib):
     assert not mismatches, f"{len(mismatches)} mismatches, first: {mismatches[0]}"
 
 
+def test_b200_catalog_decisions_match_reference(planner_lib):
+    """Mini-batch choice and per-layer algorithm selection re-driven by catalogs
+    measured on B200 (tests/golden/b200/*.csv) are bit-identical to the
+    reference planner's on the same files."""
+    with gzip.open(GOLDEN, "rt") as f:
+        recs = json.load(f)["b200_records"]
+    assert len(recs) >= 18
+    checked = 0
+    for rec in recs:
+        if rec["reply"] is None:
+            continue
+        assert planner_lib.raw(**rec["request"]) == rec["reply"], rec["request"]["op"]
+        checked += 1
+    assert checked >= 18
+    # the 180 GB AlexNet-227 plan: largest batch, implicit GEMM everywhere
+    plan = [r["reply"] for r in recs if r["request"]["op"] == "plan_batch_size"][0]
+    assert plan["recommended"] == 512
+
+
 def test_golden_covers_every_error_class():
     kinds = {r["reply"]["error"]["type"] for r in _records() if "error" in r["reply"]}
     assert {"ParseError", "DuplicateKeyError", "IncompleteCatalogError", "OverflowError",
