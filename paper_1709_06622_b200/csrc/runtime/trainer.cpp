@@ -61,6 +61,7 @@ struct Node {
     size_t woff = 0, boff = 0, wcount = 0;  // flat param offsets (elements)
     float init_scale = 0.f;
     std::string algo = "gemm";
+    int algo_id = 0;  // TCB_ALGO_*
     // pool
     int f = 0, s = 0, p = 0;
     // arena offsets (bytes)
@@ -212,6 +213,14 @@ int build_graph(tcb_trainer* t) {
                 throw std::runtime_error("layer " + nd.name + ": bad geometry " + why);
             if (t->bf16 && !conv_tc_supported(nd.g, ConvMode::Fwd))
                 throw std::runtime_error("layer " + nd.name + ": bf16 path needs C % 8 == 0");
+            // the planner's per-layer algorithm (Selection.assignment) — obeyed as given
+            nd.algo_id = nd.algo == "gemm" ? TCB_ALGO_GEMM
+                         : nd.algo == "winograd" ? TCB_ALGO_WINOGRAD
+                         : nd.algo == "fft" ? TCB_ALGO_FFT : -1;
+            if (nd.algo_id < 0) throw std::runtime_error("layer " + nd.name + ": unknown algo " + nd.algo);
+            if (!algo_applies(nd.g, nd.algo_id, t->bf16 ? TCB_PREC_BF16 : TCB_PREC_FFMA_FP32))
+                throw std::runtime_error("layer " + nd.name + ": algorithm " + nd.algo +
+                                         " does not apply to this geometry");
             if (nd.residual >= 0) {
                 const Node& r = t->nodes.at(nd.residual);
                 if (r.h != nd.h || r.w != nd.w || r.c != nd.c)
@@ -320,10 +329,17 @@ int allocate(tcb_trainer* t) {
         if (nd.op != Op::Input && nd.grad_alias < 0) nd.grad = b.take(elems * es);
         if (nd.op == Op::MaxPool) nd.argmax = b.take(elems);
         if (nd.op == Op::Conv) {
-            ws = std::max(ws, t->bf16 ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
-                                      : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
+            if (nd.algo_id == TCB_ALGO_GEMM) {
+                ws = std::max(ws, t->bf16 ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
+                                          : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
+                if (t->bf16 && nd.need_dgrad) nd.wT = b.take(nd.wcount * 2);
+            } else {
+                // Winograd / FFT transformed planes; one shared region, passes run in order
+                for (ConvMode m : {ConvMode::Fwd, ConvMode::Dgrad, ConvMode::Wgrad})
+                    ws = std::max(ws, nd.algo_id == TCB_ALGO_WINOGRAD ? winograd_workspace(nd.g, m, t->dt)
+                                                                      : fft_workspace(nd.g, m));
+            }
             if (nd.bias) colsum = std::max(colsum, column_sum_workspace(nd.n * nd.h * nd.w, nd.g.k));
-            if (t->bf16 && nd.need_dgrad) nd.wT = b.take(nd.wcount * 2);
         }
     }
     for (Node& nd : t->nodes)
@@ -398,7 +414,7 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
 int refresh_transposes(tcb_trainer* t, cudaStream_t st) {
     if (!t->bf16) return TCB_OK;
     for (const Node& nd : t->nodes) {
-        if (nd.op != Op::Conv || !nd.need_dgrad) continue;
+        if (nd.op != Op::Conv || !nd.need_dgrad || nd.algo_id != TCB_ALGO_GEMM) continue;
         TRY_CUDA(pack_dgrad_weights(DType::BF16, t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
                                     t->at(nd.wT), nd.g, st));
         t->launches++;
@@ -418,7 +434,13 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                 ep.relu = nd.relu;
                 const size_t idx = static_cast<size_t>(&nd - t->nodes.data());
                 t->mark(idx, 0, st);
-                if (t->bf16)
+                const void* wgt = t->bf16 ? static_cast<const void*>(t->at<__nv_bfloat16>(t->off_wc) + nd.woff)
+                                          : static_cast<const void*>(t->at<float>(t->off_param) + nd.woff);
+                if (nd.algo_id == TCB_ALGO_WINOGRAD)
+                    TRY_CUDA(winograd_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
+                else if (nd.algo_id == TCB_ALGO_FFT)
+                    TRY_CUDA(fft_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
+                else if (t->bf16)
                     TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
                                          ep, t->at(nd.act), st));
                 else
@@ -483,7 +505,13 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         Epilogue ep;
         ep.residual = residual;
         ep.mask = mask_needed ? t->at(tgt.act) : nullptr;
-        if (t->bf16)
+        const void* cw = t->bf16 ? static_cast<const void*>(t->at<__nv_bfloat16>(t->off_wc) + con.woff)
+                                 : static_cast<const void*>(t->at<float>(t->off_param) + con.woff);
+        if (con.algo_id == TCB_ALGO_WINOGRAD)
+            TRY_CUDA(winograd_dgrad(con.g, t->dt, t->at(con.grad), cw, ep, out, t->at(t->off_ws), st));
+        else if (con.algo_id == TCB_ALGO_FFT)
+            TRY_CUDA(fft_dgrad(con.g, t->dt, t->at(con.grad), cw, ep, out, t->at(t->off_ws), st));
+        else if (t->bf16)
             TRY_CUDA(conv_tc_dgrad(con.g, t->at(con.grad), t->at(con.wT), ep, out, st));
         else
             TRY_CUDA(conv_ffma_dgrad(con.g, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
@@ -534,7 +562,13 @@ int backward(tcb_trainer* t, cudaStream_t st) {
             const Node& x = t->nodes[nd.in];
             // weight (and bias) gradient straight into the flat PS buffer
             t->mark(i, 4, st);
-            if (t->bf16)
+            if (nd.algo_id == TCB_ALGO_WINOGRAD)
+                TRY_CUDA(winograd_wgrad(nd.g, t->dt, t->at(nd.grad), t->at(x.act), grad + nd.woff,
+                                        t->at(t->off_ws), st));
+            else if (nd.algo_id == TCB_ALGO_FFT)
+                TRY_CUDA(fft_wgrad(nd.g, t->dt, t->at(nd.grad), t->at(x.act), grad + nd.woff,
+                                   t->at(t->off_ws), st));
+            else if (t->bf16)
                 TRY_CUDA(conv_tc_wgrad(nd.g, t->at(nd.grad), t->at(x.act), grad + nd.woff, t->at(t->off_ws), st));
             else
                 TRY_CUDA(conv_ffma_wgrad(nd.g, t->at<float>(nd.grad), t->at<float>(x.act), grad + nd.woff,

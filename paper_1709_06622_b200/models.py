@@ -182,6 +182,11 @@ def from_net(text: str, batch: int, classes: int | None = None, **opts):
             b.maxpool(f, s, p)
         elif tok[0] == "fc":
             fcs.append(int(tok[1]))
+    # A first fc line equal to the flattened feature size is the classifier's
+    # input vector (the junction convention), not a layer.
+    h, w, c = b.shape[b.last]
+    if len(fcs) > 1 and fcs[0] == h * w * c:
+        fcs = fcs[1:]
     if classes is not None:
         fcs[-1] = classes
     b.cfg["classes"] = fcs[-1]
@@ -259,6 +264,21 @@ def inception_v3_convs(batch=128):
         c = 2048
     return [dict(zip(("name", "h", "w", "c", "k", "r", "s", "pad_h", "pad_w", "stride"), t),
                  n=batch) for t in L]
+
+
+def apply_selection(cfg: dict, assignment: dict) -> dict:
+    """Set each feature conv's algorithm from a planner Selection.assignment
+    ({layer_id (1-based over the feature convs, as the catalog indexes them):
+    "gemm"|"winograd"|"fft"}); fc layers always run as GEMMs."""
+    out = copy.deepcopy(cfg)
+    i = 0
+    for L in out["layers"]:
+        if L["op"] == "conv" and not L["name"].startswith("fc"):
+            i += 1
+            algo = assignment.get(str(i), assignment.get(i))
+            if algo is not None:
+                L["algo"] = algo
+    return out
 
 
 CONFIGS = {"lenet": lenet, "alexnet": alexnet, "vgg16": vgg16, "resnet50": resnet50,

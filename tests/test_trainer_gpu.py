@@ -100,6 +100,39 @@ def test_alexnet_step_small_batch(oracle, prec):
     _check(oracle, _models().alexnet(batch=2, precision=prec))
 
 
+@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+def test_step_obeys_per_layer_algorithms(oracle, prec):
+    """The executor runs the planner's Selection: conv2 FFT, conv3 Winograd,
+    conv4 FFT, conv5 Winograd inside the AlexNet-227 step."""
+    m = _models()
+    cfg = m.apply_selection(m.alexnet(batch=2, precision=prec),
+                            {"2": "fft", "3": "winograd", "4": "fft", "5": "winograd"})
+    algos = [L.get("algo", "gemm") for L in cfg["layers"] if L["op"] == "conv"]
+    assert algos[:5] == ["gemm", "fft", "winograd", "fft", "winograd"]
+    _check(oracle, cfg)
+
+
+def test_profile_plan_train_loop(oracle):
+    """Profile -> reference-format catalog -> plan_batch_size -> train with the
+    chosen mini-batch and per-layer algorithms (tiny chain, all three families)."""
+    from paper_1709_06622_b200 import planner, profiler
+    m = _models()
+    base = m.from_net("input 20 20 8\nconv 3 1 1 16\npool 2 2 0\nconv 3 1 1 24\nconv 5 1 2 32\n"
+                      "pool 2 2 0\nfc 10\n", batch=1, precision="bf16")
+    prof = profiler.profile(profiler.feature_conv_specs(base), [32, 64], reps=2)
+    assert prof["csv"].startswith("layer_id,algorithm,batch_size,time_seconds,memory_bits")
+    algos = {r["algorithm"] for r in prof["rows"]}
+    assert algos == {"gemm", "winograd", "fft"}
+    plan = profiler.plan(profiler.net_text(base), prof["csv"], 180 * 10**9 * 8, 50_000)
+    rec = plan["recommended"]
+    assert rec in (32, 64)
+    sel = next(c["solve"] for c in plan["candidates"] if c["batch_size"] == rec)
+    cfg = m.apply_selection(m.from_net(profiler.net_text(base), batch=rec, precision="bf16"),
+                            sel["assignment"])
+    _check(oracle, cfg)
+    assert planner.default().call("catalog_options", catalog=prof["csv"], batch=rec)["options"]
+
+
 def test_from_net_fixture_chain(oracle):
     """The reference's own alexnet.net fixture, executed as a chain."""
     import planner_cases
