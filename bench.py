@@ -191,6 +191,53 @@ def conv_roofline(cfg, pk, reps=5):
             "peak_kind": f"bf16 dense burst ({pk['source']})"}, per_layer
 
 
+NVLINK_PEER_GBPS = 770.0  # measured per-direction peer bandwidth (B200_PROFILING.md)
+
+
+def lemmas(phases, world, param_bytes, out_dir):
+    """Paper Lemma 1 / Lemma 2 evaluated by the traincap planner (C-ABI) from
+    this run's measured StepTrace: gpu_processing = fwd + bwd, and the
+    unhidden distributed_update (reduce-scatter), parameter_update (SGD) and
+    parameter_refresh (all-gather) as overhead (PAPER.md:229-241)."""
+    from paper_1709_06622_b200 import planner
+
+    p = planner.default()
+    trace = (f"gpu_processing {(phases['fwd'] + phases['bwd']) / 1e3!r}\n"
+             f"distributed_update {phases['reduce_scatter'] / 1e3!r}\n"
+             f"parameter_update {phases['sgd'] / 1e3!r}\n"
+             f"parameter_refresh {phases['all_gather'] / 1e3!r}\n"
+             "data_loading 0 hidden\ndata_preparation 0 hidden\nhost_to_gpu_transfer 0 hidden\n")
+    with open(os.path.join(out_dir, f"steptrace_g{world}.txt"), "w") as f:
+        f.write(trace)
+    prof = p.call("estimate_overhead_ratio", trace=trace)
+    ro = prof["ratio"]
+    table = p.call("scaling_table", max_gpus=8, r=ro)["table"]
+    out = {"overhead_ratio": ro, "measured_at_gpus": world,
+           "lemma1": {str(g): {"efficiency": e, "speedup": s} for g, e, s in table},
+           "lemma1_8gpu_predicted_efficiency": table[7][1]}
+    if world > 1 and phases["reduce_scatter"] > 0:
+        rs_bytes = param_bytes * (world - 1) / world
+        b_ps = rs_bytes / (phases["reduce_scatter"] / 1e3)
+        t_c = (phases["fwd"] + phases["bwd"]) / 1e3
+        out["lemma2"] = {"param_bytes": param_bytes, "workers": world,
+                         "bandwidth_bytes_per_sec": b_ps, "compute_time_seconds": t_c,
+                         "min_parameter_servers": p.call(
+                             "min_parameter_servers", workers=world, param_bytes=param_bytes,
+                             bandwidth=b_ps, compute_time=t_c)["servers"]}
+    return out
+
+
+def ps_bandwidth(phases, world, param_bytes):
+    if world < 2:
+        return None
+    rs = param_bytes * (world - 1) / world / (phases["reduce_scatter"] / 1e3) / 1e9
+    ag = (param_bytes / 2) * (world - 1) / world / (phases["all_gather"] / 1e3) / 1e9  # bf16 refresh
+    return {"reduce_scatter_busbw_GBps": round(rs, 1), "all_gather_busbw_GBps": round(ag, 1),
+            "peak_GBps": NVLINK_PEER_GBPS, "rs_frac": round(rs / NVLINK_PEER_GBPS, 3),
+            "ag_frac": round(ag / NVLINK_PEER_GBPS, 3),
+            "peak_kind": "peer copy per direction, B200_PROFILING.md (fallback)"}
+
+
 def in_step_roofline(rows, pk, precision):
     """Dominant kernel = the tcgen05 implicit-GEMM conv (every fwd/dgrad/wgrad
     pass of the step). achieved = algorithmic conv FLOP of the step / the sum of
@@ -368,7 +415,9 @@ def main():
             "cpu_baseline": cpu,
             "phases_ms": {k: round(v, 3) for k, v in phases.items()},
             "loss": loss,
-            "ps": {"param_bytes": param_bytes, "rs_ag_bytes_per_gpu_step": rs_ag_bytes},
+            "ps": {"param_bytes": param_bytes, "rs_ag_bytes_per_gpu_step": rs_ag_bytes,
+                   "busbw": ps_bandwidth(phases, world, param_bytes)},
+            "lemmas": lemmas(phases, world, param_bytes, os.path.join(ROOT, "gpurun_out")),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -642,6 +642,117 @@ __global__ void dgrad_empty_phase_kernel(const Params p) {
     }
 }
 
+// ------------------------------------------- explicit im2col (narrow C) ----
+// A first layer sees 3 real channels padded to 8: the implicit GEMM would
+// multiply 5/8 zeros and fetch 16-byte pixels through narrow im2col boxes.
+// Instead the patch matrix is written out once, dropping the padding:
+//   col[p][r * RW + s * CV + c] = x[n][oh*sh - ph + r][ow*sw - pw + s][c]
+// (RW = S*CV rounded up to 8 so every filter row starts 16-byte aligned, zero
+// tail), and the conv becomes a plain TMA GEMM over K-dim R*RW (168 for the
+// ResNet stem instead of 392). Weights are repacked to the same column order;
+// wgrad runs the plain GEMM on col and scatters back to [K][R][S][C].
+struct NarrowPlan {
+    bool use = false;
+    int cv = 0, rw = 0, kc = 0;
+    size_t col_bytes = 0;
+    ConvGeom g1{};  // the equivalent 1x1 conv over col
+};
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+NarrowPlan narrow_plan(const ConvGeom& g) {
+    NarrowPlan q;
+    q.cv = g.c_valid > 0 && g.c_valid < g.c ? g.c_valid : g.c;
+    q.rw = (g.s * q.cv + 7) / 8 * 8;
+    q.kc = g.r * q.rw;
+    q.use = g.c <= 8 && q.cv < g.c && g.r * g.s > 1 && 2 * q.kc <= g.r * g.s * g.c;
+    if (!q.use) return q;
+    const int ho = g.ho(), wo = g.wo();
+    q.col_bytes = size_t(g.n) * ho * wo * q.kc * 2;
+    q.g1 = ConvGeom{g.n, ho, wo, q.kc, g.k, 1, 1, 0, 0, 1, 1};
+    return q;
+}
+
+template <int CV>
+__global__ void __launch_bounds__(256) im2col_rows_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          __nv_bfloat16* __restrict__ col,
+                                                          ConvGeom g, int rw, int kc,
+                                                          long long rows) {
+    const int ho = (g.h + 2 * g.pad_h - g.r) / g.stride_h + 1;
+    const int wo = (g.w + 2 * g.pad_w - g.s) / g.stride_w + 1;
+    const int span = g.s * CV;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / g.r;
+        const int r = static_cast<int>(i - p * g.r);
+        const int ow = static_cast<int>(p % wo);
+        const long long t = p / wo;
+        const int oh = static_cast<int>(t % ho);
+        const int n = static_cast<int>(t / ho);
+        const int ih = oh * g.stride_h - g.pad_h + r;
+        const int iw0 = ow * g.stride_w - g.pad_w;
+        const bool row_ok = ih >= 0 && ih < g.h;
+        const __nv_bfloat16* src = x + (size_t(n) * g.h + (row_ok ? ih : 0)) * g.w * g.c;
+        uint4* dst = reinterpret_cast<uint4*>(col + p * kc + size_t(r) * rw);
+        for (int q = 0; q < rw / 8; ++q) {
+            __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int j = q * 8 + e;
+                const int s = j / CV, c = j - s * CV;
+                const int iw = iw0 + s;
+                v[e] = (row_ok && j < span && iw >= 0 && iw < g.w) ? src[size_t(iw) * g.c + c]
+                                                                     : __float2bfloat16(0.f);
+            }
+            dst[q] = *reinterpret_cast<const uint4*>(v);
+        }
+    }
+}
+
+// w[K][R][S][C] -> wp[K][R*RW] (fwd operand, bf16)
+__global__ void narrow_pack_weights(const __nv_bfloat16* __restrict__ w,
+                                    __nv_bfloat16* __restrict__ wp, ConvGeom g, int cv, int rw) {
+    const int kc = g.r * rw;
+    const int total = g.k * kc;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int k = i / kc, j = i - k * kc;
+        const int r = j / rw, t = j - r * rw;
+        const int s = t / cv, c = t - s * cv;
+        wp[i] = t < g.s * cv ? w[((size_t(k) * g.r + r) * g.s + s) * g.c + c]
+                             : __float2bfloat16(0.f);
+    }
+}
+
+// dwp[K][R*RW] (fp32) -> dw[K][R][S][C], zero on the padded channels
+__global__ void narrow_scatter_grad(const float* __restrict__ dwp, float* __restrict__ dw,
+                                    ConvGeom g, int cv, int rw) {
+    const int total = g.k * g.r * g.s * g.c;
+    const int kc = g.r * rw;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int c = i % g.c;
+        const int rest = i / g.c;
+        const int s = rest % g.s, kr = rest / g.s;
+        const int r = kr % g.r, k = kr / g.r;
+        dw[i] = c < cv ? dwp[size_t(k) * kc + r * rw + s * cv + c] : 0.f;
+    }
+}
+
+cudaError_t narrow_im2col(const ConvGeom& g, const NarrowPlan& q, const void* x, void* col,
+                          cudaStream_t st) {
+    const long long rows = (long long)g.n * g.ho() * g.wo() * g.r;
+    const int blocks = static_cast<int>(std::min<long long>((rows + 255) / 256, num_sms() * 16LL));
+    const auto* xs = static_cast<const __nv_bfloat16*>(x);
+    auto* cs = static_cast<__nv_bfloat16*>(col);
+    switch (q.cv) {
+#define TCB_CV(n) \
+    case n: im2col_rows_kernel<n><<<blocks, 256, 0, st>>>(xs, cs, g, q.rw, q.kc, rows); break;
+        TCB_CV(1) TCB_CV(2) TCB_CV(3) TCB_CV(4) TCB_CV(5) TCB_CV(6) TCB_CV(7)
+#undef TCB_CV
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- host ----
 int pick_bn(int ncol) { return ncol >= 256 ? 256 : (ncol > 64 ? 128 : 64); }
 
@@ -772,22 +883,54 @@ bool conv_tc_supported(const ConvGeom& g, ConvMode mode) {
 }
 
 size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
+    const NarrowPlan q = narrow_plan(g);
+    if (q.use && mode == ConvMode::Fwd)
+        return align256(q.col_bytes) + align256(size_t(g.k) * q.kc * 2);
+    if (q.use && mode == ConvMode::Wgrad)
+        return align256(q.col_bytes) + align256(size_t(g.k) * q.kc * 4) +
+               conv_tc_workspace(q.g1, ConvMode::Wgrad);
     if (mode != ConvMode::Wgrad) return 0;
     const ConvShape s = make_shape(g, mode);
     const SplitPlan sp = plan_splits(s, pick_bn(s.Ncol));
     return sp.splits > 1 ? size_t(sp.splits) * s.M * s.Ncol * sizeof(float) : 0;
 }
 
+int conv_tc_launches(const ConvGeom& g, ConvMode mode) {
+    const NarrowPlan q = narrow_plan(g);
+    if (mode == ConvMode::Fwd) return q.use ? 3 : 1;
+    if (mode == ConvMode::Dgrad) return g.stride_h * g.stride_w;
+    const ConvGeom& gw = q.use ? q.g1 : g;
+    const ConvShape s = make_shape(gw, mode);
+    const int split = plan_splits(s, pick_bn(s.Ncol)).splits > 1 ? 2 : 1;
+    return split + (q.use ? 2 : 0);
+}
+
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
-                        void* y, cudaStream_t st) {
+                        void* y, cudaStream_t st, void* workspace) {
     Params p{};
-    p.s = make_shape(g, ConvMode::Fwd);
-    p.a = static_cast<const __nv_bfloat16*>(x);
+    const NarrowPlan q = narrow_plan(g);
+    const void* a_matrix = x;
+    const void* b_matrix = w;
+    if (q.use && workspace) {
+        char* ws = static_cast<char*>(workspace);
+        cudaError_t e = narrow_im2col(g, q, x, ws, st);
+        if (e != cudaSuccess) return e;
+        auto* wp = reinterpret_cast<__nv_bfloat16*>(ws + align256(q.col_bytes));
+        narrow_pack_weights<<<std::max(1, std::min(g.k * q.kc / 256 + 1, 1024)), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(w), wp, g, q.cv, q.rw);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        p.s = make_shape(q.g1, ConvMode::Fwd);
+        a_matrix = ws;
+        b_matrix = wp;
+    } else {
+        p.s = make_shape(g, ConvMode::Fwd);
+    }
+    p.a = static_cast<const __nv_bfloat16*>(a_matrix);
     p.out = y;
     p.bias = ep.bias;
     p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
     p.relu = ep.relu ? 1 : 0;
-    return dispatch<ConvMode::Fwd>(p, x, w, st);
+    return dispatch<ConvMode::Fwd>(p, a_matrix, b_matrix, st);
 }
 
 cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, const Epilogue& ep,
@@ -825,6 +968,20 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, co
 
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
                           void* workspace, cudaStream_t st) {
+    const NarrowPlan q = narrow_plan(g);
+    if (q.use) {
+        if (workspace == nullptr) return cudaErrorInvalidValue;
+        char* ws = static_cast<char*>(workspace);
+        cudaError_t e = narrow_im2col(g, q, x, ws, st);
+        if (e != cudaSuccess) return e;
+        float* dwp = reinterpret_cast<float*>(ws + align256(q.col_bytes));
+        void* rest = ws + align256(q.col_bytes) + align256(size_t(g.k) * q.kc * 4);
+        if ((e = conv_tc_wgrad(q.g1, dy, ws, dwp, rest, st)) != cudaSuccess) return e;
+        const int total = g.k * g.r * g.s * g.c;
+        narrow_scatter_grad<<<std::max(1, std::min(total / 256 + 1, 1024)), 256, 0, st>>>(
+            dwp, dw, g, q.cv, q.rw);
+        return cudaGetLastError();
+    }
     Params p{};
     p.s = make_shape(g, ConvMode::Wgrad);
     const SplitPlan sp = plan_splits(p.s, pick_bn(p.s.Ncol));

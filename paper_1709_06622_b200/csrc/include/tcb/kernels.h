@@ -11,6 +11,9 @@ namespace tcb {
 
 struct ConvGeom {
     int n, h, w, c, k, r, s, pad_h, pad_w, stride_h, stride_w;
+    // channels of x that can be non-zero (the rest are bf16 channel padding,
+    // always zero); 0 = all c. Lets narrow first layers drop the padding.
+    int c_valid = 0;
     int ho() const { return (h + 2 * pad_h - r) / stride_h + 1; }
     int wo() const { return (w + 2 * pad_w - s) / stride_w + 1; }
 };
@@ -31,9 +34,13 @@ struct Epilogue {
 // ---- tensor-core implicit GEMM (tcgen05 / TMEM), bf16 in, fp32 accumulate ----
 // Requirements: C % 8 == 0 (fwd/wgrad), K % 8 == 0 (dgrad/wgrad).
 // wTp (dgrad) is w packed per stride phase by pack_dgrad_weights.
+// Narrow-input convs (c_valid * R * S far below C * R * S, e.g. the 3-channel
+// stem) run as a plain GEMM over an explicit im2col in `workspace`; without a
+// workspace they take the implicit im2col path.
 size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode);
+int conv_tc_launches(const ConvGeom& g, ConvMode mode);  // kernels one call launches
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
-                        void* y, cudaStream_t st);
+                        void* y, cudaStream_t st, void* workspace = nullptr);
 cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wT, const Epilogue& ep,
                           void* dx, cudaStream_t st);
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,

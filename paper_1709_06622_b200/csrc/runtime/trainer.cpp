@@ -194,6 +194,7 @@ int build_graph(tcb_trainer* t) {
                             L.value("s", L.at("r").get<int>()), L.value("pad_h", L.value("pad", 0)),
                             L.value("pad_w", L.value("pad", 0)), L.value("stride_h", L.value("stride", 1)),
                             L.value("stride_w", L.value("stride", 1))};
+            if (x.c_logical < x.c) nd.g.c_valid = x.c_logical;  // zero channel padding
             nd.bias = L.value("bias", false);
             nd.relu = L.value("relu", false);
             nd.algo = L.value("algo", std::string("gemm"));
@@ -330,7 +331,8 @@ int allocate(tcb_trainer* t) {
         if (nd.op == Op::MaxPool) nd.argmax = b.take(elems);
         if (nd.op == Op::Conv) {
             if (nd.algo_id == TCB_ALGO_GEMM) {
-                ws = std::max(ws, t->bf16 ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
+                ws = std::max(ws, t->bf16 ? std::max(conv_tc_workspace(nd.g, ConvMode::Wgrad),
+                                                     conv_tc_workspace(nd.g, ConvMode::Fwd))
                                           : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
                 if (t->bf16 && nd.need_dgrad) nd.wT = b.take(nd.wcount * 2);
             } else {
@@ -442,12 +444,12 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                     TRY_CUDA(fft_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
                 else if (t->bf16)
                     TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
-                                         ep, t->at(nd.act), st));
+                                         ep, t->at(nd.act), st, t->at(t->off_ws)));
                 else
                     TRY_CUDA(conv_ffma_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
                                            ep, t->at<float>(nd.act), st));
                 t->mark(idx, 1, st);
-                t->launches++;
+                t->launches += (t->bf16 && nd.algo_id == TCB_ALGO_GEMM) ? conv_tc_launches(nd.g, ConvMode::Fwd) : 1;
                 break;
             }
             case Op::MaxPool:
@@ -573,7 +575,7 @@ int backward(tcb_trainer* t, cudaStream_t st) {
             else
                 TRY_CUDA(conv_ffma_wgrad(nd.g, t->at<float>(nd.grad), t->at<float>(x.act), grad + nd.woff,
                                          t->at(t->off_ws), st));
-            t->launches += 2;
+            t->launches += (t->bf16 && nd.algo_id == TCB_ALGO_GEMM) ? conv_tc_launches(nd.g, ConvMode::Wgrad) : 2;
             if (nd.bias) {
                 TRY_CUDA(column_sum(t->dt, t->at(nd.grad), grad + nd.boff, nd.n * nd.h * nd.w, nd.g.k,
                                     t->at<float>(t->off_colsum), st));
