@@ -80,7 +80,9 @@ int tcb_conv_plan_create(const tcb_conv_geom* g, int algo, int prec, tcb_conv_pl
 int tcb_conv_plan_destroy(tcb_conv_plan* plan);
 /* Operand-load path of the tensor-core GEMM conv: 0 = automatic (2-D TMA for
  * 1x1/stride-1 layers, im2col-mode TMA when channels % 64 == 0, cp.async
- * gather otherwise), 1 = force the cp.async gather path (A/B testing). */
+ * gather otherwise; TMA-store epilogue on K-light layers), 1 = force the
+ * cp.async gather path, 2 = automatic loads with the register epilogue
+ * everywhere (A/B testing). */
 int tcb_set_conv_operand_path(int mode);
 
 /* y = act(conv(x, w) + bias + residual); bias (fp32, K) and residual (same

@@ -40,20 +40,27 @@ constexpr int kEpilogueThreads = 256;  // warps 4-11
 constexpr int kMmaWarp = 12;
 constexpr int kThreads = kProducerThreads + kEpilogueThreads + 32;
 
-template <int BN>
+// EPI: TMA epilogue (side inputs TMA-loaded into per-warp 64B-swizzled staging,
+// outputs TMA-stored) for K-light layers whose time is the epilogue's HBM
+// traffic; it trades ring stages for 64 KB of staging.
+template <int BN, bool EPI = false>
 struct Cfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-    static constexpr int kLag = kStages - 1;  // cp.async groups in flight per producer
+    static constexpr int kStages = EPI ? (BN == 256 ? 3 : (BN == 128 ? 4 : 5))
+                                       : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
+    static constexpr int kRingBytes = kStages * kStageBytes;
+    static constexpr int kEpiWarpBytes = 4 * 2048;  // 2 slots x {in0/out, in1}, 32x32 bf16 each
+    static constexpr int kEpiBytes = EPI ? 8 * kEpiWarpBytes : 0;
     static constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
-    static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 + 256;
+    static constexpr size_t kSmem = size_t(kRingBytes) + kEpiBytes + 1024 + 512;
 };
 
 struct Params {
     CUtensorMap tmap_a;      // activation operand when it is a plain matrix (1x1/s1/p0)
     CUtensorMap tmap_b;      // weight operand (fwd / dgrad) or x (plain wgrad)
+    CUtensorMap tmap_out, tmap_res, tmap_mask;  // EPI: [M][Ncol] 32x32 boxes, SWIZZLE_64B
     ConvShape s;
     const __nv_bfloat16* a;  // fwd: x   dgrad: dy   wgrad: dy
     const __nv_bfloat16* b;  // wgrad: x (gathered)
@@ -319,19 +326,20 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
 //            landing as no-swizzle 8x16B core matrices (LBO 2 KB, SBO 128 B).
 constexpr int kGather = 0, kPlain = 1, kIm2col = 2, kIm2colC8 = 3;
 
-template <ConvMode MODE, int BN, int LOAD>
+template <ConvMode MODE, int BN, int LOAD, bool EPI>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ Params p) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, EPI>;
     constexpr bool kTmaOnly = LOAD != kGather;
     constexpr bool kTmaB = MODE != ConvMode::Wgrad || kTmaOnly;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRingBytes + C::kEpiBytes);
     uint64_t* empty = full + C::kStages;
     uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* side_bar = tempty + 2;  // EPI: [8 warps][2 slots]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(side_bar + 16);
     __shared__ int4 pixtab[2][BK];  // wgrad im2col pixel decode (gather mode), double-buffered
 
     const int tid = threadIdx.x;
@@ -346,9 +354,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], kEpilogueThreads);
         }
+        if (EPI)
+            for (int i = 0; i < 16; ++i) ptx::mbar_init(&side_bar[i], 1);
         ptx::fence_mbarrier_init();
         if (kTmaB) ptx::tma_prefetch_desc(&p.tmap_b);
         if (kTmaOnly) ptx::tma_prefetch_desc(&p.tmap_a);
+        if (EPI) ptx::tma_prefetch_desc(&p.tmap_out);
     }
     if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
@@ -566,6 +577,101 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
             __syncwarp();
         }
+    } else if constexpr (EPI) {
+        // ======================================== TMA epilogue (K-light) ======
+        // Warp (quarter, half) owns rows quarter*32..+31 and half of the tile's
+        // 32-column chunks. Per chunk: residual / mask boxes (32 x 32 bf16,
+        // SWIZZLE_64B) arrive by TMA one chunk ahead into slot seq&1; the
+        // result overwrites the residual box in place and leaves by a TMA store.
+        const int quarter = warp & 3;
+        const int half = (warp - 4) >> 2;
+        const int lane = tid & 31;
+        constexpr int kChunks = BN / 32, kHalfChunks = kChunks / 2;
+        const int c_begin = half * kHalfChunks, c_end = c_begin + kHalfChunks;
+        uint8_t* ebuf = smem + C::kRingBytes + (warp - 4) * C::kEpiWarpBytes;
+        const uint32_t ebuf_addr = ptx::smem_addr(ebuf);
+        uint64_t* sbar = side_bar + (warp - 4) * 2;
+        const uint32_t side_bytes = (p.residual ? 2048u : 0u) + (p.mask ? 2048u : 0u);
+        const int ncol = p.s.Ncol;
+        uint32_t seq = 0;
+        auto prefetch = [&](uint32_t sq, int row0, int col0) {
+            if (lane == 0 && side_bytes) {
+                const uint32_t slot = sq & 1;
+                ptx::bulk_wait_read<0>();  // the store that last used this slot has read it
+                ptx::mbar_arrive_expect_tx(&sbar[slot], side_bytes);
+                if (p.residual)
+                    ptx::tma_load_2d(ebuf_addr + slot * 4096, &p.tmap_res, &sbar[slot], col0, row0);
+                if (p.mask)
+                    ptx::tma_load_2d(ebuf_addr + slot * 4096 + 2048, &p.tmap_mask, &sbar[slot], col0,
+                                     row0);
+            }
+        };
+        int it = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+            const TileCoord tc = tile_coord(p, t);
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            const int row0 = tc.mt * BM + quarter * 32;
+            prefetch(seq, row0, tc.nt * BN + c_begin * 32);
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = c_begin; c < c_end; ++c, ++seq) {
+                const int col0 = tc.nt * BN + c * 32;
+                if (c + 1 < c_end) prefetch(seq + 1, row0, col0 + 32);
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                            acc * BN + c * 32,
+                                        v);
+                ptx::tmem_ld_wait();
+                const uint32_t slot = seq & 1;
+                uint8_t* b0 = ebuf + slot * 4096;
+                if (lane == 0 && !side_bytes) ptx::bulk_wait_read<1>();  // store(seq-2) read
+                __syncwarp();
+                if (side_bytes) ptx::mbar_wait(&sbar[slot], (seq >> 1) & 1);
+                if (col0 < ncol) {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        float x[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(v[8 * g + i]);
+                        const uint32_t off = lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4);
+                        if (p.bias) {
+                            const int cb = col0 + 8 * g;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                if (cb + i < ncol) x[i] += __ldg(p.bias + cb + i);
+                        }
+                        if (p.residual) {
+                            float r[8];
+                            unpack8(*reinterpret_cast<const uint4*>(b0 + off), r);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) x[i] += r[i];
+                        }
+                        if (p.relu) {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) x[i] = fmaxf(x[i], 0.f);
+                        }
+                        if (p.mask) {
+                            float mk[8];
+                            unpack8(*reinterpret_cast<const uint4*>(b0 + 2048 + off), mk);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) x[i] = mk[i] > 0.f ? x[i] : 0.f;
+                        }
+                        *reinterpret_cast<uint4*>(b0 + off) = pack8(x);
+                    }
+                    ptx::fence_proxy_async_smem();
+                }
+                __syncwarp();
+                if (lane == 0 && col0 < ncol) {
+                    ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * 4096, col0, row0);
+                    ptx::bulk_commit();
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+        }
+        if (lane == 0) ptx::bulk_wait<0>();
     } else {
         // ================================================= epilogue ======
         // Two warps per TMEM lane quarter (a warp may only touch lanes
@@ -647,14 +753,16 @@ __global__ void dgrad_empty_phase_kernel(const Params p) {
 // multiply 5/8 zeros and fetch 16-byte pixels through narrow im2col boxes.
 // Instead the patch matrix is written out once, dropping the padding:
 //   col[p][r * RW + s * CV + c] = x[n][oh*sh - ph + r][ow*sw - pw + s][c]
-// (RW = S*CV rounded up to 8 so every filter row starts 16-byte aligned, zero
-// tail), and the conv becomes a plain TMA GEMM over K-dim R*RW (168 for the
-// ResNet stem instead of 392). Weights are repacked to the same column order;
-// wgrad runs the plain GEMM on col and scatters back to [K][R][S][C].
+// (RW = S*CV rounded up to 8 so every filter row starts 16-byte aligned; the
+// row pitch KC = R*RW rounded up to 64 keeps TMA rows 128-byte aligned; zero
+// tails), and the conv becomes a plain TMA GEMM over K-dim KC (192 for the
+// ResNet stem instead of 392). Weights are repacked to the same column order.
+// Wgrad runs the plain GEMM on the same col (kept from the forward pass when
+// the caller says so) and scatters back to [K][R][S][C].
 struct NarrowPlan {
     bool use = false;
-    int cv = 0, rw = 0, kc = 0;
-    size_t col_bytes = 0;
+    int cv = 0, rw = 0, kc = 0, wp = 0;  // wp: input columns one output row spans
+    size_t col_bytes = 0, smem = 0;
     ConvGeom g1{};  // the equivalent 1x1 conv over col
 };
 
@@ -664,70 +772,71 @@ NarrowPlan narrow_plan(const ConvGeom& g) {
     NarrowPlan q;
     q.cv = g.c_valid > 0 && g.c_valid < g.c ? g.c_valid : g.c;
     q.rw = (g.s * q.cv + 7) / 8 * 8;
-    q.kc = g.r * q.rw;
-    q.use = g.c <= 8 && q.cv < g.c && g.r * g.s > 1 && 2 * q.kc <= g.r * g.s * g.c;
-    if (!q.use) return q;
+    q.kc = (g.r * q.rw + 63) / 64 * 64;
     const int ho = g.ho(), wo = g.wo();
+    q.wp = (wo - 1) * g.stride_w + g.s;
+    q.smem = size_t(g.r) * q.wp * q.cv * 2;
+    q.use = g.c == 8 && q.cv < g.c && g.r * g.s > 1 && 2 * q.kc <= g.r * g.s * g.c &&
+            q.smem <= 48 * 1024;
+    if (!q.use) return q;
     q.col_bytes = size_t(g.n) * ho * wo * q.kc * 2;
     q.g1 = ConvGeom{g.n, ho, wo, q.kc, g.k, 1, 1, 0, 0, 1, 1};
     return q;
 }
 
-template <int CV>
-__global__ void __launch_bounds__(256) im2col_rows_kernel(const __nv_bfloat16* __restrict__ x,
-                                                          __nv_bfloat16* __restrict__ col,
-                                                          ConvGeom g, int rw, int kc,
-                                                          long long rows) {
-    const int ho = (g.h + 2 * g.pad_h - g.r) / g.stride_h + 1;
-    const int wo = (g.w + 2 * g.pad_w - g.s) / g.stride_w + 1;
-    const int span = g.s * CV;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long p = i / g.r;
-        const int r = static_cast<int>(i - p * g.r);
-        const int ow = static_cast<int>(p % wo);
-        const long long t = p / wo;
-        const int oh = static_cast<int>(t % ho);
-        const int n = static_cast<int>(t / ho);
-        const int ih = oh * g.stride_h - g.pad_h + r;
-        const int iw0 = ow * g.stride_w - g.pad_w;
-        const bool row_ok = ih >= 0 && ih < g.h;
-        const __nv_bfloat16* src = x + (size_t(n) * g.h + (row_ok ? ih : 0)) * g.w * g.c;
-        uint4* dst = reinterpret_cast<uint4*>(col + p * kc + size_t(r) * rw);
-        for (int q = 0; q < rw / 8; ++q) {
-            __align__(16) __nv_bfloat16 v[8];
+// One block per output row (n, oh): the R input rows it reads are staged in
+// shared memory as [r][u][c] (u = input column + pad_w, only the CV real
+// channels), so col element (ow, r, t = s*CV + c) is sm[(r*WP + ow*sw)*CV + t];
+// the block's slice of col is contiguous and written in 16-byte chunks.
+__global__ void __launch_bounds__(256) narrow_im2col_kernel(const __nv_bfloat16* __restrict__ x,
+                                                            __nv_bfloat16* __restrict__ col,
+                                                            ConvGeom g, int cv, int rw, int kc,
+                                                            int wp, int ho, int wo) {
+    extern __shared__ __nv_bfloat16 sm[];
+    const int n = blockIdx.x / ho, oh = blockIdx.x - n * ho;
+    const int ih0 = oh * g.stride_h - g.pad_h;
+    for (int i = threadIdx.x; i < g.r * wp; i += blockDim.x) {
+        const int r = i / wp, u = i - r * wp;
+        const int ih = ih0 + r, iw = u - g.pad_w;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ih >= 0 && ih < g.h && iw >= 0 && iw < g.w)
+            v = __ldg(reinterpret_cast<const uint4*>(x + ((size_t(n) * g.h + ih) * g.w + iw) * 8));
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+        for (int c = 0; c < cv; ++c) sm[i * cv + c] = e[c];
+    }
+    __syncthreads();
+    const int span = g.s * cv, qpp = kc / 8;
+    uint4* dst = reinterpret_cast<uint4*>(col + size_t(blockIdx.x) * wo * kc);
+    for (int i = threadIdx.x; i < wo * qpp; i += blockDim.x) {
+        const int ow = i / qpp, col0 = (i - ow * qpp) * 8;
+        const int r = col0 / rw, t0 = col0 - r * rw;
+        const __nv_bfloat16* src = sm + (r * wp + ow * g.stride_w) * cv;
+        __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int j = q * 8 + e;
-                const int s = j / CV, c = j - s * CV;
-                const int iw = iw0 + s;
-                v[e] = (row_ok && j < span && iw >= 0 && iw < g.w) ? src[size_t(iw) * g.c + c]
-                                                                     : __float2bfloat16(0.f);
-            }
-            dst[q] = *reinterpret_cast<const uint4*>(v);
-        }
+        for (int e = 0; e < 8; ++e)
+            v[e] = (r < g.r && t0 + e < span) ? src[t0 + e] : __float2bfloat16(0.f);
+        dst[i] = *reinterpret_cast<const uint4*>(v);
     }
 }
 
-// w[K][R][S][C] -> wp[K][R*RW] (fwd operand, bf16)
+// w[K][R][S][C] -> wp[K][KC] (fwd operand, bf16)
 __global__ void narrow_pack_weights(const __nv_bfloat16* __restrict__ w,
-                                    __nv_bfloat16* __restrict__ wp, ConvGeom g, int cv, int rw) {
-    const int kc = g.r * rw;
+                                    __nv_bfloat16* __restrict__ wp, ConvGeom g, int cv, int rw,
+                                    int kc) {
     const int total = g.k * kc;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int k = i / kc, j = i - k * kc;
         const int r = j / rw, t = j - r * rw;
         const int s = t / cv, c = t - s * cv;
-        wp[i] = t < g.s * cv ? w[((size_t(k) * g.r + r) * g.s + s) * g.c + c]
-                             : __float2bfloat16(0.f);
+        wp[i] = (r < g.r && t < g.s * cv) ? w[((size_t(k) * g.r + r) * g.s + s) * g.c + c]
+                                          : __float2bfloat16(0.f);
     }
 }
 
-// dwp[K][R*RW] (fp32) -> dw[K][R][S][C], zero on the padded channels
+// dwp[K][KC] (fp32) -> dw[K][R][S][C], zero on the padded channels
 __global__ void narrow_scatter_grad(const float* __restrict__ dwp, float* __restrict__ dw,
-                                    ConvGeom g, int cv, int rw) {
+                                    ConvGeom g, int cv, int rw, int kc) {
     const int total = g.k * g.r * g.s * g.c;
-    const int kc = g.r * rw;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int c = i % g.c;
         const int rest = i / g.c;
@@ -739,17 +848,10 @@ __global__ void narrow_scatter_grad(const float* __restrict__ dwp, float* __rest
 
 cudaError_t narrow_im2col(const ConvGeom& g, const NarrowPlan& q, const void* x, void* col,
                           cudaStream_t st) {
-    const long long rows = (long long)g.n * g.ho() * g.wo() * g.r;
-    const int blocks = static_cast<int>(std::min<long long>((rows + 255) / 256, num_sms() * 16LL));
-    const auto* xs = static_cast<const __nv_bfloat16*>(x);
-    auto* cs = static_cast<__nv_bfloat16*>(col);
-    switch (q.cv) {
-#define TCB_CV(n) \
-    case n: im2col_rows_kernel<n><<<blocks, 256, 0, st>>>(xs, cs, g, q.rw, q.kc, rows); break;
-        TCB_CV(1) TCB_CV(2) TCB_CV(3) TCB_CV(4) TCB_CV(5) TCB_CV(6) TCB_CV(7)
-#undef TCB_CV
-        default: return cudaErrorInvalidValue;
-    }
+    const int ho = g.ho(), wo = g.wo();
+    narrow_im2col_kernel<<<g.n * ho, 256, q.smem, st>>>(static_cast<const __nv_bfloat16*>(x),
+                                                        static_cast<__nv_bfloat16*>(col), g, q.cv,
+                                                        q.rw, q.kc, q.wp, ho, wo);
     return cudaGetLastError();
 }
 
@@ -815,18 +917,30 @@ bool build_maps(Params& p, const void* a_matrix, const void* b_matrix, int bn) {
     return true;
 }
 
-template <ConvMode MODE, int BN, int LOAD>
+// EPI output / side-input maps: [M][Ncol] bf16, 32-row x 32-column boxes.
+bool build_epi_maps(Params& p) {
+    const auto sw = CU_TENSOR_MAP_SWIZZLE_64B;
+    if (!make_tmap_bf16_2d(&p.tmap_out, p.out, p.s.M, p.s.Ncol, 32, 32, sw)) return false;
+    if (p.residual && !make_tmap_bf16_2d(&p.tmap_res, p.residual, p.s.M, p.s.Ncol, 32, 32, sw))
+        return false;
+    if (p.mask && !make_tmap_bf16_2d(&p.tmap_mask, p.mask, p.s.M, p.s.Ncol, 32, 32, sw))
+        return false;
+    return true;
+}
+
+template <ConvMode MODE, int BN, int LOAD, bool EPI>
 cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, EPI>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, LOAD>,
+        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, LOAD, EPI>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(C::kSmem));
         if (e != cudaSuccess) return e;
         configured = true;
     }
     if (!build_maps<MODE, LOAD>(p, a_matrix, b_matrix, BN)) return cudaErrorInvalidValue;
+    if (EPI && !build_epi_maps(p)) return cudaErrorInvalidValue;
     p.m_tiles = (p.s.M + BM - 1) / BM;
     p.n_tiles = (p.s.Ncol + BN - 1) / BN;
     p.kb_total = (p.s.Kdim + BK - 1) / BK;
@@ -836,16 +950,40 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
     }
     p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
     const int grid = std::min(p.num_tiles, num_sms());
-    conv_tc_kernel<MODE, BN, LOAD><<<grid, kThreads, C::kSmem, st>>>(p);
+    conv_tc_kernel<MODE, BN, LOAD, EPI><<<grid, kThreads, C::kSmem, st>>>(p);
     return cudaGetLastError();
+}
+
+int g_epi_kb = -1;  // TMA epilogue for layers with at most this many k-blocks
+
+// The TMA epilogue needs the output rows contiguous (fwd; single-phase dgrad).
+template <ConvMode MODE>
+bool use_epi(const Params& p) {
+    if (MODE == ConvMode::Wgrad) return false;
+    if (MODE == ConvMode::Dgrad && (p.s.sh != 1 || p.s.sw != 1)) return false;
+    if (g_epi_kb < 0) {
+        const char* e = getenv("TCB_CONV_EPI_KB");
+        g_epi_kb = e ? atoi(e) : 16;
+    }
+    if (p.s.Ncol % 8 != 0) return false;
+    return (p.s.Kdim + BK - 1) / BK <= g_epi_kb;
 }
 
 template <ConvMode MODE, int LOAD>
 cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
+    if constexpr (MODE != ConvMode::Wgrad) {
+        if (use_epi<MODE>(p)) {
+            switch (pick_bn(p.s.Ncol)) {
+                case 256: return launch<MODE, 256, LOAD, true>(p, a_matrix, b_matrix, st);
+                case 128: return launch<MODE, 128, LOAD, true>(p, a_matrix, b_matrix, st);
+                default: return launch<MODE, 64, LOAD, true>(p, a_matrix, b_matrix, st);
+            }
+        }
+    }
     switch (pick_bn(p.s.Ncol)) {
-        case 256: return launch<MODE, 256, LOAD>(p, a_matrix, b_matrix, st);
-        case 128: return launch<MODE, 128, LOAD>(p, a_matrix, b_matrix, st);
-        default: return launch<MODE, 64, LOAD>(p, a_matrix, b_matrix, st);
+        case 256: return launch<MODE, 256, LOAD, false>(p, a_matrix, b_matrix, st);
+        case 128: return launch<MODE, 128, LOAD, false>(p, a_matrix, b_matrix, st);
+        default: return launch<MODE, 64, LOAD, false>(p, a_matrix, b_matrix, st);
     }
 }
 
@@ -874,6 +1012,7 @@ cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cuda
 }  // namespace
 
 void conv_tc_set_force_gather(int on) { g_force_gather = on ? 1 : 0; }
+void conv_tc_set_epi_kb(int kb) { g_epi_kb = kb; }
 
 bool conv_tc_supported(const ConvGeom& g, ConvMode mode) {
     if (g.n < 1 || g.h < 1 || g.w < 1 || g.c < 1 || g.k < 1) return false;
@@ -895,14 +1034,16 @@ size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
     return sp.splits > 1 ? size_t(sp.splits) * s.M * s.Ncol * sizeof(float) : 0;
 }
 
-int conv_tc_launches(const ConvGeom& g, ConvMode mode) {
+bool conv_tc_narrow(const ConvGeom& g) { return narrow_plan(g).use; }
+
+int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready) {
     const NarrowPlan q = narrow_plan(g);
     if (mode == ConvMode::Fwd) return q.use ? 3 : 1;
     if (mode == ConvMode::Dgrad) return g.stride_h * g.stride_w;
     const ConvGeom& gw = q.use ? q.g1 : g;
     const ConvShape s = make_shape(gw, mode);
     const int split = plan_splits(s, pick_bn(s.Ncol)).splits > 1 ? 2 : 1;
-    return split + (q.use ? 2 : 0);
+    return split + (q.use ? (cols_ready ? 1 : 2) : 0);
 }
 
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
@@ -917,7 +1058,7 @@ cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const E
         if (e != cudaSuccess) return e;
         auto* wp = reinterpret_cast<__nv_bfloat16*>(ws + align256(q.col_bytes));
         narrow_pack_weights<<<std::max(1, std::min(g.k * q.kc / 256 + 1, 1024)), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(w), wp, g, q.cv, q.rw);
+            static_cast<const __nv_bfloat16*>(w), wp, g, q.cv, q.rw, q.kc);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         p.s = make_shape(q.g1, ConvMode::Fwd);
         a_matrix = ws;
@@ -967,19 +1108,19 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, co
 }
 
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
-                          void* workspace, cudaStream_t st) {
+                          void* workspace, cudaStream_t st, bool cols_ready) {
     const NarrowPlan q = narrow_plan(g);
     if (q.use) {
         if (workspace == nullptr) return cudaErrorInvalidValue;
         char* ws = static_cast<char*>(workspace);
-        cudaError_t e = narrow_im2col(g, q, x, ws, st);
+        cudaError_t e = cols_ready ? cudaSuccess : narrow_im2col(g, q, x, ws, st);
         if (e != cudaSuccess) return e;
         float* dwp = reinterpret_cast<float*>(ws + align256(q.col_bytes));
         void* rest = ws + align256(q.col_bytes) + align256(size_t(g.k) * q.kc * 4);
         if ((e = conv_tc_wgrad(q.g1, dy, ws, dwp, rest, st)) != cudaSuccess) return e;
         const int total = g.k * g.r * g.s * g.c;
         narrow_scatter_grad<<<std::max(1, std::min(total / 256 + 1, 1024)), 256, 0, st>>>(
-            dwp, dw, g, q.cv, q.rw);
+            dwp, dw, g, q.cv, q.rw, q.kc);
         return cudaGetLastError();
     }
     Params p{};

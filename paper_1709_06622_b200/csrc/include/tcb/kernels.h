@@ -38,17 +38,23 @@ struct Epilogue {
 // stem) run as a plain GEMM over an explicit im2col in `workspace`; without a
 // workspace they take the implicit im2col path.
 size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode);
-int conv_tc_launches(const ConvGeom& g, ConvMode mode);  // kernels one call launches
+int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready = false);  // kernels per call
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
                         void* y, cudaStream_t st, void* workspace = nullptr);
 cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wT, const Epilogue& ep,
                           void* dx, cudaStream_t st);
+// cols_ready: `workspace` still holds the forward pass's explicit im2col of x
+// (narrow layers; the trainer gives them a dedicated workspace for the step).
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
-                          void* workspace, cudaStream_t st);
+                          void* workspace, cudaStream_t st, bool cols_ready = false);
+bool conv_tc_narrow(const ConvGeom& g);
 bool conv_tc_supported(const ConvGeom& g, ConvMode mode);
 // 1: always use the cp.async gather operand path (tests / A-B comparisons);
 // 0: pick plain-TMA / im2col-TMA / gather per geometry.
 void conv_tc_set_force_gather(int on);
+// TMA epilogue for layers with at most `kb` 64-deep k-blocks (0 = never,
+// -1 = default: $TCB_CONV_EPI_KB or 16).
+void conv_tc_set_epi_kb(int kb);
 
 // ---- FP32 FFMA implicit GEMM (parity mode) ----
 size_t conv_ffma_workspace(const ConvGeom& g, ConvMode mode);

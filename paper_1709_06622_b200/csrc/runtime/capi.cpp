@@ -299,7 +299,9 @@ TCB_API int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_
 TCB_API void tcb_free(void* p) { std::free(p); }
 
 TCB_API int tcb_set_conv_operand_path(int mode) {
-    if (mode < 0 || mode > 1) return fail(TCB_ERR_INVALID, "mode must be 0 (auto) or 1 (gather)");
-    conv_tc_set_force_gather(mode);
+    if (mode < 0 || mode > 2)
+        return fail(TCB_ERR_INVALID, "mode must be 0 (auto), 1 (gather) or 2 (register epilogue)");
+    conv_tc_set_force_gather(mode == 1);
+    conv_tc_set_epi_kb(mode == 2 ? 0 : -1);
     return TCB_OK;
 }

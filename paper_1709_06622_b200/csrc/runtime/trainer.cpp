@@ -66,6 +66,8 @@ struct Node {
     int f = 0, s = 0, p = 0;
     // arena offsets (bytes)
     size_t act = 0, grad = 0, argmax = 0, wT = 0;
+    size_t nws = 0;  // narrow (explicit im2col) layers: own workspace, col kept fwd -> wgrad
+    bool narrow = false;
     // backward plan for this node's OUTPUT tensor
     int final_writer = -1;              // consumer node that writes G[this] last
     std::vector<int> compute_from;      // consumers with a computed contribution
@@ -330,10 +332,14 @@ int allocate(tcb_trainer* t) {
         if (nd.op != Op::Input && nd.grad_alias < 0) nd.grad = b.take(elems * es);
         if (nd.op == Op::MaxPool) nd.argmax = b.take(elems);
         if (nd.op == Op::Conv) {
+            nd.narrow = t->bf16 && nd.algo_id == TCB_ALGO_GEMM && conv_tc_narrow(nd.g);
             if (nd.algo_id == TCB_ALGO_GEMM) {
-                ws = std::max(ws, t->bf16 ? std::max(conv_tc_workspace(nd.g, ConvMode::Wgrad),
-                                                     conv_tc_workspace(nd.g, ConvMode::Fwd))
-                                          : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
+                if (nd.narrow)
+                    nd.nws = b.take(std::max(conv_tc_workspace(nd.g, ConvMode::Wgrad),
+                                             conv_tc_workspace(nd.g, ConvMode::Fwd)));
+                else
+                    ws = std::max(ws, t->bf16 ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
+                                              : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
                 if (t->bf16 && nd.need_dgrad) nd.wT = b.take(nd.wcount * 2);
             } else {
                 // Winograd / FFT transformed planes; one shared region, passes run in order
@@ -444,7 +450,7 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                     TRY_CUDA(fft_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
                 else if (t->bf16)
                     TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
-                                         ep, t->at(nd.act), st, t->at(t->off_ws)));
+                                         ep, t->at(nd.act), st, nd.narrow ? t->at(nd.nws) : nullptr));
                 else
                     TRY_CUDA(conv_ffma_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
                                            ep, t->at<float>(nd.act), st));
@@ -571,11 +577,12 @@ int backward(tcb_trainer* t, cudaStream_t st) {
                 TRY_CUDA(fft_wgrad(nd.g, t->dt, t->at(nd.grad), t->at(x.act), grad + nd.woff,
                                    t->at(t->off_ws), st));
             else if (t->bf16)
-                TRY_CUDA(conv_tc_wgrad(nd.g, t->at(nd.grad), t->at(x.act), grad + nd.woff, t->at(t->off_ws), st));
+                TRY_CUDA(conv_tc_wgrad(nd.g, t->at(nd.grad), t->at(x.act), grad + nd.woff,
+                                       t->at(nd.narrow ? nd.nws : t->off_ws), st, nd.narrow));
             else
                 TRY_CUDA(conv_ffma_wgrad(nd.g, t->at<float>(nd.grad), t->at<float>(x.act), grad + nd.woff,
                                          t->at(t->off_ws), st));
-            t->launches += (t->bf16 && nd.algo_id == TCB_ALGO_GEMM) ? conv_tc_launches(nd.g, ConvMode::Wgrad) : 2;
+            t->launches += (t->bf16 && nd.algo_id == TCB_ALGO_GEMM) ? conv_tc_launches(nd.g, ConvMode::Wgrad, nd.narrow) : 2;
             if (nd.bias) {
                 TRY_CUDA(column_sum(t->dt, t->at(nd.grad), grad + nd.boff, nd.n * nd.h * nd.w, nd.g.k,
                                     t->at<float>(t->off_colsum), st));
@@ -860,6 +867,8 @@ TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
             L["wcount"] = nd.wcount;
             L["boff"] = nd.bias ? json(nd.boff) : json(nullptr);
             L["init_scale"] = nd.init_scale;
+            L["algo"] = nd.algo;
+            L["explicit_im2col"] = nd.narrow;
             const size_t first = nd.woff / std::max<size_t>(t->shard, 1);
             const size_t last_el = (nd.bias ? nd.boff + nd.g.k : nd.woff + nd.wcount) - 1;
             L["shards"] = {first, last_el / std::max<size_t>(t->shard, 1)};

@@ -69,14 +69,16 @@ def _host(t):
     return t.float().cpu().numpy()
 
 
-@pytest.fixture(params=["auto", "gather"])
+@pytest.fixture(params=["auto", "gather", "regepi"])
 def operand_path(request):
     """auto = 2-D TMA (1x1/s1) or im2col-mode TMA (channels % 64 == 0) where they
-    apply; gather = force the cp.async gather path. Both must agree with the oracle."""
+    apply, TMA epilogue on K-light layers; gather = force the cp.async gather
+    path; regepi = auto loads with the register epilogue everywhere. All must
+    agree with the oracle."""
     import ctypes
     lib = _dev().lib()
     lib.tcb_set_conv_operand_path.argtypes = [ctypes.c_int]
-    lib.tcb_set_conv_operand_path(1 if request.param == "gather" else 0)
+    lib.tcb_set_conv_operand_path({"auto": 0, "gather": 1, "regepi": 2}[request.param])
     yield request.param
     lib.tcb_set_conv_operand_path(0)
 
@@ -86,7 +88,7 @@ def operand_path(request):
 def test_conv_gemm_parity(oracle, prec, spec, operand_path):
     if prec == "bf16" and spec in FFMA_ONLY:
         pytest.skip("tensor-core path needs C, K multiples of 8")
-    if prec == "ffma" and operand_path == "gather":
+    if prec == "ffma" and operand_path != "auto":
         pytest.skip("operand path only applies to the tensor-core kernel")
     dev = _dev()
     name, n, h, w, c, k, r, pad, stride = spec

@@ -85,8 +85,20 @@ def test_bf16_end_to_end_drift_is_small_on_shallow_net(oracle):
 
 
 def test_resnet50_geometry_step_bf16(oracle):
-    """C3 geometry (full ResNet-50-shaped graph, 224x224) at batch 1, layer-local."""
-    _check(oracle, _models().resnet50(batch=1, precision="bf16"))
+    """C3 geometry (full ResNet-50-shaped graph, 224x224) at batch 1, layer-local.
+    The 3-channel stem runs as explicit im2col + plain GEMM (fwd and wgrad)."""
+    t, _ = _check(oracle, _models().resnet50(batch=1, precision="bf16"))
+    convs = [L for L in t.describe()["layers"] if L["op"] == "conv"]
+    assert convs[0]["explicit_im2col"] and not any(L["explicit_im2col"] for L in convs[1:])
+
+
+def test_explicit_im2col_stem_batch8(oracle):
+    """Stem-only net at batch 8: explicit-im2col fwd (TMA epilogue) and wgrad
+    (col kept from the forward pass) against the oracle, layer-local."""
+    cfg = _models().from_net("input 64 64 3\nconv 7 2 3 64\npool 3 2 1\nconv 3 1 1 64\nfc 10\n",
+                             batch=8, precision="bf16")
+    t, _ = _check(oracle, cfg)
+    assert t.describe()["layers"][1]["explicit_im2col"]
 
 
 def test_lenet_step_c1(oracle):
