@@ -74,7 +74,9 @@ int tcb_conv_out_hw(const tcb_conv_geom* g, int* ho, int* wo);
  * catalog's "absent algorithm is a value" rule
  * (/root/reference/proj/include/traincap/catalog.hpp:60-62).
  * *workspace_bytes receives the plan's scratch need; the profiler records it
- * as CostEntry::memory_bits = 8 * workspace_bytes. */
+ * as CostEntry::memory_bits = 8 * workspace_bytes. The workspace must be
+ * zero-filled once before its first use (it holds self-resetting split-K
+ * counters); it can then be reused across calls without clearing. */
 int tcb_conv_plan_create(const tcb_conv_geom* g, int algo, int prec, tcb_conv_plan** plan,
                          size_t* workspace_bytes);
 int tcb_conv_plan_destroy(tcb_conv_plan* plan);

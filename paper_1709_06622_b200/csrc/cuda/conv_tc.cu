@@ -70,6 +70,10 @@ struct Params {
     const __nv_bfloat16* mask;
     int relu;
     int m_tiles, n_tiles, splits, kb_total, kb_per_split, num_tiles;
+    // wgrad split-K reduced in-kernel: set when all units are co-resident (one
+    // wave); partials in `out`, final sums to `dw`, 2 self-resetting counters per tile
+    float* dw;
+    int* counters;
     // dgrad phase
     DgradPhase ph;
     FastDiv d_hwq, d_wq, d_ts;
@@ -311,6 +315,69 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
     }
 }
 
+
+// In-kernel split-K reduction of one wgrad tile, run by the 256 epilogue
+// threads of every split's CTA once all splits of the tile have stored their
+// partials (the units of one wave are co-resident, so waiting is safe). CTA
+// `split` sums rows [split*per, ..) of the tile over splits 0..S-1 in order —
+// the same fixed order as split_reduce, so results are deterministic.
+template <int BN>
+__device__ __forceinline__ void split_reduce_tile(const Params& p, const TileCoord& tc, int et) {
+    const ConvShape& s = p.s;
+    int* cnt = p.counters + 2 * (tc.mt * p.n_tiles + tc.nt);
+    __threadfence();
+    asm volatile("bar.sync 2, %0;" ::"n"(kEpilogueThreads) : "memory");
+    if (et == 0) {
+        atomicAdd(cnt, 1);
+        while (*reinterpret_cast<volatile int*>(cnt) < p.splits) __nanosleep(100);
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(kEpilogueThreads) : "memory");
+    __threadfence();
+    const int rows = min(BM, s.M - tc.mt * BM), cols = min(BN, s.Ncol - tc.nt * BN);
+    const int per = (rows + p.splits - 1) / p.splits;
+    const int r0 = tc.split * per, r1 = min(rows, r0 + per);
+    const size_t plane = size_t(s.M) * s.Ncol;
+    if (s.Ncol % 4 == 0) {
+        // float4 columns; up to 8 splits' loads in flight before the in-order adds
+        const int cols4 = cols / 4;
+        for (int i = et; i < (r1 - r0) * cols4; i += kEpilogueThreads) {
+            const int rr = i / cols4, cc = (i - rr * cols4) * 4;
+            const size_t o = size_t(tc.mt * BM + r0 + rr) * s.Ncol + tc.nt * BN + cc;
+            const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(p.out) + o);
+            const size_t plane4 = plane / 4;
+            float4 acc = __ldcg(src);
+            for (int k0 = 1; k0 < p.splits; k0 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (k0 + j < p.splits) v[j] = __ldcg(src + (k0 + j) * plane4);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (k0 + j < p.splits) {
+                        acc.x += v[j].x;
+                        acc.y += v[j].y;
+                        acc.z += v[j].z;
+                        acc.w += v[j].w;
+                    }
+            }
+            *reinterpret_cast<float4*>(p.dw + o) = acc;
+        }
+    } else {
+        for (int i = et; i < (r1 - r0) * cols; i += kEpilogueThreads) {
+            const int rr = i / cols, cc = i - rr * cols;
+            const size_t o = size_t(tc.mt * BM + r0 + rr) * s.Ncol + tc.nt * BN + cc;
+            const float* src = static_cast<const float*>(p.out) + o;
+            float acc = __ldcg(src);
+            for (int k = 1; k < p.splits; ++k) acc += __ldcg(src + k * plane);
+            p.dw[o] = acc;
+        }
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(kEpilogueThreads) : "memory");
+    if (et == 0 && atomicAdd(cnt + 1, 1) == p.splits - 1) {
+        cnt[0] = 0;
+        cnt[1] = 0;
+    }
+}
 
 // --------------------------------------------------------------- kernel ----
 // Operand load modes.
@@ -710,6 +777,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
+            if constexpr (MODE == ConvMode::Wgrad) {
+                if (p.counters) split_reduce_tile<BN>(p, tc, tid - kProducerThreads);
+            }
         }
     }
 
@@ -865,7 +935,9 @@ struct SplitPlan {
 SplitPlan plan_splits(const ConvShape& s, int bn) {
     const int kb_total = (s.Kdim + BK - 1) / BK;
     const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + bn - 1) / bn);
-    int want = std::max(1, (2 * num_sms() + tiles - 1) / tiles);
+    // one exact wave: splits * tiles <= #SMs, so every CTA runs one equal unit
+    // (no tail round) and the fp32 partials stay as few as the wave allows
+    int want = std::max(1, num_sms() / tiles);
     want = std::min(want, std::max(1, kb_total / 4));  // keep >= 4 k-blocks per split
     want = std::min(want, 64);
     const int per = (kb_total + want - 1) / want;
@@ -1036,13 +1108,15 @@ size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
 
 bool conv_tc_narrow(const ConvGeom& g) { return narrow_plan(g).use; }
 
-int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready) {
+int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool counters) {
     const NarrowPlan q = narrow_plan(g);
     if (mode == ConvMode::Fwd) return q.use ? 3 : 1;
     if (mode == ConvMode::Dgrad) return g.stride_h * g.stride_w;
     const ConvGeom& gw = q.use ? q.g1 : g;
     const ConvShape s = make_shape(gw, mode);
-    const int split = plan_splits(s, pick_bn(s.Ncol)).splits > 1 ? 2 : 1;
+    const SplitPlan sp = plan_splits(s, pick_bn(s.Ncol));
+    const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + pick_bn(s.Ncol) - 1) / pick_bn(s.Ncol));
+    const int split = (sp.splits > 1 && !(counters && tiles * sp.splits <= num_sms())) ? 2 : 1;
     return split + (q.use ? (cols_ready ? 1 : 2) : 0);
 }
 
@@ -1108,7 +1182,7 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, co
 }
 
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
-                          void* workspace, cudaStream_t st, bool cols_ready) {
+                          void* workspace, cudaStream_t st, bool cols_ready, int* counters) {
     const NarrowPlan q = narrow_plan(g);
     if (q.use) {
         if (workspace == nullptr) return cudaErrorInvalidValue;
@@ -1117,7 +1191,8 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
         if (e != cudaSuccess) return e;
         float* dwp = reinterpret_cast<float*>(ws + align256(q.col_bytes));
         void* rest = ws + align256(q.col_bytes) + align256(size_t(g.k) * q.kc * 4);
-        if ((e = conv_tc_wgrad(q.g1, dy, ws, dwp, rest, st)) != cudaSuccess) return e;
+        if ((e = conv_tc_wgrad(q.g1, dy, ws, dwp, rest, st, false, counters)) != cudaSuccess)
+            return e;
         const int total = g.k * g.r * g.s * g.c;
         narrow_scatter_grad<<<std::max(1, std::min(total / 256 + 1, 1024)), 256, 0, st>>>(
             dwp, dw, g, q.cv, q.rw, q.kc);
@@ -1132,8 +1207,15 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
     p.kb_per_split = sp.kb_per_split;
     p.out = sp.splits > 1 ? workspace : static_cast<void*>(dw);
     if (sp.splits > 1 && workspace == nullptr) return cudaErrorInvalidValue;
+    const int bn = pick_bn(p.s.Ncol);
+    const int tiles = ((p.s.M + BM - 1) / BM) * ((p.s.Ncol + bn - 1) / bn);
+    const bool fused = counters && sp.splits > 1 && tiles * sp.splits <= num_sms();
+    if (fused) {
+        p.dw = dw;
+        p.counters = counters;
+    }
     cudaError_t e = dispatch<ConvMode::Wgrad>(p, dy, x, st);
-    if (e != cudaSuccess || sp.splits == 1) return e;
+    if (e != cudaSuccess || sp.splits == 1 || fused) return e;
     return split_reduce(static_cast<const float*>(workspace), sp.splits,
                         size_t(p.s.M) * p.s.Ncol, dw, st);
 }

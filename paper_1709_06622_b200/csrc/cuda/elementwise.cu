@@ -75,15 +75,16 @@ __global__ void transpose_krsc_kernel(const T* __restrict__ w, T* __restrict__ w
 // w[K][R][S][C] -> per-phase packed dgrad operand [C][tr][ts][K] (see DgradPhase);
 // one (r, s) tap per blockIdx.z, 32x32 (c, k) tiles through shared memory.
 template <typename T>
-__global__ void pack_dgrad_kernel(const T* __restrict__ w, T* __restrict__ out, ConvGeom g) {
+__device__ __forceinline__ void pack_dgrad_block(const T* __restrict__ w, T* __restrict__ out,
+                                                 const ConvGeom& g, int bx, int by, int bz) {
     __shared__ T tile[32][33];
-    const int r = blockIdx.z / g.s, s = blockIdx.z % g.s;
+    const int r = bz / g.s, s = bz % g.s;
     const int ph = ((r - g.pad_h) % g.stride_h + g.stride_h) % g.stride_h;
     const int pw = ((s - g.pad_w) % g.stride_w + g.stride_w) % g.stride_w;
     const DgradPhase d = dgrad_phase(g, ph, pw);
     // taps are stored flipped (ri' = tr - 1 - ri) so the dy operand walks forward
     const int ri = d.tr - 1 - (r - d.r0) / g.stride_h, si = d.ts - 1 - (s - d.s0) / g.stride_w;
-    const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const int c0 = bx * 32, k0 = by * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int k = k0 + i, c = c0 + threadIdx.x;
         if (k < g.k && c < g.c) tile[i][threadIdx.x] = w[((size_t(k) * g.r + r) * g.s + s) * g.c + c];
@@ -94,6 +95,28 @@ __global__ void pack_dgrad_kernel(const T* __restrict__ w, T* __restrict__ out, 
         if (k < g.k && c < g.c)
             out[d.woff + ((size_t(c) * d.tr + ri) * d.ts + si) * g.k + k] = tile[threadIdx.x][i];
     }
+}
+
+template <typename T>
+__global__ void pack_dgrad_kernel(const T* __restrict__ w, T* __restrict__ out, ConvGeom g) {
+    pack_dgrad_block<T>(w, out, g, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
+// Every layer's dgrad packing in one launch: block b belongs to the job with
+// the largest block_begin <= b.
+__global__ void pack_dgrad_batched_kernel(const PackDgradJob* __restrict__ jobs, int njobs) {
+    const int b = blockIdx.x;
+    int lo = 0, hi = njobs - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (jobs[mid].block_begin <= b) lo = mid; else hi = mid - 1;
+    }
+    const PackDgradJob& j = jobs[lo];
+    const int local = b - j.block_begin;
+    const int gx = (j.g.c + 31) / 32, gy = (j.g.k + 31) / 32;
+    pack_dgrad_block<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(j.w),
+                                    static_cast<__nv_bfloat16*>(j.out), j.g, local % gx,
+                                    (local / gx) % gy, local / (gx * gy));
 }
 
 template <typename T>
@@ -122,10 +145,52 @@ __global__ void split_reduce4_kernel(const float4* __restrict__ parts, int split
                                      float4* __restrict__ out) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
          i += size_t(gridDim.x) * blockDim.x) {
-        float4 acc = parts[i];
-        for (int s = 1; s < splits; ++s) {
-            const float4 v = parts[size_t(s) * n4 + i];
-            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        float4 acc = __ldcs(parts + i);
+        for (int s0 = 1; s0 < splits; s0 += 8) {  // 8 loads in flight, adds in split order
+            float4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (s0 + j < splits) v[j] = __ldcs(parts + size_t(s0 + j) * n4 + i);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (s0 + j < splits) {
+                    acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w;
+                }
+        }
+        out[i] = acc;
+    }
+}
+
+// Many splits over few elements (early wgrad layers: up to 64 splits of a
+// 64 x 576 tile): 8 split-groups per element run in parallel, group g summing
+// splits g, g+8, ... in order, then the 8 group sums are added in order g = 0..7
+// — a fixed tree, so the result is deterministic.
+__global__ void __launch_bounds__(256) split_reduce4_tree_kernel(const float4* __restrict__ parts,
+                                                                 int splits, size_t n4,
+                                                                 float4* __restrict__ out) {
+    __shared__ float4 part[8][32];
+    const int e = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const size_t i = blockIdx.x * size_t(32) + e;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < n4) {
+        for (int s0 = g; s0 < splits; s0 += 64) {
+            float4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (s0 + 8 * j < splits) v[j] = __ldcs(parts + size_t(s0 + 8 * j) * n4 + i);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (s0 + 8 * j < splits) {
+                    acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w;
+                }
+        }
+    }
+    part[g][e] = acc;
+    __syncthreads();
+    if (g == 0 && i < n4) {
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+            acc.x += part[k][e].x; acc.y += part[k][e].y; acc.z += part[k][e].z; acc.w += part[k][e].w;
         }
         out[i] = acc;
     }
@@ -277,13 +342,39 @@ __global__ void avgpool_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, i
 
 template <typename T>
 __global__ void avgpool_bwd_kernel(const T* __restrict__ dy, T* __restrict__ dx, int N, int HW,
-                                   int C) {
+                                   int C, const T* __restrict__ mask) {
     const size_t total = size_t(N) * HW * C;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
          i += size_t(gridDim.x) * blockDim.x) {
         const int c = int(i % C);
         const int n = int(i / (size_t(HW) * C));
-        dx[i] = from_f32<T>(to_f32<T>(dy[size_t(n) * C + c]) / float(HW));
+        float v = to_f32<T>(dy[size_t(n) * C + c]) / float(HW);
+        if (mask && !(to_f32<T>(mask[i]) > 0.f)) v = 0.f;
+        dx[i] = from_f32<T>(v);
+    }
+}
+
+// bf16, C % 8 == 0: 8 channels per thread, 32-bit index math, fused ReLU mask.
+__global__ void avgpool_bwd_vec_kernel(const __nv_bfloat16* __restrict__ dy,
+                                       __nv_bfloat16* __restrict__ dx, int total8, int HW, int cg,
+                                       const __nv_bfloat16* __restrict__ mask) {
+    const float inv = 1.f / float(HW);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total8; i += gridDim.x * blockDim.x) {
+        const int ci = i % cg, n = i / (HW * cg);
+        const uint4 g = reinterpret_cast<const uint4*>(dy)[n * cg + ci];
+        const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&g);
+        uint4 m = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);  // 1.0
+        if (mask) m = reinterpret_cast<const uint4*>(mask)[i];
+        const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&m);
+        uint4 o;
+        __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 a = __bfloat1622float2(gh[j]);
+            const float2 k = __bfloat1622float2(mh[j]);
+            oh[j] = __floats2bfloat162_rn(k.x > 0.f ? a.x * inv : 0.f, k.y > 0.f ? a.y * inv : 0.f);
+        }
+        reinterpret_cast<uint4*>(dx)[i] = o;
     }
 }
 
@@ -392,6 +483,17 @@ cudaError_t pack_dgrad_weights(DType dt, const void* w, void* packed, const Conv
     return cudaGetLastError();
 }
 
+int pack_dgrad_blocks(const ConvGeom& g) {
+    return ((g.c + 31) / 32) * ((g.k + 31) / 32) * g.r * g.s;
+}
+
+cudaError_t pack_dgrad_weights_batched(const PackDgradJob* jobs, int njobs, int total_blocks,
+                                       cudaStream_t st) {
+    if (njobs == 0) return cudaSuccess;
+    pack_dgrad_batched_kernel<<<total_blocks, dim3(32, 8), 0, st>>>(jobs, njobs);
+    return cudaGetLastError();
+}
+
 size_t column_sum_workspace(int rows, int cols) {
     const int chunks = std::min(rows, 512);
     return size_t(chunks) * cols * sizeof(float);
@@ -415,8 +517,11 @@ cudaError_t split_reduce(const float* parts, int splits, size_t n, float* out, c
     if (n == 0) return cudaSuccess;
     const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(parts) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    if (vec)
-        split_reduce4_kernel<<<grid_for(n / 4), kBlock, 0, st>>>(
+    if (vec && splits >= 16 && n / 4 < size_t(num_sms()) * 256 * 4)
+        split_reduce4_tree_kernel<<<static_cast<int>((n / 4 + 31) / 32), 256, 0, st>>>(
+            reinterpret_cast<const float4*>(parts), splits, n / 4, reinterpret_cast<float4*>(out));
+    else if (vec)
+        split_reduce4_kernel<<<grid_for(n / 4, 2), kBlock, 0, st>>>(
             reinterpret_cast<const float4*>(parts), splits, n / 4, reinterpret_cast<float4*>(out));
     else
         split_reduce_kernel<<<grid_for(n), kBlock, 0, st>>>(parts, splits, n, out);
@@ -468,22 +573,22 @@ struct alignas(16) Vec {
     T v[V];
 };
 
-// Vectorised NHWC max pool: one thread = V consecutive channels of one output
-// pixel; argmax bytes stored V at a time. Same tie rule as the scalar kernel.
+// Vectorised NHWC max pool: one block per output row (n, ho), one thread =
+// V consecutive channels of one output pixel (32-bit index math only; the
+// row is contiguous so loads and stores coalesce). argmax bytes stored V at a
+// time. Same tie rule as the scalar kernel (first maximum in window order).
 template <typename T, int V>
-__global__ void maxpool_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                       uint8_t* __restrict__ arg, int N, int H, int W, int C,
-                                       int F, int S, int P, int Ho, int Wo) {
+__global__ void __launch_bounds__(256) maxpool_fwd_vec_kernel(
+    const T* __restrict__ x, T* __restrict__ y, uint8_t* __restrict__ arg, int N, int H, int W,
+    int C, int F, int S, int P, int Ho, int Wo) {
     const int cg = C / V;
-    const size_t total = size_t(N) * Ho * Wo * cg;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
-         i += size_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % cg) * V;
-        size_t t = i / cg;
-        const int wo = int(t % Wo);
-        t /= Wo;
-        const int ho = int(t % Ho);
-        const int n = int(t / Ho);
+    const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
+    const int h0 = ho * S - P;
+    const T* xn = x + size_t(n) * H * W * C;
+    const size_t orow = size_t(blockIdx.x) * Wo * C;
+    for (int i = threadIdx.x; i < Wo * cg; i += blockDim.x) {
+        const int wo = i / cg, c = (i - wo * cg) * V;
+        const int w0 = wo * S - P;
         float best[V];
         uint8_t bi[V];
 #pragma unroll
@@ -492,13 +597,12 @@ __global__ void maxpool_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ 
             bi[j] = 0;
         }
         for (int r = 0; r < F; ++r) {
-            const int h = ho * S - P + r;
+            const int h = h0 + r;
             if (h < 0 || h >= H) continue;
             for (int s = 0; s < F; ++s) {
-                const int w = wo * S - P + s;
+                const int w = w0 + s;
                 if (w < 0 || w >= W) continue;
-                const Vec<T, V> in =
-                    *reinterpret_cast<const Vec<T, V>*>(x + ((size_t(n) * H + h) * W + w) * C + c);
+                const Vec<T, V> in = *reinterpret_cast<const Vec<T, V>*>(xn + (h * W + w) * C + c);
 #pragma unroll
                 for (int j = 0; j < V; ++j) {
                     const float v = to_f32<T>(in.v[j]);
@@ -512,32 +616,30 @@ __global__ void maxpool_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ 
         Vec<T, V> out;
 #pragma unroll
         for (int j = 0; j < V; ++j) out.v[j] = from_f32<T>(best[j]);
-        const size_t o = ((size_t(n) * Ho + ho) * Wo + wo) * C + c;
+        const size_t o = orow + size_t(wo) * C + c;
         *reinterpret_cast<Vec<T, V>*>(y + o) = out;
         if (arg) {
+            Vec<uint8_t, V> a;
 #pragma unroll
-            for (int j = 0; j < V; ++j) arg[o + j] = bi[j];
+            for (int j = 0; j < V; ++j) a.v[j] = bi[j];
+            *reinterpret_cast<Vec<uint8_t, V>*>(arg + o) = a;
         }
     }
 }
 
-// Gather-form backward, V channels per thread, optional fused ReLU mask of the
-// pool input (dx *= [x > 0]).
+// Gather-form backward, one block per input row (n, h), V channels per
+// thread, optional fused ReLU mask of the pool input (dx *= [x > 0]).
 template <typename T, int V>
-__global__ void maxpool_bwd_vec_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ arg,
-                                       T* __restrict__ dx, const T* __restrict__ mask, int N,
-                                       int H, int W, int C, int F, int S, int P, int Ho, int Wo) {
+__global__ void __launch_bounds__(256) maxpool_bwd_vec_kernel(
+    const T* __restrict__ dy, const uint8_t* __restrict__ arg, T* __restrict__ dx,
+    const T* __restrict__ mask, int N, int H, int W, int C, int F, int S, int P, int Ho, int Wo) {
     const int cg = C / V;
-    const size_t total = size_t(N) * H * W * cg;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
-         i += size_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % cg) * V;
-        size_t t = i / cg;
-        const int w = int(t % W);
-        t /= W;
-        const int h = int(t % H);
-        const int n = int(t / H);
-        const int ho0 = max(0, (h + P - F + S) / S), ho1 = min(Ho - 1, (h + P) / S);
+    const int n = blockIdx.x / H, h = blockIdx.x - n * H;
+    const int ho0 = max(0, (h + P - F + S) / S), ho1 = min(Ho - 1, (h + P) / S);
+    const size_t nbase = size_t(n) * Ho * Wo * C;
+    const size_t irow = size_t(blockIdx.x) * W * C;
+    for (int i = threadIdx.x; i < W * cg; i += blockDim.x) {
+        const int w = i / cg, c = (i - w * cg) * V;
         const int wo0 = max(0, (w + P - F + S) / S), wo1 = min(Wo - 1, (w + P) / S);
         float acc[V];
 #pragma unroll
@@ -548,15 +650,16 @@ __global__ void maxpool_bwd_vec_kernel(const T* __restrict__ dy, const uint8_t* 
             for (int wo = wo0; wo <= wo1; ++wo) {
                 const int s = w - (wo * S - P);
                 if (s < 0 || s >= F) continue;
-                const size_t o = ((size_t(n) * Ho + ho) * Wo + wo) * C + c;
+                const size_t o = nbase + size_t(ho * Wo + wo) * C + c;
                 const Vec<T, V> g = *reinterpret_cast<const Vec<T, V>*>(dy + o);
+                const Vec<uint8_t, V> a = *reinterpret_cast<const Vec<uint8_t, V>*>(arg + o);
                 const uint8_t want = static_cast<uint8_t>(r * F + s);
 #pragma unroll
                 for (int j = 0; j < V; ++j)
-                    if (arg[o + j] == want) acc[j] += to_f32<T>(g.v[j]);
+                    if (a.v[j] == want) acc[j] += to_f32<T>(g.v[j]);
             }
         }
-        const size_t io = ((size_t(n) * H + h) * W + w) * C + c;
+        const size_t io = irow + size_t(w) * C + c;
         if (mask) {
             const Vec<T, V> m = *reinterpret_cast<const Vec<T, V>*>(mask + io);
 #pragma unroll
@@ -580,8 +683,9 @@ cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, i
     const size_t total = size_t(n) * ho * wo * c;
     TCB_DT_SWITCH(dt, T, {
         constexpr int V = 16 / sizeof(T);
-        if (c % V == 0 && aligned16(x) && aligned16(y))
-            maxpool_fwd_vec_kernel<T, V><<<grid_for(total / V, 2), kBlock, 0, st>>>(
+        if (c % V == 0 && aligned16(x) && aligned16(y) && (!arg || (reinterpret_cast<uintptr_t>(arg) % V) == 0) &&
+            size_t(h) * w * c < (size_t(1) << 31))
+            maxpool_fwd_vec_kernel<T, V><<<n * ho, 256, 0, st>>>(
                 static_cast<const T*>(x), static_cast<T*>(y), arg, n, h, w, c, f, s, p, ho, wo);
         else
             maxpool_fwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
@@ -596,8 +700,9 @@ cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, 
     const size_t total = size_t(n) * h * w * c;
     TCB_DT_SWITCH(dt, T, {
         constexpr int V = 16 / sizeof(T);
-        if (c % V == 0 && aligned16(dy) && aligned16(dx) && (!mask || aligned16(mask))) {
-            maxpool_bwd_vec_kernel<T, V><<<grid_for(total / V, 2), kBlock, 0, st>>>(
+        if (c % V == 0 && aligned16(dy) && aligned16(dx) && (!mask || aligned16(mask)) &&
+            (reinterpret_cast<uintptr_t>(arg) % V) == 0 && size_t(ho) * wo * c < (size_t(1) << 31)) {
+            maxpool_bwd_vec_kernel<T, V><<<n * h, 256, 0, st>>>(
                 static_cast<const T*>(dy), arg, static_cast<T*>(dx), static_cast<const T*>(mask), n,
                 h, w, c, f, s, p, ho, wo);
         } else {
@@ -619,9 +724,18 @@ cudaError_t avgpool_global_fwd(DType dt, const void* x, void* y, int n, int hw, 
 }
 
 cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw, int c,
-                               cudaStream_t st) {
-    TCB_DT_SWITCH(dt, T, (avgpool_bwd_kernel<T><<<grid_for(size_t(n) * hw * c, 2), kBlock, 0, st>>>(
-                              static_cast<const T*>(dy), static_cast<T*>(dx), n, hw, c)));
+                               cudaStream_t st, const void* mask) {
+    const size_t total = size_t(n) * hw * c;
+    if (dt == DType::BF16 && c % 8 == 0 && total / 8 < (size_t(1) << 31) && aligned16(dy) &&
+        aligned16(dx) && (!mask || aligned16(mask))) {
+        avgpool_bwd_vec_kernel<<<grid_for(total / 8, 2), kBlock, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx),
+            static_cast<int>(total / 8), hw, c / 8, static_cast<const __nv_bfloat16*>(mask));
+        return cudaGetLastError();
+    }
+    TCB_DT_SWITCH(dt, T, (avgpool_bwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
+                              static_cast<const T*>(dy), static_cast<T*>(dx), n, hw, c,
+                              static_cast<const T*>(mask))));
     return cudaGetLastError();
 }
 

@@ -38,15 +38,22 @@ struct Epilogue {
 // stem) run as a plain GEMM over an explicit im2col in `workspace`; without a
 // workspace they take the implicit im2col path.
 size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode);
-int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready = false);  // kernels per call
+int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready = false,
+                     bool counters = false);  // kernels per call
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
                         void* y, cudaStream_t st, void* workspace = nullptr);
 cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wT, const Epilogue& ep,
                           void* dx, cudaStream_t st);
 // cols_ready: `workspace` still holds the forward pass's explicit im2col of x
 // (narrow layers; the trainer gives them a dedicated workspace for the step).
+// counters: a dedicated, zero-initialised int buffer of at least
+// conv_tc_counter_ints() entries (self-resetting, reusable across calls, not
+// shared with concurrent launches). With it, split-K partials are reduced
+// inside the GEMM kernel; without it a separate split_reduce pass runs.
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
-                          void* workspace, cudaStream_t st, bool cols_ready = false);
+                          void* workspace, cudaStream_t st, bool cols_ready = false,
+                          int* counters = nullptr);
+inline constexpr int conv_tc_counter_ints() { return 2 * 1024; }
 bool conv_tc_narrow(const ConvGeom& g);
 bool conv_tc_supported(const ConvGeom& g, ConvMode mode);
 // 1: always use the cp.async gather operand path (tests / A-B comparisons);
@@ -97,6 +104,16 @@ cudaError_t transpose_krsc(DType dt, const void* w, void* wT, int K, int R, int 
 // B operand of conv_tc_dgrad; same total size as w; plain transpose at stride 1).
 cudaError_t pack_dgrad_weights(DType dt, const void* w, void* packed, const ConvGeom& g,
                                cudaStream_t st);
+// All bf16 dgrad packings of a network in one launch (job table in device memory).
+struct PackDgradJob {
+    const void* w;
+    void* out;
+    ConvGeom g;
+    int block_begin;  // prefix sum of pack_dgrad_blocks over earlier jobs
+};
+int pack_dgrad_blocks(const ConvGeom& g);
+cudaError_t pack_dgrad_weights_batched(const PackDgradJob* jobs, int njobs, int total_blocks,
+                                       cudaStream_t st);
 // out[j] = sum_i in[i][j] (rows x cols, fp32 result), deterministic.
 cudaError_t column_sum(DType dt, const void* in, float* out, int rows, int cols, float* ws,
                        cudaStream_t st);
@@ -120,7 +137,7 @@ cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, 
 cudaError_t avgpool_global_fwd(DType dt, const void* x, void* y, int n, int hw, int c,
                                cudaStream_t st);
 cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw, int c,
-                               cudaStream_t st);
+                               cudaStream_t st, const void* mask = nullptr);
 // logits rows are `ld` apart (ld >= classes; padded columns get zero gradient)
 cudaError_t softmax_xent(DType dt, const void* logits, const int32_t* labels, void* dlogits,
                          float* loss, int n, int classes, int ld, cudaStream_t st);

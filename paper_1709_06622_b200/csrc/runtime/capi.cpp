@@ -66,9 +66,11 @@ ConvPlanLayout conv_plan_layout(const ConvGeom& g, int algo, int prec) {
                             fft_workspace(g, ConvMode::Wgrad)});
     }
     L.colsum = column_sum_workspace(static_cast<int>(P), g.k);
+    L.counters = algo == TCB_ALGO_GEMM && prec == TCB_PREC_BF16 ? conv_tc_counter_ints() * sizeof(int) : 0;
     L.off_wT = align256(L.wgrad);
     L.off_colsum = L.off_wT + align256(L.wT);
-    L.total = L.off_colsum + align256(L.colsum);
+    L.off_counters = L.off_colsum + align256(L.colsum);
+    L.total = L.off_counters + align256(L.counters);
     return L;
 }
 
@@ -213,7 +215,10 @@ TCB_API int tcb_conv_wgrad(const tcb_conv_plan* plan, const void* dy, const void
     switch (plan->algo) {
         case TCB_ALGO_GEMM:
             e = plan->prec == TCB_PREC_BF16
-                    ? conv_tc_wgrad(plan->g, dy, x, dw, workspace, st)
+                    ? conv_tc_wgrad(plan->g, dy, x, dw, workspace, st, false,
+                                    workspace ? reinterpret_cast<int*>(static_cast<char*>(workspace) +
+                                                                       plan->layout.off_counters)
+                                              : nullptr)
                     : conv_ffma_wgrad(plan->g, static_cast<const float*>(dy),
                                       static_cast<const float*>(x), dw, workspace, st);
             break;

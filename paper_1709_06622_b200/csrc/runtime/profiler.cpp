@@ -38,6 +38,7 @@ struct DevBuf {
     void* p = nullptr;
     explicit DevBuf(size_t bytes) {
         if (cudaMalloc(&p, std::max<size_t>(bytes, 256)) != cudaSuccess) p = nullptr;
+        if (p) cudaMemset(p, 0, std::max<size_t>(bytes, 256));  // workspaces: split-K counters at 0
     }
     ~DevBuf() {
         if (p) cudaFree(p);
@@ -105,7 +106,10 @@ Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int rep
     };
     auto run_wgrad = [&]() -> cudaError_t {
         if (algo == TCB_ALGO_GEMM)
-            return dt == DType::BF16 ? conv_tc_wgrad(g, dy.p, x.p, static_cast<float*>(dw.p), ws.p, st)
+            return dt == DType::BF16 ? conv_tc_wgrad(g, dy.p, x.p, static_cast<float*>(dw.p), ws.p, st,
+                                                     false,
+                                                     reinterpret_cast<int*>(static_cast<char*>(ws.p) +
+                                                                            L.off_counters))
                                      : conv_ffma_wgrad(g, static_cast<float*>(dy.p), static_cast<float*>(x.p),
                                                        static_cast<float*>(dw.p), ws.p, st);
         if (algo == TCB_ALGO_WINOGRAD)

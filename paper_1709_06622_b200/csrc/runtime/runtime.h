@@ -20,8 +20,8 @@ bool geom_valid(const ConvGeom& g, std::string* why);
 
 // Byte layout of a conv plan's workspace: [wgrad split partials | wT | bias column sums].
 struct ConvPlanLayout {
-    size_t wgrad, wT, colsum;
-    size_t off_wT, off_colsum, total;
+    size_t wgrad, wT, colsum, counters;
+    size_t off_wT, off_colsum, off_counters, total;
 };
 ConvPlanLayout conv_plan_layout(const ConvGeom& g, int algo, int prec);
 bool algo_applies(const ConvGeom& g, int algo, int prec);

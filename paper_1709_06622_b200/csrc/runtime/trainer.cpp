@@ -108,6 +108,11 @@ struct tcb_trainer {
     size_t off_param = 0, off_grad = 0, off_mom = 0, off_wc = 0, off_ws = 0, off_colsum = 0;
     size_t off_labels = 0, off_loss = 0, off_input_f32 = 0;
     size_t ws_bytes = 0, colsum_bytes = 0;
+    size_t off_pack_jobs = 0;  // device table of the batched dgrad weight packing
+    size_t off_counters = 0;   // split-K counters of the in-kernel wgrad reduction
+    bool fused_split_reduce = false;  // config "fused_split_reduce" / $TCB_FUSED_SPLIT_REDUCE
+    int pack_njobs = 0, pack_blocks = 0;
+    bool pack_jobs_ready = false;
 
     cudaStream_t stream = nullptr;  // stream of the last step call
     bool timing = false;
@@ -158,6 +163,10 @@ int build_graph(tcb_trainer* t) {
     t->batch = cfg.at("batch").get<int>();
     t->classes = cfg.at("classes").get<int>();
     t->seed = cfg.value("seed", uint64_t(20260810));
+    {
+        const char* e = std::getenv("TCB_FUSED_SPLIT_REDUCE");
+        t->fused_split_reduce = cfg.value("fused_split_reduce", e != nullptr && e[0] == '1');
+    }
     t->lr = cfg.value("lr", 0.01f);
     t->momentum = cfg.value("momentum", 0.9f);
     t->weight_decay = cfg.value("weight_decay", 0.f);
@@ -358,6 +367,8 @@ int allocate(tcb_trainer* t) {
     t->ws_bytes = ws;
     t->colsum_bytes = colsum;
     t->off_ws = b.take(ws);
+    t->off_pack_jobs = b.take(t->nodes.size() * sizeof(PackDgradJob));
+    t->off_counters = b.take(conv_tc_counter_ints() * sizeof(int));
     t->off_colsum = b.take(colsum);
     t->off_labels = b.take(size_t(t->batch) * 4);
     t->off_loss = b.take(size_t(t->batch + 1) * 4);
@@ -368,7 +379,8 @@ int allocate(tcb_trainer* t) {
     if (e != cudaSuccess)
         return fail(TCB_ERR_OOM, "arena of " + std::to_string(t->arena_bytes) + " bytes: " +
                                      cudaGetErrorString(e));
-    return TCB_OK;
+    // zeroed once: the split-K counters in the workspaces must start at 0 (they reset themselves)
+    return check_cuda(cudaMemset(t->arena, 0, t->arena_bytes), "arena memset");
 }
 
 int pack_input(tcb_trainer* t, cudaStream_t st) {
@@ -421,12 +433,25 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
 // ------------------------------------------------------------------ step ---
 int refresh_transposes(tcb_trainer* t, cudaStream_t st) {
     if (!t->bf16) return TCB_OK;
-    for (const Node& nd : t->nodes) {
-        if (nd.op != Op::Conv || !nd.need_dgrad || nd.algo_id != TCB_ALGO_GEMM) continue;
-        TRY_CUDA(pack_dgrad_weights(DType::BF16, t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
-                                    t->at(nd.wT), nd.g, st));
-        t->launches++;
+    if (!t->pack_jobs_ready) {
+        std::vector<PackDgradJob> jobs;
+        int blocks = 0;
+        for (const Node& nd : t->nodes) {
+            if (nd.op != Op::Conv || !nd.need_dgrad || nd.algo_id != TCB_ALGO_GEMM) continue;
+            jobs.push_back({t->at<__nv_bfloat16>(t->off_wc) + nd.woff, t->at(nd.wT), nd.g, blocks});
+            blocks += pack_dgrad_blocks(nd.g);
+        }
+        t->pack_njobs = static_cast<int>(jobs.size());
+        t->pack_blocks = blocks;
+        if (!jobs.empty())
+            TRY_CUDA(cudaMemcpy(t->at(t->off_pack_jobs), jobs.data(), jobs.size() * sizeof(PackDgradJob),
+                                cudaMemcpyHostToDevice));
+        t->pack_jobs_ready = true;
     }
+    if (t->pack_njobs == 0) return TCB_OK;
+    TRY_CUDA(pack_dgrad_weights_batched(t->at<PackDgradJob>(t->off_pack_jobs), t->pack_njobs,
+                                        t->pack_blocks, st));
+    t->launches++;
     return TCB_OK;
 }
 
@@ -528,12 +553,13 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         return TCB_OK;
     }
     // the ReLU mask fuses into the pool backward when nothing else must be added first
-    const bool fuse_mask = mask_needed && extras.empty() && con.op == Op::MaxPool;
+    const bool fuse_mask = mask_needed && extras.empty();
     if (con.op == Op::MaxPool)
         TRY_CUDA(maxpool_bwd(t->dt, t->at(con.grad), t->at<uint8_t>(con.argmax), out, tgt.n, tgt.h, tgt.w,
                              tgt.c, con.f, con.s, con.p, st, fuse_mask ? t->at(tgt.act) : nullptr));
     else
-        TRY_CUDA(avgpool_global_bwd(t->dt, t->at(con.grad), out, tgt.n, tgt.h * tgt.w, tgt.c, st));
+        TRY_CUDA(avgpool_global_bwd(t->dt, t->at(con.grad), out, tgt.n, tgt.h * tgt.w, tgt.c, st,
+                                    fuse_mask ? t->at(tgt.act) : nullptr));
     t->launches++;
     for (const void* e : extras) {
         TRY_CUDA(add_inplace(t->dt, out, e, elems, st));
@@ -578,11 +604,12 @@ int backward(tcb_trainer* t, cudaStream_t st) {
                                    t->at(t->off_ws), st));
             else if (t->bf16)
                 TRY_CUDA(conv_tc_wgrad(nd.g, t->at(nd.grad), t->at(x.act), grad + nd.woff,
-                                       t->at(nd.narrow ? nd.nws : t->off_ws), st, nd.narrow));
+                                       t->at(nd.narrow ? nd.nws : t->off_ws), st, nd.narrow,
+                                       t->fused_split_reduce ? t->at<int>(t->off_counters) : nullptr));
             else
                 TRY_CUDA(conv_ffma_wgrad(nd.g, t->at<float>(nd.grad), t->at<float>(x.act), grad + nd.woff,
                                          t->at(t->off_ws), st));
-            t->launches += (t->bf16 && nd.algo_id == TCB_ALGO_GEMM) ? conv_tc_launches(nd.g, ConvMode::Wgrad, nd.narrow) : 2;
+            t->launches += (t->bf16 && nd.algo_id == TCB_ALGO_GEMM) ? conv_tc_launches(nd.g, ConvMode::Wgrad, nd.narrow, t->fused_split_reduce) : 2;
             if (nd.bias) {
                 TRY_CUDA(column_sum(t->dt, t->at(nd.grad), grad + nd.boff, nd.n * nd.h * nd.w, nd.g.k,
                                     t->at<float>(t->off_colsum), st));

@@ -116,7 +116,8 @@ class ConvPlan:
                                          ctypes.byref(h), ctypes.byref(ws)))
         self.handle = h
         self.workspace_bytes = ws.value
-        self.workspace = torch.empty(max(ws.value, 1), dtype=torch.uint8, device="cuda")
+        # zero-filled once: split-K counters inside must start at 0 (they self-reset)
+        self.workspace = torch.zeros(max(ws.value, 1), dtype=torch.uint8, device="cuda")
 
     def __del__(self):
         try:
