@@ -109,6 +109,10 @@ int tcb_maxpool_fwd(int dtype, const void* x, void* y, uint8_t* argmax, int n, i
                     int c, int f, int stride, int pad, void* stream);
 int tcb_maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, void* dx, int n, int h,
                     int w, int c, int f, int stride, int pad, void* stream);
+/* Backward of maxpool(relu(x)) in one pass: y is the pool output; windows
+ * with y <= 0 route no gradient (y equals the ReLU'd input at the argmax). */
+int tcb_maxpool_relu_bwd(int dtype, const void* dy, const uint8_t* argmax, const void* y, void* dx,
+                         int n, int h, int w, int c, int f, int stride, int pad, void* stream);
 int tcb_avgpool_global_fwd(int dtype, const void* x, void* y, int n, int hw, int c, void* stream);
 int tcb_avgpool_global_bwd(int dtype, const void* dy, void* dx, int n, int hw, int c,
                            void* stream);

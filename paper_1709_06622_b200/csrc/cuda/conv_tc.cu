@@ -64,6 +64,7 @@ struct Params {
     ConvShape s;
     const __nv_bfloat16* a;  // fwd: x   dgrad: dy   wgrad: dy
     const __nv_bfloat16* b;  // wgrad: x (gathered)
+    const __nv_bfloat16* wk; // dgrad TMA paths: the KRSC filters themselves (MN-major B)
     void* out;               // bf16 (fwd/dgrad) or fp32 partials [split][M][Ncol] (wgrad)
     const float* bias;
     const __nv_bfloat16* residual;
@@ -523,7 +524,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                                                     static_cast<uint16_t>(sx),
                                                     static_cast<uint16_t>(r));
                         }
-                        ptx::tma_load_2d(b_smem, &p.tmap_b, &full[stage], kb * BK, tc.nt * BN);
+                        if constexpr (MODE == ConvMode::Dgrad) {
+                            // B straight from w[K][R*S][C]: the k-block is filters k0..k0+63
+                            // of one (flipped) phase tap; BN/64 channel boxes of 8 KB
+                            uint32_t tap, k0, ri, si;
+                            s.d_k.divmod(static_cast<uint32_t>(kb * BK), tap, k0);
+                            p.d_ts.divmod(tap, ri, si);
+                            const int rf = p.ph.r0 + (p.ph.tr - 1 - static_cast<int>(ri)) * s.sh;
+                            const int sf = p.ph.s0 + (p.ph.ts - 1 - static_cast<int>(si)) * s.sw;
+#pragma unroll
+                            for (int j = 0; j < BN / 64; ++j)
+                                ptx::tma_load_3d(b_smem + j * 8192, &p.tmap_b, &full[stage],
+                                                 tc.nt * BN + j * 64, rf * s.S + sf,
+                                                 static_cast<int>(k0));
+                        } else {
+                            ptx::tma_load_2d(b_smem, &p.tmap_b, &full[stage], kb * BK, tc.nt * BN);
+                        }
                     }
                     if (++stage == C::kStages) {
                         stage = 0;
@@ -601,7 +617,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     } else if (warp == kMmaWarp) {
         // =============================================== MMA issuer ======
         constexpr uint32_t kMN = MODE == ConvMode::Wgrad ? 1u : 0u;
-        constexpr uint32_t idesc = ptx::make_idesc(1, BM, BN, kMN, kMN);
+        // dgrad with TMA operands reads B (the filters) MN-major
+        constexpr bool kBmn = MODE == ConvMode::Wgrad || (MODE == ConvMode::Dgrad && kTmaOnly);
+        constexpr uint32_t idesc = ptx::make_idesc(1, BM, BN, kMN, kBmn ? 1u : 0u);
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -627,6 +645,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                         } else if constexpr (LOAD == kIm2colC8) {
                             ad = ptx::interleave_desc(a_addr + k * 4096, 2048, 128);
                             bd = ptx::sw128_desc(b_addr + k * 32, 16, 1024);
+                        } else if constexpr (kBmn) {
+                            ad = ptx::sw128_desc(a_addr + k * 32, 16, 1024);
+                            bd = ptx::sw128_desc(b_addr + k * 2048, 8192, 1024);
                         } else {
                             ad = ptx::sw128_desc(a_addr + k * 32, 16, 1024);
                             bd = ptx::sw128_desc(b_addr + k * 32, 16, 1024);
@@ -847,7 +868,7 @@ NarrowPlan narrow_plan(const ConvGeom& g) {
     q.wp = (wo - 1) * g.stride_w + g.s;
     q.smem = size_t(g.r) * q.wp * q.cv * 2;
     q.use = g.c == 8 && q.cv < g.c && g.r * g.s > 1 && 2 * q.kc <= g.r * g.s * g.c &&
-            q.smem <= 48 * 1024;
+            q.smem <= 48 * 1024 && q.kc <= 1024;
     if (!q.use) return q;
     q.col_bytes = size_t(g.n) * ho * wo * q.kc * 2;
     q.g1 = ConvGeom{g.n, ho, wo, q.kc, g.k, 1, 1, 0, 0, 1, 1};
@@ -875,17 +896,30 @@ __global__ void __launch_bounds__(256) narrow_im2col_kernel(const __nv_bfloat16*
         for (int c = 0; c < cv; ++c) sm[i * cv + c] = e[c];
     }
     __syncthreads();
+    // one warp per output pixel, lane = 16-byte chunk q of its col row: the
+    // (r, t0) decode of a chunk is per-lane constant, stores are contiguous
     const int span = g.s * cv, qpp = kc / 8;
-    uint4* dst = reinterpret_cast<uint4*>(col + size_t(blockIdx.x) * wo * kc);
-    for (int i = threadIdx.x; i < wo * qpp; i += blockDim.x) {
-        const int ow = i / qpp, col0 = (i - ow * qpp) * 8;
-        const int r = col0 / rw, t0 = col0 - r * rw;
-        const __nv_bfloat16* src = sm + (r * wp + ow * g.stride_w) * cv;
-        __align__(16) __nv_bfloat16 v[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    int q_off[4], q_ok[4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-            v[e] = (r < g.r && t0 + e < span) ? src[t0 + e] : __float2bfloat16(0.f);
-        dst[i] = *reinterpret_cast<const uint4*>(v);
+    for (int k = 0; k < 4; ++k) {
+        const int q = lane + 32 * k;
+        const int col0 = q * 8, r = col0 / rw, t0 = col0 - r * rw;
+        q_ok[k] = q < qpp ? (r < g.r ? min(8, max(0, span - t0)) : 0) : -1;
+        q_off[k] = r * wp * cv + t0;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(col + size_t(blockIdx.x) * wo * kc);
+    for (int ow = warp; ow < wo; ow += nwarps) {
+        const __nv_bfloat16* base = sm + ow * g.stride_w * cv;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (q_ok[k] < 0) break;
+            __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                v[e] = e < q_ok[k] ? base[q_off[k] + e] : __float2bfloat16(0.f);
+            dst[size_t(ow) * qpp + lane + 32 * k] = *reinterpret_cast<const uint4*>(v);
+        }
     }
 }
 
@@ -971,8 +1005,13 @@ bool build_maps(Params& p, const void* a_matrix, const void* b_matrix, int bn) {
         return make_tmap_im2col_bf16(&p.tmap_b, b_matrix, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
                                      s.pw - (s.S - 1), s.ph - (s.R - 1), s.sw, s.sh, BK);
     }
-    // weight operand: row-major [Ncol][Kdim] bf16, boxes of BN rows x 64
-    if (!make_tmap_bf16_2d(&p.tmap_b, b_matrix, s.Ncol, s.Kdim, bn)) return false;
+    // weight operand: row-major [Ncol][Kdim] bf16, boxes of BN rows x 64 (fwd, gather
+    // dgrad on packed w^T); TMA dgrad reads the KRSC filters as [K][R*S][C] boxes
+    if (MODE == ConvMode::Dgrad && LOAD != kGather) {
+        if (!make_tmap_filters_bf16(&p.tmap_b, p.wk, s.K, size_t(s.R) * s.S, s.C)) return false;
+    } else if (!make_tmap_bf16_2d(&p.tmap_b, b_matrix, s.Ncol, s.Kdim, bn)) {
+        return false;
+    }
     if (LOAD == kPlain) return make_tmap_bf16_2d(&p.tmap_a, a_matrix, s.M, s.Kdim, BM);
     if (LOAD == kIm2colC8)
         return make_tmap_im2col_bf16(&p.tmap_a, a_matrix, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
@@ -1061,13 +1100,17 @@ cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, c
 
 int g_force_gather = -1;  // test hook: 1 = always use the cp.async gather path
 
-template <ConvMode MODE>
-cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
+bool force_gather() {
     if (g_force_gather < 0) {
         const char* e = getenv("TCB_CONV_FORCE_GATHER");
         g_force_gather = (e && e[0] == '1') ? 1 : 0;
     }
-    if (!g_force_gather) {
+    return g_force_gather == 1;
+}
+
+template <ConvMode MODE>
+cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
+    if (!force_gather()) {
         const bool plain = MODE == ConvMode::Dgrad
                                ? plain_geometry(p.s) && p.ph.tr == 1 && p.ph.ts == 1
                                : plain_geometry(p.s);
@@ -1148,8 +1191,17 @@ cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const E
     return dispatch<ConvMode::Fwd>(p, a_matrix, b_matrix, st);
 }
 
-cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, const Epilogue& ep,
-                          void* dx, cudaStream_t st) {
+bool conv_tc_dgrad_needs_pack(const ConvGeom& g) {
+    if (force_gather()) return true;
+    const bool plain = g.r == 1 && g.s == 1 && g.pad_h == 0 && g.pad_w == 0 && g.stride_h == 1 &&
+                       g.stride_w == 1;
+    const bool im2col = g.k % 64 == 0 && g.r <= 16 && g.s <= 16 && g.pad_h <= 15 && g.pad_w <= 15;
+    return !(plain || im2col);
+}
+
+cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* w, const void* wTp,
+                          const Epilogue& ep, void* dx, cudaStream_t st) {
+    if (conv_tc_dgrad_needs_pack(g) && wTp == nullptr) return cudaErrorInvalidValue;
     for (int ph = 0; ph < g.stride_h; ++ph) {
         for (int pw = 0; pw < g.stride_w; ++pw) {
             Params p{};
@@ -1162,6 +1214,7 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, co
             p.d_wq = FastDiv(static_cast<uint32_t>(p.ph.Wq));
             p.d_ts = FastDiv(static_cast<uint32_t>(std::max(p.ph.ts, 1)));
             p.a = static_cast<const __nv_bfloat16*>(dy);
+            p.wk = static_cast<const __nv_bfloat16*>(w);
             p.out = dx;
             p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
             p.mask = static_cast<const __nv_bfloat16*>(ep.mask);
@@ -1173,7 +1226,9 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wTp, co
                 e = cudaGetLastError();
             } else {
                 e = dispatch<ConvMode::Dgrad>(
-                    p, dy, static_cast<const __nv_bfloat16*>(wTp) + p.ph.woff, st);
+                    p, dy, wTp ? static_cast<const void*>(static_cast<const __nv_bfloat16*>(wTp) + p.ph.woff)
+                               : nullptr,
+                    st);
             }
             if (e != cudaSuccess) return e;
         }

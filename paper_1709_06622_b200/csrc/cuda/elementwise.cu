@@ -301,7 +301,7 @@ __global__ void maxpool_fwd_kernel(const T* __restrict__ x, T* __restrict__ y,
 template <typename T>
 __global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ arg,
                                    T* __restrict__ dx, int N, int H, int W, int C, int F, int S,
-                                   int P, int Ho, int Wo) {
+                                   int P, int Ho, int Wo, const T* __restrict__ ymask) {
     const size_t total = size_t(N) * H * W * C;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
          i += size_t(gridDim.x) * blockDim.x) {
@@ -322,7 +322,8 @@ __global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __re
                 const int s = w - (wo * S - P);
                 if (s < 0 || s >= F) continue;
                 const size_t o = ((size_t(n) * Ho + ho) * Wo + wo) * C + c;
-                if (arg[o] == r * F + s) acc += to_f32<T>(dy[o]);
+                if (arg[o] == r * F + s && (!ymask || to_f32<T>(ymask[o]) > 0.f))
+                    acc += to_f32<T>(dy[o]);
             }
         }
         dx[i] = from_f32<T>(acc);
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_vec_kernel(
 template <typename T, int V>
 __global__ void __launch_bounds__(256) maxpool_bwd_vec_kernel(
     const T* __restrict__ dy, const uint8_t* __restrict__ arg, T* __restrict__ dx,
-    const T* __restrict__ mask, int N, int H, int W, int C, int F, int S, int P, int Ho, int Wo) {
+    const T* __restrict__ ymask, int N, int H, int W, int C, int F, int S, int P, int Ho, int Wo) {
     const int cg = C / V;
     const int n = blockIdx.x / H, h = blockIdx.x - n * H;
     const int ho0 = max(0, (h + P - F + S) / S), ho1 = min(Ho - 1, (h + P) / S);
@@ -654,22 +655,223 @@ __global__ void __launch_bounds__(256) maxpool_bwd_vec_kernel(
                 const Vec<T, V> g = *reinterpret_cast<const Vec<T, V>*>(dy + o);
                 const Vec<uint8_t, V> a = *reinterpret_cast<const Vec<uint8_t, V>*>(arg + o);
                 const uint8_t want = static_cast<uint8_t>(r * F + s);
+                if (ymask) {
+                    const Vec<T, V> y = *reinterpret_cast<const Vec<T, V>*>(ymask + o);
 #pragma unroll
-                for (int j = 0; j < V; ++j)
-                    if (a.v[j] == want) acc[j] += to_f32<T>(g.v[j]);
+                    for (int j = 0; j < V; ++j)
+                        if (a.v[j] == want && to_f32<T>(y.v[j]) > 0.f) acc[j] += to_f32<T>(g.v[j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        if (a.v[j] == want) acc[j] += to_f32<T>(g.v[j]);
+                }
             }
         }
         const size_t io = irow + size_t(w) * C + c;
-        if (mask) {
-            const Vec<T, V> m = *reinterpret_cast<const Vec<T, V>*>(mask + io);
-#pragma unroll
-            for (int j = 0; j < V; ++j)
-                if (!(to_f32<T>(m.v[j]) > 0.f)) acc[j] = 0.f;
-        }
         Vec<T, V> out;
 #pragma unroll
         for (int j = 0; j < V; ++j) out.v[j] = from_f32<T>(acc[j]);
         *reinterpret_cast<Vec<T, V>*>(dx + io) = out;
+    }
+}
+
+// bf16 specialisations, 8 channels per thread as 4 packed bf16x2 lanes:
+// max / strict-greater via __hmax2 / __hgt2_mask (bit-identical to the
+// scalar rule: first maximum in window order wins), argmax codes as 16-bit
+// halves; backward matches argmax bytes with __vcmpeq4 and selects dy bits
+// with the mask, accumulating in fp32 as the generic kernel does.
+__global__ void __launch_bounds__(256) maxpool_fwd_bf16x8_kernel(
+    const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ arg,
+    int H, int W, int C, int F, int S, int P, int Ho, int Wo) {
+    const int cg = C / 8;
+    const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
+    const int h0 = ho * S - P;
+    const __nv_bfloat16* xn = x + size_t(n) * H * W * C;
+    const size_t orow = size_t(blockIdx.x) * Wo * C;
+    for (int i = threadIdx.x; i < Wo * cg; i += blockDim.x) {
+        const int wo = i / cg, c = (i - wo * cg) * 8;
+        const int w0 = wo * S - P;
+        __nv_bfloat162 best[4];
+        uint32_t idx[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            best[j] = __halves2bfloat162(__ushort_as_bfloat16(0xFF80u), __ushort_as_bfloat16(0xFF80u));
+            idx[j] = 0;
+        }
+        for (int r = 0; r < F; ++r) {
+            const int h = h0 + r;
+            if (h < 0 || h >= H) continue;
+            for (int sx = 0; sx < F; ++sx) {
+                const int w = w0 + sx;
+                if (w < 0 || w >= W) continue;
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(xn + (h * W + w) * C + c));
+                const uint32_t code = static_cast<uint32_t>(r * F + sx) * 0x00010001u;
+                const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&vw[j]);
+                    const uint32_t gt = __hgt2_mask(b, best[j]);
+                    best[j] = __hmax2(best[j], b);
+                    idx[j] = (idx[j] & ~gt) | (code & gt);
+                }
+            }
+        }
+        const size_t o = orow + size_t(wo) * C + c;
+        uint4 out;
+        out.x = *reinterpret_cast<uint32_t*>(&best[0]);
+        out.y = *reinterpret_cast<uint32_t*>(&best[1]);
+        out.z = *reinterpret_cast<uint32_t*>(&best[2]);
+        out.w = *reinterpret_cast<uint32_t*>(&best[3]);
+        *reinterpret_cast<uint4*>(y + o) = out;
+        if (arg)
+            *reinterpret_cast<uint2*>(arg + o) =
+                make_uint2(__byte_perm(idx[0], idx[1], 0x6420), __byte_perm(idx[2], idx[3], 0x6420));
+    }
+}
+
+__global__ void __launch_bounds__(256) maxpool_bwd_bf16x8_kernel(
+    const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
+    __nv_bfloat16* __restrict__ dx, const __nv_bfloat16* __restrict__ ymask, int H, int W, int C,
+    int F, int S, int P, int Ho, int Wo) {
+    const int cg = C / 8;
+    const int n = blockIdx.x / H, h = blockIdx.x - n * H;
+    const int ho0 = max(0, (h + P - F + S) / S), ho1 = min(Ho - 1, (h + P) / S);
+    const size_t nbase = size_t(n) * Ho * Wo * C;
+    const size_t irow = size_t(blockIdx.x) * W * C;
+    const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
+    for (int i = threadIdx.x; i < W * cg; i += blockDim.x) {
+        const int w = i / cg, c = (i - w * cg) * 8;
+        const int wo0 = max(0, (w + P - F + S) / S), wo1 = min(Wo - 1, (w + P) / S);
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int ho = ho0; ho <= ho1; ++ho) {
+            const int r = h - (ho * S - P);
+            if (r < 0 || r >= F) continue;
+            for (int wo = wo0; wo <= wo1; ++wo) {
+                const int sx = w - (wo * S - P);
+                if (sx < 0 || sx >= F) continue;
+                const size_t o = nbase + size_t(ho * Wo + wo) * C + c;
+                const uint4 g = __ldg(reinterpret_cast<const uint4*>(dy + o));
+                const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + o));
+                const uint32_t want = static_cast<uint32_t>(r * F + sx) * 0x01010101u;
+                const uint32_t lo = __vcmpeq4(a.x, want), hi = __vcmpeq4(a.y, want);
+                uint32_t m[4] = {__byte_perm(lo, 0, 0x1100), __byte_perm(lo, 0, 0x3322),
+                                 __byte_perm(hi, 0, 0x1100), __byte_perm(hi, 0, 0x3322)};
+                if (ymask) {
+                    const uint4 yv = __ldg(reinterpret_cast<const uint4*>(ymask + o));
+                    const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        m[j] &= __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&yw[j]), zero2);
+                }
+                const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t sel = gw[j] & m[j];
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sel));
+                    acc[2 * j] += f.x;
+                    acc[2 * j + 1] += f.y;
+                }
+            }
+        }
+        uint4 out;
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+            ow[j] = *reinterpret_cast<const uint32_t*>(&b);
+        }
+        *reinterpret_cast<uint4*>(dx + irow + size_t(w) * C + c) = out;
+    }
+}
+
+// The ResNet stem pool (3x3, stride 2, pad 1) backward, owner-computes: the
+// thread of output window (ho, wo) writes input pixels (2ho + a, 2wo + b),
+// a, b in {0, 1}, each fed by the windows (ho + dh, wo + dw) whose tap
+// (a + 1 - 2dh, b + 1 - 2dw) lies in the filter — 9 (window, tap) pairs known
+// at compile time, no index division per pixel. Windows are summed in
+// (ho, wo) order, as in the generic kernel.
+__device__ __forceinline__ void pool_window_add(float (&acc)[8], const uint4& g, const uint2& a,
+                                                const uint32_t (&ypos)[4], bool use_y, int tap) {
+    const uint32_t want = static_cast<uint32_t>(tap) * 0x01010101u;
+    const uint32_t lo = __vcmpeq4(a.x, want), hi = __vcmpeq4(a.y, want);
+    uint32_t m[4] = {__byte_perm(lo, 0, 0x1100), __byte_perm(lo, 0, 0x3322),
+                     __byte_perm(hi, 0, 0x1100), __byte_perm(hi, 0, 0x3322)};
+    const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t sel = gw[j] & m[j] & (use_y ? ypos[j] : 0xFFFFFFFFu);
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sel));
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+    }
+}
+
+__global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1_bf16_kernel(
+    const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
+    __nv_bfloat16* __restrict__ dx, const __nv_bfloat16* __restrict__ ymask, int H, int W, int C,
+    int Ho, int Wo) {
+    const int cg = C / 8;
+    const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
+    const size_t nbase = size_t(n) * Ho * Wo * C;
+    const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
+    const bool use_y = ymask != nullptr;
+    for (int i = threadIdx.x; i < Wo * cg; i += blockDim.x) {
+        const int wo = i / cg, c = (i - wo * cg) * 8;
+        uint4 g[2][2];
+        uint2 a[2][2];
+        uint32_t yp[2][2][4];
+        bool ok[2][2];
+#pragma unroll
+        for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+            for (int dw = 0; dw < 2; ++dw) {
+                ok[dh][dw] = ho + dh < Ho && wo + dw < Wo;
+                g[dh][dw] = make_uint4(0, 0, 0, 0);
+                a[dh][dw] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) yp[dh][dw][j] = 0;
+                if (ok[dh][dw]) {
+                    const size_t o = nbase + size_t((ho + dh) * Wo + wo + dw) * C + c;
+                    g[dh][dw] = __ldg(reinterpret_cast<const uint4*>(dy + o));
+                    a[dh][dw] = __ldg(reinterpret_cast<const uint2*>(arg + o));
+                    if (use_y) {
+                        const uint4 yv = __ldg(reinterpret_cast<const uint4*>(ymask + o));
+                        const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            yp[dh][dw][j] =
+                                __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&yw[j]), zero2);
+                    }
+                }
+            }
+#pragma unroll
+        for (int ai = 0; ai < 2; ++ai)
+#pragma unroll
+            for (int bi = 0; bi < 2; ++bi) {
+                const int h = 2 * ho + ai, w = 2 * wo + bi;
+                if (h >= H || w >= W) continue;
+                float acc[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll
+                for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+                    for (int dw = 0; dw < 2; ++dw) {
+                        const int r = ai + 1 - 2 * dh, sx = bi + 1 - 2 * dw;
+                        if (r < 0 || sx < 0) continue;  // compile-time after unrolling
+                        pool_window_add(acc, g[dh][dw], a[dh][dw], yp[dh][dw], use_y, r * 3 + sx);
+                    }
+                uint4 out;
+                uint32_t* ow = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+                    ow[j] = *reinterpret_cast<const uint32_t*>(&b);
+                }
+                *reinterpret_cast<uint4*>(dx + ((size_t(n) * H + h) * W + w) * C + c) = out;
+            }
     }
 }
 
@@ -681,6 +883,13 @@ cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, i
                         int c, int f, int s, int p, cudaStream_t st) {
     const int ho = (h + 2 * p - f) / s + 1, wo = (w + 2 * p - f) / s + 1;
     const size_t total = size_t(n) * ho * wo * c;
+    if (dt == DType::BF16 && c % 8 == 0 && aligned16(x) && aligned16(y) &&
+        (!arg || (reinterpret_cast<uintptr_t>(arg) % 8) == 0) && size_t(h) * w * c < (size_t(1) << 31)) {
+        maxpool_fwd_bf16x8_kernel<<<n * ho, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
+                                                         static_cast<__nv_bfloat16*>(y), arg, h, w, c,
+                                                         f, s, p, ho, wo);
+        return cudaGetLastError();
+    }
     TCB_DT_SWITCH(dt, T, {
         constexpr int V = 16 / sizeof(T);
         if (c % V == 0 && aligned16(x) && aligned16(y) && (!arg || (reinterpret_cast<uintptr_t>(arg) % V) == 0) &&
@@ -695,22 +904,36 @@ cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, i
 }
 
 cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, int n, int h,
-                        int w, int c, int f, int s, int p, cudaStream_t st, const void* mask) {
+                        int w, int c, int f, int s, int p, cudaStream_t st, const void* ymask) {
     const int ho = (h + 2 * p - f) / s + 1, wo = (w + 2 * p - f) / s + 1;
     const size_t total = size_t(n) * h * w * c;
+    if (dt == DType::BF16 && c % 8 == 0 && aligned16(dy) && aligned16(dx) &&
+        (!ymask || aligned16(ymask)) && (reinterpret_cast<uintptr_t>(arg) % 8) == 0 &&
+        size_t(ho) * wo * c < (size_t(1) << 31) && f == 3 && s == 2 && p == 1) {
+        maxpool_bwd_k3s2p1_bf16_kernel<<<n * ho, 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(dy), arg, static_cast<__nv_bfloat16*>(dx),
+            static_cast<const __nv_bfloat16*>(ymask), h, w, c, ho, wo);
+        return cudaGetLastError();
+    }
+    if (dt == DType::BF16 && c % 8 == 0 && aligned16(dy) && aligned16(dx) &&
+        (!ymask || aligned16(ymask)) && (reinterpret_cast<uintptr_t>(arg) % 8) == 0 &&
+        size_t(ho) * wo * c < (size_t(1) << 31)) {
+        maxpool_bwd_bf16x8_kernel<<<n * h, 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(dy), arg, static_cast<__nv_bfloat16*>(dx),
+            static_cast<const __nv_bfloat16*>(ymask), h, w, c, f, s, p, ho, wo);
+        return cudaGetLastError();
+    }
     TCB_DT_SWITCH(dt, T, {
         constexpr int V = 16 / sizeof(T);
-        if (c % V == 0 && aligned16(dy) && aligned16(dx) && (!mask || aligned16(mask)) &&
+        if (c % V == 0 && aligned16(dy) && aligned16(dx) && (!ymask || aligned16(ymask)) &&
             (reinterpret_cast<uintptr_t>(arg) % V) == 0 && size_t(ho) * wo * c < (size_t(1) << 31)) {
             maxpool_bwd_vec_kernel<T, V><<<n * h, 256, 0, st>>>(
-                static_cast<const T*>(dy), arg, static_cast<T*>(dx), static_cast<const T*>(mask), n,
+                static_cast<const T*>(dy), arg, static_cast<T*>(dx), static_cast<const T*>(ymask), n,
                 h, w, c, f, s, p, ho, wo);
         } else {
             maxpool_bwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
-                static_cast<const T*>(dy), arg, static_cast<T*>(dx), n, h, w, c, f, s, p, ho, wo);
-            if (mask)
-                relu_mask_kernel<T><<<grid_for(total, 4), kBlock, 0, st>>>(
-                    static_cast<T*>(dx), static_cast<const T*>(mask), total);
+                static_cast<const T*>(dy), arg, static_cast<T*>(dx), n, h, w, c, f, s, p, ho, wo,
+                static_cast<const T*>(ymask));
         }
     });
     return cudaGetLastError();

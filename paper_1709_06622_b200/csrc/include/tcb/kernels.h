@@ -42,8 +42,12 @@ int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready = false,
                      bool counters = false);  // kernels per call
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
                         void* y, cudaStream_t st, void* workspace = nullptr);
-cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* wT, const Epilogue& ep,
-                          void* dx, cudaStream_t st);
+// Dgrad reads the KRSC filters `w` directly (MN-major TMA boxes) whenever its
+// operands load by TMA; only gather-path geometries (conv_tc_dgrad_needs_pack)
+// need `wT` = pack_dgrad_weights(w), otherwise it may be NULL.
+bool conv_tc_dgrad_needs_pack(const ConvGeom& g);
+cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* w, const void* wT,
+                          const Epilogue& ep, void* dx, cudaStream_t st);
 // cols_ready: `workspace` still holds the forward pass's explicit im2col of x
 // (narrow layers; the trainer gives them a dedicated workspace for the step).
 // counters: a dedicated, zero-initialised int buffer of at least
@@ -130,10 +134,13 @@ cudaError_t relu_mask_inplace(DType dt, void* g, const void* act, size_t n, cuda
 
 cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, int h, int w,
                         int c, int f, int s, int p, cudaStream_t st);
-// mask (may be NULL): the pool input; dx *= [mask > 0] (fused ReLU backward)
+// ymask (may be NULL): the pool OUTPUT y; windows with y <= 0 route no
+// gradient. That is the fused ReLU backward of a ReLU'd pool input x: every
+// window whose argmax is x[p] has y = x[p], so [x[p] > 0] == [y > 0] — and y
+// is a quarter of x's size.
 cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, int n, int h,
                         int w, int c, int f, int s, int p, cudaStream_t st,
-                        const void* mask = nullptr);
+                        const void* ymask = nullptr);
 cudaError_t avgpool_global_fwd(DType dt, const void* x, void* y, int n, int hw, int c,
                                cudaStream_t st);
 cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw, int c,

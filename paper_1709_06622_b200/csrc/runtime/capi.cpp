@@ -192,9 +192,13 @@ TCB_API int tcb_conv_dgrad(const tcb_conv_plan* plan, const void* dy, const void
         case TCB_ALGO_GEMM:
             if (plan->prec == TCB_PREC_BF16) {
                 if (!workspace) return fail(TCB_ERR_INVALID, "bf16 dgrad needs the plan workspace");
-                void* wT = static_cast<char*>(workspace) + plan->layout.off_wT;
-                e = pack_dgrad_weights(DType::BF16, w, wT, plan->g, st);
-                if (e == cudaSuccess) e = conv_tc_dgrad(plan->g, dy, wT, ep, dx, st);
+                void* wT = nullptr;
+                e = cudaSuccess;
+                if (conv_tc_dgrad_needs_pack(plan->g)) {
+                    wT = static_cast<char*>(workspace) + plan->layout.off_wT;
+                    e = pack_dgrad_weights(DType::BF16, w, wT, plan->g, st);
+                }
+                if (e == cudaSuccess) e = conv_tc_dgrad(plan->g, dy, w, wT, ep, dx, st);
             } else {
                 e = conv_ffma_dgrad(plan->g, static_cast<const float*>(dy),
                                     static_cast<const float*>(w), ep, static_cast<float*>(dx), st);
@@ -242,6 +246,15 @@ TCB_API int tcb_maxpool_fwd(int dtype, const void* x, void* y, uint8_t* argmax, 
     return check_cuda(maxpool_fwd(dt_of(dtype), x, y, argmax, n, h, w, c, f, stride, pad,
                                   static_cast<cudaStream_t>(stream)),
                       "maxpool_fwd");
+}
+
+TCB_API int tcb_maxpool_relu_bwd(int dtype, const void* dy, const uint8_t* argmax, const void* y,
+                                 void* dx, int n, int h, int w, int c, int f, int stride, int pad,
+                                 void* stream) {
+    if (!y) return fail(TCB_ERR_INVALID, "maxpool_relu_bwd needs the pool output y");
+    return check_cuda(maxpool_bwd(dt_of(dtype), dy, argmax, dx, n, h, w, c, f, stride, pad,
+                                  static_cast<cudaStream_t>(stream), y),
+                      "maxpool_relu_bwd");
 }
 
 TCB_API int tcb_maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, void* dx, int n,

@@ -95,8 +95,10 @@ Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int rep
     auto run_dgrad = [&]() -> cudaError_t {
         if (algo == TCB_ALGO_GEMM) {
             if (dt == DType::BF16) {
-                cudaError_t e = pack_dgrad_weights(DType::BF16, w.p, wTp, g, st);
-                return e != cudaSuccess ? e : conv_tc_dgrad(g, dy.p, wTp, none, dx.p, st);
+                // the packing pass is part of the measured dgrad where the geometry needs it
+                cudaError_t e = conv_tc_dgrad_needs_pack(g) ? pack_dgrad_weights(DType::BF16, w.p, wTp, g, st)
+                                                            : cudaSuccess;
+                return e != cudaSuccess ? e : conv_tc_dgrad(g, dy.p, w.p, wTp, none, dx.p, st);
             }
             return conv_ffma_dgrad(g, static_cast<float*>(dy.p), static_cast<float*>(w.p), none,
                                    static_cast<float*>(dx.p), st);

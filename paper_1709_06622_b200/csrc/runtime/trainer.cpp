@@ -68,6 +68,7 @@ struct Node {
     size_t act = 0, grad = 0, argmax = 0, wT = 0;
     size_t nws = 0;  // narrow (explicit im2col) layers: own workspace, col kept fwd -> wgrad
     bool narrow = false;
+    bool pack_wT = false;  // bf16 dgrad on the gather path needs the packed w^T
     // backward plan for this node's OUTPUT tensor
     int final_writer = -1;              // consumer node that writes G[this] last
     std::vector<int> compute_from;      // consumers with a computed contribution
@@ -349,7 +350,8 @@ int allocate(tcb_trainer* t) {
                 else
                     ws = std::max(ws, t->bf16 ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
                                               : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
-                if (t->bf16 && nd.need_dgrad) nd.wT = b.take(nd.wcount * 2);
+                nd.pack_wT = t->bf16 && nd.need_dgrad && conv_tc_dgrad_needs_pack(nd.g);
+                if (nd.pack_wT) nd.wT = b.take(nd.wcount * 2);
             } else {
                 // Winograd / FFT transformed planes; one shared region, passes run in order
                 for (ConvMode m : {ConvMode::Fwd, ConvMode::Dgrad, ConvMode::Wgrad})
@@ -437,7 +439,7 @@ int refresh_transposes(tcb_trainer* t, cudaStream_t st) {
         std::vector<PackDgradJob> jobs;
         int blocks = 0;
         for (const Node& nd : t->nodes) {
-            if (nd.op != Op::Conv || !nd.need_dgrad || nd.algo_id != TCB_ALGO_GEMM) continue;
+            if (nd.op != Op::Conv || !nd.pack_wT) continue;
             jobs.push_back({t->at<__nv_bfloat16>(t->off_wc) + nd.woff, t->at(nd.wT), nd.g, blocks});
             blocks += pack_dgrad_blocks(nd.g);
         }
@@ -545,7 +547,8 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         else if (con.algo_id == TCB_ALGO_FFT)
             TRY_CUDA(fft_dgrad(con.g, t->dt, t->at(con.grad), cw, ep, out, t->at(t->off_ws), st));
         else if (t->bf16)
-            TRY_CUDA(conv_tc_dgrad(con.g, t->at(con.grad), t->at(con.wT), ep, out, st));
+            TRY_CUDA(conv_tc_dgrad(con.g, t->at(con.grad), cw, con.pack_wT ? t->at(con.wT) : nullptr, ep,
+                                   out, st));
         else
             TRY_CUDA(conv_ffma_dgrad(con.g, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
                                      ep, static_cast<float*>(out), st));
@@ -556,7 +559,7 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
     const bool fuse_mask = mask_needed && extras.empty();
     if (con.op == Op::MaxPool)
         TRY_CUDA(maxpool_bwd(t->dt, t->at(con.grad), t->at<uint8_t>(con.argmax), out, tgt.n, tgt.h, tgt.w,
-                             tgt.c, con.f, con.s, con.p, st, fuse_mask ? t->at(tgt.act) : nullptr));
+                             tgt.c, con.f, con.s, con.p, st, fuse_mask ? t->at(con.act) : nullptr));
     else
         TRY_CUDA(avgpool_global_bwd(t->dt, t->at(con.grad), out, tgt.n, tgt.h * tgt.w, tgt.c, st,
                                     fuse_mask ? t->at(tgt.act) : nullptr));

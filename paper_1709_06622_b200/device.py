@@ -173,10 +173,16 @@ def maxpool_fwd(x, f, s, p):
     return y, arg
 
 
-def maxpool_bwd(dy, arg, shape, f, s, p):
+def maxpool_bwd(dy, arg, shape, f, s, p, relu_y=None):
+    """relu_y: the pool output of a ReLU'd input — fuses the ReLU backward."""
     n, h, w, c = shape
     dx = torch.empty(n, h, w, c, dtype=dy.dtype, device="cuda")
-    check(lib().tcb_maxpool_bwd(DT[dy.dtype], _p(dy), _p(arg), _p(dx), n, h, w, c, f, s, p, _stream()))
+    if relu_y is not None:
+        check(lib().tcb_maxpool_relu_bwd(DT[dy.dtype], _p(dy), _p(arg), _p(relu_y), _p(dx), n, h, w,
+                                         c, f, s, p, _stream()))
+    else:
+        check(lib().tcb_maxpool_bwd(DT[dy.dtype], _p(dy), _p(arg), _p(dx), n, h, w, c, f, s, p,
+                                    _stream()))
     return dx
 
 

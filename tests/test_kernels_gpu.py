@@ -186,6 +186,28 @@ def test_maxpool_parity(oracle, dtype, pool):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("pool", [(3, 2, 1), (2, 2, 0)])
+def test_maxpool_relu_ties_parity(oracle, dtype, pool):
+    """ReLU'd input quantised to a few levels (many ties, many zeros): argmax
+    keeps the first maximum in window order, and the fused ReLU backward
+    (mask from the pool output) equals maxpool_bwd followed by the ReLU mask."""
+    dev = _dev()
+    f, s, p = pool
+    n, h, w, c = 2, 14, 12, 16
+    bf = dtype == "bf16"
+    dt = torch.bfloat16 if bf else torch.float32
+    x = np.maximum(np.round(_rand(oracle, (n, h, w, c), 31, 1.0, bf) * 2.0) / 2.0, 0.0).astype(np.float32)
+    y, arg = dev.maxpool_fwd(_to_dev(x, dt), f, s, p)
+    ry, rarg = oracle.maxpool_fwd(x, n, h, w, c, f, s, p)
+    assert np.array_equal(arg.cpu().numpy().ravel(), rarg)
+    assert np.array_equal(_host(y).ravel(), ry.astype(np.float32))
+    dy = _rand(oracle, tuple(y.shape), 32, 1.0, bf)
+    dx = dev.maxpool_bwd(_to_dev(dy, dt), arg, (n, h, w, c), f, s, p, relu_y=y)
+    rdx = oracle.maxpool_bwd(dy, rarg, n, h, w, c, f, s, p) * (x.ravel() > 0)
+    assert rel_err(_host(dx), rdx) <= TOL["bf16" if bf else "ffma"]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_avgpool_and_softmax_parity(oracle, dtype):
     dev = _dev()
     bf = dtype == "bf16"
