@@ -9,7 +9,8 @@ import ctypes
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_DIR = os.path.join(PKG_DIR, "lib")
+# $TCB_LIB_DIR: an alternative in-tree build directory (A/B measurements)
+LIB_DIR = os.environ.get("TCB_LIB_DIR") or os.path.join(PKG_DIR, "lib")
 
 _cache: dict[str, ctypes.CDLL] = {}
 
