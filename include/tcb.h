@@ -164,6 +164,15 @@ int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t* id128);
  * images = keep the device-resident synthetic batch. */
 int tcb_trainer_set_batch(tcb_trainer* t, const float* host_images, const int32_t* host_labels,
                           void* stream);
+/* Pipelined input (the paper's steps 2-4 hidden behind compute): copies a
+ * host batch (pinned for overlap) into one of two device staging slots on the
+ * trainer's own copy stream and returns; the next tcb_trainer_step consumes
+ * the oldest staged batch (waiting on its copy, converting it on the device).
+ * format: TCB_INPUT_F32 (NHWC fp32) or TCB_INPUT_U8 (NHWC uint8 pixels u,
+ * x = (u + 0.5) / 128 - 1). At most two batches may be staged ahead. */
+enum { TCB_INPUT_F32 = 0, TCB_INPUT_U8 = 1 };
+int tcb_trainer_stage_batch(tcb_trainer* t, const void* host_images, int format,
+                            const int32_t* host_labels);
 int tcb_trainer_step(tcb_trainer* t, void* stream);
 int tcb_trainer_loss(tcb_trainer* t, float* loss_host, void* stream);
 /* Per-phase device times of the last timed step (ms): fwd, bwd, reduce-scatter,

@@ -250,6 +250,19 @@ __global__ void pack_channels_kernel(const float* __restrict__ src, T* __restric
     }
 }
 
+// uint8 pixels -> (u + 0.5) / 128 - 1 in (-1, 1), channel-padded to cp.
+template <typename T>
+__global__ void pack_channels_u8_kernel(const uint8_t* __restrict__ src, T* __restrict__ dst,
+                                        size_t pixels, int cl, int cp) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < pixels * cp;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const size_t px = i / cp;
+        const int c = int(i % cp);
+        dst[i] = from_f32<T>(c < cl ? __fsub_rn(__fmul_rn(float(src[px * cl + c]) + 0.5f, 0.0078125f), 1.f)
+                                    : 0.f);
+    }
+}
+
 template <typename T>
 __global__ void add_kernel(T* y, const T* x, size_t n) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
@@ -544,6 +557,13 @@ cudaError_t sgd_momentum(float* w, const float* g, float* v, DType cdt, void* wc
             sgd_kernel<CT><<<grid_for(n, 4), kBlock, 0, st>>>(w, g, v, static_cast<CT*>(wc), n, lr,
                                                               mom, wd, gscale);
     });
+    return cudaGetLastError();
+}
+
+cudaError_t pack_channels_u8(DType dt, const uint8_t* src, void* dst, size_t pixels, int cl, int cp,
+                             cudaStream_t st) {
+    TCB_DT_SWITCH(dt, T, (pack_channels_u8_kernel<T><<<grid_for(pixels * cp, 4), kBlock, 0, st>>>(
+                              src, static_cast<T*>(dst), pixels, cl, cp)));
     return cudaGetLastError();
 }
 

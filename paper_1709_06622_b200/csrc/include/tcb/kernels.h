@@ -127,6 +127,9 @@ cudaError_t split_reduce(const float* parts, int splits, size_t n, float* out, c
 cudaError_t sgd_momentum(float* w, const float* g, float* v, DType cdt, void* wc, size_t n,
                          float lr, float mom, float wd, float gscale, cudaStream_t st);
 // dst[px][c] = c < cl ? src[px][c] : 0 for c < cp (fp32 src, dst in dt): channel padding.
+// uint8 NHWC pixels u -> (u + 0.5) / 128 - 1, channel-padded (staged host batches)
+cudaError_t pack_channels_u8(DType dt, const uint8_t* src, void* dst, size_t pixels, int cl, int cp,
+                             cudaStream_t st);
 cudaError_t pack_channels(DType dt, const float* src, void* dst, size_t pixels, int cl, int cp,
                           cudaStream_t st);
 cudaError_t add_inplace(DType dt, void* y, const void* x, size_t n, cudaStream_t st);

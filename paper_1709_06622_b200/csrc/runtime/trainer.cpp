@@ -108,6 +108,14 @@ struct tcb_trainer {
     size_t arena_bytes = 0;
     size_t off_param = 0, off_grad = 0, off_mom = 0, off_wc = 0, off_ws = 0, off_colsum = 0;
     size_t off_labels = 0, off_loss = 0, off_input_f32 = 0;
+    // staged host batches (pipelined H2D): two slots filled on a copy stream,
+    // consumed in order by the next steps
+    size_t off_stage[2] = {0, 0}, off_stage_labels[2] = {0, 0}, stage_bytes = 0;
+    int stage_format[2] = {0, 0};
+    uint64_t stage_w = 0, stage_r = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t staged[2]{}, consumed[2]{};
+    bool consumed_recorded[2] = {false, false};
     size_t ws_bytes = 0, colsum_bytes = 0;
     size_t off_pack_jobs = 0;  // device table of the batched dgrad weight packing
     size_t off_counters = 0;   // split-K counters of the in-kernel wgrad reduction
@@ -376,6 +384,11 @@ int allocate(tcb_trainer* t) {
     t->off_loss = b.take(size_t(t->batch + 1) * 4);
     const Node& in = t->nodes[0];
     t->off_input_f32 = b.take(size_t(in.n) * in.h * in.w * in.c_logical * 4);
+    t->stage_bytes = size_t(in.n) * in.h * in.w * in.c_logical * 4;  // fp32 worst case
+    for (int k = 0; k < 2; ++k) {
+        t->off_stage[k] = b.take(t->stage_bytes);
+        t->off_stage_labels[k] = b.take(size_t(t->batch) * 4);
+    }
     t->arena_bytes = b.top;
     cudaError_t e = cudaMalloc(&t->arena, t->arena_bytes);
     if (e != cudaSuccess)
@@ -718,6 +731,14 @@ TCB_API int tcb_trainer_create(const char* config_json, tcb_trainer** out) {
 TCB_API int tcb_trainer_destroy(tcb_trainer* t) {
     if (!t) return TCB_OK;
     if (t->comm) ncclCommDestroy(t->comm);
+    if (t->copy_stream) {
+        cudaStreamSynchronize(t->copy_stream);
+        cudaStreamDestroy(t->copy_stream);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(t->staged[k]);
+            cudaEventDestroy(t->consumed[k]);
+        }
+    }
     for (cudaEvent_t& e : t->ph.e)
         if (e) cudaEventDestroy(e);
     for (auto& a : t->lev)
@@ -776,11 +797,65 @@ TCB_API int tcb_trainer_set_batch(tcb_trainer* t, const float* host_images, cons
     return TCB_OK;
 }
 
+TCB_API int tcb_trainer_stage_batch(tcb_trainer* t, const void* host_images, int format,
+                                    const int32_t* host_labels) {
+    if (!t || !host_images || !host_labels) return fail(TCB_ERR_INVALID, "NULL argument");
+    if (format != TCB_INPUT_F32 && format != TCB_INPUT_U8)
+        return fail(TCB_ERR_INVALID, "format must be TCB_INPUT_F32 or TCB_INPUT_U8");
+    if (t->stage_w - t->stage_r >= 2)
+        return fail(TCB_ERR_INVALID, "two batches already staged; run a step first");
+    TRY(ensure_ready(t, t->stream));
+    if (!t->copy_stream) {
+        TRY_CUDA(cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            TRY_CUDA(cudaEventCreateWithFlags(&t->staged[k], cudaEventDisableTiming));
+            TRY_CUDA(cudaEventCreateWithFlags(&t->consumed[k], cudaEventDisableTiming));
+        }
+    }
+    const int k = static_cast<int>(t->stage_w % 2);
+    // the slot is rewritten only after the step that consumed it has packed it
+    if (t->consumed_recorded[k]) TRY_CUDA(cudaStreamWaitEvent(t->copy_stream, t->consumed[k], 0));
+    const Node& in = t->nodes[0];
+    const size_t elems = size_t(in.n) * in.h * in.w * in.c_logical;
+    TRY_CUDA(cudaMemcpyAsync(t->at(t->off_stage[k]), host_images,
+                             elems * (format == TCB_INPUT_U8 ? 1 : 4), cudaMemcpyHostToDevice,
+                             t->copy_stream));
+    TRY_CUDA(cudaMemcpyAsync(t->at(t->off_stage_labels[k]), host_labels, size_t(t->batch) * 4,
+                             cudaMemcpyHostToDevice, t->copy_stream));
+    TRY_CUDA(cudaEventRecord(t->staged[k], t->copy_stream));
+    t->stage_format[k] = format;
+    ++t->stage_w;
+    return TCB_OK;
+}
+
+// The oldest staged batch (if any) becomes this step's input.
+static int consume_staged(tcb_trainer* t, cudaStream_t st) {
+    if (t->stage_r == t->stage_w) return TCB_OK;
+    const int k = static_cast<int>(t->stage_r % 2);
+    TRY_CUDA(cudaStreamWaitEvent(st, t->staged[k], 0));
+    const Node& in = t->nodes[0];
+    const size_t px = size_t(in.n) * in.h * in.w;
+    if (t->stage_format[k] == TCB_INPUT_U8)
+        TRY_CUDA(pack_channels_u8(t->dt, t->at<uint8_t>(t->off_stage[k]), t->at(in.act), px, in.c_logical,
+                                  in.c, st));
+    else
+        TRY_CUDA(pack_channels(t->dt, t->at<float>(t->off_stage[k]), t->at(in.act), px, in.c_logical, in.c,
+                               st));
+    TRY_CUDA(cudaMemcpyAsync(t->at(t->off_labels), t->at(t->off_stage_labels[k]), size_t(t->batch) * 4,
+                             cudaMemcpyDeviceToDevice, st));
+    TRY_CUDA(cudaEventRecord(t->consumed[k], st));
+    t->consumed_recorded[k] = true;
+    ++t->stage_r;
+    t->launches++;
+    return TCB_OK;
+}
+
 TCB_API int tcb_trainer_step(tcb_trainer* t, void* stream) {
     if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
     auto st = static_cast<cudaStream_t>(stream);
     TRY(ensure_ready(t, st));
     t->launches = 0;
+    TRY(consume_staged(t, st));
     cudaEvent_t* e = t->ph.e;
     if (t->timing) TRY_CUDA(cudaEventRecord(e[0], st));
     TRY(forward(t, st));

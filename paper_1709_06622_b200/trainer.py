@@ -26,6 +26,7 @@ def _lib():
         L.tcb_nccl_unique_id.argtypes = [ctypes.c_char_p]
         L.tcb_trainer_join.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
         L.tcb_trainer_set_batch.argtypes = [_vp, _vp, _vp, _vp]
+        L.tcb_trainer_stage_batch.argtypes = [_vp, _vp, ctypes.c_int, _vp]
         L.tcb_trainer_step.argtypes = [_vp, _vp]
         L.tcb_trainer_loss.argtypes = [_vp, ctypes.POINTER(ctypes.c_float), _vp]
         L.tcb_trainer_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_float)]
@@ -87,6 +88,14 @@ class Trainer:
         device.check(_lib().tcb_trainer_set_batch(
             self.handle, None if images is None else _vp(images.data_ptr()),
             None if labels is None else _vp(labels.data_ptr()), self._stream()))
+
+    def stage_batch(self, images, labels):
+        """Pipelined input: queue a pinned host batch (NHWC uint8 pixels or fp32)
+        for the next step; the H2D copy runs on the trainer's copy stream,
+        overlapping the current step."""
+        fmt = {torch.uint8: 1, torch.float32: 0}[images.dtype]
+        device.check(_lib().tcb_trainer_stage_batch(self.handle, _vp(images.data_ptr()), fmt,
+                                                    _vp(labels.data_ptr())))
 
     def step(self):
         device.check(_lib().tcb_trainer_step(self.handle, self._stream()))

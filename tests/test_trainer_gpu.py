@@ -176,6 +176,34 @@ def test_host_batch_path_matches_resident_batch(oracle):
     assert torch.equal(a.tensor("grad"), b.tensor("grad"))
 
 
+def test_staged_u8_batches_pipeline(oracle):
+    """Staged uint8 batches (copy stream, two slots) feed consecutive steps in
+    order and equal the synchronous fp32 host path on the converted values."""
+    from paper_1709_06622_b200.trainer import Trainer
+    cfg = _models().tiny_resnet(batch=4, precision="bf16")
+    a, b = Trainer(cfg), Trainer(cfg)
+    lay = a.describe()
+    n, h, w = lay["layers"][0]["shape"][:3]
+    cl = lay["layers"][0]["c_logical"]
+    rng = np.random.default_rng(5)
+    batches = [rng.integers(0, 256, (n, h, w, cl), dtype=np.uint8) for _ in range(3)]
+    labels = [rng.integers(0, cfg["classes"], (n,), dtype=np.int32) for _ in range(3)]
+    pinned = [(torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory())
+              for x, y in zip(batches, labels)]
+    a.stage_batch(*pinned[0])
+    a.stage_batch(*pinned[1])
+    for i in range(3):
+        a.step()
+        if i + 2 < 3:
+            a.stage_batch(*pinned[i + 2])
+        xf = ((batches[i].astype(np.float32) + 0.5) * np.float32(0.0078125) - 1).astype(np.float32)
+        b.set_batch(torch.from_numpy(xf).pin_memory(), torch.from_numpy(labels[i]).pin_memory())
+        b.step()
+        torch.cuda.synchronize()
+        assert torch.equal(a.tensor("grad"), b.tensor("grad")), i
+        assert torch.equal(a.tensor("param"), b.tensor("param")), i
+
+
 def test_loss_decreases_over_steps():
     from paper_1709_06622_b200.trainer import Trainer
     cfg = _models().tiny_resnet(batch=8, precision="bf16", lr=0.05)
