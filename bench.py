@@ -238,7 +238,7 @@ def ps_bandwidth(phases, world, param_bytes):
             "peak_kind": "peer copy per direction, B200_PROFILING.md (fallback)"}
 
 
-def in_step_roofline(rows, pk, precision):
+def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
     """Dominant kernel = the tcgen05 implicit-GEMM conv (every fwd/dgrad/wgrad
     pass of the step). achieved = algorithmic conv FLOP of the step / the sum of
     the conv passes' CUDA-event times measured inside a real training step
@@ -252,8 +252,17 @@ def in_step_roofline(rows, pk, precision):
     achieved = flop / ms / 1e9
     bf = precision == "bf16"
     peak = pk["bf16_tflops_sustained"] if bf and "bf16_tflops_sustained" in pk else pk.get("bf16_tflops", 1590.0)
+    traffic, tsrc = None, None
+    tpath = os.path.join(ROOT, "profiles", f"r01_conv_traffic_{model}_bs{batch}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        traffic = tj["conv_dram_bytes_per_step"]
+        tsrc = f"profiles/{os.path.basename(tpath)}: {tj['source']}"
     return {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_unit": "DRAM bytes per step, all conv_tc launches (same unit as flop_per_step)",
+            "traffic_source": tsrc,
             "kernel": "conv_tc_kernel (tcgen05/TMEM implicit GEMM, TMA im2col; all conv passes of one step)",
             "flop_per_step": flop, "conv_ms_per_step": round(ms, 3),
             "frac_of_burst_peak": round(achieved / pk.get("bf16_tflops", 1590.0), 4),
@@ -376,7 +385,7 @@ def main():
     pk = peaks()
     roof = None
     if rank == 0:
-        roof = in_step_roofline(layer_rows, pk, args.precision)
+        roof = in_step_roofline(layer_rows, pk, args.precision, args.model, args.batch)
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         with open(os.path.join(ROOT, "gpurun_out", f"conv_in_step_{args.model}_{args.precision}.json"), "w") as f:
             json.dump(layer_rows, f, indent=1)
