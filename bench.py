@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--isolated-roofline", action="store_true",
                     help="also time every conv pass alone (warm L2) via the plan C-ABI")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="aggregate after backward instead of reducing shards during it")
     return ap.parse_args()
 
 
@@ -252,6 +254,19 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
     achieved = flop / ms / 1e9
     bf = precision == "bf16"
     peak = pk["bf16_tflops_sustained"] if bf and "bf16_tflops_sustained" in pk else pk.get("bf16_tflops", 1590.0)
+    # per-pass roofline time max(FLOP / tensor peak, bytes / HBM peak), summed
+    hbm = pk.get("hbm_gbs", 6548.2)
+    bound_ms, tensor_ms, hbm_ms, nbytes = 0.0, 0.0, 0.0, 0.0
+    for r in rows:
+        for pname in ("fwd", "dgrad", "wgrad"):
+            if r.get(pname + "_ms") is None:
+                continue
+            tf = r["flop"] / (peak * 1e9)
+            tb = r.get(pname + "_bytes", 0) / (hbm * 1e6)
+            bound_ms += max(tf, tb)
+            tensor_ms += tf
+            hbm_ms += tb
+            nbytes += r.get(pname + "_bytes", 0)
     traffic, tsrc = None, None
     tpath = os.path.join(ROOT, "profiles", f"r01_conv_traffic_{model}_bs{batch}.json")
     if os.path.exists(tpath):
@@ -266,6 +281,12 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
             "kernel": "conv_tc_kernel (tcgen05/TMEM implicit GEMM, TMA im2col; all conv passes of one step)",
             "flop_per_step": flop, "conv_ms_per_step": round(ms, 3),
             "frac_of_burst_peak": round(achieved / pk.get("bf16_tflops", 1590.0), 4),
+            "algorithmic_bytes_per_step": nbytes,
+            "combined_roofline": {
+                "bound_ms": round(bound_ms, 3), "tensor_only_ms": round(tensor_ms, 3),
+                "hbm_only_ms": round(hbm_ms, 3), "measured_ms": round(ms, 3),
+                "frac": round(bound_ms / ms, 4),
+                "note": "sum over conv passes of max(FLOP/tensor peak, algorithmic bytes/HBM peak)"},
             "peak_kind": f"bf16 dense sustained ({pk['source']}; kernel timed inside the step)"}
 
 
@@ -302,6 +323,7 @@ def main():
 
     cfg = models.build(args.model, batch=args.batch, precision=args.precision)
     cfg["n_ps"] = args.n_ps
+    cfg["overlap_comm"] = not args.no_overlap
     tr = Trainer(cfg, rank, world, nid)
     stream = torch.cuda.current_stream()
 
@@ -316,12 +338,32 @@ def main():
         tr.step()
     barrier()
 
-    # phase breakdown (StepTrace for Lemma 1) and per-conv-pass times of one extra step
+    # phase breakdown (StepTrace for Lemma 1): median over 3 steps with only the
+    # six phase events; then per-conv-pass times from one step with layer events
     tr.enable_timing(True)
+    samples = []
+    for _ in range(3):
+        tr.step()
+        samples.append(tr.phase_times())
+    phases = {k: sorted(sm[k] for sm in samples)[1] for k in samples[0]}
+    tr.enable_timing(False)
     tr.enable_layer_timing(True)
     tr.step()
-    phases = tr.phase_times()
+    torch.cuda.synchronize()
     layer_rows = tr.layer_times()
+    # algorithmic bytes per conv pass (each tensor touched once; fused residual /
+    # ReLU-mask side inputs counted where the epilogue reads them)
+    geo = {L["conv_index"]: L for L in tr.describe()["layers"] if L["op"] == "conv"}
+    es = 2 if args.precision == "bf16" else 4
+    for r in layer_rows:
+        L = geo[r["conv_index"]]
+        n, h, w, c, k, rr, ss, ph, pw, sh, sw = L["geom"]
+        ho, wo = (h + 2 * ph - rr) // sh + 1, (w + 2 * pw - ss) // sw + 1
+        x, y, wt = n * h * w * c * es, n * ho * wo * k * es, k * rr * ss * c * es
+        res = L.get("residual", -1) is not None and L.get("residual", -1) >= 0
+        r["fwd_bytes"] = x + wt + y + (y if res else 0)
+        r["dgrad_bytes"] = y + wt + 3 * x if r["dgrad_ms"] is not None else 0  # + residual grad + mask
+        r["wgrad_bytes"] = y + x + k * rr * ss * c * 4
     tr.enable_timing(False)
     tr.enable_layer_timing(False)
     launches_per_step = tr.launch_count()
@@ -402,6 +444,14 @@ def main():
                "kind": "port",
                "sample": f"1 training step of {args.model} at batch 1 (fwd+bwd+SGD, fp64 accumulate) "
                          f"= {r['seconds_per_step']:.2f} s"}
+        # decision path (§8 d4-i): this planner vs the compiled reference planner on
+        # the B200-measured catalogs, same requests, replies must be identical
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            from planner_timing import time_planners
+            cpu["planner"] = time_planners(100)
+        except Exception as exc:  # noqa: BLE001 — report, never fail the bench line
+            cpu["planner"] = {"error": repr(exc)}
 
     if rank == 0:
         layout = tr.describe()
@@ -423,6 +473,7 @@ def main():
             "config": {"workload": f"{args.model}_synthetic_224" if args.model == "resnet50" else args.model,
                        "per_gpu_batch": args.batch, "global_batch": args.batch * world,
                        "ps_shards": args.n_ps or world, "precision": args.precision,
+                       "comm_overlap": (not args.no_overlap) and world > 1 and (args.n_ps in (0, world)),
                        "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (per-step activations >> 126 MB); no flush"},
             "clocks": clk,
@@ -466,5 +517,23 @@ def run_reference(args):
     }), flush=True)
 
 
+def _clean_stdout():
+    """Libraries (NCCL, torch) may print to fd 1; the driver parses exactly one
+    JSON line from stdout. Route fd 1 to stderr for the whole run and give the
+    JSON printers a private handle on the original stdout."""
+    global print  # noqa: PLW0603 — only the JSON line goes to the real stdout
+    real = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    builtin_print = print
+
+    def print(*a, **k):  # noqa: A001
+        k.setdefault("file", real)
+        builtin_print(*a, **k)
+        if k["file"] is real:
+            real.flush()
+
+
 if __name__ == "__main__":
+    _clean_stdout()
     main()

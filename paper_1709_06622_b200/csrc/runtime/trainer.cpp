@@ -119,6 +119,17 @@ struct tcb_trainer {
     size_t ws_bytes = 0, colsum_bytes = 0;
     size_t off_pack_jobs = 0;  // device table of the batched dgrad weight packing
     size_t off_counters = 0;   // split-K counters of the in-kernel wgrad reduction
+    // Overlapped PS aggregation (N_ps = G): shard s is reduced to its owner on
+    // the comm stream as soon as backward has written every gradient in it
+    bool overlap = true;                    // config "overlap_comm"
+    cudaStream_t comm_stream = nullptr;
+    // the overlapped shard reduces run on their own communicator limited to a
+    // few CTAs, so they steal almost no SMs from the persistent conv kernels
+    ncclComm_t comm_bg = nullptr;
+    int comm_bg_ctas = 2;                   // config "overlap_ctas"
+    std::vector<cudaEvent_t> ev_ready;      // per shard
+    cudaEvent_t ev_comm_done = nullptr, ev_bwd_start = nullptr;
+    std::map<int, std::vector<int>> shard_trigger;  // node index -> shards it completes
     bool fused_split_reduce = false;  // config "fused_split_reduce" / $TCB_FUSED_SPLIT_REDUCE
     int pack_njobs = 0, pack_blocks = 0;
     bool pack_jobs_ready = false;
@@ -134,6 +145,9 @@ struct tcb_trainer {
     std::vector<std::array<cudaEvent_t, 6>> lev;
     cudaStream_t lev_stream = nullptr;
 
+    bool overlap_active() const {
+        return overlap && world > 1 && (n_ps <= 0 || n_ps >= world) && comm_stream != nullptr;
+    }
     void mark(size_t node, int slot, cudaStream_t st) {
         if (layer_timing) cudaEventRecord(lev[node][slot], st);
     }
@@ -172,6 +186,8 @@ int build_graph(tcb_trainer* t) {
     t->batch = cfg.at("batch").get<int>();
     t->classes = cfg.at("classes").get<int>();
     t->seed = cfg.value("seed", uint64_t(20260810));
+    t->overlap = t->cfg.value("overlap_comm", true);
+    t->comm_bg_ctas = t->cfg.value("overlap_ctas", 2);
     {
         const char* e = std::getenv("TCB_FUSED_SPLIT_REDUCE");
         t->fused_split_reduce = cfg.value("fused_split_reduce", e != nullptr && e[0] == '1');
@@ -332,6 +348,24 @@ void plan_params(tcb_trainer* t) {
     const size_t unit = size_t(t->world) * kParamAlign;
     t->param_padded = round_up(std::max<size_t>(off, 1), unit);
     t->shard = t->param_padded / t->world;
+    // shard s is complete after the backward wgrad of the lowest-index conv
+    // touching it (backward runs from the last node down); shards holding only
+    // padding go out with the first wgrad
+    t->shard_trigger.clear();
+    {
+        std::vector<int> first_node(t->world, -1);
+        int last_conv = -1;
+        for (int i = 0; i < static_cast<int>(t->nodes.size()); ++i) {
+            const Node& nd = t->nodes[i];
+            if (nd.op != Op::Conv) continue;
+            last_conv = i;
+            const size_t lo = nd.woff, hi = (nd.bias ? nd.boff + nd.g.k : nd.woff + nd.wcount);
+            for (size_t sh = lo / t->shard; sh < t->world && sh * t->shard < hi; ++sh)
+                if (first_node[sh] < 0) first_node[sh] = i;
+        }
+        for (int sh = t->world - 1; sh >= 0; --sh)
+            t->shard_trigger[first_node[sh] >= 0 ? first_node[sh] : last_conv].push_back(sh);
+    }
 }
 
 int allocate(tcb_trainer* t) {
@@ -588,6 +622,22 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
     return TCB_OK;
 }
 
+// Overlapped aggregation: reduce each gradient shard that node i completed to
+// its owner on the comm stream (same order on every rank).
+int issue_ready_shards(tcb_trainer* t, int i, cudaStream_t st) {
+    auto it = t->shard_trigger.find(i);
+    if (it == t->shard_trigger.end()) return TCB_OK;
+    float* grad = t->at<float>(t->off_grad);
+    for (int sh : it->second) {
+        TRY_CUDA(cudaEventRecord(t->ev_ready[sh], st));
+        TRY_CUDA(cudaStreamWaitEvent(t->comm_stream, t->ev_ready[sh], 0));
+        float* g = grad + size_t(sh) * t->shard;
+        TRY_NCCL(ncclReduce(g, g, t->shard, ncclFloat32, ncclSum, sh, t->comm_bg, t->comm_stream));
+        t->launches++;
+    }
+    return TCB_OK;
+}
+
 int backward(tcb_trainer* t, cudaStream_t st) {
     TRY(refresh_transposes(t, st));
     float* grad = t->at<float>(t->off_grad);
@@ -632,6 +682,7 @@ int backward(tcb_trainer* t, cudaStream_t st) {
                 t->launches += 2;
             }
             t->mark(i, 5, st);
+            if (t->overlap_active()) TRY(issue_ready_shards(t, i, st));
             if (nd.need_dgrad) {
                 t->mark(i, 2, st);
                 TRY(backward_contribution(t, i, nd.in, st));
@@ -654,7 +705,22 @@ int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, 
     char* wc = t->at<char>(t->off_wc);
     const int owners = (t->n_ps > 0 && t->n_ps < t->world) ? t->n_ps : t->world;
 
-    if (t->world > 1 && owners == t->world) {
+    if (t->overlap_active()) {
+        // shard reduces already in flight on the comm stream (issued during
+        // backward); own-shard SGD and the all-gather follow there, and the
+        // compute stream waits only at the end
+        cudaStream_t cs = t->comm_stream;
+        if (after_rs) TRY_CUDA(cudaEventRecord(after_rs, cs));
+        const size_t o = t->rank * t->shard;
+        TRY_CUDA(sgd_momentum(param + o, grad + o, mom + o, t->dt, t->bf16 ? wc + o * 2 : nullptr, t->shard,
+                              t->lr, t->momentum, t->weight_decay, gscale, cs));
+        t->launches++;
+        if (after_sgd) TRY_CUDA(cudaEventRecord(after_sgd, cs));
+        TRY_NCCL(ncclAllGather(wc + o * wes, wc, t->shard, wdt, t->comm, cs));
+        t->launches++;
+        TRY_CUDA(cudaEventRecord(t->ev_comm_done, cs));
+        TRY_CUDA(cudaStreamWaitEvent(st, t->ev_comm_done, 0));
+    } else if (t->world > 1 && owners == t->world) {
         // PS shards = GPUs: reduce-scatter (in place) -> SGD on own shard -> all-gather
         TRY_NCCL(ncclReduceScatter(grad, grad + t->rank * t->shard, t->shard, ncclFloat32, ncclSum,
                                    t->comm, st));
@@ -730,6 +796,13 @@ TCB_API int tcb_trainer_create(const char* config_json, tcb_trainer** out) {
 
 TCB_API int tcb_trainer_destroy(tcb_trainer* t) {
     if (!t) return TCB_OK;
+    if (t->comm_stream) {
+        cudaStreamSynchronize(t->comm_stream);
+        for (cudaEvent_t e : t->ev_ready) cudaEventDestroy(e);
+        if (t->ev_comm_done) cudaEventDestroy(t->ev_comm_done);
+        cudaStreamDestroy(t->comm_stream);
+    }
+    if (t->comm_bg) ncclCommDestroy(t->comm_bg);
     if (t->comm) ncclCommDestroy(t->comm);
     if (t->copy_stream) {
         cudaStreamSynchronize(t->copy_stream);
@@ -768,6 +841,16 @@ TCB_API int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t*
         ncclUniqueId id;
         std::memcpy(&id, id128, sizeof(id));
         TRY_NCCL(ncclCommInitRank(&t->comm, world, id, rank));
+        if (t->overlap) {
+            ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+            cfg.minCTAs = 1;
+            cfg.maxCTAs = std::max(1, t->comm_bg_ctas);
+            TRY_NCCL(ncclCommSplit(t->comm, 0, rank, &t->comm_bg, &cfg));
+            TRY_CUDA(cudaStreamCreateWithFlags(&t->comm_stream, cudaStreamNonBlocking));
+            t->ev_ready.resize(world);
+            for (cudaEvent_t& e : t->ev_ready) TRY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            TRY_CUDA(cudaEventCreateWithFlags(&t->ev_comm_done, cudaEventDisableTiming));
+        }
     }
     return TCB_OK;
 }

@@ -5,17 +5,18 @@
 tag=${1:-r01s}
 out=gpurun_out
 mkdir -p $out
-run() { python -m torch.distributed.run --nnodes=1 --nproc-per-node $1 --master-addr 127.0.0.1 --master-port $2 "${@:3}"; }
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
 timeout 600 python bench.py --no-cpu-baseline > $out/${tag}_bench_g1.json 2> $out/${tag}_bench_g1.err
-timeout 600 run 2 29511 bench.py --gpus 2 --no-cpu-baseline > $out/${tag}_bench_g2.json 2> $out/${tag}_bench_g2.err
-timeout 600 run 4 29512 bench.py --gpus 4 --no-cpu-baseline > $out/${tag}_bench_g4.json 2> $out/${tag}_bench_g4.err
-timeout 300 run 2 29513 scripts/nccl_busbw.py > $out/${tag}_busbw_g2.json 2> $out/${tag}_busbw_g2.err
-timeout 300 run 4 29514 scripts/nccl_busbw.py > $out/${tag}_busbw_g4.json 2> $out/${tag}_busbw_g4.err
+timeout 600 $TR --nproc-per-node 2 --master-port 29511 bench.py --gpus 2 --no-cpu-baseline > $out/${tag}_bench_g2.json 2> $out/${tag}_bench_g2.err
+timeout 600 $TR --nproc-per-node 4 --master-port 29512 bench.py --gpus 4 --no-cpu-baseline > $out/${tag}_bench_g4.json 2> $out/${tag}_bench_g4.err
+timeout 600 $TR --nproc-per-node 4 --master-port 29519 bench.py --gpus 4 --no-cpu-baseline --no-e2e --no-overlap > $out/${tag}_bench_g4_nooverlap.json 2> $out/${tag}_bench_g4_nooverlap.err
+timeout 300 $TR --nproc-per-node 2 --master-port 29513 scripts/nccl_busbw.py > $out/${tag}_busbw_g2.json 2> $out/${tag}_busbw_g2.err
+timeout 300 $TR --nproc-per-node 4 --master-port 29514 scripts/nccl_busbw.py > $out/${tag}_busbw_g4.json 2> $out/${tag}_busbw_g4.err
 for n in 1 2 4; do
-  timeout 600 run 4 2952$n bench.py --gpus 4 --model vgg16 --batch 64 --n-ps $n --no-cpu-baseline --no-e2e \
+  timeout 600 $TR --nproc-per-node 4 --master-port 2952$n bench.py --gpus 4 --model vgg16 --batch 64 --n-ps $n --no-cpu-baseline --no-e2e \
     > $out/${tag}_vgg_g4_nps$n.json 2> $out/${tag}_vgg_g4_nps$n.err
 done
 timeout 900 python -m pytest tests/test_ps_multigpu.py -x -q -p no:cacheprovider --timeout 300 > $out/${tag}_pytest_multigpu.log 2>&1
 echo "rc=$?" >> $out/${tag}_pytest_multigpu.log
-timeout 600 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+[ -s $out/${tag}_traffic.csv ] || timeout 600 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
   --clock-control none --csv --log-file $out/${tag}_traffic.csv python scripts/step_profile.py > $out/${tag}_traffic.log 2>&1
