@@ -62,8 +62,10 @@ def parse():
     ap.add_argument("--isolated-roofline", action="store_true",
                     help="also time every conv pass alone (warm L2) via the plan C-ABI")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-overlap", action="store_true",
-                    help="aggregate after backward instead of reducing shards during it")
+    ap.add_argument("--overlap", action="store_true",
+                    help="reduce gradient shards during backward on a low-CTA communicator "
+                         "(off by default: measured slower on ResNet-50, DESIGN.md §6)")
+    ap.add_argument("--no-overlap", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -323,7 +325,7 @@ def main():
 
     cfg = models.build(args.model, batch=args.batch, precision=args.precision)
     cfg["n_ps"] = args.n_ps
-    cfg["overlap_comm"] = not args.no_overlap
+    cfg["overlap_comm"] = args.overlap
     tr = Trainer(cfg, rank, world, nid)
     stream = torch.cuda.current_stream()
 
@@ -473,7 +475,7 @@ def main():
             "config": {"workload": f"{args.model}_synthetic_224" if args.model == "resnet50" else args.model,
                        "per_gpu_batch": args.batch, "global_batch": args.batch * world,
                        "ps_shards": args.n_ps or world, "precision": args.precision,
-                       "comm_overlap": (not args.no_overlap) and world > 1 and (args.n_ps in (0, world)),
+                       "comm_overlap": args.overlap and world > 1 and (args.n_ps in (0, world)),
                        "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (per-step activations >> 126 MB); no flush"},
             "clocks": clk,

@@ -960,6 +960,8 @@ cudaError_t narrow_im2col(const ConvGeom& g, const NarrowPlan& q, const void* x,
 }
 
 // ---------------------------------------------------------------- host ----
+int g_sm_reserve = 0;  // SMs left free for concurrent communication kernels
+
 int pick_bn(int ncol) { return ncol >= 256 ? 256 : (ncol > 64 ? 128 : 64); }
 
 struct SplitPlan {
@@ -971,7 +973,7 @@ SplitPlan plan_splits(const ConvShape& s, int bn) {
     const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + bn - 1) / bn);
     // one exact wave: splits * tiles <= #SMs, so every CTA runs one equal unit
     // (no tail round) and the fp32 partials stay as few as the wave allows
-    int want = std::max(1, num_sms() / tiles);
+    int want = std::max(1, (num_sms() - g_sm_reserve) / tiles);
     want = std::min(want, std::max(1, kb_total / 4));  // keep >= 4 k-blocks per split
     want = std::min(want, 64);
     const int per = (kb_total + want - 1) / want;
@@ -1060,7 +1062,7 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
         p.kb_per_split = p.kb_total;
     }
     p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
-    const int grid = std::min(p.num_tiles, num_sms());
+    const int grid = std::min(p.num_tiles, std::max(1, num_sms() - g_sm_reserve));
     conv_tc_kernel<MODE, BN, LOAD, EPI><<<grid, kThreads, C::kSmem, st>>>(p);
     return cudaGetLastError();
 }
@@ -1128,6 +1130,7 @@ cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cuda
 
 void conv_tc_set_force_gather(int on) { g_force_gather = on ? 1 : 0; }
 void conv_tc_set_epi_kb(int kb) { g_epi_kb = kb; }
+void conv_tc_set_sm_reserve(int sms) { g_sm_reserve = std::max(0, sms); }
 
 bool conv_tc_supported(const ConvGeom& g, ConvMode mode) {
     if (g.n < 1 || g.h < 1 || g.w < 1 || g.c < 1 || g.k < 1) return false;

@@ -66,6 +66,9 @@ void conv_tc_set_force_gather(int on);
 // TMA epilogue for layers with at most `kb` 64-deep k-blocks (0 = never,
 // -1 = default: $TCB_CONV_EPI_KB or 16).
 void conv_tc_set_epi_kb(int kb);
+// Persistent conv kernels use at most #SMs - sms CTAs (SMs kept free for
+// communication kernels running concurrently).
+void conv_tc_set_sm_reserve(int sms);
 
 // ---- FP32 FFMA implicit GEMM (parity mode) ----
 size_t conv_ffma_workspace(const ConvGeom& g, ConvMode mode);

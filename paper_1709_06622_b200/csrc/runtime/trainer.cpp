@@ -121,12 +121,12 @@ struct tcb_trainer {
     size_t off_counters = 0;   // split-K counters of the in-kernel wgrad reduction
     // Overlapped PS aggregation (N_ps = G): shard s is reduced to its owner on
     // the comm stream as soon as backward has written every gradient in it
-    bool overlap = true;                    // config "overlap_comm"
+    bool overlap = false;                   // config "overlap_comm" (measured: see DESIGN §6)
     cudaStream_t comm_stream = nullptr;
     // the overlapped shard reduces run on their own communicator limited to a
     // few CTAs, so they steal almost no SMs from the persistent conv kernels
     ncclComm_t comm_bg = nullptr;
-    int comm_bg_ctas = 2;                   // config "overlap_ctas"
+    int comm_bg_ctas = 8;                   // config "overlap_ctas"
     std::vector<cudaEvent_t> ev_ready;      // per shard
     cudaEvent_t ev_comm_done = nullptr, ev_bwd_start = nullptr;
     std::map<int, std::vector<int>> shard_trigger;  // node index -> shards it completes
@@ -186,8 +186,8 @@ int build_graph(tcb_trainer* t) {
     t->batch = cfg.at("batch").get<int>();
     t->classes = cfg.at("classes").get<int>();
     t->seed = cfg.value("seed", uint64_t(20260810));
-    t->overlap = t->cfg.value("overlap_comm", true);
-    t->comm_bg_ctas = t->cfg.value("overlap_ctas", 2);
+    t->overlap = t->cfg.value("overlap_comm", false);
+    t->comm_bg_ctas = t->cfg.value("overlap_ctas", 8);
     {
         const char* e = std::getenv("TCB_FUSED_SPLIT_REDUCE");
         t->fused_split_reduce = cfg.value("fused_split_reduce", e != nullptr && e[0] == '1');
@@ -640,6 +640,11 @@ int issue_ready_shards(tcb_trainer* t, int i, cudaStream_t st) {
 
 int backward(tcb_trainer* t, cudaStream_t st) {
     TRY(refresh_transposes(t, st));
+    // overlapped shard reduces run on comm_bg_ctas SMs: keep them free
+    conv_tc_set_sm_reserve(t->overlap_active() ? t->comm_bg_ctas : 0);
+    struct Reset {
+        ~Reset() { conv_tc_set_sm_reserve(0); }
+    } reset;
     float* grad = t->at<float>(t->off_grad);
     for (int i = static_cast<int>(t->nodes.size()) - 1; i >= 0; --i) {
         const Node& nd = t->nodes[i];
