@@ -74,13 +74,16 @@ def _single_rank_grads(cfg, data_rank):
     return t.tensor("param").cpu().numpy(), t.tensor("grad").cpu().numpy()
 
 
-@pytest.mark.parametrize("n_ps", [0, 1])
-def test_two_gpu_ps_step_bit_exact(oracle, n_ps):
+@pytest.mark.parametrize("n_ps,overlap", [(0, False), (1, False), (0, True)])
+def test_two_gpu_ps_step_bit_exact(oracle, n_ps, overlap):
+    """overlap: per-shard ncclReduce to the owner issued during backward on the
+    low-CTA communicator; must give the same bits as reduce-scatter."""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     from paper_1709_06622_b200 import models
     cfg = models.tiny_resnet(batch=8, precision="bf16")
     cfg["n_ps"] = n_ps
+    cfg["overlap_comm"] = overlap
     w0, g0 = _single_rank_grads(cfg, 0)
     _, g1 = _single_rank_grads(cfg, 1)
     s = (g0 + g1).astype(np.float32)
