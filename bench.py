@@ -231,15 +231,28 @@ def lemmas(phases, world, param_bytes, out_dir):
     return out
 
 
+def busbw_peak(world, op):
+    """Best NCCL busbw for `op` measured on this box type by scripts/nccl_busbw.py
+    (profiles/r01_nccl_busbw_g<G>.json), else the peer-copy fallback."""
+    path = os.path.join(ROOT, "profiles", f"r01_nccl_busbw_g{world}.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        best = max(r["busbw_GBps"] for r in d["results"] if r["op"] == op)
+        return best, f"NCCL {d['nccl']} {op} microbenchmark, best over 8 MB-1 GB (profiles/{os.path.basename(path)})"
+    return NVLINK_PEER_GBPS, "peer copy per direction, B200_PROFILING.md (fallback)"
+
+
 def ps_bandwidth(phases, world, param_bytes):
     if world < 2:
         return None
     rs = param_bytes * (world - 1) / world / (phases["reduce_scatter"] / 1e3) / 1e9
     ag = (param_bytes / 2) * (world - 1) / world / (phases["all_gather"] / 1e3) / 1e9  # bf16 refresh
+    prs, src = busbw_peak(world, "reduce_scatter")
+    pag, _ = busbw_peak(world, "all_gather")
     return {"reduce_scatter_busbw_GBps": round(rs, 1), "all_gather_busbw_GBps": round(ag, 1),
-            "peak_GBps": NVLINK_PEER_GBPS, "rs_frac": round(rs / NVLINK_PEER_GBPS, 3),
-            "ag_frac": round(ag / NVLINK_PEER_GBPS, 3),
-            "peak_kind": "peer copy per direction, B200_PROFILING.md (fallback)"}
+            "rs_peak_GBps": prs, "ag_peak_GBps": pag, "rs_frac": round(rs / prs, 3),
+            "ag_frac": round(ag / pag, 3), "peak_kind": src}
 
 
 def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
