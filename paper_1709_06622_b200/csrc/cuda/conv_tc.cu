@@ -434,6 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: the prologue above overlapped the previous kernel's tail; nothing
+    // it wrote is read before this point. Let the next kernel queue up early.
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
     const uint32_t smem_base = ptx::smem_addr(smem);
 
     if (warp < 4 && kTmaOnly) {
@@ -961,6 +965,11 @@ cudaError_t narrow_im2col(const ConvGeom& g, const NarrowPlan& q, const void* x,
 
 // ---------------------------------------------------------------- host ----
 int g_sm_reserve = 0;  // SMs left free for concurrent communication kernels
+// programmatic dependent launch of the conv kernels ($TCB_PDL=0 disables)
+const bool g_pdl = [] {
+    const char* e = getenv("TCB_PDL");
+    return !(e && e[0] == '0');
+}();
 
 int pick_bn(int ncol) { return ncol >= 256 ? 256 : (ncol > 64 ? 128 : 64); }
 
@@ -1063,8 +1072,17 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
     }
     p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
     const int grid = std::min(p.num_tiles, std::max(1, num_sms() - g_sm_reserve));
-    conv_tc_kernel<MODE, BN, LOAD, EPI><<<grid, kThreads, C::kSmem, st>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, conv_tc_kernel<MODE, BN, LOAD, EPI>, p);
 }
 
 int g_epi_kb = -1;  // TMA epilogue for layers with at most this many k-blocks

@@ -153,6 +153,18 @@ __device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const void* des
         : "memory");
 }
 
+// ------------------------------------------- programmatic dependent launch ----
+// Wait until the preceding grid (launched before us in the stream) completed
+// and its memory is visible; a no-op when launched without the PDL attribute.
+__device__ __forceinline__ void griddep_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+// Allow the next grid in the stream to start launching (its CTAs still begin
+// only where resources free up, and it must griddep_wait before reading ours).
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // --------------------------------------------------------------- tcgen05 ----
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
