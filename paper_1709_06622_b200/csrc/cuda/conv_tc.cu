@@ -48,12 +48,12 @@ struct Cfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = EPI ? (BN == 256 ? 3 : (BN == 128 ? 4 : 5))
-                                       : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
+    static constexpr int kStages = EPI ? (BN == 256 ? 3 : BN == 192 ? 4 : BN == 128 ? 4 : 5)
+                                       : (BN == 256 ? 4 : BN == 192 ? 5 : BN == 128 ? 6 : 8);
     static constexpr int kRingBytes = kStages * kStageBytes;
     static constexpr int kEpiWarpBytes = 4 * 2048;  // 2 slots x {in0/out, in1}, 32x32 bf16 each
     static constexpr int kEpiBytes = EPI ? 8 * kEpiWarpBytes : 0;
-    static constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
+    static constexpr uint32_t kTmemCols = BN == 192 ? 512 : 2 * BN;  // two accumulators (pow2)
     static constexpr size_t kSmem = size_t(kRingBytes) + kEpiBytes + 1024 + 512;
 };
 
@@ -971,7 +971,17 @@ const bool g_pdl = [] {
     return !(e && e[0] == '0');
 }();
 
-int pick_bn(int ncol) { return ncol >= 256 ? 256 : (ncol > 64 ? 128 : 64); }
+// Tile width: the fewest padded columns among {256, 192} (ties -> 256) above
+// 128 columns — e.g. Ncol = 576 (3x3x64 wgrad) runs as 3 x 192 instead of
+// 3 x 256 with a quarter-empty last tile. 192 needs the TMA operand paths
+// (the wgrad cp.async gather assumes 128 % (BN/8) == 0).
+int pick_bn(int ncol, bool allow192 = true) {
+    if (ncol <= 64) return 64;
+    if (ncol <= 128) return 128;
+    const int w256 = (ncol + 255) / 256 * 256 - ncol;
+    const int w192 = (ncol + 191) / 192 * 192 - ncol;
+    return allow192 && w192 < w256 ? 192 : 256;
+}
 
 struct SplitPlan {
     int splits, kb_per_split;
@@ -1102,21 +1112,27 @@ bool use_epi(const Params& p) {
 
 template <ConvMode MODE, int LOAD>
 cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
+    const int bn = pick_bn(p.s.Ncol, !(MODE == ConvMode::Wgrad && LOAD == kGather));
     if constexpr (MODE != ConvMode::Wgrad) {
         if (use_epi<MODE>(p)) {
-            switch (pick_bn(p.s.Ncol)) {
+            switch (bn) {
                 case 256: return launch<MODE, 256, LOAD, true>(p, a_matrix, b_matrix, st);
+                case 192: return launch<MODE, 192, LOAD, true>(p, a_matrix, b_matrix, st);
                 case 128: return launch<MODE, 128, LOAD, true>(p, a_matrix, b_matrix, st);
                 default: return launch<MODE, 64, LOAD, true>(p, a_matrix, b_matrix, st);
             }
         }
     }
-    switch (pick_bn(p.s.Ncol)) {
+    switch (bn) {
         case 256: return launch<MODE, 256, LOAD, false>(p, a_matrix, b_matrix, st);
+        case 192:
+            if constexpr (MODE == ConvMode::Wgrad && LOAD == kGather) return cudaErrorInvalidValue;
+            else return launch<MODE, 192, LOAD, false>(p, a_matrix, b_matrix, st);
         case 128: return launch<MODE, 128, LOAD, false>(p, a_matrix, b_matrix, st);
         default: return launch<MODE, 64, LOAD, false>(p, a_matrix, b_matrix, st);
     }
 }
+
 
 int g_force_gather = -1;  // test hook: 1 = always use the cp.async gather path
 
@@ -1126,6 +1142,14 @@ bool force_gather() {
         g_force_gather = (e && e[0] == '1') ? 1 : 0;
     }
     return g_force_gather == 1;
+}
+
+// Wgrad tile width, consistent with the operand path dispatch() will pick.
+int wgrad_bn(const ConvShape& s) {
+    const bool tma = !force_gather() &&
+                     (plain_geometry(s) || (s.C % 64 == 0 && s.R <= 16 && s.S <= 16 && s.ph <= 15 &&
+                                            s.pw <= 15));
+    return pick_bn(s.Ncol, tma);
 }
 
 template <ConvMode MODE>
@@ -1166,7 +1190,7 @@ size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
                conv_tc_workspace(q.g1, ConvMode::Wgrad);
     if (mode != ConvMode::Wgrad) return 0;
     const ConvShape s = make_shape(g, mode);
-    const SplitPlan sp = plan_splits(s, pick_bn(s.Ncol));
+    const SplitPlan sp = plan_splits(s, wgrad_bn(s));
     return sp.splits > 1 ? size_t(sp.splits) * s.M * s.Ncol * sizeof(float) : 0;
 }
 
@@ -1178,8 +1202,9 @@ int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool cou
     if (mode == ConvMode::Dgrad) return g.stride_h * g.stride_w;
     const ConvGeom& gw = q.use ? q.g1 : g;
     const ConvShape s = make_shape(gw, mode);
-    const SplitPlan sp = plan_splits(s, pick_bn(s.Ncol));
-    const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + pick_bn(s.Ncol) - 1) / pick_bn(s.Ncol));
+    const int bn = wgrad_bn(s);
+    const SplitPlan sp = plan_splits(s, bn);
+    const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + bn - 1) / bn);
     const int split = (sp.splits > 1 && !(counters && tiles * sp.splits <= num_sms())) ? 2 : 1;
     return split + (q.use ? (cols_ready ? 1 : 2) : 0);
 }
@@ -1276,14 +1301,14 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
     }
     Params p{};
     p.s = make_shape(g, ConvMode::Wgrad);
-    const SplitPlan sp = plan_splits(p.s, pick_bn(p.s.Ncol));
+    const SplitPlan sp = plan_splits(p.s, wgrad_bn(p.s));
     p.a = static_cast<const __nv_bfloat16*>(dy);
     p.b = static_cast<const __nv_bfloat16*>(x);
     p.splits = sp.splits;
     p.kb_per_split = sp.kb_per_split;
     p.out = sp.splits > 1 ? workspace : static_cast<void*>(dw);
     if (sp.splits > 1 && workspace == nullptr) return cudaErrorInvalidValue;
-    const int bn = pick_bn(p.s.Ncol);
+    const int bn = wgrad_bn(p.s);
     const int tiles = ((p.s.M + BM - 1) / BM) * ((p.s.Ncol + bn - 1) / bn);
     const bool fused = counters && sp.splits > 1 && tiles * sp.splits <= num_sms();
     if (fused) {
