@@ -43,16 +43,20 @@ constexpr int kThreads = kProducerThreads + kEpilogueThreads + 32;
 // EPI: TMA epilogue (side inputs TMA-loaded into per-warp 64B-swizzled staging,
 // outputs TMA-stored) for K-light layers whose time is the epilogue's HBM
 // traffic; it trades ring stages for 64 KB of staging.
-template <int BN, bool EPI = false>
+// EPI = side-input slots per epilogue warp: 0 (register epilogue), 2 (one chunk
+// of lookahead) or 4 (BN >= 192: a warp's whole share of the tile prefetched at
+// once, traded for ring stages — for 1-2 k-block layers).
+template <int BN, int EPI = 0>
 struct Cfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = EPI ? (BN == 256 ? 3 : BN == 192 ? 4 : BN == 128 ? 4 : 5)
-                                       : (BN == 256 ? 4 : BN == 192 ? 5 : BN == 128 ? 6 : 8);
+    static constexpr int kStages = EPI == 4   ? 2
+                                   : EPI == 2 ? (BN == 256 ? 3 : BN == 192 ? 4 : BN == 128 ? 4 : 5)
+                                              : (BN == 256 ? 4 : BN == 192 ? 5 : BN == 128 ? 6 : 8);
     static constexpr int kRingBytes = kStages * kStageBytes;
-    static constexpr int kEpiWarpBytes = 4 * 2048;  // 2 slots x {in0/out, in1}, 32x32 bf16 each
-    static constexpr int kEpiBytes = EPI ? 8 * kEpiWarpBytes : 0;
+    static constexpr int kEpiWarpBytes = EPI * 2 * 2048;  // slot = {in0/out, in1}, 32x32 bf16 each
+    static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
     static constexpr uint32_t kTmemCols = BN == 192 ? 512 : 2 * BN;  // two accumulators (pow2)
     static constexpr size_t kSmem = size_t(kRingBytes) + kEpiBytes + 1024 + 512;
 };
@@ -394,7 +398,7 @@ __device__ __forceinline__ void split_reduce_tile(const Params& p, const TileCoo
 //            landing as no-swizzle 8x16B core matrices (LBO 2 KB, SBO 128 B).
 constexpr int kGather = 0, kPlain = 1, kIm2col = 2, kIm2colC8 = 3;
 
-template <ConvMode MODE, int BN, int LOAD, bool EPI>
+template <ConvMode MODE, int BN, int LOAD, int EPI>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ Params p) {
     using C = Cfg<BN, EPI>;
     constexpr bool kTmaOnly = LOAD != kGather;
@@ -406,9 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     uint64_t* empty = full + C::kStages;
     uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
-    uint64_t* side_bar = tempty + 2;  // EPI: [8 warps][2 slots]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(side_bar + 16);
-    __shared__ int4 pixtab[2][BK];  // wgrad im2col pixel decode (gather mode), double-buffered
+    uint64_t* side_bar = tempty + 2;  // EPI: [8 warps][EPI slots]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(side_bar + 8 * EPI);
+    // wgrad im2col pixel decode (gather mode), double-buffered; a stub elsewhere
+    constexpr int kPixRows = MODE == ConvMode::Wgrad ? BK : 1;
+    __shared__ int4 pixtab[2][kPixRows];
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -422,12 +428,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], kEpilogueThreads);
         }
-        if (EPI)
-            for (int i = 0; i < 16; ++i) ptx::mbar_init(&side_bar[i], 1);
+        for (int i = 0; i < 8 * EPI; ++i) ptx::mbar_init(&side_bar[i], 1);
         ptx::fence_mbarrier_init();
         if (kTmaB) ptx::tma_prefetch_desc(&p.tmap_b);
         if (kTmaOnly) ptx::tma_prefetch_desc(&p.tmap_a);
-        if (EPI) ptx::tma_prefetch_desc(&p.tmap_out);
+        if (EPI > 0) ptx::tma_prefetch_desc(&p.tmap_out);
     }
     if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
@@ -669,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
             __syncwarp();
         }
-    } else if constexpr (EPI) {
+    } else if constexpr (EPI > 0) {
         // ======================================== TMA epilogue (K-light) ======
         // Warp (quarter, half) owns rows quarter*32..+31 and half of the tile's
         // 32-column chunks. Per chunk: residual / mask boxes (32 x 32 bf16,
@@ -682,20 +687,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const int c_begin = half * kHalfChunks, c_end = c_begin + kHalfChunks;
         uint8_t* ebuf = smem + C::kRingBytes + (warp - 4) * C::kEpiWarpBytes;
         const uint32_t ebuf_addr = ptx::smem_addr(ebuf);
-        uint64_t* sbar = side_bar + (warp - 4) * 2;
+        uint64_t* sbar = side_bar + (warp - 4) * EPI;
         const uint32_t side_bytes = (p.residual ? 2048u : 0u) + (p.mask ? 2048u : 0u);
         const int ncol = p.s.Ncol;
+        // kWhole: one slot per chunk of the warp's share, all loaded at tile start
+        constexpr bool kWhole = EPI >= kHalfChunks;
         uint32_t seq = 0;
+        auto load_slot = [&](uint32_t slot, int row0, int col0) {  // lane 0
+            ptx::mbar_arrive_expect_tx(&sbar[slot], side_bytes);
+            if (p.residual)
+                ptx::tma_load_2d(ebuf_addr + slot * 4096, &p.tmap_res, &sbar[slot], col0, row0);
+            if (p.mask)
+                ptx::tma_load_2d(ebuf_addr + slot * 4096 + 2048, &p.tmap_mask, &sbar[slot], col0, row0);
+        };
         auto prefetch = [&](uint32_t sq, int row0, int col0) {
             if (lane == 0 && side_bytes) {
-                const uint32_t slot = sq & 1;
                 ptx::bulk_wait_read<0>();  // the store that last used this slot has read it
-                ptx::mbar_arrive_expect_tx(&sbar[slot], side_bytes);
-                if (p.residual)
-                    ptx::tma_load_2d(ebuf_addr + slot * 4096, &p.tmap_res, &sbar[slot], col0, row0);
-                if (p.mask)
-                    ptx::tma_load_2d(ebuf_addr + slot * 4096 + 2048, &p.tmap_mask, &sbar[slot], col0,
-                                     row0);
+                load_slot(sq & 1, row0, col0);
             }
         };
         int it = 0;
@@ -704,23 +712,33 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int row0 = tc.mt * BM + quarter * 32;
-            prefetch(seq, row0, tc.nt * BN + c_begin * 32);
+            if constexpr (kWhole) {
+                if (lane == 0 && side_bytes) {
+                    ptx::bulk_wait_read<0>();  // the previous tile's stores have read every slot
+                    for (int c = c_begin; c < c_end; ++c) load_slot(c - c_begin, row0, tc.nt * BN + c * 32);
+                }
+            } else {
+                prefetch(seq, row0, tc.nt * BN + c_begin * 32);
+            }
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = c_begin; c < c_end; ++c, ++seq) {
                 const int col0 = tc.nt * BN + c * 32;
-                if (c + 1 < c_end) prefetch(seq + 1, row0, col0 + 32);
+                if (!kWhole && c + 1 < c_end) prefetch(seq + 1, row0, col0 + 32);
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                             acc * BN + c * 32,
                                         v);
                 ptx::tmem_ld_wait();
-                const uint32_t slot = seq & 1;
+                const uint32_t slot = kWhole ? static_cast<uint32_t>(c - c_begin) : (seq & 1);
                 uint8_t* b0 = ebuf + slot * 4096;
-                if (lane == 0 && !side_bytes) ptx::bulk_wait_read<1>();  // store(seq-2) read
+                if (lane == 0 && !side_bytes) {  // the store that last used this slot has read it
+                    if constexpr (kWhole) ptx::bulk_wait_read<kHalfChunks - 1>();
+                    else ptx::bulk_wait_read<1>();
+                }
                 __syncwarp();
-                if (side_bytes) ptx::mbar_wait(&sbar[slot], (seq >> 1) & 1);
+                if (side_bytes) ptx::mbar_wait(&sbar[slot], kWhole ? (it & 1) : ((seq >> 1) & 1));
                 if (col0 < ncol) {
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
@@ -1060,7 +1078,7 @@ bool build_epi_maps(Params& p) {
     return true;
 }
 
-template <ConvMode MODE, int BN, int LOAD, bool EPI>
+template <ConvMode MODE, int BN, int LOAD, int EPI>
 cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
     using C = Cfg<BN, EPI>;
     static bool configured = false;
@@ -1072,7 +1090,7 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
         configured = true;
     }
     if (!build_maps<MODE, LOAD>(p, a_matrix, b_matrix, BN)) return cudaErrorInvalidValue;
-    if (EPI && !build_epi_maps(p)) return cudaErrorInvalidValue;
+    if (EPI > 0 && !build_epi_maps(p)) return cudaErrorInvalidValue;
     p.m_tiles = (p.s.M + BM - 1) / BM;
     p.n_tiles = (p.s.Ncol + BN - 1) / BN;
     p.kb_total = (p.s.Kdim + BK - 1) / BK;
@@ -1115,21 +1133,30 @@ cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, c
     const int bn = pick_bn(p.s.Ncol, !(MODE == ConvMode::Wgrad && LOAD == kGather));
     if constexpr (MODE != ConvMode::Wgrad) {
         if (use_epi<MODE>(p)) {
+            static const int deep_kb = [] {  // whole-share side-input prefetch up to this many k-blocks
+                const char* e = getenv("TCB_EPI_DEEP_KB");
+                return e ? atoi(e) : 2;
+            }();
+            const bool deep = (p.s.Kdim + BK - 1) / BK <= deep_kb;
             switch (bn) {
-                case 256: return launch<MODE, 256, LOAD, true>(p, a_matrix, b_matrix, st);
-                case 192: return launch<MODE, 192, LOAD, true>(p, a_matrix, b_matrix, st);
-                case 128: return launch<MODE, 128, LOAD, true>(p, a_matrix, b_matrix, st);
-                default: return launch<MODE, 64, LOAD, true>(p, a_matrix, b_matrix, st);
+                case 256:
+                    return deep ? launch<MODE, 256, LOAD, 4>(p, a_matrix, b_matrix, st)
+                                : launch<MODE, 256, LOAD, 2>(p, a_matrix, b_matrix, st);
+                case 192:
+                    return deep ? launch<MODE, 192, LOAD, 4>(p, a_matrix, b_matrix, st)
+                                : launch<MODE, 192, LOAD, 2>(p, a_matrix, b_matrix, st);
+                case 128: return launch<MODE, 128, LOAD, 2>(p, a_matrix, b_matrix, st);
+                default: return launch<MODE, 64, LOAD, 2>(p, a_matrix, b_matrix, st);
             }
         }
     }
     switch (bn) {
-        case 256: return launch<MODE, 256, LOAD, false>(p, a_matrix, b_matrix, st);
+        case 256: return launch<MODE, 256, LOAD, 0>(p, a_matrix, b_matrix, st);
         case 192:
             if constexpr (MODE == ConvMode::Wgrad && LOAD == kGather) return cudaErrorInvalidValue;
-            else return launch<MODE, 192, LOAD, false>(p, a_matrix, b_matrix, st);
-        case 128: return launch<MODE, 128, LOAD, false>(p, a_matrix, b_matrix, st);
-        default: return launch<MODE, 64, LOAD, false>(p, a_matrix, b_matrix, st);
+            else return launch<MODE, 192, LOAD, 0>(p, a_matrix, b_matrix, st);
+        case 128: return launch<MODE, 128, LOAD, 0>(p, a_matrix, b_matrix, st);
+        default: return launch<MODE, 64, LOAD, 0>(p, a_matrix, b_matrix, st);
     }
 }
 
