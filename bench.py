@@ -524,10 +524,14 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64-accumulate", "data": "synthetic",
-        "config": {"workload": f"{args.model}_synthetic_224", "per_gpu_batch": 1,
-                   "precision": args.precision},
+        # same workload as the B200 arm; each timed step is a bounded sample of it
+        # (one image through the full fwd + bwd + SGD step), the rate is images/s
+        "config": {"workload": f"{args.model}_synthetic_224" if args.model == "resnet50" else args.model,
+                   "per_gpu_batch": args.batch, "global_batch": args.batch * args.gpus,
+                   "precision": args.precision, "parallelism": f"dp{args.gpus}"},
         "cpu_baseline": {"kind": "port", "cores": r["cores"], "value": v, "unit": "images/s",
-                         "sample": f"{args.model} training step at batch 1 per timed step"},
+                         "sample": f"{args.model} training step on 1 image of the {args.batch}-image "
+                                   f"batch per timed step ({sec:.2f} s), median of {args.steps}"},
         "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
