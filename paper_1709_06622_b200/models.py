@@ -139,15 +139,19 @@ def resnet50(batch=256, stages=(3, 4, 6, 3), width=64, image=224, **opts):
         for bi in range(blocks):
             stride = 2 if (bi == 0 and si > 0) else 1
             pre = f"s{si + 1}b{bi + 1}"
+            y = b.conv(planes, 1, src=x, name=pre + "_c1")
+            y = b.conv(planes, 3, pad=1, stride=stride, name=pre + "_c2")
+            # the projection comes after c1 in graph order so that c1 (dense, stride 1)
+            # is the final writer of the block input's gradient: the strided projection
+            # dgrad then writes plain zeros at the pixels its stride skips, instead of
+            # copying c1's gradient x ReLU mask there
             if bi == 0:
                 short = b.conv(planes * 4, 1, stride=stride, relu=False, src=x, name=pre + "_proj")
             else:
                 short = x
-            y = b.conv(planes, 1, src=x, name=pre + "_c1")
-            y = b.conv(planes, 3, pad=1, stride=stride, name=pre + "_c2")
             # no BN: a small init gain on the branch's last conv keeps the residual
             # stream's variance bounded over the 16 blocks (Fixup-style)
-            x = b.conv(planes * 4, 1, residual=short, name=pre + "_c3", init_gain=0.2)
+            x = b.conv(planes * 4, 1, src=y, residual=short, name=pre + "_c3", init_gain=0.2)
             inplanes = planes * 4
     b.avgpool()
     b.fc(b.cfg["classes"], relu=False, name="fc")
