@@ -1,6 +1,7 @@
 // Shared device helpers: fast integer division, the implicit-GEMM view of a
 // convolution, dtype load/store, launch checks.
 #pragma once
+#include <utility>
 
 #include <cstdint>
 #include <cuda_bf16.h>
@@ -132,6 +133,31 @@ inline int num_sms() {
         if (sms <= 0) sms = 148;
     }
     return sms;
+}
+
+
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor drains and must call pdl_wait() before touching
+// anything the predecessor wrote.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 }  // namespace tcb

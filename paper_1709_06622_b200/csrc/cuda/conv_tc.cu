@@ -837,6 +837,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 // Dgrad phases without any filter tap (e.g. odd pixels of a 1x1 stride-2
 // conv): dx = residual_grad * mask (or 0).
 __global__ void dgrad_empty_phase_kernel(const Params p) {
+    pdl_wait();
+    pdl_trigger();
     const int groups = p.s.Ncol / 8;  // C % 8 == 0 on the tensor-core path
     const size_t total = size_t(p.s.M) * groups;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
@@ -1295,8 +1297,7 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* w, cons
             if (p.s.Kdim == 0) {
                 const size_t total = size_t(p.s.M) * (p.s.Ncol / 8);
                 const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 8192));
-                dgrad_empty_phase_kernel<<<blocks, 256, 0, st>>>(p);
-                e = cudaGetLastError();
+                e = launch_pdl(dgrad_empty_phase_kernel, dim3(blocks), dim3(256), 0, st, p);
             } else {
                 e = dispatch<ConvMode::Dgrad>(
                     p, dy, wTp ? static_cast<const void*>(static_cast<const __nv_bfloat16*>(wTp) + p.ph.woff)

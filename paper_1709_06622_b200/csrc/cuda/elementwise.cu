@@ -143,6 +143,8 @@ __global__ void split_reduce_kernel(const float* __restrict__ parts, int splits,
 
 __global__ void split_reduce4_kernel(const float4* __restrict__ parts, int splits, size_t n4,
                                      float4* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
          i += size_t(gridDim.x) * blockDim.x) {
         float4 acc = __ldcs(parts + i);
@@ -169,6 +171,8 @@ __global__ void __launch_bounds__(256) split_reduce4_tree_kernel(const float4* _
                                                                  int splits, size_t n4,
                                                                  float4* __restrict__ out) {
     __shared__ float4 part[8][32];
+    pdl_wait();
+    pdl_trigger();
     const int e = threadIdx.x & 31, g = threadIdx.x >> 5;
     const size_t i = blockIdx.x * size_t(32) + e;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -532,11 +536,13 @@ cudaError_t split_reduce(const float* parts, int splits, size_t n, float* out, c
     const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(parts) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0);
     if (vec && splits >= 16 && n / 4 < size_t(num_sms()) * 256 * 4)
-        split_reduce4_tree_kernel<<<static_cast<int>((n / 4 + 31) / 32), 256, 0, st>>>(
-            reinterpret_cast<const float4*>(parts), splits, n / 4, reinterpret_cast<float4*>(out));
+        return launch_pdl(split_reduce4_tree_kernel, dim3(static_cast<int>((n / 4 + 31) / 32)), dim3(256), 0,
+                          st, reinterpret_cast<const float4*>(parts), splits, n / 4,
+                          reinterpret_cast<float4*>(out));
     else if (vec)
-        split_reduce4_kernel<<<grid_for(n / 4, 2), kBlock, 0, st>>>(
-            reinterpret_cast<const float4*>(parts), splits, n / 4, reinterpret_cast<float4*>(out));
+        return launch_pdl(split_reduce4_kernel, dim3(grid_for(n / 4, 2)), dim3(kBlock), 0, st,
+                          reinterpret_cast<const float4*>(parts), splits, n / 4,
+                          reinterpret_cast<float4*>(out));
     else
         split_reduce_kernel<<<grid_for(n), kBlock, 0, st>>>(parts, splits, n, out);
     return cudaGetLastError();
