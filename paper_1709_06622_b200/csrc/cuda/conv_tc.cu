@@ -46,14 +46,19 @@ constexpr int kThreads = kProducerThreads + kEpilogueThreads + 32;
 // EPI = side-input slots per epilogue warp: 0 (register epilogue), 2 (one chunk
 // of lookahead) or 4 (BN >= 192: a warp's whole share of the tile prefetched at
 // once, traded for ring stages — for 1-2 k-block layers).
-template <int BN, int EPI = 0>
+// CTA2: a cluster pair runs M = 256 tiles with tcgen05 cta_group::2 — each CTA
+// holds its 128 A rows and half of the B columns, so per-SM operand traffic
+// drops by a third and more stages fit.
+template <int BN, int EPI = 0, bool CTA2 = false>
 struct Cfg {
     static constexpr int kABytes = BM * BK * 2;
-    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2 / (CTA2 ? 2 : 1);  // this CTA's share
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = EPI == 4   ? 2
-                                   : EPI == 2 ? (BN == 256 ? 3 : BN == 192 ? 4 : BN == 128 ? 4 : 5)
-                                              : (BN == 256 ? 4 : BN == 192 ? 5 : BN == 128 ? 6 : 8);
+    static constexpr int kStages =
+        CTA2 ? (EPI == 4 ? 2 : EPI == 2 ? (BN == 256 ? 4 : 6) : (BN == 256 ? 6 : 8))
+             : EPI == 4 ? 2
+             : EPI == 2 ? (BN == 256 ? 3 : BN == 192 ? 4 : BN == 128 ? 4 : 5)
+                        : (BN == 256 ? 4 : BN == 192 ? 5 : BN == 128 ? 6 : 8);
     static constexpr int kRingBytes = kStages * kStageBytes;
     static constexpr int kEpiWarpBytes = EPI * 2 * 2048;  // slot = {in0/out, in1}, 32x32 bf16 each
     static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
@@ -75,6 +80,8 @@ struct Params {
     const __nv_bfloat16* mask;
     int relu;
     int m_tiles, n_tiles, splits, kb_total, kb_per_split, num_tiles;
+    int cta2;     // host decision: run as CTA pairs (num_tiles then counts pair units)
+    int m_pairs;  // ceil(m_tiles / 2)
     // wgrad split-K reduced in-kernel: set when all units are co-resident (one
     // wave); partials in `out`, final sums to `dw`, 2 self-resetting counters per tile
     float* dw;
@@ -88,12 +95,18 @@ struct TileCoord {
     int split, mt, nt, kb_begin, kb_end;
 };
 
-__device__ __forceinline__ TileCoord tile_coord(const Params& p, int t) {
+template <bool CTA2 = false>
+__device__ __forceinline__ TileCoord tile_coord(const Params& p, int t, uint32_t rank = 0) {
     TileCoord c;
     c.nt = t % p.n_tiles;
     const int rest = t / p.n_tiles;
-    c.mt = rest % p.m_tiles;
-    c.split = rest / p.m_tiles;
+    if constexpr (CTA2) {
+        c.mt = 2 * (rest % p.m_pairs) + static_cast<int>(rank);
+        c.split = rest / p.m_pairs;
+    } else {
+        c.mt = rest % p.m_tiles;
+        c.split = rest / p.m_tiles;
+    }
     c.kb_begin = c.split * p.kb_per_split;
     c.kb_end = min(p.kb_total, c.kb_begin + p.kb_per_split);
     return c;
@@ -398,9 +411,12 @@ __device__ __forceinline__ void split_reduce_tile(const Params& p, const TileCoo
 //            landing as no-swizzle 8x16B core matrices (LBO 2 KB, SBO 128 B).
 constexpr int kGather = 0, kPlain = 1, kIm2col = 2, kIm2colC8 = 3;
 
-template <ConvMode MODE, int BN, int LOAD, int EPI>
+template <ConvMode MODE, int BN, int LOAD, int EPI, bool CTA2>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ Params p) {
-    using C = Cfg<BN, EPI>;
+    using C = Cfg<BN, EPI, CTA2>;
+    const uint32_t rank = CTA2 ? ptx::cluster_ctarank() : 0u;  // 0 = the pair's MMA leader
+    const int unit0 = CTA2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+    const int ustride = CTA2 ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
     constexpr bool kTmaOnly = LOAD != kGather;
     constexpr bool kTmaB = MODE != ConvMode::Wgrad || kTmaOnly;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -426,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], kEpilogueThreads);
+            ptx::mbar_init(&tempty[i], (CTA2 ? 2 : 1) * kEpilogueThreads);
         }
         for (int i = 0; i < 8 * EPI; ++i) ptx::mbar_init(&side_bar[i], 1);
         ptx::fence_mbarrier_init();
@@ -434,9 +450,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         if (kTmaOnly) ptx::tma_prefetch_desc(&p.tmap_a);
         if (EPI > 0) ptx::tma_prefetch_desc(&p.tmap_out);
     }
-    if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    if (warp == kMmaWarp) {
+        if constexpr (CTA2) ptx::tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
+        else ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CTA2) ptx::cluster_sync();  // peer barriers initialised before any remote signal
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // PDL: the prologue above overlapped the previous kernel's tail; nothing
@@ -451,8 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             const ConvShape& s = p.s;
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                const TileCoord tc = tile_coord(p, t);
+            for (int t = unit0; t < p.num_tiles; t += ustride) {
+                const TileCoord tc = tile_coord<CTA2>(p, t, rank);
                 // im2col base position of the tile's first GEMM row (fwd / dgrad)
                 int bn = 0, bw = 0, bh = 0;
                 if constexpr ((LOAD == kIm2col || LOAD == kIm2colC8) && MODE != ConvMode::Wgrad) {
@@ -475,37 +495,50 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t a_smem = smem_base + stage * C::kStageBytes;
                     const uint32_t b_smem = a_smem + C::kABytes;
-                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    // CTA pairs: both CTAs load their shares, completion bytes land on the
+                    // leader's barrier, which expects the pair's total
+                    const uint32_t bar_u = CTA2 ? ptx::leader_addr(ptx::smem_addr(&full[stage]))
+                                                : ptx::smem_addr(&full[stage]);
+                    if (!CTA2 || rank == 0)
+                        ptx::mbar_arrive_expect_tx(&full[stage], (CTA2 ? 2 : 1) * C::kStageBytes);
+                    auto ld2 = [&](uint32_t dst, const CUtensorMap* m, int c0, int c1) {
+                        if constexpr (CTA2) ptx::tma_load_2d_2sm(dst, m, bar_u, c0, c1);
+                        else ptx::tma_load_2d(dst, m, &full[stage], c0, c1);
+                    };
+                    auto ldi = [&](uint32_t dst, const CUtensorMap* m, int c, int w, int h, int n,
+                                   uint16_t ow, uint16_t oh) {
+                        if constexpr (CTA2) ptx::tma_load_im2col_4d_2sm(dst, m, bar_u, c, w, h, n, ow, oh);
+                        else ptx::tma_load_im2col_4d(dst, m, &full[stage], c, w, h, n, ow, oh);
+                    };
+                    // B boxes of 64 N-elements: a pair's CTA takes its half
+                    constexpr int kNB = CTA2 ? BN / 128 : BN / 64;
+                    const int jb0 = CTA2 ? static_cast<int>(rank) * kNB : 0;
                     if constexpr (MODE == ConvMode::Wgrad) {
                         // A = dy [P][K]: MN-major 64-channel x 64-pixel boxes (8 KB each)
-                        ptx::tma_load_2d(a_smem, &p.tmap_a, &full[stage], tc.mt * BM, kb * BK);
-                        ptx::tma_load_2d(a_smem + 8192, &p.tmap_a, &full[stage], tc.mt * BM + 64,
-                                         kb * BK);
+                        ld2(a_smem, &p.tmap_a, tc.mt * BM, kb * BK);
+                        ld2(a_smem + 8192, &p.tmap_a, tc.mt * BM + 64, kb * BK);
                         if constexpr (LOAD == kPlain) {
 #pragma unroll
-                            for (int j = 0; j < BN / 64; ++j)
-                                ptx::tma_load_2d(b_smem + j * 8192, &p.tmap_b, &full[stage],
-                                                 tc.nt * BN + j * 64, kb * BK);
+                            for (int j = 0; j < kNB; ++j)
+                                ld2(b_smem + j * 8192, &p.tmap_b, tc.nt * BN + (jb0 + j) * 64, kb * BK);
                         } else {
                             // B = im2col(x): 64 pixels x 64 channels of one tap per box
                             const int4 px = wgrad_pixel(s, kb * BK);
                             const int pn = px.x >= 0 ? px.x / s.H : s.N;
 #pragma unroll
-                            for (int j = 0; j < BN / 64; ++j) {
-                                int col0 = tc.nt * BN + j * 64;
+                            for (int j = 0; j < kNB; ++j) {
+                                int col0 = tc.nt * BN + (jb0 + j) * 64;
                                 if (col0 >= s.Ncol) col0 = 0;  // padding columns: never stored
                                 uint32_t rs, c0, r, sx;
                                 s.d_c.divmod(static_cast<uint32_t>(col0), rs, c0);
                                 s.d_s.divmod(rs, r, sx);
-                                ptx::tma_load_im2col_4d(b_smem + j * 8192, &p.tmap_b, &full[stage],
-                                                        static_cast<int>(c0), px.z, px.y, pn,
-                                                        static_cast<uint16_t>(sx),
-                                                        static_cast<uint16_t>(r));
+                                ldi(b_smem + j * 8192, &p.tmap_b, static_cast<int>(c0), px.z, px.y, pn,
+                                    static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
                             }
                         }
                     } else {
                         if constexpr (LOAD == kPlain) {
-                            ptx::tma_load_2d(a_smem, &p.tmap_a, &full[stage], kb * BK, tc.mt * BM);
+                            ld2(a_smem, &p.tmap_a, kb * BK, tc.mt * BM);
                         } else if constexpr (LOAD == kIm2colC8) {
                             const int taps = s.R * s.S;
 #pragma unroll
@@ -528,10 +561,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                                 s.d_k.divmod(kk0, tap, c0);
                                 p.d_ts.divmod(tap, r, sx);
                             }
-                            ptx::tma_load_im2col_4d(a_smem, &p.tmap_a, &full[stage],
-                                                    static_cast<int>(c0), bw, bh, bn,
-                                                    static_cast<uint16_t>(sx),
-                                                    static_cast<uint16_t>(r));
+                            ldi(a_smem, &p.tmap_a, static_cast<int>(c0), bw, bh, bn,
+                                static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
                         }
                         if constexpr (MODE == ConvMode::Dgrad) {
                             // B straight from w[K][R*S][C]: the k-block is filters k0..k0+63
@@ -542,12 +573,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                             const int rf = p.ph.r0 + (p.ph.tr - 1 - static_cast<int>(ri)) * s.sh;
                             const int sf = p.ph.s0 + (p.ph.ts - 1 - static_cast<int>(si)) * s.sw;
 #pragma unroll
-                            for (int j = 0; j < BN / 64; ++j)
-                                ptx::tma_load_3d(b_smem + j * 8192, &p.tmap_b, &full[stage],
-                                                 tc.nt * BN + j * 64, rf * s.S + sf,
-                                                 static_cast<int>(k0));
+                            for (int j = 0; j < kNB; ++j) {
+                                if constexpr (CTA2)
+                                    ptx::tma_load_3d_2sm(b_smem + j * 8192, &p.tmap_b, bar_u,
+                                                         tc.nt * BN + (jb0 + j) * 64, rf * s.S + sf,
+                                                         static_cast<int>(k0));
+                                else
+                                    ptx::tma_load_3d(b_smem + j * 8192, &p.tmap_b, &full[stage],
+                                                     tc.nt * BN + (jb0 + j) * 64, rf * s.S + sf,
+                                                     static_cast<int>(k0));
+                            }
                         } else {
-                            ptx::tma_load_2d(b_smem, &p.tmap_b, &full[stage], kb * BK, tc.nt * BN);
+                            // K-major weights: this CTA's BN / (1 + CTA2) rows
+                            ld2(b_smem, &p.tmap_b, kb * BK, tc.nt * BN + (CTA2 ? static_cast<int>(rank) * BN / 2 : 0));
                         }
                     }
                     if (++stage == C::kStages) {
@@ -562,8 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         int stage = 0;
         uint32_t phase = 0;
         int kb_seq = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const TileCoord tc = tile_coord(p, t);
+        for (int t = unit0; t < p.num_tiles; t += ustride) {
+            const TileCoord tc = tile_coord<CTA2>(p, t, rank);
             int row_n = 0, row_hb = 0, row_wb = 0;
             bool row_ok = false;
             WgradCol col{0, 0, 0, false};
@@ -625,15 +663,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         ptx::cp_async_wait<0>();
     } else if (warp == kMmaWarp) {
         // =============================================== MMA issuer ======
+        // (CTA pairs: the leader issues M = 256 MMAs over both CTAs' smem; the
+        // follower's MMA warp only takes part in the TMEM alloc / dealloc)
         constexpr uint32_t kMN = MODE == ConvMode::Wgrad ? 1u : 0u;
         // dgrad with TMA operands reads B (the filters) MN-major
         constexpr bool kBmn = MODE == ConvMode::Wgrad || (MODE == ConvMode::Dgrad && kTmaOnly);
-        constexpr uint32_t idesc = ptx::make_idesc(1, BM, BN, kMN, kBmn ? 1u : 0u);
+        constexpr uint32_t idesc = ptx::make_idesc(1, CTA2 ? 2 * BM : BM, BN, kMN, kBmn ? 1u : 0u);
+        if (!CTA2 || rank == 0) {
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-            const TileCoord tc = tile_coord(p, t);
+        for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
+            const TileCoord tc = tile_coord<CTA2>(p, t, rank);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -661,9 +702,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                             ad = ptx::sw128_desc(a_addr + k * 32, 16, 1024);
                             bd = ptx::sw128_desc(b_addr + k * 32, 16, 1024);
                         }
-                        ptx::umma_f16(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
+                        if constexpr (CTA2)
+                            ptx::umma_f16_2sm(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
+                        else
+                            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
                     }
-                    ptx::umma_commit(&empty[stage]);
+                    if constexpr (CTA2) ptx::umma_commit_2sm(&empty[stage], 3);
+                    else ptx::umma_commit(&empty[stage]);
                 }
                 __syncwarp();
                 if (++stage == C::kStages) {
@@ -671,8 +716,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     phase ^= 1;
                 }
             }
-            if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
+            if (ptx::elect_one()) {
+                if constexpr (CTA2) ptx::umma_commit_2sm(&tfull[acc], 3);
+                else ptx::umma_commit(&tfull[acc]);
+            }
             __syncwarp();
+        }
         }
     } else if constexpr (EPI > 0) {
         // ======================================== TMA epilogue (K-light) ======
@@ -707,8 +756,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             }
         };
         int it = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-            const TileCoord tc = tile_coord(p, t);
+        for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
+            const TileCoord tc = tile_coord<CTA2>(p, t, rank);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int row0 = tc.mt * BM + quarter * 32;
@@ -779,7 +828,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 }
             }
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[acc]);
+            if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
+            else ptx::mbar_arrive(&tempty[acc]);
         }
         if (lane == 0) ptx::bulk_wait<0>();
     } else {
@@ -792,8 +842,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const int c_begin = half * kHalfChunks, c_end = c_begin + kHalfChunks;
         const int row = quarter * 32 + (tid & 31);
         int it = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-            const TileCoord tc = tile_coord(p, t);
+        for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
+            const TileCoord tc = tile_coord<CTA2>(p, t, rank);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int m = tc.mt * BM + row;
@@ -819,7 +869,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 cur = nxt;
             }
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[acc]);
+            if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
+            else ptx::mbar_arrive(&tempty[acc]);
             if constexpr (MODE == ConvMode::Wgrad) {
                 if (p.counters) split_reduce_tile<BN>(p, tc, tid - kProducerThreads);
             }
@@ -827,10 +878,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CTA2) ptx::cluster_sync();  // the leader's MMAs read the follower's smem
+    else __syncthreads();
     if (warp == kMmaWarp) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+        if constexpr (CTA2) ptx::tmem_dealloc_2sm<C::kTmemCols>(tmem_base);
+        else ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
     }
 }
 
@@ -1007,12 +1060,14 @@ struct SplitPlan {
     int splits, kb_per_split;
 };
 
-SplitPlan plan_splits(const ConvShape& s, int bn) {
+SplitPlan plan_splits(const ConvShape& s, int bn, bool pair = false) {
     const int kb_total = (s.Kdim + BK - 1) / BK;
-    const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + bn - 1) / bn);
-    // one exact wave: splits * tiles <= #SMs, so every CTA runs one equal unit
-    // (no tail round) and the fp32 partials stay as few as the wave allows
-    int want = std::max(1, (num_sms() - g_sm_reserve) / tiles);
+    const int m_tiles = (s.M + BM - 1) / BM;
+    const int tiles = (pair ? (m_tiles + 1) / 2 : m_tiles) * ((s.Ncol + bn - 1) / bn);
+    // one exact wave: splits * tiles <= #SMs (#pairs), so every CTA runs one equal
+    // unit (no tail round) and the fp32 partials stay as few as the wave allows
+    const int slots = (num_sms() - g_sm_reserve) / (pair ? 2 : 1);
+    int want = std::max(1, slots / tiles);
     want = std::min(want, std::max(1, kb_total / 4));  // keep >= 4 k-blocks per split
     want = std::min(want, 64);
     const int per = (kb_total + want - 1) / want;
@@ -1080,39 +1135,60 @@ bool build_epi_maps(Params& p) {
     return true;
 }
 
-template <ConvMode MODE, int BN, int LOAD, int EPI>
+template <ConvMode MODE, int BN, int LOAD, int EPI, bool CTA2 = false>
 cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
-    using C = Cfg<BN, EPI>;
+    using C = Cfg<BN, EPI, CTA2>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, LOAD, EPI>,
+        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, LOAD, EPI, CTA2>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(C::kSmem));
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (!build_maps<MODE, LOAD>(p, a_matrix, b_matrix, BN)) return cudaErrorInvalidValue;
+    // K-major weight boxes: a pair's CTA loads BN / 2 rows
+    if (!build_maps<MODE, LOAD>(p, a_matrix, b_matrix, CTA2 ? BN / 2 : BN)) return cudaErrorInvalidValue;
     if (EPI > 0 && !build_epi_maps(p)) return cudaErrorInvalidValue;
     p.m_tiles = (p.s.M + BM - 1) / BM;
+    p.m_pairs = (p.m_tiles + 1) / 2;
     p.n_tiles = (p.s.Ncol + BN - 1) / BN;
     p.kb_total = (p.s.Kdim + BK - 1) / BK;
+    p.cta2 = CTA2 ? 1 : 0;
     if (MODE != ConvMode::Wgrad) {
         p.splits = 1;
         p.kb_per_split = p.kb_total;
     }
-    p.num_tiles = p.m_tiles * p.n_tiles * p.splits;
-    const int grid = std::min(p.num_tiles, std::max(1, num_sms() - g_sm_reserve));
+    p.num_tiles = (CTA2 ? p.m_pairs : p.m_tiles) * p.n_tiles * p.splits;
+    const int sms = std::max(2, num_sms() - g_sm_reserve);
+    const int grid = CTA2 ? 2 * std::min(p.num_tiles, sms / 2) : std::min(p.num_tiles, sms);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CTA2 ? 2 : 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, conv_tc_kernel<MODE, BN, LOAD, EPI>, p);
+    cfg.numAttrs = CTA2 ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, conv_tc_kernel<MODE, BN, LOAD, EPI, CTA2>, p);
+}
+
+// CTA pairs for K-heavy TMA-operand layers with at least two 128-row tiles
+// ($TCB_CTA2=0 disables; $TCB_CTA2_KB = minimum k-blocks, default 17).
+bool cta2_wanted(int load, int bn, int m_tiles, int kb_total) {
+    static const int min_kb = [] {
+        const char* e = getenv("TCB_CTA2");
+        if (e && e[0] == '0') return 1 << 30;
+        const char* k = getenv("TCB_CTA2_KB");
+        return k ? atoi(k) : 17;
+    }();
+    return (load == kPlain || load == kIm2col) && (bn == 128 || bn == 256) && m_tiles >= 2 &&
+           kb_total >= min_kb;
 }
 
 int g_epi_kb = -1;  // TMA epilogue for layers with at most this many k-blocks
@@ -1152,6 +1228,13 @@ cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, c
             }
         }
     }
+    if constexpr (LOAD == kPlain || LOAD == kIm2col) {
+        const bool pair = MODE == ConvMode::Wgrad
+                              ? p.cta2 != 0
+                              : cta2_wanted(LOAD, bn, (p.s.M + BM - 1) / BM, (p.s.Kdim + BK - 1) / BK);
+        if (pair && bn == 256) return launch<MODE, 256, LOAD, 0, true>(p, a_matrix, b_matrix, st);
+        if (pair && bn == 128) return launch<MODE, 128, LOAD, 0, true>(p, a_matrix, b_matrix, st);
+    }
     switch (bn) {
         case 256: return launch<MODE, 256, LOAD, 0>(p, a_matrix, b_matrix, st);
         case 192:
@@ -1171,6 +1254,15 @@ bool force_gather() {
         g_force_gather = (e && e[0] == '1') ? 1 : 0;
     }
     return g_force_gather == 1;
+}
+
+// Wgrad as CTA pairs (same operand-path rule as dispatch(), same tile width).
+bool wgrad_pair(const ConvShape& s, int bn) {
+    if (force_gather()) return false;
+    const bool plain = plain_geometry(s);
+    const bool im2col = s.C % 64 == 0 && s.R <= 16 && s.S <= 16 && s.ph <= 15 && s.pw <= 15;
+    if (!plain && !im2col) return false;
+    return cta2_wanted(plain ? kPlain : kIm2col, bn, (s.M + BM - 1) / BM, (s.Kdim + BK - 1) / BK);
 }
 
 // Wgrad tile width, consistent with the operand path dispatch() will pick.
@@ -1219,7 +1311,8 @@ size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
                conv_tc_workspace(q.g1, ConvMode::Wgrad);
     if (mode != ConvMode::Wgrad) return 0;
     const ConvShape s = make_shape(g, mode);
-    const SplitPlan sp = plan_splits(s, wgrad_bn(s));
+    const int bn = wgrad_bn(s);
+    const SplitPlan sp = plan_splits(s, bn, wgrad_pair(s, bn));
     return sp.splits > 1 ? size_t(sp.splits) * s.M * s.Ncol * sizeof(float) : 0;
 }
 
@@ -1232,8 +1325,9 @@ int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool cou
     const ConvGeom& gw = q.use ? q.g1 : g;
     const ConvShape s = make_shape(gw, mode);
     const int bn = wgrad_bn(s);
-    const SplitPlan sp = plan_splits(s, bn);
-    const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + bn - 1) / bn);
+    const bool pair = wgrad_pair(s, bn);
+    const SplitPlan sp = plan_splits(s, bn, pair);
+    const int tiles = (pair ? ((s.M + BM - 1) / BM + 1) / 2 * 2 : (s.M + BM - 1) / BM) * ((s.Ncol + bn - 1) / bn);
     const int split = (sp.splits > 1 && !(counters && tiles * sp.splits <= num_sms())) ? 2 : 1;
     return split + (q.use ? (cols_ready ? 1 : 2) : 0);
 }
@@ -1329,7 +1423,10 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
     }
     Params p{};
     p.s = make_shape(g, ConvMode::Wgrad);
-    const SplitPlan sp = plan_splits(p.s, wgrad_bn(p.s));
+    const int bn0 = wgrad_bn(p.s);
+    const bool pair = wgrad_pair(p.s, bn0);
+    p.cta2 = pair ? 1 : 0;
+    const SplitPlan sp = plan_splits(p.s, bn0, pair);
     p.a = static_cast<const __nv_bfloat16*>(dy);
     p.b = static_cast<const __nv_bfloat16*>(x);
     p.splits = sp.splits;

@@ -36,6 +36,9 @@ GEOMS = [
     ("plain_1x1_k48", 2, 7, 9, 200, 48, 1, 0, 1),
     ("bn192_fwd_k192", 2, 9, 9, 64, 192, 3, 1, 1),
     ("bn192_dgrad_c192", 2, 9, 9, 192, 64, 1, 0, 1),
+    ("cta2_fwd_dgrad_3x3", 2, 16, 16, 128, 256, 3, 1, 1),
+    ("cta2_ragged_3x3", 3, 9, 11, 128, 128, 3, 1, 1),
+    ("cta2_wgrad_1x1", 8, 14, 14, 256, 512, 1, 0, 1),
     ("dgrad_phase_3x3_s2_odd", 2, 15, 13, 32, 48, 3, 1, 2),
     ("dgrad_phase_5x5_s3", 2, 17, 16, 16, 24, 5, 2, 3),
     ("im2col_ragged", 3, 9, 11, 64, 72, 3, 1, 1),
