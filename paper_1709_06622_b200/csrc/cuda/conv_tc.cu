@@ -1179,13 +1179,13 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
 }
 
 // CTA pairs for K-heavy TMA-operand layers with at least two 128-row tiles
-// ($TCB_CTA2=0 disables; $TCB_CTA2_KB = minimum k-blocks, default 17).
+// ($TCB_CTA2=0 disables; $TCB_CTA2_KB = minimum k-blocks, default 9).
 bool cta2_wanted(int load, int bn, int m_tiles, int kb_total) {
     static const int min_kb = [] {
         const char* e = getenv("TCB_CTA2");
         if (e && e[0] == '0') return 1 << 30;
         const char* k = getenv("TCB_CTA2_KB");
-        return k ? atoi(k) : 17;
+        return k ? atoi(k) : 9;
     }();
     return (load == kPlain || load == kIm2col) && (bn == 128 || bn == 256) && m_tiles >= 2 &&
            kb_total >= min_kb;
@@ -1200,7 +1200,7 @@ bool use_epi(const Params& p) {
     if (MODE == ConvMode::Dgrad && (p.s.sh != 1 || p.s.sw != 1)) return false;
     if (g_epi_kb < 0) {
         const char* e = getenv("TCB_CONV_EPI_KB");
-        g_epi_kb = e ? atoi(e) : 16;
+        g_epi_kb = e ? atoi(e) : 8;
     }
     if (p.s.Ncol % 8 != 0) return false;
     return (p.s.Kdim + BK - 1) / BK <= g_epi_kb;
