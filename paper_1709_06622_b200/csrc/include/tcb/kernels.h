@@ -64,7 +64,7 @@ bool conv_tc_supported(const ConvGeom& g, ConvMode mode);
 // 0: pick plain-TMA / im2col-TMA / gather per geometry.
 void conv_tc_set_force_gather(int on);
 // TMA epilogue for layers with at most `kb` 64-deep k-blocks (0 = never,
-// -1 = default: $TCB_CONV_EPI_KB or 16).
+// -1 = default: $TCB_CONV_EPI_KB or 8).
 void conv_tc_set_epi_kb(int kb);
 // Persistent conv kernels use at most #SMs - sms CTAs (SMs kept free for
 // communication kernels running concurrently).
