@@ -1,16 +1,14 @@
 #!/bin/bash
-# 2/4-GPU pass: weak-scaling bench, NCCL busbw microbench, VGG-16 N_ps sweep,
-# multi-GPU PS tests, plus the one-GPU conv DRAM-traffic capture.
-#   gpurun --gpus 4 --timeout 2400 -- bash scripts/multi_gpu_check.sh r01s
-tag=${1:-r01s}
+# 2/4-GPU pass: weak-scaling bench (with e2e), NCCL busbw microbench, VGG-16 N_ps
+# sweep, multi-GPU PS tests.
+#   gpurun --gpus 4 --timeout 2400 -- bash scripts/multi_gpu_check.sh <tag>
+tag=${1:-r01}
 out=gpurun_out
 mkdir -p $out
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
 timeout 600 python bench.py --no-cpu-baseline > $out/${tag}_bench_g1.json 2> $out/${tag}_bench_g1.err
 timeout 600 $TR --nproc-per-node 2 --master-port 29511 bench.py --gpus 2 --no-cpu-baseline > $out/${tag}_bench_g2.json 2> $out/${tag}_bench_g2.err
 timeout 600 $TR --nproc-per-node 4 --master-port 29512 bench.py --gpus 4 --no-cpu-baseline > $out/${tag}_bench_g4.json 2> $out/${tag}_bench_g4.err
-timeout 600 $TR --nproc-per-node 4 --master-port 29519 bench.py --gpus 4 --no-cpu-baseline --no-e2e --no-overlap > $out/${tag}_bench_g4_nooverlap.json 2> $out/${tag}_bench_g4_nooverlap.err
-timeout 300 $TR --nproc-per-node 2 --master-port 29513 scripts/nccl_busbw.py > $out/${tag}_busbw_g2.json 2> $out/${tag}_busbw_g2.err
 timeout 300 $TR --nproc-per-node 4 --master-port 29514 scripts/nccl_busbw.py > $out/${tag}_busbw_g4.json 2> $out/${tag}_busbw_g4.err
 for n in 1 2 4; do
   timeout 600 $TR --nproc-per-node 4 --master-port 2952$n bench.py --gpus 4 --model vgg16 --batch 64 --n-ps $n --no-cpu-baseline --no-e2e \
@@ -18,5 +16,3 @@ for n in 1 2 4; do
 done
 timeout 900 python -m pytest tests/test_ps_multigpu.py -x -q -p no:cacheprovider --timeout 300 > $out/${tag}_pytest_multigpu.log 2>&1
 echo "rc=$?" >> $out/${tag}_pytest_multigpu.log
-[ -s $out/${tag}_traffic.csv ] || timeout 600 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-  --clock-control none --csv --log-file $out/${tag}_traffic.csv python scripts/step_profile.py > $out/${tag}_traffic.log 2>&1
