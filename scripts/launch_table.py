@@ -11,7 +11,9 @@ for r in rows:
         hdr = r
         continue
     if hdr and len(r) == len(hdr):
-        data.append(dict(zip(hdr, r)))
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name", "gpu__time_duration.sum") == "gpu__time_duration.sum":
+            data.append(d)
 scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
 agg = collections.defaultdict(lambda: [0, 0.0])
 tot = 0.0
@@ -23,4 +25,4 @@ for d in data:
     tot += us
 print(f"{len(data)} launches, {tot / 1000:.3f} ms of kernel time")
 for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
-    print(f"{us / 1000:8.3f} ms {us / tot * 100:5.1f}%  n={n:4d}  {k}")
+    print(f"{us:9.1f} us {us / tot * 100:5.1f}%  n={n:4d}  {k}")

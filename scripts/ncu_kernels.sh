@@ -14,11 +14,12 @@ cap() {  # name regex count skip
   ncu -i /tmp/${tag}_$1.ncu-rep --page raw --csv > $out/${tag}_ncu_$1.csv 2>> $out/${tag}_ncu_$1.log
   ncu -i /tmp/${tag}_$1.ncu-rep --page details --csv > $out/${tag}_ncu_$1_details.csv 2>> $out/${tag}_ncu_$1.log
 }
-cap fwd_epi "conv_tc_kernel<\\(tcb::ConvMode\\)0, \\(int\\)256, \\(int\\)1, \\(bool\\)1>" 2
-cap stem "narrow_im2col|conv_tc_kernel<\\(tcb::ConvMode\\)0, \\(int\\)64, \\(int\\)1, \\(bool\\)1>" 2
-cap dgrad_epi "conv_tc_kernel<\\(tcb::ConvMode\\)1, \\(int\\)256, \\(int\\)1, \\(bool\\)1>" 2
-cap wgrad_3x3 "conv_tc_kernel<\\(tcb::ConvMode\\)2, \\(int\\)256, \\(int\\)2, \\(bool\\)0>" 2
-cap wgrad_1x1 "conv_tc_kernel<\\(tcb::ConvMode\\)2, \\(int\\)256, \\(int\\)1, \\(bool\\)0>" 2
-cap fwd_3x3 "conv_tc_kernel<\\(tcb::ConvMode\\)0, \\(int\\)256, \\(int\\)2, \\(bool\\)0>" 2
-cap dgrad_3x3 "conv_tc_kernel<\\(tcb::ConvMode\\)1, \\(int\\)256, \\(int\\)2, \\(bool\\)0>" 2
+cap fwd_epi "conv_tc_kernel<\\(tcb::ConvMode\\)0, \\(int\\)256, \\(int\\)1, \\(int\\)2, \\(bool\\)0>" 2
+cap dgrad_epi "conv_tc_kernel<\\(tcb::ConvMode\\)1, \\(int\\)256, \\(int\\)1, \\(int\\)2, \\(bool\\)0>" 2
+cap fwd_3x3_cta2 "conv_tc_kernel<\\(tcb::ConvMode\\)0, \\(int\\)256, \\(int\\)2, \\(int\\)0, \\(bool\\)1>" 2
+cap dgrad_3x3_cta2 "conv_tc_kernel<\\(tcb::ConvMode\\)1, \\(int\\)128, \\(int\\)2, \\(int\\)0, \\(bool\\)1>" 2
+cap wgrad_3x3_cta2 "conv_tc_kernel<\\(tcb::ConvMode\\)2, \\(int\\)256, \\(int\\)2, \\(int\\)0, \\(bool\\)1>" 2
+cap wgrad_1x1_cta2 "conv_tc_kernel<\\(tcb::ConvMode\\)2, \\(int\\)256, \\(int\\)1, \\(int\\)0, \\(bool\\)1>" 2
+cap stem "narrow_im2col|maxpool" 3
+cap misc "split_reduce|sgd4|dgrad_empty" 4
 du -sh $out
