@@ -498,6 +498,7 @@ def main():
             "cpu_baseline": cpu,
             "phases_ms": {k: round(v, 3) for k, v in phases.items()},
             "loss": loss,
+            "hbm_arena_bytes": layout.get("arena_bytes"),
             "ps": {"param_bytes": param_bytes, "rs_ag_bytes_per_gpu_step": rs_ag_bytes,
                    "busbw": ps_bandwidth(phases, world, param_bytes)},
             "lemmas": lemmas(phases, world, param_bytes, os.path.join(ROOT, "gpurun_out")),
