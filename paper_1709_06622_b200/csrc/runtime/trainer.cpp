@@ -1037,7 +1037,6 @@ TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
     d["param_count"] = t->param_count;
     d["param_padded"] = t->param_padded;
     d["shard"] = t->shard;
-    d["arena_bytes"] = t->arena_bytes;  // HBM the step uses (0 before the first step)
     d["arena_bytes"] = t->arena_bytes;
     json layers = json::array();
     for (size_t i = 0; i < t->nodes.size(); ++i) {
