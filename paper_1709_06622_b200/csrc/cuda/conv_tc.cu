@@ -960,6 +960,8 @@ __global__ void __launch_bounds__(256) narrow_im2col_kernel(const __nv_bfloat16*
                                                             __nv_bfloat16* __restrict__ col,
                                                             ConvGeom g, int cv, int rw, int kc,
                                                             int wp, int ho, int wo) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __nv_bfloat16 sm[];
     const int n = blockIdx.x / ho, oh = blockIdx.x - n * ho;
     const int ih0 = oh * g.stride_h - g.pad_h;
@@ -1004,6 +1006,8 @@ __global__ void __launch_bounds__(256) narrow_im2col_kernel(const __nv_bfloat16*
 __global__ void narrow_pack_weights(const __nv_bfloat16* __restrict__ w,
                                     __nv_bfloat16* __restrict__ wp, ConvGeom g, int cv, int rw,
                                     int kc) {
+    pdl_wait();
+    pdl_trigger();
     const int total = g.k * kc;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int k = i / kc, j = i - k * kc;
@@ -1017,6 +1021,8 @@ __global__ void narrow_pack_weights(const __nv_bfloat16* __restrict__ w,
 // dwp[K][KC] (fp32) -> dw[K][R][S][C], zero on the padded channels
 __global__ void narrow_scatter_grad(const float* __restrict__ dwp, float* __restrict__ dw,
                                     ConvGeom g, int cv, int rw, int kc) {
+    pdl_wait();
+    pdl_trigger();
     const int total = g.k * g.r * g.s * g.c;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int c = i % g.c;
@@ -1030,10 +1036,9 @@ __global__ void narrow_scatter_grad(const float* __restrict__ dwp, float* __rest
 cudaError_t narrow_im2col(const ConvGeom& g, const NarrowPlan& q, const void* x, void* col,
                           cudaStream_t st) {
     const int ho = g.ho(), wo = g.wo();
-    narrow_im2col_kernel<<<g.n * ho, 256, q.smem, st>>>(static_cast<const __nv_bfloat16*>(x),
-                                                        static_cast<__nv_bfloat16*>(col), g, q.cv,
-                                                        q.rw, q.kc, q.wp, ho, wo);
-    return cudaGetLastError();
+    return launch_pdl(narrow_im2col_kernel, dim3(g.n * ho), dim3(256), q.smem, st,
+                      static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(col), g, q.cv,
+                      q.rw, q.kc, q.wp, ho, wo);
 }
 
 // ---------------------------------------------------------------- host ----
@@ -1343,9 +1348,9 @@ cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const E
         cudaError_t e = narrow_im2col(g, q, x, ws, st);
         if (e != cudaSuccess) return e;
         auto* wp = reinterpret_cast<__nv_bfloat16*>(ws + align256(q.col_bytes));
-        narrow_pack_weights<<<std::max(1, std::min(g.k * q.kc / 256 + 1, 1024)), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(w), wp, g, q.cv, q.rw, q.kc);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        e = launch_pdl(narrow_pack_weights, dim3(std::max(1, std::min(g.k * q.kc / 256 + 1, 1024))), dim3(256),
+                       0, st, static_cast<const __nv_bfloat16*>(w), wp, g, q.cv, q.rw, q.kc);
+        if (e != cudaSuccess) return e;
         p.s = make_shape(q.g1, ConvMode::Fwd);
         a_matrix = ws;
         b_matrix = wp;
@@ -1417,9 +1422,8 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
         if ((e = conv_tc_wgrad(q.g1, dy, ws, dwp, rest, st, false, counters)) != cudaSuccess)
             return e;
         const int total = g.k * g.r * g.s * g.c;
-        narrow_scatter_grad<<<std::max(1, std::min(total / 256 + 1, 1024)), 256, 0, st>>>(
-            dwp, dw, g, q.cv, q.rw, q.kc);
-        return cudaGetLastError();
+        return launch_pdl(narrow_scatter_grad, dim3(std::max(1, std::min(total / 256 + 1, 1024))), dim3(256), 0,
+                          st, static_cast<const float*>(dwp), dw, g, q.cv, q.rw, q.kc);
     }
     Params p{};
     p.s = make_shape(g, ConvMode::Wgrad);

@@ -222,6 +222,8 @@ template <typename CT>
 __global__ void sgd4_kernel(float4* __restrict__ w, const float4* __restrict__ g,
                             float4* __restrict__ v, CT* __restrict__ wc, size_t n4, float lr,
                             float mom, float wd, float gscale) {
+    pdl_wait();
+    pdl_trigger();
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
          i += size_t(gridDim.x) * blockDim.x) {
         float4 wi = w[i], gi = g[i], vi = v[i];
@@ -350,6 +352,8 @@ __global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __re
 template <typename T>
 __global__ void avgpool_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, int N, int HW,
                                    int C) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N * C) return;
     const int n = i / C, c = i % C;
@@ -376,6 +380,8 @@ __global__ void avgpool_bwd_kernel(const T* __restrict__ dy, T* __restrict__ dx,
 __global__ void avgpool_bwd_vec_kernel(const __nv_bfloat16* __restrict__ dy,
                                        __nv_bfloat16* __restrict__ dx, int total8, int HW, int cg,
                                        const __nv_bfloat16* __restrict__ mask) {
+    pdl_wait();
+    pdl_trigger();
     const float inv = 1.f / float(HW);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total8; i += gridDim.x * blockDim.x) {
         const int ci = i % cg, n = i / (HW * cg);
@@ -401,6 +407,8 @@ template <typename T>
 __global__ void softmax_xent_kernel(const T* __restrict__ logits, const int32_t* __restrict__ lab,
                                     T* __restrict__ dl, float* __restrict__ row_loss, int N,
                                     int K, int ld) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float red[32];
     const int n = blockIdx.x;
     const T* z = logits + size_t(n) * ld;
@@ -556,9 +564,10 @@ cudaError_t sgd_momentum(float* w, const float* g, float* v, DType cdt, void* wc
                      reinterpret_cast<uintptr_t>(v) % 16 == 0;
     TCB_DT_SWITCH(cdt, CT, {
         if (vec)
-            sgd4_kernel<CT><<<grid_for(n / 4, 2), kBlock, 0, st>>>(
-                reinterpret_cast<float4*>(w), reinterpret_cast<const float4*>(g),
-                reinterpret_cast<float4*>(v), static_cast<CT*>(wc), n / 4, lr, mom, wd, gscale);
+            return launch_pdl(sgd4_kernel<CT>, dim3(grid_for(n / 4, 2)), dim3(kBlock), 0, st,
+                              reinterpret_cast<float4*>(w), reinterpret_cast<const float4*>(g),
+                              reinterpret_cast<float4*>(v), static_cast<CT*>(wc), n / 4, lr, mom, wd,
+                              gscale);
         else
             sgd_kernel<CT><<<grid_for(n, 4), kBlock, 0, st>>>(w, g, v, static_cast<CT*>(wc), n, lr,
                                                               mom, wd, gscale);
@@ -709,6 +718,8 @@ __global__ void __launch_bounds__(256) maxpool_bwd_vec_kernel(
 __global__ void __launch_bounds__(256) maxpool_fwd_bf16x8_kernel(
     const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ arg,
     int H, int W, int C, int F, int S, int P, int Ho, int Wo) {
+    pdl_wait();
+    pdl_trigger();
     const int cg = C / 8;
     const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
     const int h0 = ho * S - P;
@@ -838,6 +849,8 @@ __global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1_bf16_kernel(
     const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
     __nv_bfloat16* __restrict__ dx, const __nv_bfloat16* __restrict__ ymask, int H, int W, int C,
     int Ho, int Wo) {
+    pdl_wait();
+    pdl_trigger();
     const int cg = C / 8;
     const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
     const size_t nbase = size_t(n) * Ho * Wo * C;
@@ -911,10 +924,9 @@ cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, i
     const size_t total = size_t(n) * ho * wo * c;
     if (dt == DType::BF16 && c % 8 == 0 && aligned16(x) && aligned16(y) &&
         (!arg || (reinterpret_cast<uintptr_t>(arg) % 8) == 0) && size_t(h) * w * c < (size_t(1) << 31)) {
-        maxpool_fwd_bf16x8_kernel<<<n * ho, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
-                                                         static_cast<__nv_bfloat16*>(y), arg, h, w, c,
-                                                         f, s, p, ho, wo);
-        return cudaGetLastError();
+        return launch_pdl(maxpool_fwd_bf16x8_kernel, dim3(n * ho), dim3(256), 0, st,
+                          static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), arg, h, w,
+                          c, f, s, p, ho, wo);
     }
     TCB_DT_SWITCH(dt, T, {
         constexpr int V = 16 / sizeof(T);
@@ -936,10 +948,9 @@ cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, 
     if (dt == DType::BF16 && c % 8 == 0 && aligned16(dy) && aligned16(dx) &&
         (!ymask || aligned16(ymask)) && (reinterpret_cast<uintptr_t>(arg) % 8) == 0 &&
         size_t(ho) * wo * c < (size_t(1) << 31) && f == 3 && s == 2 && p == 1) {
-        maxpool_bwd_k3s2p1_bf16_kernel<<<n * ho, 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(dy), arg, static_cast<__nv_bfloat16*>(dx),
-            static_cast<const __nv_bfloat16*>(ymask), h, w, c, ho, wo);
-        return cudaGetLastError();
+        return launch_pdl(maxpool_bwd_k3s2p1_bf16_kernel, dim3(n * ho), dim3(256), 0, st,
+                          static_cast<const __nv_bfloat16*>(dy), arg, static_cast<__nv_bfloat16*>(dx),
+                          static_cast<const __nv_bfloat16*>(ymask), h, w, c, ho, wo);
     }
     if (dt == DType::BF16 && c % 8 == 0 && aligned16(dy) && aligned16(dx) &&
         (!ymask || aligned16(ymask)) && (reinterpret_cast<uintptr_t>(arg) % 8) == 0 &&
@@ -967,9 +978,10 @@ cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, 
 
 cudaError_t avgpool_global_fwd(DType dt, const void* x, void* y, int n, int hw, int c,
                                cudaStream_t st) {
-    TCB_DT_SWITCH(dt, T, (avgpool_fwd_kernel<T><<<(n * c + kBlock - 1) / kBlock, kBlock, 0, st>>>(
-                              static_cast<const T*>(x), static_cast<T*>(y), n, hw, c)));
-    return cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    TCB_DT_SWITCH(dt, T, (e = launch_pdl(avgpool_fwd_kernel<T>, dim3((n * c + kBlock - 1) / kBlock), dim3(kBlock),
+                                        0, st, static_cast<const T*>(x), static_cast<T*>(y), n, hw, c)));
+    return e;
 }
 
 cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw, int c,
@@ -977,10 +989,9 @@ cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw
     const size_t total = size_t(n) * hw * c;
     if (dt == DType::BF16 && c % 8 == 0 && total / 8 < (size_t(1) << 31) && aligned16(dy) &&
         aligned16(dx) && (!mask || aligned16(mask))) {
-        avgpool_bwd_vec_kernel<<<grid_for(total / 8, 2), kBlock, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx),
-            static_cast<int>(total / 8), hw, c / 8, static_cast<const __nv_bfloat16*>(mask));
-        return cudaGetLastError();
+        return launch_pdl(avgpool_bwd_vec_kernel, dim3(grid_for(total / 8, 2)), dim3(kBlock), 0, st,
+                          static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx),
+                          static_cast<int>(total / 8), hw, c / 8, static_cast<const __nv_bfloat16*>(mask));
     }
     TCB_DT_SWITCH(dt, T, (avgpool_bwd_kernel<T><<<grid_for(total, 2), kBlock, 0, st>>>(
                               static_cast<const T*>(dy), static_cast<T*>(dx), n, hw, c,
@@ -990,9 +1001,11 @@ cudaError_t avgpool_global_bwd(DType dt, const void* dy, void* dx, int n, int hw
 
 cudaError_t softmax_xent(DType dt, const void* logits, const int32_t* labels, void* dlogits,
                          float* loss, int n, int classes, int ld, cudaStream_t st) {
-    TCB_DT_SWITCH(dt, T, (softmax_xent_kernel<T><<<n, kBlock, 0, st>>>(
-                              static_cast<const T*>(logits), labels, static_cast<T*>(dlogits),
-                              loss + 1, n, classes, ld)));
+    cudaError_t e = cudaSuccess;
+    TCB_DT_SWITCH(dt, T, (e = launch_pdl(softmax_xent_kernel<T>, dim3(n), dim3(kBlock), 0, st,
+                                        static_cast<const T*>(logits), labels, static_cast<T*>(dlogits),
+                                        loss + 1, n, classes, ld)));
+    if (e != cudaSuccess) return e;
     mean_kernel<<<1, 32, 0, st>>>(loss, loss + 1, n);
     return cudaGetLastError();
 }
