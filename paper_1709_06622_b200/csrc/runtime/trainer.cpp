@@ -131,6 +131,12 @@ struct tcb_trainer {
     cudaEvent_t ev_comm_done = nullptr, ev_bwd_start = nullptr;
     std::map<int, std::vector<int>> shard_trigger;  // node index -> shards it completes
     bool fused_split_reduce = false;  // config "fused_split_reduce" / $TCB_FUSED_SPLIT_REDUCE
+    // CUDA graph of the step (config "cuda_graph", $TCB_GRAPH)
+    bool use_graph = true;
+    int eager_steps = 0, graph_launches = 0;
+    cudaGraphExec_t graph_exec = nullptr;
+    cudaStream_t graph_stream = nullptr;
+    cudaEvent_t graph_in = nullptr, graph_out = nullptr;
     int pack_njobs = 0, pack_blocks = 0;
     bool pack_jobs_ready = false;
 
@@ -187,6 +193,10 @@ int build_graph(tcb_trainer* t) {
     t->classes = cfg.at("classes").get<int>();
     t->seed = cfg.value("seed", uint64_t(20260810));
     t->overlap = t->cfg.value("overlap_comm", false);
+    {
+        const char* e = std::getenv("TCB_GRAPH");
+        t->use_graph = t->cfg.value("cuda_graph", !(e && e[0] == '0'));
+    }
     t->comm_bg_ctas = t->cfg.value("overlap_ctas", 8);
     {
         const char* e = std::getenv("TCB_FUSED_SPLIT_REDUCE");
@@ -801,6 +811,13 @@ TCB_API int tcb_trainer_create(const char* config_json, tcb_trainer** out) {
 
 TCB_API int tcb_trainer_destroy(tcb_trainer* t) {
     if (!t) return TCB_OK;
+    if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
+    if (t->graph_stream) {
+        cudaStreamSynchronize(t->graph_stream);
+        cudaStreamDestroy(t->graph_stream);
+        cudaEventDestroy(t->graph_in);
+        cudaEventDestroy(t->graph_out);
+    }
     if (t->comm_stream) {
         cudaStreamSynchronize(t->comm_stream);
         for (cudaEvent_t e : t->ev_ready) cudaEventDestroy(e);
@@ -938,12 +955,62 @@ static int consume_staged(tcb_trainer* t, cudaStream_t st) {
     return TCB_OK;
 }
 
+// The step's launches (everything after the staged-input conversion) are
+// recorded once into a CUDA graph and replayed: every kernel argument, tensor
+// map and NCCL buffer is fixed for the trainer's lifetime. Timed steps (phase
+// or layer events) run eagerly; $TCB_GRAPH=0 / config "cuda_graph": false
+// disables the graph.
+static int step_body(tcb_trainer* t, cudaStream_t st) {
+    TRY(forward(t, st));
+    TRY(backward(t, st));
+    return aggregate_and_update(t, st, nullptr, nullptr);
+}
+
+static int graph_step(tcb_trainer* t, cudaStream_t st) {
+    // captured and replayed on the trainer's own stream (the caller's may be the
+    // legacy default stream, which cannot be captured), fenced by events
+    if (!t->graph_stream) {
+        TRY_CUDA(cudaStreamCreateWithFlags(&t->graph_stream, cudaStreamNonBlocking));
+        TRY_CUDA(cudaEventCreateWithFlags(&t->graph_in, cudaEventDisableTiming));
+        TRY_CUDA(cudaEventCreateWithFlags(&t->graph_out, cudaEventDisableTiming));
+    }
+    cudaStream_t gs = t->graph_stream;
+    if (!t->graph_exec) {
+        cudaGraph_t g = nullptr;
+        TRY_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+        const int rc = step_body(t, gs);
+        const cudaError_t ce = cudaStreamEndCapture(gs, &g);
+        if (rc != TCB_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        TRY_CUDA(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&t->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        TRY_CUDA(ie);
+        t->graph_launches = t->launches;
+    }
+    t->launches = t->graph_launches;
+    TRY_CUDA(cudaEventRecord(t->graph_in, st));
+    TRY_CUDA(cudaStreamWaitEvent(gs, t->graph_in, 0));
+    TRY_CUDA(cudaGraphLaunch(t->graph_exec, gs));
+    TRY_CUDA(cudaEventRecord(t->graph_out, gs));
+    return check_cuda(cudaStreamWaitEvent(st, t->graph_out, 0), "graph fence");
+}
+
 TCB_API int tcb_trainer_step(tcb_trainer* t, void* stream) {
     if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
     auto st = static_cast<cudaStream_t>(stream);
     TRY(ensure_ready(t, st));
     t->launches = 0;
     TRY(consume_staged(t, st));
+    const int staged_launches = t->launches;
+    // eager warm-up steps first (one-time kernel attribute setup stays out of the capture)
+    if (t->use_graph && !t->timing && !t->layer_timing && ++t->eager_steps > 2) {
+        TRY(graph_step(t, st));
+        t->launches += staged_launches;
+        return TCB_OK;
+    }
     cudaEvent_t* e = t->ph.e;
     if (t->timing) TRY_CUDA(cudaEventRecord(e[0], st));
     TRY(forward(t, st));

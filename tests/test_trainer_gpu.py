@@ -204,6 +204,22 @@ def test_staged_u8_batches_pipeline(oracle):
         assert torch.equal(a.tensor("param"), b.tensor("param")), i
 
 
+def test_cuda_graph_replay_matches_eager_steps():
+    """After two eager warm-up steps the trainer replays a captured CUDA graph
+    of the step; parameters and momentum must match eager execution bitwise."""
+    from paper_1709_06622_b200.trainer import Trainer
+    cfg = _models().tiny_resnet(batch=4, precision="bf16")
+    eager = dict(cfg, cuda_graph=False)
+    a, b = Trainer(cfg), Trainer(eager)
+    for _ in range(6):
+        a.step()
+        b.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.tensor("param"), b.tensor("param"))
+    assert torch.equal(a.tensor("grad"), b.tensor("grad"))
+    assert a.launch_count() == b.launch_count()
+
+
 def test_loss_decreases_over_steps():
     from paper_1709_06622_b200.trainer import Trainer
     cfg = _models().tiny_resnet(batch=8, precision="bf16", lr=0.05)
