@@ -370,7 +370,7 @@ void plan_params(tcb_trainer* t) {
             if (nd.op != Op::Conv) continue;
             last_conv = i;
             const size_t lo = nd.woff, hi = (nd.bias ? nd.boff + nd.g.k : nd.woff + nd.wcount);
-            for (size_t sh = lo / t->shard; sh < t->world && sh * t->shard < hi; ++sh)
+            for (size_t sh = lo / t->shard; sh < static_cast<size_t>(t->world) && sh * t->shard < hi; ++sh)
                 if (first_node[sh] < 0) first_node[sh] = i;
         }
         for (int sh = t->world - 1; sh >= 0; --sh)
