@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--batch", type=int, default=256, help="images per GPU")
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "ffma"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "ffma"])
     ap.add_argument("--n-ps", type=int, default=0, help="PS shards (0 = one per GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
@@ -156,7 +156,8 @@ def conv_roofline(cfg, pk, reps=5):
     per_layer = []
     launches = 0
     for name, g in models.conv_layers(cfg):
-        c = g["c"] if not bf else -(-g["c"] // 8) * 8
+        cp = 8 if bf else 4 if cfg["precision"] == "tf32" else 1
+        c = -(-g["c"] // cp) * cp
         geo = device.geom(g["n"], g["h"], g["w"], c, g["k"], g["r"], g["s"], pad=g["pad_h"],
                           stride=g["stride_h"], pad_w=g["pad_w"], stride_w=g["stride_w"])
         plan = device.ConvPlan(geo, "gemm", cfg["precision"])
@@ -187,7 +188,8 @@ def conv_roofline(cfg, pk, reps=5):
         per_layer.append(row)
         del plan, x, w, dy
     achieved = total_flop / total_ms / 1e9
-    peak = pk["bf16_tflops"] if bf else pk.get("fp32_tflops", 75.0)
+    peak = {"bf16": pk["bf16_tflops"], "tf32": pk["bf16_tflops"] / 2}.get(cfg["precision"],
+                                                                          pk.get("fp32_tflops", 75.0))
     return {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": None,
             "kernel": "conv_tc_kernel (tcgen05 implicit GEMM, fwd+dgrad+wgrad of every conv)",
@@ -267,8 +269,9 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
         flop += r["flop"] * len(passes)
         ms += sum(passes)
     achieved = flop / ms / 1e9
-    bf = precision == "bf16"
-    peak = pk["bf16_tflops_sustained"] if bf and "bf16_tflops_sustained" in pk else pk.get("bf16_tflops", 1590.0)
+    peak = pk["bf16_tflops_sustained"] if "bf16_tflops_sustained" in pk else pk.get("bf16_tflops", 1590.0)
+    if precision == "tf32":  # dense tf32 tensor peak = half the bf16 one (1.1 vs 2.25 PF nominal)
+        peak = peak / 2
     # per-pass roofline time max(FLOP / tensor peak, bytes / HBM peak), summed
     hbm = pk.get("hbm_gbs", 6548.2)
     bound_ms, tensor_ms, hbm_ms, nbytes = 0.0, 0.0, 0.0, 0.0
@@ -295,7 +298,7 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
             "traffic_source": tsrc,
             "kernel": "conv_tc_kernel (tcgen05/TMEM implicit GEMM, TMA im2col; all conv passes of one step)",
             "flop_per_step": flop, "conv_ms_per_step": round(ms, 3),
-            "frac_of_burst_peak": round(achieved / pk.get("bf16_tflops", 1590.0), 4),
+            "frac_of_burst_peak": round(achieved / (pk.get("bf16_tflops", 1590.0) / (2 if precision == "tf32" else 1)), 4),
             "algorithmic_bytes_per_step": nbytes,
             "combined_roofline": {
                 "bound_ms": round(bound_ms, 3), "tensor_only_ms": round(tensor_ms, 3),
@@ -483,7 +486,7 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "bf16" if args.precision == "bf16" else "f32",
+            "dtype": {"bf16": "bf16", "tf32": "tf32"}.get(args.precision, "f32"),
             "data": "synthetic (counter-based RNG images/labels, random-init weights)",
             "config": {"workload": f"{args.model}_synthetic_224" if args.model == "resnet50" else args.model,
                        "per_gpu_batch": args.batch, "global_batch": args.batch * world,

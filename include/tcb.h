@@ -20,7 +20,10 @@
  *   - handles are not thread-safe: one host thread per GPU.
  *   - tensors are NHWC; conv weights are KRSC ([out][fh][fw][in]).
  *   - dtype of activations/weights follows the plan precision:
- *       TCB_PREC_FFMA_FP32 -> float,  TCB_PREC_BF16 -> bf16 (uint16_t bits).
+ *       TCB_PREC_FFMA_FP32 -> float (SIMT FFMA),
+ *       TCB_PREC_TF32      -> float (tcgen05 kind::tf32 GEMM convs; C, K % 4 == 0;
+ *                             Winograd / FFT have no TF32 plan: UNSUPPORTED),
+ *       TCB_PREC_BF16      -> bf16 (uint16_t bits).
  *     Weight gradients are always fp32 (they land in the PS flat buffer).
  */
 #ifndef TCB_H_

@@ -337,6 +337,20 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_byte
     return d;
 }
 
+// MN-major tf32 operands: SWIZZLE_128B_BASE32B (layout type 1) — 128-byte
+// rows, 32-byte granules XOR-ed with (row & 3), 4-row K groups SBO apart,
+// 32-element MN blocks LBO apart. (Plain SWIZZLE_128B is K-major-only for tf32.)
+__device__ __forceinline__ uint64_t sw128b32_desc(uint32_t saddr, uint32_t lbo_bytes,
+                                                  uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(1) << 61;  // SWIZZLE_128B_BASE32B
+    return d;
+}
+
 // No-swizzle ("interleaved") descriptor: 8-row x 16-byte core matrices,
 // K-direction core matrices LBO apart, 8-row groups SBO apart.
 __device__ __forceinline__ uint64_t interleave_desc(uint32_t saddr, uint32_t lbo_bytes,

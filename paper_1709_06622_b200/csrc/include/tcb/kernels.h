@@ -79,6 +79,17 @@ cudaError_t conv_ffma_dgrad(const ConvGeom& g, const float* dy, const float* w,
 cudaError_t conv_ffma_wgrad(const ConvGeom& g, const float* dy, const float* x, float* dw,
                             void* workspace, cudaStream_t st);
 
+// ---- TF32 tensor-core implicit GEMM (tcgen05 kind::tf32; fp32 storage) ----
+// Requirements: C % 4 == 0 and K % 4 == 0 (16-byte fp32 chunks).
+bool conv_tf32_supported(const ConvGeom& g);
+size_t conv_tf32_workspace(const ConvGeom& g, ConvMode mode);
+cudaError_t conv_tf32_fwd(const ConvGeom& g, const float* x, const float* w, const Epilogue& ep,
+                          float* y, cudaStream_t st);
+cudaError_t conv_tf32_dgrad(const ConvGeom& g, const float* dy, const float* w,
+                            const Epilogue& ep, float* dx, cudaStream_t st);
+cudaError_t conv_tf32_wgrad(const ConvGeom& g, const float* dy, const float* x, float* dw,
+                            void* workspace, cudaStream_t st);
+
 // ---- Winograd F(2x2,3x3) (3x3, stride 1) ----
 size_t winograd_workspace(const ConvGeom& g, ConvMode mode, DType dt);
 bool winograd_supported(const ConvGeom& g);

@@ -54,8 +54,9 @@ ConvPlanLayout conv_plan_layout(const ConvGeom& g, int algo, int prec) {
     const size_t P = size_t(g.n) * g.ho() * g.wo();
     const DType dt = prec == TCB_PREC_BF16 ? DType::BF16 : DType::F32;
     if (algo == TCB_ALGO_GEMM) {
-        L.wgrad = prec == TCB_PREC_BF16 ? conv_tc_workspace(g, ConvMode::Wgrad)
-                                        : conv_ffma_workspace(g, ConvMode::Wgrad);
+        L.wgrad = prec == TCB_PREC_BF16   ? conv_tc_workspace(g, ConvMode::Wgrad)
+                  : prec == TCB_PREC_TF32 ? conv_tf32_workspace(g, ConvMode::Wgrad)
+                                          : conv_ffma_workspace(g, ConvMode::Wgrad);
         L.wT = prec == TCB_PREC_BF16 ? size_t(g.k) * g.r * g.s * g.c * 2 : 0;
     } else if (algo == TCB_ALGO_WINOGRAD) {
         L.wgrad = std::max({winograd_workspace(g, ConvMode::Fwd, dt),
@@ -76,9 +77,10 @@ ConvPlanLayout conv_plan_layout(const ConvGeom& g, int algo, int prec) {
 
 bool algo_applies(const ConvGeom& g, int algo, int prec) {
     if (algo == TCB_ALGO_GEMM)
-        return prec == TCB_PREC_FFMA_FP32 ||
+        return prec == TCB_PREC_FFMA_FP32 || (prec == TCB_PREC_TF32 && conv_tf32_supported(g)) ||
                (prec == TCB_PREC_BF16 && conv_tc_supported(g, ConvMode::Fwd) &&
                 conv_tc_supported(g, ConvMode::Wgrad) && conv_tc_supported(g, ConvMode::Dgrad));
+    // Winograd / FFT run fp32 SIMT transforms: no tensor-core (TF32) variant
     if (prec == TCB_PREC_TF32) return false;
     if (algo == TCB_ALGO_WINOGRAD) return winograd_supported(g);
     if (algo == TCB_ALGO_FFT) return fft_supported(g);
@@ -167,8 +169,10 @@ TCB_API int tcb_conv_fwd(const tcb_conv_plan* plan, const void* x, const void* w
     cudaError_t e;
     switch (plan->algo) {
         case TCB_ALGO_GEMM:
-            e = plan->prec == TCB_PREC_BF16
-                    ? conv_tc_fwd(plan->g, x, w, ep, y, st)
+            e = plan->prec == TCB_PREC_BF16 ? conv_tc_fwd(plan->g, x, w, ep, y, st)
+                : plan->prec == TCB_PREC_TF32
+                    ? conv_tf32_fwd(plan->g, static_cast<const float*>(x),
+                                    static_cast<const float*>(w), ep, static_cast<float*>(y), st)
                     : conv_ffma_fwd(plan->g, static_cast<const float*>(x),
                                     static_cast<const float*>(w), ep, static_cast<float*>(y), st);
             break;
@@ -199,6 +203,9 @@ TCB_API int tcb_conv_dgrad(const tcb_conv_plan* plan, const void* dy, const void
                     e = pack_dgrad_weights(DType::BF16, w, wT, plan->g, st);
                 }
                 if (e == cudaSuccess) e = conv_tc_dgrad(plan->g, dy, w, wT, ep, dx, st);
+            } else if (plan->prec == TCB_PREC_TF32) {
+                e = conv_tf32_dgrad(plan->g, static_cast<const float*>(dy),
+                                    static_cast<const float*>(w), ep, static_cast<float*>(dx), st);
             } else {
                 e = conv_ffma_dgrad(plan->g, static_cast<const float*>(dy),
                                     static_cast<const float*>(w), ep, static_cast<float*>(dx), st);
@@ -223,6 +230,9 @@ TCB_API int tcb_conv_wgrad(const tcb_conv_plan* plan, const void* dy, const void
                                     workspace ? reinterpret_cast<int*>(static_cast<char*>(workspace) +
                                                                        plan->layout.off_counters)
                                               : nullptr)
+                : plan->prec == TCB_PREC_TF32
+                    ? conv_tf32_wgrad(plan->g, static_cast<const float*>(dy),
+                                      static_cast<const float*>(x), dw, workspace, st)
                     : conv_ffma_wgrad(plan->g, static_cast<const float*>(dy),
                                       static_cast<const float*>(x), dw, workspace, st);
             break;

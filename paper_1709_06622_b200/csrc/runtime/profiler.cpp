@@ -85,6 +85,9 @@ Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int rep
     auto* wTp = static_cast<char*>(ws.p) + L.off_wT;
     Epilogue none;
     auto run_fwd = [&]() -> cudaError_t {
+        if (algo == TCB_ALGO_GEMM && prec == TCB_PREC_TF32)
+            return conv_tf32_fwd(g, static_cast<float*>(x.p), static_cast<float*>(w.p), none,
+                                 static_cast<float*>(y.p), st);
         if (algo == TCB_ALGO_GEMM)
             return dt == DType::BF16 ? conv_tc_fwd(g, x.p, w.p, none, y.p, st)
                                      : conv_ffma_fwd(g, static_cast<float*>(x.p), static_cast<float*>(w.p),
@@ -100,6 +103,9 @@ Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int rep
                                                             : cudaSuccess;
                 return e != cudaSuccess ? e : conv_tc_dgrad(g, dy.p, w.p, wTp, none, dx.p, st);
             }
+            if (prec == TCB_PREC_TF32)
+                return conv_tf32_dgrad(g, static_cast<float*>(dy.p), static_cast<float*>(w.p), none,
+                                       static_cast<float*>(dx.p), st);
             return conv_ffma_dgrad(g, static_cast<float*>(dy.p), static_cast<float*>(w.p), none,
                                    static_cast<float*>(dx.p), st);
         }
@@ -107,6 +113,9 @@ Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int rep
         return fft_dgrad(g, dt, dy.p, w.p, none, dx.p, ws.p, st);
     };
     auto run_wgrad = [&]() -> cudaError_t {
+        if (algo == TCB_ALGO_GEMM && prec == TCB_PREC_TF32)
+            return conv_tf32_wgrad(g, static_cast<float*>(dy.p), static_cast<float*>(x.p),
+                                   static_cast<float*>(dw.p), ws.p, st);
         if (algo == TCB_ALGO_GEMM)
             return dt == DType::BF16 ? conv_tc_wgrad(g, dy.p, x.p, static_cast<float*>(dw.p), ws.p, st,
                                                      false,
@@ -168,14 +177,17 @@ using namespace tcb;
 // Request JSON:
 //   {"layers": [{"h","w","c","k","r","s","pad_h","pad_w","stride_h","stride_w"}, ...],
 //    "batches": [32, 64, ...], "algorithms": ["gemm", "winograd", "fft"],
-//    "precision": "bf16"|"ffma", "reps": 5}
+//    "precision": "bf16"|"tf32"|"ffma", "reps": 5}
 // Reply JSON: {"csv": <catalog CSV>, "rows": [per-measurement detail], "skipped": [...]}.
 TCB_API int tcb_profile_catalog(const char* request_json, char** reply_out) {
     if (!request_json || !reply_out) return fail(TCB_ERR_INVALID, "NULL argument");
     try {
         const json req = json::parse(request_json);
-        const bool bf16 = req.value("precision", std::string("bf16")) == "bf16";
-        const int prec = bf16 ? TCB_PREC_BF16 : TCB_PREC_FFMA_FP32;
+        const std::string pname = req.value("precision", std::string("bf16"));
+        const bool bf16 = pname == "bf16";
+        const int prec = bf16 ? TCB_PREC_BF16 : pname == "tf32" ? TCB_PREC_TF32 : TCB_PREC_FFMA_FP32;
+        // tensor-core layouts pad channels: 16-byte chunks = 8 bf16 / 4 fp32
+        const int cpad = bf16 ? 8 : prec == TCB_PREC_TF32 ? 4 : 1;
         const int reps = std::max(1, req.value("reps", 5));
         std::vector<traincap::CostEntry> rows;
         json detail = json::array(), skipped = json::array();
@@ -189,8 +201,8 @@ TCB_API int tcb_profile_catalog(const char* request_json, char** reply_out) {
                 ConvGeom g{n,
                            L.at("h").get<int>(),
                            L.at("w").get<int>(),
-                           bf16 ? (c_log + 7) / 8 * 8 : c_log,
-                           bf16 ? (L.at("k").get<int>() + 7) / 8 * 8 : L.at("k").get<int>(),
+                           (c_log + cpad - 1) / cpad * cpad,
+                           (L.at("k").get<int>() + cpad - 1) / cpad * cpad,
                            L.at("r").get<int>(),
                            L.value("s", L.at("r").get<int>()),
                            L.value("pad_h", 0),

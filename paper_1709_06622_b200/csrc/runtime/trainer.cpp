@@ -90,6 +90,8 @@ struct tcb_trainer {
     json cfg;
     DType dt = DType::BF16;
     bool bf16 = true;
+    bool tf32 = false;  // fp32 storage, GEMM convs on tcgen05 kind::tf32
+    int cpad = 8;       // channel padding of the tensor-core layouts (16-byte rows)
     int batch = 0, classes = 0;
     uint64_t seed = 20260810;
     float lr = 0.01f, momentum = 0.9f, weight_decay = 0.f;
@@ -187,7 +189,12 @@ namespace {
 // --------------------------------------------------------------- build ----
 int build_graph(tcb_trainer* t) {
     const json& cfg = t->cfg;
-    t->bf16 = cfg.value("precision", std::string("bf16")) == "bf16";
+    const std::string prec = cfg.value("precision", std::string("bf16"));
+    if (prec != "bf16" && prec != "tf32" && prec != "ffma")
+        throw std::runtime_error("precision must be bf16, tf32 or ffma, got " + prec);
+    t->bf16 = prec == "bf16";
+    t->tf32 = prec == "tf32";
+    t->cpad = t->bf16 ? 8 : t->tf32 ? 4 : 1;
     t->dt = t->bf16 ? DType::BF16 : DType::F32;
     t->batch = cfg.at("batch").get<int>();
     t->classes = cfg.at("classes").get<int>();
@@ -226,16 +233,17 @@ int build_graph(tcb_trainer* t) {
             nd.h = L.at("h").get<int>();
             nd.w = L.at("w").get<int>();
             nd.c_logical = L.at("c").get<int>();
-            nd.c = t->bf16 ? static_cast<int>(round_up(nd.c_logical, 8)) : nd.c_logical;
+            nd.c = static_cast<int>(round_up(nd.c_logical, t->cpad));
         } else if (op == "conv") {
             nd.op = Op::Conv;
             nd.in = src("in");
             nd.residual = src("residual");
             const Node& x = t->nodes.at(nd.in);
-            // bf16 tensor-core path: output channels padded to a multiple of 8 (16-byte
-            // NHWC rows); padded filters are zero, so padded channels stay exactly 0.
+            // tensor-core paths: output channels padded to a multiple of 8 (bf16) / 4
+            // (tf32) — 16-byte NHWC rows; padded filters are zero, so padded channels
+            // stay exactly 0.
             const int k_logical = L.at("k").get<int>();
-            const int k_alloc = t->bf16 ? static_cast<int>(round_up(k_logical, 8)) : k_logical;
+            const int k_alloc = static_cast<int>(round_up(k_logical, t->cpad));
             nd.g = ConvGeom{x.n, x.h, x.w, x.c, k_alloc, L.at("r").get<int>(),
                             L.value("s", L.at("r").get<int>()), L.value("pad_h", L.value("pad", 0)),
                             L.value("pad_w", L.value("pad", 0)), L.value("stride_h", L.value("stride", 1)),
@@ -265,7 +273,11 @@ int build_graph(tcb_trainer* t) {
                          : nd.algo == "winograd" ? TCB_ALGO_WINOGRAD
                          : nd.algo == "fft" ? TCB_ALGO_FFT : -1;
             if (nd.algo_id < 0) throw std::runtime_error("layer " + nd.name + ": unknown algo " + nd.algo);
-            if (!algo_applies(nd.g, nd.algo_id, t->bf16 ? TCB_PREC_BF16 : TCB_PREC_FFMA_FP32))
+            // tf32 mode: GEMM layers on tensor cores; Winograd / FFT layers run their fp32 kernels
+            const int lprec = t->bf16 ? TCB_PREC_BF16
+                              : (t->tf32 && nd.algo_id == TCB_ALGO_GEMM) ? TCB_PREC_TF32
+                                                                         : TCB_PREC_FFMA_FP32;
+            if (!algo_applies(nd.g, nd.algo_id, lprec))
                 throw std::runtime_error("layer " + nd.name + ": algorithm " + nd.algo +
                                          " does not apply to this geometry");
             if (nd.residual >= 0) {
@@ -400,8 +412,9 @@ int allocate(tcb_trainer* t) {
                     nd.nws = b.take(std::max(conv_tc_workspace(nd.g, ConvMode::Wgrad),
                                              conv_tc_workspace(nd.g, ConvMode::Fwd)));
                 else
-                    ws = std::max(ws, t->bf16 ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
-                                              : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
+                    ws = std::max(ws, t->bf16   ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
+                                      : t->tf32 ? conv_tf32_workspace(nd.g, ConvMode::Wgrad)
+                                                : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
                 nd.pack_wT = t->bf16 && nd.need_dgrad && conv_tc_dgrad_needs_pack(nd.g);
                 if (nd.pack_wT) nd.wT = b.take(nd.wcount * 2);
             } else {
@@ -535,6 +548,9 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                 else if (t->bf16)
                     TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
                                          ep, t->at(nd.act), st, nd.narrow ? t->at(nd.nws) : nullptr));
+                else if (t->tf32)
+                    TRY_CUDA(conv_tf32_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
+                                           ep, t->at<float>(nd.act), st));
                 else
                     TRY_CUDA(conv_ffma_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
                                            ep, t->at<float>(nd.act), st));
@@ -606,6 +622,9 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         else if (t->bf16)
             TRY_CUDA(conv_tc_dgrad(con.g, t->at(con.grad), cw, con.pack_wT ? t->at(con.wT) : nullptr, ep,
                                    out, st));
+        else if (t->tf32)
+            TRY_CUDA(conv_tf32_dgrad(con.g, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
+                                     ep, static_cast<float*>(out), st));
         else
             TRY_CUDA(conv_ffma_dgrad(con.g, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
                                      ep, static_cast<float*>(out), st));
@@ -687,6 +706,9 @@ int backward(tcb_trainer* t, cudaStream_t st) {
                 TRY_CUDA(conv_tc_wgrad(nd.g, t->at(nd.grad), t->at(x.act), grad + nd.woff,
                                        t->at(nd.narrow ? nd.nws : t->off_ws), st, nd.narrow,
                                        t->fused_split_reduce ? t->at<int>(t->off_counters) : nullptr));
+            else if (t->tf32)
+                TRY_CUDA(conv_tf32_wgrad(nd.g, t->at<float>(nd.grad), t->at<float>(x.act), grad + nd.woff,
+                                         t->at(t->off_ws), st));
             else
                 TRY_CUDA(conv_ffma_wgrad(nd.g, t->at<float>(nd.grad), t->at<float>(x.act), grad + nd.woff,
                                          t->at(t->off_ws), st));
@@ -1096,7 +1118,7 @@ TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
     if (!t || !json_out) return fail(TCB_ERR_INVALID, "NULL argument");
     if (!t->arena) plan_params(t);
     json d;
-    d["precision"] = t->bf16 ? "bf16" : "ffma";
+    d["precision"] = t->bf16 ? "bf16" : t->tf32 ? "tf32" : "ffma";
     d["batch"] = t->batch;
     d["classes"] = t->classes;
     d["world"] = t->world;

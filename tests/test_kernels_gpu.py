@@ -2,8 +2,9 @@
 on identical seeded inputs, through the C-ABI (libtcb.so).
 
 Tolerances (north_star): normwise relative error <= 1e-5 in fp32-FFMA mode,
-<= 2e-2 in the bf16 tensor-core mode (the oracle is fed the same
-bf16-rounded inputs; outputs are bf16). Integer/byte work (RNG, labels,
+<= 2e-2 in the TF32 and bf16 tensor-core modes (bf16: the oracle is fed the
+same bf16-rounded inputs; outputs are bf16. TF32: fp32 inputs and outputs,
+tf32 multiplies). Integer/byte work (RNG, labels,
 argmax) and the SGD update are bit-exact.
 SURVEY §8 rows: a14 (conv fwd/dgrad/wgrad), a16 (SGD), a17 (pools, loss), d1 (RNG).
 """
@@ -15,7 +16,7 @@ from oracle_binding import elem_err, rel_err
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-TOL = {"ffma": 1e-5, "bf16": 2e-2}
+TOL = {"ffma": 1e-5, "tf32": 2e-2, "bf16": 2e-2}
 SEED = 20260810
 
 # (name, n, h, w, c, k, r, pad, stride) — drawn from the BASELINE configs' layer shapes,
@@ -47,6 +48,10 @@ GEOMS = [
     ("im2col_5x5_pad2", 2, 8, 8, 128, 64, 5, 2, 1),
     ("c8_3x3", 2, 12, 10, 8, 24, 3, 1, 1),
     ("c8_11x11_s4", 2, 35, 35, 8, 96, 11, 2, 4),
+]
+C4_ONLY = [  # channel counts % 4 but not % 8: fp32 modes only
+    ("c4_3x3_k20", 2, 9, 9, 12, 20, 3, 1, 1),
+    ("c4_5x5_s2", 2, 13, 11, 4, 36, 5, 2, 2),
 ]
 FFMA_ONLY = [
     ("lenet_conv1_c1", 4, 28, 28, 1, 20, 5, 0, 1),
@@ -89,13 +94,13 @@ def operand_path(request):
     lib.tcb_set_conv_operand_path(0)
 
 
-@pytest.mark.parametrize("prec", ["ffma", "bf16"])
-@pytest.mark.parametrize("spec", GEOMS + FFMA_ONLY, ids=lambda s: s[0])
+@pytest.mark.parametrize("prec", ["ffma", "tf32", "bf16"])
+@pytest.mark.parametrize("spec", GEOMS + C4_ONLY + FFMA_ONLY, ids=lambda s: s[0])
 def test_conv_gemm_parity(oracle, prec, spec, operand_path):
-    if prec == "bf16" and spec in FFMA_ONLY:
-        pytest.skip("tensor-core path needs C, K multiples of 8")
-    if prec == "ffma" and operand_path != "auto":
-        pytest.skip("operand path only applies to the tensor-core kernel")
+    if (prec != "ffma" and spec in FFMA_ONLY) or (prec == "bf16" and spec in C4_ONLY):
+        pytest.skip("tensor-core paths need C, K multiples of 8 (bf16) / 4 (tf32)")
+    if prec != "bf16" and operand_path != "auto":
+        pytest.skip("operand path only applies to the bf16 tensor-core kernel")
     dev = _dev()
     name, n, h, w, c, k, r, pad, stride = spec
     g = dev.geom(n, h, w, c, k, r, pad=pad, stride=stride)
@@ -139,6 +144,8 @@ def test_conv_gemm_parity(oracle, prec, spec, operand_path):
     assert torch.equal(dw, dw2), "wgrad must be bitwise deterministic"
     if prec == "ffma":
         assert elem_err(_host(y), ref, 1e-2) <= 1e-4
+    if prec == "tf32":  # 10-bit mantissa products, fp32 accumulate: far inside 2e-2
+        assert rel_err(_host(y0), ref0) <= 2e-3 and rel_err(_host(dw), refw) <= 2e-3
 
 
 def test_fill_and_labels_bit_exact(oracle):

@@ -1,6 +1,6 @@
 """Step-level parity: the C++ executor's full training step (fwd -> loss ->
 bwd -> fused SGD) vs the CPU oracle step on identical seeded inputs/weights.
-Tolerances: normwise 1e-5 (fp32-FFMA mode), 2e-2 (bf16 tensor-core mode).
+Tolerances: normwise 1e-5 (fp32-FFMA mode), 2e-2 (TF32 / bf16 tensor-core modes).
 SURVEY §8 rows a14-a17 end to end, d1 (synthetic inputs)."""
 import numpy as np
 import pytest
@@ -11,7 +11,7 @@ from oracle_step import DeviceTeacher, OracleStep
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-TOL = {"ffma": 1e-5, "bf16": 2e-2}
+TOL = {"ffma": 1e-5, "tf32": 2e-2, "bf16": 2e-2}
 
 
 def _models():
@@ -39,7 +39,7 @@ def _check(oracle, cfg, per_layer=True, teacher=None):
     t = _run_step(cfg)
     lay = t.describe()
     ref = OracleStep(oracle, cfg, lay)
-    teacher = (prec == "bf16") if teacher is None else teacher
+    teacher = (prec != "ffma") if teacher is None else teacher
     ref.run(teacher=DeviceTeacher(t, lay) if teacher else None)
     if teacher:
         assert len(ref.local_err) >= 2 * sum(L["op"] == "conv" for L in lay["layers"]) - 1
@@ -75,7 +75,7 @@ def _check(oracle, cfg, per_layer=True, teacher=None):
     return t, worst
 
 
-@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+@pytest.mark.parametrize("prec", ["ffma", "tf32", "bf16"])
 def test_tiny_resnet_step(oracle, prec):
     _check(oracle, _models().tiny_resnet(batch=4, precision=prec))
 
@@ -92,6 +92,15 @@ def test_resnet50_geometry_step_bf16(oracle):
     assert convs[0]["explicit_im2col"] and not any(L["explicit_im2col"] for L in convs[1:])
 
 
+def test_resnet50_geometry_step_tf32(oracle):
+    """C3 geometry in the TF32 tensor-core mode (fp32 storage, the 3-channel
+    input padded to 4 so the stem runs on tcgen05 kind::tf32 too), layer-local."""
+    t, _ = _check(oracle, _models().resnet50(batch=1, precision="tf32"))
+    lay = t.describe()
+    assert lay["precision"] == "tf32"
+    assert lay["layers"][0]["shape"][3] == 4
+
+
 def test_explicit_im2col_stem_batch8(oracle):
     """Stem-only net at batch 8: explicit-im2col fwd (TMA epilogue) and wgrad
     (col kept from the forward pass) against the oracle, layer-local."""
@@ -106,7 +115,7 @@ def test_lenet_step_c1(oracle):
     _check(oracle, _models().lenet(batch=64))
 
 
-@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+@pytest.mark.parametrize("prec", ["ffma", "tf32", "bf16"])
 def test_alexnet_step_small_batch(oracle, prec):
     """C2 geometry (227x227x3, ungrouped AlexNet + 4096/4096/1000) at N=2."""
     _check(oracle, _models().alexnet(batch=2, precision=prec))
