@@ -66,6 +66,10 @@ def parse():
                     help="reduce gradient shards during backward on a low-CTA communicator "
                          "(off by default: measured slower on ResNet-50, DESIGN.md §6)")
     ap.add_argument("--no-overlap", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--ps-transport", choices=["auto", "nccl", "nvls"], default="auto",
+                    help="PS step: NCCL reduce-scatter + SGD + all-gather, or one fused kernel "
+                         "over NVSwitch multicast (bf16, PS shards = GPUs); auto = nvls where it "
+                         "applies and the system has multicast, else nccl")
     return ap.parse_args()
 
 
@@ -200,7 +204,7 @@ def conv_roofline(cfg, pk, reps=5):
 NVLINK_PEER_GBPS = 770.0  # measured per-direction peer bandwidth (B200_PROFILING.md)
 
 
-def lemmas(phases, world, param_bytes, out_dir):
+def lemmas(phases, world, param_bytes, out_dir, transport="nccl"):
     """Paper Lemma 1 / Lemma 2 evaluated by the traincap planner (C-ABI) from
     this run's measured StepTrace: gpu_processing = fwd + bwd, and the
     unhidden distributed_update (reduce-scatter), parameter_update (SGD) and
@@ -221,9 +225,12 @@ def lemmas(phases, world, param_bytes, out_dir):
     out = {"overhead_ratio": ro, "measured_at_gpus": world,
            "lemma1": {str(g): {"efficiency": e, "speedup": s} for g, e, s in table},
            "lemma1_8gpu_predicted_efficiency": table[7][1]}
-    if world > 1 and phases["reduce_scatter"] > 0:
+    # PS aggregation time: the reduce-scatter phase (NCCL), or the fused
+    # multicast kernel (NVLS: its reduce half moves the gradient)
+    agg_ms = phases["sgd"] if transport == "nvls" else phases["reduce_scatter"]
+    if world > 1 and agg_ms > 0:
         rs_bytes = param_bytes * (world - 1) / world
-        b_ps = rs_bytes / (phases["reduce_scatter"] / 1e3)
+        b_ps = rs_bytes / (agg_ms / 1e3)
         t_c = (phases["fwd"] + phases["bwd"]) / 1e3
         out["lemma2"] = {"param_bytes": param_bytes, "workers": world,
                          "bandwidth_bytes_per_sec": b_ps, "compute_time_seconds": t_c,
@@ -245,9 +252,21 @@ def busbw_peak(world, op):
     return NVLINK_PEER_GBPS, "peer copy per direction, B200_PROFILING.md (fallback)"
 
 
-def ps_bandwidth(phases, world, param_bytes):
+def ps_bandwidth(phases, world, param_bytes, transport="nccl"):
     if world < 2:
         return None
+    if transport == "nvls":
+        # one kernel: multimem.ld_reduce of the own shard (the switch reads every
+        # GPU's slice: each GPU's whole fp32 buffer leaves over its NVLinks once)
+        # + multimem.st of the bf16 shard; phases: barrier / fused kernel / barrier
+        t = phases["sgd"] / 1e3
+        egress = param_bytes + param_bytes / 2 / world
+        return {"transport": "nvls", "fused_kernel_ms": round(phases["sgd"], 4),
+                "barriers_ms": round(phases["reduce_scatter"] + phases["all_gather"], 4),
+                "nvlink_egress_GBps_per_gpu": round(egress / t / 1e9, 1),
+                "nvlink_peak_GBps": NVLINK_PEER_GBPS, "nvlink_frac": round(egress / t / 1e9 / NVLINK_PEER_GBPS, 3),
+                "rs_ag_equivalent_busbw_GBps": round(param_bytes * (world - 1) / world / t / 1e9, 1),
+                "peak_kind": "peer copy per direction, B200_PROFILING.md"}
     rs = param_bytes * (world - 1) / world / (phases["reduce_scatter"] / 1e3) / 1e9
     ag = (param_bytes / 2) * (world - 1) / world / (phases["all_gather"] / 1e3) / 1e9  # bf16 refresh
     prs, src = busbw_peak(world, "reduce_scatter")
@@ -342,7 +361,20 @@ def main():
     cfg = models.build(args.model, batch=args.batch, precision=args.precision)
     cfg["n_ps"] = args.n_ps
     cfg["overlap_comm"] = args.overlap
-    tr = Trainer(cfg, rank, world, nid)
+    nvls_ok = world > 1 and args.precision == "bf16" and args.n_ps in (0, world) and not args.overlap
+    transport = args.ps_transport
+    if transport == "auto":
+        transport = "nvls" if nvls_ok else "nccl"
+    cfg["ps_transport"] = transport
+    transport_note = None
+    try:
+        tr = Trainer(cfg, rank, world, nid)
+    except RuntimeError as e:
+        if args.ps_transport != "auto" or transport != "nvls":
+            raise
+        transport_note = f"nvls unavailable ({e}); nccl"
+        transport = cfg["ps_transport"] = "nccl"
+        tr = Trainer(cfg, rank, world, nid)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -492,6 +524,7 @@ def main():
                        "per_gpu_batch": args.batch, "global_batch": args.batch * world,
                        "ps_shards": args.n_ps or world, "precision": args.precision,
                        "comm_overlap": args.overlap and world > 1 and (args.n_ps in (0, world)),
+                       "ps_transport": (transport_note or transport) if world > 1 else None,
                        "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (per-step activations >> 126 MB); no flush"},
             "clocks": clk,
@@ -503,8 +536,8 @@ def main():
             "loss": loss,
             "hbm_arena_bytes": layout.get("arena_bytes"),
             "ps": {"param_bytes": param_bytes, "rs_ag_bytes_per_gpu_step": rs_ag_bytes,
-                   "busbw": ps_bandwidth(phases, world, param_bytes)},
-            "lemmas": lemmas(phases, world, param_bytes, os.path.join(ROOT, "gpurun_out")),
+                   "busbw": ps_bandwidth(phases, world, param_bytes, transport)},
+            "lemmas": lemmas(phases, world, param_bytes, os.path.join(ROOT, "gpurun_out"), transport),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

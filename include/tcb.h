@@ -140,6 +140,21 @@ int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_dtype, v
                      size_t n, float lr, float momentum, float weight_decay, float grad_scale,
                      void* stream);
 
+/* Fused PS step of one shard over NVSwitch multicast (what the trainer's
+ * NVLS path launches): grad_mc / wcompute_mc are multicast addresses of the
+ * fp32 gradient and bf16 weight buffers, grad / w / v this GPU's buffers;
+ * elements [begin, begin + n), n and begin multiples of 4. */
+int tcb_ps_nvls_update(const float* grad_mc, float* grad, float* w, float* v, void* wcompute_mc,
+                       size_t begin, size_t n, float lr, float momentum, float weight_decay,
+                       float grad_scale, void* stream);
+/* All-GPU barrier on P2P-mapped signal pads (slots 2048 + rank); epoch_dev
+ * is a zero-initialised device u32 per rank. */
+int tcb_nvls_barrier(void* const* signal_pads_dev, uint32_t* epoch_dev, int rank, int world, void* stream);
+/* Microbenchmark halves of tcb_ps_nvls_update: mode 1 = multicast reduce only,
+ * 2 = multicast store only. */
+int tcb_nvls_probe(int mode, const float* grad_mc, float* grad, const float* w, void* wcompute_mc,
+                   size_t begin, size_t n, void* stream);
+
 /* ------------------------------------------------------------ profiler -- */
 /* Measures every (conv layer, algorithm, mini-batch) on this GPU and returns
  * the reference's cost catalog: rows of traincap::CostEntry
@@ -163,6 +178,18 @@ int tcb_trainer_destroy(tcb_trainer* t);
 int tcb_nccl_unique_id(uint8_t* id128);
 /* Join a world of `world` ranks (one process per GPU). world == 1 needs no id. */
 int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t* id128);
+/* NVSwitch-multicast parameter-server step (after join, before the first
+ * step; bf16, PS shards = GPUs): the flat fp32 gradient buffer and the bf16
+ * compute-weight buffer (param_padded elements each, see describe) live in
+ * caller-allocated symmetric memory bound to multicast objects (e.g. torch
+ * symmetric memory). `grad`/`wcompute` are this GPU's buffers, `*_mc` their
+ * multicast addresses, `signal_pads_dev` a device array of the world's
+ * P2P-mapped signal pads (>= (2048 + world) u32 each, slots 2048.. are used).
+ * Each step then runs barrier -> one kernel (multimem reduce of the own
+ * shard + momentum SGD + multimem store of the bf16 weights) -> barrier,
+ * replacing NCCL reduce-scatter / SGD / all-gather. */
+int tcb_trainer_attach_nvls(tcb_trainer* t, void* grad, const void* grad_mc, void* wcompute,
+                            void* wcompute_mc, void* const* signal_pads_dev);
 /* Loads a mini-batch from HOST memory (NHWC fp32 images, int32 labels). NULL
  * images = keep the device-resident synthetic batch. */
 int tcb_trainer_set_batch(tcb_trainer* t, const float* host_images, const int32_t* host_labels,

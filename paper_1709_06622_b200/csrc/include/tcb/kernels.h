@@ -90,6 +90,21 @@ cudaError_t conv_tf32_dgrad(const ConvGeom& g, const float* dy, const float* w,
 cudaError_t conv_tf32_wgrad(const ConvGeom& g, const float* dy, const float* x, float* dw,
                             void* workspace, cudaStream_t st);
 
+// ---- parameter-server step over NVSwitch multicast (ps_nvls.cu) ----
+// Barrier across `world` GPUs on P2P-mapped signal pads (device array of
+// per-rank pad pointers; slots slot0 .. slot0 + world - 1 are used);
+// `epoch_dev` is a zero-initialised per-rank device counter.
+cudaError_t nvls_barrier(uint32_t* const* pads_dev, uint32_t* epoch_dev, int slot0, int rank, int world,
+                         cudaStream_t st);
+// Fused reduce-scatter + momentum SGD + all-gather of elements [begin, begin+n)
+// of the flat buffer: grad_mc / wc_mc are multicast addresses of the fp32
+// gradient and bf16 compute-weight buffers; grad, w, v are local.
+cudaError_t ps_nvls_update(const float* grad_mc, float* grad, float* w, float* v, void* wc_mc, size_t begin,
+                           size_t n, float lr, float mom, float wd, float gscale, cudaStream_t st);
+// microbenchmark halves of ps_nvls_update: 1 = multicast reduce only, 2 = multicast store only
+cudaError_t nvls_probe(int mode, const float* grad_mc, float* grad, const float* w, void* wc_mc, size_t begin,
+                       size_t n, cudaStream_t st);
+
 // ---- Winograd F(2x2,3x3) (3x3, stride 1) ----
 size_t winograd_workspace(const ConvGeom& g, ConvMode mode, DType dt);
 bool winograd_supported(const ConvGeom& g);

@@ -315,6 +315,29 @@ TCB_API int tcb_cast(int src_dtype, const void* src, int dst_dtype, void* dst, s
                       "cast");
 }
 
+TCB_API int tcb_ps_nvls_update(const float* grad_mc, float* grad, float* w, float* v, void* wcompute_mc,
+                               size_t begin, size_t n, float lr, float momentum, float weight_decay,
+                               float grad_scale, void* stream) {
+    if (!grad_mc || !grad || !w || !v || !wcompute_mc) return fail(TCB_ERR_INVALID, "NULL argument");
+    return check_cuda(ps_nvls_update(grad_mc, grad, w, v, wcompute_mc, begin, n, lr, momentum, weight_decay,
+                                     grad_scale, static_cast<cudaStream_t>(stream)),
+                      "ps_nvls_update");
+}
+
+TCB_API int tcb_nvls_barrier(void* const* signal_pads_dev, uint32_t* epoch_dev, int rank, int world,
+                             void* stream) {
+    if (!signal_pads_dev || !epoch_dev) return fail(TCB_ERR_INVALID, "NULL argument");
+    return check_cuda(nvls_barrier(reinterpret_cast<uint32_t* const*>(signal_pads_dev), epoch_dev, 2048, rank,
+                                   world, static_cast<cudaStream_t>(stream)),
+                      "nvls_barrier");
+}
+
+TCB_API int tcb_nvls_probe(int mode, const float* grad_mc, float* grad, const float* w, void* wcompute_mc,
+                           size_t begin, size_t n, void* stream) {
+    return check_cuda(nvls_probe(mode, grad_mc, grad, w, wcompute_mc, begin, n, static_cast<cudaStream_t>(stream)),
+                      "nvls_probe");
+}
+
 TCB_API int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_dtype,
                              void* w_compute, size_t n, float lr, float momentum,
                              float weight_decay, float grad_scale, void* stream) {

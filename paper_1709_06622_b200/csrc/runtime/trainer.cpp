@@ -164,6 +164,19 @@ struct tcb_trainer {
     T* at(size_t off) const {
         return reinterpret_cast<T*>(static_cast<char*>(arena) + off);
     }
+
+    // NVLS parameter-server path (tcb_trainer_attach_nvls): the fp32 gradient
+    // and bf16 compute-weight buffers live in caller-provided symmetric memory
+    // bound to NVSwitch multicast objects; RS + SGD + AG is one kernel.
+    bool nvls = false;
+    float* ext_grad = nullptr;
+    const float* grad_mc = nullptr;
+    void* ext_wc = nullptr;
+    void* wc_mc = nullptr;
+    uint32_t* const* pads_dev = nullptr;
+    uint32_t* nvls_epoch = nullptr;
+    float* grad_ptr() const { return ext_grad ? ext_grad : at<float>(off_grad); }
+    void* wc_ptr() const { return ext_wc ? ext_wc : at(off_wc); }
 };
 
 namespace tcb {
@@ -469,7 +482,7 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
     float* param = t->at<float>(t->off_param);
     TRY_CUDA(cudaMemsetAsync(param, 0, t->param_padded * 4, st));
     TRY_CUDA(cudaMemsetAsync(t->at(t->off_mom), 0, t->param_padded * 4, st));
-    TRY_CUDA(cudaMemsetAsync(t->at(t->off_grad), 0, t->param_padded * 4, st));
+    TRY_CUDA(cudaMemsetAsync(t->grad_ptr(), 0, t->param_padded * 4, st));
     for (const Node& nd : t->nodes) {
         if (nd.op != Op::Conv) continue;
         const int cl = t->nodes[nd.in].c_logical, cp = nd.g.c;
@@ -480,14 +493,14 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
                                   1000 + nd.conv_index, -nd.init_scale, nd.init_scale, st));
         } else {
             // generate the logical stream in the grad buffer, scatter into padded channels
-            float* scratch = t->at<float>(t->off_grad);
+            float* scratch = t->grad_ptr();
             TRY_CUDA(fill_uniform(DType::F32, scratch, outer * cl, t->seed, 1000 + nd.conv_index,
                                   -nd.init_scale, nd.init_scale, st));
             TRY_CUDA(pack_channels(DType::F32, scratch, param + nd.woff, outer, cl, cp, st));
         }
     }
     if (t->bf16)
-        TRY_CUDA(cast(DType::F32, param, DType::BF16, t->at(t->off_wc), t->param_padded, st));
+        TRY_CUDA(cast(DType::F32, param, DType::BF16, t->wc_ptr(), t->param_padded, st));
     // synthetic mini-batch: worker r uses seed + r (distinct mini-batches);
     // "data_rank" overrides r (tests replay one rank's batch on a single GPU)
     const Node& in = t->nodes[0];
@@ -496,7 +509,7 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
                           data_seed, 1, -1.f, 1.f, st));
     TRY_CUDA(fill_labels(t->at<int32_t>(t->off_labels), t->batch, t->classes, data_seed, st));
     TRY(pack_input(t, st));
-    TRY_CUDA(cudaMemsetAsync(t->at(t->off_grad), 0, t->param_padded * 4, st));
+    TRY_CUDA(cudaMemsetAsync(t->grad_ptr(), 0, t->param_padded * 4, st));
     TRY_CUDA(cudaStreamSynchronize(st));
     t->initialized = true;
     return TCB_OK;
@@ -510,7 +523,7 @@ int refresh_transposes(tcb_trainer* t, cudaStream_t st) {
         int blocks = 0;
         for (const Node& nd : t->nodes) {
             if (nd.op != Op::Conv || !nd.pack_wT) continue;
-            jobs.push_back({t->at<__nv_bfloat16>(t->off_wc) + nd.woff, t->at(nd.wT), nd.g, blocks});
+            jobs.push_back({static_cast<__nv_bfloat16*>(t->wc_ptr()) + nd.woff, t->at(nd.wT), nd.g, blocks});
             blocks += pack_dgrad_blocks(nd.g);
         }
         t->pack_njobs = static_cast<int>(jobs.size());
@@ -539,14 +552,14 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                 ep.relu = nd.relu;
                 const size_t idx = static_cast<size_t>(&nd - t->nodes.data());
                 t->mark(idx, 0, st);
-                const void* wgt = t->bf16 ? static_cast<const void*>(t->at<__nv_bfloat16>(t->off_wc) + nd.woff)
+                const void* wgt = t->bf16 ? static_cast<const void*>(static_cast<__nv_bfloat16*>(t->wc_ptr()) + nd.woff)
                                           : static_cast<const void*>(t->at<float>(t->off_param) + nd.woff);
                 if (nd.algo_id == TCB_ALGO_WINOGRAD)
                     TRY_CUDA(winograd_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
                 else if (nd.algo_id == TCB_ALGO_FFT)
                     TRY_CUDA(fft_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
                 else if (t->bf16)
-                    TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), t->at<__nv_bfloat16>(t->off_wc) + nd.woff,
+                    TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), static_cast<__nv_bfloat16*>(t->wc_ptr()) + nd.woff,
                                          ep, t->at(nd.act), st, nd.narrow ? t->at(nd.nws) : nullptr));
                 else if (t->tf32)
                     TRY_CUDA(conv_tf32_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
@@ -613,7 +626,7 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         Epilogue ep;
         ep.residual = residual;
         ep.mask = mask_needed ? t->at(tgt.act) : nullptr;
-        const void* cw = t->bf16 ? static_cast<const void*>(t->at<__nv_bfloat16>(t->off_wc) + con.woff)
+        const void* cw = t->bf16 ? static_cast<const void*>(static_cast<__nv_bfloat16*>(t->wc_ptr()) + con.woff)
                                  : static_cast<const void*>(t->at<float>(t->off_param) + con.woff);
         if (con.algo_id == TCB_ALGO_WINOGRAD)
             TRY_CUDA(winograd_dgrad(con.g, t->dt, t->at(con.grad), cw, ep, out, t->at(t->off_ws), st));
@@ -656,7 +669,7 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
 int issue_ready_shards(tcb_trainer* t, int i, cudaStream_t st) {
     auto it = t->shard_trigger.find(i);
     if (it == t->shard_trigger.end()) return TCB_OK;
-    float* grad = t->at<float>(t->off_grad);
+    float* grad = t->grad_ptr();
     for (int sh : it->second) {
         TRY_CUDA(cudaEventRecord(t->ev_ready[sh], st));
         TRY_CUDA(cudaStreamWaitEvent(t->comm_stream, t->ev_ready[sh], 0));
@@ -674,7 +687,7 @@ int backward(tcb_trainer* t, cudaStream_t st) {
     struct Reset {
         ~Reset() { conv_tc_set_sm_reserve(0); }
     } reset;
-    float* grad = t->at<float>(t->off_grad);
+    float* grad = t->grad_ptr();
     for (int i = static_cast<int>(t->nodes.size()) - 1; i >= 0; --i) {
         const Node& nd = t->nodes[i];
         if (nd.op != Op::Input && nd.op != Op::Loss && nd.compute_from.empty() &&
@@ -733,13 +746,13 @@ int backward(tcb_trainer* t, cudaStream_t st) {
 }
 
 int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, cudaEvent_t after_sgd) {
-    float* grad = t->at<float>(t->off_grad);
+    float* grad = t->grad_ptr();
     float* param = t->at<float>(t->off_param);
     float* mom = t->at<float>(t->off_mom);
     const float gscale = 1.0f / static_cast<float>(t->world);
     const ncclDataType_t wdt = t->bf16 ? ncclBfloat16 : ncclFloat32;
     const size_t wes = t->bf16 ? 2 : 4;
-    char* wc = t->at<char>(t->off_wc);
+    char* wc = static_cast<char*>(t->wc_ptr());
     const int owners = (t->n_ps > 0 && t->n_ps < t->world) ? t->n_ps : t->world;
 
     if (t->overlap_active()) {
@@ -757,6 +770,20 @@ int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, 
         t->launches++;
         TRY_CUDA(cudaEventRecord(t->ev_comm_done, cs));
         TRY_CUDA(cudaStreamWaitEvent(st, t->ev_comm_done, 0));
+    } else if (t->nvls) {
+        // PS shards = GPUs over NVSwitch multicast: every GPU's gradients are
+        // written (barrier) -> one kernel reduces the own shard in the switch,
+        // applies SGD and multicasts the bf16 weights -> all weights delivered
+        // (barrier) before the next forward reads them
+        constexpr int kSlot0 = 2048;
+        TRY_CUDA(nvls_barrier(t->pads_dev, t->nvls_epoch, kSlot0, t->rank, t->world, st));
+        if (after_rs) TRY_CUDA(cudaEventRecord(after_rs, st));
+        const size_t o = t->rank * t->shard;
+        TRY_CUDA(ps_nvls_update(t->grad_mc, grad, param, mom, t->wc_mc, o, t->shard, t->lr, t->momentum,
+                                t->weight_decay, gscale, st));
+        if (after_sgd) TRY_CUDA(cudaEventRecord(after_sgd, st));
+        TRY_CUDA(nvls_barrier(t->pads_dev, t->nvls_epoch, kSlot0, t->rank, t->world, st));
+        t->launches += 3;
     } else if (t->world > 1 && owners == t->world) {
         // PS shards = GPUs: reduce-scatter (in place) -> SGD on own shard -> all-gather
         TRY_NCCL(ncclReduceScatter(grad, grad + t->rank * t->shard, t->shard, ncclFloat32, ncclSum,
@@ -862,6 +889,7 @@ TCB_API int tcb_trainer_destroy(tcb_trainer* t) {
         for (cudaEvent_t e : a)
             if (e) cudaEventDestroy(e);
     if (t->arena) cudaFree(t->arena);
+    if (t->nvls_epoch) cudaFree(t->nvls_epoch);
     delete t;
     return TCB_OK;
 }
@@ -896,6 +924,31 @@ TCB_API int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t*
             TRY_CUDA(cudaEventCreateWithFlags(&t->ev_comm_done, cudaEventDisableTiming));
         }
     }
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_attach_nvls(tcb_trainer* t, void* grad, const void* grad_mc, void* wcompute,
+                                    void* wcompute_mc, void* const* signal_pads_dev) {
+    if (!t || !grad || !grad_mc || !wcompute || !wcompute_mc || !signal_pads_dev)
+        return fail(TCB_ERR_INVALID, "NULL argument");
+    if (t->initialized) return fail(TCB_ERR_INVALID, "attach before the first step");
+    if (!t->bf16) return fail(TCB_ERR_UNSUPPORTED, "the NVLS parameter-server path is bf16-only");
+    if (t->world < 2 || (t->n_ps > 0 && t->n_ps < t->world))
+        return fail(TCB_ERR_UNSUPPORTED, "the NVLS path needs world > 1 and PS shards = GPUs");
+    if (t->overlap) return fail(TCB_ERR_INVALID, "overlap_comm and the NVLS path are exclusive");
+    if (reinterpret_cast<uintptr_t>(grad) % 16 || reinterpret_cast<uintptr_t>(grad_mc) % 16 ||
+        reinterpret_cast<uintptr_t>(wcompute) % 16 || reinterpret_cast<uintptr_t>(wcompute_mc) % 16)
+        return fail(TCB_ERR_INVALID, "NVLS buffers must be 16-byte aligned");
+    t->ext_grad = static_cast<float*>(grad);
+    t->grad_mc = static_cast<const float*>(grad_mc);
+    t->ext_wc = wcompute;
+    t->wc_mc = wcompute_mc;
+    t->pads_dev = reinterpret_cast<uint32_t* const*>(signal_pads_dev);
+    if (!t->nvls_epoch) {
+        TRY_CUDA(cudaMalloc(&t->nvls_epoch, sizeof(uint32_t)));
+        TRY_CUDA(cudaMemset(t->nvls_epoch, 0, sizeof(uint32_t)));
+    }
+    t->nvls = true;
     return TCB_OK;
 }
 
@@ -1174,9 +1227,9 @@ TCB_API int tcb_trainer_tensor(tcb_trainer* t, const char* name, void** ptr, siz
     void* p = nullptr;
     auto node_bytes = [&](const Node& nd) { return size_t(nd.n) * nd.h * nd.w * nd.c * es; };
     if (n == "param") { p = t->at(t->off_param); b = t->param_padded * 4; }
-    else if (n == "grad") { p = t->at(t->off_grad); b = t->param_padded * 4; }
+    else if (n == "grad") { p = t->grad_ptr(); b = t->param_padded * 4; }
     else if (n == "momentum") { p = t->at(t->off_mom); b = t->param_padded * 4; }
-    else if (n == "wcompute") { p = t->at(t->off_wc); b = t->param_padded * es; }
+    else if (n == "wcompute") { p = t->wc_ptr(); b = t->param_padded * es; }
     else if (n == "labels") { p = t->at(t->off_labels); b = size_t(t->batch) * 4; }
     else if (n == "loss") { p = t->at(t->off_loss); b = size_t(t->batch + 1) * 4; }
     else if (n == "input") { p = t->at(t->nodes[0].act); b = node_bytes(t->nodes[0]); }

@@ -2,7 +2,10 @@
 
 One Trainer per GPU process. For world > 1 the NCCL unique id is created on
 rank 0 and broadcast with torch.distributed (plumbing only); the gradient
-aggregation / parameter refresh itself runs inside the C++ step over NCCL.
+aggregation / parameter refresh itself runs inside the C++ step — over NCCL
+(reduce-scatter, SGD, all-gather), or with cfg["ps_transport"] = "nvls" as
+one fused kernel over NVSwitch multicast on buffers allocated here with torch
+symmetric memory (allocation / handle exchange only).
 """
 from __future__ import annotations
 
@@ -37,6 +40,7 @@ def _lib():
         L.tcb_trainer_launch_count.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
         L.tcb_trainer_enable_layer_timing.argtypes = [_vp, ctypes.c_int]
         L.tcb_trainer_layer_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p)]
+        L.tcb_trainer_attach_nvls.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
         L.tcb_free.argtypes = [_vp]
         _bound = True
     return L
@@ -70,6 +74,34 @@ class Trainer:
         self.rank, self.world = rank, world
         if world > 1 or nccl_id is not None:
             device.check(_lib().tcb_trainer_join(self.handle, rank, world, nccl_id))
+        self._symm = None
+        if world > 1 and cfg.get("ps_transport", "nccl") == "nvls":
+            self.attach_nvls()
+
+    def attach_nvls(self, group=None):
+        """Place the flat gradient / bf16 weight buffers in symmetric memory
+        bound to NVSwitch multicast objects and switch the PS step to the fused
+        multimem kernel (tcb_trainer_attach_nvls). Needs torch.distributed."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        group = group or dist.group.WORLD
+        n = self.describe()["param_padded"]
+        bufs, handles, mcs = [], [], []
+        for dt in (torch.float32, torch.bfloat16):
+            t = symm.empty(n, dtype=dt, device="cuda")
+            h = symm.rendezvous(t, group.group_name)
+            if not h.multicast_ptr:
+                raise RuntimeError("NVLS multicast is not available on this system")
+            delta = t.data_ptr() - h.buffer_ptrs[h.rank]
+            if delta < 0:
+                raise RuntimeError("unexpected symmetric-memory layout")
+            bufs.append(t)
+            handles.append(h)
+            mcs.append(h.multicast_ptr + delta)
+        device.check(_lib().tcb_trainer_attach_nvls(self.handle, _vp(bufs[0].data_ptr()), _vp(mcs[0]),
+                                                    _vp(bufs[1].data_ptr()), _vp(mcs[1]),
+                                                    _vp(handles[0].signal_pad_ptrs_dev)))
+        self._symm = (bufs, handles)  # keep the allocations alive
 
     def __del__(self):
         try:

@@ -7,7 +7,9 @@ Expected result, built from single-GPU replays of each rank's batch
 (data_rank = r): s = g_0 + g_1 (fp32; a 2-term sum is order-free) and
 w' = oracle.sgd(w0, s, v0 = 0, grad_scale = 1/2), bit-exact on every owned
 shard and on the gathered compute copy. N_ps = 1 < G (grouped ncclReduce to
-the single owner + broadcast) must give the same bits.
+the single owner + broadcast) and the fused NVSwitch-multicast step
+(ps_transport = "nvls": multimem reduce + SGD + multimem store in one kernel)
+must give the same bits.
 """
 import os
 import socket
@@ -25,7 +27,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _rank_main(rank, world, port, cfg, q):
+def _rank_main(rank, world, port, cfg, q, steps=1):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -36,7 +38,8 @@ def _rank_main(rank, world, port, cfg, q):
     nid = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(nid, src=0)
     t = Trainer(cfg, rank, world, nid[0])
-    t.step()
+    for _ in range(steps):
+        t.step()
     torch.cuda.synchronize()
     d = t.describe()
     q.put((rank, d["shard"], t.tensor("param").cpu().numpy(),
@@ -45,12 +48,12 @@ def _rank_main(rank, world, port, cfg, q):
     dist.destroy_process_group()
 
 
-def _run_world(cfg, world):
+def _run_world(cfg, world, steps=1):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, cfg, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, cfg, q, steps)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
@@ -74,16 +77,19 @@ def _single_rank_grads(cfg, data_rank):
     return t.tensor("param").cpu().numpy(), t.tensor("grad").cpu().numpy()
 
 
-@pytest.mark.parametrize("n_ps,overlap", [(0, False), (1, False), (0, True)])
-def test_two_gpu_ps_step_bit_exact(oracle, n_ps, overlap):
+@pytest.mark.parametrize("n_ps,overlap,transport", [(0, False, "nccl"), (1, False, "nccl"),
+                                                    (0, True, "nccl"), (0, False, "nvls")])
+def test_two_gpu_ps_step_bit_exact(oracle, n_ps, overlap, transport):
     """overlap: per-shard ncclReduce to the owner issued during backward on the
-    low-CTA communicator; must give the same bits as reduce-scatter."""
+    low-CTA communicator; nvls: the fused multicast kernel. Both must give the
+    same bits as reduce-scatter."""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     from paper_1709_06622_b200 import models
     cfg = models.tiny_resnet(batch=8, precision="bf16")
     cfg["n_ps"] = n_ps
     cfg["overlap_comm"] = overlap
+    cfg["ps_transport"] = transport
     w0, g0 = _single_rank_grads(cfg, 0)
     _, g1 = _single_rank_grads(cfg, 1)
     s = (g0 + g1).astype(np.float32)
@@ -102,3 +108,18 @@ def test_two_gpu_ps_step_bit_exact(oracle, n_ps, overlap):
         assert np.array_equal(param[sl], w_exp[sl]), f"rank {r} master shard"
     for r in range(2):
         assert np.array_equal(res[r][2], wc_exp), f"rank {r} gathered compute weights"
+
+
+def test_two_gpu_nvls_matches_nccl_over_steps():
+    """Five steps (the last ones replayed from a CUDA graph, barriers included):
+    the NVSwitch-multicast PS step and the NCCL one end bitwise equal (a
+    2-term fp32 sum is order-free)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from paper_1709_06622_b200 import models
+    cfg = models.tiny_resnet(batch=8, precision="bf16")
+    ref = _run_world(dict(cfg, ps_transport="nccl"), 2, steps=5)
+    got = _run_world(dict(cfg, ps_transport="nvls"), 2, steps=5)
+    for r in range(2):
+        assert np.array_equal(got[r][1], ref[r][1]), f"rank {r} master params"
+        assert np.array_equal(got[r][2], ref[r][2]), f"rank {r} compute weights"
