@@ -117,6 +117,17 @@ int tcb_maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, void* dx, 
 int tcb_maxpool_relu_bwd(int dtype, const void* dy, const uint8_t* argmax, const void* y, void* dx,
                          int n, int h, int w, int c, int f, int stride, int pad, void* stream);
 int tcb_avgpool_global_fwd(int dtype, const void* x, void* y, int n, int hw, int c, void* stream);
+/* Windowed average pool (Inception's branch pool), padding counted (/ f*f);
+ * c must fill 16-byte vectors (8 bf16 / 4 fp32). The backward optionally
+ * fuses the ReLU mask of the pool input (mask_act may be NULL). */
+int tcb_avgpool2d_fwd(int dtype, const void* x, void* y, int n, int h, int w, int c, int f, int stride,
+                      int pad, void* stream);
+int tcb_avgpool2d_bwd(int dtype, const void* dy, const void* mask_act, void* dx, int n, int h, int w, int c,
+                      int f, int stride, int pad, void* stream);
+/* rows x width elements between row-pitched buffers: channel concat of NHWC
+ * tensors (forward) and the split of its gradient (backward). */
+int tcb_slice_copy(int dtype, const void* src, size_t src_pitch, void* dst, size_t dst_pitch, int width,
+                   size_t rows, void* stream);
 int tcb_avgpool_global_bwd(int dtype, const void* dy, void* dx, int n, int hw, int c,
                            void* stream);
 /* mean softmax cross-entropy over n rows of `classes` logits; writes

@@ -299,6 +299,46 @@ void oracle_avgpool_bwd(const float* dy, double* dx, int n, int hw, int c) {
                 dx[((size_t)b * hw + i) * c + ch] = (double)dy[(size_t)b * c + ch] / hw;
 }
 
+void oracle_avgpool2d_fwd(const float* x, double* y, int n, int h, int w, int c, int f, int s, int p) {
+    const int ho = out_extent(h, f, p, s), wo = out_extent(w, f, p, s);
+    for (int b = 0; b < n; ++b)
+        for (int i = 0; i < ho; ++i)
+            for (int j = 0; j < wo; ++j)
+                for (int ch = 0; ch < c; ++ch) {
+                    double acc = 0;
+                    for (int r = 0; r < f; ++r) {
+                        const int hh = i * s - p + r;
+                        if (hh < 0 || hh >= h) continue;
+                        for (int q = 0; q < f; ++q) {
+                            const int ww = j * s - p + q;
+                            if (ww < 0 || ww >= w) continue;
+                            acc += x[(((size_t)b * h + hh) * w + ww) * c + ch];
+                        }
+                    }
+                    y[(((size_t)b * ho + i) * wo + j) * c + ch] = acc / (f * f);
+                }
+}
+
+void oracle_avgpool2d_bwd(const float* dy, double* dx, int n, int h, int w, int c, int f, int s, int p) {
+    const int ho = out_extent(h, f, p, s), wo = out_extent(w, f, p, s);
+    memset(dx, 0, sizeof(double) * (size_t)n * h * w * c);
+    for (int b = 0; b < n; ++b)
+        for (int i = 0; i < ho; ++i)
+            for (int j = 0; j < wo; ++j)
+                for (int ch = 0; ch < c; ++ch) {
+                    const double g = (double)dy[(((size_t)b * ho + i) * wo + j) * c + ch] / (f * f);
+                    for (int r = 0; r < f; ++r) {
+                        const int hh = i * s - p + r;
+                        if (hh < 0 || hh >= h) continue;
+                        for (int q = 0; q < f; ++q) {
+                            const int ww = j * s - p + q;
+                            if (ww < 0 || ww >= w) continue;
+                            dx[(((size_t)b * h + hh) * w + ww) * c + ch] += g;
+                        }
+                    }
+                }
+}
+
 double oracle_softmax_xent(const float* z, const int32_t* labels, double* dl, int n, int classes) {
     double total = 0.0;
     for (int b = 0; b < n; ++b) {

@@ -47,6 +47,10 @@ void oracle_maxpool_bwd(const float* dy, const uint8_t* arg, double* dx, int n, 
                         int c, int f, int s, int p);
 void oracle_avgpool_fwd(const float* x, double* y, int n, int hw, int c);
 void oracle_avgpool_bwd(const float* dy, double* dx, int n, int hw, int c);
+/* Windowed average pool (Inception's 3x3 / s1 / p1 branch pool): every
+ * window divides by f*f, padding counted (count_include_pad). */
+void oracle_avgpool2d_fwd(const float* x, double* y, int n, int h, int w, int c, int f, int s, int p);
+void oracle_avgpool2d_bwd(const float* dy, double* dx, int n, int h, int w, int c, int f, int s, int p);
 /* returns mean loss; dl = (softmax - onehot)/n */
 double oracle_softmax_xent(const float* logits, const int32_t* labels, double* dl, int n,
                            int classes);

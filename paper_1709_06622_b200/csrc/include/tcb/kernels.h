@@ -105,6 +105,19 @@ cudaError_t ps_nvls_update(const float* grad_mc, float* grad, float* w, float* v
 cudaError_t nvls_probe(int mode, const float* grad_mc, float* grad, const float* w, void* wc_mc, size_t begin,
                        size_t n, cudaStream_t st);
 
+// ---- graph operators for branched networks (graph_ops.cu) ----
+// rows x width elements from src (row pitch src_pitch) to dst (row pitch
+// dst_pitch): concat forward / backward as channel-slice copies
+cudaError_t slice_copy(DType dt, const void* src, size_t src_pitch, void* dst, size_t dst_pitch, int width,
+                       size_t rows, cudaStream_t st);
+// windowed average pool, padding counted (/ f*f); c % (16 B / element) == 0
+bool avgpool2d_supported(DType dt, int c);
+cudaError_t avgpool2d_fwd(DType dt, const void* x, void* y, int n, int h, int w, int c, int f, int s, int p,
+                          cudaStream_t st);
+// dx = [mask > 0] * (sum of the covering windows' dy / f^2); mask may be NULL
+cudaError_t avgpool2d_bwd(DType dt, const void* dy, void* dx, int n, int h, int w, int c, int f, int s, int p,
+                          cudaStream_t st, const void* mask = nullptr);
+
 // ---- Winograd F(2x2,3x3) (3x3, stride 1) ----
 size_t winograd_workspace(const ConvGeom& g, ConvMode mode, DType dt);
 bool winograd_supported(const ConvGeom& g);

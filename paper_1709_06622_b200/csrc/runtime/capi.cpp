@@ -267,6 +267,33 @@ TCB_API int tcb_maxpool_relu_bwd(int dtype, const void* dy, const uint8_t* argma
                       "maxpool_relu_bwd");
 }
 
+TCB_API int tcb_avgpool2d_fwd(int dtype, const void* x, void* y, int n, int h, int w, int c, int f, int stride,
+                              int pad, void* stream) {
+    if (f < 1 || stride < 1 || pad < 0) return fail(TCB_ERR_INVALID, "bad pool window");
+    if (!avgpool2d_supported(dt_of(dtype), c)) return fail(TCB_ERR_UNSUPPORTED, "channels must fill 16-byte vectors");
+    return check_cuda(avgpool2d_fwd(dt_of(dtype), x, y, n, h, w, c, f, stride, pad, static_cast<cudaStream_t>(stream)),
+                      "avgpool2d_fwd");
+}
+
+TCB_API int tcb_avgpool2d_bwd(int dtype, const void* dy, const void* mask_act, void* dx, int n, int h, int w,
+                              int c, int f, int stride, int pad, void* stream) {
+    if (f < 1 || stride < 1 || pad < 0) return fail(TCB_ERR_INVALID, "bad pool window");
+    if (!avgpool2d_supported(dt_of(dtype), c)) return fail(TCB_ERR_UNSUPPORTED, "channels must fill 16-byte vectors");
+    return check_cuda(avgpool2d_bwd(dt_of(dtype), dy, dx, n, h, w, c, f, stride, pad,
+                                    static_cast<cudaStream_t>(stream), mask_act),
+                      "avgpool2d_bwd");
+}
+
+TCB_API int tcb_slice_copy(int dtype, const void* src, size_t src_pitch, void* dst, size_t dst_pitch, int width,
+                           size_t rows, void* stream) {
+    if ((!src || !dst) && rows && width) return fail(TCB_ERR_INVALID, "NULL argument");
+    if (width < 0 || size_t(width) > src_pitch || size_t(width) > dst_pitch)
+        return fail(TCB_ERR_INVALID, "width exceeds a pitch");
+    return check_cuda(slice_copy(dt_of(dtype), src, src_pitch, dst, dst_pitch, width, rows,
+                                 static_cast<cudaStream_t>(stream)),
+                      "slice_copy");
+}
+
 TCB_API int tcb_maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, void* dx, int n,
                             int h, int w, int c, int f, int stride, int pad, void* stream) {
     return check_cuda(maxpool_bwd(dt_of(dtype), dy, argmax, dx, n, h, w, c, f, stride, pad,

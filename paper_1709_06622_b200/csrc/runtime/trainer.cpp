@@ -46,7 +46,7 @@ constexpr size_t kParamAlign = 64;  // elements
 
 size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-enum class Op { Input, Conv, MaxPool, AvgPool, Loss };
+enum class Op { Input, Conv, MaxPool, AvgPool, Loss, Concat };
 
 struct Node {
     Op op = Op::Input;
@@ -62,8 +62,10 @@ struct Node {
     float init_scale = 0.f;
     std::string algo = "gemm";
     int algo_id = 0;  // TCB_ALGO_*
-    // pool
+    // pool (avgpool: f == 0 -> global average)
     int f = 0, s = 0, p = 0;
+    // concat: inputs and their channel offsets in this tensor
+    std::vector<int> ins, coff;
     // arena offsets (bytes)
     size_t act = 0, grad = 0, argmax = 0, wT = 0;
     size_t nws = 0;  // narrow (explicit im2col) layers: own workspace, col kept fwd -> wgrad
@@ -313,9 +315,42 @@ int build_graph(tcb_trainer* t) {
                 nd.w = (x.w + 2 * nd.p - nd.f) / nd.s + 1;
                 if (nd.f > 15 || nd.h < 1 || nd.w < 1)
                     throw std::runtime_error("layer " + nd.name + ": bad pool window");
+            } else if (L.contains("f")) {
+                // windowed average pool (Inception's 3x3 / s1 / p1 branch pool)
+                nd.f = L.at("f").get<int>();
+                nd.s = L.value("stride", nd.f);
+                nd.p = L.value("pad", 0);
+                nd.h = (x.h + 2 * nd.p - nd.f) / nd.s + 1;
+                nd.w = (x.w + 2 * nd.p - nd.f) / nd.s + 1;
+                if (nd.f < 1 || nd.h < 1 || nd.w < 1 || !avgpool2d_supported(t->dt, nd.c))
+                    throw std::runtime_error("layer " + nd.name + ": bad average-pool window / channels");
             } else {
                 nd.h = nd.w = 1;
             }
+        } else if (op == "concat") {
+            // channel concatenation of same-size NHWC tensors (Inception branch outputs)
+            nd.op = Op::Concat;
+            for (const json& nm : L.at("in")) {
+                auto it = by_name.find(nm.get<std::string>());
+                if (it == by_name.end()) throw std::runtime_error("unknown tensor " + nm.dump());
+                const Node& x = t->nodes.at(it->second);
+                if (nd.ins.empty()) {
+                    nd.n = x.n;
+                    nd.h = x.h;
+                    nd.w = x.w;
+                } else if (x.n != nd.n || x.h != nd.h || x.w != nd.w) {
+                    throw std::runtime_error("layer " + nd.name + ": concat inputs differ in size");
+                }
+                if (x.c != x.c_logical)
+                    throw std::runtime_error("layer " + nd.name + ": concat input " + x.name +
+                                             " has padded channels");
+                nd.ins.push_back(it->second);
+                nd.coff.push_back(nd.c);
+                nd.c += x.c;
+            }
+            if (nd.ins.size() < 2) throw std::runtime_error("layer " + nd.name + ": concat needs 2+ inputs");
+            nd.c_logical = nd.c;
+            nd.in = nd.ins[0];
         } else if (op == "loss") {
             nd.op = Op::Loss;
             nd.in = src("in");
@@ -341,6 +376,9 @@ int build_graph(tcb_trainer* t) {
                 t->nodes[nd.residual].alias_from.push_back(i);
         } else if (nd.op == Op::MaxPool || nd.op == Op::AvgPool) {
             if (t->nodes[nd.in].op != Op::Input) t->nodes[nd.in].compute_from.push_back(i);
+        } else if (nd.op == Op::Concat) {
+            for (int j : nd.ins)
+                if (t->nodes[j].op != Op::Input) t->nodes[j].compute_from.push_back(i);
         }
     }
     for (Node& nd : t->nodes) {
@@ -577,9 +615,24 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                 t->launches++;
                 break;
             case Op::AvgPool:
-                TRY_CUDA(avgpool_global_fwd(t->dt, t->at(x->act), t->at(nd.act), x->n, x->h * x->w, x->c, st));
+                if (nd.f > 0)
+                    TRY_CUDA(avgpool2d_fwd(t->dt, t->at(x->act), t->at(nd.act), x->n, x->h, x->w, x->c, nd.f,
+                                           nd.s, nd.p, st));
+                else
+                    TRY_CUDA(avgpool_global_fwd(t->dt, t->at(x->act), t->at(nd.act), x->n, x->h * x->w, x->c, st));
                 t->launches++;
                 break;
+            case Op::Concat: {
+                const size_t rows = size_t(nd.n) * nd.h * nd.w;
+                const size_t es = dtype_size(t->dt);
+                for (size_t k = 0; k < nd.ins.size(); ++k) {
+                    const Node& xi = t->nodes[nd.ins[k]];
+                    TRY_CUDA(slice_copy(t->dt, t->at(xi.act), xi.c, t->at<char>(nd.act) + nd.coff[k] * es, nd.c,
+                                        xi.c, rows, st));
+                    t->launches++;
+                }
+                break;
+            }
             case Op::Loss: {
                 const Node& z = t->nodes[t->logits];
                 TRY_CUDA(softmax_xent(t->dt, t->at(z.act), t->at<int32_t>(t->off_labels), t->at(z.grad),
@@ -646,9 +699,29 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
     }
     // the ReLU mask fuses into the pool backward when nothing else must be added first
     const bool fuse_mask = mask_needed && extras.empty();
+    if (con.op == Op::Concat) {
+        // this input's channel range of the concatenated gradient
+        size_t k = 0;
+        while (con.ins[k] != ti) ++k;
+        TRY_CUDA(slice_copy(t->dt, t->at<char>(con.grad) + con.coff[k] * dtype_size(t->dt), con.c, out, tgt.c,
+                            tgt.c, size_t(tgt.n) * tgt.h * tgt.w, st));
+        t->launches++;
+        for (const void* e : extras) {
+            TRY_CUDA(add_inplace(t->dt, out, e, elems, st));
+            t->launches++;
+        }
+        if (mask_needed) {
+            TRY_CUDA(relu_mask_inplace(t->dt, out, t->at(tgt.act), elems, st));
+            t->launches++;
+        }
+        return TCB_OK;
+    }
     if (con.op == Op::MaxPool)
         TRY_CUDA(maxpool_bwd(t->dt, t->at(con.grad), t->at<uint8_t>(con.argmax), out, tgt.n, tgt.h, tgt.w,
                              tgt.c, con.f, con.s, con.p, st, fuse_mask ? t->at(con.act) : nullptr));
+    else if (con.f > 0)
+        TRY_CUDA(avgpool2d_bwd(t->dt, t->at(con.grad), out, tgt.n, tgt.h, tgt.w, tgt.c, con.f, con.s, con.p, st,
+                               fuse_mask ? t->at(tgt.act) : nullptr));
     else
         TRY_CUDA(avgpool_global_bwd(t->dt, t->at(con.grad), out, tgt.n, tgt.h * tgt.w, tgt.c, st,
                                     fuse_mask ? t->at(tgt.act) : nullptr));
@@ -740,6 +813,9 @@ int backward(tcb_trainer* t, cudaStream_t st) {
             }
         } else if (nd.op == Op::MaxPool || nd.op == Op::AvgPool) {
             if (t->nodes[nd.in].op != Op::Input) TRY(backward_contribution(t, i, nd.in, st));
+        } else if (nd.op == Op::Concat) {
+            for (int j : nd.ins)
+                if (t->nodes[j].op != Op::Input) TRY(backward_contribution(t, i, j, st));
         }
     }
     return TCB_OK;
@@ -1186,7 +1262,7 @@ TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
         json L;
         L["index"] = i;
         L["name"] = nd.name;
-        static const char* ops[] = {"input", "conv", "maxpool", "avgpool", "loss"};
+        static const char* ops[] = {"input", "conv", "maxpool", "avgpool", "loss", "concat"};
         L["op"] = ops[static_cast<int>(nd.op)];
         L["in"] = nd.in;
         L["residual"] = nd.residual;
@@ -1208,7 +1284,11 @@ TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
             const size_t last_el = (nd.bias ? nd.boff + nd.g.k : nd.woff + nd.wcount) - 1;
             L["shards"] = {first, last_el / std::max<size_t>(t->shard, 1)};
         }
-        if (nd.op == Op::MaxPool) L["pool"] = {nd.f, nd.s, nd.p};
+        if (nd.op == Op::MaxPool || (nd.op == Op::AvgPool && nd.f > 0)) L["pool"] = {nd.f, nd.s, nd.p};
+        if (nd.op == Op::Concat) {
+            L["ins"] = nd.ins;
+            L["coff"] = nd.coff;
+        }
         layers.push_back(std::move(L));
     }
     d["layers"] = std::move(layers);

@@ -70,6 +70,10 @@ def lib() -> ctypes.CDLL:
     L.tcb_conv_dgrad.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.tcb_conv_wgrad.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.tcb_maxpool_fwd.argtypes = [ctypes.c_int, _vp, _vp, _vp] + [ctypes.c_int] * 7 + [_vp]
+    L.tcb_avgpool2d_fwd.argtypes = [ctypes.c_int, _vp, _vp] + [ctypes.c_int] * 7 + [_vp]
+    L.tcb_avgpool2d_bwd.argtypes = [ctypes.c_int, _vp, _vp, _vp] + [ctypes.c_int] * 7 + [_vp]
+    L.tcb_slice_copy.argtypes = [ctypes.c_int, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t, ctypes.c_int,
+                                 ctypes.c_size_t, _vp]
     L.tcb_maxpool_bwd.argtypes = [ctypes.c_int, _vp, _vp, _vp] + [ctypes.c_int] * 7 + [_vp]
     L.tcb_avgpool_global_fwd.argtypes = [ctypes.c_int, _vp, _vp] + [ctypes.c_int] * 3 + [_vp]
     L.tcb_avgpool_global_bwd.argtypes = [ctypes.c_int, _vp, _vp] + [ctypes.c_int] * 3 + [_vp]
@@ -184,6 +188,35 @@ def maxpool_bwd(dy, arg, shape, f, s, p, relu_y=None):
         check(lib().tcb_maxpool_bwd(DT[dy.dtype], _p(dy), _p(arg), _p(dx), n, h, w, c, f, s, p,
                                     _stream()))
     return dx
+
+
+def avgpool2d_fwd(x, f, s, p):
+    n, h, w, c = x.shape
+    ho, wo = (h + 2 * p - f) // s + 1, (w + 2 * p - f) // s + 1
+    y = torch.empty(n, ho, wo, c, dtype=x.dtype, device="cuda")
+    check(lib().tcb_avgpool2d_fwd(DT[x.dtype], _p(x), _p(y), n, h, w, c, f, s, p, _stream()))
+    return y
+
+
+def avgpool2d_bwd(dy, shape, f, s, p, mask=None):
+    n, h, w, c = shape
+    dx = torch.empty(n, h, w, c, dtype=dy.dtype, device="cuda")
+    check(lib().tcb_avgpool2d_bwd(DT[dy.dtype], _p(dy), _p(mask), _p(dx), n, h, w, c, f, s, p, _stream()))
+    return dx
+
+
+def concat(xs):
+    """Channel concat of NHWC tensors via tcb_slice_copy (what the executor runs)."""
+    n, h, w = xs[0].shape[:3]
+    C = sum(x.shape[3] for x in xs)
+    y = torch.empty(n, h, w, C, dtype=xs[0].dtype, device="cuda")
+    off = 0
+    for x in xs:
+        c = x.shape[3]
+        check(lib().tcb_slice_copy(DT[x.dtype], _p(x), c, ctypes.c_void_p(y.data_ptr() + off * y.element_size()),
+                                   C, c, n * h * w, _stream()))
+        off += c
+    return y
 
 
 def avgpool_fwd(x):

@@ -3,7 +3,9 @@
 A model is a JSON-able dict: {"batch", "classes", "precision", "seed", "lr",
 "momentum", "weight_decay", "layers": [...]}; layers are in topological order
 and name their inputs. Ops: input, conv (fc layers are convs spanning the
-whole input map), maxpool, avgpool (global), loss (softmax cross-entropy).
+whole input map), maxpool, avgpool (global, or windowed with f/stride/pad),
+concat (channel concatenation of same-size tensors), loss (softmax
+cross-entropy).
 
 Configs follow BASELINE.json:
   C1 lenet        28x28x1, the CPU-oracle scale case
@@ -11,7 +13,10 @@ Configs follow BASELINE.json:
   C3 resnet50     224x224x3, torchvision v1.5 geometry (stride on the 3x3),
                   ResNet-50-shaped: conv/ReLU/residual topology exact, no BN
                   (the reference's network model has no normalisation layers)
-  C4 inception_v3 299x299x3 conv list (per-layer algorithm profiling)
+  C4 inception_v3 299x299x3, torchvision geometry without the aux head: the
+                  full branched graph (5b-7c modules, concat, avg/max pool
+                  branches), no BN; `inception_v3_convs` lists its convs for
+                  the per-layer algorithm profiling
   C5 vgg16        224x224x3, 13 convs + 25088/4096/4096/1000 classifier
 `from_net` builds a chain from the reference's `.net` format (conv/pool/fc),
 so the planner's network model and the executor share one description.
@@ -73,11 +78,27 @@ class _Builder:
         self.last = name
         return name
 
-    def avgpool(self):
-        name = self._name("gap")
-        _, _, c = self.shape[self.last]
-        self.layers.append({"name": name, "op": "avgpool", "in": self.last})
-        self.shape[name] = (1, 1, c)
+    def avgpool(self, f=None, stride=None, pad=0, src=None):
+        """Global average pool, or a windowed one (count_include_pad) with f."""
+        src = src or self.last
+        h, w, c = self.shape[src]
+        if f is None:
+            name = self._name("gap")
+            self.layers.append({"name": name, "op": "avgpool", "in": src})
+            self.shape[name] = (1, 1, c)
+        else:
+            stride = f if stride is None else stride
+            name = self._name("apool")
+            self.layers.append({"name": name, "op": "avgpool", "in": src, "f": f, "stride": stride, "pad": pad})
+            self.shape[name] = ((h + 2 * pad - f) // stride + 1, (w + 2 * pad - f) // stride + 1, c)
+        self.last = name
+        return name
+
+    def concat(self, srcs, name=None):
+        name = name or self._name("cat")
+        h, w, _ = self.shape[srcs[0]]
+        self.layers.append({"name": name, "op": "concat", "in": list(srcs)})
+        self.shape[name] = (h, w, sum(self.shape[x][2] for x in srcs))
         self.last = name
         return name
 
@@ -270,6 +291,82 @@ def inception_v3_convs(batch=128):
                  n=batch) for t in L]
 
 
+def inception_v3(batch=128, image=299, width=1.0, **opts):
+    """C4: Inception-v3 (torchvision geometry, no aux head, no BN) as a
+    branched graph — every module's branches, their channel concat, the 3x3
+    average-pool (stride 1, pad 1) and max-pool branches. `width` scales every
+    channel count (multiples of 8 kept) for small parity cases. Its convs in
+    graph order are `inception_v3_convs` (the planner's layer ids)."""
+    def ch(k):
+        return max(8, int(round(k * width / 8)) * 8)
+
+    b = _Builder(batch, image, image, 3, **opts)
+    b.conv(ch(32), 3, stride=2, name="Conv2d_1a_3x3")
+    b.conv(ch(32), 3, name="Conv2d_2a_3x3")
+    b.conv(ch(64), 3, pad=1, name="Conv2d_2b_3x3")
+    b.maxpool(3, 2)
+    b.conv(ch(80), 1, name="Conv2d_3b_1x1")
+    b.conv(ch(192), 3, name="Conv2d_4a_3x3")
+    x = b.maxpool(3, 2)
+    for i, pool_feat in enumerate((32, 64, 64)):  # Mixed_5b/5c/5d (35x35)
+        p = f"Mixed_5{'bcd'[i]}"
+        b1 = b.conv(ch(64), 1, src=x, name=p + "_b1x1")
+        b5 = b.conv(ch(48), 1, src=x, name=p + "_b5x5_1")
+        b5 = b.conv(ch(64), 5, pad=2, src=b5, name=p + "_b5x5_2")
+        b3 = b.conv(ch(64), 1, src=x, name=p + "_b3x3dbl_1")
+        b3 = b.conv(ch(96), 3, pad=1, src=b3, name=p + "_b3x3dbl_2")
+        b3 = b.conv(ch(96), 3, pad=1, src=b3, name=p + "_b3x3dbl_3")
+        bp = b.avgpool(3, 1, 1, src=x)
+        bp = b.conv(ch(pool_feat), 1, src=bp, name=p + "_bpool")
+        x = b.concat([b1, b5, b3, bp], name=p)
+    # Mixed_6a (35 -> 17)
+    b3 = b.conv(ch(384), 3, stride=2, src=x, name="Mixed_6a_b3x3")
+    bd = b.conv(ch(64), 1, src=x, name="Mixed_6a_dbl_1")
+    bd = b.conv(ch(96), 3, pad=1, src=bd, name="Mixed_6a_dbl_2")
+    bd = b.conv(ch(96), 3, stride=2, src=bd, name="Mixed_6a_dbl_3")
+    bp = b.maxpool(3, 2, src=x)
+    x = b.concat([b3, bd, bp], name="Mixed_6a")
+    for i, c7 in enumerate((128, 160, 160, 192)):  # Mixed_6b-6e (17x17)
+        p = f"Mixed_6{'bcde'[i]}"
+        b1 = b.conv(ch(192), 1, src=x, name=p + "_b1x1")
+        b7 = b.conv(ch(c7), 1, src=x, name=p + "_b7x7_1")
+        b7 = b.conv(ch(c7), 1, 7, pad=0, pad_w=3, src=b7, name=p + "_b7x7_2")
+        b7 = b.conv(ch(192), 7, 1, pad=3, pad_w=0, src=b7, name=p + "_b7x7_3")
+        bd = b.conv(ch(c7), 1, src=x, name=p + "_dbl_1")
+        bd = b.conv(ch(c7), 7, 1, pad=3, pad_w=0, src=bd, name=p + "_dbl_2")
+        bd = b.conv(ch(c7), 1, 7, pad=0, pad_w=3, src=bd, name=p + "_dbl_3")
+        bd = b.conv(ch(c7), 7, 1, pad=3, pad_w=0, src=bd, name=p + "_dbl_4")
+        bd = b.conv(ch(192), 1, 7, pad=0, pad_w=3, src=bd, name=p + "_dbl_5")
+        bp = b.avgpool(3, 1, 1, src=x)
+        bp = b.conv(ch(192), 1, src=bp, name=p + "_bpool")
+        x = b.concat([b1, b7, bd, bp], name=p)
+    # Mixed_7a (17 -> 8)
+    b3 = b.conv(ch(192), 1, src=x, name="Mixed_7a_b3x3_1")
+    b3 = b.conv(ch(320), 3, stride=2, src=b3, name="Mixed_7a_b3x3_2")
+    b7 = b.conv(ch(192), 1, src=x, name="Mixed_7a_b7x7x3_1")
+    b7 = b.conv(ch(192), 1, 7, pad=0, pad_w=3, src=b7, name="Mixed_7a_b7x7x3_2")
+    b7 = b.conv(ch(192), 7, 1, pad=3, pad_w=0, src=b7, name="Mixed_7a_b7x7x3_3")
+    b7 = b.conv(ch(192), 3, stride=2, src=b7, name="Mixed_7a_b7x7x3_4")
+    bp = b.maxpool(3, 2, src=x)
+    x = b.concat([b3, b7, bp], name="Mixed_7a")
+    for i in range(2):  # Mixed_7b / 7c (8x8)
+        p = f"Mixed_7{'bc'[i]}"
+        b1 = b.conv(ch(320), 1, src=x, name=p + "_b1x1")
+        t3 = b.conv(ch(384), 1, src=x, name=p + "_b3x3_1")
+        t3a = b.conv(ch(384), 1, 3, pad=0, pad_w=1, src=t3, name=p + "_b3x3_2a")
+        t3b = b.conv(ch(384), 3, 1, pad=1, pad_w=0, src=t3, name=p + "_b3x3_2b")
+        td = b.conv(ch(448), 1, src=x, name=p + "_dbl_1")
+        td = b.conv(ch(384), 3, pad=1, src=td, name=p + "_dbl_2")
+        tda = b.conv(ch(384), 1, 3, pad=0, pad_w=1, src=td, name=p + "_dbl_3a")
+        tdb = b.conv(ch(384), 3, 1, pad=1, pad_w=0, src=td, name=p + "_dbl_3b")
+        bp = b.avgpool(3, 1, 1, src=x)
+        bp = b.conv(ch(192), 1, src=bp, name=p + "_bpool")
+        x = b.concat([b1, t3a, t3b, tda, tdb, bp], name=p)
+    b.avgpool()
+    b.fc(b.cfg["classes"], relu=False, name="fc")
+    return b.done()
+
+
 def apply_selection(cfg: dict, assignment: dict) -> dict:
     """Set each feature conv's algorithm from a planner Selection.assignment
     ({layer_id (1-based over the feature convs, as the catalog indexes them):
@@ -286,7 +383,7 @@ def apply_selection(cfg: dict, assignment: dict) -> dict:
 
 
 CONFIGS = {"lenet": lenet, "alexnet": alexnet, "vgg16": vgg16, "resnet50": resnet50,
-           "tiny_resnet": tiny_resnet}
+           "tiny_resnet": tiny_resnet, "inception_v3": inception_v3}
 
 
 def build(name: str, **kw):
@@ -313,7 +410,15 @@ def conv_layers(cfg):
             f, s, p = L["f"], L["stride"], L["pad"]
             shapes[L["name"]] = ((h + 2 * p - f) // s + 1, (w + 2 * p - f) // s + 1, c)
         elif L["op"] == "avgpool":
-            shapes[L["name"]] = (1, 1, shapes[L["in"]][2])
+            h, w, c = shapes[L["in"]]
+            if "f" in L:
+                f, s, p = L["f"], L["stride"], L["pad"]
+                shapes[L["name"]] = ((h + 2 * p - f) // s + 1, (w + 2 * p - f) // s + 1, c)
+            else:
+                shapes[L["name"]] = (1, 1, c)
+        elif L["op"] == "concat":
+            h, w, _ = shapes[L["in"][0]]
+            shapes[L["name"]] = (h, w, sum(shapes[x][2] for x in L["in"]))
     return out
 
 

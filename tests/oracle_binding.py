@@ -40,6 +40,8 @@ class Oracle:
         L.oracle_maxpool_bwd.argtypes = [_f32p, _u8p, _f64p] + [ctypes.c_int] * 7
         L.oracle_avgpool_fwd.argtypes = [_f32p, _f64p] + [ctypes.c_int] * 3
         L.oracle_avgpool_bwd.argtypes = [_f32p, _f64p] + [ctypes.c_int] * 3
+        L.oracle_avgpool2d_fwd.argtypes = [_f32p, _f64p] + [ctypes.c_int] * 7
+        L.oracle_avgpool2d_bwd.argtypes = [_f32p, _f64p] + [ctypes.c_int] * 7
         L.oracle_softmax_xent.argtypes = [_f32p, _i32p, _f64p, ctypes.c_int, ctypes.c_int]
         L.oracle_softmax_xent.restype = ctypes.c_double
         L.oracle_sgd.argtypes = [_f32p, _f32p, _f32p, ctypes.c_size_t] + [ctypes.c_float] * 4
@@ -113,6 +115,17 @@ class Oracle:
     def avgpool_bwd(self, dy, n, hw, c):
         dx = np.empty(n * hw * c, np.float64)
         self.lib.oracle_avgpool_bwd(np.ascontiguousarray(dy, np.float32).ravel(), dx, n, hw, c)
+        return dx
+
+    def avgpool2d_fwd(self, x, n, h, w, c, f, s, p):
+        ho, wo = (h + 2 * p - f) // s + 1, (w + 2 * p - f) // s + 1
+        y = np.empty(n * ho * wo * c, np.float64)
+        self.lib.oracle_avgpool2d_fwd(np.ascontiguousarray(x, np.float32).ravel(), y, n, h, w, c, f, s, p)
+        return y
+
+    def avgpool2d_bwd(self, dy, n, h, w, c, f, s, p):
+        dx = np.empty(n * h * w * c, np.float64)
+        self.lib.oracle_avgpool2d_bwd(np.ascontiguousarray(dy, np.float32).ravel(), dx, n, h, w, c, f, s, p)
         return dx
 
     def softmax_xent(self, z, labels, n, classes):

@@ -2,7 +2,7 @@
 
 Walks the same model graph as the C++ executor (paper_1709_06622_b200/models.py
 config) with the C oracle ops (oracle/numerics.c, fp64 accumulation):
-forward (conv + bias + residual + ReLU, max/avg pools), softmax
+forward (conv + bias + residual + ReLU, max/avg pools, channel concat), softmax
 cross-entropy, backward (dgrad with residual-gradient fan-in and ReLU masks,
 wgrad + bias grads in the flat PS layout), then the momentum-SGD update of
 paper step 6. In bf16 mode every stored
@@ -128,7 +128,15 @@ class OracleStep:
             elif L["op"] == "avgpool":
                 xin = act[L["in"]]
                 n, h, w, c = xin.shape
-                y = self._st(o.avgpool_fwd(xin, n, h * w, c)).reshape(n, 1, 1, c)
+                if "pool" in L:
+                    f, s, p = L["pool"]
+                    y = self._st(o.avgpool2d_fwd(xin, n, h, w, c, f, s, p)).reshape(
+                        n, L["shape"][1], L["shape"][2], c)
+                else:
+                    y = self._st(o.avgpool_fwd(xin, n, h * w, c)).reshape(n, 1, 1, c)
+                act[i] = adopt("fwd", i, y, teacher.act(i) if teacher else None)
+            elif L["op"] == "concat":
+                y = np.concatenate([act[j] for j in L["ins"]], axis=-1)
                 act[i] = adopt("fwd", i, y, teacher.act(i) if teacher else None)
             elif L["op"] == "loss":
                 z = act[L["in"]]
@@ -174,8 +182,18 @@ class OracleStep:
             elif L["op"] == "avgpool":
                 xin = act[L["in"]]
                 n, h, w, c = xin.shape
-                dx = o.avgpool_bwd(gi.reshape(n, c), n, h * w, c).reshape(xin.shape)
-                contrib.setdefault(L["in"], []).append(dx)
+                if "pool" in L:
+                    f, s, p = L["pool"]
+                    dx = o.avgpool2d_bwd(gi, n, h, w, c, f, s, p).reshape(xin.shape)
+                else:
+                    dx = o.avgpool_bwd(gi.reshape(n, c), n, h * w, c).reshape(xin.shape)
+                if self.layers[L["in"]]["op"] != "input":
+                    contrib.setdefault(L["in"], []).append(dx)
+            elif L["op"] == "concat":
+                for j, off in zip(L["ins"], L["coff"]):
+                    if self.layers[j]["op"] != "input":
+                        cj = act[j].shape[-1]
+                        contrib.setdefault(j, []).append(gi[..., off:off + cj].astype(np.float64))
         self.loss, self.act, self.G, self.grads = loss, act, G, grads
         return loss
 

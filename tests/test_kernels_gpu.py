@@ -220,6 +220,38 @@ def test_maxpool_relu_ties_parity(oracle, dtype, pool):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("pool", [(3, 1, 1), (3, 2, 0), (2, 2, 1), (5, 3, 2)])
+def test_avgpool2d_parity(oracle, dtype, pool):
+    """Windowed average pool (Inception's branch pool, padding counted) and its
+    owner-computes backward, with and without the fused ReLU mask."""
+    dev = _dev()
+    bf = dtype == "bf16"
+    f, s, p = pool
+    n, h, w, c = 2, 11, 9, 24
+    x = _rand(oracle, (n, h, w, c), 21, 1.0, bf)
+    dt = torch.bfloat16 if bf else torch.float32
+    tol = TOL["bf16" if bf else "ffma"]
+    y = dev.avgpool2d_fwd(_to_dev(x, dt), f, s, p)
+    assert rel_err(_host(y), oracle.avgpool2d_fwd(x, n, h, w, c, f, s, p)) <= tol
+    ho, wo = y.shape[1], y.shape[2]
+    dy = _rand(oracle, (n, ho, wo, c), 22, 1.0, bf)
+    ref = oracle.avgpool2d_bwd(dy, n, h, w, c, f, s, p)
+    dx = dev.avgpool2d_bwd(_to_dev(dy, dt), (n, h, w, c), f, s, p)
+    assert rel_err(_host(dx), ref) <= tol
+    mask = _rand(oracle, (n, h, w, c), 23, 1.0, bf)
+    dxm = dev.avgpool2d_bwd(_to_dev(dy, dt), (n, h, w, c), f, s, p, mask=_to_dev(mask, dt))
+    assert rel_err(_host(dxm), np.where(mask.ravel() > 0, ref, 0.0)) <= tol
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_concat_slice_copy_bit_exact(dtype):
+    dev = _dev()
+    xs = [torch.randn(2, 5, 7, c, device="cuda").to(dtype) for c in (8, 24, 16, 3)]
+    got = dev.concat(xs)  # the last width (3) takes the scalar path
+    assert torch.equal(got, torch.cat(xs, dim=3))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_avgpool_and_softmax_parity(oracle, dtype):
     dev = _dev()
     bf = dtype == "bf16"

@@ -79,6 +79,21 @@ def test_maxpool_matches_torch_fp64(oracle, pool):
                                rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("pool", [(3, 1, 1), (3, 2, 0), (2, 2, 1)])
+def test_avgpool2d_matches_torch_fp64(oracle, pool):
+    f, s, p = pool
+    n, h, w, c = 2, 9, 8, 3
+    x = oracle.uniform(n * h * w * c, 13, 1)
+    ho, wo = (h + 2 * p - f) // s + 1, (w + 2 * p - f) // s + 1
+    dy = oracle.uniform(n * ho * wo * c, 13, 2)
+    X = _t(x, (n, h, w, c)).requires_grad_(True)
+    Y = F.avg_pool2d(X, f, s, p, count_include_pad=True)
+    np.testing.assert_allclose(oracle.avgpool2d_fwd(x, n, h, w, c, f, s, p), _nhwc(Y.detach()), rtol=1e-12)
+    Y.backward(_t(dy, (n, ho, wo, c)))
+    np.testing.assert_allclose(oracle.avgpool2d_bwd(dy, n, h, w, c, f, s, p), _nhwc(X.grad),
+                               rtol=1e-12, atol=1e-15)
+
+
 def test_avgpool_and_softmax_xent_match_torch_fp64(oracle):
     n, hw, c, classes = 3, 5, 8, 10
     x = oracle.uniform(n * hw * c, 11, 1)

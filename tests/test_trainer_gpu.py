@@ -101,6 +101,34 @@ def test_resnet50_geometry_step_tf32(oracle):
     assert lay["layers"][0]["shape"][3] == 4
 
 
+@pytest.mark.parametrize("prec", ["ffma", "bf16"])
+def test_inception_v3_step(oracle, prec):
+    """C4 graph (every Inception-v3 module: 1x1 / 5x5 / 3x3-double / 1x7-7x1 /
+    1x3-3x1 split branches, 3x3 average-pool and max-pool branches, channel
+    concat with fan-out gradients) at width 1/4, 75x75, batch 2."""
+    cfg = _models().inception_v3(batch=2, image=75, width=0.25, classes=10, precision=prec)
+    t, _ = _check(oracle, cfg)
+    ops = [L["op"] for L in t.describe()["layers"]]
+    assert ops.count("concat") == 11 and ops.count("conv") == 95
+
+
+def test_inception_v3_mixed_algorithms_step(oracle):
+    """The executor obeys a per-layer Selection on the C4 graph: FFT / Winograd
+    on stride-1 3x3 and 5x5 branch convs, GEMM elsewhere (bf16, layer-local)."""
+    m = _models()
+    cfg = m.inception_v3(batch=2, image=75, width=0.25, classes=10, precision="bf16")
+    names = [n for n, _ in m.conv_layers(cfg)]
+    sel = {}
+    for i, n in enumerate(names, 1):
+        if n.endswith("_b3x3dbl_2") or n == "Mixed_6a_dbl_2" or n.endswith("_dbl_2") and n.startswith("Mixed_7"):
+            sel[str(i)] = "winograd"
+        elif n.endswith("_b5x5_2"):
+            sel[str(i)] = "fft"
+    cfg = m.apply_selection(cfg, sel)
+    assert sum(L.get("algo") == "winograd" for L in cfg["layers"]) >= 5
+    _check(oracle, cfg)
+
+
 def test_explicit_im2col_stem_batch8(oracle):
     """Stem-only net at batch 8: explicit-im2col fwd (TMA epilogue) and wgrad
     (col kept from the forward pass) against the oracle, layer-local."""
