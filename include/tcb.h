@@ -184,6 +184,12 @@ int tcb_profile_catalog(const char* request_json, char** reply_out);
 typedef struct tcb_trainer tcb_trainer;
 
 int tcb_trainer_create(const char* config_json, tcb_trainer** out);
+/* The step's exact HBM layout for a model config, without a GPU or any
+ * allocation: JSON {"arena_bytes", "algorithm_workspace_bytes",
+ * "resident_bytes" (arena minus conv workspaces: activations, gradients,
+ * fan-in temporaries, parameters, momentum, staging), "param_padded", ...}
+ * (free with tcb_free). The planner's memory model for branched graphs. */
+int tcb_trainer_layout(const char* config_json, char** json_out);
 int tcb_trainer_destroy(tcb_trainer* t);
 /* NCCL unique id for rank 0 to broadcast (128 bytes). */
 int tcb_nccl_unique_id(uint8_t* id128);

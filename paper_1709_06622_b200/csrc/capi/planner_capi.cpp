@@ -261,6 +261,15 @@ J dispatch(const J& req) {
         out = plan_json(tc::plan_batch_size(network_of(req.at("network")), cat,
                                             req.at("gpu_bits").get<std::int64_t>(),
                                             req.at("dataset").get<std::int64_t>(), cands));
+    } else if (op == "plan_batch_size_graph") {
+        // branched networks: resident bits per candidate from the executor layout
+        const auto cat = catalog_of(req);
+        std::vector<std::pair<std::int64_t, std::int64_t>> res;
+        for (const auto& [k, v] : req.at("resident_bits").items())
+            res.emplace_back(std::stoll(k), v.get<std::int64_t>());
+        std::sort(res.begin(), res.end());
+        out = plan_json(tc::plan_batch_size_resident(cat, res, req.at("gpu_bits").get<std::int64_t>(),
+                                                     req.at("dataset").get<std::int64_t>()));
     } else if (op == "default_batch_candidates") {
         out["candidates"] = tc::default_batch_candidates(catalog_of(req));
     } else if (op == "model_caveats") {

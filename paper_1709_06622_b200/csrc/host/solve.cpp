@@ -299,11 +299,11 @@ constexpr const char* kClassifierCaveat =
     "classifier memory uses a fixed per-junction bias charge and batch-independent "
     "activations; treat classifier totals as approximate";
 
-BatchCandidateResult assess(const NetworkSpec& net, const AlgorithmCatalog& cat,
-                            std::int64_t gpu_bits, std::int64_t dataset, std::int64_t b) {
+BatchCandidateResult assess_bound(const AlgorithmCatalog& cat, std::int64_t dataset, std::int64_t b,
+                                  const MemoryBreakdown& breakdown) {
     BatchCandidateResult c;
     c.batch_size = b;
-    c.breakdown = memory_bound(gpu_bits, net, b);
+    c.breakdown = breakdown;
     const LayerOptions opts = catalog_options(cat, b);
     c.solve = solve_selection(opts, c.breakdown.bound);
     if (!c.solve.feasible()) return c;
@@ -321,7 +321,55 @@ BatchCandidateResult assess(const NetworkSpec& net, const AlgorithmCatalog& cat,
     return c;
 }
 
+BatchCandidateResult assess(const NetworkSpec& net, const AlgorithmCatalog& cat,
+                            std::int64_t gpu_bits, std::int64_t dataset, std::int64_t b) {
+    return assess_bound(cat, dataset, b, memory_bound(gpu_bits, net, b));
+}
+
+void recommend(BatchPlan& plan) {
+    for (const BatchCandidateResult& c : plan.candidates) {
+        if (!c.epoch_time_seconds) continue;
+        if (!plan.recommended) {
+            plan.recommended = c.batch_size;
+            continue;
+        }
+        const auto holder =
+            std::find_if(plan.candidates.begin(), plan.candidates.end(),
+                         [&](const BatchCandidateResult& x) { return x.batch_size == *plan.recommended; });
+        const double incumbent = *holder->epoch_time_seconds;
+        const double mine = *c.epoch_time_seconds;
+        if (mine < incumbent || (mine == incumbent && c.batch_size > *plan.recommended))
+            plan.recommended = c.batch_size;
+    }
+}
+
 }  // namespace
+
+BatchPlan plan_batch_size_resident(const AlgorithmCatalog& catalog,
+                                   const std::vector<std::pair<std::int64_t, std::int64_t>>& resident_bits,
+                                   std::int64_t gpu_total_bits, std::int64_t dataset_size) {
+    if (resident_bits.empty()) throw DomainError("candidate batch-size list must not be empty");
+    if (dataset_size < 1) throw DomainError("dataset size must be >= 1");
+    std::vector<std::future<BatchCandidateResult>> work;
+    for (const auto& [b, bits] : resident_bits) {
+        if (!catalog.has_batch_size(b))
+            throw CandidateNotInCatalogError("batch size " + std::to_string(b) +
+                                             " is not declared in the catalog");
+        if (bits < 0) throw DomainError("resident bits must be >= 0");
+        MemoryBreakdown m;
+        m.batch_size = b;
+        m.gpu_total = gpu_total_bits;
+        m.feature_maps = bits;
+        if (__builtin_sub_overflow(gpu_total_bits, bits, &m.bound))
+            throw OverflowError("integer overflow in memory arithmetic");
+        work.push_back(std::async(std::launch::async, assess_bound, std::cref(catalog), dataset_size, b, m));
+    }
+    BatchPlan plan;
+    for (auto& w : work) plan.candidates.push_back(w.get());
+    recommend(plan);
+    plan.advisories = advise_refinement(plan, NetworkSpec{});
+    return plan;
+}
 
 BatchPlan plan_batch_size(const NetworkSpec& network, const AlgorithmCatalog& catalog,
                           std::int64_t gpu_total_bits, std::int64_t dataset_size,
@@ -346,21 +394,7 @@ BatchPlan plan_batch_size(const NetworkSpec& network, const AlgorithmCatalog& ca
                                   std::cref(catalog), gpu_total_bits, dataset_size, b));
     BatchPlan plan;
     for (auto& w : work) plan.candidates.push_back(w.get());
-
-    for (const BatchCandidateResult& c : plan.candidates) {
-        if (!c.epoch_time_seconds) continue;
-        if (!plan.recommended) {
-            plan.recommended = c.batch_size;
-            continue;
-        }
-        const auto holder =
-            std::find_if(plan.candidates.begin(), plan.candidates.end(),
-                         [&](const BatchCandidateResult& x) { return x.batch_size == *plan.recommended; });
-        const double incumbent = *holder->epoch_time_seconds;
-        const double mine = *c.epoch_time_seconds;
-        if (mine < incumbent || (mine == incumbent && c.batch_size > *plan.recommended))
-            plan.recommended = c.batch_size;
-    }
+    recommend(plan);
     plan.advisories = advise_refinement(plan, network);
     return plan;
 }

@@ -306,6 +306,15 @@ BatchPlan plan_batch_size(const NetworkSpec& network, const AlgorithmCatalog& ca
                           std::int64_t gpu_total_bits, std::int64_t dataset_size,
                           const std::vector<std::int64_t>& candidates);
 std::vector<Advisory> advise_refinement(const BatchPlan& plan, const NetworkSpec& network);
+// Branched networks (ResNet / Inception): no chain memory model
+// (Eq 2-5) applies, so the caller supplies each candidate's resident bits —
+// the executor's exact HBM layout without the conv workspaces
+// (tcb_trainer_layout) — and the workspace bound is gpu_total_bits minus
+// them. Selection, epoch time, the recommendation rule and the advisories
+// are those of plan_batch_size. Breakdown: feature_maps = resident bits.
+BatchPlan plan_batch_size_resident(const AlgorithmCatalog& catalog,
+                                   const std::vector<std::pair<std::int64_t, std::int64_t>>& resident_bits,
+                                   std::int64_t gpu_total_bits, std::int64_t dataset_size);
 std::vector<std::string> model_caveats();
 
 // ---------------------------------------------------------------------------

@@ -110,6 +110,7 @@ struct tcb_trainer {
     // arena
     void* arena = nullptr;
     size_t arena_bytes = 0;
+    size_t algorithm_ws_bytes = 0;  // conv workspaces inside the arena (depend on the algorithms)
     size_t off_param = 0, off_grad = 0, off_mom = 0, off_wc = 0, off_ws = 0, off_colsum = 0;
     size_t off_labels = 0, off_loss = 0, off_input_f32 = 0;
     // staged host batches (pipelined H2D): two slots filled on a copy stream,
@@ -441,7 +442,9 @@ void plan_params(tcb_trainer* t) {
     }
 }
 
-int allocate(tcb_trainer* t) {
+// dry: lay the arena out (offsets, arena_bytes, algorithm_ws_bytes) without
+// allocating — the exact HBM need of the step for the planner (tcb_trainer_layout)
+int allocate(tcb_trainer* t, bool dry = false) {
     const size_t es = dtype_size(t->dt);
     Bump b;
     plan_params(t);
@@ -459,9 +462,12 @@ int allocate(tcb_trainer* t) {
         if (nd.op == Op::Conv) {
             nd.narrow = t->bf16 && nd.algo_id == TCB_ALGO_GEMM && conv_tc_narrow(nd.g);
             if (nd.algo_id == TCB_ALGO_GEMM) {
-                if (nd.narrow)
-                    nd.nws = b.take(std::max(conv_tc_workspace(nd.g, ConvMode::Wgrad),
-                                             conv_tc_workspace(nd.g, ConvMode::Fwd)));
+                if (nd.narrow) {
+                    const size_t nb = std::max(conv_tc_workspace(nd.g, ConvMode::Wgrad),
+                                               conv_tc_workspace(nd.g, ConvMode::Fwd));
+                    nd.nws = b.take(nb);
+                    t->algorithm_ws_bytes += round_up(std::max<size_t>(nb, 1), kAlign);
+                }
                 else
                     ws = std::max(ws, t->bf16   ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
                                       : t->tf32 ? conv_tf32_workspace(nd.g, ConvMode::Wgrad)
@@ -498,6 +504,8 @@ int allocate(tcb_trainer* t) {
         t->off_stage_labels[k] = b.take(size_t(t->batch) * 4);
     }
     t->arena_bytes = b.top;
+    t->algorithm_ws_bytes += round_up(std::max<size_t>(ws, 1), kAlign);
+    if (dry) return TCB_OK;
     cudaError_t e = cudaMalloc(&t->arena, t->arena_bytes);
     if (e != cudaSuccess)
         return fail(TCB_ERR_OOM, "arena of " + std::to_string(t->arena_bytes) + " bytes: " +
@@ -1000,6 +1008,32 @@ TCB_API int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t*
             TRY_CUDA(cudaEventCreateWithFlags(&t->ev_comm_done, cudaEventDisableTiming));
         }
     }
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_layout(const char* config_json, char** json_out) {
+    if (!config_json || !json_out) return fail(TCB_ERR_INVALID, "NULL argument");
+    auto t = std::make_unique<tcb_trainer>();
+    try {
+        t->cfg = json::parse(config_json);
+        TRY(build_graph(t.get()));
+        TRY(allocate(t.get(), /*dry=*/true));
+    } catch (const std::exception& e) {
+        return fail(TCB_ERR_INVALID, std::string("model config: ") + e.what());
+    }
+    json d;
+    d["arena_bytes"] = t->arena_bytes;
+    d["algorithm_workspace_bytes"] = t->algorithm_ws_bytes;
+    d["resident_bytes"] = t->arena_bytes - t->algorithm_ws_bytes;
+    d["param_padded"] = t->param_padded;
+    d["param_count"] = t->param_count;
+    d["batch"] = t->batch;
+    int convs = 0;
+    for (const Node& nd : t->nodes) convs += nd.op == Op::Conv;
+    d["conv_layers"] = convs;
+    const std::string out = d.dump();
+    *json_out = static_cast<char*>(std::malloc(out.size() + 1));
+    std::memcpy(*json_out, out.c_str(), out.size() + 1);
     return TCB_OK;
 }
 

@@ -79,3 +79,32 @@ def plan(net: str, catalog_csv: str, gpu_bits: int, dataset: int, candidates=Non
     if candidates:
         req["candidates"] = list(candidates)
     return p.call("plan_batch_size", **req)
+
+
+def layout(cfg: dict) -> dict:
+    """The executor's exact HBM layout of `cfg` (no GPU, no allocation):
+    arena / algorithm-workspace / resident bytes (tcb_trainer_layout)."""
+    import ctypes
+    import json
+
+    from . import device
+    L = device.lib()
+    L.tcb_trainer_layout.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p)]
+    L.tcb_free.argtypes = [ctypes.c_void_p]
+    out = ctypes.c_char_p()
+    device.check(L.tcb_trainer_layout(json.dumps(cfg).encode(), ctypes.byref(out)))
+    d = json.loads(out.value.decode())
+    L.tcb_free(ctypes.cast(out, ctypes.c_void_p))
+    return d
+
+
+def plan_graph(build, catalog_csv: str, batches, gpu_bits: int, dataset: int, planner_handle=None) -> dict:
+    """Mini-batch + per-layer algorithm plan for a branched network (ResNet,
+    Inception): `build(batch) -> cfg`; each candidate's
+    workspace bound is gpu_bits minus the executor's resident bits at that
+    batch (its exact layout without conv workspaces), then the reference's
+    selection / epoch-time / recommendation rules (plan_batch_size_resident)."""
+    p = planner_handle or planner.default()
+    resident = {str(b): layout(build(b))["resident_bytes"] * 8 for b in batches}
+    return p.call("plan_batch_size_graph", catalog=catalog_csv, resident_bits=resident, gpu_bits=gpu_bits,
+                  dataset=dataset)

@@ -18,18 +18,23 @@ def _up(v, a):
     return (v + a - 1) // a * a
 
 
+def _pad(cfg):
+    # tensor-core layouts pad channels to 16-byte rows: 8 bf16 / 4 fp32 (tf32)
+    return {"bf16": 8, "tf32": 4}.get(cfg.get("precision", "bf16"), 1)
+
+
 def layout(cfg: dict, world: int) -> dict:
-    bf16 = cfg.get("precision", "bf16") == "bf16"
+    pad = _pad(cfg)
     ch = {}
     layers = []
     off = 0
     logical = 0
     for L in cfg["layers"]:
         if L["op"] == "input":
-            ch[L["name"]] = (_up(L["c"], 8) if bf16 else L["c"], L["c"])
+            ch[L["name"]] = (_up(L["c"], pad), L["c"])
         elif L["op"] == "conv":
             c_alloc, c_log = ch[L["in"]]
-            k_alloc = _up(L["k"], 8) if bf16 else L["k"]
+            k_alloc = _up(L["k"], pad)
             ch[L["name"]] = (k_alloc, L["k"])
             wcount = k_alloc * L["r"] * L["s"] * c_alloc
             entry = {"name": L["name"], "woff": off, "wcount": wcount, "boff": None}
@@ -42,6 +47,8 @@ def layout(cfg: dict, world: int) -> dict:
             layers.append(entry)
         elif L["op"] in ("maxpool", "avgpool"):
             ch[L["name"]] = ch[L["in"]]
+        elif L["op"] == "concat":
+            ch[L["name"]] = (sum(ch[x][0] for x in L["in"]), sum(ch[x][1] for x in L["in"]))
     padded = _up(max(off, 1), world * ALIGN)
     shard = padded // world
     for e in layers:
@@ -51,10 +58,9 @@ def layout(cfg: dict, world: int) -> dict:
 
 
 def _k_of(entry, cfg):
-    bf16 = cfg.get("precision", "bf16") == "bf16"
     for L in cfg["layers"]:
         if L.get("name") == entry["name"]:
-            return _up(L["k"], 8) if bf16 else L["k"]
+            return _up(L["k"], _pad(cfg))
     raise KeyError(entry["name"])
 
 

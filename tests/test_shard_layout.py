@@ -12,7 +12,7 @@ import pytest
 import shard_oracle
 
 MODELS = [("lenet", dict(batch=64)), ("alexnet", dict(batch=8)), ("vgg16", dict(batch=2)),
-          ("resnet50", dict(batch=2)), ("tiny_resnet", dict(batch=2))]
+          ("resnet50", dict(batch=2)), ("tiny_resnet", dict(batch=2)), ("inception_v3", dict(batch=2))]
 
 
 def _describe(cfg):
@@ -27,7 +27,7 @@ def _describe(cfg):
     return d
 
 
-@pytest.mark.parametrize("precision", ["bf16", "ffma"])
+@pytest.mark.parametrize("precision", ["bf16", "tf32", "ffma"])
 @pytest.mark.parametrize("model,kw", MODELS, ids=[m for m, _ in MODELS])
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
 def test_layout_matches_restatement(model, kw, precision, world):
@@ -58,6 +58,9 @@ def test_true_parameter_counts():
     assert counts["alexnet"] == 62_378_344         # ungrouped AlexNet, fc 9216 first
     assert counts["resnet50"] == 25_503_912        # torchvision ResNet-50 minus 53,120 BN params
     assert counts["lenet"] == 431_080
+    # torchvision Inception-v3 without the aux head (23,834,568) minus its BN
+    # affine parameters: 2 per conv output channel, sum of k over the 94 convs = 17,216
+    assert _describe(models.build("inception_v3", batch=2, precision="ffma"))["param_count"] == 23_834_568 - 34_432
 
 
 def _gloo_rank(rank, world, port, q):
