@@ -76,6 +76,12 @@ struct Node {
     std::vector<int> compute_from;      // consumers with a computed contribution
     std::vector<int> alias_from;        // consumers whose G[out] adds via the residual path
     std::map<int, size_t> tmp;          // consumer -> temp buffer offset (non-final computed)
+    // non-final GEMM-conv consumers accumulate into one buffer through their
+    // dgrad epilogue's residual input (in place), instead of a temp each plus
+    // separate add passes at the final writer (Inception's 3-4 way fan-out)
+    std::vector<int> chain;
+    size_t acc = 0;
+    int acc_written = 0;                // per step
     int grad_alias = -1;                // G[this] is G[grad_alias] (no copy)
 };
 
@@ -483,9 +489,19 @@ int allocate(tcb_trainer* t, bool dry = false) {
             if (nd.bias) colsum = std::max(colsum, column_sum_workspace(nd.n * nd.h * nd.w, nd.g.k));
         }
     }
-    for (Node& nd : t->nodes)
-        for (int c : nd.compute_from)
-            if (c != nd.final_writer) nd.tmp[c] = b.take(size_t(nd.n) * nd.h * nd.w * nd.c * es);
+    for (Node& nd : t->nodes) {
+        nd.chain.clear();
+        nd.tmp.clear();
+        for (int c : nd.compute_from) {
+            if (c == nd.final_writer) continue;
+            const Node& con = t->nodes[c];
+            if (con.op == Op::Conv && con.algo_id == TCB_ALGO_GEMM)
+                nd.chain.push_back(c);
+            else
+                nd.tmp[c] = b.take(size_t(nd.n) * nd.h * nd.w * nd.c * es);
+        }
+        if (!nd.chain.empty()) nd.acc = b.take(size_t(nd.n) * nd.h * nd.w * nd.c * es);
+    }
     for (int i = static_cast<int>(t->nodes.size()) - 1; i >= 0; --i)
         if (t->nodes[i].grad_alias >= 0) t->nodes[i].grad = t->nodes[t->nodes[i].grad_alias].grad;
     t->ws_bytes = ws;
@@ -660,16 +676,21 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
     const Node& con = t->nodes[ci];
     const bool final = tgt.final_writer == ci;
     const size_t elems = size_t(tgt.n) * tgt.h * tgt.w * tgt.c;
-    void* out = final ? t->at(tgt.grad) : t->at(tgt.tmp.at(ci));
+    const bool chained = !final && std::find(tgt.chain.begin(), tgt.chain.end(), ci) != tgt.chain.end();
+    void* out = final ? t->at(tgt.grad) : chained ? t->at(tgt.acc) : t->at(tgt.tmp.at(ci));
     const Node* producer = &tgt;
     const bool mask_needed = final && producer->op == Op::Conv && producer->relu;
 
-    // extra contributions to fold in (only at the final writer)
+    // extra contributions to fold in: at the final writer every other one; a
+    // chained contribution adds the running sum of the chain (in place)
     std::vector<const void*> extras;
     if (final) {
-        for (int c : tgt.compute_from)
-            if (c != ci) extras.push_back(t->at(tgt.tmp.at(c)));
+        if (!tgt.chain.empty()) extras.push_back(t->at(tgt.acc));
+        for (const auto& [c, off] : tgt.tmp)
+            if (c != ci) extras.push_back(t->at(off));
         for (int a : tgt.alias_from) extras.push_back(t->at(t->nodes[a].grad));
+    } else if (chained) {
+        if (tgt.acc_written++ > 0) extras.push_back(t->at(tgt.acc));
     }
     if (con.op == Op::Conv) {
         // combine extras into one residual operand for the dgrad epilogue
@@ -763,6 +784,7 @@ int issue_ready_shards(tcb_trainer* t, int i, cudaStream_t st) {
 
 int backward(tcb_trainer* t, cudaStream_t st) {
     TRY(refresh_transposes(t, st));
+    for (Node& nd : t->nodes) nd.acc_written = 0;
     // overlapped shard reduces run on comm_bg_ctas SMs: keep them free
     conv_tc_set_sm_reserve(t->overlap_active() ? t->comm_bg_ctas : 0);
     struct Reset {
