@@ -294,6 +294,8 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
     # per-pass roofline time max(FLOP / tensor peak, bytes / HBM peak), summed
     hbm = pk.get("hbm_gbs", 6548.2)
     bound_ms, tensor_ms, hbm_ms, nbytes = 0.0, 0.0, 0.0, 0.0
+    # passes split by their own roofline bound (arithmetic intensity vs ridge)
+    split = {"tensor": [0, 0.0, 0.0, 0.0], "hbm": [0, 0.0, 0.0, 0.0]}  # count, flop, bytes, ms
     for r in rows:
         for pname in ("fwd", "dgrad", "wgrad"):
             if r.get(pname + "_ms") is None:
@@ -304,6 +306,11 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
             tensor_ms += tf
             hbm_ms += tb
             nbytes += r.get(pname + "_bytes", 0)
+            sp = split["tensor" if tf >= tb else "hbm"]
+            sp[0] += 1
+            sp[1] += r["flop"]
+            sp[2] += r.get(pname + "_bytes", 0)
+            sp[3] += r[pname + "_ms"]
     traffic, tsrc = None, None
     tpath = os.path.join(ROOT, "profiles", f"r01_conv_traffic_{model}_bs{batch}.json")
     if os.path.exists(tpath):
@@ -324,6 +331,14 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
                 "hbm_only_ms": round(hbm_ms, 3), "measured_ms": round(ms, 3),
                 "frac": round(bound_ms / ms, 4),
                 "note": "sum over conv passes of max(FLOP/tensor peak, algorithmic bytes/HBM peak)"},
+            "tensor_bound_passes": {
+                "count": split["tensor"][0], "ms": round(split["tensor"][3], 3),
+                "achieved_TFLOPs": round(split["tensor"][1] / max(split["tensor"][3], 1e-9) / 1e9, 1),
+                "frac_of_tensor_peak": round(split["tensor"][1] / max(split["tensor"][3], 1e-9) / 1e9 / peak, 4)},
+            "hbm_bound_passes": {
+                "count": split["hbm"][0], "ms": round(split["hbm"][3], 3),
+                "achieved_GBps": round(split["hbm"][2] / max(split["hbm"][3], 1e-9) / 1e6, 1),
+                "frac_of_hbm_peak": round(split["hbm"][2] / max(split["hbm"][3], 1e-9) / 1e6 / hbm, 4)},
             "peak_kind": f"bf16 dense sustained ({pk['source']}; kernel timed inside the step)"}
 
 
