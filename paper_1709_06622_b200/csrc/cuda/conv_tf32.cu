@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "tma.cuh"
 
 namespace tcb {
 namespace {
@@ -45,6 +46,8 @@ struct Cfg {
 };
 
 struct Params {
+    CUtensorMap tmap_a, tmap_b;  // TMA operand paths (one producer thread)
+    int load;                    // kGather / kPlain / kIm2col
     ConvShape s;
     const float* a;  // fwd: x   dgrad: dy   wgrad: dy
     const float* b;  // fwd/dgrad: w   wgrad: x
@@ -63,6 +66,11 @@ struct Params {
     FastDiv d_hwq, d_wq, d_ts;
 };
 
+// Operand loads: kGather = cp.async by 128 threads (any C, K % 4 == 0);
+// kPlain = 1x1/s1/p0, every operand a plain matrix by 2-D TMA; kIm2col = the
+// activation operand by im2col-mode TMA (one tap x 32 channels per k-block).
+constexpr int kGather = 0, kPlain = 1, kIm2col = 2;
+
 // K-major rows (SWIZZLE_128B): 16-byte chunk j of row r lands at j ^ (r & 7).
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
     return row * 128u + ((chunk ^ (row & 7u)) << 4);
@@ -72,7 +80,7 @@ __device__ __forceinline__ uint32_t swz_mn(uint32_t row, uint32_t chunk) {
     return row * 128u + ((chunk ^ ((row & 3u) << 1)) << 4);
 }
 
-template <ConvMode MODE, int BN>
+template <ConvMode MODE, int BN, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2) conv_tf32_kernel(const __grid_constant__ Params p) {
     using C = Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -97,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tf32_kernel(const __grid_con
 
     if (tid == 0) {
         for (int i = 0; i < C::kStages; ++i) {
-            ptx::mbar_init(&full[i], kProducerThreads);
+            ptx::mbar_init(&full[i], TMA ? 1 : kProducerThreads);
             ptx::mbar_init(&empty[i], 1);
         }
         ptx::mbar_init(accfull, 1);
@@ -110,7 +118,97 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tf32_kernel(const __grid_con
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t smem_base = ptx::smem_addr(smem);
 
-    if (warp < 4) {
+    if (warp < 4 && TMA) {
+        // =========================================== TMA producer (1 thread) ======
+        if (tid == 0 && has_k) {
+            int bn = 0, bh = 0, bw = 0;  // im2col base of the tile's first GEMM row (fwd / dgrad)
+            if (MODE != ConvMode::Wgrad && p.load == kIm2col) {
+                uint32_t n, rem, a, b;
+                const uint32_t m0 = static_cast<uint32_t>(mt * BM);
+                if constexpr (MODE == ConvMode::Fwd) {
+                    s.d_howo.divmod(m0, n, rem);
+                    s.d_wo.divmod(rem, a, b);
+                    bh = static_cast<int>(a) * s.sh - s.ph;
+                    bw = static_cast<int>(b) * s.sw - s.pw;
+                } else {
+                    p.d_hwq.divmod(m0, n, rem);
+                    p.d_wq.divmod(rem, a, b);
+                    bh = static_cast<int>(a) + p.ph.bh - (p.ph.tr - 1);
+                    bw = static_cast<int>(b) + p.ph.bw - (p.ph.ts - 1);
+                }
+                bn = static_cast<int>(n);
+            }
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = kb_begin; kb < kb_end; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t a_smem = smem_base + stage * C::kStageBytes;
+                const uint32_t b_smem = a_smem + C::kABytes;
+                uint64_t* bar = &full[stage];
+                ptx::mbar_arrive_expect_tx(bar, C::kStageBytes);
+                const int kk0 = kb * BKE;
+                if constexpr (MODE == ConvMode::Fwd) {
+                    if (p.load == kPlain) {
+                        ptx::tma_load_2d(a_smem, &p.tmap_a, bar, kk0, mt * BM);
+                    } else {
+                        uint32_t tap, c0, r, sx;
+                        s.d_c.divmod(static_cast<uint32_t>(kk0), tap, c0);
+                        s.d_s.divmod(tap, r, sx);
+                        ptx::tma_load_im2col_4d(a_smem, &p.tmap_a, bar, static_cast<int>(c0), bw, bh, bn,
+                                                static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+                    }
+                    ptx::tma_load_2d(b_smem, &p.tmap_b, bar, kk0, nt * BN);
+                } else if constexpr (MODE == ConvMode::Dgrad) {
+                    // k-block = 32 filters k0.. of one phase tap; im2col offsets count the
+                    // tap from the far corner (ho = base + r'), i.e. ti = tr - 1 - r'
+                    uint32_t t, k0, rr, ss;
+                    s.d_k.divmod(static_cast<uint32_t>(kk0), t, k0);
+                    p.d_ts.divmod(t, rr, ss);
+                    if (p.load == kPlain)
+                        ptx::tma_load_2d(a_smem, &p.tmap_a, bar, static_cast<int>(k0), mt * BM);
+                    else
+                        ptx::tma_load_im2col_4d(a_smem, &p.tmap_a, bar, static_cast<int>(k0), bw, bh, bn,
+                                                static_cast<uint16_t>(ss), static_cast<uint16_t>(rr));
+                    const int rf = p.ph.r0 + (p.ph.tr - 1 - static_cast<int>(rr)) * s.sh;
+                    const int sf = p.ph.s0 + (p.ph.ts - 1 - static_cast<int>(ss)) * s.sw;
+#pragma unroll
+                    for (int j = 0; j < BN / 32; ++j)
+                        ptx::tma_load_3d(b_smem + j * kMnBlock, &p.tmap_b, bar, nt * BN + j * 32, rf * s.S + sf,
+                                         static_cast<int>(k0));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BM / 32; ++j)
+                        ptx::tma_load_2d(a_smem + j * kMnBlock, &p.tmap_a, bar, mt * BM + j * 32, kk0);
+                    if (p.load == kPlain) {
+#pragma unroll
+                        for (int j = 0; j < BN / 32; ++j)
+                            ptx::tma_load_2d(b_smem + j * kMnBlock, &p.tmap_b, bar, nt * BN + j * 32, kk0);
+                    } else {
+                        uint32_t n, rem, ho, wo;
+                        s.d_howo.divmod(static_cast<uint32_t>(kk0), n, rem);
+                        s.d_wo.divmod(rem, ho, wo);
+                        const int ph = static_cast<int>(ho) * s.sh - s.ph, pw = static_cast<int>(wo) * s.sw - s.pw;
+#pragma unroll
+                        for (int j = 0; j < BN / 32; ++j) {
+                            int col0 = nt * BN + j * 32;
+                            if (col0 >= s.Ncol) col0 = 0;  // padding columns: never stored
+                            uint32_t tap, c0, r, sx;
+                            s.d_c.divmod(static_cast<uint32_t>(col0), tap, c0);
+                            s.d_s.divmod(tap, r, sx);
+                            ptx::tma_load_im2col_4d(b_smem + j * kMnBlock, &p.tmap_b, bar, static_cast<int>(c0), pw,
+                                                    ph, static_cast<int>(n), static_cast<uint16_t>(sx),
+                                                    static_cast<uint16_t>(r));
+                        }
+                    }
+                }
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+    if (warp < 4 && !TMA) {
         // ================================================ producers ======
         constexpr int kCpr = BN / 4;                      // 16-B chunks per MN-major B row
         constexpr int kRowsPerPass = kProducerThreads / kCpr;
@@ -274,7 +372,8 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tf32_kernel(const __grid_con
             }
         }
         ptx::cp_async_wait<0>();
-
+    }
+    if (warp < 4) {
         // ================================================= epilogue ======
         // Thread = TMEM lane = tile row. Each 32-column chunk is staged through a
         // warp-private 32x32 fp32 smem tile (the drained operand ring) and
@@ -360,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tf32_kernel(const __grid_con
                 *reinterpret_cast<float4*>(p.out + rows[q] + col) = x;
             }
         }
-    } else {
+    } else if (warp == kMmaWarp) {
         // =============================================== MMA issuer ======
         constexpr uint32_t kAmn = MODE == ConvMode::Wgrad ? 1u : 0u;
         constexpr uint32_t kBmn = MODE == ConvMode::Fwd ? 0u : 1u;
@@ -423,9 +522,9 @@ Plan make_plan(const ConvShape& s, ConvMode mode) {
     return pl;
 }
 
-template <ConvMode MODE, int BN>
+template <ConvMode MODE, int BN, bool TMA>
 cudaError_t launch(const Params& p, int grid, cudaStream_t st) {
-    auto kern = conv_tf32_kernel<MODE, BN>;
+    auto kern = conv_tf32_kernel<MODE, BN, TMA>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -437,6 +536,59 @@ cudaError_t launch(const Params& p, int grid, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// $TCB_TF32_GATHER=1 / conv_tf32_set_force_gather: always the cp.async gather operands
+int g_force_gather = [] {
+    const char* e = getenv("TCB_TF32_GATHER");
+    return e && e[0] == '1' ? 1 : 0;
+}();
+bool force_gather() { return g_force_gather != 0; }
+
+bool plain_geometry(const ConvShape& s) {
+    return s.R == 1 && s.S == 1 && s.ph == 0 && s.pw == 0 && s.sh == 1 && s.sw == 1;
+}
+
+// im2col TMA: whole 32-channel slices of one tap per k-block, small corners
+bool im2col_geometry(const ConvShape& s, int channels) {
+    return channels % BKE == 0 && s.R <= 16 && s.S <= 16 && s.ph <= 15 && s.pw <= 15;
+}
+
+template <ConvMode MODE>
+int pick_load(const ConvShape& s) {
+    if (force_gather()) return kGather;
+    if (MODE == ConvMode::Dgrad && s.K % BKE != 0) return kGather;  // k-blocks within one tap
+    if (plain_geometry(s)) return kPlain;
+    return im2col_geometry(s, MODE == ConvMode::Dgrad ? s.K : s.C) ? kIm2col : kGather;
+}
+
+template <ConvMode MODE>
+bool build_maps(Params& p, int bn) {
+    const ConvShape& s = p.s;
+    const auto k_major = CU_TENSOR_MAP_SWIZZLE_128B, mn_major = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    if constexpr (MODE == ConvMode::Fwd) {
+        const bool a = p.load == kPlain
+                           ? make_tmap_f32_2d(&p.tmap_a, p.a, s.M, s.C, BM, k_major)
+                           : make_tmap_im2col_f32(&p.tmap_a, p.a, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
+                                                  s.pw - (s.S - 1), s.ph - (s.R - 1), s.sw, s.sh, BM, k_major);
+        return a && make_tmap_f32_2d(&p.tmap_b, p.b, s.Ncol, s.Kdim, bn, k_major);
+    } else if constexpr (MODE == ConvMode::Dgrad) {
+        bool a;
+        if (p.load == kPlain) {
+            a = make_tmap_f32_2d(&p.tmap_a, p.a, s.M, s.K, BM, k_major);
+        } else {
+            const int lw = p.ph.bw - (p.ph.ts - 1), lh = p.ph.bh - (p.ph.tr - 1);
+            a = make_tmap_im2col_f32(&p.tmap_a, p.a, s.N, s.Ho, s.Wo, s.K, lw, lh, lw + p.ph.Wq - s.Wo,
+                                     lh + p.ph.Hq - s.Ho, 1, 1, BM, k_major);
+        }
+        return a && make_tmap_filters_f32(&p.tmap_b, p.b, s.K, size_t(s.R) * s.S, s.C);
+    } else {
+        const bool a = make_tmap_f32_2d(&p.tmap_a, p.a, s.Kdim, s.K, BKE, mn_major);
+        return a && (p.load == kPlain
+                         ? make_tmap_f32_2d(&p.tmap_b, p.b, s.Kdim, s.C, BKE, mn_major)
+                         : make_tmap_im2col_f32(&p.tmap_b, p.b, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
+                                                s.pw - (s.S - 1), s.ph - (s.R - 1), s.sw, s.sh, BKE, mn_major));
+    }
+}
+
 template <ConvMode MODE>
 cudaError_t run(Params p, const Plan& pl, cudaStream_t st) {
     p.m_tiles = pl.m_tiles;
@@ -444,10 +596,16 @@ cudaError_t run(Params p, const Plan& pl, cudaStream_t st) {
     p.kb_total = pl.kb_total;
     p.kb_per_split = pl.kb_per_split;
     const int grid = pl.m_tiles * pl.n_tiles * pl.splits;
-    return pl.bn == 64 ? launch<MODE, 64>(p, grid, st) : launch<MODE, 128>(p, grid, st);
+    p.load = p.s.Kdim > 0 ? pick_load<MODE>(p.s) : kGather;
+    if (p.load != kGather && !build_maps<MODE>(p, pl.bn)) return cudaErrorInvalidValue;
+    if (p.load != kGather)
+        return pl.bn == 64 ? launch<MODE, 64, true>(p, grid, st) : launch<MODE, 128, true>(p, grid, st);
+    return pl.bn == 64 ? launch<MODE, 64, false>(p, grid, st) : launch<MODE, 128, false>(p, grid, st);
 }
 
 }  // namespace
+
+void conv_tf32_set_force_gather(int on) { g_force_gather = on ? 1 : 0; }
 
 bool conv_tf32_supported(const ConvGeom& g) {
     return g.c % 4 == 0 && g.k % 4 == 0 && g.c > 0 && g.k > 0;

@@ -82,6 +82,9 @@ cudaError_t conv_ffma_wgrad(const ConvGeom& g, const float* dy, const float* x, 
 // ---- TF32 tensor-core implicit GEMM (tcgen05 kind::tf32; fp32 storage) ----
 // Requirements: C % 4 == 0 and K % 4 == 0 (16-byte fp32 chunks).
 bool conv_tf32_supported(const ConvGeom& g);
+// 1: always the cp.async gather operands; 0: 2-D / im2col TMA where the geometry
+// allows (also $TCB_TF32_GATHER=1)
+void conv_tf32_set_force_gather(int on);
 size_t conv_tf32_workspace(const ConvGeom& g, ConvMode mode);
 cudaError_t conv_tf32_fwd(const ConvGeom& g, const float* x, const float* w, const Epilogue& ep,
                           float* y, cudaStream_t st);

@@ -380,6 +380,7 @@ TCB_API int tcb_set_conv_operand_path(int mode) {
     if (mode < 0 || mode > 2)
         return fail(TCB_ERR_INVALID, "mode must be 0 (auto), 1 (gather) or 2 (register epilogue)");
     conv_tc_set_force_gather(mode == 1);
+    conv_tf32_set_force_gather(mode == 1);
     conv_tc_set_epi_kb(mode == 2 ? 0 : -1);
     return TCB_OK;
 }

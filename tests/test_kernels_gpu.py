@@ -82,10 +82,10 @@ def _host(t):
 
 @pytest.fixture(params=["auto", "gather", "regepi"])
 def operand_path(request):
-    """auto = 2-D TMA (1x1/s1) or im2col-mode TMA (channels % 64 == 0) where they
-    apply, TMA epilogue on K-light layers; gather = force the cp.async gather
-    path; regepi = auto loads with the register epilogue everywhere. All must
-    agree with the oracle."""
+    """auto = 2-D TMA (1x1/s1) or im2col-mode TMA (channels % 64 == 0 for bf16,
+    % 32 for tf32) where they apply, TMA epilogue on K-light layers; gather =
+    force the cp.async gather path (bf16 and tf32); regepi = auto loads with the
+    register epilogue everywhere (bf16). All must agree with the oracle."""
     import ctypes
     lib = _dev().lib()
     lib.tcb_set_conv_operand_path.argtypes = [ctypes.c_int]
@@ -99,8 +99,8 @@ def operand_path(request):
 def test_conv_gemm_parity(oracle, prec, spec, operand_path):
     if (prec != "ffma" and spec in FFMA_ONLY) or (prec == "bf16" and spec in C4_ONLY):
         pytest.skip("tensor-core paths need C, K multiples of 8 (bf16) / 4 (tf32)")
-    if prec != "bf16" and operand_path != "auto":
-        pytest.skip("operand path only applies to the bf16 tensor-core kernel")
+    if (prec == "ffma" and operand_path != "auto") or (prec == "tf32" and operand_path == "regepi"):
+        pytest.skip("operand path does not apply to this kernel")
     dev = _dev()
     name, n, h, w, c, k, r, pad, stride = spec
     g = dev.geom(n, h, w, c, k, r, pad=pad, stride=stride)
