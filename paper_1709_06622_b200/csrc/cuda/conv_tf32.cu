@@ -69,7 +69,9 @@ struct Params {
 // Operand loads: kGather = cp.async by 128 threads (any C, K % 4 == 0);
 // kPlain = 1x1/s1/p0, every operand a plain matrix by 2-D TMA; kIm2col = the
 // activation operand by im2col-mode TMA (one tap x 32 channels per k-block).
-constexpr int kGather = 0, kPlain = 1, kIm2col = 2;
+// kIm2colC4 = fwd with C == 4 (the padded RGB stem): eight one-tap boxes of
+// 128 pixels x 16 B per k-block, landing as no-swizzle 8x16B core matrices.
+constexpr int kGather = 0, kPlain = 1, kIm2col = 2, kIm2colC4 = 3;
 
 // K-major rows (SWIZZLE_128B): 16-byte chunk j of row r lands at j ^ (r & 7).
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tf32_kernel(const __grid_con
         // =========================================== TMA producer (1 thread) ======
         if (tid == 0 && has_k) {
             int bn = 0, bh = 0, bw = 0;  // im2col base of the tile's first GEMM row (fwd / dgrad)
-            if (MODE != ConvMode::Wgrad && p.load == kIm2col) {
+            if (MODE != ConvMode::Wgrad && (p.load == kIm2col || p.load == kIm2colC4)) {
                 uint32_t n, rem, a, b;
                 const uint32_t m0 = static_cast<uint32_t>(mt * BM);
                 if constexpr (MODE == ConvMode::Fwd) {
@@ -150,6 +152,17 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tf32_kernel(const __grid_con
                 if constexpr (MODE == ConvMode::Fwd) {
                     if (p.load == kPlain) {
                         ptx::tma_load_2d(a_smem, &p.tmap_a, bar, kk0, mt * BM);
+                    } else if (p.load == kIm2colC4) {
+                        const int taps = s.R * s.S;
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            int tap = kb * 8 + jj;
+                            if (tap >= taps) tap = 0;  // K tail: the B rows there are zero
+                            uint32_t r, sx;
+                            s.d_s.divmod(static_cast<uint32_t>(tap), r, sx);
+                            ptx::tma_load_im2col_4d(a_smem + jj * 2048, &p.tmap_a, bar, 0, bw, bh, bn,
+                                                    static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+                        }
                     } else {
                         uint32_t tap, c0, r, sx;
                         s.d_c.divmod(static_cast<uint32_t>(kk0), tap, c0);
@@ -475,7 +488,9 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tf32_kernel(const __grid_con
 #pragma unroll
                 for (int k = 0; k < BKE / 8; ++k) {
                     const uint64_t ad = kAmn ? ptx::sw128b32_desc(a_addr + k * 1024, kMnBlock, 512)
-                                             : ptx::sw128_desc(a_addr + k * 32, 16, 1024);
+                                        : (TMA && p.load == kIm2colC4)
+                                            ? ptx::interleave_desc(a_addr + k * 4096, 2048, 128)
+                                            : ptx::sw128_desc(a_addr + k * 32, 16, 1024);
                     const uint64_t bd = kBmn ? ptx::sw128b32_desc(b_addr + k * 1024, kMnBlock, 512)
                                              : ptx::sw128_desc(b_addr + k * 32, 16, 1024);
                     ptx::umma_tf32(tmem_base, ad, bd, idesc, (kb > kb_begin || k > 0) ? 1u : 0u);
@@ -557,6 +572,8 @@ int pick_load(const ConvShape& s) {
     if (force_gather()) return kGather;
     if (MODE == ConvMode::Dgrad && s.K % BKE != 0) return kGather;  // k-blocks within one tap
     if (plain_geometry(s)) return kPlain;
+    if (MODE == ConvMode::Fwd && s.C == 4 && s.R <= 16 && s.S <= 16 && s.ph <= 15 && s.pw <= 15)
+        return kIm2colC4;
     return im2col_geometry(s, MODE == ConvMode::Dgrad ? s.K : s.C) ? kIm2col : kGather;
 }
 
@@ -567,6 +584,10 @@ bool build_maps(Params& p, int bn) {
     if constexpr (MODE == ConvMode::Fwd) {
         const bool a = p.load == kPlain
                            ? make_tmap_f32_2d(&p.tmap_a, p.a, s.M, s.C, BM, k_major)
+                       : p.load == kIm2colC4
+                           ? make_tmap_im2col_f32(&p.tmap_a, p.a, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
+                                                  s.pw - (s.S - 1), s.ph - (s.R - 1), s.sw, s.sh, BM,
+                                                  CU_TENSOR_MAP_SWIZZLE_NONE, 4)
                            : make_tmap_im2col_f32(&p.tmap_a, p.a, s.N, s.H, s.W, s.C, -s.pw, -s.ph,
                                                   s.pw - (s.S - 1), s.ph - (s.R - 1), s.sw, s.sh, BM, k_major);
         return a && make_tmap_f32_2d(&p.tmap_b, p.b, s.Ncol, s.Kdim, bn, k_major);

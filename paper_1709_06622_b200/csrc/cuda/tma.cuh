@@ -146,7 +146,7 @@ inline bool make_tmap_filters_f32(CUtensorMap* map, const void* base, uint64_t k
 // im2col view of an NHWC fp32 tensor: `pixels` filter-base positions x 32 channels
 inline bool make_tmap_im2col_f32(CUtensorMap* map, const void* base, int n, int h, int w, int c, int lower_w,
                                  int lower_h, int upper_w, int upper_h, int stride_w, int stride_h,
-                                 uint32_t pixels, CUtensorMapSwizzle swizzle) {
+                                 uint32_t pixels, CUtensorMapSwizzle swizzle, uint32_t channels = 32) {
     EncodeIm2colFn fn = encode_im2col_fn();
     if (!fn) return false;
     const cuuint64_t dims[4] = {cuuint64_t(c), cuuint64_t(w), cuuint64_t(h), cuuint64_t(n)};
@@ -154,8 +154,8 @@ inline bool make_tmap_im2col_f32(CUtensorMap* map, const void* base, int n, int 
     const int lower[2] = {lower_w, lower_h};
     const int upper[2] = {upper_w, upper_h};
     const cuuint32_t estr[4] = {1, cuuint32_t(stride_w), cuuint32_t(stride_h), 1};
-    if (fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, lower, upper, 32,
-           pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    if (fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, lower, upper,
+           channels, pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     int drv = 0;

@@ -52,6 +52,7 @@ GEOMS = [
 C4_ONLY = [  # channel counts % 4 but not % 8: fp32 modes only
     ("c4_3x3_k20", 2, 9, 9, 12, 20, 3, 1, 1),
     ("c4_5x5_s2", 2, 13, 11, 4, 36, 5, 2, 2),
+    ("c4_stem_7x7_s2", 2, 32, 30, 4, 64, 7, 3, 2),  # tf32 4-channel im2col-TMA stem
 ]
 FFMA_ONLY = [
     ("lenet_conv1_c1", 4, 28, 28, 1, 20, 5, 0, 1),
