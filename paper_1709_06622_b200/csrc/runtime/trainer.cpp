@@ -24,6 +24,7 @@
 #include <chrono>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <sstream>
 #include <vector>
@@ -238,6 +239,20 @@ int build_graph(tcb_trainer* t) {
     t->world = cfg.value("world", 1);  // layout planning before join (join overrides)
 
     std::map<std::string, int> by_name;
+    // bf16: conv outputs narrower than 64 channels, and those read by a spatial
+    // (R*S > 1) conv with K % 64 != 0, get K rounded up to 64 allocated channels,
+    // so their consumers meet the im2col-TMA operand path (whole 64-channel
+    // slices) instead of the cp.async gather; the extra channels are zero
+    // filters and stay exactly 0. Not for tensors that feed a channel concat.
+    const bool pad_narrow = t->bf16 && cfg.value("pad_narrow_channels", true);
+    std::set<std::string> concat_inputs, spatial_inputs;
+    for (const json& L : cfg.at("layers")) {
+        const std::string lop = L.value("op", std::string());
+        if (lop == "concat")
+            for (const json& nm : L.at("in")) concat_inputs.insert(nm.get<std::string>());
+        if (lop == "conv" && L.value("r", 1) * L.value("s", L.value("r", 1)) > 1 && L.contains("in"))
+            spatial_inputs.insert(L.at("in").get<std::string>());
+    }
     int conv_idx = 0;
     for (const json& L : cfg.at("layers")) {
         Node nd;
@@ -265,7 +280,9 @@ int build_graph(tcb_trainer* t) {
             // (tf32) — 16-byte NHWC rows; padded filters are zero, so padded channels
             // stay exactly 0.
             const int k_logical = L.at("k").get<int>();
-            const int k_alloc = static_cast<int>(round_up(k_logical, t->cpad));
+            const bool widen = pad_narrow && !concat_inputs.count(nd.name) &&
+                               (k_logical < 64 || (k_logical % 64 != 0 && spatial_inputs.count(nd.name)));
+            const int k_alloc = static_cast<int>(round_up(k_logical, widen ? 64 : t->cpad));
             nd.g = ConvGeom{x.n, x.h, x.w, x.c, k_alloc, L.at("r").get<int>(),
                             L.value("s", L.at("r").get<int>()), L.value("pad_h", L.value("pad", 0)),
                             L.value("pad_w", L.value("pad", 0)), L.value("stride_h", L.value("stride", 1)),

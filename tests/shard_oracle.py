@@ -23,8 +23,24 @@ def _pad(cfg):
     return {"bf16": 8, "tf32": 4}.get(cfg.get("precision", "bf16"), 1)
 
 
+def _k_alloc(L, cfg, concat_inputs):
+    # bf16 rounds a conv's K up to 64 when K < 64, or when a spatial (R*S > 1) conv
+    # reads it and K % 64 != 0 — unless the tensor feeds a concat
+    spatial = {x["in"] for x in cfg["layers"] if x["op"] == "conv" and x["r"] * x["s"] > 1}
+    if cfg.get("precision", "bf16") == "bf16" and cfg.get("pad_narrow_channels", True) \
+            and L["name"] not in concat_inputs \
+            and (L["k"] < 64 or (L["k"] % 64 and L["name"] in spatial)):
+        return _up(L["k"], 64)
+    return _up(L["k"], _pad(cfg))
+
+
+def _concat_inputs(cfg):
+    return {x for L in cfg["layers"] if L["op"] == "concat" for x in L["in"]}
+
+
 def layout(cfg: dict, world: int) -> dict:
     pad = _pad(cfg)
+    cat_in = _concat_inputs(cfg)
     ch = {}
     layers = []
     off = 0
@@ -34,7 +50,7 @@ def layout(cfg: dict, world: int) -> dict:
             ch[L["name"]] = (_up(L["c"], pad), L["c"])
         elif L["op"] == "conv":
             c_alloc, c_log = ch[L["in"]]
-            k_alloc = _up(L["k"], pad)
+            k_alloc = _k_alloc(L, cfg, cat_in)
             ch[L["name"]] = (k_alloc, L["k"])
             wcount = k_alloc * L["r"] * L["s"] * c_alloc
             entry = {"name": L["name"], "woff": off, "wcount": wcount, "boff": None}
@@ -60,7 +76,7 @@ def layout(cfg: dict, world: int) -> dict:
 def _k_of(entry, cfg):
     for L in cfg["layers"]:
         if L.get("name") == entry["name"]:
-            return _up(L["k"], _pad(cfg))
+            return _k_alloc(L, cfg, _concat_inputs(cfg))
     raise KeyError(entry["name"])
 
 
