@@ -178,6 +178,7 @@ using namespace tcb;
 //   {"layers": [{"h","w","c","k","r","s","pad_h","pad_w","stride_h","stride_w"}, ...],
 //    "batches": [32, 64, ...], "algorithms": ["gemm", "winograd", "fft"],
 //    "precision": "bf16"|"tf32"|"ffma", "reps": 5}
+//   (a layer may carry "c_alloc", "k_alloc", "c_valid": the executor's allocation)
 // Reply JSON: {"csv": <catalog CSV>, "rows": [per-measurement detail], "skipped": [...]}.
 TCB_API int tcb_profile_catalog(const char* request_json, char** reply_out) {
     if (!request_json || !reply_out) return fail(TCB_ERR_INVALID, "NULL argument");
@@ -198,17 +199,20 @@ TCB_API int tcb_profile_catalog(const char* request_json, char** reply_out) {
             for (const json& bj : req.at("batches")) {
                 const int n = bj.get<int>();
                 const int c_log = L.at("c").get<int>();
+                // "c_alloc" / "k_alloc" / "c_valid": the executor's channel allocation
+                // (tcb_trainer_describe), so the catalog times what the step runs
                 ConvGeom g{n,
                            L.at("h").get<int>(),
                            L.at("w").get<int>(),
-                           (c_log + cpad - 1) / cpad * cpad,
-                           (L.at("k").get<int>() + cpad - 1) / cpad * cpad,
+                           L.value("c_alloc", (c_log + cpad - 1) / cpad * cpad),
+                           L.value("k_alloc", (L.at("k").get<int>() + cpad - 1) / cpad * cpad),
                            L.at("r").get<int>(),
                            L.value("s", L.at("r").get<int>()),
                            L.value("pad_h", 0),
                            L.value("pad_w", L.value("pad_h", 0)),
                            L.value("stride_h", 1),
                            L.value("stride_w", L.value("stride_h", 1))};
+                if (L.contains("c_valid") && L.at("c_valid").get<int>() < g.c) g.c_valid = L.at("c_valid").get<int>();
                 for (const json& aj : req.at("algorithms")) {
                     const std::string algo = aj.get<std::string>();
                     const int id = algo_id(algo);

@@ -30,9 +30,34 @@ def profile(layers: list[dict], batches: list[int], algorithms=("gemm", "winogra
 
 
 def conv_layer_specs(cfg: dict) -> list[dict]:
-    """Per-image conv geometries (layer order) of a model config."""
-    return [{k: g[k] for k in ("h", "w", "c", "k", "r", "s", "pad_h", "pad_w", "stride_h", "stride_w")}
-            for _, g in models.conv_layers(cfg)]
+    """Per-image conv geometries (layer order) of a model config, with the
+    executor's channel allocation (c_alloc / k_alloc / c_valid from
+    tcb_trainer_describe — no GPU needed) so a profiled catalog times exactly
+    the convs the training step runs."""
+    specs = [{k: g[k] for k in ("h", "w", "c", "k", "r", "s", "pad_h", "pad_w", "stride_h", "stride_w")}
+             for _, g in models.conv_layers(cfg)]
+    try:
+        import ctypes as _ct
+
+        from . import trainer as _tr
+        L = _tr._lib()
+        h = _ct.c_void_p()
+        device.check(L.tcb_trainer_create(json.dumps(cfg).encode(), _ct.byref(h)))
+        out = _ct.c_char_p()
+        device.check(L.tcb_trainer_describe(h, _ct.byref(out)))
+        d = json.loads(out.value.decode())
+        L.tcb_free(_ct.cast(out, _ct.c_void_p))
+        L.tcb_trainer_destroy(h)
+    except device.TcbError:
+        return specs
+    convs = [x for x in d["layers"] if x["op"] == "conv"]
+    for sp, x in zip(specs, convs):
+        n, h, w, c, k = x["geom"][:5]
+        sp["c_alloc"], sp["k_alloc"] = c, k
+        cl = d["layers"][x["in"]]["c_logical"]
+        if cl < c:
+            sp["c_valid"] = cl
+    return specs
 
 
 def net_text(cfg: dict) -> str:
