@@ -944,7 +944,7 @@ NarrowPlan narrow_plan(const ConvGeom& g) {
     const int ho = g.ho(), wo = g.wo();
     q.wp = (wo - 1) * g.stride_w + g.s;
     q.smem = size_t(g.r) * q.wp * q.cv * 2;
-    q.use = g.c == 8 && q.cv < g.c && g.r * g.s > 1 && 2 * q.kc <= g.r * g.s * g.c &&
+    q.use = g.c == 8 && q.cv < g.c && g.r * g.s > 1 && q.kc < g.r * g.s * g.c &&
             q.smem <= 48 * 1024 && q.kc <= 1024;
     if (!q.use) return q;
     q.col_bytes = size_t(g.n) * ho * wo * q.kc * 2;
