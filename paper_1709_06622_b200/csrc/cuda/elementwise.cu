@@ -269,6 +269,23 @@ __global__ void pack_channels_u8_kernel(const uint8_t* __restrict__ src, T* __re
     }
 }
 
+// bf16, 8 padded channels (the RGB input): one pixel per thread, cl <= 8 bytes
+// in, one 16-byte row out (same arithmetic as pack_channels_u8_kernel)
+__global__ void pack_u8_bf16x8_kernel(const uint8_t* __restrict__ src, uint4* __restrict__ dst, size_t pixels,
+                                      int cl) {
+    pdl_wait();
+    pdl_trigger();
+    for (size_t px = blockIdx.x * size_t(blockDim.x) + threadIdx.x; px < pixels;
+         px += size_t(gridDim.x) * blockDim.x) {
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            v[c] = __float2bfloat16_rn(
+                c < cl ? __fsub_rn(__fmul_rn(float(__ldg(src + px * cl + c)) + 0.5f, 0.0078125f), 1.f) : 0.f);
+        dst[px] = *reinterpret_cast<const uint4*>(v);
+    }
+}
+
 template <typename T>
 __global__ void add_kernel(T* y, const T* x, size_t n) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
@@ -577,6 +594,9 @@ cudaError_t sgd_momentum(float* w, const float* g, float* v, DType cdt, void* wc
 
 cudaError_t pack_channels_u8(DType dt, const uint8_t* src, void* dst, size_t pixels, int cl, int cp,
                              cudaStream_t st) {
+    if (dt == DType::BF16 && cp == 8 && cl <= 8 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0)
+        return launch_pdl(pack_u8_bf16x8_kernel, dim3(grid_for(pixels, 2)), dim3(kBlock), 0, st, src,
+                          static_cast<uint4*>(dst), pixels, cl);
     TCB_DT_SWITCH(dt, T, (pack_channels_u8_kernel<T><<<grid_for(pixels * cp, 4), kBlock, 0, st>>>(
                               src, static_cast<T*>(dst), pixels, cl, cp)));
     return cudaGetLastError();
