@@ -727,18 +727,26 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         ep.mask = mask_needed ? t->at(tgt.act) : nullptr;
         const void* cw = t->bf16 ? static_cast<const void*>(static_cast<__nv_bfloat16*>(t->wc_ptr()) + con.woff)
                                  : static_cast<const void*>(t->at<float>(t->off_param) + con.woff);
+        // a fully connected layer (filter = whole unpadded input map, 1x1 output) runs
+        // its dgrad as the equivalent 1x1 conv over a 1x1 image of H*W*C channels:
+        // the same memory, dx rows = images and 1/(H*W) of the reduction depth
+        // (the other taps only ever meet zero padding)
+        const ConvGeom& cg = con.g;
+        const bool fc = cg.r == cg.h && cg.s == cg.w && cg.pad_h == 0 && cg.pad_w == 0 && cg.ho() == 1 &&
+                        cg.wo() == 1 && (cg.h > 1 || cg.w > 1);
+        const ConvGeom dg = fc ? ConvGeom{cg.n, 1, 1, cg.h * cg.w * cg.c, cg.k, 1, 1, 0, 0, 1, 1} : cg;
         if (con.algo_id == TCB_ALGO_WINOGRAD)
             TRY_CUDA(winograd_dgrad(con.g, t->dt, t->at(con.grad), cw, ep, out, t->at(t->off_ws), st));
         else if (con.algo_id == TCB_ALGO_FFT)
             TRY_CUDA(fft_dgrad(con.g, t->dt, t->at(con.grad), cw, ep, out, t->at(t->off_ws), st));
         else if (t->bf16)
-            TRY_CUDA(conv_tc_dgrad(con.g, t->at(con.grad), cw, con.pack_wT ? t->at(con.wT) : nullptr, ep,
+            TRY_CUDA(conv_tc_dgrad(dg, t->at(con.grad), cw, (con.pack_wT && !fc) ? t->at(con.wT) : nullptr, ep,
                                    out, st));
         else if (t->tf32)
-            TRY_CUDA(conv_tf32_dgrad(con.g, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
+            TRY_CUDA(conv_tf32_dgrad(dg, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
                                      ep, static_cast<float*>(out), st));
         else
-            TRY_CUDA(conv_ffma_dgrad(con.g, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
+            TRY_CUDA(conv_ffma_dgrad(dg, t->at<float>(con.grad), t->at<float>(t->off_param) + con.woff,
                                      ep, static_cast<float*>(out), st));
         t->launches++;
         return TCB_OK;
