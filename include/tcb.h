@@ -207,6 +207,14 @@ int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t* id128);
  * replacing NCCL reduce-scatter / SGD / all-gather. */
 int tcb_trainer_attach_nvls(tcb_trainer* t, void* grad, const void* grad_mc, void* wcompute,
                             void* wcompute_mc, void* const* signal_pads_dev);
+/* Asynchronous PS (config "ps_async": the aggregation + update of step s runs
+ * on the trainer's own stream behind step s+1, which computes with weights
+ * one update old — the paper's asynchronous policy): over
+ * NVLS the second bf16 weight buffer is caller-provided too. */
+int tcb_trainer_attach_nvls_async(tcb_trainer* t, void* wcompute2, void* wcompute2_mc);
+/* Makes `stream` wait for every update issued so far (asynchronous PS; no-op
+ * otherwise). */
+int tcb_trainer_finish(tcb_trainer* t, void* stream);
 /* Loads a mini-batch from HOST memory (NHWC fp32 images, int32 labels). NULL
  * images = keep the device-resident synthetic batch. */
 int tcb_trainer_set_batch(tcb_trainer* t, const float* host_images, const int32_t* host_labels,

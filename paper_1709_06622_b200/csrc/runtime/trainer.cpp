@@ -60,6 +60,7 @@ struct Node {
     bool bias = false, relu = false, need_dgrad = true;
     int conv_index = 0;
     size_t woff = 0, boff = 0, wcount = 0;  // flat param offsets (elements)
+    size_t bcomp = 0;                        // offset in the compact fp32 bias copies
     float init_scale = 0.f;
     std::string algo = "gemm";
     int algo_id = 0;  // TCB_ALGO_*
@@ -186,7 +187,35 @@ struct tcb_trainer {
     uint32_t* const* pads_dev = nullptr;
     uint32_t* nvls_epoch = nullptr;
     float* grad_ptr() const { return ext_grad ? ext_grad : at<float>(off_grad); }
-    void* wc_ptr() const { return ext_wc ? ext_wc : at(off_wc); }
+    void* wc_ptr() const {
+        if (async_ps) return wc_buf(wc_rd);
+        return ext_wc ? ext_wc : at(off_wc);
+    }
+
+    // Asynchronous PS (config "ps_async"): the aggregation +
+    // update of step s runs on its own stream, hidden behind step s+1, which
+    // computes with the weights one update old (staleness 1). Double-buffered
+    // bf16 weights: W_j lives in buffer j % 2; step s reads W_max(s-1,0) while
+    // update s writes W_s+1 into the other buffer.
+    bool async_ps = false;
+    size_t off_wc2 = 0;
+    void* ext_wc2 = nullptr;
+    void* wc2_mc = nullptr;
+    int wc_rd = 0;
+    long long step_idx = 0;
+    // fp32 biases the forward reads, refreshed from a bf16 weight buffer after
+    // every update whenever the local fp32 master is not the source of truth
+    // (world > 1: only the owned shard of it is current; asynchronous PS: the
+    // step reads the weights one update old). One copy per weight buffer.
+    bool bias_from_wc = false;
+    size_t bias_total = 0, off_biasc[2] = {0, 0};
+    cudaStream_t ps_stream = nullptr;
+    cudaEvent_t ev_bwd_done = nullptr, ev_upd[2] = {nullptr, nullptr};
+    void* wc_buf(int i) const {
+        if (i == 0) return ext_wc ? ext_wc : at(off_wc);
+        return ext_wc2 ? ext_wc2 : at(off_wc2);
+    }
+    void* wc_mc_buf(int i) const { return i == 0 ? wc_mc : wc2_mc; }
 };
 
 namespace tcb {
@@ -223,9 +252,10 @@ int build_graph(tcb_trainer* t) {
     t->classes = cfg.at("classes").get<int>();
     t->seed = cfg.value("seed", uint64_t(20260810));
     t->overlap = t->cfg.value("overlap_comm", false);
+    t->async_ps = cfg.value("ps_async", false);
     {
         const char* e = std::getenv("TCB_GRAPH");
-        t->use_graph = t->cfg.value("cuda_graph", !(e && e[0] == '0'));
+        t->use_graph = t->cfg.value("cuda_graph", !(e && e[0] == '0')) && !t->async_ps;
     }
     t->comm_bg_ctas = t->cfg.value("overlap_ctas", 8);
     {
@@ -441,6 +471,12 @@ void plan_params(tcb_trainer* t) {
             logical += nd.c_logical;
         }
     }
+    t->bias_total = 0;
+    for (Node& nd : t->nodes)
+        if (nd.op == Op::Conv && nd.bias) {
+            nd.bcomp = t->bias_total;
+            t->bias_total += nd.g.k;
+        }
     t->param_count = logical;
     const size_t unit = size_t(t->world) * kParamAlign;
     t->param_padded = round_up(std::max<size_t>(off, 1), unit);
@@ -475,6 +511,10 @@ int allocate(tcb_trainer* t, bool dry = false) {
     t->off_grad = b.take(t->param_padded * 4);
     t->off_mom = b.take(t->param_padded * 4);  // only the owned shard is used
     t->off_wc = t->bf16 ? b.take(t->param_padded * 2) : t->off_param;
+    if (t->async_ps) t->off_wc2 = b.take(t->param_padded * 2);
+    t->bias_from_wc = t->bf16 && (t->world > 1 || t->async_ps) && t->bias_total > 0;
+    if (t->bias_from_wc)
+        for (int k = 0; k < (t->async_ps ? 2 : 1); ++k) t->off_biasc[k] = b.take(t->bias_total * 4);
     size_t ws = 0, colsum = 0;
     for (Node& nd : t->nodes) {
         const size_t elems = size_t(nd.n) * nd.h * nd.w * nd.c;
@@ -556,6 +596,8 @@ int pack_input(tcb_trainer* t, cudaStream_t st) {
                       "pack_input");
 }
 
+int refresh_biases(tcb_trainer* t, const void* wc, int k, cudaStream_t st);
+
 int initialize(tcb_trainer* t, cudaStream_t st) {
     // parameters: deterministic per-layer streams, tag = 1000 + conv index
     float* param = t->at<float>(t->off_param);
@@ -580,6 +622,9 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
     }
     if (t->bf16)
         TRY_CUDA(cast(DType::F32, param, DType::BF16, t->wc_ptr(), t->param_padded, st));
+    if (t->async_ps)  // W_0 in both buffers
+        TRY_CUDA(cudaMemcpyAsync(t->wc_buf(1), t->wc_buf(0), t->param_padded * 2, cudaMemcpyDeviceToDevice, st));
+    for (int k = 0; k < (t->async_ps ? 2 : 1); ++k) TRY(refresh_biases(t, t->wc_buf(k), k, st));
     // synthetic mini-batch: worker r uses seed + r (distinct mini-batches);
     // "data_rank" overrides r (tests replay one rank's batch on a single GPU)
     const Node& in = t->nodes[0];
@@ -626,7 +671,9 @@ int forward(tcb_trainer* t, cudaStream_t st) {
             case Op::Input: break;
             case Op::Conv: {
                 Epilogue ep;
-                ep.bias = nd.bias ? t->at<float>(t->off_param) + nd.boff : nullptr;
+                ep.bias = !nd.bias ? nullptr
+                          : t->bias_from_wc ? t->at<float>(t->off_biasc[t->async_ps ? t->wc_rd : 0]) + nd.bcomp
+                                            : t->at<float>(t->off_param) + nd.boff;
                 ep.residual = nd.residual >= 0 ? t->at(t->nodes[nd.residual].act) : nullptr;
                 ep.relu = nd.relu;
                 const size_t idx = static_cast<size_t>(&nd - t->nodes.data());
@@ -876,14 +923,29 @@ int backward(tcb_trainer* t, cudaStream_t st) {
     return TCB_OK;
 }
 
-int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, cudaEvent_t after_sgd) {
+// fp32 bias copy k <- the bias segments of bf16 weight buffer `wc`
+int refresh_biases(tcb_trainer* t, const void* wc, int k, cudaStream_t st) {
+    if (!t->bias_from_wc) return TCB_OK;
+    for (const Node& nd : t->nodes) {
+        if (nd.op != Op::Conv || !nd.bias) continue;
+        TRY_CUDA(cast(DType::BF16, static_cast<const __nv_bfloat16*>(wc) + nd.boff, DType::F32,
+                      t->at<float>(t->off_biasc[k]) + nd.bcomp, nd.g.k, st));
+        t->launches++;
+    }
+    return TCB_OK;
+}
+
+// wc_out: the bf16 weight buffer the update writes (-1: the one the step read)
+int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, cudaEvent_t after_sgd,
+                         int wc_out = -1) {
     float* grad = t->grad_ptr();
     float* param = t->at<float>(t->off_param);
     float* mom = t->at<float>(t->off_mom);
     const float gscale = 1.0f / static_cast<float>(t->world);
     const ncclDataType_t wdt = t->bf16 ? ncclBfloat16 : ncclFloat32;
     const size_t wes = t->bf16 ? 2 : 4;
-    char* wc = static_cast<char*>(t->wc_ptr());
+    char* wc = static_cast<char*>(wc_out >= 0 ? t->wc_buf(wc_out) : t->wc_ptr());
+    void* wc_mc = wc_out >= 0 ? t->wc_mc_buf(wc_out) : t->wc_mc;
     const int owners = (t->n_ps > 0 && t->n_ps < t->world) ? t->n_ps : t->world;
 
     if (t->overlap_active()) {
@@ -910,7 +972,7 @@ int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, 
         TRY_CUDA(nvls_barrier(t->pads_dev, t->nvls_epoch, kSlot0, t->rank, t->world, st));
         if (after_rs) TRY_CUDA(cudaEventRecord(after_rs, st));
         const size_t o = t->rank * t->shard;
-        TRY_CUDA(ps_nvls_update(t->grad_mc, grad, param, mom, t->wc_mc, o, t->shard, t->lr, t->momentum,
+        TRY_CUDA(ps_nvls_update(t->grad_mc, grad, param, mom, wc_mc, o, t->shard, t->lr, t->momentum,
                                 t->weight_decay, gscale, st));
         if (after_sgd) TRY_CUDA(cudaEventRecord(after_sgd, st));
         TRY_CUDA(nvls_barrier(t->pads_dev, t->nvls_epoch, kSlot0, t->rank, t->world, st));
@@ -968,7 +1030,7 @@ int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, 
         t->launches++;
         if (after_sgd) TRY_CUDA(cudaEventRecord(after_sgd, st));
     }
-    return TCB_OK;
+    return refresh_biases(t, wc, wc_out >= 0 ? wc_out : 0, st);
 }
 
 }  // namespace
@@ -1003,6 +1065,12 @@ TCB_API int tcb_trainer_destroy(tcb_trainer* t) {
         for (cudaEvent_t e : t->ev_ready) cudaEventDestroy(e);
         if (t->ev_comm_done) cudaEventDestroy(t->ev_comm_done);
         cudaStreamDestroy(t->comm_stream);
+    }
+    if (t->ps_stream) {
+        cudaStreamSynchronize(t->ps_stream);
+        cudaStreamDestroy(t->ps_stream);
+        cudaEventDestroy(t->ev_bwd_done);
+        for (cudaEvent_t e : t->ev_upd) cudaEventDestroy(e);
     }
     if (t->comm_bg) ncclCommDestroy(t->comm_bg);
     if (t->comm) ncclCommDestroy(t->comm);
@@ -1230,6 +1298,63 @@ static int graph_step(tcb_trainer* t, cudaStream_t st) {
     return check_cuda(cudaStreamWaitEvent(st, t->graph_out, 0), "graph fence");
 }
 
+// Asynchronous PS step s: forward / backward on the caller's stream with
+// W_max(s-1,0); the aggregation + update on ps_stream writes W_s+1 into the
+// other weight buffer while step s+1 computes. Waits: forward s needs update
+// s-2 (it wrote W_s-1); backward s rewrites the gradient update s-1 reads.
+static int async_step(tcb_trainer* t, cudaStream_t st) {
+    if (!t->ps_stream) {
+        if (!t->bf16 || t->overlap || (t->n_ps > 0 && t->n_ps < t->world))
+            return fail(TCB_ERR_UNSUPPORTED, "ps_async needs bf16, PS shards = GPUs and no overlap_comm");
+        if (t->nvls && !t->wc2_mc)
+            return fail(TCB_ERR_INVALID, "ps_async over NVLS needs tcb_trainer_attach_nvls_async");
+        int lo = 0, hi = 0;
+        TRY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        TRY_CUDA(cudaStreamCreateWithPriority(&t->ps_stream, cudaStreamNonBlocking, hi));
+        TRY_CUDA(cudaEventCreateWithFlags(&t->ev_bwd_done, cudaEventDisableTiming));
+        for (auto& e : t->ev_upd) TRY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const long long s = t->step_idx;
+    t->wc_rd = s >= 1 ? static_cast<int>((s - 1) % 2) : 0;
+    if (s >= 2) TRY_CUDA(cudaStreamWaitEvent(st, t->ev_upd[(s - 2) % 2], 0));
+    cudaEvent_t* e = t->ph.e;
+    if (t->timing) TRY_CUDA(cudaEventRecord(e[0], st));
+    TRY(forward(t, st));
+    if (t->timing) TRY_CUDA(cudaEventRecord(e[1], st));
+    if (s >= 1) TRY_CUDA(cudaStreamWaitEvent(st, t->ev_upd[(s - 1) % 2], 0));
+    TRY(backward(t, st));
+    if (t->timing) TRY_CUDA(cudaEventRecord(e[2], st));
+    TRY_CUDA(cudaEventRecord(t->ev_bwd_done, st));
+    TRY_CUDA(cudaStreamWaitEvent(t->ps_stream, t->ev_bwd_done, 0));
+    TRY(aggregate_and_update(t, t->ps_stream, t->timing ? e[3] : nullptr, t->timing ? e[4] : nullptr,
+                             static_cast<int>((s + 1) % 2)));
+    TRY_CUDA(cudaEventRecord(t->ev_upd[s % 2], t->ps_stream));
+    if (t->timing) {  // phase timing measures the update itself: join it
+        TRY_CUDA(cudaStreamWaitEvent(st, t->ev_upd[s % 2], 0));
+        TRY_CUDA(cudaEventRecord(e[5], st));
+    }
+    ++t->step_idx;
+    return check_cuda(cudaGetLastError(), "async step");
+}
+
+// The caller's stream waits for every update issued so far (asynchronous PS);
+// a no-op otherwise.
+TCB_API int tcb_trainer_finish(tcb_trainer* t, void* stream) {
+    if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
+    if (t->async_ps && t->step_idx > 0)
+        TRY_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), t->ev_upd[(t->step_idx - 1) % 2], 0));
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_attach_nvls_async(tcb_trainer* t, void* wcompute2, void* wcompute2_mc) {
+    if (!t || !wcompute2 || !wcompute2_mc) return fail(TCB_ERR_INVALID, "NULL argument");
+    if (!t->nvls || !t->async_ps) return fail(TCB_ERR_INVALID, "attach_nvls first, with ps_async");
+    if (t->initialized) return fail(TCB_ERR_INVALID, "attach before the first step");
+    t->ext_wc2 = wcompute2;
+    t->wc2_mc = wcompute2_mc;
+    return TCB_OK;
+}
+
 TCB_API int tcb_trainer_step(tcb_trainer* t, void* stream) {
     if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
     auto st = static_cast<cudaStream_t>(stream);
@@ -1243,6 +1368,7 @@ TCB_API int tcb_trainer_step(tcb_trainer* t, void* stream) {
         t->launches += staged_launches;
         return TCB_OK;
     }
+    if (t->async_ps) return async_step(t, st);
     cudaEvent_t* e = t->ph.e;
     if (t->timing) TRY_CUDA(cudaEventRecord(e[0], st));
     TRY(forward(t, st));
@@ -1390,7 +1516,10 @@ TCB_API int tcb_trainer_tensor(tcb_trainer* t, const char* name, void** ptr, siz
     if (n == "param") { p = t->at(t->off_param); b = t->param_padded * 4; }
     else if (n == "grad") { p = t->grad_ptr(); b = t->param_padded * 4; }
     else if (n == "momentum") { p = t->at(t->off_mom); b = t->param_padded * 4; }
-    else if (n == "wcompute") { p = t->wc_ptr(); b = t->param_padded * es; }
+    else if (n == "wcompute") {  // the latest weights (asynchronous PS: W_step_idx)
+        p = t->async_ps ? t->wc_buf(static_cast<int>(t->step_idx % 2)) : t->wc_ptr();
+        b = t->param_padded * es;
+    }
     else if (n == "labels") { p = t->at(t->off_labels); b = size_t(t->batch) * 4; }
     else if (n == "loss") { p = t->at(t->off_loss); b = size_t(t->batch + 1) * 4; }
     else if (n == "input") { p = t->at(t->nodes[0].act); b = node_bytes(t->nodes[0]); }

@@ -41,6 +41,8 @@ def _lib():
         L.tcb_trainer_enable_layer_timing.argtypes = [_vp, ctypes.c_int]
         L.tcb_trainer_layer_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p)]
         L.tcb_trainer_attach_nvls.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+        L.tcb_trainer_attach_nvls_async.argtypes = [_vp, _vp, _vp]
+        L.tcb_trainer_finish.argtypes = [_vp, _vp]
         L.tcb_free.argtypes = [_vp]
         _bound = True
     return L
@@ -87,7 +89,8 @@ class Trainer:
         group = group or dist.group.WORLD
         n = self.describe()["param_padded"]
         bufs, handles, mcs = [], [], []
-        for dt in (torch.float32, torch.bfloat16):
+        dts = (torch.float32, torch.bfloat16) + ((torch.bfloat16,) if self.cfg.get("ps_async") else ())
+        for dt in dts:
             t = symm.empty(n, dtype=dt, device="cuda")
             h = symm.rendezvous(t, group.group_name)
             if not h.multicast_ptr:
@@ -101,6 +104,8 @@ class Trainer:
         device.check(_lib().tcb_trainer_attach_nvls(self.handle, _vp(bufs[0].data_ptr()), _vp(mcs[0]),
                                                     _vp(bufs[1].data_ptr()), _vp(mcs[1]),
                                                     _vp(handles[0].signal_pad_ptrs_dev)))
+        if len(bufs) > 2:  # asynchronous PS: the second weight buffer
+            device.check(_lib().tcb_trainer_attach_nvls_async(self.handle, _vp(bufs[2].data_ptr()), _vp(mcs[2])))
         self._symm = (bufs, handles)  # keep the allocations alive
 
     def __del__(self):
@@ -131,6 +136,10 @@ class Trainer:
 
     def step(self):
         device.check(_lib().tcb_trainer_step(self.handle, self._stream()))
+
+    def finish(self):
+        """Join the in-flight parameter updates (asynchronous PS) into the stream."""
+        device.check(_lib().tcb_trainer_finish(self.handle, self._stream()))
 
     def loss(self) -> float:
         out = ctypes.c_float()

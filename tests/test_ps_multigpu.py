@@ -123,3 +123,30 @@ def test_two_gpu_nvls_matches_nccl_over_steps():
     for r in range(2):
         assert np.array_equal(got[r][1], ref[r][1]), f"rank {r} master params"
         assert np.array_equal(got[r][2], ref[r][2]), f"rank {r} compute weights"
+
+
+@pytest.mark.parametrize("transport", ["nccl", "nvls"])
+def test_two_gpu_async_ps_is_one_step_stale(oracle, transport):
+    """Asynchronous PS (the paper's policy): step 1 computes
+    with W_0 while update 0 is in flight, so with fixed per-rank batches both
+    updates apply the same summed gradient s = g_0 + g_1 of W_0:
+    W_2 = sgd(sgd(W_0, s), s), bit-exact, on the owned shards and in the
+    gathered bf16 weights."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from paper_1709_06622_b200 import models
+    cfg = models.tiny_resnet(batch=8, precision="bf16")
+    cfg["ps_transport"] = transport
+    w0, g0 = _single_rank_grads(cfg, 0)
+    _, g1 = _single_rank_grads(cfg, 1)
+    s = (g0 + g1).astype(np.float32)
+    w1, v1 = oracle.sgd(w0, s, np.zeros_like(w0), cfg["lr"], cfg["momentum"], cfg["weight_decay"], 0.5)
+    w2, _ = oracle.sgd(w1, s, v1, cfg["lr"], cfg["momentum"], cfg["weight_decay"], 0.5)
+    res = _run_world(dict(cfg, ps_async=True), 2, steps=2)
+    padded = res[0][1].size
+    w2 = np.concatenate([w2, np.zeros(padded - w2.size, np.float32)])
+    per = res[0][0]
+    for r in range(2):
+        sl = slice(r * per, (r + 1) * per)
+        assert np.array_equal(res[r][1][sl], w2[sl]), f"rank {r} master shard"
+        assert np.array_equal(res[r][2], oracle.round_bf16(w2)), f"rank {r} compute weights"

@@ -257,6 +257,28 @@ def test_cuda_graph_replay_matches_eager_steps():
     assert a.launch_count() == b.launch_count()
 
 
+def test_async_ps_single_gpu_staleness_one(oracle):
+    """ps_async on one GPU: the update of step 0 overlaps step 1, which still
+    computes with W_0, so both updates apply g(W_0): W_2 = sgd(sgd(W_0, g), g)."""
+    from paper_1709_06622_b200.trainer import Trainer
+    cfg = _models().tiny_resnet(batch=4, precision="bf16")
+    c0 = dict(cfg, lr=0.0)
+    t0 = Trainer(c0)
+    t0.step()
+    torch.cuda.synchronize()
+    w0 = t0.tensor("param").cpu().numpy()
+    g = t0.tensor("grad").cpu().numpy()
+    w1, v1 = oracle.sgd(w0, g, np.zeros_like(w0), cfg["lr"], cfg["momentum"], cfg["weight_decay"], 1.0)
+    w2, _ = oracle.sgd(w1, g, v1, cfg["lr"], cfg["momentum"], cfg["weight_decay"], 1.0)
+    t = Trainer(dict(cfg, ps_async=True))
+    t.step()
+    t.step()
+    t.finish()
+    torch.cuda.synchronize()
+    assert np.array_equal(t.tensor("param").cpu().numpy(), w2)
+    assert np.array_equal(t.tensor("wcompute").float().cpu().numpy(), oracle.round_bf16(w2))
+
+
 def test_loss_decreases_over_steps():
     from paper_1709_06622_b200.trainer import Trainer
     cfg = _models().tiny_resnet(batch=8, precision="bf16", lr=0.05)
