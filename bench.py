@@ -70,6 +70,9 @@ def parse():
                     help="PS step: NCCL reduce-scatter + SGD + all-gather, or one fused kernel "
                          "over NVSwitch multicast (bf16, PS shards = GPUs); auto = nvls where it "
                          "applies and the system has multicast, else nccl")
+    ap.add_argument("--ps-async", action="store_true",
+                    help="asynchronous PS (the paper's policy): each step's aggregation + update "
+                         "runs behind the next step, which uses one-update-old weights")
     return ap.parse_args()
 
 
@@ -399,6 +402,7 @@ def main():
     if transport == "auto":
         transport = "nvls" if nvls_ok else "nccl"
     cfg["ps_transport"] = transport
+    cfg["ps_async"] = args.ps_async
     transport_note = None
     try:
         tr = Trainer(cfg, rank, world, nid)
@@ -461,6 +465,7 @@ def main():
     start.record(stream)
     for _ in range(args.steps):
         tr.step()
+    tr.finish()  # asynchronous PS: the last update belongs to the timed work
     end.record(stream)
     barrier()
     t_wall1 = time.time()
@@ -497,6 +502,7 @@ def main():
             if i + 1 < args.steps:
                 tr.stage_batch(*host[(i + 1) % 2])
             lossbuf.copy_(tr.tensor("loss")[:1], non_blocking=True)
+        tr.finish()
         e_end.record(stream)
         barrier()
         ems = e_start.elapsed_time(e_end)
@@ -560,6 +566,7 @@ def main():
                        "ps_shards": args.n_ps or world, "precision": args.precision,
                        "comm_overlap": args.overlap and world > 1 and (args.n_ps in (0, world)),
                        "ps_transport": (transport_note or transport) if world > 1 else None,
+                       "ps_async": args.ps_async,
                        "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (per-step activations >> 126 MB); no flush"},
             "clocks": clk,
