@@ -975,30 +975,44 @@ __global__ void __launch_bounds__(256) narrow_im2col_kernel(const __nv_bfloat16*
         for (int c = 0; c < cv; ++c) sm[i * cv + c] = e[c];
     }
     __syncthreads();
-    // one warp per output pixel, lane = 16-byte chunk q of its col row: the
-    // (r, t0) decode of a chunk is per-lane constant, stores are contiguous
     const int span = g.s * cv, qpp = kc / 8;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    int q_off[4], q_ok[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int q = lane + 32 * k;
-        const int col0 = q * 8, r = col0 / rw, t0 = col0 - r * rw;
-        q_ok[k] = q < qpp ? (r < g.r ? min(8, max(0, span - t0)) : 0) : -1;
-        q_off[k] = r * wp * cv + t0;
-    }
     uint4* dst = reinterpret_cast<uint4*>(col + size_t(blockIdx.x) * wo * kc);
-    for (int ow = warp; ow < wo; ow += nwarps) {
-        const __nv_bfloat16* base = sm + ow * g.stride_w * cv;
+    if (qpp >= 16) {
+        // wide col rows: one warp per output pixel, lane = chunk q (its (r, t0)
+        // decode is per-lane constant)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+        int q_off[4], q_ok[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (q_ok[k] < 0) break;
-            __align__(16) __nv_bfloat16 v[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                v[e] = e < q_ok[k] ? base[q_off[k] + e] : __float2bfloat16(0.f);
-            dst[size_t(ow) * qpp + lane + 32 * k] = *reinterpret_cast<const uint4*>(v);
+            const int q = lane + 32 * k;
+            const int col0 = q * 8, r = col0 / rw, t0 = col0 - r * rw;
+            q_ok[k] = q < qpp ? (r < g.r ? min(8, max(0, span - t0)) : 0) : -1;
+            q_off[k] = r * wp * cv + t0;
         }
+        for (int ow = warp; ow < wo; ow += nwarps) {
+            const __nv_bfloat16* base = sm + ow * g.stride_w * cv;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (q_ok[k] < 0) break;
+                __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = e < q_ok[k] ? base[q_off[k] + e] : __float2bfloat16(0.f);
+                dst[size_t(ow) * qpp + lane + 32 * k] = *reinterpret_cast<const uint4*>(v);
+            }
+        }
+        return;
+    }
+    // narrow col rows (KC < 128): thread = one chunk of one pixel, consecutive
+    // threads on consecutive chunks, so every lane is busy and stores coalesce
+    for (int i = threadIdx.x; i < wo * qpp; i += blockDim.x) {
+        const int ow = i / qpp, q = i - ow * qpp;
+        const int col0 = q * 8, r = col0 / rw, t0 = col0 - r * rw;
+        const int ok = r < g.r ? min(8, max(0, span - t0)) : 0;
+        const __nv_bfloat16* base = sm + ow * g.stride_w * cv + r * wp * cv + t0;
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = e < ok ? base[e] : __float2bfloat16(0.f);
+        dst[i] = *reinterpret_cast<const uint4*>(v);
     }
 }
 
