@@ -261,6 +261,7 @@ J dispatch(const J& req) {
         out = plan_json(tc::plan_batch_size(network_of(req.at("network")), cat,
                                             req.at("gpu_bits").get<std::int64_t>(),
                                             req.at("dataset").get<std::int64_t>(), cands));
+#ifndef TCB_REFERENCE_SHIM  // this build's extension: the reference planner has no branched-graph entry
     } else if (op == "plan_batch_size_graph") {
         // branched networks: resident bits per candidate from the executor layout
         const auto cat = catalog_of(req);
@@ -270,6 +271,7 @@ J dispatch(const J& req) {
         std::sort(res.begin(), res.end());
         out = plan_json(tc::plan_batch_size_resident(cat, res, req.at("gpu_bits").get<std::int64_t>(),
                                                      req.at("dataset").get<std::int64_t>()));
+#endif
     } else if (op == "default_batch_candidates") {
         out["candidates"] = tc::default_batch_candidates(catalog_of(req));
     } else if (op == "model_caveats") {
