@@ -107,8 +107,8 @@ __global__ void avgpool2d_fwd_kernel(const T* __restrict__ x, T* __restrict__ y,
 
 // one thread per (input pixel, V channels): sum of the covering windows' dy / f^2
 template <typename T>
-__global__ void avgpool2d_bwd_kernel(const T* __restrict__ dy, T* __restrict__ dx, PoolShape ps,
-                                     const T* __restrict__ mask) {
+__global__ void avgpool2d_bwd_kernel(const T* __restrict__ dy, T* dx, PoolShape ps, const T* __restrict__ mask,
+                                     const T* residual) {
     pdl_wait();
     pdl_trigger();
     constexpr int V = Vec<T>::N;
@@ -135,6 +135,12 @@ __global__ void avgpool2d_bwd_kernel(const T* __restrict__ dy, T* __restrict__ d
             }
 #pragma unroll
         for (int e = 0; e < V; ++e) acc[e] *= inv;
+        if (residual) {  // may alias dx: read before the write below, same thread
+            float r[V];
+            load_vec(residual + i * V, r);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[e] += r[e];
+        }
         if (mask) {
             float m[V];
             load_vec(mask + i * V, m);
@@ -184,17 +190,18 @@ cudaError_t avgpool2d_fwd(DType dt, const void* x, void* y, int n, int h, int w,
 }
 
 cudaError_t avgpool2d_bwd(DType dt, const void* dy, void* dx, int n, int h, int w, int c, int f, int s, int p,
-                          cudaStream_t st, const void* mask) {
-    if (!avgpool2d_supported(dt, c) || !a16(dy) || !a16(dx) || (mask && !a16(mask))) return cudaErrorInvalidValue;
+                          cudaStream_t st, const void* mask, const void* residual) {
+    if (!avgpool2d_supported(dt, c) || !a16(dy) || !a16(dx) || (mask && !a16(mask)) || (residual && !a16(residual)))
+        return cudaErrorInvalidValue;
     PoolShape ps{n, h, w, c, (h + 2 * p - f) / s + 1, (w + 2 * p - f) / s + 1, f, s, p};
     const size_t total = size_t(n) * h * w * c / (16 / dtype_size(dt));
     if (dt == DType::F32)
         return launch_pdl(avgpool2d_bwd_kernel<float>, dim3(grid_for(total, 2)), dim3(kBlock), 0, st,
                           static_cast<const float*>(dy), static_cast<float*>(dx), ps,
-                          static_cast<const float*>(mask));
+                          static_cast<const float*>(mask), static_cast<const float*>(residual));
     return launch_pdl(avgpool2d_bwd_kernel<__nv_bfloat16>, dim3(grid_for(total, 2)), dim3(kBlock), 0, st,
                       static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx), ps,
-                      static_cast<const __nv_bfloat16*>(mask));
+                      static_cast<const __nv_bfloat16*>(mask), static_cast<const __nv_bfloat16*>(residual));
 }
 
 }  // namespace tcb

@@ -118,8 +118,9 @@ bool avgpool2d_supported(DType dt, int c);
 cudaError_t avgpool2d_fwd(DType dt, const void* x, void* y, int n, int h, int w, int c, int f, int s, int p,
                           cudaStream_t st);
 // dx = [mask > 0] * (sum of the covering windows' dy / f^2); mask may be NULL
+// residual (may alias dx): added before the mask — accumulating fan-in gradients in place
 cudaError_t avgpool2d_bwd(DType dt, const void* dy, void* dx, int n, int h, int w, int c, int f, int s, int p,
-                          cudaStream_t st, const void* mask = nullptr);
+                          cudaStream_t st, const void* mask = nullptr, const void* residual = nullptr);
 
 // ---- Winograd F(2x2,3x3) (3x3, stride 1) ----
 size_t winograd_workspace(const ConvGeom& g, ConvMode mode, DType dt);

@@ -552,7 +552,7 @@ int allocate(tcb_trainer* t, bool dry = false) {
         for (int c : nd.compute_from) {
             if (c == nd.final_writer) continue;
             const Node& con = t->nodes[c];
-            if (con.op == Op::Conv && con.algo_id == TCB_ALGO_GEMM)
+            if ((con.op == Op::Conv && con.algo_id == TCB_ALGO_GEMM) || (con.op == Op::AvgPool && con.f > 0))
                 nd.chain.push_back(c);
             else
                 nd.tmp[c] = b.take(size_t(nd.n) * nd.h * nd.w * nd.c * es);
@@ -815,6 +815,12 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
             TRY_CUDA(relu_mask_inplace(t->dt, out, t->at(tgt.act), elems, st));
             t->launches++;
         }
+        return TCB_OK;
+    }
+    if (con.op == Op::AvgPool && con.f > 0 && chained) {  // accumulate into the chain in place
+        TRY_CUDA(avgpool2d_bwd(t->dt, t->at(con.grad), out, tgt.n, tgt.h, tgt.w, tgt.c, con.f, con.s, con.p, st,
+                               nullptr, extras.empty() ? nullptr : extras[0]));
+        t->launches++;
         return TCB_OK;
     }
     if (con.op == Op::MaxPool)
