@@ -1210,19 +1210,26 @@ bool cta2_wanted(int load, int bn, int m_tiles, int kb_total) {
            kb_total >= min_kb;
 }
 
-int g_epi_kb = -1;  // TMA epilogue for layers with at most this many k-blocks
+int g_epi_kb = -1;  // TMA epilogue for 1x1 layers with at most this many k-blocks
+int g_epi_kb_spatial = -1;  // ... and for spatial (im2col) layers
 
 // The TMA epilogue needs the output rows contiguous (fwd; single-phase dgrad).
+// Thresholds measured over whole steps (scripts/ab_epi_kb.sh): 1x1 layers lose
+// past 12 k-blocks (ResNet-50's 1024-wide 1x1s), spatial ones gain up to 24
+// (Inception-v3's 5x5 / 1x7 / 7x1 branches).
 template <ConvMode MODE>
 bool use_epi(const Params& p) {
     if (MODE == ConvMode::Wgrad) return false;
     if (MODE == ConvMode::Dgrad && (p.s.sh != 1 || p.s.sw != 1)) return false;
     if (g_epi_kb < 0) {
         const char* e = getenv("TCB_CONV_EPI_KB");
-        g_epi_kb = e ? atoi(e) : 8;
+        g_epi_kb = e ? atoi(e) : 12;
+        const char* f = getenv("TCB_CONV_EPI_KB_SPATIAL");
+        g_epi_kb_spatial = f ? atoi(f) : (e ? g_epi_kb : 24);
     }
     if (p.s.Ncol % 8 != 0) return false;
-    return (p.s.Kdim + BK - 1) / BK <= g_epi_kb;
+    const int kb = (p.s.Kdim + BK - 1) / BK;
+    return kb <= (plain_geometry(p.s) ? g_epi_kb : g_epi_kb_spatial);
 }
 
 template <ConvMode MODE, int LOAD>
@@ -1311,7 +1318,7 @@ cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cuda
 }  // namespace
 
 void conv_tc_set_force_gather(int on) { g_force_gather = on ? 1 : 0; }
-void conv_tc_set_epi_kb(int kb) { g_epi_kb = kb; }
+void conv_tc_set_epi_kb(int kb) { g_epi_kb = g_epi_kb_spatial = kb; }
 void conv_tc_set_sm_reserve(int sms) { g_sm_reserve = std::max(0, sms); }
 
 bool conv_tc_supported(const ConvGeom& g, ConvMode mode) {
