@@ -1087,7 +1087,11 @@ SplitPlan plan_splits(const ConvShape& s, int bn, bool pair = false) {
     // unit (no tail round) and the fp32 partials stay as few as the wave allows
     const int slots = (num_sms() - g_sm_reserve) / (pair ? 2 : 1);
     int want = std::max(1, slots / tiles);
-    want = std::min(want, std::max(1, kb_total / 4));  // keep >= 4 k-blocks per split
+    static const int min_kb = [] {  // keep >= this many k-blocks per split
+        const char* e = getenv("TCB_SPLIT_MIN_KB");
+        return e ? std::max(1, atoi(e)) : 4;
+    }();
+    want = std::min(want, std::max(1, kb_total / min_kb));
     want = std::min(want, 64);
     const int per = (kb_total + want - 1) / want;
     return {(kb_total + per - 1) / per, per};
