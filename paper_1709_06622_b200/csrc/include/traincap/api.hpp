@@ -22,7 +22,7 @@
 #include <string_view>
 #include <vector>
 
-namespace traincap {
+namespace traincap __attribute__((visibility("default"))) {
 
 // ---------------------------------------------------------------------------
 // Errors (reference: include/traincap/errors.hpp:10-89)

@@ -564,7 +564,7 @@ int allocate(tcb_trainer* t, bool dry = false) {
     t->ws_bytes = ws;
     t->colsum_bytes = colsum;
     t->off_ws = b.take(ws);
-    t->off_pack_jobs = b.take(t->nodes.size() * sizeof(PackDgradJob));
+    t->off_pack_jobs = b.take((t->async_ps ? 2 : 1) * t->nodes.size() * sizeof(PackDgradJob));
     t->off_counters = b.take(conv_tc_counter_ints() * sizeof(int));
     t->off_colsum = b.take(colsum);
     t->off_labels = b.take(size_t(t->batch) * 4);
@@ -642,24 +642,33 @@ int initialize(tcb_trainer* t, cudaStream_t st) {
 // ------------------------------------------------------------------ step ---
 int refresh_transposes(tcb_trainer* t, cudaStream_t st) {
     if (!t->bf16) return TCB_OK;
+    // one job table per bf16 weight buffer: asynchronous PS alternates the
+    // buffer the step reads (wc_rd), and the packed w^T must come from the same
+    // weights as the forward and the other dgrads of that step
+    const int nbuf = t->async_ps ? 2 : 1;
     if (!t->pack_jobs_ready) {
-        std::vector<PackDgradJob> jobs;
-        int blocks = 0;
-        for (const Node& nd : t->nodes) {
-            if (nd.op != Op::Conv || !nd.pack_wT) continue;
-            jobs.push_back({static_cast<__nv_bfloat16*>(t->wc_ptr()) + nd.woff, t->at(nd.wT), nd.g, blocks});
-            blocks += pack_dgrad_blocks(nd.g);
+        int blocks = 0, njobs = 0;
+        for (int b = 0; b < nbuf; ++b) {
+            std::vector<PackDgradJob> jobs;
+            blocks = 0;
+            for (const Node& nd : t->nodes) {
+                if (nd.op != Op::Conv || !nd.pack_wT) continue;
+                jobs.push_back({static_cast<__nv_bfloat16*>(t->wc_buf(b)) + nd.woff, t->at(nd.wT), nd.g, blocks});
+                blocks += pack_dgrad_blocks(nd.g);
+            }
+            njobs = static_cast<int>(jobs.size());
+            if (!jobs.empty())
+                TRY_CUDA(cudaMemcpy(t->at<PackDgradJob>(t->off_pack_jobs) + size_t(b) * t->nodes.size(), jobs.data(),
+                                    jobs.size() * sizeof(PackDgradJob), cudaMemcpyHostToDevice));
         }
-        t->pack_njobs = static_cast<int>(jobs.size());
+        t->pack_njobs = njobs;
         t->pack_blocks = blocks;
-        if (!jobs.empty())
-            TRY_CUDA(cudaMemcpy(t->at(t->off_pack_jobs), jobs.data(), jobs.size() * sizeof(PackDgradJob),
-                                cudaMemcpyHostToDevice));
         t->pack_jobs_ready = true;
     }
     if (t->pack_njobs == 0) return TCB_OK;
-    TRY_CUDA(pack_dgrad_weights_batched(t->at<PackDgradJob>(t->off_pack_jobs), t->pack_njobs,
-                                        t->pack_blocks, st));
+    const size_t table = t->async_ps ? static_cast<size_t>(t->wc_rd) : 0;
+    TRY_CUDA(pack_dgrad_weights_batched(t->at<PackDgradJob>(t->off_pack_jobs) + table * t->nodes.size(),
+                                        t->pack_njobs, t->pack_blocks, st));
     t->launches++;
     return TCB_OK;
 }
@@ -1493,6 +1502,7 @@ TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
             L["init_scale"] = nd.init_scale;
             L["algo"] = nd.algo;
             L["explicit_im2col"] = nd.narrow;
+            L["packed_dgrad_weights"] = nd.pack_wT;
             const size_t first = nd.woff / std::max<size_t>(t->shard, 1);
             const size_t last_el = (nd.bias ? nd.boff + nd.g.k : nd.woff + nd.wcount) - 1;
             L["shards"] = {first, last_el / std::max<size_t>(t->shard, 1)};

@@ -187,6 +187,21 @@ def tiny_resnet(batch=4, **opts):
     return resnet50(batch, stages=(2, 1), width=8, image=20, **opts)
 
 
+def tiny_packnet(batch=4, **opts):
+    """Small chain whose middle 3x3 conv has K % 64 != 0 (96 filters) and feeds
+    a 1x1 conv, so its bf16 dgrad takes the cp.async-gather path with the
+    per-step packed w^T (the executor's pack_wT layers: AlexNet conv1-style and
+    many Inception-v3 convs)."""
+    opts.setdefault("classes", 10)
+    b = _Builder(batch, 12, 12, 8, **opts)
+    b.conv(64, 3, pad=1, bias=True)
+    b.conv(96, 3, pad=1, bias=True)
+    b.conv(64, 1)
+    b.avgpool()
+    b.fc(b.cfg["classes"], relu=False)
+    return b.done()
+
+
 def from_net(text: str, batch: int, classes: int | None = None, **opts):
     """Chain network from the reference `.net` format (input/conv/pool/fc):
     ReLU after every conv and every fc but the last; pools are max pools."""

@@ -28,6 +28,8 @@ def _port():
 
 
 def _rank_main(rank, world, port, cfg, q, steps=1):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -40,6 +42,7 @@ def _rank_main(rank, world, port, cfg, q, steps=1):
     t = Trainer(cfg, rank, world, nid[0])
     for _ in range(steps):
         t.step()
+    t.finish()
     torch.cuda.synchronize()
     d = t.describe()
     q.put((rank, d["shard"], t.tensor("param").cpu().numpy(),
@@ -150,3 +153,26 @@ def test_two_gpu_async_ps_is_one_step_stale(oracle, transport):
         sl = slice(r * per, (r + 1) * per)
         assert np.array_equal(res[r][1][sl], w2[sl]), f"rank {r} master shard"
         assert np.array_equal(res[r][2], oracle.round_bf16(w2)), f"rank {r} compute weights"
+
+
+@pytest.mark.parametrize("transport", ["nccl", "nvls"])
+def test_two_gpu_async_ps_four_steps_pack_layer(oracle, transport):
+    """Four asynchronous steps on 2 GPUs (both weight buffers read) on a model
+    with a per-step packed w^T dgrad layer: W_4 from the one-step-stale
+    recurrence over the summed per-rank gradients, bit-exact."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from async_ref import expected_async_weights
+    from paper_1709_06622_b200 import models
+    cfg = models.tiny_packnet(batch=8, precision="bf16")
+    cfg["ps_transport"] = transport
+    w0, _ = _single_rank_grads(cfg, 0)
+    res = _run_world(dict(cfg, ps_async=True), 2, steps=4)
+    w4 = expected_async_weights(oracle, cfg, w0, 4, ranks=2)
+    padded = res[0][1].size
+    w4 = np.concatenate([w4, np.zeros(padded - w4.size, np.float32)])
+    per = res[0][0]
+    for r in range(2):
+        sl = slice(r * per, (r + 1) * per)
+        assert np.array_equal(res[r][1][sl], w4[sl]), f"rank {r} master shard"
+        assert np.array_equal(res[r][2], oracle.round_bf16(w4)), f"rank {r} compute weights"

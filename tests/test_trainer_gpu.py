@@ -279,6 +279,31 @@ def test_async_ps_single_gpu_staleness_one(oracle):
     assert np.array_equal(t.tensor("wcompute").float().cpu().numpy(), oracle.round_bf16(w2))
 
 
+@pytest.mark.parametrize("model", ["tiny_resnet", "tiny_packnet"])
+def test_async_ps_four_steps_staleness_one(oracle, model):
+    """ps_async over four steps, so the step reads weight buffer 1 (steps 2)
+    as well as buffer 0: every step's gradient must be taken at the
+    one-update-old weights, including the dgrad of layers whose bf16 w^T is
+    packed per step (tiny_packnet's K = 96 3x3 conv)."""
+    from async_ref import expected_async_weights
+    from paper_1709_06622_b200.trainer import Trainer
+    cfg = getattr(_models(), model)(batch=4, precision="bf16")
+    t = Trainer(dict(cfg, ps_async=True))
+    t0 = Trainer(dict(cfg, lr=0.0))
+    t0.step()
+    torch.cuda.synchronize()
+    w0 = t0.tensor("param").cpu().numpy()
+    if model == "tiny_packnet":
+        assert any(L.get("packed_dgrad_weights") for L in t0.describe()["layers"])
+    for _ in range(4):
+        t.step()
+    t.finish()
+    torch.cuda.synchronize()
+    w4 = expected_async_weights(oracle, cfg, w0, 4)
+    assert np.array_equal(t.tensor("param").cpu().numpy(), w4)
+    assert np.array_equal(t.tensor("wcompute").float().cpu().numpy(), oracle.round_bf16(w4))
+
+
 def test_loss_decreases_over_steps():
     from paper_1709_06622_b200.trainer import Trainer
     cfg = _models().tiny_resnet(batch=8, precision="bf16", lr=0.05)
