@@ -1158,6 +1158,8 @@ bool build_epi_maps(Params& p) {
     return true;
 }
 
+ConvTcLaunchInfo g_last_launch{};  // test hook: the configuration of the last conv_tc_kernel launch
+
 template <ConvMode MODE, int BN, int LOAD, int EPI, bool CTA2 = false>
 cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
     using C = Cfg<BN, EPI, CTA2>;
@@ -1198,6 +1200,8 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = CTA2 ? 2 : 1;
+    g_last_launch = ConvTcLaunchInfo{static_cast<int>(MODE), LOAD, BN, EPI, CTA2 ? 1 : 0, p.splits,
+                                     p.num_tiles, grid, p.counters != nullptr ? 1 : 0};
     return cudaLaunchKernelEx(&cfg, conv_tc_kernel<MODE, BN, LOAD, EPI, CTA2>, p);
 }
 
@@ -1322,6 +1326,7 @@ cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cuda
 }  // namespace
 
 void conv_tc_set_force_gather(int on) { g_force_gather = on ? 1 : 0; }
+ConvTcLaunchInfo conv_tc_last_launch() { return g_last_launch; }
 void conv_tc_set_epi_kb(int kb) { g_epi_kb = g_epi_kb_spatial = kb; }
 void conv_tc_set_sm_reserve(int sms) { g_sm_reserve = std::max(0, sms); }
 

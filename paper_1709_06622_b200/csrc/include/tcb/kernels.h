@@ -63,6 +63,14 @@ bool conv_tc_supported(const ConvGeom& g, ConvMode mode);
 // 1: always use the cp.async gather operand path (tests / A-B comparisons);
 // 0: pick plain-TMA / im2col-TMA / gather per geometry.
 void conv_tc_set_force_gather(int on);
+// Test hook: configuration of the most recent conv_tc_kernel launch (mode,
+// operand path 0 gather / 1 plain TMA / 2 im2col TMA / 3 8-channel im2col,
+// tile width, TMA-epilogue slots, CTA pair, split-K factor, work units, grid,
+// in-kernel split reduction).
+struct ConvTcLaunchInfo {
+    int mode, load, bn, epi, cta2, splits, units, grid, fused_reduce;
+};
+ConvTcLaunchInfo conv_tc_last_launch();
 // TMA epilogue for layers with at most `kb` 64-deep k-blocks (0 = never,
 // -1 = default: $TCB_CONV_EPI_KB or 8).
 void conv_tc_set_epi_kb(int kb);

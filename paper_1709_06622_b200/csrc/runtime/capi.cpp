@@ -376,6 +376,14 @@ TCB_API int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_
 
 TCB_API void tcb_free(void* p) { std::free(p); }
 
+TCB_API int tcb_conv_last_launch_info(int* out9) {
+    if (!out9) return fail(TCB_ERR_INVALID, "NULL argument");
+    const ConvTcLaunchInfo i = conv_tc_last_launch();
+    const int v[9] = {i.mode, i.load, i.bn, i.epi, i.cta2, i.splits, i.units, i.grid, i.fused_reduce};
+    for (int k = 0; k < 9; ++k) out9[k] = v[k];
+    return TCB_OK;
+}
+
 TCB_API int tcb_set_conv_operand_path(int mode) {
     if (mode < 0 || mode > 2)
         return fail(TCB_ERR_INVALID, "mode must be 0 (auto), 1 (gather) or 2 (register epilogue)");

@@ -246,3 +246,14 @@ def sgd_momentum(w, g, v, lr, mom, wd=0.0, gscale=1.0, w_compute=None):
     cdt = DT[w_compute.dtype] if w_compute is not None else 0
     check(lib().tcb_sgd_momentum(_p(w), _p(g), _p(v), cdt, _p(w_compute), w.numel(), lr, mom, wd,
                                  gscale, _stream()))
+
+
+LAUNCH_FIELDS = ("mode", "load", "bn", "epi", "cta2", "splits", "units", "grid", "fused_reduce")
+
+
+def last_launch() -> dict:
+    """Configuration of the last bf16 tensor-core conv kernel launch (test hook,
+    tcb_conv_last_launch_info)."""
+    out = (ctypes.c_int * 9)()
+    check(lib().tcb_conv_last_launch_info(out))
+    return dict(zip(LAUNCH_FIELDS, list(out)))

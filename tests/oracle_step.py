@@ -48,6 +48,51 @@ class DeviceTeacher:
         return np.ascontiguousarray(a[..., :L["c_logical"]]).ravel()
 
 
+class SubsetTeacher(DeviceTeacher):
+    """The device's tensors restricted to a few images of its batch (sliced on
+    the device before the copy), for layer-local parity of a large-batch step:
+    every op but the weight gradient is independent per image."""
+
+    def __init__(self, trainer, layout, images):
+        super().__init__(trainer, layout)
+        self.images = list(images)
+
+    def _sub(self, name, i, dtype=None):
+        import torch
+        L = self.layers[i]
+        t = self.t.tensor(f"{name}:{i}", dtype=dtype).view(*L["shape"])
+        return t[torch.tensor(self.images, device=t.device)][..., :L["c_logical"]]
+
+    def act(self, i):
+        return self._sub("act", i).float().cpu().numpy()
+
+    def grad(self, i):
+        return self._sub("dact", i).float().cpu().numpy()
+
+    def argmax(self, i):
+        import torch
+        return np.ascontiguousarray(self._sub("argmax", i, torch.uint8).cpu().numpy()).ravel()
+
+    def full(self, name, i, channels=None):
+        """A whole-batch tensor (logical channels, or the given channel subset)."""
+        import torch
+        L = self.layers[i]
+        t = self.t.tensor(f"{name}:{i}").view(*L["shape"])[..., :L["c_logical"]]
+        if channels is not None:
+            t = t[..., torch.tensor(channels, device=t.device)]
+        return t.float().cpu().numpy()
+
+    def layout(self):
+        """Copy of the layout with the batch dimension set to the subset size."""
+        import copy
+        lay = copy.deepcopy({"layers": self.layers})
+        for L in lay["layers"]:
+            L["shape"][0] = len(self.images)
+            if "geom" in L:
+                L["geom"][0] = len(self.images)
+        return lay
+
+
 class OracleStep:
     def __init__(self, oracle, cfg: dict, layout: dict, rank: int = 0, world: int = 1):
         self.o = oracle
@@ -87,17 +132,30 @@ class OracleStep:
         lab = self.o.labels(n, self.cfg["classes"], self.seed + self.rank)
         return x, lab
 
-    def run(self, x=None, labels=None, teacher=None):
+    def run(self, x=None, labels=None, teacher=None, wgrad=True, loss_batch=None, argmax_src=None):
         """One step. With `teacher` (an object exposing the DEVICE's tensors:
         act(i), grad(i), argmax(i), in logical channels), every op is
         recomputed from the device's own inputs — layer-local parity — and the
-        relative error of each device output is recorded in self.local_err."""
+        relative error of each device output is recorded in self.local_err.
+        Image-subset replays of a large batch (SubsetTeacher): `loss_batch` is
+        the device's batch N (the loss gradient is (p - y) / N), and
+        wgrad=False skips the weight gradients (they sum over all N images;
+        checked separately per sampled layer). `argmax_src`: end to end, but
+        the step's discrete decisions taken from the device — max-pool argmax
+        routing and the ReLU masks (a near-tie of two window values, or a
+        pre-activation within rounding of 0, is decided by the last bit, fp32
+        vs fp64, and moves a whole gradient value). The fraction of
+        disagreeing decisions is recorded in self.argmax_mismatch /
+        self.relu_mismatch."""
         o = self.o
         if x is None:
             x, labels = self.inputs()
         act = {0: self._st(x)}
         wq = {i: (self._st(w) if self.bf16 else w) for i, (w, _) in self.params.items()}
         self.local_err = {}
+        self.argmax_mismatch = {}
+        self.relu_mismatch = {}
+        relu_on = {}
 
         def adopt(kind, i, ref, dev_value):
             if teacher is None:
@@ -114,7 +172,15 @@ class OracleStep:
                 xin = act[L["in"]]
                 g = self._geom(L, xin.shape[-1])
                 res = act[L["residual"]] if L["residual"] >= 0 else None
-                y = o.conv_fwd(g, xin, wq[i], bias=self.params[i][1], residual=res, relu=L["relu"])
+                if argmax_src is not None and L["relu"] and teacher is None:
+                    pre = o.conv_fwd(g, xin, wq[i], bias=self.params[i][1], residual=res, relu=False)
+                    pre = pre.reshape(g["n"], L["shape"][1], L["shape"][2], g["k"])
+                    dev_on = argmax_src.act(i) > 0
+                    self.relu_mismatch[L["name"]] = float(np.mean(dev_on != (pre > 0)))
+                    y = np.where(dev_on, pre, 0.0)
+                    relu_on[i] = dev_on
+                else:
+                    y = o.conv_fwd(g, xin, wq[i], bias=self.params[i][1], residual=res, relu=L["relu"])
                 y = self._st(y).reshape(g["n"], L["shape"][1], L["shape"][2], g["k"])
                 act[i] = adopt("fwd", i, y, teacher.act(i) if teacher else None)
             elif L["op"] == "maxpool":
@@ -124,7 +190,14 @@ class OracleStep:
                 y, arg = o.maxpool_fwd(xin, n, h, w, c, f, s, p)
                 y = self._st(y).reshape(L["shape"][0], L["shape"][1], L["shape"][2], c)
                 act[i] = adopt("fwd", i, y, teacher.act(i) if teacher else None)
-                L["_arg"] = teacher.argmax(i) if teacher else arg
+                if teacher:
+                    L["_arg"] = teacher.argmax(i)
+                elif argmax_src is not None:
+                    dev_arg = argmax_src.argmax(i)
+                    self.argmax_mismatch[L["name"]] = float(np.mean(dev_arg != arg))
+                    L["_arg"] = dev_arg
+                else:
+                    L["_arg"] = arg
             elif L["op"] == "avgpool":
                 xin = act[L["in"]]
                 n, h, w, c = xin.shape
@@ -142,6 +215,8 @@ class OracleStep:
                 z = act[L["in"]]
                 n = z.shape[0]
                 loss, dl = o.softmax_xent(z.reshape(n, -1), labels, n, z.shape[-1])
+                if loss_batch:
+                    dl = dl * (n / loss_batch)
                 logits_idx = L["in"]
                 dlogits = self._st(dl).reshape(z.shape)
                 dlogits = adopt("grad", logits_idx, dlogits,
@@ -158,15 +233,16 @@ class OracleStep:
                 parts = contrib.get(i, [])
                 tot = np.sum(parts, axis=0) if parts else np.zeros_like(act[i], np.float64)
                 if L["op"] == "conv" and L["relu"]:
-                    tot = np.where(act[i] > 0, tot, 0.0)
+                    tot = np.where(relu_on[i] if i in relu_on else act[i] > 0, tot, 0.0)
                 ref = self._st(tot).reshape(act[i].shape)
                 G[i] = adopt("grad", i, ref, teacher.grad(i) if teacher else None)
             gi = G[i]
             if L["op"] == "conv":
                 xin = act[L["in"]]
                 g = self._geom(L, xin.shape[-1])
-                dw, db = o.conv_wgrad(g, gi, xin, want_db=True)
-                grads[i] = (dw, db if L["bias"] else None)
+                if wgrad:
+                    dw, db = o.conv_wgrad(g, gi, xin, want_db=True)
+                    grads[i] = (dw, db if L["bias"] else None)
                 if L["residual"] >= 0 and self.layers[L["residual"]]["op"] != "input":
                     contrib.setdefault(L["residual"], []).append(gi.astype(np.float64))
                 if self.layers[L["in"]]["op"] != "input":

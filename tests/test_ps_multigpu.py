@@ -176,3 +176,30 @@ def test_two_gpu_async_ps_four_steps_pack_layer(oracle, transport):
         sl = slice(r * per, (r + 1) * per)
         assert np.array_equal(res[r][1][sl], w4[sl]), f"rank {r} master shard"
         assert np.array_equal(res[r][2], oracle.round_bf16(w4)), f"rank {r} compute weights"
+
+
+def test_four_gpu_nvls_matches_nccl_within_fp32_tolerance():
+    """4 GPUs, three steps (the third a replayed CUDA graph): the NVSwitch
+    multicast PS step (multimem.ld_reduce sums the four fp32 gradients in the
+    switch, in an unspecified order) against NCCL reduce-scatter + SGD +
+    all-gather. A 4-term fp32 sum is order-dependent, so the master weights
+    agree to fp32 rounding (normwise 1e-6) rather than bitwise, and the
+    gathered bf16 copies differ only where that rounding crosses a bf16 tie."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    from oracle_binding import rel_err
+    from paper_1709_06622_b200 import models
+    cfg = models.tiny_resnet(batch=8, precision="bf16")
+    ref = _run_world(dict(cfg, ps_transport="nccl"), 4, steps=3)
+    got = _run_world(dict(cfg, ps_transport="nvls"), 4, steps=3)
+    w0 = _single_rank_grads(cfg, 0)[0]
+    for r in range(4):
+        per = ref[r][0]
+        sl = slice(r * per, (r + 1) * per)
+        d_ref = ref[r][1][sl] - np.concatenate([w0, np.zeros(ref[r][1].size - w0.size, np.float32)])[sl]
+        d_got = got[r][1][sl] - np.concatenate([w0, np.zeros(got[r][1].size - w0.size, np.float32)])[sl]
+        e = rel_err(d_got, d_ref)  # on the update itself, not the weights
+        print(f"rank {r}: normwise update difference nvls vs nccl = {e:.3e}")
+        assert e <= 1e-5, (r, e)
+        mism = np.mean(got[r][2] != ref[r][2])
+        assert mism <= 1e-3, (r, mism)
