@@ -138,22 +138,17 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU oracle ---
 def cpu_oracle_step(model, precision, steps=1, batch=1):
-    """Time the CPU oracle training step (tests/oracle_step.py over oracle/liboracle.so)."""
-    import ctypes
-
+    """Time the CPU oracle training step (tests/oracle_step.py over
+    oracle/liboracle.so). The model layout comes from its Python restatement
+    (tests/layout_oracle.py), so this arm loads nothing from the product."""
+    import layout_oracle
     import oracle_binding
     import oracle_step
-    from paper_1709_06622_b200 import device, models, trainer
+    from paper_1709_06622_b200 import models
 
     orc = oracle_binding.Oracle(os.path.join(ROOT, "oracle", "liboracle.so"))
     cfg = models.build(model, batch=batch, precision=precision)
-    L = trainer._lib()
-    h = ctypes.c_void_p()
-    device.check(L.tcb_trainer_create(json.dumps(cfg).encode(), ctypes.byref(h)))
-    out = ctypes.c_char_p()
-    device.check(L.tcb_trainer_describe(h, ctypes.byref(out)))
-    layout = json.loads(out.value.decode())
-    L.tcb_trainer_destroy(h)
+    layout = layout_oracle.describe(cfg)
     st = oracle_step.OracleStep(orc, cfg, layout)
     x, lab = st.inputs()
     times = []
@@ -297,25 +292,70 @@ def ps_bandwidth(phases, world, param_bytes, transport="nccl"):
             "ag_frac": round(ag / pag, 3), "peak_kind": src}
 
 
-def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
-    """Dominant kernel = the tcgen05 implicit-GEMM conv (every fwd/dgrad/wgrad
-    pass of the step). achieved = algorithmic conv FLOP of the step / the sum of
-    the conv passes' CUDA-event times measured inside a real training step
-    (real cache state; each pass includes its split-K reduction / bias sum)."""
+def tensor_peak(pk, precision):
+    """Dense tensor / FMA peak for the precision: bf16 from MEASURED_PEAKS.json
+    (sustained: the conv kernels run inside a long step); tf32 and fp32-FFMA
+    from profiles/*_measured_peaks_tf32_ffma.json (cuBLAS measured the same
+    way by scripts/measure_peaks.py) when present."""
+    if precision == "bf16":
+        return pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1400.0)), \
+            f"bf16 dense sustained, cuBLAS ({pk['source']} MEASURED_PEAKS.json)"
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_measured_peaks_tf32_ffma.json")))
+    if files:
+        with open(files[-1]) as f:
+            d = json.load(f)
+        key = "tf32_tflops_sustained" if precision == "tf32" else "fp32_tflops_sustained"
+        return d[key], f"{precision} sustained, cuBLAS measured (profiles/{os.path.basename(files[-1])})"
+    if precision == "tf32":
+        return pk.get("bf16_tflops_sustained", 1400.0) / 2, "tf32 = bf16 / 2 (assumed: no tf32 measurement)"
+    return 75.0, "fp32 FFMA nominal (assumed: no measurement)"
+
+
+def in_step_roofline(rows, pk, precision, model="resnet50", batch=256, kernels=None, step_ms=None):
+    """Dominant kernel = the tensor-core implicit-GEMM conv (every fwd/dgrad/
+    wgrad pass of the step). achieved = algorithmic conv FLOP of one step / the
+    summed device durations of that kernel's launches in one graph-replayed
+    step, exactly as the timed region runs it (CUPTI activity records;
+    `kernels`). Its share of all kernel time in that step, times the timed
+    ms/step, is the conv time inside the driver-timed step (<= ms/step). The
+    eager per-pass CUDA-event times (`rows`, events between passes, no graph or
+    PDL overlap) only split the passes into tensor- and HBM-bound ones."""
     flop = 0.0
-    ms = 0.0
+    ev_ms = 0.0
     for r in rows:
         passes = [r["fwd_ms"], r["wgrad_ms"]] + ([r["dgrad_ms"]] if r["dgrad_ms"] is not None else [])
         flop += r["flop"] * len(passes)
-        ms += sum(passes)
-    achieved = flop / ms / 1e9
-    peak = pk["bf16_tflops_sustained"] if "bf16_tflops_sustained" in pk else pk.get("bf16_tflops", 1590.0)
-    if precision == "tf32":  # dense tf32 tensor peak = half the bf16 one (1.1 vs 2.25 PF nominal)
-        peak = peak / 2
-    # per-pass roofline time max(FLOP / tensor peak, bytes / HBM peak), summed
+        ev_ms += sum(passes)
+    peak, peak_kind = tensor_peak(pk, precision)
     hbm = pk.get("hbm_gbs", 6548.2)
+    name = CONV_KERNEL[precision]
+    conv_us = step_us = None
+    launches = 0
+    if kernels:
+        step_us = sum(d for _, _, d in kernels)
+        conv = [d for n, _, d in kernels if name in n]
+        conv_us, launches = sum(conv), len(conv)
+    if conv_us:
+        achieved = flop / (conv_us * 1e-6) / 1e12
+        timing = ("CUPTI activity durations of every conv kernel launch in one graph-replayed step "
+                  "(torch.profiler, second of two profiled steps after the timed region)")
+    else:  # no CUPTI: the eager layer-event times
+        achieved = flop / ev_ms / 1e9
+        timing = "CUDA events around each conv pass of one eager step (no CUPTI records)"
+    share = conv_us / step_us if conv_us and step_us else None
+    out = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+           "frac": round(achieved / peak, 4), "traffic": None,
+           "kernel": f"{name} (tcgen05/TMEM implicit GEMM, TMA operands; all conv passes of one step)",
+           "flop_per_step": flop, "launches_per_step": launches or None,
+           "conv_kernel_ms_per_step": round(conv_us / 1e3, 3) if conv_us else None,
+           "step_kernel_ms": round(step_us / 1e3, 3) if step_us else None,
+           "conv_share_of_step_kernel_time": round(share, 4) if share else None,
+           "conv_ms_in_timed_step": round(share * step_ms, 3) if share and step_ms else None,
+           "timing": timing, "peak_kind": peak_kind,
+           "frac_of_burst_peak": round(achieved / (pk.get("bf16_tflops", 1590.0)), 4) if precision == "bf16" else None}
+    # per-pass split by each pass's own bound (eager layer events; diagnostics)
     bound_ms, tensor_ms, hbm_ms, nbytes = 0.0, 0.0, 0.0, 0.0
-    # passes split by their own roofline bound (arithmetic intensity vs ridge)
     split = {"tensor": [0, 0.0, 0.0, 0.0], "hbm": [0, 0.0, 0.0, 0.0]}  # count, flop, bytes, ms
     for r in rows:
         for pname in ("fwd", "dgrad", "wgrad"):
@@ -332,35 +372,80 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256):
             sp[1] += r["flop"]
             sp[2] += r.get(pname + "_bytes", 0)
             sp[3] += r[pname + "_ms"]
-    traffic, tsrc = None, None
-    tpath = os.path.join(ROOT, "profiles", f"r01_conv_traffic_{model}_bs{batch}.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
+    import glob
+    tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_conv_traffic_{model}_bs{batch}.json")))
+    if tfiles and precision == "bf16":
+        with open(tfiles[-1]) as f:
             tj = json.load(f)
-        traffic = tj["conv_dram_bytes_per_step"]
-        tsrc = f"profiles/{os.path.basename(tpath)}: {tj['source']}"
-    return {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic,
-            "traffic_unit": "DRAM bytes per step, all conv_tc launches (same unit as flop_per_step)",
-            "traffic_source": tsrc,
-            "kernel": "conv_tc_kernel (tcgen05/TMEM implicit GEMM, TMA im2col; all conv passes of one step)",
-            "flop_per_step": flop, "conv_ms_per_step": round(ms, 3),
-            "frac_of_burst_peak": round(achieved / (pk.get("bf16_tflops", 1590.0) / (2 if precision == "tf32" else 1)), 4),
-            "algorithmic_bytes_per_step": nbytes,
-            "combined_roofline": {
-                "bound_ms": round(bound_ms, 3), "tensor_only_ms": round(tensor_ms, 3),
-                "hbm_only_ms": round(hbm_ms, 3), "measured_ms": round(ms, 3),
-                "frac": round(bound_ms / ms, 4),
-                "note": "sum over conv passes of max(FLOP/tensor peak, algorithmic bytes/HBM peak)"},
-            "tensor_bound_passes": {
-                "count": split["tensor"][0], "ms": round(split["tensor"][3], 3),
-                "achieved_TFLOPs": round(split["tensor"][1] / max(split["tensor"][3], 1e-9) / 1e9, 1),
-                "frac_of_tensor_peak": round(split["tensor"][1] / max(split["tensor"][3], 1e-9) / 1e9 / peak, 4)},
-            "hbm_bound_passes": {
-                "count": split["hbm"][0], "ms": round(split["hbm"][3], 3),
-                "achieved_GBps": round(split["hbm"][2] / max(split["hbm"][3], 1e-9) / 1e6, 1),
-                "frac_of_hbm_peak": round(split["hbm"][2] / max(split["hbm"][3], 1e-9) / 1e6 / hbm, 4)},
-            "peak_kind": f"bf16 dense sustained ({pk['source']}; kernel timed inside the step)"}
+        out["traffic"] = tj["conv_dram_bytes_per_step"]
+        out["traffic_unit"] = "DRAM bytes per step, all conv launches (same unit as flop_per_step)"
+        out["traffic_source"] = f"profiles/{os.path.basename(tfiles[-1])}: {tj['source']}"
+    out["algorithmic_bytes_per_step"] = nbytes
+    out["combined_roofline"] = {
+        "bound_ms": round(bound_ms, 3), "tensor_only_ms": round(tensor_ms, 3), "hbm_only_ms": round(hbm_ms, 3),
+        "measured_ms": round(conv_us / 1e3, 3) if conv_us else round(ev_ms, 3),
+        "frac": round(bound_ms / (conv_us / 1e3 if conv_us else ev_ms), 4),
+        "note": "sum over conv passes of max(FLOP/tensor peak, algorithmic bytes/HBM peak) vs the in-graph conv time"}
+    out["eager_layer_events"] = {
+        "conv_ms": round(ev_ms, 3),
+        "tensor_bound_passes": {
+            "count": split["tensor"][0], "ms": round(split["tensor"][3], 3),
+            "achieved_TFLOPs": round(split["tensor"][1] / max(split["tensor"][3], 1e-9) / 1e9, 1),
+            "frac_of_tensor_peak": round(split["tensor"][1] / max(split["tensor"][3], 1e-9) / 1e9 / peak, 4)},
+        "hbm_bound_passes": {
+            "count": split["hbm"][0], "ms": round(split["hbm"][3], 3),
+            "achieved_GBps": round(split["hbm"][2] / max(split["hbm"][3], 1e-9) / 1e6, 1),
+            "frac_of_hbm_peak": round(split["hbm"][2] / max(split["hbm"][3], 1e-9) / 1e6 / hbm, 4)}}
+    return out
+
+
+# ------------------------------------------- kernels inside the graph step ---
+CONV_KERNEL = {"bf16": "conv_tc_kernel", "tf32": "conv_tf32_kernel", "ffma": "conv_ffma_kernel"}
+
+
+def step_kernels(tr, steps=2):
+    """Every kernel of `steps` training steps exactly as the timed region runs
+    them (the replayed CUDA graph, PDL overlap included), with its device
+    duration from CUPTI activity records (torch.profiler; kernels launched by
+    libtcb.so and NCCL alike). Returns per-step lists of (name, start_us, dur_us)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            tr.step()
+        tr.finish()
+        torch.cuda.synchronize()
+    path = tempfile.mktemp(suffix=".json")
+    prof.export_chrome_trace(path)
+    with open(path) as f:
+        trace = json.load(f)
+    os.unlink(path)
+    ks = sorted((e["ts"], e["dur"], e["name"]) for e in trace.get("traceEvents", [])
+                if e.get("cat") == "kernel" and "dur" in e)
+    if not ks:
+        return []
+    # split into steps at the largest gaps between consecutive kernels
+    per = len(ks) // steps if steps else len(ks)
+    return [[(n, ts, d) for ts, d, n in ks[i * per:(i + 1) * per]] for i in range(steps)]
+
+
+def summarize_step(kernels):
+    """Kernel classes of one step: count, summed device time, share."""
+    import re
+    tot = sum(d for _, _, d in kernels) or 1.0
+    cls = {}
+    for n, _, d in kernels:
+        key = re.sub(r"\(.*", "", n)
+        key = key.replace("void ", "").replace("tcb::", "").replace("(anonymous namespace)::", "")
+        c = cls.setdefault(key, [0, 0.0])
+        c[0] += 1
+        c[1] += d
+    span = (kernels[-1][1] + kernels[-1][2] - kernels[0][1]) if kernels else 0.0
+    return {"kernels": len(kernels), "kernel_us": round(tot, 1), "span_us": round(span, 1),
+            "classes": {k: {"n": v[0], "us": round(v[1], 1), "share": round(v[1] / tot, 4)}
+                        for k, v in sorted(cls.items(), key=lambda kv: -kv[1][1])}}
 
 
 # ------------------------------------------------------------------ main ---
@@ -515,10 +600,17 @@ def main():
                "ms_per_step": round(ems / args.steps, 3),
                "input": "uint8 NHWC pixels, pinned, staged one step ahead on a copy stream"}
 
+    # every kernel of two more steps exactly as timed (graph replay), CUPTI durations
+    kern_steps = step_kernels(tr, 2)
+    step_kern = summarize_step(kern_steps[-1]) if kern_steps else None
     pk = peaks()
     roof = None
     if rank == 0:
-        roof = in_step_roofline(layer_rows, pk, args.precision, args.model, args.batch)
+        roof = in_step_roofline(layer_rows, pk, args.precision, args.model, args.batch,
+                                kern_steps[-1] if kern_steps else None, ms / args.steps)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", f"step_kernels_{args.model}_{args.precision}_g{world}.json"), "w") as f:
+            json.dump({"summary": step_kern, "kernels": kern_steps[-1] if kern_steps else []}, f, indent=1)
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         with open(os.path.join(ROOT, "gpurun_out", f"conv_in_step_{args.model}_{args.precision}.json"), "w") as f:
             json.dump(layer_rows, f, indent=1)
@@ -575,6 +667,9 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "phases_ms": {k: round(v, 3) for k, v in phases.items()},
+            "step_kernels": ({k: step_kern[k] for k in ("kernels", "kernel_us", "span_us")} |
+                             {"top": dict(list(step_kern["classes"].items())[:8]),
+                              "source": "CUPTI, one graph-replayed step"}) if step_kern else None,
             "loss": loss,
             "hbm_arena_bytes": layout.get("arena_bytes"),
             "ps": {"param_bytes": param_bytes, "rs_ag_bytes_per_gpu_step": rs_ag_bytes,

@@ -99,3 +99,31 @@ def test_gloo_two_ranks_agree_on_shard_table():
         assert (r0, r1) == (0, 1)
         assert (s0, p0, t0) == (s1, p1, t1)
         assert s0 * 2 == p0
+
+
+KEYS = ("index", "name", "op", "in", "residual", "shape", "c_logical", "conv_index", "geom", "relu",
+        "bias", "woff", "wcount", "boff", "algo", "shards", "pool", "ins", "coff")
+
+
+@pytest.mark.parametrize("precision", ["bf16", "ffma"])
+@pytest.mark.parametrize("model,kw", MODELS, ids=[m for m, _ in MODELS])
+def test_full_description_matches_restatement(model, kw, precision):
+    """tests/layout_oracle.py (what the CPU oracle step and bench's reference
+    arm use instead of the product library) reproduces tcb_trainer_describe
+    node for node, init scales bit-exact in fp32."""
+    import numpy as np
+
+    import layout_oracle
+    from paper_1709_06622_b200 import models
+    cfg = models.build(model, precision=precision, **kw)
+    dev = _describe(cfg)
+    ref = layout_oracle.describe(cfg)
+    for k in ("param_count", "param_padded", "shard", "batch", "classes"):
+        assert dev[k] == ref[k], k
+    assert len(dev["layers"]) == len(ref["layers"])
+    for a, b in zip(dev["layers"], ref["layers"]):
+        for k in KEYS:
+            if k in a or k in b:
+                assert a.get(k) == b.get(k), (a["name"], k, a.get(k), b.get(k))
+        if a["op"] == "conv":
+            assert np.float32(a["init_scale"]) == np.float32(b["init_scale"]), a["name"]
