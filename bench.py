@@ -332,14 +332,19 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256, kernels=N
     name = CONV_KERNEL[precision]
     conv_us = step_us = None
     launches = 0
+    raw_us = None
     if kernels:
-        step_us = sum(d for _, _, d in kernels)
-        conv = [d for n, _, d in kernels if name in n]
-        conv_us, launches = sum(conv), len(conv)
+        ex = exclusive_times(kernels)
+        step_us = sum(e for *_, e in ex)
+        conv = [(d, e) for n, _, d, e in ex if name in n]
+        conv_us, launches = sum(e for _, e in conv), len(conv)
+        raw_us = sum(d for d, _ in conv)
     if conv_us:
         achieved = flop / (conv_us * 1e-6) / 1e12
-        timing = ("CUPTI activity durations of every conv kernel launch in one graph-replayed step "
-                  "(torch.profiler, second of two profiled steps after the timed region)")
+        timing = ("CUPTI activity records of every conv kernel launch in one graph-replayed step "
+                  "(torch.profiler, second of two profiled steps after the timed region); exclusive "
+                  "time: PDL lets a kernel start while its predecessor drains, so each instant is "
+                  "attributed to the earliest-started running kernel")
     else:  # no CUPTI: the eager layer-event times
         achieved = flop / ev_ms / 1e9
         timing = "CUDA events around each conv pass of one eager step (no CUPTI records)"
@@ -349,6 +354,7 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256, kernels=N
            "kernel": f"{name} (tcgen05/TMEM implicit GEMM, TMA operands; all conv passes of one step)",
            "flop_per_step": flop, "launches_per_step": launches or None,
            "conv_kernel_ms_per_step": round(conv_us / 1e3, 3) if conv_us else None,
+           "conv_kernel_ms_raw_durations": round(raw_us / 1e3, 3) if raw_us else None,
            "step_kernel_ms": round(step_us / 1e3, 3) if step_us else None,
            "conv_share_of_step_kernel_time": round(share, 4) if share else None,
            "conv_ms_in_timed_step": round(share * step_ms, 3) if share and step_ms else None,
@@ -431,21 +437,50 @@ def step_kernels(tr, steps=2):
     return [[(n, ts, d) for ts, d, n in ks[i * per:(i + 1) * per]] for i in range(steps)]
 
 
-def summarize_step(kernels):
-    """Kernel classes of one step: count, summed device time, share."""
+def exclusive_times(kernels):
+    """Per-kernel EXCLUSIVE device time: with programmatic dependent launch a
+    kernel is resident (and its CUPTI duration runs) while it waits in
+    griddepcontrol.wait for its predecessor, so raw durations overlap. Each
+    instant of the step is attributed to the earliest-started kernel still
+    running (the one doing the work the others wait for); the exclusive times
+    then sum to the busy span of the step."""
+    out = []
+    frontier = None  # latest end time covered so far
+    for n, ts, d in kernels:  # sorted by start
+        end = ts + d
+        if frontier is None or ts >= frontier:
+            ex = d
+        else:
+            ex = max(0.0, end - frontier)
+        frontier = end if frontier is None else max(frontier, end)
+        out.append((n, ts, d, ex))
+    return out
+
+
+def kernel_class(name):
     import re
-    tot = sum(d for _, _, d in kernels) or 1.0
+    n = name.replace("(anonymous namespace)::", "").replace("void ", "").replace("tcb::", "")
+    n = re.sub(r"<.*>", "", n)
+    return re.sub(r"\(.*\)$", "", n).strip()
+
+
+def summarize_step(kernels):
+    """Kernel classes of one step: count, summed raw and exclusive device time."""
+    ex = exclusive_times(kernels)
+    tot = sum(e for *_, e in ex) or 1.0
+    raw = sum(d for _, _, d in kernels)
     cls = {}
-    for n, _, d in kernels:
-        key = re.sub(r"\(.*", "", n)
-        key = key.replace("void ", "").replace("tcb::", "").replace("(anonymous namespace)::", "")
-        c = cls.setdefault(key, [0, 0.0])
+    for n, _, d, e in ex:
+        c = cls.setdefault(kernel_class(n), [0, 0.0, 0.0])
         c[0] += 1
         c[1] += d
-    span = (kernels[-1][1] + kernels[-1][2] - kernels[0][1]) if kernels else 0.0
-    return {"kernels": len(kernels), "kernel_us": round(tot, 1), "span_us": round(span, 1),
-            "classes": {k: {"n": v[0], "us": round(v[1], 1), "share": round(v[1] / tot, 4)}
-                        for k, v in sorted(cls.items(), key=lambda kv: -kv[1][1])}}
+        c[2] += e
+    span = (max(ts + d for _, ts, d in kernels) - kernels[0][1]) if kernels else 0.0
+    return {"kernels": len(kernels), "kernel_us_raw": round(raw, 1), "kernel_us_exclusive": round(tot, 1),
+            "span_us": round(span, 1),
+            "classes": {k: {"n": v[0], "us_raw": round(v[1], 1), "us_exclusive": round(v[2], 1),
+                            "share": round(v[2] / tot, 4)}
+                        for k, v in sorted(cls.items(), key=lambda kv: -kv[1][2])}}
 
 
 # ------------------------------------------------------------------ main ---
@@ -667,7 +702,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "phases_ms": {k: round(v, 3) for k, v in phases.items()},
-            "step_kernels": ({k: step_kern[k] for k in ("kernels", "kernel_us", "span_us")} |
+            "step_kernels": ({k: step_kern[k] for k in ("kernels", "kernel_us_exclusive", "span_us")} |
                              {"top": dict(list(step_kern["classes"].items())[:8]),
                               "source": "CUPTI, one graph-replayed step"}) if step_kern else None,
             "loss": loss,

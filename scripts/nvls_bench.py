@@ -99,8 +99,11 @@ for n in (1 << 22, 1 << 24, 25_559_040):
            "nvlink_counters_rank0_nccl_rs_ag_x20": rcnt,
            "nvlink_counters_rank0_nccl_per_step_GB": (
                {k: round(v / 20 / 1e9, 4) for k, v in rcnt.items()} if rcnt else None),
-           "algorithmic_egress_GB_fused": round((shard * 4 * (world - 1) + shard * 2 * (world - 1)) / 1e9, 4),
-           "algorithmic_egress_GB_rs_ag": round((shard * 4 * (world - 1) + shard * 2 * (world - 1)) / 1e9, 4)}
+           # per GPU and launch: NVLS reads every GPU's whole fp32 buffer through the switch
+           # (own shard included) and multicasts the bf16 shard once; RS + AG move the
+           # other ranks' (G-1)/G of the fp32 buffer out and the bf16 shard to G-1 peers
+           "model_egress_GB_fused": round((n * 4 + shard * 2) / 1e9, 4),
+           "model_egress_GB_rs_ag": round((shard * 4 * (world - 1) + shard * 2 * (world - 1)) / 1e9, 4)}
     out["rows"].append(row)
     del g, wc, hg, hw
 if rank == 0:
