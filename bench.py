@@ -217,7 +217,19 @@ def conv_roofline(cfg, pk, reps=5):
             "peak_kind": f"bf16 dense burst ({pk['source']})"}, per_layer
 
 
-NVLINK_PEER_GBPS = 770.0  # measured per-direction peer bandwidth (B200_PROFILING.md)
+def _nvlink_peak():
+    """Per-direction NVLink peer bandwidth measured on this pool's boxes
+    (scripts/nvlink_peak.py -> profiles/r*_nvlink_peak_g2.json), else the
+    guide's 770 GB/s."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_nvlink_peak_g*.json")))
+    if files:
+        with open(files[-1]) as f:
+            return json.load(f)["peer_copy_GBps_per_direction"], f"measured peer copy (profiles/{os.path.basename(files[-1])})"
+    return 770.0, "peer copy per direction, B200_PROFILING.md (fallback)"
+
+
+NVLINK_PEER_GBPS, NVLINK_PEER_SRC = _nvlink_peak()
 
 
 def lemmas(phases, world, param_bytes, out_dir, transport="nccl"):
@@ -265,7 +277,7 @@ def busbw_peak(world, op):
             d = json.load(f)
         best = max(r["busbw_GBps"] for r in d["results"] if r["op"] == op)
         return best, f"NCCL {d['nccl']} {op} microbenchmark, best over 8 MB-1 GB (profiles/{os.path.basename(path)})"
-    return NVLINK_PEER_GBPS, "peer copy per direction, B200_PROFILING.md (fallback)"
+    return NVLINK_PEER_GBPS, NVLINK_PEER_SRC
 
 
 def ps_bandwidth(phases, world, param_bytes, transport="nccl"):
@@ -282,7 +294,7 @@ def ps_bandwidth(phases, world, param_bytes, transport="nccl"):
                 "nvlink_egress_GBps_per_gpu": round(egress / t / 1e9, 1),
                 "nvlink_peak_GBps": NVLINK_PEER_GBPS, "nvlink_frac": round(egress / t / 1e9 / NVLINK_PEER_GBPS, 3),
                 "rs_ag_equivalent_busbw_GBps": round(param_bytes * (world - 1) / world / t / 1e9, 1),
-                "peak_kind": "peer copy per direction, B200_PROFILING.md"}
+                "peak_kind": NVLINK_PEER_SRC}
     rs = param_bytes * (world - 1) / world / (phases["reduce_scatter"] / 1e3) / 1e9
     ag = (param_bytes / 2) * (world - 1) / world / (phases["all_gather"] / 1e3) / 1e9  # bf16 refresh
     prs, src = busbw_peak(world, "reduce_scatter")
@@ -336,7 +348,7 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256, kernels=N
     if kernels:
         ex = exclusive_times(kernels)
         step_us = sum(e for *_, e in ex)
-        conv = [(d, e) for n, _, d, e in ex if name in n]
+        conv = [(d, e) for n, _, d, e in ex if any(k in n for k in name)]
         conv_us, launches = sum(e for _, e in conv), len(conv)
         raw_us = sum(d for d, _ in conv)
     if conv_us:
@@ -351,7 +363,7 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256, kernels=N
     share = conv_us / step_us if conv_us and step_us else None
     out = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
            "frac": round(achieved / peak, 4), "traffic": None,
-           "kernel": f"{name} (tcgen05/TMEM implicit GEMM, TMA operands; all conv passes of one step)",
+           "kernel": f"{' + '.join(name)} (tcgen05/TMEM implicit GEMM, TMA operands; all conv passes of one step)",
            "flop_per_step": flop, "launches_per_step": launches or None,
            "conv_kernel_ms_per_step": round(conv_us / 1e3, 3) if conv_us else None,
            "conv_kernel_ms_raw_durations": round(raw_us / 1e3, 3) if raw_us else None,
@@ -406,7 +418,8 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256, kernels=N
 
 
 # ------------------------------------------- kernels inside the graph step ---
-CONV_KERNEL = {"bf16": "conv_tc_kernel", "tf32": "conv_tf32_kernel", "ffma": "conv_ffma_kernel"}
+CONV_KERNEL = {"bf16": ("conv_tc_kernel", "conv_win_kernel"), "tf32": ("conv_tf32_kernel",),
+               "ffma": ("conv_ffma_kernel",)}
 
 
 def step_kernels(tr, steps=2):

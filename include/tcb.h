@@ -88,12 +88,17 @@ int tcb_conv_plan_destroy(tcb_conv_plan* plan);
  * gather otherwise; TMA-store epilogue on K-light layers), 1 = force the
  * cp.async gather path, 2 = automatic loads with the register epilogue
  * everywhere (A/B testing). */
-int tcb_set_conv_operand_path(int mode);
+int tcb_set_conv_operand_path(int mode); /* 0 auto, 1 gather, 2 register epilogue, 3 auto w/o window,
+                                           4 window wherever it applies */
 /* Test hook: the configuration of the last bf16 tensor-core conv kernel launch
  * on this process: {mode (0 fwd / 1 dgrad / 2 wgrad), operand path (0 cp.async
- * gather, 1 2-D TMA, 2 im2col TMA, 3 8-channel im2col TMA), tile N, TMA-epilogue
- * slots, CTA pair, split-K factor, work units, grid CTAs, in-kernel split reduce}. */
-int tcb_conv_last_launch_info(int* out9);
+ * gather, 1 2-D TMA, 2 im2col TMA, 3 8-channel im2col TMA, 4 window), tile N,
+ * TMA-epilogue slots, CTA pair, split-K factor, work units, grid CTAs, in-kernel
+ * split reduce, weight operand resident in shared memory}. */
+int tcb_conv_last_launch_info(int* out10);
+/* Diagnostics: per-CTA role timing of the window conv kernel (8 x u64 per CTA)
+ * written to a device buffer on each launch; NULL switches it off. */
+int tcb_conv_win_debug(void* dev_buffer);
 
 /* y = act(conv(x, w) + bias + residual); bias (fp32, K) and residual (same
  * dtype/shape as y) may be NULL; relu != 0 applies max(0, .). */

@@ -683,7 +683,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
-                if (ptx::elect_one()) {
+                {
+                    // warp-collective issue: all lanes run the loop, one elected lane
+                    // issues each tcgen05 instruction (no divergent region per k-block)
                     const uint32_t a_addr = smem_base + stage * C::kStageBytes;
                     const uint32_t b_addr = a_addr + C::kABytes;
 #pragma unroll
@@ -703,24 +705,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                             bd = ptx::sw128_desc(b_addr + k * 32, 16, 1024);
                         }
                         if constexpr (CTA2)
-                            ptx::umma_f16_2sm(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
+                            ptx::umma_f16_2sm_elect(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
                         else
-                            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
+                            ptx::umma_f16_elect(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
                     }
-                    if constexpr (CTA2) ptx::umma_commit_2sm(&empty[stage], 3);
-                    else ptx::umma_commit(&empty[stage]);
+                    if constexpr (CTA2) ptx::umma_commit_2sm_elect(&empty[stage], 3);
+                    else ptx::umma_commit_elect(&empty[stage]);
                 }
-                __syncwarp();
                 if (++stage == C::kStages) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (ptx::elect_one()) {
-                if constexpr (CTA2) ptx::umma_commit_2sm(&tfull[acc], 3);
-                else ptx::umma_commit(&tfull[acc]);
-            }
-            __syncwarp();
+            if constexpr (CTA2) ptx::umma_commit_2sm_elect(&tfull[acc], 3);
+            else ptx::umma_commit_elect(&tfull[acc]);
         }
         }
     } else if constexpr (EPI > 0) {
@@ -1201,7 +1199,7 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = CTA2 ? 2 : 1;
     g_last_launch = ConvTcLaunchInfo{static_cast<int>(MODE), LOAD, BN, EPI, CTA2 ? 1 : 0, p.splits,
-                                     p.num_tiles, grid, p.counters != nullptr ? 1 : 0};
+                                     p.num_tiles, grid, p.counters != nullptr ? 1 : 0, 0};
     return cudaLaunchKernelEx(&cfg, conv_tc_kernel<MODE, BN, LOAD, EPI, CTA2>, p);
 }
 
@@ -1327,6 +1325,7 @@ cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cuda
 
 void conv_tc_set_force_gather(int on) { g_force_gather = on ? 1 : 0; }
 ConvTcLaunchInfo conv_tc_last_launch() { return g_last_launch; }
+void conv_tc_note_launch(const ConvTcLaunchInfo& info) { g_last_launch = info; }
 void conv_tc_set_epi_kb(int kb) { g_epi_kb = g_epi_kb_spatial = kb; }
 void conv_tc_set_sm_reserve(int sms) { g_sm_reserve = std::max(0, sms); }
 
@@ -1385,6 +1384,7 @@ cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const E
         a_matrix = ws;
         b_matrix = wp;
     } else {
+        if (!force_gather() && conv_win_applies(g, ConvMode::Fwd)) return conv_win_fwd(g, x, w, ep, y, st);
         p.s = make_shape(g, ConvMode::Fwd);
     }
     p.a = static_cast<const __nv_bfloat16*>(a_matrix);
@@ -1406,6 +1406,7 @@ bool conv_tc_dgrad_needs_pack(const ConvGeom& g) {
 cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* w, const void* wTp,
                           const Epilogue& ep, void* dx, cudaStream_t st) {
     if (conv_tc_dgrad_needs_pack(g) && wTp == nullptr) return cudaErrorInvalidValue;
+    if (!force_gather() && conv_win_applies(g, ConvMode::Dgrad)) return conv_win_dgrad(g, dy, w, ep, dx, st);
     for (int ph = 0; ph < g.stride_h; ++ph) {
         for (int pw = 0; pw < g.stride_w; ++pw) {
             Params p{};

@@ -1,0 +1,607 @@
+// Window implicit-GEMM convolution for stride-1 R x S layers (sm_100a).
+//
+// The im2col TMA path (conv_tc.cu) brings one 128-pixel x 64-channel box per
+// filter tap, so every input pixel crosses L2 -> SM R*S times; on the
+// 56x56x64 and 28x28x128 3x3 layers that traffic, not the tensor pipe, sets
+// the pace. Here the activation operand of a tile is loaded ONCE per 64-
+// channel slice as a "window": whole padded input rows (a tiled 4-D TMA box
+// {64 ch, Wp, WR rows, 1 image}, out-of-image rows / columns zero-filled).
+// GEMM row m of a tile is flat position f0 + m of the padded output plane
+// (row-major, Wp = Wo + S - 1 columns per row, the last S - 1 of each row are
+// junk outputs that the epilogue drops), so filter tap (r, s) is the same
+// window seen through a UMMA A descriptor shifted by r*Wp + s rows of 128 B.
+// (Measured, scripts/probes/umma_shift_probe.cu: K-major SWIZZLE_128B
+// descriptors at any 128-byte row offset of a TMA-swizzled buffer read
+// correctly with base-offset 0 and at full MMA rate.)
+//
+//   warp 0 (1 thread) TMA producer: windows into a 2-4 stage ring; the weight
+//                     operand per (tap, slice) into a B ring, or loaded once
+//                     and kept resident when it fits (one N tile, <= 96 KB)
+//   warp 12           MMA issuer: tcgen05.mma kind::f16, M = 128 (or 256 over
+//                     a CTA pair: two images at the same flat offset, so both
+//                     CTAs' windows share one A descriptor), N = BN, K = 16
+//   warps 4-11        epilogue: tcgen05.ld, bias / residual / ReLU (fwd) or
+//                     residual-grad / ReLU-mask (dgrad), bf16 stores of the
+//                     valid rows; double-buffered TMEM accumulators
+//
+// Fwd: activation x, B = w[K][R*S*C] (K-major). Dgrad of a stride-1 conv is
+// the same stencil over dy with flipped taps and padding R-1-pad: activation
+// dy, B = the KRSC filters read MN-major ([K][R*S][C] boxes), no transpose.
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "ptx.cuh"
+#include "tma.cuh"
+
+namespace tcb {
+namespace {
+
+constexpr int BM = 128;
+constexpr int kEpiThreads = 256;  // warps 4-11
+constexpr int kMmaWarp = 12;
+constexpr int kThreads = 13 * 32;
+constexpr int kMaxWin = 4, kMaxB = 8;
+constexpr size_t kSmemCap = 227 * 1024 - 2048;
+
+struct WinParams {
+    CUtensorMap tmap_win;  // activation [N][Ha][Wa][Ca] bf16, box {64, Wp, WR, 1}
+    CUtensorMap tmap_b;    // fwd: w [Ncol][R*S*Ca] (K-major); dgrad: filters [Ca][R*S][Ncol]
+    int n_img, Ho, Wo;     // GEMM output grid per image (fwd: y, dgrad: dx)
+    int pad_h, pad_w;      // window padding (fwd: the conv's; dgrad: R-1-pad_h, S-1-pad_w)
+    int R, S;              // taps of the stencil (dgrad: flipped)
+    int Wp, tiles_img, slices;
+    int Ncol, n_tiles, units;
+    uint32_t win_bytes, win_stride, b_bytes;
+    int win_stages, b_stages;
+    void* out;
+    const float* bias;
+    const __nv_bfloat16* residual;
+    const __nv_bfloat16* mask;
+    int relu;
+    FastDiv d_wp, d_tiles, d_ntiles;
+    unsigned long long* dbg;  // optional per-CTA role timing (tcb_conv_win_debug)
+};
+
+__device__ __forceinline__ long long clk(bool on) { return on ? clock64() : 0; }
+
+struct Unit {
+    int img, nt, row0, off0, f0;
+};
+
+template <bool CTA2>
+__device__ __forceinline__ Unit unit_of(const WinParams& p, int u, uint32_t rank) {
+    Unit t;
+    uint32_t rest, nt, g, j;
+    p.d_ntiles.divmod(static_cast<uint32_t>(u), rest, nt);
+    p.d_tiles.divmod(rest, g, j);
+    t.nt = static_cast<int>(nt);
+    t.img = CTA2 ? 2 * static_cast<int>(g) + static_cast<int>(rank) : static_cast<int>(g);
+    t.f0 = static_cast<int>(j) * BM;
+    uint32_t r0, o0;
+    p.d_wp.divmod(static_cast<uint32_t>(t.f0), r0, o0);
+    t.row0 = static_cast<int>(r0);
+    t.off0 = static_cast<int>(o0);
+    return t;
+}
+
+__device__ __forceinline__ void unpack8(uint4 v, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 x = __bfloat1622float2(h[i]);
+        f[2 * i] = x.x;
+        f[2 * i + 1] = x.y;
+    }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+    uint4 v;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return v;
+}
+
+// One 32-column accumulator chunk of one output row: fused epilogue + bf16 store.
+__device__ __forceinline__ void store_chunk(const WinParams& p, size_t orow, int col0, const uint32_t (&acc)[32]) {
+    const size_t base = orow * p.Ncol + col0;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + base;
+    if (col0 + 32 <= p.Ncol) {
+        uint4 rv[4], mv[4];
+        if (p.residual) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) rv[g] = __ldg(reinterpret_cast<const uint4*>(p.residual + base) + g);
+        }
+        if (p.mask) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) mv[g] = __ldg(reinterpret_cast<const uint4*>(p.mask + base) + g);
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(acc[8 * g + i]);
+            if (p.bias) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] += __ldg(p.bias + col0 + 8 * g + i);
+            }
+            if (p.residual) {
+                float r[8];
+                unpack8(rv[g], r);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] += r[i];
+            }
+            if (p.relu) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (p.mask) {
+                float mk[8];
+                unpack8(mv[g], mk);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = mk[i] > 0.f ? v[i] : 0.f;
+            }
+            reinterpret_cast<uint4*>(out)[g] = pack8(v);
+        }
+    } else {
+        for (int i = 0; i < 32 && col0 + i < p.Ncol; ++i) {
+            float x = __uint_as_float(acc[i]);
+            if (p.bias) x += p.bias[col0 + i];
+            if (p.residual) x += __bfloat162float(p.residual[base + i]);
+            if (p.relu) x = fmaxf(x, 0.f);
+            if (p.mask && !(__bfloat162float(p.mask[base + i]) > 0.f)) x = 0.f;
+            out[i] = __float2bfloat16_rn(x);
+        }
+    }
+}
+
+template <int BN, bool CTA2, bool BRES, bool DGRAD>
+__global__ void __launch_bounds__(kThreads, 1) conv_win_kernel(const __grid_constant__ WinParams p) {
+    // this CTA's share of the B tile per (tap, slice): K-major rows (fwd) or 64-channel
+    // MN-major boxes (dgrad); a pair splits the N columns
+    constexpr uint32_t kBBytes = BN * 64 * 2 / (CTA2 ? 2 : 1);
+    constexpr int kNB = DGRAD ? (BN / (CTA2 ? 2 : 1)) / 64 : 1;  // dgrad boxes per B tile
+    const uint32_t rank = CTA2 ? ptx::cluster_ctarank() : 0u;
+    const int unit0 = CTA2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+    const int ustride = CTA2 ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t wfull[kMaxWin], wempty[kMaxWin], bfull[kMaxB], bempty[kMaxB];
+    __shared__ uint64_t tfull[2], tempty[2], bres_bar;
+    __shared__ uint32_t tmem_slot;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int taps = p.R * p.S;
+    constexpr uint32_t kTmemCols = 2 * BN;
+
+    if (tid == 0) {
+        for (int i = 0; i < p.win_stages; ++i) {
+            ptx::mbar_init(&wfull[i], 1);
+            ptx::mbar_init(&wempty[i], 1);
+        }
+        for (int i = 0; i < p.b_stages; ++i) {
+            ptx::mbar_init(&bfull[i], 1);
+            ptx::mbar_init(&bempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], (CTA2 ? 2 : 1) * kEpiThreads);
+        }
+        ptx::mbar_init(&bres_bar, 1);
+        ptx::fence_mbarrier_init();
+        ptx::tma_prefetch_desc(&p.tmap_win);
+        ptx::tma_prefetch_desc(&p.tmap_b);
+    }
+    if (warp == kMmaWarp) {
+        if constexpr (CTA2) ptx::tmem_alloc_2sm<kTmemCols>(&tmem_slot);
+        else ptx::tmem_alloc<kTmemCols>(&tmem_slot);
+    }
+    ptx::tc_fence_before();
+    if constexpr (CTA2) ptx::cluster_sync();
+    else __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = tmem_slot;
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
+    const uint32_t smem_base = ptx::smem_addr(smem);
+    const uint32_t b_base = smem_base + p.win_stages * p.win_stride;
+
+    if (warp == 0) {
+        // ================================================ TMA producer ======
+        if (tid == 0) {
+            auto leader = [&](uint64_t* bar) {
+                return CTA2 ? ptx::leader_addr(ptx::smem_addr(bar)) : ptx::smem_addr(bar);
+            };
+            // B box(es) of stencil tap `tap` (window order) and channel slice cs
+            auto load_b = [&](uint32_t dst, uint64_t* bar, int tap, int cs, int nt) {
+                const uint32_t bar_u = leader(bar);
+                if constexpr (DGRAD) {
+                    const int ti = tap / p.S, tj = tap - ti * p.S;
+                    const int ft = (p.R - 1 - ti) * p.S + (p.S - 1 - tj);  // flipped filter tap
+                    const int c0 = nt * BN + (CTA2 ? static_cast<int>(rank) * (BN / 2) : 0);
+#pragma unroll
+                    for (int j = 0; j < kNB; ++j) {
+                        if constexpr (CTA2) ptx::tma_load_3d_2sm(dst + j * 8192, &p.tmap_b, bar_u, c0 + j * 64, ft, cs * 64);
+                        else ptx::tma_load_3d(dst + j * 8192, &p.tmap_b, bar, c0 + j * 64, ft, cs * 64);
+                    }
+                } else {
+                    const int kk = tap * p.slices * 64 + cs * 64;
+                    const int r0 = nt * BN + (CTA2 ? static_cast<int>(rank) * (BN / 2) : 0);
+                    if constexpr (CTA2) ptx::tma_load_2d_2sm(dst, &p.tmap_b, bar_u, kk, r0);
+                    else ptx::tma_load_2d(dst, &p.tmap_b, bar, kk, r0);
+                }
+            };
+            if constexpr (BRES) {
+                // the whole B operand of the (single) N tile, once
+                if (!CTA2 || rank == 0)
+                    ptx::mbar_arrive_expect_tx(&bres_bar, (CTA2 ? 2u : 1u) * kBBytes * taps * p.slices);
+                for (int cs = 0; cs < p.slices; ++cs)
+                    for (int tap = 0; tap < taps; ++tap)
+                        load_b(b_base + (cs * taps + tap) * kBBytes, &bres_bar, tap, cs, 0);
+            }
+            int ws = 0, bs = 0;
+            uint32_t wph = 0, bph = 0;
+            long long t_w = 0, t_b = 0, t0 = clk(p.dbg != nullptr);
+            for (int u = unit0; u < p.units; u += ustride) {
+                const Unit t = unit_of<CTA2>(p, u, rank);
+                for (int cs = 0; cs < p.slices; ++cs) {
+                    long long a = clk(p.dbg != nullptr);
+                    ptx::mbar_wait(&wempty[ws], wph ^ 1);
+                    t_w += clk(p.dbg != nullptr) - a;
+                    const uint32_t wdst = smem_base + ws * p.win_stride;
+                    if (!CTA2 || rank == 0) ptx::mbar_arrive_expect_tx(&wfull[ws], (CTA2 ? 2u : 1u) * p.win_bytes);
+                    if constexpr (CTA2)
+                        ptx::tma_load_4d_2sm(wdst, &p.tmap_win, leader(&wfull[ws]), cs * 64, -p.pad_w,
+                                             t.row0 - p.pad_h, t.img);
+                    else
+                        ptx::tma_load_4d(wdst, &p.tmap_win, &wfull[ws], cs * 64, -p.pad_w, t.row0 - p.pad_h, t.img);
+                    if (++ws == p.win_stages) {
+                        ws = 0;
+                        wph ^= 1;
+                    }
+                    if constexpr (!BRES) {
+                        for (int tap = 0; tap < taps; ++tap) {
+                            long long b = clk(p.dbg != nullptr);
+                            ptx::mbar_wait(&bempty[bs], bph ^ 1);
+                            t_b += clk(p.dbg != nullptr) - b;
+                            if (!CTA2 || rank == 0) ptx::mbar_arrive_expect_tx(&bfull[bs], (CTA2 ? 2u : 1u) * kBBytes);
+                            load_b(b_base + bs * kBBytes, &bfull[bs], tap, cs, t.nt);
+                            if (++bs == p.b_stages) {
+                                bs = 0;
+                                bph ^= 1;
+                            }
+                        }
+                    }
+                }
+            }
+            if (p.dbg) {
+                unsigned long long* d = p.dbg + blockIdx.x * 8;
+                d[0] = clk(p.dbg != nullptr) - t0;
+                d[1] = t_w;
+                d[2] = t_b;
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // =============================================== MMA issuer ======
+        // one thread runs the whole issue loop: descriptors advance by plain
+        // 64-bit adds of the 16-byte start-address field (taps: Wp*8 per filter
+        // row, 8 per column; k steps: 2 for K-major, 128 for MN-major B)
+        constexpr uint32_t idesc = ptx::make_idesc(1, CTA2 ? 2 * BM : BM, BN, 0u, DGRAD ? 1u : 0u);
+        constexpr uint64_t kBStep = DGRAD ? 128 : 2;
+        if (!CTA2 || rank == 0) {  // the whole warp runs the loop; one elected lane issues
+            if constexpr (BRES) {
+                ptx::mbar_wait(&bres_bar, 0);
+                ptx::tc_fence_after();
+            }
+            int ws = 0, bs = 0, it = 0;
+            uint32_t wph = 0, bph = 0;
+            const uint64_t row_step = static_cast<uint64_t>(p.Wp) * 8;
+            long long m_t = 0, m_w = 0, m_b = 0, m0 = clk(p.dbg != nullptr);
+            for (int u = unit0; u < p.units; u += ustride, ++it) {
+                const Unit t = unit_of<CTA2>(p, u, rank);
+                const int acc = it & 1;
+                long long a = clk(p.dbg != nullptr);
+                ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+                m_t += clk(p.dbg != nullptr) - a;
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                uint32_t accum = 0;
+                for (int cs = 0; cs < p.slices; ++cs) {
+                    a = clk(p.dbg != nullptr);
+                    ptx::mbar_wait(&wfull[ws], wph);
+                    m_w += clk(p.dbg != nullptr) - a;
+                    const uint64_t a0 = ptx::sw128_desc(smem_base + ws * p.win_stride + t.off0 * 128, 16, 1024);
+                    const uint64_t bres0 = BRES ? ptx::sw128_desc(b_base + cs * taps * kBBytes, DGRAD ? 8192 : 16, 1024) : 0;
+                    uint64_t a_row = a0;
+                    int tap = 0;
+                    for (int ti = 0; ti < p.R; ++ti, a_row += row_step) {
+                        uint64_t ad = a_row;
+                        for (int tj = 0; tj < p.S; ++tj, ++tap, ad += 8) {
+                            uint64_t bd;
+                            if constexpr (BRES) {
+                                bd = bres0 + static_cast<uint64_t>(tap) * (kBBytes >> 4);
+                            } else {
+                                long long b = clk(p.dbg != nullptr);
+                                ptx::mbar_wait(&bfull[bs], bph);
+                                m_b += clk(p.dbg != nullptr) - b;
+                                bd = ptx::sw128_desc(b_base + bs * kBBytes, DGRAD ? 8192 : 16, 1024);
+                            }
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                if constexpr (CTA2) ptx::umma_f16_2sm_elect(d_tmem, ad + 2 * k, bd + kBStep * k, idesc, accum);
+                                else ptx::umma_f16_elect(d_tmem, ad + 2 * k, bd + kBStep * k, idesc, accum);
+                                accum = 1;
+                            }
+                            if constexpr (!BRES) {
+                                if constexpr (CTA2) ptx::umma_commit_2sm_elect(&bempty[bs], 3);
+                                else ptx::umma_commit_elect(&bempty[bs]);
+                                if (++bs == p.b_stages) {
+                                    bs = 0;
+                                    bph ^= 1;
+                                }
+                            }
+                        }
+                    }
+                    if constexpr (CTA2) ptx::umma_commit_2sm_elect(&wempty[ws], 3);
+                    else ptx::umma_commit_elect(&wempty[ws]);
+                    if (++ws == p.win_stages) {
+                        ws = 0;
+                        wph ^= 1;
+                    }
+                }
+                if constexpr (CTA2) ptx::umma_commit_2sm_elect(&tfull[acc], 3);
+                else ptx::umma_commit_elect(&tfull[acc]);
+            }
+            if (p.dbg && (tid & 31) == 0) {
+                unsigned long long* d = p.dbg + blockIdx.x * 8;
+                d[3] = clk(p.dbg != nullptr) - m0;
+                d[4] = m_t;
+                d[5] = m_w;
+                d[6] = m_b;
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ================================================= epilogue ======
+        const int quarter = warp & 3;
+        const int half = (warp - 4) >> 2;
+        constexpr int kChunks = BN / 32, kHalf = kChunks / 2;
+        const int row = quarter * 32 + (tid & 31);
+        int it = 0;
+        long long e_wait = 0, e_start = clk(p.dbg != nullptr);
+        for (int u = unit0; u < p.units; u += ustride, ++it) {
+            const Unit t = unit_of<CTA2>(p, u, rank);
+            const int acc = it & 1;
+            uint32_t ho, wq;
+            p.d_wp.divmod(static_cast<uint32_t>(t.f0 + row), ho, wq);
+            const bool valid = t.img < p.n_img && static_cast<int>(ho) < p.Ho && static_cast<int>(wq) < p.Wo;
+            const size_t orow = (static_cast<size_t>(t.img) * p.Ho + ho) * p.Wo + wq;
+            long long e0 = clk(p.dbg != nullptr);
+            ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+            if (p.dbg && tid == 128) e_wait += clk(p.dbg != nullptr) - e0;
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = half * kHalf; c < (half + 1) * kHalf; ++c) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, v);
+                ptx::tmem_ld_wait();
+                const int col0 = t.nt * BN + c * 32;
+                if (valid && col0 < p.Ncol) store_chunk(p, orow, col0, v);
+            }
+            ptx::tc_fence_before();
+            if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
+            else ptx::mbar_arrive(&tempty[acc]);
+        }
+        if (p.dbg && tid == 128) p.dbg[blockIdx.x * 8 + 7] = (static_cast<unsigned long long>(clk(p.dbg != nullptr) - e_start) << 32) |
+                                                            static_cast<unsigned long long>(e_wait & 0xffffffff);
+    }
+
+    ptx::tc_fence_before();
+    if constexpr (CTA2) ptx::cluster_sync();
+    else __syncthreads();
+    if (warp == kMmaWarp) {
+        ptx::tc_fence_after();
+        if constexpr (CTA2) ptx::tmem_dealloc_2sm<kTmemCols>(tmem_base);
+        else ptx::tmem_dealloc<kTmemCols>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------- host ----
+struct WinPlan {
+    bool use = false;
+    int Ha, Wa, Ca, Ho, Wo, pad_h, pad_w, R, S, Ncol;
+    int Wp, WR, tiles_img, slices, bn, n_tiles;
+    bool cta2, bres;
+    uint32_t win_bytes, win_stride, b_bytes;
+    int win_stages, b_stages;
+    size_t smem;
+};
+
+int g_win_mode = -1;  // $TCB_WIN: 0 off, 1 on (default, N = 64 tiles), 2 every applicable geometry
+unsigned long long* g_win_dbg = nullptr;  // role timing buffer, 8 x u64 per CTA (diagnostics)
+
+bool win_enabled() {
+    if (g_win_mode < 0) {
+        const char* e = getenv("TCB_WIN");
+        g_win_mode = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
+    }
+    return g_win_mode >= 1;
+}
+
+// mode: 0 fwd (activation x), 1 dgrad (activation dy).
+WinPlan win_plan(const ConvGeom& g, int mode) {
+    WinPlan q;
+    if (!win_enabled() || g.stride_h != 1 || g.stride_w != 1 || g.r * g.s < 2) return q;
+    if (mode == 0) {
+        q.Ha = g.h; q.Wa = g.w; q.Ca = g.c; q.Ncol = g.k;
+        q.Ho = g.ho(); q.Wo = g.wo();
+        q.pad_h = g.pad_h; q.pad_w = g.pad_w;
+    } else {
+        q.Ha = g.ho(); q.Wa = g.wo(); q.Ca = g.k; q.Ncol = g.c;
+        q.Ho = g.h; q.Wo = g.w;
+        q.pad_h = g.r - 1 - g.pad_h; q.pad_w = g.s - 1 - g.pad_w;
+        if (q.pad_h < 0 || q.pad_w < 0) return q;
+    }
+    q.R = g.r; q.S = g.s;
+    if (q.Ca % 64 != 0 || q.Ncol % 8 != 0 || q.pad_h > 15 || q.pad_w > 15) return q;
+    q.Wp = q.Wo + q.S - 1;
+    if (q.Wp > 64) return q;  // wide rows: a window of whole rows costs more than it saves
+    // rows a 128-position tile can touch: positions [off0, off0 + 127 + (R-1)*Wp + S-1]
+    q.WR = (q.Wp - 1 + BM - 1 + (q.R - 1) * q.Wp + q.S - 1) / q.Wp + 1;
+    q.win_bytes = static_cast<uint32_t>(q.WR) * q.Wp * 128;
+    if (q.WR > 256 || q.win_bytes > 64 * 1024) return q;
+    q.win_stride = (q.win_bytes + 1023) / 1024 * 1024;
+    q.tiles_img = (q.Ho * q.Wp + BM - 1) / BM;
+    q.slices = q.Ca / 64;
+    q.bn = q.Ncol <= 64 ? 64 : q.Ncol <= 128 ? 128 : 256;
+    // Measured (scripts/win_ab2.sh, bs256): the window wins where the im2col path's
+    // 64-column tiles re-read each input pixel per tap at a low MMA width (ResNet
+    // stage 1: fwd 117 -> 77 us, dgrad 130 -> 78 us); with 128/256-column tiles the
+    // im2col path is already MMA-paced and the window's junk columns cost more
+    // (stage 2: 66 vs 68 us, stage 3: 45 vs 54 us). $TCB_WIN=2 forces it on for every
+    // applicable geometry (tests).
+    if (q.bn != 64 && g_win_mode != 2) return q;
+    q.n_tiles = (q.Ncol + q.bn - 1) / q.bn;
+    // CTA pairs (two images per unit): N split in halves; dgrad halves must be whole
+    // 64-channel MN-major boxes
+    static const int env_cta2 = [] { const char* e = getenv("TCB_WIN_CTA2"); return e ? atoi(e) : -1; }();
+    static const int env_bres = [] { const char* e = getenv("TCB_WIN_BRES"); return e ? atoi(e) : -1; }();
+    static const int env_wst = [] { const char* e = getenv("TCB_WIN_WSTAGES"); return e ? atoi(e) : 0; }();
+    static const int env_bst = [] { const char* e = getenv("TCB_WIN_BSTAGES"); return e ? atoi(e) : 0; }();
+    // CTA pairs measured slower at N = 64 (stage 1 fwd: 107 vs 77 us single)
+    q.cta2 = g.n >= 2 && q.bn >= 128 && env_cta2 != 0;
+    q.b_bytes = static_cast<uint32_t>(q.bn) * 64 * 2 / (q.cta2 ? 2 : 1);
+    const size_t b_all = size_t(q.b_bytes) * q.R * q.S * q.slices;
+    q.bres = q.n_tiles == 1 && b_all <= 96 * 1024 && env_bres != 0;
+    const size_t b_ring = q.bres ? b_all : 0;
+    q.b_stages = q.bres ? 1 : 0;
+    // window stages first (>= 2), then B stages (>= 3) with what is left
+    for (q.win_stages = env_wst > 1 ? std::min(env_wst, kMaxWin) : kMaxWin; q.win_stages >= 2; --q.win_stages) {
+        const size_t wbytes = size_t(q.win_stages) * q.win_stride;
+        if (q.bres) {
+            if (wbytes + b_ring + 1024 <= kSmemCap) break;
+        } else {
+            const size_t left = kSmemCap - std::min(kSmemCap, wbytes + 1024);
+            const int bst = static_cast<int>(std::min<size_t>(env_bst > 2 ? std::min(env_bst, kMaxB) : kMaxB,
+                                                              left / q.b_bytes));
+            if (bst >= 3) {
+                q.b_stages = bst;
+                break;
+            }
+        }
+    }
+    if (q.win_stages < 2) return q;
+    q.smem = size_t(q.win_stages) * q.win_stride + (q.bres ? b_ring : size_t(q.b_stages) * q.b_bytes) + 1024;
+    q.use = true;
+    return q;
+}
+
+template <int BN, bool CTA2, bool BRES, bool DGRAD>
+cudaError_t launch_win(WinParams& p, const WinPlan& q, cudaStream_t st) {
+    auto kern = conv_win_kernel<BN, CTA2, BRES, DGRAD>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(q.smem));
+    if (e != cudaSuccess) return e;
+    const int sms = num_sms();
+    const int grid = CTA2 ? 2 * std::min(p.units, sms / 2) : std::min(p.units, sms);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = q.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CTA2 ? 2 : 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = CTA2 ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <bool DGRAD>
+cudaError_t dispatch_win(WinParams& p, const WinPlan& q, cudaStream_t st) {
+#define TCB_WIN_CASE(BN)                                                              \
+    if (q.bn == BN) {                                                                 \
+        if (q.cta2) return q.bres ? launch_win<BN, true, true, DGRAD>(p, q, st)       \
+                                  : launch_win<BN, true, false, DGRAD>(p, q, st);     \
+        return q.bres ? launch_win<BN, false, true, DGRAD>(p, q, st)                  \
+                      : launch_win<BN, false, false, DGRAD>(p, q, st);                \
+    }
+    TCB_WIN_CASE(64)
+    TCB_WIN_CASE(128)
+    TCB_WIN_CASE(256)
+#undef TCB_WIN_CASE
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t run_win(const ConvGeom& g, const WinPlan& q, bool dgrad, const void* act, const void* b,
+                    const Epilogue& ep, void* out, cudaStream_t st) {
+    WinParams p{};
+    if (!make_tmap_window_bf16(&p.tmap_win, act, g.n, q.Ha, q.Wa, q.Ca, q.Wp, q.WR)) return cudaErrorInvalidValue;
+    if (dgrad) {
+        if (!make_tmap_filters_bf16(&p.tmap_b, b, g.k, size_t(g.r) * g.s, g.c)) return cudaErrorInvalidValue;
+    } else if (!make_tmap_bf16_2d(&p.tmap_b, b, q.Ncol, size_t(g.r) * g.s * g.c, q.cta2 ? q.bn / 2 : q.bn)) {
+        return cudaErrorInvalidValue;
+    }
+    p.n_img = g.n;
+    p.Ho = q.Ho;
+    p.Wo = q.Wo;
+    p.pad_h = q.pad_h;
+    p.pad_w = q.pad_w;
+    p.R = q.R;
+    p.S = q.S;
+    p.Wp = q.Wp;
+    p.tiles_img = q.tiles_img;
+    p.slices = q.slices;
+    p.Ncol = q.Ncol;
+    p.n_tiles = q.n_tiles;
+    const int groups = q.cta2 ? (g.n + 1) / 2 : g.n;
+    p.units = groups * q.tiles_img * q.n_tiles;
+    p.win_bytes = q.win_bytes;
+    p.win_stride = q.win_stride;
+    p.b_bytes = q.b_bytes;
+    p.win_stages = q.win_stages;
+    p.b_stages = q.b_stages;
+    p.out = out;
+    p.bias = ep.bias;
+    p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
+    p.mask = static_cast<const __nv_bfloat16*>(ep.mask);
+    p.relu = ep.relu ? 1 : 0;
+    p.d_wp = FastDiv(static_cast<uint32_t>(q.Wp));
+    p.d_tiles = FastDiv(static_cast<uint32_t>(q.tiles_img));
+    p.d_ntiles = FastDiv(static_cast<uint32_t>(q.n_tiles));
+    p.dbg = g_win_dbg;
+    conv_tc_note_launch(ConvTcLaunchInfo{dgrad ? 1 : 0, 4, q.bn, 0, q.cta2 ? 1 : 0, 1, p.units,
+                                         q.cta2 ? 2 * std::min(p.units, num_sms() / 2) : std::min(p.units, num_sms()),
+                                         0, q.bres ? 1 : 0});
+    return dgrad ? dispatch_win<true>(p, q, st) : dispatch_win<false>(p, q, st);
+}
+
+}  // namespace
+
+void conv_win_set_mode(int on) { g_win_mode = on < 0 ? -1 : on; }
+void conv_win_set_debug(void* buf) { g_win_dbg = static_cast<unsigned long long*>(buf); }
+
+bool conv_win_applies(const ConvGeom& g, ConvMode mode) {
+    return mode != ConvMode::Wgrad && win_plan(g, mode == ConvMode::Fwd ? 0 : 1).use;
+}
+
+cudaError_t conv_win_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep, void* y,
+                         cudaStream_t st) {
+    const WinPlan q = win_plan(g, 0);
+    if (!q.use) return cudaErrorInvalidValue;
+    return run_win(g, q, false, x, w, ep, y, st);
+}
+
+cudaError_t conv_win_dgrad(const ConvGeom& g, const void* dy, const void* w, const Epilogue& ep, void* dx,
+                           cudaStream_t st) {
+    const WinPlan q = win_plan(g, 1);
+    if (!q.use) return cudaErrorInvalidValue;
+    return run_win(g, q, true, dy, w, ep, dx, st);
+}
+
+}  // namespace tcb

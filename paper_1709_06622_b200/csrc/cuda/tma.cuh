@@ -61,6 +61,22 @@ inline bool make_tmap_filters_bf16(CUtensorMap* map, const void* base, uint64_t 
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// NHWC bf16 tensor [n][h][w][c] read in tiled boxes of 64 channels x bw pixels x
+// bh rows x 1 image (128-byte swizzle): a conv "window" of whole padded input
+// rows; out-of-image rows/columns (the padding) read as zero.
+inline bool make_tmap_window_bf16(CUtensorMap* map, const void* base, int n, int h, int w, int c,
+                                  uint32_t bw, uint32_t bh) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[4] = {cuuint64_t(c), cuuint64_t(w), cuuint64_t(h), cuuint64_t(n)};
+    const cuuint64_t strides[3] = {cuuint64_t(c) * 2, cuuint64_t(w) * c * 2, cuuint64_t(h) * w * c * 2};
+    const cuuint32_t box[4] = {64, bw, bh, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                     const cuuint64_t*, const cuuint64_t*, const int*, const int*,
                                     cuuint32_t, cuuint32_t, const cuuint32_t*,

@@ -68,9 +68,22 @@ void conv_tc_set_force_gather(int on);
 // tile width, TMA-epilogue slots, CTA pair, split-K factor, work units, grid,
 // in-kernel split reduction).
 struct ConvTcLaunchInfo {
-    int mode, load, bn, epi, cta2, splits, units, grid, fused_reduce;
+    int mode, load, bn, epi, cta2, splits, units, grid, fused_reduce, b_resident;
 };
 ConvTcLaunchInfo conv_tc_last_launch();
+void conv_tc_note_launch(const ConvTcLaunchInfo& info);
+
+// Window implicit GEMM (conv_win.cu): stride-1 R x S convs whose activation
+// operand has whole 64-channel slices; one TMA window of padded input rows per
+// tile and slice, every tap a shifted UMMA descriptor into it (fwd, and the
+// stride-1 dgrad over dy with flipped taps). Operand path 4 in ConvTcLaunchInfo.
+bool conv_win_applies(const ConvGeom& g, ConvMode mode);
+cudaError_t conv_win_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep, void* y,
+                         cudaStream_t st);
+cudaError_t conv_win_dgrad(const ConvGeom& g, const void* dy, const void* w, const Epilogue& ep, void* dx,
+                           cudaStream_t st);
+void conv_win_set_mode(int on);  // 0 off, 1 on (N = 64 tiles), 2 all applicable, -1 from $TCB_WIN
+void conv_win_set_debug(void* buf);  // diagnostics: per-CTA role timing (8 x u64 per CTA) or nullptr
 // TMA epilogue for layers with at most `kb` 64-deep k-blocks (0 = never,
 // -1 = default: $TCB_CONV_EPI_KB or 8).
 void conv_tc_set_epi_kb(int kb);

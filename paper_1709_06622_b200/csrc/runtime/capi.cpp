@@ -376,19 +376,30 @@ TCB_API int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_
 
 TCB_API void tcb_free(void* p) { std::free(p); }
 
-TCB_API int tcb_conv_last_launch_info(int* out9) {
-    if (!out9) return fail(TCB_ERR_INVALID, "NULL argument");
+// Diagnostics: per-CTA role timing of the window conv kernel into a device
+// buffer of 8 x u64 per CTA (producer total / window-slot wait / B-slot wait,
+// MMA total / accumulator wait / window wait / B wait, epilogue total<<32|wait),
+// or nullptr to switch it off.
+TCB_API int tcb_conv_win_debug(void* dev_buffer) {
+    conv_win_set_debug(dev_buffer);
+    return TCB_OK;
+}
+
+TCB_API int tcb_conv_last_launch_info(int* out10) {
+    if (!out10) return fail(TCB_ERR_INVALID, "NULL argument");
     const ConvTcLaunchInfo i = conv_tc_last_launch();
-    const int v[9] = {i.mode, i.load, i.bn, i.epi, i.cta2, i.splits, i.units, i.grid, i.fused_reduce};
-    for (int k = 0; k < 9; ++k) out9[k] = v[k];
+    const int v[10] = {i.mode, i.load, i.bn, i.epi, i.cta2, i.splits, i.units, i.grid, i.fused_reduce, i.b_resident};
+    for (int k = 0; k < 10; ++k) out10[k] = v[k];
     return TCB_OK;
 }
 
 TCB_API int tcb_set_conv_operand_path(int mode) {
-    if (mode < 0 || mode > 2)
-        return fail(TCB_ERR_INVALID, "mode must be 0 (auto), 1 (gather) or 2 (register epilogue)");
+    if (mode < 0 || mode > 4)
+        return fail(TCB_ERR_INVALID, "mode must be 0 (auto), 1 (gather), 2 (register epilogue), 3 (auto "
+                                     "without the window path) or 4 (window path wherever it applies)");
     conv_tc_set_force_gather(mode == 1);
     conv_tf32_set_force_gather(mode == 1);
     conv_tc_set_epi_kb(mode == 2 ? 0 : -1);
+    conv_win_set_mode(mode == 3 ? 0 : mode == 4 ? 2 : -1);
     return TCB_OK;
 }

@@ -248,12 +248,12 @@ def sgd_momentum(w, g, v, lr, mom, wd=0.0, gscale=1.0, w_compute=None):
                                  gscale, _stream()))
 
 
-LAUNCH_FIELDS = ("mode", "load", "bn", "epi", "cta2", "splits", "units", "grid", "fused_reduce")
+LAUNCH_FIELDS = ("mode", "load", "bn", "epi", "cta2", "splits", "units", "grid", "fused_reduce", "b_resident")
 
 
 def last_launch() -> dict:
     """Configuration of the last bf16 tensor-core conv kernel launch (test hook,
     tcb_conv_last_launch_info)."""
-    out = (ctypes.c_int * 9)()
+    out = (ctypes.c_int * 10)()
     check(lib().tcb_conv_last_launch_info(out))
     return dict(zip(LAUNCH_FIELDS, list(out)))

@@ -87,16 +87,20 @@ def _host(t):
     return t.float().cpu().numpy()
 
 
-@pytest.fixture(params=["auto", "gather", "regepi"])
+@pytest.fixture(params=["auto", "gather", "regepi", "nowin", "allwin"])
 def operand_path(request):
-    """auto = 2-D TMA (1x1/s1) or im2col-mode TMA (channels % 64 == 0 for bf16,
-    % 32 for tf32) where they apply, TMA epilogue on K-light layers; gather =
-    force the cp.async gather path (bf16 and tf32); regepi = auto loads with the
-    register epilogue everywhere (bf16). All must agree with the oracle."""
+    """auto = the window path (stride-1 R x S, activation channels % 64 == 0:
+    one TMA window of padded rows per tile, taps as shifted descriptors), else
+    2-D TMA (1x1/s1) or im2col-mode TMA (channels % 64 == 0 for bf16, % 32 for
+    tf32), TMA epilogue on K-light layers; gather = force the cp.async gather
+    path (bf16 and tf32); regepi = auto loads with the register epilogue
+    everywhere (bf16); nowin = auto without the window path (bf16); allwin =
+    the window path on every geometry it applies to (128/256-column tiles and
+    CTA pairs included; bf16). All must agree with the oracle."""
     import ctypes
     lib = _dev().lib()
     lib.tcb_set_conv_operand_path.argtypes = [ctypes.c_int]
-    lib.tcb_set_conv_operand_path({"auto": 0, "gather": 1, "regepi": 2}[request.param])
+    lib.tcb_set_conv_operand_path({"auto": 0, "gather": 1, "regepi": 2, "nowin": 3, "allwin": 4}[request.param])
     yield request.param
     lib.tcb_set_conv_operand_path(0)
 
@@ -106,7 +110,7 @@ def operand_path(request):
 def test_conv_gemm_parity(oracle, prec, spec, operand_path):
     if (prec != "ffma" and spec in FFMA_ONLY) or (prec == "bf16" and spec in C4_ONLY):
         pytest.skip("tensor-core paths need C, K multiples of 8 (bf16) / 4 (tf32)")
-    if (prec == "ffma" and operand_path != "auto") or (prec == "tf32" and operand_path == "regepi"):
+    if (prec == "ffma" and operand_path != "auto") or (prec == "tf32" and operand_path in ("regepi", "nowin", "allwin")):
         pytest.skip("operand path does not apply to this kernel")
     dev = _dev()
     name, n, h, w, c, k, r, pad, stride = spec
@@ -156,6 +160,60 @@ def test_conv_gemm_parity(oracle, prec, spec, operand_path):
         assert elem_err(_host(y), ref, 1e-2) <= 1e-4 * max(1.0, (fan_in / 2048) ** 0.5)
     if prec == "tf32":  # 10-bit mantissa products, fp32 accumulate: far inside 2e-2
         assert rel_err(_host(y0), ref0) <= 2e-3 and rel_err(_host(dw), refw) <= 2e-3
+
+
+WINDOW_CASES = [  # (name, n, h, w, c, k, (r, s), (ph, pw), expected fwd / dgrad configuration)
+    ("rn50_s1_3x3", 3, 56, 56, 64, 64, (3, 3), (1, 1), dict(fwd=(64, 0, 1), dgrad=(64, 0, 1))),
+    ("rn50_s2_3x3", 2, 28, 28, 128, 128, (3, 3), (1, 1), dict(fwd=(128, 1, 0), dgrad=(128, 1, 0))),
+    ("rn50_s3_3x3_k256", 2, 14, 14, 256, 256, (3, 3), (1, 1), dict(fwd=(256, 1, 0), dgrad=(256, 1, 0))),
+    ("incep_5x5_48_64", 3, 35, 35, 64, 64, (5, 5), (2, 2), dict(fwd=(64, 0, 0), dgrad=(64, 0, 0))),
+    ("incep_7x1_192", 2, 17, 17, 192, 192, (7, 1), (3, 0), dict(fwd=(256, 1, 0), dgrad=(256, 1, 0))),
+]
+
+
+@pytest.fixture
+def all_window():
+    import ctypes
+    lib = _dev().lib()
+    lib.tcb_set_conv_operand_path.argtypes = [ctypes.c_int]
+    lib.tcb_set_conv_operand_path(4)
+    yield
+    lib.tcb_set_conv_operand_path(0)
+
+
+@pytest.mark.parametrize("spec", WINDOW_CASES, ids=lambda s: s[0])
+def test_window_conv_path(oracle, spec, all_window):
+    """The window implicit GEMM at real layer sizes: fwd with the fused
+    bias + residual + ReLU epilogue, dgrad with residual-grad + ReLU mask,
+    against the oracle (bf16, 2e-2) and bitwise against itself; the launch
+    configuration (tile N, CTA pair, resident weights) is the planned one."""
+    dev = _dev()
+    name, n, h, w, c, k, (rr, ss), (ph, pw), want = spec
+    g = dev.geom(n, h, w, c, k, rr, ss, pad=ph, pad_w=pw)
+    gd = g.as_dict()
+    plan = dev.ConvPlan(g, "gemm", "bf16")
+    bf = torch.bfloat16
+    x = _rand(oracle, (n, h, w, c), 1, 1.0, True)
+    wt = _rand(oracle, (k, rr, ss, c), 2, (6.0 / (c * rr * ss)) ** 0.5, True)
+    bias = _rand(oracle, (k,), 3, 0.1)
+    res = _rand(oracle, (n, g.ho, g.wo, k), 4, 0.5, True)
+    dy = _rand(oracle, (n, g.ho, g.wo, k), 5, 1.0, True)
+    mask = _rand(oracle, (n, h, w, c), 6, 1.0, True)
+    rgrad = _rand(oracle, (n, h, w, c), 7, 0.5, True)
+    y = plan.fwd(_to_dev(x, bf), _to_dev(wt, bf), bias=_to_dev(bias, torch.float32), residual=_to_dev(res, bf),
+                 relu=True)
+    info = dev.last_launch()
+    assert info["load"] == 4 and (info["bn"], info["cta2"], info["b_resident"]) == want["fwd"], info
+    ref = oracle.conv_fwd(gd, x, wt, bias=bias, residual=res, relu=True)
+    assert rel_err(_host(y), ref) <= 2e-2, rel_err(_host(y), ref)
+    dx = plan.dgrad(_to_dev(dy, bf), _to_dev(wt, bf), residual=_to_dev(rgrad, bf), mask=_to_dev(mask, bf))
+    info = dev.last_launch()
+    assert info["load"] == 4 and (info["bn"], info["cta2"], info["b_resident"]) == want["dgrad"], info
+    refd = oracle.conv_dgrad(gd, dy, wt, residual=rgrad, mask=mask)
+    assert rel_err(_host(dx), refd) <= 2e-2, rel_err(_host(dx), refd)
+    y2 = plan.fwd(_to_dev(x, bf), _to_dev(wt, bf), bias=_to_dev(bias, torch.float32), residual=_to_dev(res, bf),
+                  relu=True)
+    assert torch.equal(y, y2)
 
 
 def test_wgrad_many_splits_and_cta_pairs(oracle):
