@@ -496,6 +496,22 @@ def summarize_step(kernels):
                         for k, v in sorted(cls.items(), key=lambda kv: -kv[1][2])}}
 
 
+KNOB_DEFAULTS = {  # the executor's A/B switches (read once from the environment) and their defaults
+    "TCB_GRAPH": "1 (replay the step as a CUDA graph)", "TCB_PDL": "1 (programmatic dependent launch)",
+    "TCB_WIN": "1 (window conv for 64-column stride-1 tiles)", "TCB_CTA2": "1", "TCB_CTA2_KB": "9",
+    "TCB_CONV_EPI_KB": "12", "TCB_CONV_EPI_KB_SPATIAL": "24", "TCB_EPI_DEEP_KB": "2",
+    "TCB_SPLIT_MIN_KB": "4", "TCB_CONV_FORCE_GATHER": "0", "TCB_FUSED_SPLIT_REDUCE": "0",
+    "TCB_NVLS_TIMEOUT_MS": "10000"}
+
+
+def runtime_knobs():
+    """Every TCB_* knob in effect for this run: defaults plus any overrides."""
+    eff = {k: v.split(" ")[0] for k, v in KNOB_DEFAULTS.items()}
+    over = {k: v for k, v in os.environ.items() if k.startswith("TCB_")}
+    eff.update(over)
+    return {"effective": eff, "overridden": sorted(over)}
+
+
 # ------------------------------------------------------------------ main ---
 def main():
     args = parse()
@@ -709,6 +725,7 @@ def main():
                        "ps_async": args.ps_async,
                        "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (per-step activations >> 126 MB); no flush"},
+            "knobs": runtime_knobs(),
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,

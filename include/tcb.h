@@ -168,9 +168,12 @@ int tcb_sgd_momentum(float* w, const float* grad, float* v, int compute_dtype, v
 int tcb_ps_nvls_update(const float* grad_mc, float* grad, float* w, float* v, void* wcompute_mc,
                        size_t begin, size_t n, float lr, float momentum, float weight_decay,
                        float grad_scale, void* stream);
-/* All-GPU barrier on P2P-mapped signal pads (slots 2048 + rank); epoch_dev
- * is a zero-initialised device u32 per rank. */
-int tcb_nvls_barrier(void* const* signal_pads_dev, uint32_t* epoch_dev, int rank, int world, void* stream);
+/* All-GPU barrier on P2P-mapped signal pads (slots slot0 + rank); epoch_dev
+ * is a zero-initialised device u32 per rank. The wait is bounded: a peer that
+ * does not arrive within timeout_ns sets *err_dev = 1 and the kernel returns
+ * (failure detection instead of a hung GPU). */
+int tcb_nvls_barrier(void* const* signal_pads_dev, uint32_t* epoch_dev, int rank, int world, int slot0,
+                     uint32_t* err_dev, uint64_t timeout_ns, void* stream);
 /* Microbenchmark halves of tcb_ps_nvls_update: mode 1 = multicast reduce only,
  * 2 = multicast store only. */
 int tcb_nvls_probe(int mode, const float* grad_mc, float* grad, const float* w, void* wcompute_mc,
@@ -211,12 +214,15 @@ int tcb_trainer_join(tcb_trainer* t, int rank, int world, const uint8_t* id128);
  * caller-allocated symmetric memory bound to multicast objects (e.g. torch
  * symmetric memory). `grad`/`wcompute` are this GPU's buffers, `*_mc` their
  * multicast addresses, `signal_pads_dev` a device array of the world's
- * P2P-mapped signal pads (>= (2048 + world) u32 each, slots 2048.. are used).
+ * P2P-mapped signal pads of signal_pad_bytes each (the barrier uses the slots
+ * min(2048, words - world) .. + world - 1; pads under 256 + world words are
+ * rejected). A peer that never reaches the barrier is reported by
+ * tcb_trainer_health / tcb_trainer_loss as TCB_ERR_NCCL instead of hanging.
  * Each step then runs barrier -> one kernel (multimem reduce of the own
  * shard + momentum SGD + multimem store of the bf16 weights) -> barrier,
  * replacing NCCL reduce-scatter / SGD / all-gather. */
 int tcb_trainer_attach_nvls(tcb_trainer* t, void* grad, const void* grad_mc, void* wcompute,
-                            void* wcompute_mc, void* const* signal_pads_dev);
+                            void* wcompute_mc, void* const* signal_pads_dev, size_t signal_pad_bytes);
 /* Asynchronous PS (config "ps_async": the aggregation + update of step s runs
  * on the trainer's own stream behind step s+1, which computes with weights
  * one update old — the paper's asynchronous policy): over
@@ -240,6 +246,12 @@ int tcb_trainer_stage_batch(tcb_trainer* t, const void* host_images, int format,
                             const int32_t* host_labels);
 int tcb_trainer_step(tcb_trainer* t, void* stream);
 int tcb_trainer_loss(tcb_trainer* t, float* loss_host, void* stream);
+/* Failure detection (synchronises `stream`): NCCL asynchronous errors (the
+ * communicators are aborted, never left hanging) and the NVLS barrier's bounded
+ * wait ($TCB_NVLS_TIMEOUT_MS, default 10 s). TCB_ERR_NCCL once a peer failed;
+ * the trainer stays failed. tcb_trainer_step polls the NCCL half (no sync) and
+ * tcb_trainer_loss runs the whole check. */
+int tcb_trainer_health(tcb_trainer* t, void* stream);
 /* Per-phase device times of the last timed step (ms): fwd, bwd, reduce-scatter,
  * sgd, all-gather — the StepTrace the Lemma-1 estimate consumes. */
 int tcb_trainer_phase_times(tcb_trainer* t, float* ms5);

@@ -108,8 +108,18 @@ __global__ void __launch_bounds__(256) nvls_probe_kernel(int mode, const float* 
 
 // All-GPU barrier on the signal pads (P2P-mapped, one u32 slot per peer).
 // Epochs are counted on the device so the kernel replays inside CUDA graphs.
+// The wait is bounded: a peer that does not arrive within timeout_ns (a rank
+// that stalled or died) sets *err = 1 and the barrier gives up instead of
+// hanging the GPU; the host reports TCB_ERR_NCCL at its next health check.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void nvls_barrier_kernel(uint32_t* const* __restrict__ pads, uint32_t* __restrict__ epoch,
-                                    int slot0, int rank, int world) {
+                                    int slot0, int rank, int world, uint32_t* __restrict__ err,
+                                    uint64_t timeout_ns) {
     __shared__ uint32_t e;
     if (threadIdx.x == 0) {
         e = *epoch + 1;
@@ -123,9 +133,18 @@ __global__ void nvls_barrier_kernel(uint32_t* const* __restrict__ pads, uint32_t
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(to), "r"(e) : "memory");
         const uint32_t* from = pads[rank] + slot0 + p;
         uint32_t got = 0;
-        do {
+        const uint64_t t0 = globaltimer_ns();
+        for (uint32_t spin = 0;; ++spin) {
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(got) : "l"(from) : "memory");
-        } while (static_cast<int32_t>(got - e) < 0);
+            if (static_cast<int32_t>(got - e) >= 0) break;
+            if ((spin & 1023) == 1023) {
+                if (*reinterpret_cast<volatile uint32_t*>(err) != 0) break;  // another lane timed out
+                if (globaltimer_ns() - t0 > timeout_ns) {
+                    atomicExch(err, 1u);
+                    break;
+                }
+            }
+        }
     }
     __syncthreads();
 }
@@ -133,9 +152,9 @@ __global__ void nvls_barrier_kernel(uint32_t* const* __restrict__ pads, uint32_t
 }  // namespace
 
 cudaError_t nvls_barrier(uint32_t* const* pads_dev, uint32_t* epoch_dev, int slot0, int rank, int world,
-                         cudaStream_t st) {
-    if (world > 32) return cudaErrorInvalidValue;
-    nvls_barrier_kernel<<<1, 32, 0, st>>>(pads_dev, epoch_dev, slot0, rank, world);
+                         cudaStream_t st, uint32_t* err_dev, uint64_t timeout_ns) {
+    if (world > 32 || err_dev == nullptr) return cudaErrorInvalidValue;
+    nvls_barrier_kernel<<<1, 32, 0, st>>>(pads_dev, epoch_dev, slot0, rank, world, err_dev, timeout_ns);
     return cudaGetLastError();
 }
 

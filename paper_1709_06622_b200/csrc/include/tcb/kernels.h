@@ -119,7 +119,7 @@ cudaError_t conv_tf32_wgrad(const ConvGeom& g, const float* dy, const float* x, 
 // per-rank pad pointers; slots slot0 .. slot0 + world - 1 are used);
 // `epoch_dev` is a zero-initialised per-rank device counter.
 cudaError_t nvls_barrier(uint32_t* const* pads_dev, uint32_t* epoch_dev, int slot0, int rank, int world,
-                         cudaStream_t st);
+                         cudaStream_t st, uint32_t* err_dev, uint64_t timeout_ns);
 // Fused reduce-scatter + momentum SGD + all-gather of elements [begin, begin+n)
 // of the flat buffer: grad_mc / wc_mc are multicast addresses of the fp32
 // gradient and bf16 compute-weight buffers; grad, w, v are local.

@@ -352,10 +352,10 @@ TCB_API int tcb_ps_nvls_update(const float* grad_mc, float* grad, float* w, floa
 }
 
 TCB_API int tcb_nvls_barrier(void* const* signal_pads_dev, uint32_t* epoch_dev, int rank, int world,
-                             void* stream) {
-    if (!signal_pads_dev || !epoch_dev) return fail(TCB_ERR_INVALID, "NULL argument");
-    return check_cuda(nvls_barrier(reinterpret_cast<uint32_t* const*>(signal_pads_dev), epoch_dev, 2048, rank,
-                                   world, static_cast<cudaStream_t>(stream)),
+                             int slot0, uint32_t* err_dev, uint64_t timeout_ns, void* stream) {
+    if (!signal_pads_dev || !epoch_dev || !err_dev) return fail(TCB_ERR_INVALID, "NULL argument");
+    return check_cuda(nvls_barrier(reinterpret_cast<uint32_t* const*>(signal_pads_dev), epoch_dev, slot0, rank,
+                                   world, static_cast<cudaStream_t>(stream), err_dev, timeout_ns),
                       "nvls_barrier");
 }
 

@@ -61,7 +61,11 @@ int algo_id(const std::string& a) {
     return -1;
 }
 
-Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int reps, cudaStream_t st) {
+// fused: the in-kernel split-K wgrad reduction, exactly as the executor runs it
+// (config "fused_split_reduce" / $TCB_FUSED_SPLIT_REDUCE, default off), so the
+// catalog's wgrad cost is the one the step pays.
+Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int reps, cudaStream_t st,
+                 bool fused) {
     Measured m;
     if (!algo_applies(g, algo, prec)) {
         m.why = "unsupported";
@@ -119,8 +123,9 @@ Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int rep
         if (algo == TCB_ALGO_GEMM)
             return dt == DType::BF16 ? conv_tc_wgrad(g, dy.p, x.p, static_cast<float*>(dw.p), ws.p, st,
                                                      false,
-                                                     reinterpret_cast<int*>(static_cast<char*>(ws.p) +
-                                                                            L.off_counters))
+                                                     fused ? reinterpret_cast<int*>(static_cast<char*>(ws.p) +
+                                                                                    L.off_counters)
+                                                           : nullptr)
                                      : conv_ffma_wgrad(g, static_cast<float*>(dy.p), static_cast<float*>(x.p),
                                                        static_cast<float*>(dw.p), ws.p, st);
         if (algo == TCB_ALGO_WINOGRAD)
@@ -190,6 +195,8 @@ TCB_API int tcb_profile_catalog(const char* request_json, char** reply_out) {
         // tensor-core layouts pad channels: 16-byte chunks = 8 bf16 / 4 fp32
         const int cpad = bf16 ? 8 : prec == TCB_PREC_TF32 ? 4 : 1;
         const int reps = std::max(1, req.value("reps", 5));
+        const char* fe = std::getenv("TCB_FUSED_SPLIT_REDUCE");
+        const bool fused = req.value("fused_split_reduce", fe != nullptr && fe[0] == '1');
         std::vector<traincap::CostEntry> rows;
         json detail = json::array(), skipped = json::array();
         cudaStream_t st = nullptr;
@@ -217,7 +224,7 @@ TCB_API int tcb_profile_catalog(const char* request_json, char** reply_out) {
                     const std::string algo = aj.get<std::string>();
                     const int id = algo_id(algo);
                     if (id < 0) return fail(TCB_ERR_INVALID, "unknown algorithm " + algo);
-                    const Measured m = measure(g, id, prec, layer_id > 1, reps, st);
+                    const Measured m = measure(g, id, prec, layer_id > 1, reps, st, fused);
                     if (!m.ok) {
                         skipped.push_back({{"layer_id", layer_id}, {"batch", n}, {"algorithm", algo},
                                            {"why", m.why}});

@@ -185,7 +185,12 @@ struct tcb_trainer {
     void* ext_wc = nullptr;
     void* wc_mc = nullptr;
     uint32_t* const* pads_dev = nullptr;
-    uint32_t* nvls_epoch = nullptr;
+    uint32_t* nvls_epoch = nullptr;  // [0] barrier epoch, [1] barrier timeout flag
+    int nvls_slot0 = 2048;           // first signal-pad slot of the PS barrier
+    uint64_t nvls_timeout_ns = 10ull * 1000 * 1000 * 1000;  // $TCB_NVLS_TIMEOUT_MS
+    // failure detection: a collective that failed, or a barrier that
+    // timed out, poisons the trainer; every later call reports it
+    std::string failed;
     float* grad_ptr() const { return ext_grad ? ext_grad : at<float>(off_grad); }
     void* wc_ptr() const {
         if (async_ps) return wc_buf(wc_rd);
@@ -983,14 +988,15 @@ int aggregate_and_update(tcb_trainer* t, cudaStream_t st, cudaEvent_t after_rs, 
         // written (barrier) -> one kernel reduces the own shard in the switch,
         // applies SGD and multicasts the bf16 weights -> all weights delivered
         // (barrier) before the next forward reads them
-        constexpr int kSlot0 = 2048;
-        TRY_CUDA(nvls_barrier(t->pads_dev, t->nvls_epoch, kSlot0, t->rank, t->world, st));
+        TRY_CUDA(nvls_barrier(t->pads_dev, t->nvls_epoch, t->nvls_slot0, t->rank, t->world, st,
+                              t->nvls_epoch + 1, t->nvls_timeout_ns));
         if (after_rs) TRY_CUDA(cudaEventRecord(after_rs, st));
         const size_t o = t->rank * t->shard;
         TRY_CUDA(ps_nvls_update(t->grad_mc, grad, param, mom, wc_mc, o, t->shard, t->lr, t->momentum,
                                 t->weight_decay, gscale, st));
         if (after_sgd) TRY_CUDA(cudaEventRecord(after_sgd, st));
-        TRY_CUDA(nvls_barrier(t->pads_dev, t->nvls_epoch, kSlot0, t->rank, t->world, st));
+        TRY_CUDA(nvls_barrier(t->pads_dev, t->nvls_epoch, t->nvls_slot0, t->rank, t->world, st,
+                              t->nvls_epoch + 1, t->nvls_timeout_ns));
         t->launches += 3;
     } else if (t->world > 1 && owners == t->world) {
         // PS shards = GPUs: reduce-scatter (in place) -> SGD on own shard -> all-gather
@@ -1168,9 +1174,22 @@ TCB_API int tcb_trainer_layout(const char* config_json, char** json_out) {
 }
 
 TCB_API int tcb_trainer_attach_nvls(tcb_trainer* t, void* grad, const void* grad_mc, void* wcompute,
-                                    void* wcompute_mc, void* const* signal_pads_dev) {
+                                    void* wcompute_mc, void* const* signal_pads_dev, size_t signal_pad_bytes) {
     if (!t || !grad || !grad_mc || !wcompute || !wcompute_mc || !signal_pads_dev)
         return fail(TCB_ERR_INVALID, "NULL argument");
+    {
+        // the barrier's slots sit at the top of the pad, clear of the low slots the
+        // symmetric-memory runtime uses for its own barriers
+        const long words = static_cast<long>(signal_pad_bytes / sizeof(uint32_t));
+        const long slot0 = std::min<long>(2048, words - t->world);
+        if (slot0 < 256)
+            return fail(TCB_ERR_INVALID, "signal pad of " + std::to_string(signal_pad_bytes) +
+                                             " bytes is too small for the NVLS barrier of " +
+                                             std::to_string(t->world) + " ranks");
+        t->nvls_slot0 = static_cast<int>(slot0);
+        if (const char* e = std::getenv("TCB_NVLS_TIMEOUT_MS"))
+            t->nvls_timeout_ns = static_cast<uint64_t>(std::max(1L, std::atol(e))) * 1000000ull;
+    }
     if (t->initialized) return fail(TCB_ERR_INVALID, "attach before the first step");
     if (!t->bf16) return fail(TCB_ERR_UNSUPPORTED, "the NVLS parameter-server path is bf16-only");
     if (t->world < 2 || (t->n_ps > 0 && t->n_ps < t->world))
@@ -1185,11 +1204,54 @@ TCB_API int tcb_trainer_attach_nvls(tcb_trainer* t, void* grad, const void* grad
     t->wc_mc = wcompute_mc;
     t->pads_dev = reinterpret_cast<uint32_t* const*>(signal_pads_dev);
     if (!t->nvls_epoch) {
-        TRY_CUDA(cudaMalloc(&t->nvls_epoch, sizeof(uint32_t)));
-        TRY_CUDA(cudaMemset(t->nvls_epoch, 0, sizeof(uint32_t)));
+        TRY_CUDA(cudaMalloc(&t->nvls_epoch, 2 * sizeof(uint32_t)));
+        TRY_CUDA(cudaMemset(t->nvls_epoch, 0, 2 * sizeof(uint32_t)));
     }
     t->nvls = true;
     return TCB_OK;
+}
+
+// Failure detection: NCCL's asynchronous errors (a peer died, a network /
+// NVLink error) are polled on the host without blocking; on one the
+// communicators are aborted so no collective hangs, and the trainer is poisoned.
+static int poll_comm_errors(tcb_trainer* t) {
+    if (!t->failed.empty()) return fail(TCB_ERR_NCCL, t->failed);
+    for (ncclComm_t* c : {&t->comm, &t->comm_bg}) {
+        if (!*c) continue;
+        ncclResult_t async = ncclSuccess;
+        const ncclResult_t r = ncclCommGetAsyncError(*c, &async);
+        if (r != ncclSuccess || (async != ncclSuccess && async != ncclInProgress)) {
+            t->failed = std::string("NCCL communicator failed: ") +
+                        ncclGetErrorString(r != ncclSuccess ? r : async) + " (communicators aborted)";
+            if (t->comm_bg) ncclCommAbort(t->comm_bg);
+            if (t->comm) ncclCommAbort(t->comm);
+            t->comm_bg = t->comm = nullptr;
+            return fail(TCB_ERR_NCCL, t->failed);
+        }
+    }
+    return TCB_OK;
+}
+
+// Full health check (synchronises `st`): NCCL async errors and the NVLS
+// barrier's timeout flag.
+static int check_health(tcb_trainer* t, cudaStream_t st) {
+    TRY(poll_comm_errors(t));
+    if (t->nvls_epoch) {
+        uint32_t flag = 0;
+        TRY_CUDA(cudaMemcpyAsync(&flag, t->nvls_epoch + 1, sizeof(flag), cudaMemcpyDeviceToHost, st));
+        TRY_CUDA(cudaStreamSynchronize(st));
+        if (flag != 0) {
+            t->failed = "NVLS parameter-server barrier timed out: a peer rank did not arrive within " +
+                        std::to_string(t->nvls_timeout_ns / 1000000) + " ms";
+            return fail(TCB_ERR_NCCL, t->failed);
+        }
+    }
+    return TCB_OK;
+}
+
+TCB_API int tcb_trainer_health(tcb_trainer* t, void* stream) {
+    if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
+    return check_health(t, static_cast<cudaStream_t>(stream));
 }
 
 static int ensure_ready(tcb_trainer* t, cudaStream_t st) {
@@ -1372,6 +1434,7 @@ TCB_API int tcb_trainer_attach_nvls_async(tcb_trainer* t, void* wcompute2, void*
 
 TCB_API int tcb_trainer_step(tcb_trainer* t, void* stream) {
     if (!t) return fail(TCB_ERR_INVALID, "NULL trainer");
+    TRY(poll_comm_errors(t));
     auto st = static_cast<cudaStream_t>(stream);
     TRY(ensure_ready(t, st));
     t->launches = 0;
@@ -1400,7 +1463,7 @@ TCB_API int tcb_trainer_loss(tcb_trainer* t, float* loss_host, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     TRY_CUDA(cudaMemcpyAsync(loss_host, t->at(t->off_loss), 4, cudaMemcpyDeviceToHost, st));
     TRY_CUDA(cudaStreamSynchronize(st));
-    return TCB_OK;
+    return check_health(t, st);
 }
 
 TCB_API int tcb_trainer_enable_timing(tcb_trainer* t, int on) {

@@ -40,7 +40,8 @@ def _lib():
         L.tcb_trainer_launch_count.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
         L.tcb_trainer_enable_layer_timing.argtypes = [_vp, ctypes.c_int]
         L.tcb_trainer_layer_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p)]
-        L.tcb_trainer_attach_nvls.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+        L.tcb_trainer_attach_nvls.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t]
+        L.tcb_trainer_health.argtypes = [_vp, _vp]
         L.tcb_trainer_attach_nvls_async.argtypes = [_vp, _vp, _vp]
         L.tcb_trainer_finish.argtypes = [_vp, _vp]
         L.tcb_free.argtypes = [_vp]
@@ -103,7 +104,8 @@ class Trainer:
             mcs.append(h.multicast_ptr + delta)
         device.check(_lib().tcb_trainer_attach_nvls(self.handle, _vp(bufs[0].data_ptr()), _vp(mcs[0]),
                                                     _vp(bufs[1].data_ptr()), _vp(mcs[1]),
-                                                    _vp(handles[0].signal_pad_ptrs_dev)))
+                                                    _vp(handles[0].signal_pad_ptrs_dev),
+                                                    int(handles[0].signal_pad_size)))
         if len(bufs) > 2:  # asynchronous PS: the second weight buffer
             device.check(_lib().tcb_trainer_attach_nvls_async(self.handle, _vp(bufs[2].data_ptr()), _vp(mcs[2])))
         self._symm = (bufs, handles)  # keep the allocations alive
@@ -145,6 +147,11 @@ class Trainer:
         out = ctypes.c_float()
         device.check(_lib().tcb_trainer_loss(self.handle, ctypes.byref(out), self._stream()))
         return out.value
+
+    def health(self):
+        """Failure detection: raises on an NCCL asynchronous error or an NVLS
+        barrier timeout (a peer rank stalled or died); synchronises the stream."""
+        device.check(_lib().tcb_trainer_health(self.handle, self._stream()))
 
     def enable_timing(self, on=True):
         device.check(_lib().tcb_trainer_enable_timing(self.handle, int(on)))

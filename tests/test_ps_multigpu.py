@@ -203,3 +203,33 @@ def test_four_gpu_nvls_matches_nccl_within_fp32_tolerance():
         assert e <= 1e-5, (r, e)
         mism = np.mean(got[r][2] != ref[r][2])
         assert mism <= 1e-3, (r, mism)
+
+
+def test_nvls_barrier_times_out_instead_of_hanging():
+    """Failure detection on one GPU: a 2-rank barrier whose peer never
+    arrives (both pad pointers local, rank 1 silent) gives up after the
+    timeout, raises the device error flag and returns — no hung GPU."""
+    import ctypes
+    import time
+    from paper_1709_06622_b200 import device
+    L = device.lib()
+    vp = ctypes.c_void_p
+    L.tcb_nvls_barrier.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_uint64, vp]
+    pads = [torch.zeros(4096, dtype=torch.int32, device="cuda") for _ in range(2)]
+    pad_ptrs = torch.tensor([p.data_ptr() for p in pads], dtype=torch.int64, device="cuda")
+    epoch = torch.zeros(1, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    t0 = time.time()
+    device.check(L.tcb_nvls_barrier(vp(pad_ptrs.data_ptr()), vp(epoch.data_ptr()), 0, 2, 2048,
+                                    vp(err.data_ptr()), 50_000_000, vp(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 5.0
+    assert int(err.item()) == 1 and int(epoch.item()) == 1
+    # a complete barrier (the peer's signal present) does not set the flag
+    err.zero_()
+    pads[0][2048 + 1] = 2  # rank 1's arrival for epoch 2, seen in rank 0's pad
+    device.check(L.tcb_nvls_barrier(vp(pad_ptrs.data_ptr()), vp(epoch.data_ptr()), 0, 2, 2048,
+                                    vp(err.data_ptr()), 50_000_000, vp(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
