@@ -232,19 +232,40 @@ def _nvlink_peak():
 NVLINK_PEER_GBPS, NVLINK_PEER_SRC = _nvlink_peak()
 
 
-def lemmas(phases, world, param_bytes, out_dir, transport="nccl"):
+def data_steps(data_ms, step_ms, e2e_ms):
+    """Paper steps 2-4 for the StepTrace, each with its measured time and
+    whether it is hidden. host_to_gpu_transfer is hidden only
+    when the e2e step (staged H2D + preparation + loss readback) is longer than
+    the device-resident step by less than a quarter of the copy time; the
+    on-device preparation runs on the step stream and is never hidden; loading
+    is hidden when one batch is produced faster than a step (a background
+    loader keeps up)."""
+    gap = (e2e_ms - step_ms) if e2e_ms is not None else None
+    h2d = max(data_ms.get("host_to_gpu_transfer", 0.0), 0.0)
+    prep = max(data_ms.get("data_preparation", 0.0), 0.0)
+    return {"data_loading": (data_ms.get("data_loading", 0.0), data_ms.get("data_loading", 0.0) < step_ms),
+            "data_preparation": (prep, False),
+            "host_to_gpu_transfer": (h2d, gap is not None and gap - prep < 0.25 * h2d),
+            "e2e_minus_device_ms": round(gap, 4) if gap is not None else None}
+
+
+def lemmas(phases, world, param_bytes, out_dir, transport="nccl", data=None):
     """Paper Lemma 1 / Lemma 2 evaluated by the traincap planner (C-ABI) from
     this run's measured StepTrace: gpu_processing = fwd + bwd, and the
     unhidden distributed_update (reduce-scatter), parameter_update (SGD) and
-    parameter_refresh (all-gather) as overhead (PAPER.md:229-241)."""
+    parameter_refresh (all-gather) as overhead, plus the measured data steps
+    (data_steps(): hidden only where the e2e run proves the overlap)
+    (PAPER.md:229-241)."""
     from paper_1709_06622_b200 import planner
 
     p = planner.default()
     trace = (f"gpu_processing {(phases['fwd'] + phases['bwd']) / 1e3!r}\n"
              f"distributed_update {phases['reduce_scatter'] / 1e3!r}\n"
              f"parameter_update {phases['sgd'] / 1e3!r}\n"
-             f"parameter_refresh {phases['all_gather'] / 1e3!r}\n"
-             "data_loading 0 hidden\ndata_preparation 0 hidden\nhost_to_gpu_transfer 0 hidden\n")
+             f"parameter_refresh {phases['all_gather'] / 1e3!r}\n")
+    for step in ("data_loading", "data_preparation", "host_to_gpu_transfer"):
+        ms, hidden = (data or {}).get(step, (0.0, True))
+        trace += f"{step} {ms / 1e3!r}{' hidden' if hidden else ''}\n"
     with open(os.path.join(out_dir, f"steptrace_g{world}.txt"), "w") as f:
         f.write(trace)
     prof = p.call("estimate_overhead_ratio", trace=trace)
@@ -576,12 +597,37 @@ def main():
 
     # phase breakdown (StepTrace for Lemma 1): median over 3 steps with only the
     # six phase events; then per-conv-pass times from one step with layer events
+    # host batches (uint8 NHWC pixels, what a decoding data loader hands over,
+    # pinned): the e2e arm's input and the StepTrace's data steps (paper steps
+    # 2-4). The synthetic "dataset" is two decoded batches in pageable host
+    # memory; data_loading = host time to load one batch from it into the pinned
+    # staging buffer (torch's multithreaded copy), median of 3.
+    inp = tr.describe()["layers"][0]
+    n_img, hh, ww = args.batch, inp["shape"][1], inp["shape"][2]
+    gen = torch.Generator().manual_seed(1234 + rank)
+    dataset = [(torch.randint(0, 256, (n_img, hh, ww, inp["c_logical"]), dtype=torch.uint8, generator=gen),
+                torch.randint(0, tr.cfg["classes"], (n_img,), dtype=torch.int32, generator=gen)) for _ in range(2)]
+    host = [(torch.empty_like(x).pin_memory(), torch.empty_like(y).pin_memory()) for x, y in dataset]
+    loads = []
+    for i in range(3):
+        t0 = time.perf_counter()
+        host[i % 2][0].copy_(dataset[i % 2][0])
+        host[i % 2][1].copy_(dataset[i % 2][1])
+        loads.append(time.perf_counter() - t0)
+    for i in range(2):
+        host[i][0].copy_(dataset[i][0])
+        host[i][1].copy_(dataset[i][1])
+    load_ms = sorted(loads)[1] * 1e3
     tr.enable_timing(True)
-    samples = []
-    for _ in range(3):
+    samples, dsamples = [], []
+    for i in range(3):
+        tr.stage_batch(*host[i % 2])
         tr.step()
         samples.append(tr.phase_times())
+        dsamples.append(tr.data_times())
     phases = {k: sorted(sm[k] for sm in samples)[1] for k in samples[0]}
+    data_ms = {k: sorted(sm[k] for sm in dsamples)[1] for k in dsamples[0]}
+    data_ms["data_loading"] = load_ms
     tr.enable_timing(False)
     tr.enable_layer_timing(True)
     tr.step()
@@ -630,17 +676,9 @@ def main():
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        # uint8 NHWC pixels (what a decoding data loader hands over), two pinned
-        # host batches alternating; each step's batch is staged (H2D on the
-        # trainer's copy stream) while the previous step computes — the paper's
-        # pipelined steps 2-4
-        inp = tr.describe()["layers"][0]
-        n, h, w = args.batch, inp["shape"][1], inp["shape"][2]
-        cl = inp["c_logical"]
-        gen = torch.Generator().manual_seed(1234 + rank)
-        host = [(torch.randint(0, 256, (n, h, w, cl), dtype=torch.uint8, generator=gen).pin_memory(),
-                 torch.randint(0, tr.cfg["classes"], (n,), dtype=torch.int32, generator=gen).pin_memory())
-                for _ in range(2)]
+        # the two pinned host batches alternate; each step's batch is staged (H2D
+        # on the trainer's copy stream) while the previous step computes — the
+        # paper's pipelined steps 2-4
         lossbuf = torch.empty(1, dtype=torch.float32).pin_memory()
         barrier()
         e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -700,6 +738,7 @@ def main():
         except Exception as exc:  # noqa: BLE001 — report, never fail the bench line
             cpu["planner"] = {"error": repr(exc)}
 
+    dsteps = data_steps(data_ms, ms / args.steps, e2e["ms_per_step"] if e2e else None)
     if rank == 0:
         layout = tr.describe()
         param_bytes = layout["param_padded"] * 4
@@ -739,7 +778,8 @@ def main():
             "hbm_arena_bytes": layout.get("arena_bytes"),
             "ps": {"param_bytes": param_bytes, "rs_ag_bytes_per_gpu_step": rs_ag_bytes,
                    "busbw": ps_bandwidth(phases, world, param_bytes, transport)},
-            "lemmas": lemmas(phases, world, param_bytes, os.path.join(ROOT, "gpurun_out"), transport),
+            "data_steps_ms": dsteps,
+            "lemmas": lemmas(phases, world, param_bytes, os.path.join(ROOT, "gpurun_out"), transport, dsteps),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -256,6 +256,10 @@ int tcb_trainer_health(tcb_trainer* t, void* stream);
  * sgd, all-gather — the StepTrace the Lemma-1 estimate consumes. */
 int tcb_trainer_phase_times(tcb_trainer* t, float* ms5);
 int tcb_trainer_enable_timing(tcb_trainer* t, int on);
+/* Paper steps 3-4 of the last staged batch consumed while timing was on:
+ * {host-to-device copy ms on the copy stream, on-device preparation ms}
+ * (-1 where none was timed). */
+int tcb_trainer_data_times(tcb_trainer* t, float* ms2);
 /* Introspection for tests: JSON description of the layer table, flat-buffer
  * layout (per-layer offsets) and shard table; caller frees with tcb_free. */
 int tcb_trainer_describe(tcb_trainer* t, char** json_out);

@@ -128,6 +128,11 @@ struct tcb_trainer {
     uint64_t stage_w = 0, stage_r = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t staged[2]{}, consumed[2]{};
+    // paper steps 3-4 measured into the StepTrace (timing mode): the staged
+    // batch's host-to-device copy on the copy stream, its on-device preparation
+    // (uint8 -> compute dtype, channel padding) on the step stream
+    cudaEvent_t ev_h2d[2]{}, ev_prep[2]{};
+    bool h2d_timed = false, prep_timed = false;
     bool consumed_recorded[2] = {false, false};
     size_t ws_bytes = 0, colsum_bytes = 0;
     size_t off_pack_jobs = 0;  // device table of the batched dgrad weight packing
@@ -1105,6 +1110,10 @@ TCB_API int tcb_trainer_destroy(tcb_trainer* t) {
     }
     for (cudaEvent_t& e : t->ph.e)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+        if (t->ev_h2d[i]) cudaEventDestroy(t->ev_h2d[i]);
+        if (t->ev_prep[i]) cudaEventDestroy(t->ev_prep[i]);
+    }
     for (auto& a : t->lev)
         for (cudaEvent_t e : a)
             if (e) cudaEventDestroy(e);
@@ -1299,11 +1308,23 @@ TCB_API int tcb_trainer_stage_batch(tcb_trainer* t, const void* host_images, int
     if (t->consumed_recorded[k]) TRY_CUDA(cudaStreamWaitEvent(t->copy_stream, t->consumed[k], 0));
     const Node& in = t->nodes[0];
     const size_t elems = size_t(in.n) * in.h * in.w * in.c_logical;
+    if (t->timing) {
+        if (!t->ev_h2d[0])
+            for (int i = 0; i < 2; ++i) {
+                TRY_CUDA(cudaEventCreate(&t->ev_h2d[i]));
+                TRY_CUDA(cudaEventCreate(&t->ev_prep[i]));
+            }
+        TRY_CUDA(cudaEventRecord(t->ev_h2d[0], t->copy_stream));
+    }
     TRY_CUDA(cudaMemcpyAsync(t->at(t->off_stage[k]), host_images,
                              elems * (format == TCB_INPUT_U8 ? 1 : 4), cudaMemcpyHostToDevice,
                              t->copy_stream));
     TRY_CUDA(cudaMemcpyAsync(t->at(t->off_stage_labels[k]), host_labels, size_t(t->batch) * 4,
                              cudaMemcpyHostToDevice, t->copy_stream));
+    if (t->timing) {
+        TRY_CUDA(cudaEventRecord(t->ev_h2d[1], t->copy_stream));
+        t->h2d_timed = true;
+    }
     TRY_CUDA(cudaEventRecord(t->staged[k], t->copy_stream));
     t->stage_format[k] = format;
     ++t->stage_w;
@@ -1317,6 +1338,8 @@ static int consume_staged(tcb_trainer* t, cudaStream_t st) {
     TRY_CUDA(cudaStreamWaitEvent(st, t->staged[k], 0));
     const Node& in = t->nodes[0];
     const size_t px = size_t(in.n) * in.h * in.w;
+    const bool timed = t->timing && t->ev_prep[0];
+    if (timed) TRY_CUDA(cudaEventRecord(t->ev_prep[0], st));
     if (t->stage_format[k] == TCB_INPUT_U8)
         TRY_CUDA(pack_channels_u8(t->dt, t->at<uint8_t>(t->off_stage[k]), t->at(in.act), px, in.c_logical,
                                   in.c, st));
@@ -1325,6 +1348,10 @@ static int consume_staged(tcb_trainer* t, cudaStream_t st) {
                                st));
     TRY_CUDA(cudaMemcpyAsync(t->at(t->off_labels), t->at(t->off_stage_labels[k]), size_t(t->batch) * 4,
                              cudaMemcpyDeviceToDevice, st));
+    if (timed) {
+        TRY_CUDA(cudaEventRecord(t->ev_prep[1], st));
+        t->prep_timed = true;
+    }
     TRY_CUDA(cudaEventRecord(t->consumed[k], st));
     t->consumed_recorded[k] = true;
     ++t->stage_r;
@@ -1478,6 +1505,23 @@ TCB_API int tcb_trainer_phase_times(tcb_trainer* t, float* ms5) {
     cudaEvent_t* e = t->ph.e;
     TRY_CUDA(cudaEventSynchronize(e[5]));
     for (int i = 0; i < 5; ++i) TRY_CUDA(cudaEventElapsedTime(&ms5[i], e[i], e[i + 1]));
+    return TCB_OK;
+}
+
+// Paper steps 3-4 of the last timed staged batch: {host-to-device copy ms
+// (copy stream), on-device preparation ms (uint8 -> compute dtype)}; -1 where
+// no staged batch was timed.
+TCB_API int tcb_trainer_data_times(tcb_trainer* t, float* ms2) {
+    if (!t || !ms2) return fail(TCB_ERR_INVALID, "NULL argument");
+    ms2[0] = ms2[1] = -1.f;
+    if (t->h2d_timed) {
+        TRY_CUDA(cudaEventSynchronize(t->ev_h2d[1]));
+        TRY_CUDA(cudaEventElapsedTime(&ms2[0], t->ev_h2d[0], t->ev_h2d[1]));
+    }
+    if (t->prep_timed) {
+        TRY_CUDA(cudaEventSynchronize(t->ev_prep[1]));
+        TRY_CUDA(cudaEventElapsedTime(&ms2[1], t->ev_prep[0], t->ev_prep[1]));
+    }
     return TCB_OK;
 }
 

@@ -148,6 +148,12 @@ class Trainer:
         device.check(_lib().tcb_trainer_loss(self.handle, ctypes.byref(out), self._stream()))
         return out.value
 
+    def data_times(self) -> dict:
+        """Paper steps 3-4 of the last staged batch consumed with timing on."""
+        ms = (ctypes.c_float * 2)()
+        device.check(_lib().tcb_trainer_data_times(self.handle, ms))
+        return {"host_to_gpu_transfer": ms[0], "data_preparation": ms[1]}
+
     def health(self):
         """Failure detection: raises on an NCCL asynchronous error or an NVLS
         barrier timeout (a peer rank stalled or died); synchronises the stream."""
