@@ -493,7 +493,7 @@ def exclusive_times(kernels):
 
 def kernel_class(name):
     import re
-    n = name.replace("(anonymous namespace)::", "").replace("void ", "").replace("tcb::", "")
+    n = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("void ", "").replace("tcb::", "")
     n = re.sub(r"<.*>", "", n)
     return re.sub(r"\(.*\)$", "", n).strip()
 

@@ -89,10 +89,14 @@ struct Params {
     // dgrad phase
     DgradPhase ph;
     FastDiv d_hwq, d_wq, d_ts;
+    // batched plain GEMMs (Winograd / FFT transform planes): `batch` independent
+    // [M x Kdim] x [Ncol x Kdim]^T problems in contiguous planes; 3-D tensor maps
+    // carry the plane index, outputs (and wgrad partials) are [split][batch][M][Ncol]
+    int batch;
 };
 
 struct TileCoord {
-    int split, mt, nt, kb_begin, kb_end;
+    int split, mt, nt, kb_begin, kb_end, b;
 };
 
 template <bool CTA2 = false>
@@ -100,13 +104,16 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& p, int t, uint32_t
     TileCoord c;
     c.nt = t % p.n_tiles;
     const int rest = t / p.n_tiles;
+    int outer;
     if constexpr (CTA2) {
         c.mt = 2 * (rest % p.m_pairs) + static_cast<int>(rank);
-        c.split = rest / p.m_pairs;
+        outer = rest / p.m_pairs;
     } else {
         c.mt = rest % p.m_tiles;
-        c.split = rest / p.m_tiles;
+        outer = rest / p.m_tiles;
     }
+    c.b = outer % p.batch;
+    c.split = outer / p.batch;
     c.kb_begin = c.split * p.kb_per_split;
     c.kb_end = min(p.kb_total, c.kb_begin + p.kb_per_split);
     return c;
@@ -277,7 +284,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
     if (m >= s.M || col0 >= s.Ncol) return;
     if constexpr (MODE == ConvMode::Wgrad) {
         float* out = static_cast<float*>(p.out) +
-                     (static_cast<size_t>(tc.split) * s.M + m) * s.Ncol + col0;
+                     ((static_cast<size_t>(tc.split) * p.batch + tc.b) * s.M + m) * s.Ncol + col0;
         if (col0 + 32 <= s.Ncol) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
@@ -288,7 +295,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
             for (int i = 0; i < 32 && col0 + i < s.Ncol; ++i) out[i] = __uint_as_float(acc[i]);
         }
     } else {
-        const size_t base = row * s.Ncol + col0;
+        const size_t base = (static_cast<size_t>(tc.b) * s.M + row) * s.Ncol + col0;
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + base;
         const bool full = col0 + 32 <= s.Ncol;
 #pragma unroll
@@ -502,8 +509,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     if (!CTA2 || rank == 0)
                         ptx::mbar_arrive_expect_tx(&full[stage], (CTA2 ? 2 : 1) * C::kStageBytes);
                     auto ld2 = [&](uint32_t dst, const CUtensorMap* m, int c0, int c1) {
-                        if constexpr (CTA2) ptx::tma_load_2d_2sm(dst, m, bar_u, c0, c1);
-                        else ptx::tma_load_2d(dst, m, &full[stage], c0, c1);
+                        if (LOAD == kPlain && p.batch > 1) {  // plane index = third map dimension
+                            if constexpr (CTA2) ptx::tma_load_3d_2sm(dst, m, bar_u, c0, c1, tc.b);
+                            else ptx::tma_load_3d(dst, m, &full[stage], c0, c1, tc.b);
+                        } else {
+                            if constexpr (CTA2) ptx::tma_load_2d_2sm(dst, m, bar_u, c0, c1);
+                            else ptx::tma_load_2d(dst, m, &full[stage], c0, c1);
+                        }
                     };
                     auto ldi = [&](uint32_t dst, const CUtensorMap* m, int c, int w, int h, int n,
                                    uint16_t ow, uint16_t oh) {
@@ -1077,10 +1089,10 @@ struct SplitPlan {
     int splits, kb_per_split;
 };
 
-SplitPlan plan_splits(const ConvShape& s, int bn, bool pair = false) {
+SplitPlan plan_splits(const ConvShape& s, int bn, bool pair = false, int batch = 1) {
     const int kb_total = (s.Kdim + BK - 1) / BK;
     const int m_tiles = (s.M + BM - 1) / BM;
-    const int tiles = (pair ? (m_tiles + 1) / 2 : m_tiles) * ((s.Ncol + bn - 1) / bn);
+    const int tiles = (pair ? (m_tiles + 1) / 2 : m_tiles) * ((s.Ncol + bn - 1) / bn) * batch;
     // one exact wave: splits * tiles <= #SMs (#pairs), so every CTA runs one equal
     // unit (no tail round) and the fp32 partials stay as few as the wave allows
     const int slots = (num_sms() - g_sm_reserve) / (pair ? 2 : 1);
@@ -1114,6 +1126,15 @@ bool im2col_ok(const Params& p) {
 template <ConvMode MODE, int LOAD>
 bool build_maps(Params& p, const void* a_matrix, const void* b_matrix, int bn) {
     const ConvShape& s = p.s;
+    if (LOAD == kPlain && p.batch > 1) {
+        // batched planes: [batch][rows][cols] bf16 with the plane as the third dimension
+        if (MODE == ConvMode::Wgrad)
+            return make_tmap_bf16_3d(&p.tmap_a, a_matrix, p.batch, s.Kdim, s.K, BK, 64) &&
+                   make_tmap_bf16_3d(&p.tmap_b, b_matrix, p.batch, s.Kdim, s.C, BK, 64);
+        if (MODE != ConvMode::Fwd) return false;
+        return make_tmap_bf16_3d(&p.tmap_b, b_matrix, p.batch, s.Ncol, s.Kdim, bn, 64) &&
+               make_tmap_bf16_3d(&p.tmap_a, a_matrix, p.batch, s.M, s.Kdim, BM, 64);
+    }
     if (MODE == ConvMode::Wgrad) {
         if (LOAD == kGather) return true;
         // dy [P][K], MN-major 64 x 64 boxes
@@ -1181,7 +1202,8 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
         p.splits = 1;
         p.kb_per_split = p.kb_total;
     }
-    p.num_tiles = (CTA2 ? p.m_pairs : p.m_tiles) * p.n_tiles * p.splits;
+    if (p.batch < 1) p.batch = 1;
+    p.num_tiles = (CTA2 ? p.m_pairs : p.m_tiles) * p.n_tiles * p.batch * p.splits;
     const int sms = std::max(2, num_sms() - g_sm_reserve);
     const int grid = CTA2 ? 2 * std::min(p.num_tiles, sms / 2) : std::min(p.num_tiles, sms);
     cudaLaunchConfig_t cfg{};
@@ -1225,7 +1247,7 @@ int g_epi_kb_spatial = -1;  // ... and for spatial (im2col) layers
 // (Inception-v3's 5x5 / 1x7 / 7x1 branches).
 template <ConvMode MODE>
 bool use_epi(const Params& p) {
-    if (MODE == ConvMode::Wgrad) return false;
+    if (MODE == ConvMode::Wgrad || p.batch > 1) return false;
     if (MODE == ConvMode::Dgrad && (p.s.sh != 1 || p.s.sw != 1)) return false;
     if (g_epi_kb < 0) {
         const char* e = getenv("TCB_CONV_EPI_KB");
@@ -1393,6 +1415,50 @@ cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const E
     p.residual = static_cast<const __nv_bfloat16*>(ep.residual);
     p.relu = ep.relu ? 1 : 0;
     return dispatch<ConvMode::Fwd>(p, a_matrix, b_matrix, st);
+}
+
+// Batched plain GEMMs (Winograd's 16 / FFT's 40 transform-plane products in ONE
+// launch): y[b] = x[b] * w[b]^T for b < batch, x[b] [M][Kdim], w[b] [Ncol][Kdim],
+// y[b] [M][Ncol] bf16, g the 1x1 / stride-1 / unpadded "conv" of one plane.
+cudaError_t conv_tc_fwd_batched(const ConvGeom& g, int batch, const void* x, const void* w, void* y,
+                                cudaStream_t st) {
+    Params p{};
+    p.s = make_shape(g, ConvMode::Fwd);
+    if (!plain_geometry(p.s) || batch < 1) return cudaErrorInvalidValue;
+    p.batch = batch;
+    p.a = static_cast<const __nv_bfloat16*>(x);
+    p.out = y;
+    return dispatch_bn<ConvMode::Fwd, kPlain>(p, x, w, st);
+}
+
+size_t conv_tc_wgrad_batched_workspace(const ConvGeom& g, int batch) {
+    const ConvShape s = make_shape(g, ConvMode::Wgrad);
+    const int bn = wgrad_bn(s);
+    const SplitPlan sp = plan_splits(s, bn, wgrad_pair(s, bn), batch);
+    return sp.splits > 1 ? size_t(sp.splits) * batch * s.M * s.Ncol * sizeof(float) : 0;
+}
+
+// dw[b] [Ncol=K][Kdim... ] = dy[b]^T x[b] summed over the plane's pixels, fp32,
+// one launch (split-K over the batch's tiles) + one fixed-order reduction.
+cudaError_t conv_tc_wgrad_batched(const ConvGeom& g, int batch, const void* dy, const void* x, float* dw,
+                                  void* workspace, cudaStream_t st) {
+    Params p{};
+    p.s = make_shape(g, ConvMode::Wgrad);
+    if (!plain_geometry(p.s) || batch < 1) return cudaErrorInvalidValue;
+    const int bn = wgrad_bn(p.s);
+    const bool pair = wgrad_pair(p.s, bn);
+    p.cta2 = pair ? 1 : 0;
+    const SplitPlan sp = plan_splits(p.s, bn, pair, batch);
+    p.batch = batch;
+    p.a = static_cast<const __nv_bfloat16*>(dy);
+    p.b = static_cast<const __nv_bfloat16*>(x);
+    p.splits = sp.splits;
+    p.kb_per_split = sp.kb_per_split;
+    p.out = sp.splits > 1 ? workspace : static_cast<void*>(dw);
+    if (sp.splits > 1 && workspace == nullptr) return cudaErrorInvalidValue;
+    cudaError_t e = dispatch_bn<ConvMode::Wgrad, kPlain>(p, dy, x, st);
+    if (e != cudaSuccess || sp.splits == 1) return e;
+    return split_reduce(static_cast<const float*>(workspace), sp.splits, size_t(batch) * p.s.M * p.s.Ncol, dw, st);
 }
 
 bool conv_tc_dgrad_needs_pack(const ConvGeom& g) {

@@ -45,6 +45,21 @@ inline bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// `planes` contiguous row-major bf16 matrices [rows][cols] as one 3-D map
+// (the plane index is the third coordinate), boxes of box_rows x box_cols x 1.
+inline bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t planes, uint64_t rows, uint64_t cols,
+                              uint32_t box_rows, uint32_t box_cols = 64) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {cols, rows, planes};
+    const cuuint64_t strides[2] = {cols * 2, rows * cols * 2};
+    const cuuint32_t box[3] = {box_cols, box_rows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // KRSC bf16 filter bank viewed as [K][R*S][C] (C contiguous), read in boxes of
 // 64 filters x 1 tap x 64 channels: an MN-major (channel-contiguous) 128B-
 // swizzled operand tile for the dgrad GEMM, taken straight from the weights.

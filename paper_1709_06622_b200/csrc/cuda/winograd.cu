@@ -63,67 +63,91 @@ Tiles make_tiles(int n, int h, int w, int c, int k, int pad) {
 
 // ---------------------------------------------------------------- input ---
 // V[xi][t][c] = (B^T d B)[xi], d = 4x4 input patch at (2i - pad, 2j - pad).
-template <typename T, int VW>
-__global__ void wino_input_kernel(const T* __restrict__ x, T* __restrict__ V, Tiles tl) {
-    const int cg = tl.c / VW;
-    const size_t total = tl.T * cg;
+// Shared-memory-staged input transform (the path in use): one block per
+// (image, tile row, channel slice of 128 bytes: 64 bf16 / 32 fp32 channels).
+// The 4 input rows the tile row reads are staged once in shared memory as
+// [row][padded column][channel] with the zero padding materialised (each
+// input element leaves HBM once instead of once per overlapping patch), then
+// every thread transforms one (tile, channel pair) patch out of shared memory
+// — 16 values in registers instead of 16 x 8 — and stores the 16 planes; the
+// lanes of a warp hold consecutive channel pairs, so every plane store is a
+// contiguous 128-byte segment.
+template <typename T>
+__global__ void __launch_bounds__(256) wino_input_smem_kernel(const T* __restrict__ x, T* __restrict__ V,
+                                                              Tiles tl, int cslice) {
+    extern __shared__ __align__(16) uint8_t wsm_raw[];
+    T* sm = reinterpret_cast<T*>(wsm_raw);
+    constexpr int VE = 16 / sizeof(T);
+    const int n = blockIdx.x / tl.th, i = blockIdx.x - n * tl.th;
+    const int c0 = blockIdx.y * cslice;
+    const int cw = min(cslice, tl.c - c0);
+    const int Wp = 2 * tl.tw + 2;
+    const int vpr = cw / VE;
+    for (int idx = threadIdx.x; idx < 4 * Wp * vpr; idx += blockDim.x) {
+        const int v = idx % vpr, rest = idx / vpr;
+        const int u = rest % Wp, a = rest / Wp;
+        const int hh = 2 * i - tl.pad + a, ww = u - tl.pad;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (hh >= 0 && hh < tl.h && ww >= 0 && ww < tl.w)
+            val = __ldg(reinterpret_cast<const uint4*>(x + ((size_t(n) * tl.h + hh) * tl.w + ww) * tl.c + c0 + v * VE));
+        *reinterpret_cast<uint4*>(sm + (a * Wp + u) * cslice + v * VE) = val;
+    }
+    __syncthreads();
+    const int pairs = cw / 2;
     const size_t plane = tl.T * tl.c;
-    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
-         idx += size_t(gridDim.x) * blockDim.x) {
-        const int c = int(idx % cg) * VW;
-        const size_t t = idx / cg;
-        const int j = int(t % tl.tw);
-        const int i = int((t / tl.tw) % tl.th);
-        const int n = int(t / (size_t(tl.tw) * tl.th));
-        float d[4][4][VW];
+    const size_t trow = (size_t(n) * tl.th + i) * tl.tw;
+    // channel pairs as float2 through packed fp32x2 adds (FADD2: both channels at once)
+    auto ld = [&](int a, int col, int pc) -> float2 {
+        const T* q = sm + (a * Wp + col) * cslice + 2 * pc;
+        if constexpr (sizeof(T) == 2) return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(q));
+        else return *reinterpret_cast<const float2*>(q);
+    };
+    auto add = [](float2 x, float2 y) { return __fadd2_rn(x, y); };
+    auto sub = [](float2 x, float2 y) { return __fadd2_rn(x, make_float2(-y.x, -y.y)); };
+    for (int idx = threadIdx.x; idx < tl.tw * pairs; idx += blockDim.x) {
+        const int pc = idx % pairs, j = idx / pairs;
+        float2 d[4][4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int hh = 2 * i - tl.pad + a;
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int ww = 2 * j - tl.pad + b;
-                if (hh >= 0 && hh < tl.h && ww >= 0 && ww < tl.w) {
-                    const Vec<T, VW> v =
-                        *reinterpret_cast<const Vec<T, VW>*>(x + ((size_t(n) * tl.h + hh) * tl.w + ww) * tl.c + c);
+            for (int b = 0; b < 4; ++b) d[a][b] = ld(a, 2 * j + b, pc);
+        float2 r[4][4];  // B^T d
 #pragma unroll
-                    for (int e = 0; e < VW; ++e) d[a][b][e] = to_f32<T>(v.v[e]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VW; ++e) d[a][b][e] = 0.f;
-                }
-            }
+        for (int b = 0; b < 4; ++b) {
+            r[0][b] = sub(d[0][b], d[2][b]);
+            r[1][b] = add(d[1][b], d[2][b]);
+            r[2][b] = sub(d[2][b], d[1][b]);
+            r[3][b] = sub(d[1][b], d[3][b]);
         }
-        // rows: B^T d
-        float r[4][4][VW];
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-#pragma unroll
-            for (int e = 0; e < VW; ++e) {
-                r[0][b][e] = d[0][b][e] - d[2][b][e];
-                r[1][b][e] = d[1][b][e] + d[2][b][e];
-                r[2][b][e] = d[2][b][e] - d[1][b][e];
-                r[3][b][e] = d[1][b][e] - d[3][b][e];
-            }
-        // cols: (B^T d) B
+        T* dst = V + (trow + j) * tl.c + c0 + 2 * pc;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-            float o[4][VW];
-#pragma unroll
-            for (int e = 0; e < VW; ++e) {
-                o[0][e] = r[a][0][e] - r[a][2][e];
-                o[1][e] = r[a][1][e] + r[a][2][e];
-                o[2][e] = r[a][2][e] - r[a][1][e];
-                o[3][e] = r[a][1][e] - r[a][3][e];
-            }
+            const float2 o[4] = {sub(r[a][0], r[a][2]), add(r[a][1], r[a][2]), sub(r[a][2], r[a][1]),
+                                 sub(r[a][1], r[a][3])};
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                Vec<T, VW> out;
-#pragma unroll
-                for (int e = 0; e < VW; ++e) out.v[e] = from_f32<T>(o[b][e]);
-                *reinterpret_cast<Vec<T, VW>*>(V + (a * 4 + b) * plane + t * tl.c + c) = out;
+                T* q = dst + (a * 4 + b) * plane;
+                if constexpr (sizeof(T) == 2) *reinterpret_cast<__nv_bfloat162*>(q) = __floats2bfloat162_rn(o[b].x, o[b].y);
+                else *reinterpret_cast<float2*>(q) = o[b];
             }
         }
     }
+}
+
+// Input transform launch: 128-byte channel slices, halved while the staged
+// rows would exceed 48 KB (wide images).
+template <typename T>
+cudaError_t wino_input(const T* x, T* V, const Tiles& tl, cudaStream_t st) {
+    constexpr int VE = 16 / sizeof(T);
+    int cslice = 128 / static_cast<int>(sizeof(T));
+    const int Wp = 2 * tl.tw + 2;
+    while (cslice > VE && size_t(4) * Wp * cslice * sizeof(T) > 48 * 1024) cslice /= 2;
+    if (tl.c % VE != 0) return cudaErrorInvalidValue;
+    const size_t smem = size_t(4) * Wp * cslice * sizeof(T);
+    if (smem > 48 * 1024) return cudaErrorInvalidValue;
+    const dim3 grid(static_cast<unsigned>(size_t(tl.n) * tl.th), static_cast<unsigned>((tl.c + cslice - 1) / cslice));
+    wino_input_smem_kernel<T><<<grid, 256, smem, st>>>(x, V, tl, cslice);
+    return cudaGetLastError();
 }
 
 // --------------------------------------------------------------- filter ---
@@ -336,7 +360,7 @@ WinoLayout layout_for(const Tiles& tl, size_t es, bool wgrad, const ConvGeom& ge
     L.m = al(16 * tl.T * tl.k * es);
     L.u = al(16 * size_t(tl.k) * tl.c * es);
     L.du = wgrad ? al(16 * size_t(tl.k) * tl.c * 4) : 0;
-    L.gemm_ws = wgrad ? al(dt == DType::BF16 ? conv_tc_workspace(gemm_g, ConvMode::Wgrad)
+    L.gemm_ws = wgrad ? al(dt == DType::BF16 ? conv_tc_wgrad_batched_workspace(gemm_g, 16)
                                              : conv_ffma_workspace(gemm_g, ConvMode::Wgrad))
                       : 0;
     L.total = L.v + L.m + L.u + L.du + L.gemm_ws;
@@ -371,24 +395,29 @@ cudaError_t wino_conv(const Tiles& tl, DType dt, const void* src, const void* w,
     void* V = base;
     void* M = base + L.v;
     void* U = base + L.v + L.m;
+    cudaError_t e = cudaSuccess;
     WINO_DT(dt, T, VW, {
-        wino_input_kernel<T, VW><<<grid_of(tl.T * tl.c / VW), kBlock, 0, st>>>(
-            static_cast<const T*>(src), static_cast<T*>(V), tl);
-        wino_filter_kernel<T><<<grid_of(size_t(tl.k) * tl.c), kBlock, 0, st>>>(
-            static_cast<const T*>(w), static_cast<T*>(U), tl.k, tl.c, flip_transpose);
+        e = wino_input<T>(static_cast<const T*>(src), static_cast<T*>(V), tl, st);
+        if (e == cudaSuccess)
+            wino_filter_kernel<T><<<grid_of(size_t(tl.k) * tl.c), kBlock, 0, st>>>(
+                static_cast<const T*>(w), static_cast<T*>(U), tl.k, tl.c, flip_transpose);
     });
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    for (int xi = 0; xi < 16; ++xi) {
-        const char* Vx = static_cast<const char*>(V) + xi * tl.T * tl.c * es;
-        const char* Ux = static_cast<const char*>(U) + xi * size_t(tl.k) * tl.c * es;
-        char* Mx = static_cast<char*>(M) + xi * tl.T * tl.k * es;
-        Epilogue none;
-        e = dt == DType::BF16 ? conv_tc_fwd(gg, Vx, Ux, none, Mx, st)
-                              : conv_ffma_fwd(gg, reinterpret_cast<const float*>(Vx),
-                                              reinterpret_cast<const float*>(Ux), none,
-                                              reinterpret_cast<float*>(Mx), st);
+    if (dt == DType::BF16) {
+        // the 16 transform-position GEMMs in one batched tcgen05 launch
+        e = conv_tc_fwd_batched(gg, 16, V, U, M, st);
         if (e != cudaSuccess) return e;
+    } else {
+        for (int xi = 0; xi < 16; ++xi) {
+            const char* Vx = static_cast<const char*>(V) + xi * tl.T * tl.c * es;
+            const char* Ux = static_cast<const char*>(U) + xi * size_t(tl.k) * tl.c * es;
+            char* Mx = static_cast<char*>(M) + xi * tl.T * tl.k * es;
+            Epilogue none;
+            e = conv_ffma_fwd(gg, reinterpret_cast<const float*>(Vx), reinterpret_cast<const float*>(Ux), none,
+                              reinterpret_cast<float*>(Mx), st);
+            if (e != cudaSuccess) return e;
+        }
     }
     WINO_DT(dt, T, VW, {
         wino_output_kernel<T, VW><<<grid_of(tl.T * tl.k / VW), kBlock, 0, st>>>(
@@ -445,22 +474,28 @@ cudaError_t winograd_wgrad(const ConvGeom& g, DType dt, const void* dy, const vo
     void* Z = base + L.v;
     float* dU = reinterpret_cast<float*>(base + L.v + L.m + L.u);
     void* gws = base + L.v + L.m + L.u + L.du;
+    cudaError_t e = cudaSuccess;
     WINO_DT(dt, T, VW, {
-        wino_input_kernel<T, VW><<<grid_of(tl.T * tl.c / VW), kBlock, 0, st>>>(
-            static_cast<const T*>(x), static_cast<T*>(V), tl);
-        wino_dy_kernel<T, VW><<<grid_of(tl.T * tl.k / VW), kBlock, 0, st>>>(
-            static_cast<const T*>(dy), static_cast<T*>(Z), tl);
+        e = wino_input<T>(static_cast<const T*>(x), static_cast<T*>(V), tl, st);
+        if (e == cudaSuccess)
+            wino_dy_kernel<T, VW><<<grid_of(tl.T * tl.k / VW), kBlock, 0, st>>>(
+                static_cast<const T*>(dy), static_cast<T*>(Z), tl);
     });
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    for (int xi = 0; xi < 16; ++xi) {
-        const char* Vx = static_cast<const char*>(V) + xi * tl.T * tl.c * es;
-        const char* Zx = static_cast<const char*>(Z) + xi * tl.T * tl.k * es;
-        float* dUx = dU + xi * size_t(tl.k) * tl.c;
-        e = dt == DType::BF16 ? conv_tc_wgrad(gg, Zx, Vx, dUx, gws, st)
-                              : conv_ffma_wgrad(gg, reinterpret_cast<const float*>(Zx),
-                                                reinterpret_cast<const float*>(Vx), dUx, gws, st);
+    if (dt == DType::BF16) {
+        // the 16 tile-reduction GEMMs in one batched launch (split-K over all of them)
+        e = conv_tc_wgrad_batched(gg, 16, Z, V, dU, gws, st);
         if (e != cudaSuccess) return e;
+    } else {
+        for (int xi = 0; xi < 16; ++xi) {
+            const char* Vx = static_cast<const char*>(V) + xi * tl.T * tl.c * es;
+            const char* Zx = static_cast<const char*>(Z) + xi * tl.T * tl.k * es;
+            float* dUx = dU + xi * size_t(tl.k) * tl.c;
+            e = conv_ffma_wgrad(gg, reinterpret_cast<const float*>(Zx), reinterpret_cast<const float*>(Vx), dUx,
+                                gws, st);
+            if (e != cudaSuccess) return e;
+        }
     }
     wino_dw_kernel<<<grid_of(size_t(tl.k) * tl.c), kBlock, 0, st>>>(dU, dw, tl.k, tl.c);
     return cudaGetLastError();

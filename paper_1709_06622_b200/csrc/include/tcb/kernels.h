@@ -59,6 +59,13 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
                           int* counters = nullptr);
 inline constexpr int conv_tc_counter_ints() { return 2 * 1024; }
 bool conv_tc_narrow(const ConvGeom& g);
+// Batched plain GEMMs on the tcgen05 kernel (one launch for all planes): g is
+// the 1x1 / stride-1 / unpadded conv of one plane; planes are contiguous.
+cudaError_t conv_tc_fwd_batched(const ConvGeom& g, int batch, const void* x, const void* w, void* y,
+                                cudaStream_t st);
+size_t conv_tc_wgrad_batched_workspace(const ConvGeom& g, int batch);
+cudaError_t conv_tc_wgrad_batched(const ConvGeom& g, int batch, const void* dy, const void* x, float* dw,
+                                  void* workspace, cudaStream_t st);
 bool conv_tc_supported(const ConvGeom& g, ConvMode mode);
 // 1: always use the cp.async gather operand path (tests / A-B comparisons);
 // 0: pick plain-TMA / im2col-TMA / gather per geometry.
