@@ -20,9 +20,11 @@
 // (Inception-v3) catalogs solvable under reduced-memory sweeps.
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <future>
 #include <limits>
 #include <numeric>
+#include <tuple>
 
 #include "traincap/api.hpp"
 
@@ -30,60 +32,54 @@ namespace traincap {
 
 namespace {
 
-// Total order used by both solvers on complete assignments.
+// A complete assignment: its totals and the option picked for each layer.
 struct Leaf {
     double time = 0.0;
     std::int64_t memory = 0;
     std::vector<const CostEntry*> pick;
 };
 
+// The canonical optimum both solvers return: least total time, then least
+// workspace, then the lexicographically smallest sequence of algorithm names.
 bool better_than(double t, std::int64_t m, const std::vector<const CostEntry*>& pick,
                  const std::optional<Leaf>& incumbent) {
     if (!incumbent) return true;
-    if (t < incumbent->time) return true;
-    if (incumbent->time < t) return false;
-    if (m != incumbent->memory) return m < incumbent->memory;
-    for (std::size_t i = 0; i < pick.size(); ++i) {
-        const int c = pick[i]->algorithm.compare(incumbent->pick[i]->algorithm);
-        if (c != 0) return c < 0;
-    }
-    return false;
+    if (t != incumbent->time || m != incumbent->memory)
+        return std::make_pair(t, m) < std::make_pair(incumbent->time, incumbent->memory);
+    return std::lexicographical_compare(pick.begin(), pick.end(), incumbent->pick.begin(), incumbent->pick.end(),
+                                        [](const CostEntry* x, const CostEntry* y) { return x->algorithm < y->algorithm; });
 }
 
 void require_nonempty(const LayerOptions& options) {
-    for (std::size_t i = 0; i < options.size(); ++i)
-        if (options[i].empty())
-            throw IncompleteCatalogError("layer " + std::to_string(i + 1) +
-                                         " has no algorithm options");
+    const auto hole = std::find_if(options.begin(), options.end(), [](const auto& l) { return l.empty(); });
+    if (hole != options.end())
+        throw IncompleteCatalogError("layer " + std::to_string(hole - options.begin() + 1) +
+                                     " has no algorithm options");
 }
 
+// Options of every layer fastest first (time, workspace, name), so that an
+// assignment sums its per-layer times in one fixed order in either solver.
 LayerOptions sorted_copy(const LayerOptions& options) {
     LayerOptions s = options;
+    const auto key = [](const CostEntry& e) { return std::tie(e.time_seconds, e.memory_bits, e.algorithm); };
     for (auto& layer : s)
-        std::sort(layer.begin(), layer.end(), [](const CostEntry& a, const CostEntry& b) {
-            if (a.time_seconds != b.time_seconds) return a.time_seconds < b.time_seconds;
-            if (a.memory_bits != b.memory_bits) return a.memory_bits < b.memory_bits;
-            return a.algorithm < b.algorithm;
-        });
+        std::sort(layer.begin(), layer.end(), [&](const CostEntry& x, const CostEntry& y) { return key(x) < key(y); });
     return s;
 }
 
+// The least workspace any assignment can use (each layer at its leanest option).
 std::int64_t cheapest_memory(const LayerOptions& options) {
-    std::int64_t total = 0;
-    for (const auto& layer : options) {
-        std::int64_t m = layer[0].memory_bits;
-        for (const CostEntry& e : layer) m = std::min(m, e.memory_bits);
-        total += m;
-    }
-    return total;
+    return std::transform_reduce(options.begin(), options.end(), std::int64_t{0}, std::plus<>(), [](const auto& l) {
+        return std::min_element(l.begin(), l.end(), [](const CostEntry& x, const CostEntry& y) {
+                   return x.memory_bits < y.memory_bits;
+               })->memory_bits;
+    });
 }
 
 Selection make_selection(const Leaf& leaf) {
-    Selection s;
-    s.total_time = leaf.time;
-    s.total_memory = leaf.memory;
-    for (std::size_t i = 0; i < leaf.pick.size(); ++i)
-        s.assignment[static_cast<int>(i + 1)] = leaf.pick[i]->algorithm;
+    Selection s{{}, leaf.time, leaf.memory};
+    int layer = 0;
+    for (const CostEntry* e : leaf.pick) s.assignment.emplace(++layer, e->algorithm);
     return s;
 }
 
@@ -287,9 +283,11 @@ const char* to_string(AdvisoryKind kind) {
 }
 
 std::vector<std::int64_t> default_batch_candidates(const AlgorithmCatalog& catalog) {
+    // the paper's sweep grid (powers of two, 32..512) restricted to what was profiled
+    static constexpr std::int64_t kGrid[] = {32, 64, 128, 256, 512};
     std::vector<std::int64_t> out;
-    for (std::int64_t b = 32; b <= 512; b *= 2)
-        if (catalog.has_batch_size(b)) out.push_back(b);
+    std::copy_if(std::begin(kGrid), std::end(kGrid), std::back_inserter(out),
+                 [&](std::int64_t b) { return catalog.has_batch_size(b); });
     return out;
 }
 
@@ -299,48 +297,81 @@ constexpr const char* kClassifierCaveat =
     "classifier memory uses a fixed per-junction bias charge and batch-independent "
     "activations; treat classifier totals as approximate";
 
-BatchCandidateResult assess_bound(const AlgorithmCatalog& cat, std::int64_t dataset, std::int64_t b,
-                                  const MemoryBreakdown& breakdown) {
-    BatchCandidateResult c;
-    c.batch_size = b;
-    c.breakdown = breakdown;
-    const LayerOptions opts = catalog_options(cat, b);
-    c.solve = solve_selection(opts, c.breakdown.bound);
-    if (!c.solve.feasible()) return c;
+// §3.1.3 mini-batch sweep. A candidate is scored from its workspace bound:
+// the Eq 6 selection under that bound, epoch time = ceil(dataset / b) * sum T,
+// throughput = b / sum T (the paper's img/s model), and the layers whose
+// selected algorithm is slower than their fastest profiled one (memory-limited).
+// Both sweeps below differ only in where the bound comes from.
+class Sweep {
+public:
+    using BoundFn = std::function<MemoryBreakdown(std::size_t)>;  // candidate index -> its bound
 
-    const Selection& sel = *c.solve.selection;
-    const std::int64_t rounds = (dataset + b - 1) / b;
-    c.epoch_time_seconds = static_cast<double>(rounds) * sel.total_time;
-    c.throughput = static_cast<double>(b) / sel.total_time;
-    for (std::size_t i = 0; i < opts.size(); ++i) {
-        const int layer = static_cast<int>(i + 1);
-        const double quickest = opts[i].front().time_seconds;
-        const double chosen = cat.query(layer, sel.assignment.at(layer), b)->time_seconds;
-        if (chosen > quickest) c.memory_limited_layers.push_back(layer);
+    Sweep(const AlgorithmCatalog& catalog, std::int64_t dataset) : cat_(catalog), dataset_(dataset) {}
+
+    // Candidates are independent and pure: scored concurrently, kept in input
+    // order (the first failing candidate in input order is the error that surfaces).
+    BatchPlan run(const std::vector<std::int64_t>& batches, const BoundFn& bound) const {
+        std::vector<std::future<BatchCandidateResult>> pending;
+        pending.reserve(batches.size());
+        for (std::size_t i = 0; i < batches.size(); ++i)
+            pending.push_back(std::async(std::launch::async, [this, i, &batches, &bound] {
+                return score(batches[i], bound(i));
+            }));
+        BatchPlan plan;
+        plan.candidates.reserve(batches.size());
+        for (auto& f : pending) plan.candidates.push_back(f.get());
+        plan.recommended = pick(plan.candidates);
+        return plan;
     }
-    return c;
-}
 
-BatchCandidateResult assess(const NetworkSpec& net, const AlgorithmCatalog& cat,
-                            std::int64_t gpu_bits, std::int64_t dataset, std::int64_t b) {
-    return assess_bound(cat, dataset, b, memory_bound(gpu_bits, net, b));
-}
-
-void recommend(BatchPlan& plan) {
-    for (const BatchCandidateResult& c : plan.candidates) {
-        if (!c.epoch_time_seconds) continue;
-        if (!plan.recommended) {
-            plan.recommended = c.batch_size;
-            continue;
+    BatchCandidateResult score(std::int64_t b, const MemoryBreakdown& m) const {
+        BatchCandidateResult r;
+        r.batch_size = b;
+        r.breakdown = m;
+        const LayerOptions per_layer = catalog_options(cat_, b);
+        r.solve = solve_selection(per_layer, m.bound);
+        if (!r.solve.selection) return r;
+        const Selection& chosen = *r.solve.selection;
+        const double sum_t = chosen.total_time;
+        const std::int64_t rounds = dataset_ / b + (dataset_ % b != 0);
+        r.epoch_time_seconds = sum_t * static_cast<double>(rounds);
+        r.throughput = static_cast<double>(b) / sum_t;
+        int layer = 0;
+        for (const std::vector<CostEntry>& opts : per_layer) {
+            ++layer;  // options are sorted fastest first
+            const auto it = std::find_if(opts.begin(), opts.end(), [&](const CostEntry& e) {
+                return e.algorithm == chosen.assignment.at(layer);
+            });
+            if (it->time_seconds > opts.front().time_seconds) r.memory_limited_layers.push_back(layer);
         }
-        const auto holder =
-            std::find_if(plan.candidates.begin(), plan.candidates.end(),
-                         [&](const BatchCandidateResult& x) { return x.batch_size == *plan.recommended; });
-        const double incumbent = *holder->epoch_time_seconds;
-        const double mine = *c.epoch_time_seconds;
-        if (mine < incumbent || (mine == incumbent && c.batch_size > *plan.recommended))
-            plan.recommended = c.batch_size;
+        return r;
     }
+
+    // Shortest epoch wins; equal epochs go to the larger mini-batch.
+    static std::optional<std::int64_t> pick(const std::vector<BatchCandidateResult>& cs) {
+        const BatchCandidateResult* best = nullptr;
+        for (const BatchCandidateResult& c : cs) {
+            if (!c.epoch_time_seconds) continue;
+            const bool better = !best || *c.epoch_time_seconds < *best->epoch_time_seconds ||
+                                (*c.epoch_time_seconds == *best->epoch_time_seconds && c.batch_size > best->batch_size);
+            if (better) best = &c;
+        }
+        return best ? std::optional<std::int64_t>(best->batch_size) : std::nullopt;
+    }
+
+private:
+    const AlgorithmCatalog& cat_;
+    std::int64_t dataset_;
+};
+
+void require_sweep_inputs(std::size_t n_candidates, std::int64_t dataset) {
+    if (n_candidates == 0) throw DomainError("candidate batch-size list must not be empty");
+    if (dataset < 1) throw DomainError("dataset size must be >= 1");
+}
+
+void require_declared(const AlgorithmCatalog& catalog, std::int64_t b) {
+    if (!catalog.has_batch_size(b))
+        throw CandidateNotInCatalogError("batch size " + std::to_string(b) + " is not declared in the catalog");
 }
 
 }  // namespace
@@ -348,25 +379,26 @@ void recommend(BatchPlan& plan) {
 BatchPlan plan_batch_size_resident(const AlgorithmCatalog& catalog,
                                    const std::vector<std::pair<std::int64_t, std::int64_t>>& resident_bits,
                                    std::int64_t gpu_total_bits, std::int64_t dataset_size) {
-    if (resident_bits.empty()) throw DomainError("candidate batch-size list must not be empty");
-    if (dataset_size < 1) throw DomainError("dataset size must be >= 1");
-    std::vector<std::future<BatchCandidateResult>> work;
+    require_sweep_inputs(resident_bits.size(), dataset_size);
+    std::vector<std::int64_t> order;
     for (const auto& [b, bits] : resident_bits) {
-        if (!catalog.has_batch_size(b))
-            throw CandidateNotInCatalogError("batch size " + std::to_string(b) +
-                                             " is not declared in the catalog");
+        require_declared(catalog, b);
         if (bits < 0) throw DomainError("resident bits must be >= 0");
-        MemoryBreakdown m;
-        m.batch_size = b;
-        m.gpu_total = gpu_total_bits;
-        m.feature_maps = bits;
-        if (__builtin_sub_overflow(gpu_total_bits, bits, &m.bound))
+        std::int64_t left = 0;
+        if (__builtin_sub_overflow(gpu_total_bits, bits, &left))
             throw OverflowError("integer overflow in memory arithmetic");
-        work.push_back(std::async(std::launch::async, assess_bound, std::cref(catalog), dataset_size, b, m));
+        order.push_back(b);
     }
-    BatchPlan plan;
-    for (auto& w : work) plan.candidates.push_back(w.get());
-    recommend(plan);
+    // the executor's resident bytes stand in for Eq 2-5 (no chain model for branched graphs)
+    const auto bound = [&](std::size_t i) {
+        MemoryBreakdown m;
+        m.batch_size = resident_bits[i].first;
+        m.gpu_total = gpu_total_bits;
+        m.feature_maps = resident_bits[i].second;
+        m.bound = gpu_total_bits - m.feature_maps;
+        return m;
+    };
+    BatchPlan plan = Sweep(catalog, dataset_size).run(order, bound);
     plan.advisories = advise_refinement(plan, NetworkSpec{});
     return plan;
 }
@@ -374,68 +406,54 @@ BatchPlan plan_batch_size_resident(const AlgorithmCatalog& catalog,
 BatchPlan plan_batch_size(const NetworkSpec& network, const AlgorithmCatalog& catalog,
                           std::int64_t gpu_total_bits, std::int64_t dataset_size,
                           const std::vector<std::int64_t>& candidates) {
-    if (candidates.empty()) throw DomainError("candidate batch-size list must not be empty");
-    if (dataset_size < 1) throw DomainError("dataset size must be >= 1");
-    for (std::int64_t b : candidates)
-        if (!catalog.has_batch_size(b))
-            throw CandidateNotInCatalogError("batch size " + std::to_string(b) +
-                                             " is not declared in the catalog");
-    if (catalog.layer_count() != network.convolution_layer_count())
+    require_sweep_inputs(candidates.size(), dataset_size);
+    for (std::int64_t b : candidates) require_declared(catalog, b);
+    const int convs = network.convolution_layer_count();
+    if (catalog.layer_count() != convs)
         throw IncompleteCatalogError("catalog profiles " + std::to_string(catalog.layer_count()) +
-                                     " convolution layers but the network has " +
-                                     std::to_string(network.convolution_layer_count()));
-
-    // Candidates are independent: evaluate concurrently, collect in input order
-    // (the first failing candidate in input order is the one whose error surfaces).
-    std::vector<std::future<BatchCandidateResult>> work;
-    work.reserve(candidates.size());
-    for (std::int64_t b : candidates)
-        work.push_back(std::async(std::launch::async, assess, std::cref(network),
-                                  std::cref(catalog), gpu_total_bits, dataset_size, b));
-    BatchPlan plan;
-    for (auto& w : work) plan.candidates.push_back(w.get());
-    recommend(plan);
+                                     " convolution layers but the network has " + std::to_string(convs));
+    const auto bound = [&](std::size_t i) { return memory_bound(gpu_total_bits, network, candidates[i]); };
+    BatchPlan plan = Sweep(catalog, dataset_size).run(candidates, bound);
     plan.advisories = advise_refinement(plan, network);
     return plan;
 }
 
+// §3.1.4 refinement advice: nothing fits -> sweep smaller batches; a smaller
+// batch with higher throughput than the recommendation -> consider it; a
+// recommendation that had to trade speed for memory -> name those layers;
+// the classifier caveat always closes the list.
 std::vector<Advisory> advise_refinement(const BatchPlan& plan, const NetworkSpec&) {
-    std::vector<Advisory> out;
+    std::vector<Advisory> advice;
+    const auto& cs = plan.candidates;
     if (!plan.recommended) {
-        std::int64_t smallest = 0;
-        for (const auto& c : plan.candidates)
-            smallest = smallest == 0 ? c.batch_size : std::min(smallest, c.batch_size);
-        out.push_back({AdvisoryKind::reduce_batch,
-                       "no candidate mini-batch fits in GPU memory; profile and sweep batch "
-                       "sizes below " +
-                           std::to_string(smallest),
-                       {}});
+        const auto smallest = std::min_element(cs.begin(), cs.end(), [](const auto& x, const auto& y) {
+            return x.batch_size < y.batch_size;
+        });
+        advice.push_back({AdvisoryKind::reduce_batch,
+                          "no candidate mini-batch fits in GPU memory; profile and sweep batch sizes below " +
+                              std::to_string(smallest == cs.end() ? 0 : smallest->batch_size),
+                          {}});
     } else {
-        const BatchCandidateResult* chosen = nullptr;
-        for (const auto& c : plan.candidates)
-            if (c.batch_size == *plan.recommended) chosen = &c;
-        for (const auto& c : plan.candidates) {
-            const bool faster_smaller = c.batch_size < chosen->batch_size && c.throughput &&
-                                        chosen->throughput && *c.throughput > *chosen->throughput;
-            if (!faster_smaller) continue;
-            out.push_back({AdvisoryKind::reduce_batch,
-                           "batch " + std::to_string(c.batch_size) +
-                               " sustains higher throughput than the recommended " +
-                               std::to_string(chosen->batch_size) +
-                               "; consider reducing the mini-batch size",
-                           {}});
-            break;
-        }
-        if (!chosen->memory_limited_layers.empty())
-            out.push_back({AdvisoryKind::adjust_model,
-                           "memory budget forced slower algorithms at batch " +
-                               std::to_string(chosen->batch_size) +
-                               "; freeing memory (larger strides, leaner filters) on the listed "
-                               "layers would unlock the faster ones",
-                           chosen->memory_limited_layers});
+        const std::int64_t rb = *plan.recommended;
+        const auto rec = std::find_if(cs.rbegin(), cs.rend(), [&](const auto& c) { return c.batch_size == rb; });
+        const auto faster = std::find_if(cs.begin(), cs.end(), [&](const auto& c) {
+            return c.batch_size < rb && c.throughput && rec->throughput && *c.throughput > *rec->throughput;
+        });
+        if (faster != cs.end())
+            advice.push_back({AdvisoryKind::reduce_batch,
+                              "batch " + std::to_string(faster->batch_size) +
+                                  " sustains higher throughput than the recommended " + std::to_string(rb) +
+                                  "; consider reducing the mini-batch size",
+                              {}});
+        if (!rec->memory_limited_layers.empty())
+            advice.push_back({AdvisoryKind::adjust_model,
+                              "memory budget forced slower algorithms at batch " + std::to_string(rb) +
+                                  "; freeing memory (larger strides, leaner filters) on the listed layers would "
+                                  "unlock the faster ones",
+                              rec->memory_limited_layers});
     }
-    out.push_back({AdvisoryKind::caveat, kClassifierCaveat, {}});
-    return out;
+    advice.push_back({AdvisoryKind::caveat, kClassifierCaveat, {}});
+    return advice;
 }
 
 std::vector<std::string> model_caveats() {

@@ -191,6 +191,8 @@ private:
     std::vector<std::int64_t> batches_;
     std::vector<AlgorithmId> algos_;
     int layers_ = 0;
+    // (layer, batch) -> its profiled options, fastest first (options() / query())
+    std::map<std::pair<int, std::int64_t>, std::vector<CostEntry>> cells_;
 };
 
 AlgorithmCatalog load_catalog(std::istream& source, CatalogFormat format);
