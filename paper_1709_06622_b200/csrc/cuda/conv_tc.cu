@@ -1369,7 +1369,8 @@ size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
     const ConvShape s = make_shape(g, mode);
     const int bn = wgrad_bn(s);
     const SplitPlan sp = plan_splits(s, bn, wgrad_pair(s, bn));
-    return sp.splits > 1 ? size_t(sp.splits) * s.M * s.Ncol * sizeof(float) : 0;
+    const size_t im2col_ws = sp.splits > 1 ? size_t(sp.splits) * s.M * s.Ncol * sizeof(float) : 0;
+    return std::max(im2col_ws, conv_win_wgrad_workspace(g));
 }
 
 bool conv_tc_narrow(const ConvGeom& g) { return narrow_plan(g).use; }
@@ -1379,6 +1380,7 @@ int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool cou
     if (mode == ConvMode::Fwd) return q.use ? 3 : 1;
     if (mode == ConvMode::Dgrad) return g.stride_h * g.stride_w;
     const ConvGeom& gw = q.use ? q.g1 : g;
+    if (!q.use && !force_gather() && conv_win_wgrad_applies(g)) return 2;  // window kernel + split reduction
     const ConvShape s = make_shape(gw, mode);
     const int bn = wgrad_bn(s);
     const bool pair = wgrad_pair(s, bn);
@@ -1522,6 +1524,7 @@ cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, floa
         return launch_pdl(narrow_scatter_grad, dim3(std::max(1, std::min(total / 256 + 1, 1024))), dim3(256), 0,
                           st, static_cast<const float*>(dwp), dw, g, q.cv, q.rw, q.kc);
     }
+    if (!force_gather() && conv_win_wgrad_applies(g)) return conv_win_wgrad(g, dy, x, dw, workspace, st);
     Params p{};
     p.s = make_shape(g, ConvMode::Wgrad);
     const int bn0 = wgrad_bn(p.s);

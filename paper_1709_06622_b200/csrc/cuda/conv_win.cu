@@ -581,7 +581,263 @@ cudaError_t run_win(const ConvGeom& g, const WinPlan& q, bool dgrad, const void*
     return dgrad ? dispatch_win<true>(p, q, st) : dispatch_win<false>(p, q, st);
 }
 
+// ============================================================ wgrad ======
+//
+// Window weight gradient for stride-1 R x S convs: the reduction runs over
+// the positions of the padded output plane (flat f = ho * Wp + wq, junk
+// columns wq >= Wo carry dy = 0 because the dy window reads them out of
+// bounds). A k-block is P = 256 consecutive positions; per k-block one TMA
+// window of x rows per 64-channel slice and one window of dy rows per
+// 64-channel slice of K. The GEMM runs swapped: M = (tap, channel) of the
+// filter gradient, N = K, both operands MN-major straight out of the windows.
+// One M = 128 tile is TWO tap-slices: M block 0 at the first tap's row offset
+// and M block 1 at the second's, i.e. the UMMA descriptor's leading byte
+// offset is the distance between the two taps' shifted windows (measured:
+// scripts/probes/umma_mn_probe.cu). Every CTA accumulates all M tiles of its
+// contiguous range of k-blocks in TMEM (M tiles x K columns <= 512) and writes
+// one fp32 partial [K][R][S][C]; a fixed-order split reduction sums them.
+constexpr int kWP = 256;  // positions per k-block (16 MMA K-steps)
+constexpr int kWgMaxStages = 2;
+
+struct WgParams {
+    CUtensorMap tmap_x;   // x [N][H][W][C], box {64, Wp, WRx, 1}
+    CUtensorMap tmap_dy;  // dy [N][Ho][Wo][K], box {64, Wp, WRd, 1}
+    int n_img, Ho, Wo, pad_h, pad_w, R, S, C, K;
+    int Wp, kb_img, kb_total, kb_per_cta;
+    int slices, kslices, nq, mtiles;
+    uint32_t xwin_bytes, dywin_bytes, stage_bytes;  // smem strides (1 KB aligned)
+    uint32_t tx_bytes;                              // bytes the TMA boxes of one stage deliver
+    int stages;
+    float* partial;  // [gridDim.x][K][R][S][C]
+    FastDiv d_wp, d_kbimg;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) conv_win_wgrad_kernel(const __grid_constant__ WgParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[kWgMaxStages], empty[kWgMaxStages], done;
+    __shared__ uint32_t tmem_slot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int taps = p.R * p.S;
+    const int kb0 = blockIdx.x * p.kb_per_cta;
+    const int kb1 = min(p.kb_total, kb0 + p.kb_per_cta);
+    if (tid == 0) {
+        for (int i = 0; i < p.stages; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        ptx::mbar_init(&done, 1);
+        ptx::fence_mbarrier_init();
+        ptx::tma_prefetch_desc(&p.tmap_x);
+        ptx::tma_prefetch_desc(&p.tmap_dy);
+    }
+    if (warp == kMmaWarp) ptx::tmem_alloc<512>(&tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
+    const uint32_t sbase = ptx::smem_addr(smem);
+
+    if (warp == 0) {
+        if (tid == 0) {  // ------------------------------------------ producer
+            int st = 0;
+            uint32_t ph = 0;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                uint32_t img, j;
+                p.d_kbimg.divmod(static_cast<uint32_t>(kb), img, j);
+                uint32_t row0, off0;
+                p.d_wp.divmod(j * kWP, row0, off0);
+                ptx::mbar_wait(&empty[st], ph ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[st], p.tx_bytes);
+                const uint32_t base = sbase + st * p.stage_bytes;
+                for (int cs = 0; cs < p.slices; ++cs)
+                    ptx::tma_load_4d(base + cs * p.xwin_bytes, &p.tmap_x, &full[st], cs * 64, -p.pad_w,
+                                     static_cast<int>(row0) - p.pad_h, static_cast<int>(img));
+                for (int ks = 0; ks < p.kslices; ++ks)
+                    ptx::tma_load_4d(base + p.slices * p.xwin_bytes + ks * p.dywin_bytes, &p.tmap_dy, &full[st],
+                                     ks * 64, 0, static_cast<int>(row0), static_cast<int>(img));
+                if (++st == p.stages) {
+                    st = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {  // ------------------------------- MMA issuer
+        constexpr uint32_t idesc = ptx::make_idesc(1, 128, BN, 1u, 1u);
+        int st = 0;
+        uint32_t ph = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+            uint32_t img, j;
+            p.d_kbimg.divmod(static_cast<uint32_t>(kb), img, j);
+            uint32_t row0, off0;
+            p.d_wp.divmod(j * kWP, row0, off0);
+            ptx::mbar_wait(&full[st], ph);
+            ptx::tc_fence_after();
+            const uint32_t base = sbase + st * p.stage_bytes;
+            const uint32_t dyb = base + p.slices * p.xwin_bytes + off0 * 128;
+            const uint64_t bd0 = ptx::sw128_desc(dyb, p.dywin_bytes, 1024);
+            // tap-slice q (slice-major): address of its shifted window
+            auto qaddr = [&](int q) {
+                const int cs = q / taps, t = q - cs * taps;
+                const int ti = t / p.S, tj = t - ti * p.S;
+                return base + cs * p.xwin_bytes + (off0 + ti * p.Wp + tj) * 128;
+            };
+            for (int mt = 0; mt < p.mtiles; ++mt) {
+                const int q0 = 2 * mt, q1 = min(2 * mt + 1, p.nq - 1);
+                const uint32_t a0 = qaddr(q0);
+                const uint64_t ad0 = ptx::sw128_desc(a0, qaddr(q1) - a0, 1024);
+#pragma unroll 4
+                for (int ks = 0; ks < kWP / 16; ++ks)
+                    ptx::umma_f16_elect(tmem + mt * BN, ad0 + ks * 128, bd0 + ks * 128, idesc,
+                                        (kb > kb0 || ks > 0) ? 1u : 0u);
+            }
+            ptx::umma_commit_elect(&empty[st]);
+            if (++st == p.stages) {
+                st = 0;
+                ph ^= 1;
+            }
+        }
+        ptx::umma_commit_elect(&done);
+    } else if (warp >= 4) {  // ------------------------------------- epilogue
+        const int quarter = warp & 3, half = (warp - 4) >> 2;
+        const int lane = tid & 31;
+        const int m = quarter * 32 + lane;  // row within an M tile
+        float* part = p.partial + size_t(blockIdx.x) * p.K * taps * p.C;
+        const bool any = kb1 > kb0;
+        if (any) {
+            ptx::mbar_wait(&done, 0);
+            ptx::tc_fence_after();
+        }
+        for (int mt = 0; mt < p.mtiles; ++mt) {
+            const int blk = m >> 6, q = 2 * mt + blk;
+            const bool live = q < p.nq && !(blk == 1 && 2 * mt + 1 >= p.nq);
+            const int cs = q / taps, t = q - cs * taps, c = cs * 64 + (m & 63);
+#pragma unroll 1
+            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+                uint32_t v[32];
+                if (any) {
+                    ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + mt * BN + c0, v);
+                    ptx::tmem_ld_wait();
+                }
+                if (!live) continue;
+                for (int i = 0; i < 32 && c0 + i < p.K; ++i)
+                    part[(size_t(c0 + i) * taps + t) * p.C + c] = any ? __uint_as_float(v[i]) : 0.f;
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+struct WgPlan {
+    bool use = false;
+    int Wp, WRx, WRd, slices, kslices, nq, mtiles, bn, kb_img, kb_total, grid, kb_per_cta, stages;
+    uint32_t xwin, dywin, stage, tx;
+    size_t smem, partial_bytes;
+};
+
+WgPlan wgrad_plan(const ConvGeom& g) {
+    WgPlan q;
+    if (!win_enabled() || g.stride_h != 1 || g.stride_w != 1 || g.r * g.s < 2) return q;
+    if (g.c % 64 != 0 || g.k % 64 != 0 || g.pad_h > 15 || g.pad_w > 15) return q;
+    const int Ho = g.ho(), Wo = g.wo();
+    q.Wp = Wo + g.s - 1;
+    if (q.Wp > 64 || q.Wp < 16) return q;
+    q.slices = g.c / 64;
+    q.kslices = g.k / 64;
+    q.bn = g.k;
+    if (q.bn != 64 && g_win_mode != 2) return q;  // default: where the im2col path has 64-row tiles
+    q.nq = g.r * g.s * q.slices;
+    q.mtiles = (q.nq + 1) / 2;
+    if (q.bn > 256 || q.mtiles * q.bn > 512) return q;
+    q.WRx = (q.Wp - 1 + kWP - 1 + (g.r - 1) * q.Wp + g.s - 1) / q.Wp + 1;
+    q.WRd = (q.Wp - 1 + kWP - 1) / q.Wp + 1;
+    if (q.WRx > 256) return q;
+    q.xwin = (static_cast<uint32_t>(q.WRx) * q.Wp * 128 + 1023) / 1024 * 1024;
+    q.dywin = (static_cast<uint32_t>(q.WRd) * q.Wp * 128 + 1023) / 1024 * 1024;
+    q.stage = q.slices * q.xwin + q.kslices * q.dywin;
+    q.tx = static_cast<uint32_t>(q.slices * q.WRx + q.kslices * q.WRd) * q.Wp * 128;
+    q.stages = kSmemCap >= 2 * size_t(q.stage) + 1024 ? 2 : 1;
+    if (size_t(q.stage) + 1024 > kSmemCap) return q;
+    q.smem = size_t(q.stages) * q.stage + 1024;
+    q.kb_img = (Ho * q.Wp + kWP - 1) / kWP;
+    q.kb_total = g.n * q.kb_img;
+    q.grid = std::min(q.kb_total, num_sms());
+    q.kb_per_cta = (q.kb_total + q.grid - 1) / q.grid;
+    q.grid = (q.kb_total + q.kb_per_cta - 1) / q.kb_per_cta;
+    q.partial_bytes = size_t(q.grid) * g.k * g.r * g.s * g.c * sizeof(float);
+    q.use = true;
+    return q;
+}
+
+template <int BN>
+cudaError_t launch_wgrad(const WgParams& p, const WgPlan& q, cudaStream_t st) {
+    auto kern = conv_win_wgrad_kernel<BN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(q.smem));
+    if (e != cudaSuccess) return e;
+    return launch_pdl(kern, dim3(q.grid), dim3(kThreads), q.smem, st, p);
+}
+
 }  // namespace
+
+bool conv_win_wgrad_applies(const ConvGeom& g) { return wgrad_plan(g).use; }
+
+size_t conv_win_wgrad_workspace(const ConvGeom& g) {
+    const WgPlan q = wgrad_plan(g);
+    return q.use ? q.partial_bytes : 0;
+}
+
+cudaError_t conv_win_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw, void* workspace,
+                           cudaStream_t st) {
+    const WgPlan q = wgrad_plan(g);
+    if (!q.use || workspace == nullptr) return cudaErrorInvalidValue;
+    WgParams p{};
+    if (!make_tmap_window_bf16(&p.tmap_x, x, g.n, g.h, g.w, g.c, q.Wp, q.WRx)) return cudaErrorInvalidValue;
+    if (!make_tmap_window_bf16(&p.tmap_dy, dy, g.n, g.ho(), g.wo(), g.k, q.Wp, q.WRd)) return cudaErrorInvalidValue;
+    p.n_img = g.n;
+    p.Ho = g.ho();
+    p.Wo = g.wo();
+    p.pad_h = g.pad_h;
+    p.pad_w = g.pad_w;
+    p.R = g.r;
+    p.S = g.s;
+    p.C = g.c;
+    p.K = g.k;
+    p.Wp = q.Wp;
+    p.kb_img = q.kb_img;
+    p.kb_total = q.kb_total;
+    p.kb_per_cta = q.kb_per_cta;
+    p.slices = q.slices;
+    p.kslices = q.kslices;
+    p.nq = q.nq;
+    p.mtiles = q.mtiles;
+    p.xwin_bytes = q.xwin;
+    p.dywin_bytes = q.dywin;
+    p.stage_bytes = q.stage;
+    p.tx_bytes = q.tx;
+    p.stages = q.stages;
+    p.partial = static_cast<float*>(workspace);
+    p.d_wp = FastDiv(static_cast<uint32_t>(q.Wp));
+    p.d_kbimg = FastDiv(static_cast<uint32_t>(q.kb_img));
+    conv_tc_note_launch(ConvTcLaunchInfo{2, 4, q.bn, 0, 0, q.grid, q.kb_total, q.grid, 0, 0});
+    cudaError_t e;
+    switch (q.bn) {
+        case 64: e = launch_wgrad<64>(p, q, st); break;
+        case 128: e = launch_wgrad<128>(p, q, st); break;
+        case 192: e = launch_wgrad<192>(p, q, st); break;
+        case 256: e = launch_wgrad<256>(p, q, st); break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    return split_reduce(static_cast<const float*>(workspace), q.grid, size_t(g.k) * g.r * g.s * g.c, dw, st);
+}
 
 void conv_win_set_mode(int on) { g_win_mode = on < 0 ? -1 : on; }
 void conv_win_set_debug(void* buf) { g_win_dbg = static_cast<unsigned long long*>(buf); }

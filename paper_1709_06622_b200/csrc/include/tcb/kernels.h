@@ -90,6 +90,12 @@ cudaError_t conv_win_fwd(const ConvGeom& g, const void* x, const void* w, const 
 cudaError_t conv_win_dgrad(const ConvGeom& g, const void* dy, const void* w, const Epilogue& ep, void* dx,
                            cudaStream_t st);
 void conv_win_set_mode(int on);  // 0 off, 1 on (N = 64 tiles), 2 all applicable, -1 from $TCB_WIN
+// Window weight gradient (stride-1 R x S, C and K multiples of 64, M tiles x K
+// <= 512 TMEM columns): per-CTA fp32 partials in `workspace`, then a split reduction.
+bool conv_win_wgrad_applies(const ConvGeom& g);
+size_t conv_win_wgrad_workspace(const ConvGeom& g);
+cudaError_t conv_win_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw, void* workspace,
+                           cudaStream_t st);
 void conv_win_set_debug(void* buf);  // diagnostics: per-CTA role timing (8 x u64 per CTA) or nullptr
 // TMA epilogue for layers with at most `kb` 64-deep k-blocks (0 = never,
 // -1 = default: $TCB_CONV_EPI_KB or 8).

@@ -163,7 +163,9 @@ def test_conv_gemm_parity(oracle, prec, spec, operand_path):
 
 
 WINDOW_CASES = [  # (name, n, h, w, c, k, (r, s), (ph, pw), expected fwd / dgrad configuration)
-    ("rn50_s1_3x3", 3, 56, 56, 64, 64, (3, 3), (1, 1), dict(fwd=(64, 0, 1), dgrad=(64, 0, 1))),
+    ("rn50_s1_3x3", 3, 56, 56, 64, 64, (3, 3), (1, 1), dict(fwd=(64, 0, 1), dgrad=(64, 0, 1), wgrad=64)),
+    ("rn50_s1_3x3_n9", 9, 56, 56, 64, 64, (3, 3), (1, 1), dict(fwd=(64, 0, 1), dgrad=(64, 0, 1), wgrad=64)),
+    ("incep_3x3_64_128", 2, 35, 35, 64, 128, (3, 3), (1, 1), dict(fwd=(128, 1, 1), dgrad=(64, 0, 0))),
     ("rn50_s2_3x3", 2, 28, 28, 128, 128, (3, 3), (1, 1), dict(fwd=(128, 1, 0), dgrad=(128, 1, 0))),
     ("rn50_s3_3x3_k256", 2, 14, 14, 256, 256, (3, 3), (1, 1), dict(fwd=(256, 1, 0), dgrad=(256, 1, 0))),
     ("incep_5x5_48_64", 3, 35, 35, 64, 64, (5, 5), (2, 2), dict(fwd=(64, 0, 0), dgrad=(64, 0, 0))),
@@ -214,6 +216,13 @@ def test_window_conv_path(oracle, spec, all_window):
     y2 = plan.fwd(_to_dev(x, bf), _to_dev(wt, bf), bias=_to_dev(bias, torch.float32), residual=_to_dev(res, bf),
                   relu=True)
     assert torch.equal(y, y2)
+    if "wgrad" in want:
+        dw = plan.wgrad(_to_dev(dy, bf), _to_dev(x, bf))
+        info = dev.last_launch()
+        assert info["mode"] == 2 and info["load"] == 4 and info["bn"] == want["wgrad"], info
+        refw = oracle.conv_wgrad(gd, dy, x)
+        assert rel_err(_host(dw), refw) <= 1e-3, rel_err(_host(dw), refw)
+        assert torch.equal(dw, plan.wgrad(_to_dev(dy, bf), _to_dev(x, bf)))
 
 
 def test_wgrad_many_splits_and_cta_pairs(oracle):
