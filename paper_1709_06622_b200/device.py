@@ -149,9 +149,9 @@ class ConvPlan:
                                    _p(self.workspace), _stream()))
         return dx
 
-    def wgrad(self, dy, x, want_db=False):
+    def wgrad(self, dy, x, want_db=False, out=None):
         g = self.g
-        dw = torch.empty(g.k, g.r, g.s, g.c, dtype=torch.float32, device="cuda")
+        dw = out if out is not None else torch.empty(g.k, g.r, g.s, g.c, dtype=torch.float32, device="cuda")
         db = torch.empty(g.k, dtype=torch.float32, device="cuda") if want_db else None
         check(lib().tcb_conv_wgrad(self.handle, _p(dy), _p(x), _p(dw), _p(db),
                                    _p(self.workspace), _stream()))
