@@ -209,8 +209,20 @@ template <int N>
 int test(int iters) {
     std::vector<uint16_t> A(kRows * 64), B(N * 64);
     srand(1234 + N);
-    for (auto& v : A) v = static_cast<uint16_t>(0x3c00 + (rand() % 256) - 128) & 0xffff;  // ~ +-[0.5,2)
-    for (auto& v : B) v = static_cast<uint16_t>(0x3c00 + (rand() % 256) - 128) & 0xffff;
+    // PROBE_DATA: 0 = narrow-exponent values (default), 1 = normal-like values with
+    // full random mantissas and signs, 2 = zeros
+    const int mode = getenv("PROBE_DATA") ? atoi(getenv("PROBE_DATA")) : 0;
+    auto gen = [&]() -> uint16_t {
+        if (mode == 2) return 0;
+        if (mode == 1) {
+            const uint16_t sign = (rand() & 1) << 15;
+            const uint16_t expo = static_cast<uint16_t>(120 + rand() % 8) << 7;  // 2^-7 .. 2^0
+            return sign | expo | static_cast<uint16_t>(rand() & 0x7f);
+        }
+        return static_cast<uint16_t>(0x3c00 + (rand() % 256) - 128) & 0xffff;
+    };
+    for (auto& v : A) v = gen();
+    for (auto& v : B) v = gen();
     for (size_t i = 0; i < A.size(); i += 3) A[i] ^= 0x8000;
     uint16_t *dA, *dB;
     float* dO;
