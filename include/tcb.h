@@ -82,12 +82,19 @@ int tcb_conv_out_hw(const tcb_conv_geom* g, int* ho, int* wo);
  * counters); it can then be reused across calls without clearing. */
 int tcb_conv_plan_create(const tcb_conv_geom* g, int algo, int prec, tcb_conv_plan** plan,
                          size_t* workspace_bytes);
+/* Only the first c_valid of C input channels can be non-zero (bf16 channel
+ * padding of a narrow first layer): enables the explicit-im2col and row-window
+ * stem paths; *workspace_bytes is updated (it can grow). */
+int tcb_conv_plan_set_valid_channels(tcb_conv_plan* plan, int c_valid, size_t* workspace_bytes);
 int tcb_conv_plan_destroy(tcb_conv_plan* plan);
 /* Operand-load path of the tensor-core GEMM conv: 0 = automatic (2-D TMA for
  * 1x1/stride-1 layers, im2col-mode TMA when channels % 64 == 0, cp.async
  * gather otherwise; TMA-store epilogue on K-light layers), 1 = force the
  * cp.async gather path, 2 = automatic loads with the register epilogue
  * everywhere (A/B testing). */
+/* Row-window stem kernels for narrow even-stride first layers: 1 on (default), 0 the
+ * explicit-im2col path, -1 from $TCB_STEM. */
+int tcb_set_conv_stem(int on);
 int tcb_set_conv_operand_path(int mode); /* 0 auto, 1 gather, 2 register epilogue, 3 auto w/o window,
                                            4 window wherever it applies */
 /* Test hook: the configuration of the last bf16 tensor-core conv kernel launch

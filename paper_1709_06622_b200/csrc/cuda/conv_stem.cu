@@ -1,0 +1,708 @@
+// Row-window convolution for the narrow RGB stem (sm_100a): ResNet's 7x7/2
+// conv1, Inception's 3x3/2, any even-stride first layer over <= 4 real channels.
+//
+// The explicit-im2col path (conv_tc.cu, narrow_plan) writes a 1.2 GB patch
+// matrix for the ResNet-50 bs256 stem and reads it back twice (fwd GEMM and
+// wgrad GEMM): 335 + 249 + 291 us of the 12 ms step, all HBM time. Here the
+// patch matrix is never materialised. The input is stored once as a "stem
+// row" tensor x4[n][h][u][4] (4 bf16 channels = 8 bytes per pixel, the
+// conv's left padding as zero columns u < pad_w, zero columns up to Wst on the
+// right). One output pixel (ho, wo) reads, per filter row r, the 8 stored
+// pixels u = wo*sw .. wo*sw + 7 of input row ho*sh - pad_h + r: 32 contiguous
+// bf16 = one 64-byte K-chunk holding filter columns s = 0..7 (s >= S weighted
+// by zero). Consecutive wo start stride_w pixels = 8*stride_w bytes apart, so
+// a TILED TMA map with dims {32 elements, windows, H, N} and strides
+// {8*sw, 8*Wst, 8*Wst*H} bytes (overlapping rows) delivers the GEMM A tile of
+// a whole output row in one box per filter row: {32, BW, 1, 1}, 64-byte
+// swizzle, rows out of the image (vertical padding) zero-filled. Wider
+// filters (S > 8) take nq = ceil(S/8) chunks per filter row, chunk q starting
+// 8q/sw windows further (requires sw | 8).
+//
+//   fwd   : D[wo][k] = sum_(r,q) A_(r,q)[wo][32] * Wp_(r,q)[k][32]^T, M = 128
+//           rows (BW <= 128 valid), N = K, K-major SW64 both sides, the
+//           packed weights resident in shared memory; epilogue bias / ReLU ->
+//           bf16 y[n][ho][wo][K]. Warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+//           from double-buffered TMEM.
+//   wgrad : D[(r,q,e)][k] = sum over positions of x4-window^T * dy: the same
+//           x boxes as MN-major A operands (M = 4 chunks x 32 elements per
+//           M = 128 tile, chunks one box apart = the descriptor's leading byte
+//           offset), dy boxes {K, BW} as MN-major B, K-steps of 16 positions.
+//           Every CTA accumulates its contiguous range of output rows in TMEM
+//           and writes one fp32 partial; a fixed-order reduction sums the
+//           partials and scatters into dw[K][R][S][C] (zero on padded c, s).
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "ptx.cuh"
+#include "tma.cuh"
+
+namespace tcb {
+namespace {
+
+constexpr int kThreads = 10 * 32;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+constexpr int kMaxStages = 12;
+constexpr uint32_t kRowStride = 2176;  // fwd row buffer: 17 groups of 16 pixels, or 128 positions + 2 chunks
+constexpr size_t kSmemCap = 227 * 1024 - 2048;
+
+// K-major / MN-major 64-byte swizzle descriptor (layout type 4).
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(4) << 61;  // SWIZZLE_64B
+    return d;
+}
+
+struct StemParams {
+    CUtensorMap tmap_x;   // fwd: x4 rows {64, Wst/16, H, N}, box {64, G, 1, 1} (no swizzle);
+                          // wgrad: x4 windows {32, D1, H, N}, box {32, BW, 1, 1} (64-byte swizzle)
+    CUtensorMap tmap_b;   // fwd: packed weights [K][T*32], box {32, K}; wgrad: dy {K, Wo, N*Ho}, box {min(K,64), BW, 1}
+    CUtensorMap tmap_y;   // fwd: y {K, Wo, N*Ho}, box {min(K,64), BW, 1} (TMA store)
+    int Ho, Wo, K, T, nq, chunk_step, sh, pad_h, BW, wtiles, tiles;
+    uint32_t box_bytes, stage_bytes, b_bytes;
+    int stages;
+    // fwd
+    int R, G, g_step;     // filter rows; 16-pixel groups per row box; groups per width tile
+    uint32_t row_stride, stg_bytes;
+    const float* bias;
+    int relu;
+    int dbg;              // diagnostics ($TCB_STEM_DBG): 1 no MMA, 2 no output stores, 4 no x loads
+    // wgrad
+    int mtiles, tiles_per_cta, dy_boxes;
+    uint32_t dy_box_bytes;
+    float* partial;  // [grid][T*32][K]
+    FastDiv d_wtiles, d_ho;
+};
+
+struct Tile {
+    int n, ho, wo0;
+};
+
+__device__ __forceinline__ Tile tile_of(const StemParams& p, int u) {
+    uint32_t row, wt, n, ho;
+    p.d_wtiles.divmod(static_cast<uint32_t>(u), row, wt);
+    p.d_ho.divmod(row, n, ho);
+    return Tile{static_cast<int>(n), static_cast<int>(ho), static_cast<int>(wt) * p.BW};
+}
+
+__device__ __forceinline__ void load_x(const StemParams& p, uint32_t dst, uint64_t* bar, const Tile& t) {
+    const int h0 = t.ho * p.sh - p.pad_h;
+    for (int c = 0; c < p.T; ++c) {
+        const int r = c / p.nq, q = c - r * p.nq;
+        ptx::tma_load_4d(dst + c * p.box_bytes, &p.tmap_x, bar, 0, t.wo0 + q * p.chunk_step, h0 + r, t.n);
+    }
+}
+
+__device__ __forceinline__ uint4 pack8f(const float (&f)[8]) {
+    uint4 v;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return v;
+}
+
+// No-swizzle ("interleaved") K-major descriptor over a raw stem row: position m
+// of the tile starts 16 bytes after position m - 1 (stride 2 x 4 channels x
+// 2 bytes), so the 8-row x 16-byte core matrices along M are contiguous (SBO =
+// 128) and the second 8-element K group of a row is the next row's first
+// (LBO = 16): the overlapping windows are a descriptor, not a copy.
+__device__ __forceinline__ uint64_t rows_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;  // LBO 16 B
+    d |= static_cast<uint64_t>(8) << 32;  // SBO 128 B
+    d |= static_cast<uint64_t>(1) << 46;
+    return d;
+}
+
+// 16-byte chunk j of staging row m under the TMA store's swizzle
+__device__ __forceinline__ uint32_t stg_off(int m, int j, int row_bytes) {
+    return row_bytes == 128 ? m * 128 + ((j ^ (m & 7)) << 4) : m * 64 + ((j ^ ((m >> 1) & 3)) << 4);
+}
+
+template <int BN, int R, int NQ>
+__global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid_constant__ StemParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int kAcc = BN <= 64 ? 4 : 2;  // TMEM accumulators in flight
+    __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[kAcc], tempty[kAcc], bbar;
+    __shared__ uint32_t tmem_slot;
+    constexpr uint32_t kCols = kAcc * BN <= 64 ? 64 : kAcc * BN <= 128 ? 128 : 256;
+    constexpr int kBox = BN >= 64 ? 64 : BN;          // output channels per store box
+    constexpr int kRowB = kBox * 2;                   // staging row bytes (128 or 64)
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) {
+        for (int i = 0; i < p.stages; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < kAcc; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 8 * 32);
+        }
+        ptx::mbar_init(&bbar, 1);
+        ptx::fence_mbarrier_init();
+        ptx::tma_prefetch_desc(&p.tmap_x);
+        ptx::tma_prefetch_desc(&p.tmap_b);
+        ptx::tma_prefetch_desc(&p.tmap_y);
+    }
+    if (warp == 1) ptx::tmem_alloc<kCols>(&tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
+    const uint32_t sbase = ptx::smem_addr(smem);
+    const uint32_t bbase = sbase + p.stages * p.stage_bytes;
+    const uint32_t stg = bbase + p.T * p.b_bytes;  // 2 staging tiles of the output
+
+    if (warp == 0) {
+        if (tid == 0) {  // ---------------------------------------- producer
+            ptx::mbar_arrive_expect_tx(&bbar, p.T * p.b_bytes);
+            for (int c = 0; c < p.T; ++c) ptx::tma_load_2d(bbase + c * p.b_bytes, &p.tmap_b, &bbar, c * 32, 0);
+            int st = 0;
+            uint32_t ph = 0;
+            for (int u = blockIdx.x; u < p.tiles; u += gridDim.x) {
+                const Tile t = tile_of(p, u);
+                ptx::mbar_wait(&empty[st], ph ^ 1);
+                const uint32_t dst = sbase + st * p.stage_bytes;
+                const int h0 = t.ho * p.sh - p.pad_h, g0 = (t.wo0 / p.BW) * p.g_step;
+                if (p.dbg & 4) {
+                    ptx::mbar_arrive(&full[st]);
+                } else {
+                    ptx::mbar_arrive_expect_tx(&full[st], R * p.G * 128);
+                    for (int r = 0; r < R; ++r)
+                        ptx::tma_load_4d(dst + r * kRowStride, &p.tmap_x, &full[st], 0, g0, h0 + r, t.n);
+                }
+                if (++st == p.stages) {
+                    st = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {  // ------------------------------------ MMA issuer
+        constexpr uint32_t idesc = ptx::make_idesc(1, 128, BN, 0u, 0u);
+        ptx::mbar_wait(&bbar, 0);
+        ptx::tc_fence_after();
+        int st = 0, it = 0;
+        uint32_t ph = 0;
+        for (int u = blockIdx.x; u < p.tiles; u += gridDim.x, ++it) {
+            const int acc = it % kAcc;
+            ptx::mbar_wait(&tempty[acc], ((it / kAcc) & 1) ^ 1);
+            ptx::mbar_wait(&full[st], ph);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem + acc * BN;
+            // compile-time descriptor offsets: filter row r at r * kRowStride, chunk q 64 bytes on,
+            // K step 32 bytes; packed weight chunk (r, q) BN * 64 bytes apart
+            const uint64_t a0 = rows_desc(sbase + st * p.stage_bytes);
+            const uint64_t b0 = sw64_desc(bbase, 16, 512);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const uint64_t ad = a0 + ((r * kRowStride + q * 64) >> 4);
+                    const uint64_t bd = b0 + (((r * NQ + q) * BN * 64) >> 4);
+                    ptx::umma_f16_elect(d, ad, bd, idesc, (r | q) ? 1u : 0u);
+                    ptx::umma_f16_elect(d, ad + 2, bd + 2, idesc, 1u);
+                }
+            }
+            ptx::umma_commit_elect(&empty[st]);
+            ptx::umma_commit_elect(&tfull[acc]);
+            if (++st == p.stages) {
+                st = 0;
+                ph ^= 1;
+            }
+        }
+        __syncwarp();
+    } else {  // ------------------------------------------------------ epilogue
+        const int quarter = warp & 3, half = (warp - 2) >> 2;
+        const int row = quarter * 32 + (tid & 31);
+        const bool leader = tid == 64;
+        int it = 0;
+        for (int u = blockIdx.x; u < p.tiles; u += gridDim.x, ++it) {
+            const Tile t = tile_of(p, u);
+            const int acc = it % kAcc;
+            ptx::mbar_wait(&tfull[acc], (it / kAcc) & 1);
+            ptx::tc_fence_after();
+            constexpr int kChunks = (BN + 63) / 64;  // 32-column chunks per half
+            uint32_t v[kChunks][32];
+#pragma unroll
+            for (int ch = 0; ch < kChunks; ++ch) {
+                const int c0 = half * 32 + ch * 64;
+                if (c0 < BN && !(p.dbg & 8)) ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c0, v[ch]);
+            }
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+            // staging tile acc is free once the store issued two tiles ago has read it
+            if (leader) ptx::bulk_wait_read<1>();
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            const uint32_t sb = stg + (it & 1) * p.stg_bytes;
+            if (row < p.BW && !(p.dbg & 2)) {
+#pragma unroll
+                for (int ch = 0; ch < kChunks; ++ch) {
+                    const int c0 = half * 32 + ch * 64;
+                    if (c0 >= BN) break;
+                    const int box = c0 / kBox, j0 = (c0 % kBox) / 8;
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        float f[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            float x = __uint_as_float(v[ch][8 * g + i]);
+                            if (p.bias) x += __ldg(p.bias + c0 + 8 * g + i);
+                            f[i] = p.relu ? fmaxf(x, 0.f) : x;
+                        }
+                        const uint4 w = pack8f(f);
+                        const uint32_t a = sb + box * (p.BW * kRowB) + stg_off(row, j0 + g, kRowB);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w.x), "r"(w.y),
+                                     "r"(w.z), "r"(w.w)
+                                     : "memory");
+                    }
+                }
+            }
+            ptx::fence_proxy_async_smem();
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (leader && !(p.dbg & 2)) {
+                for (int b = 0; b < (BN + kBox - 1) / kBox; ++b)
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                            &p.tmap_y),
+                        "r"(sb + b * (p.BW * kRowB)), "r"(b * kBox), "r"(t.wo0), "r"(t.n * p.Ho + t.ho)
+                        : "memory");
+                ptx::bulk_commit();
+            }
+        }
+        if (leader) ptx::bulk_wait<0>();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<kCols>(tmem);
+    }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) conv_stem_wgrad_kernel(const __grid_constant__ StemParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[kMaxStages], empty[kMaxStages], done;
+    __shared__ uint32_t tmem_slot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int u0 = blockIdx.x * p.tiles_per_cta;
+    const int u1 = min(p.tiles, u0 + p.tiles_per_cta);
+    if (tid == 0) {
+        for (int i = 0; i < p.stages; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        ptx::mbar_init(&done, 1);
+        ptx::fence_mbarrier_init();
+        ptx::tma_prefetch_desc(&p.tmap_x);
+        ptx::tma_prefetch_desc(&p.tmap_b);
+    }
+    if (warp == 1) ptx::tmem_alloc<512>(&tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
+    const uint32_t sbase = ptx::smem_addr(smem);
+    const uint32_t xslots = static_cast<uint32_t>(p.mtiles) * 4 * p.box_bytes;
+
+    if (warp == 0) {
+        if (tid == 0) {  // ---------------------------------------- producer
+            int st = 0;
+            uint32_t ph = 0;
+            for (int u = u0; u < u1; ++u) {
+                const Tile t = tile_of(p, u);
+                ptx::mbar_wait(&empty[st], ph ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[st], p.T * p.box_bytes + p.dy_boxes * p.dy_box_bytes);
+                const uint32_t base = sbase + st * p.stage_bytes;
+                load_x(p, base, &full[st], t);
+                for (int j = 0; j < p.dy_boxes; ++j)
+                    ptx::tma_load_3d(base + xslots + j * p.dy_box_bytes, &p.tmap_b, &full[st], j * 64, t.wo0,
+                                     t.n * p.Ho + t.ho);
+                if (++st == p.stages) {
+                    st = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {  // ------------------------------------ MMA issuer
+        constexpr uint32_t idesc = ptx::make_idesc(1, 128, BN, 1u, 1u);
+        // dy rows: BN * 2 bytes; 128-byte swizzle (64-channel boxes, LBO apart) or 64-byte (BN = 32)
+        constexpr bool kDy128 = BN >= 64;
+        constexpr uint32_t kDyRow = kDy128 ? 128 : 64;
+        const int ksteps = p.BW / 16;
+        int st = 0;
+        uint32_t ph = 0;
+        for (int u = u0; u < u1; ++u) {
+            ptx::mbar_wait(&full[st], ph);
+            ptx::tc_fence_after();
+            const uint32_t base = sbase + st * p.stage_bytes;
+            const uint64_t bd0 = kDy128 ? ptx::sw128_desc(base + xslots, p.dy_box_bytes, 8 * kDyRow)
+                                        : sw64_desc(base + xslots, p.dy_box_bytes, 8 * kDyRow);
+            for (int mt = 0; mt < p.mtiles; ++mt) {
+                const uint64_t ad0 = sw64_desc(base + mt * 4 * p.box_bytes, p.box_bytes, 512);
+                for (int ks = 0; ks < ksteps; ++ks)
+                    ptx::umma_f16_elect(tmem + mt * BN, ad0 + ks * 64, bd0 + ks * (16 * kDyRow >> 4), idesc,
+                                        (u > u0 || ks > 0) ? 1u : 0u);
+            }
+            ptx::umma_commit_elect(&empty[st]);
+            if (++st == p.stages) {
+                st = 0;
+                ph ^= 1;
+            }
+        }
+        ptx::umma_commit_elect(&done);
+        __syncwarp();
+    } else if (warp < 6) {  // ----------------------------------------- epilogue
+        const int quarter = warp & 3;
+        const int m = quarter * 32 + (tid & 31);
+        const bool any = u1 > u0;
+        const int rows = p.T * 32;
+        float* part = p.partial + size_t(blockIdx.x) * rows * p.K;
+        if (any) {
+            ptx::mbar_wait(&done, 0);
+            ptx::tc_fence_after();
+        }
+        for (int mt = 0; mt < p.mtiles; ++mt) {
+            const int grow = mt * 128 + m;
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t v[32];
+                if (any) {
+                    ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + mt * BN + c0, v);
+                    ptx::tmem_ld_wait();
+                }
+                if (grow >= rows) continue;
+                float4* dst = reinterpret_cast<float4*>(part + size_t(grow) * p.K + c0);
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                    dst[g] = any ? make_float4(__uint_as_float(v[4 * g]), __uint_as_float(v[4 * g + 1]),
+                                               __uint_as_float(v[4 * g + 2]), __uint_as_float(v[4 * g + 3]))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+// x [N][H][W][C] (C = 8, cv real) -> x4 [N][H][Wst][4], zero columns around
+__global__ void stem_pack_kernel(const uint4* __restrict__ x, uint2* __restrict__ x4, int H, int W, int Wst,
+                                 int pad_w, int cv, size_t total) {
+    pdl_wait();
+    pdl_trigger();
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const int u = static_cast<int>(i % Wst);
+        const size_t row = i / Wst;
+        const int w = u - pad_w;
+        uint2 v = make_uint2(0, 0);
+        if (w >= 0 && w < W) {
+            const uint4 p = __ldg(x + row * W + w);
+            v = make_uint2(p.x, p.y);
+            if (cv < 4) v.y &= cv < 3 ? 0u : 0xFFFFu;  // channels >= cv are zero already; keep it exact
+            if (cv < 2) v.x &= 0xFFFFu;
+        }
+        x4[i] = v;
+    }
+}
+
+// w [K][R][S][C] -> wp [K][T][32]: chunk (r, q), element e = s_local * 4 + c
+__global__ void stem_pack_weights(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wp, int K,
+                                  int R, int S, int C, int cv, int nq) {
+    pdl_wait();
+    pdl_trigger();
+    const int T = R * nq, total = K * T * 32;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int e = i & 31, kt = i >> 5;
+        const int t = kt % T, k = kt / T;
+        const int r = t / nq, q = t - r * nq;
+        const int s = q * 8 + (e >> 2), c = e & 3;
+        wp[i] = (s < S && c < cv) ? w[((size_t(k) * R + r) * S + s) * C + c] : __float2bfloat16(0.f);
+    }
+}
+
+// dw[k][r][s][c] = sum over the grid's partials [g][(r, q, e)][K], zero where c >= cv
+__global__ void stem_reduce_scatter(const float* __restrict__ part, int parts, float* __restrict__ dw, int K,
+                                    int R, int S, int C, int cv, int nq) {
+    pdl_wait();
+    pdl_trigger();
+    const int total = K * R * S * C;
+    const size_t pstride = size_t(R) * nq * 32 * K;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int c = i % C, rest = i / C;
+        const int s = rest % S, kr = rest / S;
+        const int r = kr % R, k = kr / R;
+        float acc = 0.f;
+        if (c < cv) {
+            const size_t row = (size_t(r) * nq + s / 8) * 32 + (s % 8) * 4 + c;
+            const float* src = part + row * K + k;
+            for (int g = 0; g < parts; ++g) acc += __ldg(src + g * pstride);
+        }
+        dw[i] = acc;
+    }
+}
+
+struct StemPlan {
+    bool use = false;
+    int cv, nq, T, Wst, D1, BW, wtiles, tiles, Ho, Wo, chunk_step;
+    uint32_t box_bytes, b_bytes, stage_bytes, row_stride, stg_bytes;
+    int stages, G, g_step;
+    size_t smem, x4_bytes, wp_bytes;
+    // wgrad
+    int mtiles, dy_boxes, grid_wg, tiles_per_cta, wg_stages;
+    uint32_t dy_box_bytes, wg_stage_bytes;
+    size_t wg_smem, partial_bytes;
+};
+
+int g_stem_mode = -1;  // $TCB_STEM: 0 off (explicit im2col), 1 on
+
+bool stem_enabled() {
+    if (g_stem_mode < 0) {
+        const char* e = getenv("TCB_STEM");
+        g_stem_mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_stem_mode == 1;
+}
+
+size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
+
+StemPlan stem_plan(const ConvGeom& g) {
+    StemPlan q;
+    if (!stem_enabled()) return q;
+    q.cv = g.c_valid > 0 ? g.c_valid : g.c;
+    // stride 2: consecutive output positions 16 bytes apart in a 4-channel row (the forward
+    // descriptor's core-matrix row pitch)
+    if (g.c != 8 || q.cv > 4 || g.r * g.s < 2 || g.stride_w != 2) return q;
+    if (g.k != 32 && g.k != 64 && g.k != 128) return q;  // N of both GEMMs; dy boxes of 32 or 64 channels
+    q.nq = (g.s + 7) / 8;
+    q.chunk_step = 8 / g.stride_w;
+    q.T = g.r * q.nq;
+    q.Ho = g.ho();
+    q.Wo = g.wo();
+    q.Wst = std::max(g.w + g.pad_w, (q.Wo - 1) * g.stride_w + 8 * q.nq);
+    q.Wst = (q.Wst + 15) / 16 * 16;  // whole 16-pixel (128-byte) groups per stored row
+    q.D1 = (q.Wst - 8) / g.stride_w + 1;
+    q.BW = std::min((std::min(q.Wo, 128) + 15) / 16 * 16, 128);
+    q.wtiles = (q.Wo + q.BW - 1) / q.BW;
+    q.tiles = g.n * q.Ho * q.wtiles;
+    q.box_bytes = static_cast<uint32_t>(q.BW) * 64;
+    q.b_bytes = static_cast<uint32_t>(g.k) * 64;
+    q.x4_bytes = size_t(g.n) * g.h * q.Wst * 8;
+    q.wp_bytes = size_t(g.k) * q.T * 64;
+    // fwd: per stage the R stored rows a width tile reads (G 16-pixel groups each, row buffers
+    // long enough for the M = 128 descriptor's last window), packed weights resident, two
+    // output staging tiles for the TMA store
+    q.G = ((q.BW - 1) * 2 + 8 * q.nq + 15) / 16;
+    q.g_step = q.BW / 8;
+    q.row_stride = kRowStride;
+    if (static_cast<uint32_t>(std::max(q.G * 128, 16 * 128 + 64 * q.nq)) > kRowStride) return q;
+    // compiled (R, chunks) variants of the forward kernel
+    if (!((g.r == 7 && q.nq == 1) || (g.r == 3 && q.nq == 1) || (g.r == 5 && q.nq == 1) || (g.r == 11 && q.nq == 2)))
+        return q;
+    q.stage_bytes = (g.r * q.row_stride + 1023) / 1024 * 1024;
+    q.stg_bytes = (static_cast<uint32_t>(q.BW) * g.k * 2 + 1023) / 1024 * 1024;
+    const size_t fixed = size_t(q.T) * q.b_bytes + 2 * size_t(q.stg_bytes) + 1024;
+    for (q.stages = kMaxStages; q.stages >= 2; --q.stages)
+        if (size_t(q.stages) * q.stage_bytes + fixed <= kSmemCap) break;
+    if (q.stages < 2) return q;
+    q.smem = size_t(q.stages) * q.stage_bytes + fixed;
+    // wgrad: M tiles of 4 chunks; dy boxes of 64 channels (128-byte rows) or one 32-channel box
+    q.mtiles = (q.T + 3) / 4;
+    if (q.mtiles * g.k > 512 || (g.k != 32 && g.k % 64 != 0)) return q;
+    q.dy_boxes = g.k >= 64 ? g.k / 64 : 1;
+    q.dy_box_bytes = static_cast<uint32_t>(q.BW) * (g.k >= 64 ? 128 : 64);
+    q.wg_stage_bytes = (q.mtiles * 4 * q.box_bytes + q.dy_boxes * q.dy_box_bytes + 1023) / 1024 * 1024;
+    for (q.wg_stages = kMaxStages; q.wg_stages >= 2; --q.wg_stages)
+        if (size_t(q.wg_stages) * q.wg_stage_bytes + 1024 <= kSmemCap) break;
+    if (q.wg_stages < 2) return q;
+    q.wg_smem = size_t(q.wg_stages) * q.wg_stage_bytes + 1024;
+    q.grid_wg = std::min(q.tiles, num_sms());
+    q.tiles_per_cta = (q.tiles + q.grid_wg - 1) / q.grid_wg;
+    q.grid_wg = (q.tiles + q.tiles_per_cta - 1) / q.tiles_per_cta;
+    q.partial_bytes = size_t(q.grid_wg) * q.T * 32 * g.k * sizeof(float);
+    q.use = true;
+    return q;
+}
+
+bool make_x4_map(CUtensorMap* m, const void* x4, const ConvGeom& g, const StemPlan& q) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[4] = {32, cuuint64_t(q.D1), cuuint64_t(g.h), cuuint64_t(g.n)};
+    const cuuint64_t strides[3] = {cuuint64_t(g.stride_w) * 8, cuuint64_t(q.Wst) * 8, cuuint64_t(q.Wst) * 8 * g.h};
+    const cuuint32_t box[4] = {32, cuuint32_t(q.BW), 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x4), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void fill_common(StemParams& p, const ConvGeom& g, const StemPlan& q) {
+    p.Ho = q.Ho;
+    p.Wo = q.Wo;
+    p.K = g.k;
+    p.T = q.T;
+    p.nq = q.nq;
+    p.chunk_step = q.chunk_step;
+    p.sh = g.stride_h;
+    p.pad_h = g.pad_h;
+    p.BW = q.BW;
+    p.wtiles = q.wtiles;
+    p.tiles = q.tiles;
+    p.box_bytes = q.box_bytes;
+    p.d_wtiles = FastDiv(static_cast<uint32_t>(q.wtiles));
+    p.d_ho = FastDiv(static_cast<uint32_t>(q.Ho));
+}
+
+template <typename K>
+cudaError_t launch_big(K kern, dim3 grid, size_t smem, cudaStream_t st, const StemParams& p) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    return launch_pdl(kern, grid, dim3(kThreads), smem, st, p);
+}
+
+cudaError_t stem_pack(const ConvGeom& g, const StemPlan& q, const void* x, void* x4, cudaStream_t st) {
+    const size_t total = size_t(g.n) * g.h * q.Wst;
+    const int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, size_t(num_sms()) * 16));
+    return launch_pdl(stem_pack_kernel, dim3(grid), dim3(256), 0, st, static_cast<const uint4*>(x),
+                      static_cast<uint2*>(x4), g.h, g.w, q.Wst, g.pad_w, q.cv, total);
+}
+
+}  // namespace
+
+bool conv_stem_applies(const ConvGeom& g) { return stem_plan(g).use; }
+void conv_stem_set_mode(int on) { g_stem_mode = on < 0 ? -1 : (on ? 1 : 0); }
+
+size_t conv_stem_workspace(const ConvGeom& g) {
+    const StemPlan q = stem_plan(g);
+    if (!q.use) return 0;
+    return a256(q.x4_bytes) + std::max(a256(q.wp_bytes), a256(q.partial_bytes));
+}
+
+int conv_stem_launches(const ConvGeom& g, ConvMode mode, bool x_ready) {
+    if (mode == ConvMode::Fwd) return 3;
+    return x_ready ? 2 : 3;
+}
+
+cudaError_t conv_stem_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep, void* y,
+                          void* workspace, cudaStream_t st) {
+    const StemPlan q = stem_plan(g);
+    if (!q.use || workspace == nullptr || ep.residual || ep.mask) return cudaErrorInvalidValue;
+    char* ws = static_cast<char*>(workspace);
+    void* x4 = ws;
+    auto* wp = reinterpret_cast<__nv_bfloat16*>(ws + a256(q.x4_bytes));
+    cudaError_t e = stem_pack(g, q, x, x4, st);
+    if (e != cudaSuccess) return e;
+    const int wtotal = g.k * q.T * 32;
+    e = launch_pdl(stem_pack_weights, dim3(std::max(1, std::min(wtotal / 256 + 1, 512))), dim3(256), 0, st,
+                   static_cast<const __nv_bfloat16*>(w), wp, g.k, g.r, g.s, g.c, q.cv, q.nq);
+    if (e != cudaSuccess) return e;
+    StemParams p{};
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn) return cudaErrorInvalidValue;
+    {  // stored rows in 16-pixel groups, no swizzle
+        const cuuint64_t dims[4] = {64, cuuint64_t(q.Wst / 16), cuuint64_t(g.h), cuuint64_t(g.n)};
+        const cuuint64_t strides[3] = {128, cuuint64_t(q.Wst) * 8, cuuint64_t(q.Wst) * 8 * g.h};
+        const cuuint32_t box[4] = {64, cuuint32_t(q.G), 1, 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (fn(&p.tmap_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, x4, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    {  // y [N*Ho][Wo][K] stores, 64-channel (128-byte swizzle) or 32-channel (64-byte) boxes
+        const cuuint64_t dims[3] = {cuuint64_t(g.k), cuuint64_t(q.Wo), cuuint64_t(g.n) * q.Ho};
+        const cuuint64_t strides[2] = {cuuint64_t(g.k) * 2, cuuint64_t(q.Wo) * g.k * 2};
+        const cuuint32_t box[3] = {cuuint32_t(std::min(g.k, 64)), cuuint32_t(q.BW), 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (fn(&p.tmap_y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, y, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, g.k >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    if (!make_tmap_bf16_2d(&p.tmap_b, wp, g.k, size_t(q.T) * 32, g.k, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+        return cudaErrorInvalidValue;
+    fill_common(p, g, q);
+    p.stage_bytes = q.stage_bytes;
+    p.b_bytes = q.b_bytes;
+    p.stages = q.stages;
+    p.R = g.r;
+    p.G = q.G;
+    p.g_step = q.g_step;
+    p.row_stride = q.row_stride;
+    p.stg_bytes = q.stg_bytes;
+    p.bias = ep.bias;
+    p.relu = ep.relu ? 1 : 0;
+    static const int env_dbg = [] { const char* e = getenv("TCB_STEM_DBG"); return e ? atoi(e) : 0; }();
+    p.dbg = env_dbg;
+    const int grid = std::min(q.tiles, num_sms());
+    conv_tc_note_launch(ConvTcLaunchInfo{0, 5, g.k, 0, 0, 1, q.tiles, grid, 0, 1});
+#define TCB_STEM_FWD(BN, R, NQ) \
+    if (g.k == BN && g.r == R && q.nq == NQ) return launch_big(conv_stem_fwd_kernel<BN, R, NQ>, dim3(grid), q.smem, st, p);
+#define TCB_STEM_FWD_R(R, NQ) TCB_STEM_FWD(32, R, NQ) TCB_STEM_FWD(64, R, NQ) TCB_STEM_FWD(128, R, NQ)
+    TCB_STEM_FWD_R(7, 1)
+    TCB_STEM_FWD_R(3, 1)
+    TCB_STEM_FWD_R(5, 1)
+    TCB_STEM_FWD_R(11, 2)
+#undef TCB_STEM_FWD_R
+#undef TCB_STEM_FWD
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t conv_stem_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw, void* workspace,
+                            cudaStream_t st, bool x_ready) {
+    const StemPlan q = stem_plan(g);
+    if (!q.use || workspace == nullptr) return cudaErrorInvalidValue;
+    char* ws = static_cast<char*>(workspace);
+    void* x4 = ws;
+    float* part = reinterpret_cast<float*>(ws + a256(q.x4_bytes));
+    cudaError_t e = x_ready ? cudaSuccess : stem_pack(g, q, x, x4, st);
+    if (e != cudaSuccess) return e;
+    StemParams p{};
+    if (!make_x4_map(&p.tmap_x, x4, g, q)) return cudaErrorInvalidValue;
+    {
+        EncodeTiledFn fn = encode_tiled_fn();
+        if (!fn) return cudaErrorInvalidValue;
+        const cuuint64_t dims[3] = {cuuint64_t(g.k), cuuint64_t(q.Wo), cuuint64_t(g.n) * q.Ho};
+        const cuuint64_t strides[2] = {cuuint64_t(g.k) * 2, cuuint64_t(q.Wo) * g.k * 2};
+        const cuuint32_t box[3] = {cuuint32_t(std::min(g.k, 64)), cuuint32_t(q.BW), 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (fn(&p.tmap_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(dy), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, g.k >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    fill_common(p, g, q);
+    p.stage_bytes = q.wg_stage_bytes;
+    p.stages = q.wg_stages;
+    p.mtiles = q.mtiles;
+    p.tiles_per_cta = q.tiles_per_cta;
+    p.dy_boxes = q.dy_boxes;
+    p.dy_box_bytes = q.dy_box_bytes;
+    p.partial = part;
+    conv_tc_note_launch(ConvTcLaunchInfo{2, 5, g.k, 0, 0, q.grid_wg, q.tiles, q.grid_wg, 0, 0});
+    switch (g.k) {
+        case 32: e = launch_big(conv_stem_wgrad_kernel<32>, dim3(q.grid_wg), q.wg_smem, st, p); break;
+        case 64: e = launch_big(conv_stem_wgrad_kernel<64>, dim3(q.grid_wg), q.wg_smem, st, p); break;
+        case 128: e = launch_big(conv_stem_wgrad_kernel<128>, dim3(q.grid_wg), q.wg_smem, st, p); break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    const int total = g.k * g.r * g.s * g.c;
+    return launch_pdl(stem_reduce_scatter, dim3(std::max(1, std::min((total + 255) / 256, 1024))), dim3(256), 0, st,
+                      static_cast<const float*>(part), q.grid_wg, dw, g.k, g.r, g.s, g.c, q.cv, q.nq);
+}
+
+}  // namespace tcb

@@ -1359,6 +1359,7 @@ bool conv_tc_supported(const ConvGeom& g, ConvMode mode) {
 }
 
 size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
+    if (mode != ConvMode::Dgrad && conv_stem_applies(g)) return conv_stem_workspace(g);
     const NarrowPlan q = narrow_plan(g);
     if (q.use && mode == ConvMode::Fwd)
         return align256(q.col_bytes) + align256(size_t(g.k) * q.kc * 2);
@@ -1373,9 +1374,10 @@ size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
     return std::max(im2col_ws, conv_win_wgrad_workspace(g));
 }
 
-bool conv_tc_narrow(const ConvGeom& g) { return narrow_plan(g).use; }
+bool conv_tc_narrow(const ConvGeom& g) { return conv_stem_applies(g) || narrow_plan(g).use; }
 
 int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool counters) {
+    if (mode != ConvMode::Dgrad && conv_stem_applies(g)) return conv_stem_launches(g, mode, cols_ready);
     const NarrowPlan q = narrow_plan(g);
     if (mode == ConvMode::Fwd) return q.use ? 3 : 1;
     if (mode == ConvMode::Dgrad) return g.stride_h * g.stride_w;
@@ -1392,6 +1394,7 @@ int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool cou
 
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
                         void* y, cudaStream_t st, void* workspace) {
+    if (workspace && conv_stem_applies(g)) return conv_stem_fwd(g, x, w, ep, y, workspace, st);
     Params p{};
     const NarrowPlan q = narrow_plan(g);
     const void* a_matrix = x;
@@ -1510,6 +1513,7 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* w, cons
 
 cudaError_t conv_tc_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw,
                           void* workspace, cudaStream_t st, bool cols_ready, int* counters) {
+    if (conv_stem_applies(g)) return conv_stem_wgrad(g, dy, x, dw, workspace, st, cols_ready);
     const NarrowPlan q = narrow_plan(g);
     if (q.use) {
         if (workspace == nullptr) return cudaErrorInvalidValue;

@@ -96,7 +96,22 @@ bool conv_win_wgrad_applies(const ConvGeom& g);
 size_t conv_win_wgrad_workspace(const ConvGeom& g);
 cudaError_t conv_win_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw, void* workspace,
                            cudaStream_t st);
-void conv_win_set_debug(void* buf);  // diagnostics: per-CTA role timing (8 x u64 per CTA) or nullptr
+void conv_win_set_debug(void* buf);
+// Row-window stem (conv_stem.cu): even-stride first layers over <= 4 real
+// channels of an 8-channel input (ResNet 7x7/2, Inception 3x3/2). The input is
+// repacked once to 4-channel rows with zero padding columns in `workspace`
+// (kept for the weight gradient: x_ready), and one overlapping-row TMA box per
+// filter row is the GEMM A tile of a whole output row; no patch matrix.
+// Operand path 5 in ConvTcLaunchInfo.
+bool conv_stem_applies(const ConvGeom& g);
+size_t conv_stem_workspace(const ConvGeom& g);
+int conv_stem_launches(const ConvGeom& g, ConvMode mode, bool x_ready);
+cudaError_t conv_stem_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep, void* y,
+                          void* workspace, cudaStream_t st);
+cudaError_t conv_stem_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw, void* workspace,
+                            cudaStream_t st, bool x_ready);
+void conv_stem_set_mode(int on);  // 0 off (explicit im2col path), 1 on, -1 from $TCB_STEM
+  // diagnostics: per-CTA role timing (8 x u64 per CTA) or nullptr
 // TMA epilogue for layers with at most `kb` 64-deep k-blocks (0 = never,
 // -1 = default: $TCB_CONV_EPI_KB or 8).
 void conv_tc_set_epi_kb(int kb);

@@ -151,6 +151,20 @@ TCB_API int tcb_conv_plan_create(const tcb_conv_geom* g, int algo, int prec, tcb
     TCB_GUARD_END
 }
 
+// Narrow inputs: only the first c_valid of the C channels can be non-zero (the
+// rest is bf16 channel padding). Lets first layers take the explicit-im2col /
+// row-window stem paths, as the executor does; the workspace size can grow.
+TCB_API int tcb_conv_plan_set_valid_channels(tcb_conv_plan* plan, int c_valid, size_t* workspace_bytes) {
+    TCB_GUARD_BEGIN
+    if (!plan) return fail(TCB_ERR_INVALID, "NULL argument");
+    if (c_valid < 0 || c_valid > plan->g.c) return fail(TCB_ERR_INVALID, "c_valid must be in [0, C]");
+    plan->g.c_valid = c_valid;
+    plan->layout = conv_plan_layout(plan->g, plan->algo, plan->prec);
+    if (workspace_bytes) *workspace_bytes = plan->layout.total;
+    return TCB_OK;
+    TCB_GUARD_END
+}
+
 TCB_API int tcb_conv_plan_destroy(tcb_conv_plan* plan) {
     delete plan;
     return TCB_OK;
@@ -169,7 +183,8 @@ TCB_API int tcb_conv_fwd(const tcb_conv_plan* plan, const void* x, const void* w
     cudaError_t e;
     switch (plan->algo) {
         case TCB_ALGO_GEMM:
-            e = plan->prec == TCB_PREC_BF16 ? conv_tc_fwd(plan->g, x, w, ep, y, st)
+            e = plan->prec == TCB_PREC_BF16 ? conv_tc_fwd(plan->g, x, w, ep, y, st,
+                                                          plan->g.c_valid > 0 ? workspace : nullptr)
                 : plan->prec == TCB_PREC_TF32
                     ? conv_tf32_fwd(plan->g, static_cast<const float*>(x),
                                     static_cast<const float*>(w), ep, static_cast<float*>(y), st)
@@ -390,6 +405,13 @@ TCB_API int tcb_conv_last_launch_info(int* out10) {
     const ConvTcLaunchInfo i = conv_tc_last_launch();
     const int v[10] = {i.mode, i.load, i.bn, i.epi, i.cta2, i.splits, i.units, i.grid, i.fused_reduce, i.b_resident};
     for (int k = 0; k < 10; ++k) out10[k] = v[k];
+    return TCB_OK;
+}
+
+// 1 (default): row-window stem kernels for narrow even-stride first layers;
+// 0: the explicit-im2col GEMM path for them (A/B comparisons, tests).
+TCB_API int tcb_set_conv_stem(int on) {
+    conv_stem_set_mode(on);
     return TCB_OK;
 }
 

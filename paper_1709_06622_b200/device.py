@@ -66,6 +66,8 @@ def lib() -> ctypes.CDLL:
     L.tcb_conv_plan_create.argtypes = [ctypes.POINTER(ConvGeom), ctypes.c_int, ctypes.c_int,
                                        ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_size_t)]
     L.tcb_conv_plan_destroy.argtypes = [_vp]
+    L.tcb_conv_plan_set_valid_channels.argtypes = [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
+    L.tcb_set_conv_stem.argtypes = [ctypes.c_int]
     L.tcb_conv_fwd.argtypes = [_vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp]
     L.tcb_conv_dgrad.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.tcb_conv_wgrad.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
@@ -122,6 +124,15 @@ class ConvPlan:
         self.workspace_bytes = ws.value
         # zero-filled once: split-K counters inside must start at 0 (they self-reset)
         self.workspace = torch.zeros(max(ws.value, 1), dtype=torch.uint8, device="cuda")
+
+    def set_valid_channels(self, c_valid):
+        """Only the first c_valid input channels can be non-zero (narrow first
+        layers): enables the explicit-im2col / row-window stem paths."""
+        ws = ctypes.c_size_t()
+        check(lib().tcb_conv_plan_set_valid_channels(self.handle, int(c_valid), ctypes.byref(ws)))
+        self.workspace_bytes = ws.value
+        self.workspace = torch.zeros(max(ws.value, 1), dtype=torch.uint8, device="cuda")
+        return self
 
     def __del__(self):
         try:
