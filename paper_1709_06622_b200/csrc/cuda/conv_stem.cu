@@ -419,6 +419,32 @@ __global__ void stem_pack_kernel(const uint4* __restrict__ x, uint2* __restrict_
     }
 }
 
+// uint8 RGB pixels -> (u + 0.5) / 128 - 1 (the executor's input preparation,
+// pack_channels_u8) written straight into x4 (zero padding columns) and, when
+// x8 is given, into the 8-channel activation as well: the stem input costs one
+// pass over the uint8 batch instead of a pack plus a repack.
+__global__ void stem_pack_u8_kernel(const uint8_t* __restrict__ src, uint2* __restrict__ x4,
+                                    uint4* __restrict__ x8, int W, int Wst, int pad_w, int cl, size_t total) {
+    pdl_wait();
+    pdl_trigger();
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const int u = static_cast<int>(i % Wst);
+        const size_t row = i / Wst;
+        const int w = u - pad_w;
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = __float2bfloat16(0.f);
+        if (w >= 0 && w < W) {
+            const uint8_t* px = src + (row * W + w) * cl;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (c < cl) v[c] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(float(__ldg(px + c)) + 0.5f, 0.0078125f), 1.f));
+            if (x8) x8[row * W + w] = *reinterpret_cast<const uint4*>(v);
+        }
+        x4[i] = *reinterpret_cast<const uint2*>(v);
+    }
+}
+
 // w [K][R][S][C] -> wp [K][T][32]: chunk (r, q), element e = s_local * 4 + c
 __global__ void stem_pack_weights(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wp, int K,
                                   int R, int S, int C, int cv, int nq) {
@@ -583,6 +609,22 @@ cudaError_t stem_pack(const ConvGeom& g, const StemPlan& q, const void* x, void*
 }  // namespace
 
 bool conv_stem_applies(const ConvGeom& g) { return stem_plan(g).use; }
+
+cudaError_t conv_stem_pack_input(const ConvGeom& g, const void* x, void* workspace, cudaStream_t st) {
+    const StemPlan q = stem_plan(g);
+    if (!q.use || workspace == nullptr) return cudaErrorInvalidValue;
+    return stem_pack(g, q, x, workspace, st);
+}
+
+cudaError_t conv_stem_pack_u8(const ConvGeom& g, const uint8_t* src, int cl, void* x8, void* workspace,
+                              cudaStream_t st) {
+    const StemPlan q = stem_plan(g);
+    if (!q.use || workspace == nullptr || cl < 1 || cl > q.cv) return cudaErrorInvalidValue;
+    const size_t total = size_t(g.n) * g.h * q.Wst;
+    const int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, size_t(num_sms()) * 16));
+    return launch_pdl(stem_pack_u8_kernel, dim3(grid), dim3(256), 0, st, src, static_cast<uint2*>(workspace),
+                      static_cast<uint4*>(x8), g.w, q.Wst, g.pad_w, cl, total);
+}
 void conv_stem_set_mode(int on) { g_stem_mode = on < 0 ? -1 : (on ? 1 : 0); }
 
 size_t conv_stem_workspace(const ConvGeom& g) {
@@ -592,18 +634,19 @@ size_t conv_stem_workspace(const ConvGeom& g) {
 }
 
 int conv_stem_launches(const ConvGeom& g, ConvMode mode, bool x_ready) {
-    if (mode == ConvMode::Fwd) return 3;
+    (void)g;
+    if (mode == ConvMode::Fwd) return x_ready ? 2 : 3;
     return x_ready ? 2 : 3;
 }
 
 cudaError_t conv_stem_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep, void* y,
-                          void* workspace, cudaStream_t st) {
+                          void* workspace, cudaStream_t st, bool x_ready) {
     const StemPlan q = stem_plan(g);
     if (!q.use || workspace == nullptr || ep.residual || ep.mask) return cudaErrorInvalidValue;
     char* ws = static_cast<char*>(workspace);
     void* x4 = ws;
     auto* wp = reinterpret_cast<__nv_bfloat16*>(ws + a256(q.x4_bytes));
-    cudaError_t e = stem_pack(g, q, x, x4, st);
+    cudaError_t e = x_ready ? cudaSuccess : stem_pack(g, q, x, x4, st);
     if (e != cudaSuccess) return e;
     const int wtotal = g.k * q.T * 32;
     e = launch_pdl(stem_pack_weights, dim3(std::max(1, std::min(wtotal / 256 + 1, 512))), dim3(256), 0, st,

@@ -1393,8 +1393,8 @@ int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool cou
 }
 
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
-                        void* y, cudaStream_t st, void* workspace) {
-    if (workspace && conv_stem_applies(g)) return conv_stem_fwd(g, x, w, ep, y, workspace, st);
+                        void* y, cudaStream_t st, void* workspace, bool x_ready) {
+    if (workspace && conv_stem_applies(g)) return conv_stem_fwd(g, x, w, ep, y, workspace, st, x_ready);
     Params p{};
     const NarrowPlan q = narrow_plan(g);
     const void* a_matrix = x;

@@ -39,9 +39,9 @@ struct Epilogue {
 // workspace they take the implicit im2col path.
 size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode);
 int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready = false,
-                     bool counters = false);  // kernels per call
+                     bool counters = false);  // kernels per call (fwd: cols_ready = stem input packed)
 cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep,
-                        void* y, cudaStream_t st, void* workspace = nullptr);
+                        void* y, cudaStream_t st, void* workspace = nullptr, bool x_ready = false);
 // Dgrad reads the KRSC filters `w` directly (MN-major TMA boxes) whenever its
 // operands load by TMA; only gather-path geometries (conv_tc_dgrad_needs_pack)
 // need `wT` = pack_dgrad_weights(w), otherwise it may be NULL.
@@ -107,7 +107,14 @@ bool conv_stem_applies(const ConvGeom& g);
 size_t conv_stem_workspace(const ConvGeom& g);
 int conv_stem_launches(const ConvGeom& g, ConvMode mode, bool x_ready);
 cudaError_t conv_stem_fwd(const ConvGeom& g, const void* x, const void* w, const Epilogue& ep, void* y,
-                          void* workspace, cudaStream_t st);
+                          void* workspace, cudaStream_t st, bool x_ready = false);
+// The 4-channel rows at the head of the stem workspace, from the 8-channel
+// activation x, or straight from uint8 pixels (cl channels per pixel) with the
+// executor's input normalisation, also writing the 8-channel activation x8
+// when it is not NULL.
+cudaError_t conv_stem_pack_input(const ConvGeom& g, const void* x, void* workspace, cudaStream_t st);
+cudaError_t conv_stem_pack_u8(const ConvGeom& g, const uint8_t* src, int cl, void* x8, void* workspace,
+                              cudaStream_t st);
 cudaError_t conv_stem_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw, void* workspace,
                             cudaStream_t st, bool x_ready);
 void conv_stem_set_mode(int on);  // 0 off (explicit im2col path), 1 on, -1 from $TCB_STEM

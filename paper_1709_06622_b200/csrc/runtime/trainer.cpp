@@ -149,6 +149,10 @@ struct tcb_trainer {
     cudaEvent_t ev_comm_done = nullptr, ev_bwd_start = nullptr;
     std::map<int, std::vector<int>> shard_trigger;  // node index -> shards it completes
     bool fused_split_reduce = false;  // config "fused_split_reduce" / $TCB_FUSED_SPLIT_REDUCE
+    // row-window stem conv reading the input (conv_stem.cu), -1 if none: every
+    // write of the input activation also refreshes its 4-channel rows in the
+    // layer's workspace, so the step never repacks them
+    int stem_node = -1;
     // CUDA graph of the step (config "cuda_graph", $TCB_GRAPH)
     bool use_graph = true;
     int eager_steps = 0, graph_launches = 0;
@@ -534,6 +538,8 @@ int allocate(tcb_trainer* t, bool dry = false) {
         if (nd.op == Op::MaxPool) nd.argmax = b.take(elems);
         if (nd.op == Op::Conv) {
             nd.narrow = t->bf16 && nd.algo_id == TCB_ALGO_GEMM && conv_tc_narrow(nd.g);
+            if (nd.narrow && nd.in == 0 && conv_stem_applies(nd.g))
+                t->stem_node = static_cast<int>(&nd - t->nodes.data());
             if (nd.algo_id == TCB_ALGO_GEMM) {
                 if (nd.narrow) {
                     const size_t nb = std::max(conv_tc_workspace(nd.g, ConvMode::Wgrad),
@@ -602,8 +608,13 @@ int pack_input(tcb_trainer* t, cudaStream_t st) {
     const size_t px = size_t(in.n) * in.h * in.w;
     const float* src = t->at<float>(t->off_input_f32);
     t->launches++;
-    return check_cuda(pack_channels(t->dt, src, t->at(in.act), px, in.c_logical, in.c, st),
-                      "pack_input");
+    TRY(check_cuda(pack_channels(t->dt, src, t->at(in.act), px, in.c_logical, in.c, st), "pack_input"));
+    if (t->stem_node >= 0) {
+        const Node& sn = t->nodes[t->stem_node];
+        t->launches++;
+        TRY(check_cuda(conv_stem_pack_input(sn.g, t->at(in.act), t->at(sn.nws), st), "pack_input stem rows"));
+    }
+    return TCB_OK;
 }
 
 int refresh_biases(tcb_trainer* t, const void* wc, int k, cudaStream_t st);
@@ -705,7 +716,8 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                     TRY_CUDA(fft_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
                 else if (t->bf16)
                     TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), static_cast<__nv_bfloat16*>(t->wc_ptr()) + nd.woff,
-                                         ep, t->at(nd.act), st, nd.narrow ? t->at(nd.nws) : nullptr));
+                                         ep, t->at(nd.act), st, nd.narrow ? t->at(nd.nws) : nullptr,
+                                         static_cast<int>(idx) == t->stem_node));
                 else if (t->tf32)
                     TRY_CUDA(conv_tf32_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
                                            ep, t->at<float>(nd.act), st));
@@ -713,7 +725,9 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                     TRY_CUDA(conv_ffma_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,
                                            ep, t->at<float>(nd.act), st));
                 t->mark(idx, 1, st);
-                t->launches += (t->bf16 && nd.algo_id == TCB_ALGO_GEMM) ? conv_tc_launches(nd.g, ConvMode::Fwd) : 1;
+                t->launches += (t->bf16 && nd.algo_id == TCB_ALGO_GEMM)
+                                   ? conv_tc_launches(nd.g, ConvMode::Fwd, static_cast<int>(idx) == t->stem_node)
+                                   : 1;
                 break;
             }
             case Op::MaxPool:
@@ -1340,12 +1354,22 @@ static int consume_staged(tcb_trainer* t, cudaStream_t st) {
     const size_t px = size_t(in.n) * in.h * in.w;
     const bool timed = t->timing && t->ev_prep[0];
     if (timed) TRY_CUDA(cudaEventRecord(t->ev_prep[0], st));
-    if (t->stage_format[k] == TCB_INPUT_U8)
-        TRY_CUDA(pack_channels_u8(t->dt, t->at<uint8_t>(t->off_stage[k]), t->at(in.act), px, in.c_logical,
-                                  in.c, st));
-    else
-        TRY_CUDA(pack_channels(t->dt, t->at<float>(t->off_stage[k]), t->at(in.act), px, in.c_logical, in.c,
-                               st));
+    const Node* sn = t->stem_node >= 0 ? &t->nodes[t->stem_node] : nullptr;
+    if (t->stage_format[k] == TCB_INPUT_U8 && sn) {
+        TRY_CUDA(conv_stem_pack_u8(sn->g, t->at<uint8_t>(t->off_stage[k]), in.c_logical, t->at(in.act),
+                                   t->at(sn->nws), st));
+    } else {
+        if (t->stage_format[k] == TCB_INPUT_U8)
+            TRY_CUDA(pack_channels_u8(t->dt, t->at<uint8_t>(t->off_stage[k]), t->at(in.act), px, in.c_logical,
+                                      in.c, st));
+        else
+            TRY_CUDA(pack_channels(t->dt, t->at<float>(t->off_stage[k]), t->at(in.act), px, in.c_logical, in.c,
+                                   st));
+        if (sn) {
+            TRY_CUDA(conv_stem_pack_input(sn->g, t->at(in.act), t->at(sn->nws), st));
+            t->launches++;
+        }
+    }
     TRY_CUDA(cudaMemcpyAsync(t->at(t->off_labels), t->at(t->off_stage_labels[k]), size_t(t->batch) * 4,
                              cudaMemcpyDeviceToDevice, st));
     if (timed) {
@@ -1608,7 +1632,8 @@ TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
             L["boff"] = nd.bias ? json(nd.boff) : json(nullptr);
             L["init_scale"] = nd.init_scale;
             L["algo"] = nd.algo;
-            L["explicit_im2col"] = nd.narrow;
+            L["stem_rows"] = static_cast<int>(i) == t->stem_node;
+            L["explicit_im2col"] = nd.narrow && static_cast<int>(i) != t->stem_node;
             L["packed_dgrad_weights"] = nd.pack_wT;
             const size_t first = nd.woff / std::max<size_t>(t->shard, 1);
             const size_t last_el = (nd.bias ? nd.boff + nd.g.k : nd.woff + nd.wcount) - 1;

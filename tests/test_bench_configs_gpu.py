@@ -89,7 +89,7 @@ def test_resnet50_bs256_bench_step_sampled(oracle):
     wl = ["stem", "s1b1_c1", "s1b2_c2", "s1b1_proj", "s2b1_c2", "s2b3_c3", "s3b1_proj",
           "s3b4_c2", "s4b1_c2", "s4b3_c1", "fc"]
     t, worst, werr = _sampled_check(oracle, cfg, [0, 255], wl)
-    assert t.describe()["layers"][1]["explicit_im2col"]
+    assert t.describe()["layers"][1]["stem_rows"]
 
 
 def test_vgg16_ffma_step_end_to_end_n2(oracle):

@@ -91,10 +91,10 @@ def test_bf16_end_to_end_drift_is_small_on_shallow_net(oracle):
 
 def test_resnet50_geometry_step_bf16(oracle):
     """C3 geometry (full ResNet-50-shaped graph, 224x224) at batch 1, layer-local.
-    The 3-channel stem runs as explicit im2col + plain GEMM (fwd and wgrad)."""
+    The 3-channel stem runs on the row-window stem kernels (fwd and wgrad)."""
     t, _ = _check(oracle, _models().resnet50(batch=1, precision="bf16"))
     convs = [L for L in t.describe()["layers"] if L["op"] == "conv"]
-    assert convs[0]["explicit_im2col"] and not any(L["explicit_im2col"] for L in convs[1:])
+    assert convs[0]["stem_rows"] and not any(L["explicit_im2col"] or L["stem_rows"] for L in convs[1:])
 
 
 def test_resnet50_geometry_step_tf32(oracle):
@@ -134,10 +134,20 @@ def test_inception_v3_mixed_algorithms_step(oracle):
     _check(oracle, cfg)
 
 
-def test_explicit_im2col_stem_batch8(oracle):
-    """Stem-only net at batch 8: explicit-im2col fwd (TMA epilogue) and wgrad
-    (col kept from the forward pass) against the oracle, layer-local."""
+def test_row_window_stem_batch8(oracle):
+    """Stem-only net at batch 8: row-window stem fwd (input rows packed with the
+    uint8 / fp32 input preparation) and wgrad against the oracle, layer-local."""
     cfg = _models().from_net("input 64 64 3\nconv 7 2 3 64\npool 3 2 1\nconv 3 1 1 64\nfc 10\n",
+                             batch=8, precision="bf16")
+    t, _ = _check(oracle, cfg)
+    assert t.describe()["layers"][1]["stem_rows"]
+
+
+def test_explicit_im2col_first_layer_batch8(oracle):
+    """An 11x11/4 first layer (AlexNet-style; stride 4 is outside the stem
+    kernels): explicit-im2col fwd (TMA epilogue) and wgrad (col kept from the
+    forward pass) against the oracle, layer-local."""
+    cfg = _models().from_net("input 67 67 3\nconv 11 4 2 64\npool 3 2 0\nconv 3 1 1 64\nfc 10\n",
                              batch=8, precision="bf16")
     t, _ = _check(oracle, cfg)
     assert t.describe()["layers"][1]["explicit_im2col"]
@@ -218,11 +228,19 @@ def test_host_batch_path_matches_resident_batch(oracle):
     assert torch.equal(a.tensor("grad"), b.tensor("grad"))
 
 
-def test_staged_u8_batches_pipeline(oracle):
+def _stem_net(batch=4):
+    return _models().from_net("input 40 38 3\nconv 7 2 3 64\npool 3 2 1\nconv 3 1 1 64\nfc 10\n",
+                              batch=batch, precision="bf16")
+
+
+@pytest.mark.parametrize("net", ["tiny_resnet", "stem_rows"])
+def test_staged_u8_batches_pipeline(oracle, net):
     """Staged uint8 batches (copy stream, two slots) feed consecutive steps in
-    order and equal the synchronous fp32 host path on the converted values."""
+    order and equal the synchronous fp32 host path on the converted values
+    (the uint8 preparation writes the stem's 4-channel rows directly, the fp32
+    path repacks them from the 8-channel input)."""
     from paper_1709_06622_b200.trainer import Trainer
-    cfg = _models().tiny_resnet(batch=4, precision="bf16")
+    cfg = _models().tiny_resnet(batch=4, precision="bf16") if net == "tiny_resnet" else _stem_net()
     a, b = Trainer(cfg), Trainer(cfg)
     lay = a.describe()
     n, h, w = lay["layers"][0]["shape"][:3]
@@ -244,6 +262,8 @@ def test_staged_u8_batches_pipeline(oracle):
         torch.cuda.synchronize()
         assert torch.equal(a.tensor("grad"), b.tensor("grad")), i
         assert torch.equal(a.tensor("param"), b.tensor("param")), i
+    first_conv = next(L for L in a.describe()["layers"] if L["op"] == "conv")  # (planned at the first step)
+    assert first_conv["stem_rows"]  # both stems (K padded to 64) take the row-window kernels
 
 
 def test_cuda_graph_replay_matches_eager_steps():
