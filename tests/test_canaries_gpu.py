@@ -81,3 +81,36 @@ def test_conv_outputs_and_workspace_stay_in_bounds(case, path):
     assert _guards_ok(wsbuf), "workspace overrun"
     for a, b_ in zip(*runs):
         assert torch.equal(a, b_), "not bitwise reproducible"
+
+
+@pytest.mark.parametrize("case", [(4, 28, 28, 64, 64), (4, 28, 28, 256, 128), (8, 14, 14, 128, 256)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_tma_epilogue_many_tiles_per_cta(case):
+    """1x1 K-light passes with more tiles than SMs (every CTA loops over several
+    tiles): side inputs double-buffered across tiles (residual / mask) must
+    stay in order; compared against the register-epilogue path."""
+    from paper_1709_06622_b200 import device
+    n, h, w, c, k = case
+    n *= 16  # > 148 tiles of 128 rows
+    g = device.geom(n, h, w, c, k, 1)
+    plan = device.ConvPlan(g, "gemm", "bf16")
+    bf = torch.bfloat16
+    x = torch.randn(n, h, w, c, device="cuda").to(bf)
+    wt = (torch.randn(k, 1, 1, c, device="cuda") * 0.1).to(bf)
+    res = torch.randn(n, h, w, k, device="cuda").to(bf)
+    dy = torch.randn(n, h, w, k, device="cuda").to(bf)
+    L = device.lib()
+    L.tcb_set_conv_operand_path.argtypes = [ctypes.c_int]
+    outs = []
+    try:
+        for mode in (0, 2):  # auto (TMA epilogue) / register epilogue
+            L.tcb_set_conv_operand_path(mode)
+            y = plan.fwd(x, wt, residual=res, relu=True)
+            dx = plan.dgrad(dy, wt, residual=x, mask=x)
+            dx2 = plan.dgrad(dy, wt, mask=x)
+            torch.cuda.synchronize()
+            outs.append((y, dx, dx2))
+    finally:
+        L.tcb_set_conv_operand_path(0)
+    for a, b_ in zip(*outs):
+        assert torch.equal(a, b_)
