@@ -25,6 +25,7 @@
 // stride^2 dense GEMMs over disjoint pixel phases, no zero-insertion waste.
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -752,206 +753,218 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         uint8_t* ebuf = smem + C::kRingBytes + (warp - 4) * C::kEpiWarpBytes;
         const uint32_t ebuf_addr = ptx::smem_addr(ebuf);
         uint64_t* sbar = side_bar + (warp - 4) * 2 * EPI;
-        const uint32_t side_bytes = (p.residual ? 2048u : 0u) + (p.mask ? 2048u : 0u);
-        const bool narrow_slots = side_bytes <= 2048u;
-        const int nslots = narrow_slots ? 2 * EPI : EPI;
-        const uint32_t sstride = narrow_slots ? 2048u : 4096u;
-        const uint32_t mask_off = p.residual ? 2048u : 0u;
-        const int ncol = p.s.Ncol;
-        const int my_tiles = p.num_tiles > unit0 ? (p.num_tiles - unit0 + ustride - 1) / ustride : 0;
-        // dbuf: side inputs double-buffered by tile (the next tile's boxes load while this tile's
-        // chunks run); whole: one tile's boxes, loaded at tile start; else a ring of chunk slots
-        const bool dbuf = side_bytes && nslots >= 2 * kHalfChunks;
-        constexpr int kTrig = kHalfChunks > 1 ? 1 : 0;  // chunk of tile i that requests tile i + 1
-        const bool whole = !dbuf && nslots >= kHalfChunks;
-        auto load_tile = [&](int i) {  // lane 0
-            const TileCoord tq = tile_coord<CTA2>(p, unit0 + i * ustride, rank);
-            const int r0 = tq.mt * BM + quarter * 32;
-            const int sbase = dbuf ? (i & 1) * kHalfChunks : 0;
-            for (int k = 0; k < kHalfChunks && k < nslots; ++k) {
-                const uint32_t slot = static_cast<uint32_t>(sbase + k);
-                const int c0 = tq.nt * BN + (c_begin + k) * 32;
-                ptx::mbar_arrive_expect_tx(&sbar[slot], side_bytes);
-                if (p.residual) ptx::tma_load_2d(ebuf_addr + slot * sstride, &p.tmap_res, &sbar[slot], c0, r0);
-                if (p.mask)
-                    ptx::tma_load_2d(ebuf_addr + slot * sstride + mask_off, &p.tmap_mask, &sbar[slot], c0, r0);
+        // one instantiation per side-input / ReLU combination (no per-element flag tests)
+        auto run = [&](auto res_c, auto mask_c, auto relu_c) {
+            constexpr bool kRes = decltype(res_c)::value, kMask = decltype(mask_c)::value;
+            constexpr bool kRelu = decltype(relu_c)::value;
+            constexpr uint32_t side_bytes = (kRes ? 2048u : 0u) + (kMask ? 2048u : 0u);
+            constexpr bool narrow_slots = side_bytes <= 2048u;
+            const int nslots = narrow_slots ? 2 * EPI : EPI;
+            const uint32_t sstride = narrow_slots ? 2048u : 4096u;
+            constexpr uint32_t mask_off = kRes ? 2048u : 0u;
+            const int ncol = p.s.Ncol;
+            const int my_tiles = p.num_tiles > unit0 ? (p.num_tiles - unit0 + ustride - 1) / ustride : 0;
+            // dbuf: side inputs double-buffered by tile (the next tile's boxes load while this tile's
+            // chunks run); whole: one tile's boxes, loaded at tile start; else a ring of chunk slots
+            const bool dbuf = side_bytes && nslots >= 2 * kHalfChunks;
+            constexpr int kTrig = kHalfChunks > 1 ? 1 : 0;  // chunk of tile i that requests tile i + 1
+            const bool whole = !dbuf && nslots >= kHalfChunks;
+            auto load_tile = [&](int i) {  // lane 0
+                const TileCoord tq = tile_coord<CTA2>(p, unit0 + i * ustride, rank);
+                const int r0 = tq.mt * BM + quarter * 32;
+                const int sbase = dbuf ? (i & 1) * kHalfChunks : 0;
+                for (int k = 0; k < kHalfChunks && k < nslots; ++k) {
+                    const uint32_t slot = static_cast<uint32_t>(sbase + k);
+                    const int c0 = tq.nt * BN + (c_begin + k) * 32;
+                    ptx::mbar_arrive_expect_tx(&sbar[slot], side_bytes);
+                    if constexpr (kRes) ptx::tma_load_2d(ebuf_addr + slot * sstride, &p.tmap_res, &sbar[slot], c0, r0);
+                    if constexpr (kMask)
+                        ptx::tma_load_2d(ebuf_addr + slot * sstride + mask_off, &p.tmap_mask, &sbar[slot], c0, r0);
+                }
+            };
+            if constexpr (!side_bytes) {
+                // no side inputs: staging slots only hold outputs on their way to the TMA store
+                constexpr bool kWhole = EPI >= kHalfChunks;
+                const int c_end = c_begin + kHalfChunks;
+                uint32_t seq = 0;
+                int it = 0;
+                for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
+                    const TileCoord tc = tile_coord<CTA2>(p, t, rank);
+                    const int acc = it & 1;
+                    const uint32_t acc_phase = (it >> 1) & 1;
+                    const int row0 = tc.mt * BM + quarter * 32;
+                    ptx::mbar_wait(&tfull[acc], acc_phase);
+                    ptx::tc_fence_after();
+        #pragma unroll 1
+                    for (int c = c_begin; c < c_end; ++c, ++seq) {
+                        const int col0 = tc.nt * BN + c * 32;
+                        uint32_t v[32];
+                        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                                    acc * BN + c * 32,
+                                                v);
+                        ptx::tmem_ld_wait();
+                        const uint32_t slot = kWhole ? static_cast<uint32_t>(c - c_begin) : (seq & 1);
+                        uint8_t* b0 = ebuf + slot * 4096;  // (4 KB slot pitch as with two side inputs)
+                        if (lane == 0) {  // the store that last used this slot has read it
+                            if constexpr (kWhole) ptx::bulk_wait_read<kHalfChunks - 1>();
+                            else ptx::bulk_wait_read<1>();
+                        }
+                        __syncwarp();
+                        if (col0 < ncol) {
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                float x[8];
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(v[8 * g + i]);
+                                const uint32_t off = lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4);
+                                if (p.bias) {
+                                    const int cb = col0 + 8 * g;
+#pragma unroll
+                                    for (int i = 0; i < 8; ++i)
+                                        if (cb + i < ncol) x[i] += __ldg(p.bias + cb + i);
+                                }
+                                if constexpr (kRelu) {
+#pragma unroll
+                                    for (int i = 0; i < 8; ++i) x[i] = fmaxf(x[i], 0.f);
+                                }
+                                *reinterpret_cast<uint4*>(b0 + off) = pack8(x);
+                            }
+                            ptx::fence_proxy_async_smem();
+                        }
+                        __syncwarp();
+                        if (lane == 0 && col0 < ncol) {
+                            ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * 4096, col0, row0);
+                            ptx::bulk_commit();
+                        }
+                    }
+                    ptx::tc_fence_before();
+                    if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
+                    else ptx::mbar_arrive(&tempty[acc]);
+                }
+                if (lane == 0) ptx::bulk_wait<0>();
+            } else {
+                uint32_t seq = 0;  // chunk sequence (ring mode)
+                if (lane == 0 && side_bytes && (dbuf || whole) && my_tiles > 0) load_tile(0);
+        #pragma unroll 1
+                for (int i = 0; i < my_tiles; ++i) {
+                    const TileCoord tc = tile_coord<CTA2>(p, unit0 + i * ustride, rank);
+                    const int acc = i & 1;
+                    const int row0 = tc.mt * BM + quarter * 32;
+                    if (lane == 0 && side_bytes && whole && i > 0) {
+                        ptx::bulk_wait_read<0>();  // the previous tile's stores have read every slot
+                        load_tile(i);
+                    }
+                    ptx::mbar_wait(&tfull[acc], (i >> 1) & 1);
+                    ptx::tc_fence_after();
+        #pragma unroll 1
+                    for (int k = 0; k < kHalfChunks; ++k, ++seq) {
+                        const int c = c_begin + k;
+                        const int col0 = tc.nt * BN + c * 32;
+                        uint32_t slot;
+                        if (dbuf) slot = static_cast<uint32_t>((i & 1) * kHalfChunks + k);
+                        else if (whole) slot = static_cast<uint32_t>(k);
+                        else slot = seq % static_cast<uint32_t>(nslots);
+                        uint32_t v[32];
+                        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, v);
+                        ptx::tmem_ld_wait();
+                        if (lane == 0) {
+                            if (dbuf && k == kTrig && i + 1 < my_tiles) {
+                                // tile i - 1's stores (slots of tile i + 1) have long been read
+                                ptx::bulk_wait_read<kTrig>();
+                                load_tile(i + 1);
+                            } else if (side_bytes && !dbuf && !whole) {
+                                // ring of nslots chunk slots: refill the previous chunk's slot one lap ahead
+                                if (seq == 0) {
+                                    for (uint32_t s2 = 0; s2 < static_cast<uint32_t>(nslots); ++s2) {
+                                        const int qq = static_cast<int>(s2);
+                                        const int ti = qq / kHalfChunks;
+                                        if (ti >= my_tiles) break;
+                                        const TileCoord tq = tile_coord<CTA2>(p, unit0 + ti * ustride, rank);
+                                        const int c0 = tq.nt * BN + (c_begin + qq - ti * kHalfChunks) * 32;
+                                        ptx::mbar_arrive_expect_tx(&sbar[s2], side_bytes);
+                                        if constexpr (kRes)
+                                            ptx::tma_load_2d(ebuf_addr + s2 * sstride, &p.tmap_res, &sbar[s2], c0, tq.mt * BM + quarter * 32);
+                                        if constexpr (kMask)
+                                            ptx::tma_load_2d(ebuf_addr + s2 * sstride + mask_off, &p.tmap_mask, &sbar[s2], c0,
+                                                             tq.mt * BM + quarter * 32);
+                                    }
+                                } else {
+                                    const int qn = static_cast<int>(seq) - 1 + nslots;
+                                    const int ti = qn / kHalfChunks;
+                                    if (ti < my_tiles) {
+                                        ptx::bulk_wait_read<0>();
+                                        const uint32_t s2 = (seq - 1) % static_cast<uint32_t>(nslots);
+                                        const TileCoord tq = tile_coord<CTA2>(p, unit0 + ti * ustride, rank);
+                                        const int c0 = tq.nt * BN + (c_begin + qn - ti * kHalfChunks) * 32;
+                                        ptx::mbar_arrive_expect_tx(&sbar[s2], side_bytes);
+                                        if constexpr (kRes)
+                                            ptx::tma_load_2d(ebuf_addr + s2 * sstride, &p.tmap_res, &sbar[s2], c0, tq.mt * BM + quarter * 32);
+                                        if constexpr (kMask)
+                                            ptx::tma_load_2d(ebuf_addr + s2 * sstride + mask_off, &p.tmap_mask, &sbar[s2], c0,
+                                                             tq.mt * BM + quarter * 32);
+                                    }
+                                }
+                            }
+                        }
+                        uint8_t* b0 = ebuf + slot * sstride;
+                        __syncwarp();
+                        if (side_bytes) {
+                            const uint32_t ph = dbuf ? (i >> 1) & 1 : whole ? i & 1 : (seq / nslots) & 1;
+                            ptx::mbar_wait(&sbar[slot], ph);
+                        }
+                        if (col0 < ncol) {
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                float x[8];
+#pragma unroll
+                                for (int e = 0; e < 8; ++e) x[e] = __uint_as_float(v[8 * g + e]);
+                                const uint32_t off = lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4);
+                                if (p.bias) {
+                                    const int cb = col0 + 8 * g;
+#pragma unroll
+                                    for (int e = 0; e < 8; ++e)
+                                        if (cb + e < ncol) x[e] += __ldg(p.bias + cb + e);
+                                }
+                                if constexpr (kRes) {
+                                    float r[8];
+                                    unpack8(*reinterpret_cast<const uint4*>(b0 + off), r);
+#pragma unroll
+                                    for (int e = 0; e < 8; ++e) x[e] += r[e];
+                                }
+                                if constexpr (kRelu) {
+#pragma unroll
+                                    for (int e = 0; e < 8; ++e) x[e] = fmaxf(x[e], 0.f);
+                                }
+                                if constexpr (kMask) {
+                                    float mk[8];
+                                    unpack8(*reinterpret_cast<const uint4*>(b0 + mask_off + off), mk);
+#pragma unroll
+                                    for (int e = 0; e < 8; ++e) x[e] = mk[e] > 0.f ? x[e] : 0.f;
+                                }
+                                *reinterpret_cast<uint4*>(b0 + off) = pack8(x);
+                            }
+                            ptx::fence_proxy_async_smem();
+                        }
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (col0 < ncol) ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * sstride, col0, row0);
+                            ptx::bulk_commit();  // (an empty group keeps the read-wait counts in step)
+                        }
+                    }
+                    ptx::tc_fence_before();
+                    if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
+                    else ptx::mbar_arrive(&tempty[acc]);
+                }
+                if (lane == 0) ptx::bulk_wait<0>();
             }
         };
-        if (!side_bytes) {
-            // no side inputs: staging slots only hold outputs on their way to the TMA store
-            constexpr bool kWhole = EPI >= kHalfChunks;
-            const int c_end = c_begin + kHalfChunks;
-            uint32_t seq = 0;
-            int it = 0;
-            for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
-                const TileCoord tc = tile_coord<CTA2>(p, t, rank);
-                const int acc = it & 1;
-                const uint32_t acc_phase = (it >> 1) & 1;
-                const int row0 = tc.mt * BM + quarter * 32;
-                ptx::mbar_wait(&tfull[acc], acc_phase);
-                ptx::tc_fence_after();
-    #pragma unroll 1
-                for (int c = c_begin; c < c_end; ++c, ++seq) {
-                    const int col0 = tc.nt * BN + c * 32;
-                    uint32_t v[32];
-                    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                                acc * BN + c * 32,
-                                            v);
-                    ptx::tmem_ld_wait();
-                    const uint32_t slot = kWhole ? static_cast<uint32_t>(c - c_begin) : (seq & 1);
-                    uint8_t* b0 = ebuf + slot * 4096;  // (4 KB slot pitch as with two side inputs)
-                    if (lane == 0) {  // the store that last used this slot has read it
-                        if constexpr (kWhole) ptx::bulk_wait_read<kHalfChunks - 1>();
-                        else ptx::bulk_wait_read<1>();
-                    }
-                    __syncwarp();
-                    if (col0 < ncol) {
-#pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            float x[8];
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(v[8 * g + i]);
-                            const uint32_t off = lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4);
-                            if (p.bias) {
-                                const int cb = col0 + 8 * g;
-#pragma unroll
-                                for (int i = 0; i < 8; ++i)
-                                    if (cb + i < ncol) x[i] += __ldg(p.bias + cb + i);
-                            }
-                            if (p.relu) {
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) x[i] = fmaxf(x[i], 0.f);
-                            }
-                            *reinterpret_cast<uint4*>(b0 + off) = pack8(x);
-                        }
-                        ptx::fence_proxy_async_smem();
-                    }
-                    __syncwarp();
-                    if (lane == 0 && col0 < ncol) {
-                        ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * 4096, col0, row0);
-                        ptx::bulk_commit();
-                    }
-                }
-                ptx::tc_fence_before();
-                if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
-                else ptx::mbar_arrive(&tempty[acc]);
-            }
-            if (lane == 0) ptx::bulk_wait<0>();
-        } else {
-            uint32_t seq = 0;  // chunk sequence (ring mode)
-            if (lane == 0 && side_bytes && (dbuf || whole) && my_tiles > 0) load_tile(0);
-    #pragma unroll 1
-            for (int i = 0; i < my_tiles; ++i) {
-                const TileCoord tc = tile_coord<CTA2>(p, unit0 + i * ustride, rank);
-                const int acc = i & 1;
-                const int row0 = tc.mt * BM + quarter * 32;
-                if (lane == 0 && side_bytes && whole && i > 0) {
-                    ptx::bulk_wait_read<0>();  // the previous tile's stores have read every slot
-                    load_tile(i);
-                }
-                ptx::mbar_wait(&tfull[acc], (i >> 1) & 1);
-                ptx::tc_fence_after();
-    #pragma unroll 1
-                for (int k = 0; k < kHalfChunks; ++k, ++seq) {
-                    const int c = c_begin + k;
-                    const int col0 = tc.nt * BN + c * 32;
-                    uint32_t slot;
-                    if (dbuf) slot = static_cast<uint32_t>((i & 1) * kHalfChunks + k);
-                    else if (whole) slot = static_cast<uint32_t>(k);
-                    else slot = seq % static_cast<uint32_t>(nslots);
-                    uint32_t v[32];
-                    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, v);
-                    ptx::tmem_ld_wait();
-                    if (lane == 0) {
-                        if (dbuf && k == kTrig && i + 1 < my_tiles) {
-                            // tile i - 1's stores (slots of tile i + 1) have long been read
-                            ptx::bulk_wait_read<kTrig>();
-                            load_tile(i + 1);
-                        } else if (side_bytes && !dbuf && !whole) {
-                            // ring of nslots chunk slots: refill the previous chunk's slot one lap ahead
-                            if (seq == 0) {
-                                for (uint32_t s2 = 0; s2 < static_cast<uint32_t>(nslots); ++s2) {
-                                    const int qq = static_cast<int>(s2);
-                                    const int ti = qq / kHalfChunks;
-                                    if (ti >= my_tiles) break;
-                                    const TileCoord tq = tile_coord<CTA2>(p, unit0 + ti * ustride, rank);
-                                    const int c0 = tq.nt * BN + (c_begin + qq - ti * kHalfChunks) * 32;
-                                    ptx::mbar_arrive_expect_tx(&sbar[s2], side_bytes);
-                                    if (p.residual)
-                                        ptx::tma_load_2d(ebuf_addr + s2 * sstride, &p.tmap_res, &sbar[s2], c0, tq.mt * BM + quarter * 32);
-                                    if (p.mask)
-                                        ptx::tma_load_2d(ebuf_addr + s2 * sstride + mask_off, &p.tmap_mask, &sbar[s2], c0,
-                                                         tq.mt * BM + quarter * 32);
-                                }
-                            } else {
-                                const int qn = static_cast<int>(seq) - 1 + nslots;
-                                const int ti = qn / kHalfChunks;
-                                if (ti < my_tiles) {
-                                    ptx::bulk_wait_read<0>();
-                                    const uint32_t s2 = (seq - 1) % static_cast<uint32_t>(nslots);
-                                    const TileCoord tq = tile_coord<CTA2>(p, unit0 + ti * ustride, rank);
-                                    const int c0 = tq.nt * BN + (c_begin + qn - ti * kHalfChunks) * 32;
-                                    ptx::mbar_arrive_expect_tx(&sbar[s2], side_bytes);
-                                    if (p.residual)
-                                        ptx::tma_load_2d(ebuf_addr + s2 * sstride, &p.tmap_res, &sbar[s2], c0, tq.mt * BM + quarter * 32);
-                                    if (p.mask)
-                                        ptx::tma_load_2d(ebuf_addr + s2 * sstride + mask_off, &p.tmap_mask, &sbar[s2], c0,
-                                                         tq.mt * BM + quarter * 32);
-                                }
-                            }
-                        }
-                    }
-                    uint8_t* b0 = ebuf + slot * sstride;
-                    __syncwarp();
-                    if (side_bytes) {
-                        const uint32_t ph = dbuf ? (i >> 1) & 1 : whole ? i & 1 : (seq / nslots) & 1;
-                        ptx::mbar_wait(&sbar[slot], ph);
-                    }
-                    if (col0 < ncol) {
-#pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            float x[8];
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) x[e] = __uint_as_float(v[8 * g + e]);
-                            const uint32_t off = lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4);
-                            if (p.bias) {
-                                const int cb = col0 + 8 * g;
-#pragma unroll
-                                for (int e = 0; e < 8; ++e)
-                                    if (cb + e < ncol) x[e] += __ldg(p.bias + cb + e);
-                            }
-                            if (p.residual) {
-                                float r[8];
-                                unpack8(*reinterpret_cast<const uint4*>(b0 + off), r);
-#pragma unroll
-                                for (int e = 0; e < 8; ++e) x[e] += r[e];
-                            }
-                            if (p.relu) {
-#pragma unroll
-                                for (int e = 0; e < 8; ++e) x[e] = fmaxf(x[e], 0.f);
-                            }
-                            if (p.mask) {
-                                float mk[8];
-                                unpack8(*reinterpret_cast<const uint4*>(b0 + mask_off + off), mk);
-#pragma unroll
-                                for (int e = 0; e < 8; ++e) x[e] = mk[e] > 0.f ? x[e] : 0.f;
-                            }
-                            *reinterpret_cast<uint4*>(b0 + off) = pack8(x);
-                        }
-                        ptx::fence_proxy_async_smem();
-                    }
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (col0 < ncol) ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * sstride, col0, row0);
-                        ptx::bulk_commit();  // (an empty group keeps the read-wait counts in step)
-                    }
-                }
-                ptx::tc_fence_before();
-                if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
-                else ptx::mbar_arrive(&tempty[acc]);
-            }
-            if (lane == 0) ptx::bulk_wait<0>();
-        }
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        const bool hr = p.residual != nullptr, hm = p.mask != nullptr, hu = p.relu != 0;
+        if (hr && hm) { if (hu) run(T_{}, T_{}, T_{}); else run(T_{}, T_{}, F_{}); }
+        else if (hr) { if (hu) run(T_{}, F_{}, T_{}); else run(T_{}, F_{}, F_{}); }
+        else if (hm) { if (hu) run(F_{}, T_{}, T_{}); else run(F_{}, T_{}, F_{}); }
+        else { if (hu) run(F_{}, F_{}, T_{}); else run(F_{}, F_{}, F_{}); }
     } else {
         // ================================================= epilogue ======
         // Two warps per TMEM lane quarter (a warp may only touch lanes
