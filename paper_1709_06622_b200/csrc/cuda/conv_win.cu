@@ -103,17 +103,19 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
     return v;
 }
 
-// One 32-column accumulator chunk of one output row: fused epilogue + bf16 store.
+// One 32-column accumulator chunk of one output row: fused epilogue + bf16 store
+// (instantiated per bias / residual / ReLU / mask combination).
+template <bool kBias, bool kRes, bool kRelu, bool kMask>
 __device__ __forceinline__ void store_chunk(const WinParams& p, size_t orow, int col0, const uint32_t (&acc)[32]) {
     const size_t base = orow * p.Ncol + col0;
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + base;
     if (col0 + 32 <= p.Ncol) {
         uint4 rv[4], mv[4];
-        if (p.residual) {
+        if constexpr (kRes) {
 #pragma unroll
             for (int g = 0; g < 4; ++g) rv[g] = __ldg(reinterpret_cast<const uint4*>(p.residual + base) + g);
         }
-        if (p.mask) {
+        if constexpr (kMask) {
 #pragma unroll
             for (int g = 0; g < 4; ++g) mv[g] = __ldg(reinterpret_cast<const uint4*>(p.mask + base) + g);
         }
@@ -122,21 +124,21 @@ __device__ __forceinline__ void store_chunk(const WinParams& p, size_t orow, int
             float v[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(acc[8 * g + i]);
-            if (p.bias) {
+            if constexpr (kBias) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[i] += __ldg(p.bias + col0 + 8 * g + i);
             }
-            if (p.residual) {
+            if constexpr (kRes) {
                 float r[8];
                 unpack8(rv[g], r);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[i] += r[i];
             }
-            if (p.relu) {
+            if constexpr (kRelu) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
             }
-            if (p.mask) {
+            if constexpr (kMask) {
                 float mk[8];
                 unpack8(mv[g], mk);
 #pragma unroll
@@ -147,10 +149,10 @@ __device__ __forceinline__ void store_chunk(const WinParams& p, size_t orow, int
     } else {
         for (int i = 0; i < 32 && col0 + i < p.Ncol; ++i) {
             float x = __uint_as_float(acc[i]);
-            if (p.bias) x += p.bias[col0 + i];
-            if (p.residual) x += __bfloat162float(p.residual[base + i]);
-            if (p.relu) x = fmaxf(x, 0.f);
-            if (p.mask && !(__bfloat162float(p.mask[base + i]) > 0.f)) x = 0.f;
+            if constexpr (kBias) x += p.bias[col0 + i];
+            if constexpr (kRes) x += __bfloat162float(p.residual[base + i]);
+            if constexpr (kRelu) x = fmaxf(x, 0.f);
+            if (kMask && !(__bfloat162float(p.mask[base + i]) > 0.f)) x = 0.f;
             out[i] = __float2bfloat16_rn(x);
         }
     }
@@ -388,7 +390,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_kernel(const __grid_cons
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, v);
                 ptx::tmem_ld_wait();
                 const int col0 = t.nt * BN + c * 32;
-                if (valid && col0 < p.Ncol) store_chunk(p, orow, col0, v);
+                if (valid && col0 < p.Ncol) {
+                    const int f = (p.bias ? 1 : 0) | (p.residual ? 2 : 0) | (p.relu ? 4 : 0) | (p.mask ? 8 : 0);
+                    switch (f) {
+#define TCB_WIN_EPI(F) \
+    case F: store_chunk<(F & 1) != 0, (F & 2) != 0, (F & 4) != 0, (F & 8) != 0>(p, orow, col0, v); break;
+                        TCB_WIN_EPI(0) TCB_WIN_EPI(1) TCB_WIN_EPI(2) TCB_WIN_EPI(3)
+                        TCB_WIN_EPI(4) TCB_WIN_EPI(5) TCB_WIN_EPI(6) TCB_WIN_EPI(7)
+                        TCB_WIN_EPI(8) TCB_WIN_EPI(9) TCB_WIN_EPI(10) TCB_WIN_EPI(11)
+                        TCB_WIN_EPI(12) TCB_WIN_EPI(13) TCB_WIN_EPI(14) TCB_WIN_EPI(15)
+#undef TCB_WIN_EPI
+                    }
+                }
             }
             ptx::tc_fence_before();
             if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
