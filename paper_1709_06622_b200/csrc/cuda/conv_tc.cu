@@ -263,24 +263,30 @@ struct SideIn {
     uint4 k[4];
 };
 
+// Flag templates: kX = the side input / option is present; kDyn = decide at run
+// time instead (the general instantiation).
+template <bool kRes, bool kMask, bool kDyn = false>
 __device__ __forceinline__ void load_side(const Params& p, size_t row, int col0, bool valid,
                                           SideIn& f) {
+    const bool has_res = kDyn ? p.residual != nullptr : kRes, has_mask = kDyn ? p.mask != nullptr : kMask;
     if (!valid || col0 + 32 > p.s.Ncol) return;  // tail chunks take the scalar path
     const size_t base = row * p.s.Ncol + col0;
-    if (p.residual) {
+    if (has_res) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) f.r[g] = __ldg(reinterpret_cast<const uint4*>(p.residual + base) + g);
     }
-    if (p.mask) {
+    if (has_mask) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) f.k[g] = __ldg(reinterpret_cast<const uint4*>(p.mask + base) + g);
     }
 }
 
-template <ConvMode MODE>
+template <ConvMode MODE, bool kBias, bool kRes, bool kRelu, bool kMask, bool kDyn = false>
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord& tc, int m,
                                                size_t row, int col0, const uint32_t (&acc)[32],
                                                const SideIn& side) {
+    const bool has_bias = kDyn ? p.bias != nullptr : kBias, has_res = kDyn ? p.residual != nullptr : kRes;
+    const bool has_relu = kDyn ? p.relu != 0 : kRelu, has_mask = kDyn ? p.mask != nullptr : kMask;
     const ConvShape& s = p.s;
     if (m >= s.M || col0 >= s.Ncol) return;
     if constexpr (MODE == ConvMode::Wgrad) {
@@ -306,21 +312,21 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
             for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(acc[8 * g + i]);
             const int c = col0 + 8 * g;
             if (full) {
-                if (p.bias) {
+                if (has_bias) {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) v[i] += __ldg(p.bias + c + i);
                 }
-                if (p.residual) {
+                if (has_res) {
                     float r[8];
                     unpack8(side.r[g], r);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) v[i] += r[i];
                 }
-                if (p.relu) {
+                if (has_relu) {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
                 }
-                if (p.mask) {
+                if (has_mask) {
                     float mk[8];
                     unpack8(side.k[g], mk);
 #pragma unroll
@@ -330,10 +336,10 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
             } else {
                 for (int i = 0; i < 8 && c + i < s.Ncol; ++i) {
                     float x = v[i];
-                    if (p.bias) x += p.bias[c + i];
-                    if (p.residual) x += __bfloat162float(p.residual[base + 8 * g + i]);
-                    if (p.relu) x = fmaxf(x, 0.f);
-                    if (p.mask && !(__bfloat162float(p.mask[base + 8 * g + i]) > 0.f)) x = 0.f;
+                    if (has_bias) x += p.bias[c + i];
+                    if (has_res) x += __bfloat162float(p.residual[base + 8 * g + i]);
+                    if (has_relu) x = fmaxf(x, 0.f);
+                    if (has_mask && !(__bfloat162float(p.mask[base + 8 * g + i]) > 0.f)) x = 0.f;
                     out[8 * g + i] = __float2bfloat16_rn(x);
                 }
             }
@@ -974,39 +980,60 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         constexpr int kChunks = BN / 32, kHalfChunks = kChunks / 2;
         const int c_begin = half * kHalfChunks, c_end = c_begin + kHalfChunks;
         const int row = quarter * 32 + (tid & 31);
-        int it = 0;
-        for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
-            const TileCoord tc = tile_coord<CTA2>(p, t, rank);
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            const int m = tc.mt * BM + row;
-            const bool mvalid = m < p.s.M;
-            const size_t orow = mvalid ? out_row<MODE>(p, m) : 0;
-            // first chunk's residual / mask loads are in flight while the MMAs finish
-            SideIn cur{}, nxt{};
-            if constexpr (MODE != ConvMode::Wgrad)
-                load_side(p, orow, tc.nt * BN + c_begin * 32, mvalid, cur);
-            ptx::mbar_wait(&tfull[acc], acc_phase);
-            ptx::tc_fence_after();
+        auto run = [&](auto bias_c, auto res_c, auto relu_c, auto mask_c, auto dyn_c) {
+            constexpr bool kBias = decltype(bias_c)::value, kRes = decltype(res_c)::value;
+            constexpr bool kRelu = decltype(relu_c)::value, kMask = decltype(mask_c)::value;
+            constexpr bool kDyn = decltype(dyn_c)::value;
+            int it = 0;
+            for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
+                const TileCoord tc = tile_coord<CTA2>(p, t, rank);
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                const int m = tc.mt * BM + row;
+                const bool mvalid = m < p.s.M;
+                const size_t orow = mvalid ? out_row<MODE>(p, m) : 0;
+                // first chunk's residual / mask loads are in flight while the MMAs finish
+                SideIn cur{}, nxt{};
+                if constexpr (MODE != ConvMode::Wgrad)
+                    load_side<kRes, kMask, kDyn>(p, orow, tc.nt * BN + c_begin * 32, mvalid, cur);
+                ptx::mbar_wait(&tfull[acc], acc_phase);
+                ptx::tc_fence_after();
 #pragma unroll 1
-            for (int c = c_begin; c < c_end; ++c) {
-                if constexpr (MODE != ConvMode::Wgrad) {
-                    if (c + 1 < c_end) load_side(p, orow, tc.nt * BN + (c + 1) * 32, mvalid, nxt);
+                for (int c = c_begin; c < c_end; ++c) {
+                    if constexpr (MODE != ConvMode::Wgrad) {
+                        if (c + 1 < c_end) load_side<kRes, kMask, kDyn>(p, orow, tc.nt * BN + (c + 1) * 32, mvalid, nxt);
+                    }
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                                acc * BN + c * 32,
+                                            v);
+                    ptx::tmem_ld_wait();
+                    epilogue_chunk<MODE, kBias, kRes, kRelu, kMask, kDyn>(p, tc, m, orow, tc.nt * BN + c * 32, v, cur);
+                    cur = nxt;
                 }
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                            acc * BN + c * 32,
-                                        v);
-                ptx::tmem_ld_wait();
-                epilogue_chunk<MODE>(p, tc, m, orow, tc.nt * BN + c * 32, v, cur);
-                cur = nxt;
+                ptx::tc_fence_before();
+                if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
+                else ptx::mbar_arrive(&tempty[acc]);
+                if constexpr (MODE == ConvMode::Wgrad) {
+                    if (p.counters) split_reduce_tile<BN>(p, tc, tid - kProducerThreads);
+                }
             }
-            ptx::tc_fence_before();
-            if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
-            else ptx::mbar_arrive(&tempty[acc]);
-            if constexpr (MODE == ConvMode::Wgrad) {
-                if (p.counters) split_reduce_tile<BN>(p, tc, tid - kProducerThreads);
-            }
+        };
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        if constexpr (MODE == ConvMode::Wgrad) {
+            run(F_{}, F_{}, F_{}, F_{}, F_{});
+        } else {
+            // one instantiation per side-input / ReLU combination the executor issues; bias
+            // (fc layers, from_net convs) takes the run-time-checked general one
+            const int f = (p.residual ? 1 : 0) | (p.relu ? 2 : 0) | (p.mask ? 4 : 0);
+            if (p.bias) run(F_{}, F_{}, F_{}, F_{}, T_{});
+            else if (f == 0) run(F_{}, F_{}, F_{}, F_{}, F_{});
+            else if (f == 2) run(F_{}, F_{}, T_{}, F_{}, F_{});
+            else if (f == 3) run(F_{}, T_{}, T_{}, F_{}, F_{});
+            else if (f == 4) run(F_{}, F_{}, F_{}, T_{}, F_{});
+            else if (f == 5) run(F_{}, T_{}, F_{}, T_{}, F_{});
+            else run(F_{}, F_{}, F_{}, F_{}, T_{});
         }
     }
 

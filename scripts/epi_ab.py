@@ -18,6 +18,12 @@ CASES = [  # name, n, h, w, c, k, r, pad, stride
     ("s2_c1_1x1_512_128", 256, 28, 28, 512, 128, 1, 0, 1),
     ("s3_c3_1x1_256_1024", 256, 14, 14, 256, 1024, 1, 0, 1),
 ]
+REG_CASES = [  # K-heavy passes (register epilogue)
+    ("s3_c2_3x3_256", 256, 14, 14, 256, 256, 3, 1, 1),
+    ("s4_c2_3x3_512", 256, 7, 7, 512, 512, 3, 1, 1),
+    ("s4_c1_1x1_2048_512", 256, 7, 7, 2048, 512, 1, 0, 1),
+    ("s3_c1_1x1_1024_256", 256, 14, 14, 1024, 256, 1, 0, 1),
+]
 
 
 def timeit(fn, iters):
@@ -36,9 +42,10 @@ def timeit(fn, iters):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--set", default="epi", choices=["epi", "reg"])
     a = ap.parse_args()
     out = {}
-    for name, n, h, w, c, k, r, pad, st in CASES:
+    for name, n, h, w, c, k, r, pad, st in (CASES if a.set == "epi" else REG_CASES):
         g = device.geom(n, h, w, c, k, r, pad=pad, stride=st)
         plan = device.ConvPlan(g, "gemm", "bf16")
         x = torch.randn(n, h, w, c, device="cuda").bfloat16()
