@@ -439,7 +439,8 @@ def in_step_roofline(rows, pk, precision, model="resnet50", batch=256, kernels=N
 
 
 # ------------------------------------------- kernels inside the graph step ---
-CONV_KERNEL = {"bf16": ("conv_tc_kernel", "conv_win_kernel"), "tf32": ("conv_tf32_kernel",),
+CONV_KERNEL = {"bf16": ("conv_tc_kernel", "conv_win_kernel", "conv_win_wgrad_kernel", "conv_stem_fwd_kernel",
+                        "conv_stem_wgrad_kernel"), "tf32": ("conv_tf32_kernel",),
                "ffma": ("conv_ffma_kernel",)}
 
 

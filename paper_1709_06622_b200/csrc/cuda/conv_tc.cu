@@ -1646,6 +1646,7 @@ cudaError_t conv_tc_dgrad(const ConvGeom& g, const void* dy, const void* w, cons
             p.mask = static_cast<const __nv_bfloat16*>(ep.mask);
             cudaError_t e;
             if (p.s.Kdim == 0) {
+                if (ep.uncovered_zero && !ep.residual && !ep.mask) continue;
                 const size_t total = size_t(p.s.M) * (p.s.Ncol / 8);
                 const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 8192));
                 e = launch_pdl(dgrad_empty_phase_kernel, dim3(blocks), dim3(256), 0, st, p);

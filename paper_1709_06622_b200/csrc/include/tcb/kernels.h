@@ -29,6 +29,10 @@ struct Epilogue {
     const void* residual = nullptr;  // same dtype/shape as the output, added before act
     const void* mask = nullptr;      // dgrad: multiply by [mask > 0]
     bool relu = false;               // fwd: max(0, .)
+    // dgrad: dx pixels no filter tap reaches (stride phases without taps, e.g. the
+    // odd pixels of a 1x1 stride-2 conv) already hold 0 -- skip writing them
+    // (only without residual / mask)
+    bool uncovered_zero = false;
 };
 
 // ---- tensor-core implicit GEMM (tcgen05 / TMEM), bf16 in, fp32 accumulate ----

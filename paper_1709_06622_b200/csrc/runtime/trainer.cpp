@@ -780,6 +780,12 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
 
     // extra contributions to fold in: at the final writer every other one; a
     // chained contribution adds the running sum of the chain (in place)
+    // first (and only) chained contribution into a chain buffer nothing else writes
+    // before the final writer reads it: pixels this conv's taps never reach keep the
+    // zeros of the arena's initial memset across steps (the strided projection's
+    // empty dgrad phases need no zero pass)
+    const bool sole_chained = chained && tgt.acc_written == 0 && tgt.chain.size() == 1 && tgt.tmp.empty() &&
+                              tgt.alias_from.empty();
     std::vector<const void*> extras;
     if (final) {
         if (!tgt.chain.empty()) extras.push_back(t->at(tgt.acc));
@@ -805,6 +811,7 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         Epilogue ep;
         ep.residual = residual;
         ep.mask = mask_needed ? t->at(tgt.act) : nullptr;
+        ep.uncovered_zero = sole_chained && !residual && !ep.mask;
         const void* cw = t->bf16 ? static_cast<const void*>(static_cast<__nv_bfloat16*>(t->wc_ptr()) + con.woff)
                                  : static_cast<const void*>(t->at<float>(t->off_param) + con.woff);
         // a fully connected layer (filter = whole unpadded input map, 1x1 output) runs

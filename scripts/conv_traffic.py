@@ -27,7 +27,8 @@ for r in rows:
     v = float(d["Metric Value"].replace(",", "")) * SCALE.get(d["Metric Unit"], 1.0)
     per[d["ID"]]["name"] = d["Kernel Name"]
     per[d["ID"]][d["Metric Name"]] = v
-conv = [p for p in per.values() if "conv_tc_kernel" in p["name"]]
+CONV = ("conv_tc_kernel", "conv_win_kernel", "conv_win_wgrad_kernel", "conv_stem_fwd_kernel", "conv_stem_wgrad_kernel")
+conv = [p for p in per.values() if any(k in p["name"] for k in CONV)]
 allk = list(per.values())
 tot = lambda ks, m: sum(k.get(m, 0.0) for k in ks)
 out = {
