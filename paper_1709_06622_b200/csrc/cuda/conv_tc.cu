@@ -1420,6 +1420,23 @@ cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, c
                 return e ? atoi(e) : 2;
             }();
             const bool deep = (p.s.Kdim + BK - 1) / BK <= deep_kb;
+            // CTA pairs keep the TMA epilogue ($TCB_CTA2_EPI: 1 pair + TMA epilogue (default),
+            // 0 pairs take the register epilogue, -1 no pairs for TMA-epilogue layers)
+            static const int cta2_epi = [] {
+                const char* e = getenv("TCB_CTA2_EPI");
+                return e ? atoi(e) : 1;
+            }();
+            if constexpr (LOAD == kPlain || LOAD == kIm2col) {
+                if (cta2_epi >= 0 && (bn == 128 || bn == 256) &&
+                    cta2_wanted(LOAD, bn, (p.s.M + BM - 1) / BM, (p.s.Kdim + BK - 1) / BK)) {
+                    if (cta2_epi == 0) {
+                        if (bn == 256) return launch<MODE, 256, LOAD, 0, true>(p, a_matrix, b_matrix, st);
+                        return launch<MODE, 128, LOAD, 0, true>(p, a_matrix, b_matrix, st);
+                    }
+                    if (bn == 256) return launch<MODE, 256, LOAD, 2, true>(p, a_matrix, b_matrix, st);
+                    return launch<MODE, 128, LOAD, 2, true>(p, a_matrix, b_matrix, st);
+                }
+            }
             switch (bn) {
                 case 256:
                     return deep ? launch<MODE, 256, LOAD, 4>(p, a_matrix, b_matrix, st)
