@@ -702,10 +702,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_wgrad_kernel(const __gri
                 const int q0 = 2 * mt, q1 = min(2 * mt + 1, p.nq - 1);
                 const uint32_t a0 = qaddr(q0);
                 const uint64_t ad0 = ptx::sw128_desc(a0, qaddr(q1) - a0, 1024);
-#pragma unroll 4
-                for (int ks = 0; ks < kWP / 16; ++ks)
-                    ptx::umma_f16_elect(tmem + mt * BN, ad0 + ks * 128, bd0 + ks * 128, idesc,
-                                        (kb > kb0 || ks > 0) ? 1u : 0u);
+                const uint32_t first = kb > kb0 ? 1u : 0u;
+                ptx::umma_f16_elect(tmem + mt * BN, ad0, bd0, idesc, first);
+#pragma unroll
+                for (int ks = 1; ks < kWP / 16; ++ks)  // compile-time descriptor offsets
+                    ptx::umma_f16_elect(tmem + mt * BN, ad0 + ks * 128, bd0 + ks * 128, idesc, 1u);
             }
             ptx::umma_commit_elect(&empty[st]);
             if (++st == p.stages) {
