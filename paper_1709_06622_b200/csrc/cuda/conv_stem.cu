@@ -71,8 +71,8 @@ struct StemParams {
     int relu;
     int dbg;              // diagnostics ($TCB_STEM_DBG): 1 no MMA, 2 no output stores, 4 no x loads
     // wgrad
-    int mtiles, tiles_per_cta, dy_boxes;
-    uint32_t dy_box_bytes;
+    int mtiles, tiles_per_cta, dy_boxes, tr;  // tr: output rows per weight-gradient tile (1 or 2)
+    uint32_t dy_box_bytes, xslots;
     float* partial;  // [grid][T*32][K]
     FastDiv d_wtiles, d_ho;
 };
@@ -86,6 +86,13 @@ __device__ __forceinline__ Tile tile_of(const StemParams& p, int u) {
     p.d_wtiles.divmod(static_cast<uint32_t>(u), row, wt);
     p.d_ho.divmod(row, n, ho);
     return Tile{static_cast<int>(n), static_cast<int>(ho), static_cast<int>(wt) * p.BW};
+}
+
+// weight-gradient tile of tr whole output rows (one width tile per row)
+__device__ __forceinline__ Tile row_tile(const StemParams& p, int u) {
+    uint32_t n, ho;
+    p.d_ho.divmod(static_cast<uint32_t>(u * p.tr), n, ho);
+    return Tile{static_cast<int>(n), static_cast<int>(ho), 0};
 }
 
 __device__ __forceinline__ void load_x(const StemParams& p, uint32_t dst, uint64_t* bar, const Tile& t) {
@@ -314,21 +321,29 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_wgrad_kernel(const __gr
     ptx::griddep_wait();
     ptx::griddep_launch_dependents();
     const uint32_t sbase = ptx::smem_addr(smem);
-    const uint32_t xslots = static_cast<uint32_t>(p.mtiles) * 4 * p.box_bytes;
+    const uint32_t xslots = p.xslots;
 
     if (warp == 0) {
         if (tid == 0) {  // ---------------------------------------- producer
             int st = 0;
             uint32_t ph = 0;
             for (int u = u0; u < u1; ++u) {
-                const Tile t = tile_of(p, u);
+                const Tile t = p.tr == 1 ? tile_of(p, u) : row_tile(p, u);
                 ptx::mbar_wait(&empty[st], ph ^ 1);
-                ptx::mbar_arrive_expect_tx(&full[st], p.T * p.box_bytes + p.dy_boxes * p.dy_box_bytes);
+                const int nbox = p.tr == 1 ? p.T : p.T + p.sh * (p.tr - 1);
+                ptx::mbar_arrive_expect_tx(&full[st], nbox * p.box_bytes + p.tr * p.dy_boxes * p.dy_box_bytes);
                 const uint32_t base = sbase + st * p.stage_bytes;
-                load_x(p, base, &full[st], t);
-                for (int j = 0; j < p.dy_boxes; ++j)
-                    ptx::tma_load_3d(base + xslots + j * p.dy_box_bytes, &p.tmap_b, &full[st], j * 64, t.wo0,
-                                     t.n * p.Ho + t.ho);
+                if (p.tr == 1) {
+                    load_x(p, base, &full[st], t);
+                } else {  // nq = 1: the R + sh (tr - 1) input rows the tile's output rows share
+                    const int h0 = t.ho * p.sh - p.pad_h;
+                    for (int c = 0; c < nbox; ++c)
+                        ptx::tma_load_4d(base + c * p.box_bytes, &p.tmap_x, &full[st], 0, t.wo0, h0 + c, t.n);
+                }
+                for (int r = 0; r < p.tr; ++r)
+                    for (int j = 0; j < p.dy_boxes; ++j)
+                        ptx::tma_load_3d(base + xslots + (r * p.dy_boxes + j) * p.dy_box_bytes, &p.tmap_b,
+                                         &full[st], j * 64, t.wo0, t.n * p.Ho + t.ho + r);
                 if (++st == p.stages) {
                     st = 0;
                     ph ^= 1;
@@ -347,13 +362,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_wgrad_kernel(const __gr
             ptx::mbar_wait(&full[st], ph);
             ptx::tc_fence_after();
             const uint32_t base = sbase + st * p.stage_bytes;
-            const uint64_t bd0 = kDy128 ? ptx::sw128_desc(base + xslots, p.dy_box_bytes, 8 * kDyRow)
-                                        : sw64_desc(base + xslots, p.dy_box_bytes, 8 * kDyRow);
-            for (int mt = 0; mt < p.mtiles; ++mt) {
-                const uint64_t ad0 = sw64_desc(base + mt * 4 * p.box_bytes, p.box_bytes, 512);
-                for (int ks = 0; ks < ksteps; ++ks)
-                    ptx::umma_f16_elect(tmem + mt * BN, ad0 + ks * 64, bd0 + ks * (16 * kDyRow >> 4), idesc,
-                                        (u > u0 || ks > 0) ? 1u : 0u);
+            for (int r = 0; r < p.tr; ++r) {  // output row r of the tile: input rows from box sh * r
+                const uint32_t dyb = base + xslots + r * p.dy_boxes * p.dy_box_bytes;
+                const uint64_t bd0 = kDy128 ? ptx::sw128_desc(dyb, p.dy_box_bytes, 8 * kDyRow)
+                                            : sw64_desc(dyb, p.dy_box_bytes, 8 * kDyRow);
+                for (int mt = 0; mt < p.mtiles; ++mt) {
+                    const uint64_t ad0 = sw64_desc(base + (r * p.sh + mt * 4) * p.box_bytes, p.box_bytes, 512);
+                    const uint32_t acc0 = (u > u0 || r > 0) ? 1u : 0u;
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks) {  // compile-time descriptor offsets, BW / 16 <= 8 steps
+                        if (ks >= ksteps) break;
+                        ptx::umma_f16_elect(tmem + mt * BN, ad0 + ks * 64, bd0 + ks * (16 * kDyRow >> 4), idesc,
+                                            ks > 0 ? 1u : acc0);
+                    }
+                }
             }
             ptx::umma_commit_elect(&empty[st]);
             if (++st == p.stages) {
@@ -488,8 +510,8 @@ struct StemPlan {
     int stages, G, g_step;
     size_t smem, x4_bytes, wp_bytes;
     // wgrad
-    int mtiles, dy_boxes, grid_wg, tiles_per_cta, wg_stages;
-    uint32_t dy_box_bytes, wg_stage_bytes;
+    int mtiles, dy_boxes, grid_wg, tiles_per_cta, wg_stages, tr, wg_tiles;
+    uint32_t dy_box_bytes, wg_stage_bytes, xslots;
     size_t wg_smem, partial_bytes;
 };
 
@@ -550,14 +572,22 @@ StemPlan stem_plan(const ConvGeom& g) {
     if (q.mtiles * g.k > 512 || (g.k != 32 && g.k % 64 != 0)) return q;
     q.dy_boxes = g.k >= 64 ? g.k / 64 : 1;
     q.dy_box_bytes = static_cast<uint32_t>(q.BW) * (g.k >= 64 ? 128 : 64);
-    q.wg_stage_bytes = (q.mtiles * 4 * q.box_bytes + q.dy_boxes * q.dy_box_bytes + 1023) / 1024 * 1024;
-    for (q.wg_stages = kMaxStages; q.wg_stages >= 2; --q.wg_stages)
-        if (size_t(q.wg_stages) * q.wg_stage_bytes + 1024 <= kSmemCap) break;
-    if (q.wg_stages < 2) return q;
+    // two output rows per tile share R - stride of their R input rows: 9 boxes instead of 14 for
+    // the ResNet stem ($TCB_STEM_WG_ROWS=1 keeps one row per tile)
+    static const int env_rows = [] { const char* e = getenv("TCB_STEM_WG_ROWS"); return e ? atoi(e) : 2; }();
+    for (q.tr = (env_rows >= 2 && q.wtiles == 1 && q.nq == 1 && q.Ho % 2 == 0) ? 2 : 1; q.tr >= 1; --q.tr) {
+        q.xslots = static_cast<uint32_t>(q.mtiles * 4 + g.stride_h * (q.tr - 1)) * q.box_bytes;
+        q.wg_stage_bytes = (q.xslots + q.tr * q.dy_boxes * q.dy_box_bytes + 1023) / 1024 * 1024;
+        for (q.wg_stages = kMaxStages; q.wg_stages >= 2; --q.wg_stages)
+            if (size_t(q.wg_stages) * q.wg_stage_bytes + 1024 <= kSmemCap) break;
+        if (q.wg_stages >= 2) break;
+    }
+    if (q.tr < 1) return q;
     q.wg_smem = size_t(q.wg_stages) * q.wg_stage_bytes + 1024;
-    q.grid_wg = std::min(q.tiles, num_sms());
-    q.tiles_per_cta = (q.tiles + q.grid_wg - 1) / q.grid_wg;
-    q.grid_wg = (q.tiles + q.tiles_per_cta - 1) / q.tiles_per_cta;
+    q.wg_tiles = q.tiles / q.tr;
+    q.grid_wg = std::min(q.wg_tiles, num_sms());
+    q.tiles_per_cta = (q.wg_tiles + q.grid_wg - 1) / q.grid_wg;
+    q.grid_wg = (q.wg_tiles + q.tiles_per_cta - 1) / q.tiles_per_cta;
     q.partial_bytes = size_t(q.grid_wg) * q.T * 32 * g.k * sizeof(float);
     q.use = true;
     return q;
@@ -734,6 +764,9 @@ cudaError_t conv_stem_wgrad(const ConvGeom& g, const void* dy, const void* x, fl
     p.tiles_per_cta = q.tiles_per_cta;
     p.dy_boxes = q.dy_boxes;
     p.dy_box_bytes = q.dy_box_bytes;
+    p.tr = q.tr;
+    p.xslots = q.xslots;
+    p.tiles = q.wg_tiles;
     p.partial = part;
     conv_tc_note_launch(ConvTcLaunchInfo{2, 5, g.k, 0, 0, q.grid_wg, q.tiles, q.grid_wg, 0, 0});
     switch (g.k) {
