@@ -1549,7 +1549,7 @@ int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool cou
     if (mode == ConvMode::Fwd) return q.use ? 3 : 1;
     if (mode == ConvMode::Dgrad) return g.stride_h * g.stride_w;
     const ConvGeom& gw = q.use ? q.g1 : g;
-    if (!q.use && !force_gather() && conv_win_wgrad_applies(g)) return 2;  // window kernel + split reduction
+    if (!q.use && !force_gather() && conv_win_wgrad_applies(g)) return conv_win_wgrad_launches(g);
     const ConvShape s = make_shape(gw, mode);
     const int bn = wgrad_bn(s);
     const bool pair = wgrad_pair(s, bn);

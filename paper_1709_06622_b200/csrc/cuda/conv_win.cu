@@ -618,6 +618,7 @@ struct WgParams {
     int n_img, Ho, Wo, pad_h, pad_w, R, S, C, K;
     int Wp, kb_img, kb_total, kb_per_cta;
     int slices, kslices, nq, mtiles;
+    int mt0, mt1;  // the M tiles (tap-slice pairs) this launch accumulates (tap groups)
     uint32_t xwin_bytes, dywin_bytes, stage_bytes;  // smem strides (1 KB aligned)
     uint32_t tx_bytes;                              // bytes the TMA boxes of one stage deliver
     int stages;
@@ -698,15 +699,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_wgrad_kernel(const __gri
                 const int ti = t / p.S, tj = t - ti * p.S;
                 return base + cs * p.xwin_bytes + (off0 + ti * p.Wp + tj) * 128;
             };
-            for (int mt = 0; mt < p.mtiles; ++mt) {
+            for (int mt = p.mt0; mt < p.mt1; ++mt) {
                 const int q0 = 2 * mt, q1 = min(2 * mt + 1, p.nq - 1);
                 const uint32_t a0 = qaddr(q0);
                 const uint64_t ad0 = ptx::sw128_desc(a0, qaddr(q1) - a0, 1024);
                 const uint32_t first = kb > kb0 ? 1u : 0u;
-                ptx::umma_f16_elect(tmem + mt * BN, ad0, bd0, idesc, first);
+                ptx::umma_f16_elect(tmem + (mt - p.mt0) * BN, ad0, bd0, idesc, first);
 #pragma unroll
                 for (int ks = 1; ks < kWP / 16; ++ks)  // compile-time descriptor offsets
-                    ptx::umma_f16_elect(tmem + mt * BN, ad0 + ks * 128, bd0 + ks * 128, idesc, 1u);
+                    ptx::umma_f16_elect(tmem + (mt - p.mt0) * BN, ad0 + ks * 128, bd0 + ks * 128, idesc, 1u);
             }
             ptx::umma_commit_elect(&empty[st]);
             if (++st == p.stages) {
@@ -725,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_wgrad_kernel(const __gri
             ptx::mbar_wait(&done, 0);
             ptx::tc_fence_after();
         }
-        for (int mt = 0; mt < p.mtiles; ++mt) {
+        for (int mt = p.mt0; mt < p.mt1; ++mt) {
             const int blk = m >> 6, q = 2 * mt + blk;
             const bool live = q < p.nq && !(blk == 1 && 2 * mt + 1 >= p.nq);
             const int cs = q / taps, t = q - cs * taps, c = cs * 64 + (m & 63);
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_wgrad_kernel(const __gri
             for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
                 uint32_t v[32];
                 if (any) {
-                    ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + mt * BN + c0, v);
+                    ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + (mt - p.mt0) * BN + c0, v);
                     ptx::tmem_ld_wait();
                 }
                 if (!live) continue;
@@ -752,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_wgrad_kernel(const __gri
 
 struct WgPlan {
     bool use = false;
-    int Wp, WRx, WRd, slices, kslices, nq, mtiles, bn, kb_img, kb_total, grid, kb_per_cta, stages;
+    int Wp, WRx, WRd, slices, kslices, nq, mtiles, bn, kb_img, kb_total, grid, kb_per_cta, stages, groups, per_group;
     uint32_t xwin, dywin, stage, tx;
     size_t smem, partial_bytes;
 };
@@ -767,10 +768,17 @@ WgPlan wgrad_plan(const ConvGeom& g) {
     q.slices = g.c / 64;
     q.kslices = g.k / 64;
     q.bn = g.k;
-    if (q.bn != 64 && g_win_mode != 2) return q;  // default: where the im2col path has 64-row tiles
+    // default: where the im2col path has 64-row tiles (K = 64). (K = 128 as three tap groups
+    // measured 172 us against 100 us for the im2col path on ResNet stage 2: $TCB_WIN=2 only.)
+    if (q.bn != 64 && g_win_mode != 2) return q;
     q.nq = g.r * g.s * q.slices;
     q.mtiles = (q.nq + 1) / 2;
-    if (q.bn > 256 || q.mtiles * q.bn > 512) return q;
+    if (q.bn > 256) return q;
+    // M tiles beyond 512 TMEM columns run as tap groups: one launch per group over the same
+    // windows (balanced: ceil(mtiles / groups) tiles each)
+    q.groups = (q.mtiles * q.bn + 511) / 512;
+    q.per_group = (q.mtiles + q.groups - 1) / q.groups;
+    if (q.groups > 3) return q;
     q.WRx = (q.Wp - 1 + kWP - 1 + (g.r - 1) * q.Wp + g.s - 1) / q.Wp + 1;
     q.WRd = (q.Wp - 1 + kWP - 1) / q.Wp + 1;
     if (q.WRx > 256) return q;
@@ -802,6 +810,7 @@ cudaError_t launch_wgrad(const WgParams& p, const WgPlan& q, cudaStream_t st) {
 }  // namespace
 
 bool conv_win_wgrad_applies(const ConvGeom& g) { return wgrad_plan(g).use; }
+int conv_win_wgrad_launches(const ConvGeom& g) { return wgrad_plan(g).groups + 1; }
 
 size_t conv_win_wgrad_workspace(const ConvGeom& g) {
     const WgPlan q = wgrad_plan(g);
@@ -832,6 +841,8 @@ cudaError_t conv_win_wgrad(const ConvGeom& g, const void* dy, const void* x, flo
     p.kslices = q.kslices;
     p.nq = q.nq;
     p.mtiles = q.mtiles;
+    p.mt0 = 0;
+    p.mt1 = q.mtiles;
     p.xwin_bytes = q.xwin;
     p.dywin_bytes = q.dywin;
     p.stage_bytes = q.stage;
@@ -841,13 +852,17 @@ cudaError_t conv_win_wgrad(const ConvGeom& g, const void* dy, const void* x, flo
     p.d_wp = FastDiv(static_cast<uint32_t>(q.Wp));
     p.d_kbimg = FastDiv(static_cast<uint32_t>(q.kb_img));
     conv_tc_note_launch(ConvTcLaunchInfo{2, 4, q.bn, 0, 0, q.grid, q.kb_total, q.grid, 0, 0});
-    cudaError_t e;
-    switch (q.bn) {
-        case 64: e = launch_wgrad<64>(p, q, st); break;
-        case 128: e = launch_wgrad<128>(p, q, st); break;
-        case 192: e = launch_wgrad<192>(p, q, st); break;
-        case 256: e = launch_wgrad<256>(p, q, st); break;
-        default: return cudaErrorInvalidValue;
+    cudaError_t e = cudaSuccess;
+    for (int gi = 0; gi < q.groups && e == cudaSuccess; ++gi) {
+        p.mt0 = gi * q.per_group;
+        p.mt1 = std::min(q.mtiles, p.mt0 + q.per_group);
+        switch (q.bn) {
+            case 64: e = launch_wgrad<64>(p, q, st); break;
+            case 128: e = launch_wgrad<128>(p, q, st); break;
+            case 192: e = launch_wgrad<192>(p, q, st); break;
+            case 256: e = launch_wgrad<256>(p, q, st); break;
+            default: return cudaErrorInvalidValue;
+        }
     }
     if (e != cudaSuccess) return e;
     return split_reduce(static_cast<const float*>(workspace), q.grid, size_t(g.k) * g.r * g.s * g.c, dw, st);

@@ -98,6 +98,7 @@ void conv_win_set_mode(int on);  // 0 off, 1 on (N = 64 tiles), 2 all applicable
 // <= 512 TMEM columns): per-CTA fp32 partials in `workspace`, then a split reduction.
 bool conv_win_wgrad_applies(const ConvGeom& g);
 size_t conv_win_wgrad_workspace(const ConvGeom& g);
+int conv_win_wgrad_launches(const ConvGeom& g);  // tap-group launches + the split reduction
 cudaError_t conv_win_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw, void* workspace,
                            cudaStream_t st);
 void conv_win_set_debug(void* buf);
