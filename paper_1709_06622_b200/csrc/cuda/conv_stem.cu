@@ -130,7 +130,10 @@ __device__ __forceinline__ uint32_t stg_off(int m, int j, int row_bytes) {
     return row_bytes == 128 ? m * 128 + ((j ^ (m & 7)) << 4) : m * 64 + ((j ^ ((m >> 1) & 3)) << 4);
 }
 
-template <int BN, int R, int NQ>
+// CTA2: a cluster pair runs M = 256 MMAs (tcgen05 cta_group::2) over two consecutive tiles, one
+// per CTA; each CTA holds its own A rows and half of the weight rows, so one MMA instruction
+// serves two SMs ($TCB_STEM_CTA2=1; measured slower at N = 64, see stem_fwd host code).
+template <int BN, int R, int NQ, bool CTA2 = false>
 __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid_constant__ StemParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -141,6 +144,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
     constexpr int kBox = BN >= 64 ? 64 : BN;          // output channels per store box
     constexpr int kRowB = kBox * 2;                   // staging row bytes (128 or 64)
     const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t rank = CTA2 ? ptx::cluster_ctarank() : 0u;
+    const int unit0 = CTA2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+    const int ustride = CTA2 ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+    const int units = CTA2 ? (p.tiles + 1) / 2 : p.tiles;
+    constexpr uint32_t kBHalf = CTA2 ? 2u : 1u;  // this CTA's share of the weight rows
     if (tid == 0) {
         for (int i = 0; i < p.stages; ++i) {
             ptx::mbar_init(&full[i], 1);
@@ -148,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
         }
         for (int i = 0; i < kAcc; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 8 * 32);
+            ptx::mbar_init(&tempty[i], (CTA2 ? 2 : 1) * 8 * 32);
         }
         ptx::mbar_init(&bbar, 1);
         ptx::fence_mbarrier_init();
@@ -156,33 +164,48 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
         ptx::tma_prefetch_desc(&p.tmap_b);
         ptx::tma_prefetch_desc(&p.tmap_y);
     }
-    if (warp == 1) ptx::tmem_alloc<kCols>(&tmem_slot);
+    if (warp == 1) {
+        if constexpr (CTA2) ptx::tmem_alloc_2sm<kCols>(&tmem_slot);
+        else ptx::tmem_alloc<kCols>(&tmem_slot);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CTA2) ptx::cluster_sync();
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = tmem_slot;
     ptx::griddep_wait();
     ptx::griddep_launch_dependents();
     const uint32_t sbase = ptx::smem_addr(smem);
     const uint32_t bbase = sbase + p.stages * p.stage_bytes;
+    const uint32_t bchunk = p.b_bytes / kBHalf;          // one filter row's weight slice in smem
     const uint32_t stg = bbase + p.T * p.b_bytes;  // 2 staging tiles of the output
+    auto leader = [&](uint64_t* bar) {
+        return CTA2 ? ptx::leader_addr(ptx::smem_addr(bar)) : ptx::smem_addr(bar);
+    };
 
     if (warp == 0) {
         if (tid == 0) {  // ---------------------------------------- producer
-            ptx::mbar_arrive_expect_tx(&bbar, p.T * p.b_bytes);
-            for (int c = 0; c < p.T; ++c) ptx::tma_load_2d(bbase + c * p.b_bytes, &p.tmap_b, &bbar, c * 32, 0);
+            if (!CTA2 || rank == 0) ptx::mbar_arrive_expect_tx(&bbar, p.T * p.b_bytes);
+            for (int c = 0; c < p.T; ++c) {
+                if constexpr (CTA2)
+                    ptx::tma_load_2d_2sm(bbase + c * bchunk, &p.tmap_b, leader(&bbar), c * 32,
+                                         static_cast<int>(rank) * (BN / 2));
+                else
+                    ptx::tma_load_2d(bbase + c * bchunk, &p.tmap_b, &bbar, c * 32, 0);
+            }
             int st = 0;
             uint32_t ph = 0;
-            for (int u = blockIdx.x; u < p.tiles; u += gridDim.x) {
-                const Tile t = tile_of(p, u);
+            for (int u = unit0; u < units; u += ustride) {
+                const int tile = CTA2 ? min(2 * u + static_cast<int>(rank), p.tiles - 1) : u;
+                const Tile t = tile_of(p, tile);
                 ptx::mbar_wait(&empty[st], ph ^ 1);
                 const uint32_t dst = sbase + st * p.stage_bytes;
                 const int h0 = t.ho * p.sh - p.pad_h, g0 = (t.wo0 / p.BW) * p.g_step;
-                if (p.dbg & 4) {
-                    ptx::mbar_arrive(&full[st]);
-                } else {
-                    ptx::mbar_arrive_expect_tx(&full[st], R * p.G * 128);
-                    for (int r = 0; r < R; ++r)
+                if (!CTA2 || rank == 0) ptx::mbar_arrive_expect_tx(&full[st], kBHalf * R * p.G * 128);
+                for (int r = 0; r < R; ++r) {
+                    if constexpr (CTA2)
+                        ptx::tma_load_4d_2sm(dst + r * kRowStride, &p.tmap_x, leader(&full[st]), 0, g0, h0 + r, t.n);
+                    else
                         ptx::tma_load_4d(dst + r * kRowStride, &p.tmap_x, &full[st], 0, g0, h0 + r, t.n);
                 }
                 if (++st == p.stages) {
@@ -192,12 +215,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
             }
         }
     } else if (warp == 1) {  // ------------------------------------ MMA issuer
-        constexpr uint32_t idesc = ptx::make_idesc(1, 128, BN, 0u, 0u);
+        constexpr uint32_t idesc = ptx::make_idesc(1, CTA2 ? 256 : 128, BN, 0u, 0u);
+        if (!CTA2 || rank == 0) {
         ptx::mbar_wait(&bbar, 0);
         ptx::tc_fence_after();
         int st = 0, it = 0;
         uint32_t ph = 0;
-        for (int u = blockIdx.x; u < p.tiles; u += gridDim.x, ++it) {
+        for (int u = unit0; u < units; u += ustride, ++it) {
             const int acc = it % kAcc;
             ptx::mbar_wait(&tempty[acc], ((it / kAcc) & 1) ^ 1);
             ptx::mbar_wait(&full[st], ph);
@@ -212,26 +236,39 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
                     const uint64_t ad = a0 + ((r * kRowStride + q * 64) >> 4);
-                    const uint64_t bd = b0 + (((r * NQ + q) * BN * 64) >> 4);
-                    ptx::umma_f16_elect(d, ad, bd, idesc, (r | q) ? 1u : 0u);
-                    ptx::umma_f16_elect(d, ad + 2, bd + 2, idesc, 1u);
+                    const uint64_t bd = b0 + (((r * NQ + q) * (BN / kBHalf) * 64) >> 4);
+                    if constexpr (CTA2) {
+                        ptx::umma_f16_2sm_elect(d, ad, bd, idesc, (r | q) ? 1u : 0u);
+                        ptx::umma_f16_2sm_elect(d, ad + 2, bd + 2, idesc, 1u);
+                    } else {
+                        ptx::umma_f16_elect(d, ad, bd, idesc, (r | q) ? 1u : 0u);
+                        ptx::umma_f16_elect(d, ad + 2, bd + 2, idesc, 1u);
+                    }
                 }
             }
-            ptx::umma_commit_elect(&empty[st]);
-            ptx::umma_commit_elect(&tfull[acc]);
+            if constexpr (CTA2) {
+                ptx::umma_commit_2sm_elect(&empty[st], 3);
+                ptx::umma_commit_2sm_elect(&tfull[acc], 3);
+            } else {
+                ptx::umma_commit_elect(&empty[st]);
+                ptx::umma_commit_elect(&tfull[acc]);
+            }
             if (++st == p.stages) {
                 st = 0;
                 ph ^= 1;
             }
         }
+        }
         __syncwarp();
     } else {  // ------------------------------------------------------ epilogue
         const int quarter = warp & 3, half = (warp - 2) >> 2;
         const int row = quarter * 32 + (tid & 31);
-        const bool leader = tid == 64;
+        const bool store_lead = tid == 64;
         int it = 0;
-        for (int u = blockIdx.x; u < p.tiles; u += gridDim.x, ++it) {
-            const Tile t = tile_of(p, u);
+        for (int u = unit0; u < units; u += ustride, ++it) {
+            const int tile = CTA2 ? 2 * u + static_cast<int>(rank) : u;
+            const bool live = tile < p.tiles;
+            const Tile t = tile_of(p, live ? tile : p.tiles - 1);
             const int acc = it % kAcc;
             ptx::mbar_wait(&tfull[acc], (it / kAcc) & 1);
             ptx::tc_fence_after();
@@ -244,12 +281,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
             }
             ptx::tmem_ld_wait();
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[acc]);
+            if (CTA2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_addr(&tempty[acc]), 0));
+            else ptx::mbar_arrive(&tempty[acc]);
             // staging tile acc is free once the store issued two tiles ago has read it
-            if (leader) ptx::bulk_wait_read<1>();
+            if (store_lead) ptx::bulk_wait_read<1>();
             asm volatile("bar.sync 1, 256;" ::: "memory");
             const uint32_t sb = stg + (it & 1) * p.stg_bytes;
-            if (row < p.BW && !(p.dbg & 2)) {
+            if (row < p.BW && live && !(p.dbg & 2)) {
 #pragma unroll
                 for (int ch = 0; ch < kChunks; ++ch) {
                     const int c0 = half * 32 + ch * 64;
@@ -274,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
             }
             ptx::fence_proxy_async_smem();
             asm volatile("bar.sync 1, 256;" ::: "memory");
-            if (leader && !(p.dbg & 2)) {
+            if (store_lead && live && !(p.dbg & 2)) {
                 for (int b = 0; b < (BN + kBox - 1) / kBox; ++b)
                     asm volatile(
                         "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
@@ -284,13 +322,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
                 ptx::bulk_commit();
             }
         }
-        if (leader) ptx::bulk_wait<0>();
+        if (store_lead) ptx::bulk_wait<0>();
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CTA2) ptx::cluster_sync();  // the leader's MMAs read the follower's smem
+    else __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<kCols>(tmem);
+        if constexpr (CTA2) ptx::tmem_dealloc_2sm<kCols>(tmem);
+        else ptx::tmem_dealloc<kCols>(tmem);
     }
 }
 
@@ -623,6 +663,27 @@ void fill_common(StemParams& p, const ConvGeom& g, const StemPlan& q) {
 }
 
 template <typename K>
+cudaError_t launch_pair(K kern, dim3 grid, size_t smem, cudaStream_t st, const StemParams& p) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <typename K>
 cudaError_t launch_big(K kern, dim3 grid, size_t smem, cudaStream_t st, const StemParams& p) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -705,7 +766,13 @@ cudaError_t conv_stem_fwd(const ConvGeom& g, const void* x, const void* w, const
                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    if (!make_tmap_bf16_2d(&p.tmap_b, wp, g.k, size_t(q.T) * 32, g.k, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    // CTA pairs ($TCB_STEM_CTA2=1): M = 256 MMAs over two output rows, half the weight rows per
+    // CTA. Correct, but measured 0.37 vs 0.22 ms for the ResNet stem (N = 64 pairs lose, as in
+    // conv_win), so off by default.
+    static const int env_cta2 = [] { const char* e = getenv("TCB_STEM_CTA2"); return e ? atoi(e) : 0; }();
+    const bool cta2 = env_cta2 != 0 && q.tiles >= 2;
+    if (!make_tmap_bf16_2d(&p.tmap_b, wp, g.k, size_t(q.T) * 32, cta2 ? g.k / 2 : g.k, 32,
+                           CU_TENSOR_MAP_SWIZZLE_64B))
         return cudaErrorInvalidValue;
     fill_common(p, g, q);
     p.stage_bytes = q.stage_bytes;
@@ -720,10 +787,12 @@ cudaError_t conv_stem_fwd(const ConvGeom& g, const void* x, const void* w, const
     p.relu = ep.relu ? 1 : 0;
     static const int env_dbg = [] { const char* e = getenv("TCB_STEM_DBG"); return e ? atoi(e) : 0; }();
     p.dbg = env_dbg;
-    const int grid = std::min(q.tiles, num_sms());
-    conv_tc_note_launch(ConvTcLaunchInfo{0, 5, g.k, 0, 0, 1, q.tiles, grid, 0, 1});
-#define TCB_STEM_FWD(BN, R, NQ) \
-    if (g.k == BN && g.r == R && q.nq == NQ) return launch_big(conv_stem_fwd_kernel<BN, R, NQ>, dim3(grid), q.smem, st, p);
+    const int grid = cta2 ? 2 * std::min((q.tiles + 1) / 2, num_sms() / 2) : std::min(q.tiles, num_sms());
+    conv_tc_note_launch(ConvTcLaunchInfo{0, 5, g.k, 0, cta2 ? 1 : 0, 1, q.tiles, grid, 0, 1});
+#define TCB_STEM_FWD(BN, R, NQ)                                                                         \
+    if (g.k == BN && g.r == R && q.nq == NQ)                                                           \
+        return cta2 ? launch_pair(conv_stem_fwd_kernel<BN, R, NQ, true>, dim3(grid), q.smem, st, p)   \
+                    : launch_big(conv_stem_fwd_kernel<BN, R, NQ>, dim3(grid), q.smem, st, p);
 #define TCB_STEM_FWD_R(R, NQ) TCB_STEM_FWD(32, R, NQ) TCB_STEM_FWD(64, R, NQ) TCB_STEM_FWD(128, R, NQ)
     TCB_STEM_FWD_R(7, 1)
     TCB_STEM_FWD_R(3, 1)

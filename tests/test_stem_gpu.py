@@ -117,6 +117,37 @@ def test_stem_matches_explicit_im2col_path(case):
     assert torch.allclose(dw1, dw0, rtol=1e-4, atol=1e-4 * dw0.abs().max().item())
 
 
+@pytest.mark.parametrize("case", [STEMS[0], STEMS[2], STEMS[6]], ids=[STEMS[0][0], STEMS[2][0], STEMS[6][0]])
+def test_stem_cta_pairs_match_single_cta(case, monkeypatch):
+    """$TCB_STEM_CTA2=1 (M = 256 MMAs over CTA pairs, odd tile counts included)
+    gives the same bits as the single-CTA forward: same products, same fp32
+    accumulation order per output element."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, torch; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
+        "import test_stem_gpu as t;"
+        f"case = {case!r};"
+        "device, L = t._lib();"
+        "_, n, h, w, k, r, pad, stride, cv = case;"
+        "g = device.geom(n, h, w, 8, k, r, pad=pad, stride=stride);"
+        "plan = device.ConvPlan(g, 'gemm', 'bf16').set_valid_channels(cv);"
+        "x, wt, bias = t._inputs(case, 11);"
+        "y = plan.fwd(x, wt, bias=bias, relu=True); torch.cuda.synchronize();"
+        "print(device.last_launch()['cta2']);"
+        "torch.save(y.cpu(), sys.argv[1])")
+    outs = []
+    for on in ("0", "1"):
+        path = f"/tmp/stem_cta2_{on}.pt"
+        env = dict(__import__("os").environ, TCB_STEM_CTA2=on)
+        res = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True,
+                             timeout=300)
+        assert res.returncode == 0, res.stderr[-2000:]
+        assert res.stdout.strip().splitlines()[-1] == on
+        outs.append(torch.load(path))
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_stem_repeat_is_bitwise_and_in_bounds():
     """Guard regions around y / dw and the workspace; two launches bit-identical."""
     device, L = _lib()
