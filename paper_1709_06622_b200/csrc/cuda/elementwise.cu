@@ -923,24 +923,26 @@ __device__ __forceinline__ void pool_window_add(float (&acc)[8], const uint4& g,
     }
 }
 
-// 3x3 / stride 2 / pad 1 (every ResNet / VGG-style stem pool): the 9 window
-// loads are unrolled with compile-time offsets and predicated, so a thread has
-// all of them in flight at once (the generic kernel's runtime loop issued them
-// one dependent iteration at a time: latency-bound at ~4 TB/s). Same tap order
-// and tie rule (first maximum in row-major window order wins) as the generic one.
-__global__ void __launch_bounds__(256) maxpool_fwd_k3s2p1_bf16_kernel(
+// 3x3 / stride 2, pad P = 1 (ResNet / VGG-style stem pools) or 0 (Inception's
+// reduction pools): the 9 window loads are unrolled with compile-time offsets
+// and predicated, so a thread has all of them in flight at once (the generic
+// kernel's runtime loop issued them one dependent iteration at a time:
+// latency-bound at ~4 TB/s). Same tap order and tie rule (first maximum in
+// row-major window order wins) as the generic one.
+template <int P>
+__global__ void __launch_bounds__(256) maxpool_fwd_k3s2_bf16_kernel(
     const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ arg, int H, int W,
     int C, int Ho, int Wo) {
     pdl_wait();
     pdl_trigger();
     const int cg = C / 8;
     const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
-    const int h0 = ho * 2 - 1;
+    const int h0 = ho * 2 - P;
     const __nv_bfloat16* xn = x + size_t(n) * H * W * C;
     const size_t orow = size_t(blockIdx.x) * Wo * C;
     for (int i = threadIdx.x; i < Wo * cg; i += blockDim.x) {
         const int wo = i / cg, c = (i - wo * cg) * 8;
-        const int w0 = wo * 2 - 1;
+        const int w0 = wo * 2 - P;
         uint4 v[9];
 #pragma unroll
         for (int t = 0; t < 9; ++t) {
@@ -981,18 +983,24 @@ __global__ void __launch_bounds__(256) maxpool_fwd_k3s2p1_bf16_kernel(
     }
 }
 
-__global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1_bf16_kernel(
+// Owner (ob, wb) computes the 2x2 block of dx rows 2ob + ai, columns 2wb + bi
+// from the pooled outputs whose windows cover it: rows ob + dh for dh in
+// {0, 1} (P = 1) or {-1, 0} (P = 0), tap r = ai + P - 2 dh.
+template <int P>
+__global__ void __launch_bounds__(256) maxpool_bwd_k3s2_bf16_kernel(
     const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
     __nv_bfloat16* __restrict__ dx, const __nv_bfloat16* __restrict__ ymask, int H, int W, int C,
     int Ho, int Wo) {
     pdl_wait();
     pdl_trigger();
+    constexpr int kD0 = P == 1 ? 0 : -1;
     const int cg = C / 8;
-    const int n = blockIdx.x / Ho, ho = blockIdx.x - n * Ho;
+    const int OH = (H + 1) / 2, OW = (W + 1) / 2;
+    const int n = blockIdx.x / OH, ho = blockIdx.x - n * OH;
     const size_t nbase = size_t(n) * Ho * Wo * C;
     const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
     const bool use_y = ymask != nullptr;
-    for (int i = threadIdx.x; i < Wo * cg; i += blockDim.x) {
+    for (int i = threadIdx.x; i < OW * cg; i += blockDim.x) {
         const int wo = i / cg, c = (i - wo * cg) * 8;
         uint4 g[2][2];
         uint2 a[2][2];
@@ -1002,13 +1010,14 @@ __global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1_bf16_kernel(
         for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
             for (int dw = 0; dw < 2; ++dw) {
-                ok[dh][dw] = ho + dh < Ho && wo + dw < Wo;
+                const int ph = ho + dh + kD0, pw = wo + dw + kD0;
+                ok[dh][dw] = ph >= 0 && ph < Ho && pw >= 0 && pw < Wo;
                 g[dh][dw] = make_uint4(0, 0, 0, 0);
                 a[dh][dw] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) yp[dh][dw][j] = 0;
                 if (ok[dh][dw]) {
-                    const size_t o = nbase + size_t((ho + dh) * Wo + wo + dw) * C + c;
+                    const size_t o = nbase + size_t(ph * Wo + pw) * C + c;
                     g[dh][dw] = __ldg(reinterpret_cast<const uint4*>(dy + o));
                     a[dh][dw] = __ldg(reinterpret_cast<const uint2*>(arg + o));
                     if (use_y) {
@@ -1034,8 +1043,8 @@ __global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1_bf16_kernel(
                 for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
                     for (int dw = 0; dw < 2; ++dw) {
-                        const int r = ai + 1 - 2 * dh, sx = bi + 1 - 2 * dw;
-                        if (r < 0 || sx < 0) continue;  // compile-time after unrolling
+                        const int r = ai + P - 2 * (dh + kD0), sx = bi + P - 2 * (dw + kD0);
+                        if (r < 0 || sx < 0 || r > 2 || sx > 2) continue;  // compile-time after unrolling
                         pool_window_add(acc, g[dh][dw], a[dh][dw], yp[dh][dw], use_y, r * 3 + sx);
                     }
                 uint4 out;
@@ -1060,10 +1069,10 @@ cudaError_t maxpool_fwd(DType dt, const void* x, void* y, uint8_t* arg, int n, i
     const size_t total = size_t(n) * ho * wo * c;
     if (dt == DType::BF16 && c % 8 == 0 && aligned16(x) && aligned16(y) &&
         (!arg || (reinterpret_cast<uintptr_t>(arg) % 8) == 0) && size_t(h) * w * c < (size_t(1) << 31)) {
-        if (f == 3 && s == 2 && p == 1)
-            return launch_pdl(maxpool_fwd_k3s2p1_bf16_kernel, dim3(n * ho), dim3(256), 0, st,
-                              static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), arg, h, w, c,
-                              ho, wo);
+        if (f == 3 && s == 2 && (p == 0 || p == 1))
+            return launch_pdl(p == 1 ? maxpool_fwd_k3s2_bf16_kernel<1> : maxpool_fwd_k3s2_bf16_kernel<0>,
+                              dim3(n * ho), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
+                              static_cast<__nv_bfloat16*>(y), arg, h, w, c, ho, wo);
         return launch_pdl(maxpool_fwd_bf16x8_kernel, dim3(n * ho), dim3(256), 0, st,
                           static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), arg, h, w,
                           c, f, s, p, ho, wo);
@@ -1087,8 +1096,9 @@ cudaError_t maxpool_bwd(DType dt, const void* dy, const uint8_t* arg, void* dx, 
     const size_t total = size_t(n) * h * w * c;
     if (dt == DType::BF16 && c % 8 == 0 && aligned16(dy) && aligned16(dx) &&
         (!ymask || aligned16(ymask)) && (reinterpret_cast<uintptr_t>(arg) % 8) == 0 &&
-        size_t(ho) * wo * c < (size_t(1) << 31) && f == 3 && s == 2 && p == 1) {
-        return launch_pdl(maxpool_bwd_k3s2p1_bf16_kernel, dim3(n * ho), dim3(256), 0, st,
+        size_t(ho) * wo * c < (size_t(1) << 31) && f == 3 && s == 2 && (p == 0 || p == 1)) {
+        return launch_pdl(p == 1 ? maxpool_bwd_k3s2_bf16_kernel<1> : maxpool_bwd_k3s2_bf16_kernel<0>,
+                          dim3(n * ((h + 1) / 2)), dim3(256), 0, st,
                           static_cast<const __nv_bfloat16*>(dy), arg, static_cast<__nv_bfloat16*>(dx),
                           static_cast<const __nv_bfloat16*>(ymask), h, w, c, ho, wo);
     }

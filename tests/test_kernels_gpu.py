@@ -295,7 +295,7 @@ def test_maxpool_parity(oracle, dtype, pool):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-@pytest.mark.parametrize("pool", [(3, 2, 1), (2, 2, 0)])
+@pytest.mark.parametrize("pool", [(3, 2, 1), (3, 2, 0), (2, 2, 0)])
 def test_maxpool_relu_ties_parity(oracle, dtype, pool):
     """ReLU'd input quantised to a few levels (many ties, many zeros): argmax
     keeps the first maximum in window order, and the fused ReLU backward
