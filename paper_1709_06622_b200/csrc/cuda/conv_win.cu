@@ -51,6 +51,8 @@ struct WinParams {
     int pad_h, pad_w;      // window padding (fwd: the conv's; dgrad: R-1-pad_h, S-1-pad_w)
     int R, S;              // taps of the stencil (dgrad: flipped)
     int Wp, tiles_img, slices;
+    int rect, tw, th;      // rectangular tiles (wide images): th output rows x tw columns per tile
+    FastDiv d_cb;          // column blocks per tile row (rect)
     int Ncol, n_tiles, units;
     uint32_t win_bytes, win_stride, b_bytes;
     int win_stages, b_stages;
@@ -66,7 +68,7 @@ struct WinParams {
 __device__ __forceinline__ long long clk(bool on) { return on ? clock64() : 0; }
 
 struct Unit {
-    int img, nt, row0, off0, f0;
+    int img, nt, row0, off0, f0, col0;
 };
 
 template <bool CTA2>
@@ -77,11 +79,21 @@ __device__ __forceinline__ Unit unit_of(const WinParams& p, int u, uint32_t rank
     p.d_tiles.divmod(rest, g, j);
     t.nt = static_cast<int>(nt);
     t.img = CTA2 ? 2 * static_cast<int>(g) + static_cast<int>(rank) : static_cast<int>(g);
+    if (p.rect) {  // window origin at the tile's (row, column) corner; GEMM rows start at its offset 0
+        uint32_t rb, cb;
+        p.d_cb.divmod(j, rb, cb);
+        t.row0 = static_cast<int>(rb) * p.th;
+        t.col0 = static_cast<int>(cb) * p.tw;
+        t.off0 = 0;
+        t.f0 = 0;
+        return t;
+    }
     t.f0 = static_cast<int>(j) * BM;
     uint32_t r0, o0;
     p.d_wp.divmod(static_cast<uint32_t>(t.f0), r0, o0);
     t.row0 = static_cast<int>(r0);
     t.off0 = static_cast<int>(o0);
+    t.col0 = 0;
     return t;
 }
 
@@ -255,10 +267,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_kernel(const __grid_cons
                     const uint32_t wdst = smem_base + ws * p.win_stride;
                     if (!CTA2 || rank == 0) ptx::mbar_arrive_expect_tx(&wfull[ws], (CTA2 ? 2u : 1u) * p.win_bytes);
                     if constexpr (CTA2)
-                        ptx::tma_load_4d_2sm(wdst, &p.tmap_win, leader(&wfull[ws]), cs * 64, -p.pad_w,
+                        ptx::tma_load_4d_2sm(wdst, &p.tmap_win, leader(&wfull[ws]), cs * 64, t.col0 - p.pad_w,
                                              t.row0 - p.pad_h, t.img);
                     else
-                        ptx::tma_load_4d(wdst, &p.tmap_win, &wfull[ws], cs * 64, -p.pad_w, t.row0 - p.pad_h, t.img);
+                        ptx::tma_load_4d(wdst, &p.tmap_win, &wfull[ws], cs * 64, t.col0 - p.pad_w, t.row0 - p.pad_h,
+                                         t.img);
                     if (++ws == p.win_stages) {
                         ws = 0;
                         wph ^= 1;
@@ -378,7 +391,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_kernel(const __grid_cons
             const int acc = it & 1;
             uint32_t ho, wq;
             p.d_wp.divmod(static_cast<uint32_t>(t.f0 + row), ho, wq);
-            const bool valid = t.img < p.n_img && static_cast<int>(ho) < p.Ho && static_cast<int>(wq) < p.Wo;
+            bool inside = true;
+            if (p.rect) {  // (ho, wq) within the tile's window plane
+                inside = static_cast<int>(ho) < p.th && static_cast<int>(wq) < p.tw;
+                ho += t.row0;
+                wq += t.col0;
+            }
+            const bool valid = inside && t.img < p.n_img && static_cast<int>(ho) < p.Ho && static_cast<int>(wq) < p.Wo;
             const size_t orow = (static_cast<size_t>(t.img) * p.Ho + ho) * p.Wo + wq;
             long long e0 = clk(p.dbg != nullptr);
             ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -426,6 +445,7 @@ struct WinPlan {
     bool use = false;
     int Ha, Wa, Ca, Ho, Wo, pad_h, pad_w, R, S, Ncol;
     int Wp, WR, tiles_img, slices, bn, n_tiles;
+    int rect = 0, tw = 0, th = 0, cblocks = 0;
     bool cta2, bres;
     uint32_t win_bytes, win_stride, b_bytes;
     int win_stages, b_stages;
@@ -460,13 +480,39 @@ WinPlan win_plan(const ConvGeom& g, int mode) {
     q.R = g.r; q.S = g.s;
     if (q.Ca % 64 != 0 || q.Ncol % 8 != 0 || q.pad_h > 15 || q.pad_w > 15) return q;
     q.Wp = q.Wo + q.S - 1;
-    if (q.Wp > 64) return q;  // wide rows: a window of whole rows costs more than it saves
-    // rows a 128-position tile can touch: positions [off0, off0 + 127 + (R-1)*Wp + S-1]
-    q.WR = (q.Wp - 1 + BM - 1 + (q.R - 1) * q.Wp + q.S - 1) / q.Wp + 1;
+    if (q.Wp <= 64) {
+        // rows a 128-position tile can touch: positions [off0, off0 + 127 + (R-1)*Wp + S-1]
+        q.WR = (q.Wp - 1 + BM - 1 + (q.R - 1) * q.Wp + q.S - 1) / q.Wp + 1;
+        q.tiles_img = (q.Ho * q.Wp + BM - 1) / BM;
+    } else {
+        // wide rows ($TCB_WIN_RECT=0 keeps them on the im2col path): rectangular tiles of th
+        // rows x tw columns, the window {tw + S - 1 columns, th + R - 1 rows} at the tile's
+        // corner, GEMM rows = the window plane's first th rows (S - 1 junk columns each);
+        // tw minimises the tile count (one 128-row MMA tile each), then the window size
+        static const int env_rect = [] { const char* e = getenv("TCB_WIN_RECT"); return e ? atoi(e) : 1; }();
+        if (env_rect == 0) return q;
+        long best = -1;
+        for (int tw = std::max(8, q.S); tw + q.S - 1 <= BM; ++tw) {
+            const int wp = tw + q.S - 1, th = BM / wp;
+            if (th < 1) break;
+            const long tiles = long((q.Ho + th - 1) / th) * ((q.Wo + tw - 1) / tw);
+            const long cost = tiles * 4096 + long(th + q.R - 1) * wp;
+            if (best < 0 || cost < best) {
+                best = cost;
+                q.tw = tw;
+                q.th = th;
+            }
+        }
+        if (best < 0) return q;
+        q.rect = 1;
+        q.Wp = q.tw + q.S - 1;
+        q.WR = q.th + q.R - 1;
+        q.cblocks = (q.Wo + q.tw - 1) / q.tw;
+        q.tiles_img = ((q.Ho + q.th - 1) / q.th) * q.cblocks;
+    }
     q.win_bytes = static_cast<uint32_t>(q.WR) * q.Wp * 128;
-    if (q.WR > 256 || q.win_bytes > 64 * 1024) return q;
+    if (q.WR > 256 || q.Wp > 256 || q.win_bytes > 64 * 1024) return q;
     q.win_stride = (q.win_bytes + 1023) / 1024 * 1024;
-    q.tiles_img = (q.Ho * q.Wp + BM - 1) / BM;
     q.slices = q.Ca / 64;
     q.bn = q.Ncol <= 64 ? 64 : q.Ncol <= 128 ? 128 : 256;
     // Measured (scripts/win_ab2.sh, bs256): the window wins where the im2col path's
@@ -569,6 +615,10 @@ cudaError_t run_win(const ConvGeom& g, const WinPlan& q, bool dgrad, const void*
     p.S = q.S;
     p.Wp = q.Wp;
     p.tiles_img = q.tiles_img;
+    p.rect = q.rect;
+    p.tw = q.tw;
+    p.th = q.th;
+    p.d_cb = FastDiv(static_cast<uint32_t>(std::max(q.cblocks, 1)));
     p.slices = q.slices;
     p.Ncol = q.Ncol;
     p.n_tiles = q.n_tiles;
