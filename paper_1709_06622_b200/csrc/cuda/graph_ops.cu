@@ -55,6 +55,30 @@ __global__ void slice_copy_vec_kernel(const uint4* __restrict__ src, size_t src_
     }
 }
 
+// slice copy fused with a ReLU mask (bf16: the concat input's gradient is its
+// channel slice of the concat gradient times [activation > 0]; one pass instead
+// of a copy and an in-place mask). mask rows use the destination pitch.
+__global__ void slice_copy_mask_bf16_kernel(const uint4* __restrict__ src, size_t src_pitch, uint4* __restrict__ dst,
+                                            size_t dst_pitch, int width, size_t rows,
+                                            const uint4* __restrict__ mask) {
+    pdl_wait();
+    pdl_trigger();
+    const size_t total = rows * width;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t r = i / width;
+        const int c = static_cast<int>(i - r * width);
+        uint4 v = src[r * src_pitch + c];
+        const uint4 m = __ldg(mask + r * dst_pitch + c);
+        uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+        const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m);
+        const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            vw[j] &= __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&mw[j]), zero2);
+        dst[r * dst_pitch + c] = v;
+    }
+}
+
 template <typename T>
 __global__ void slice_copy_kernel(const T* __restrict__ src, size_t src_pitch, T* __restrict__ dst,
                                   size_t dst_pitch, int width, size_t rows) {
@@ -173,6 +197,22 @@ cudaError_t slice_copy(DType dt, const void* src, size_t src_pitch, void* dst, s
             static_cast<const __nv_bfloat16*>(src), src_pitch, static_cast<__nv_bfloat16*>(dst), dst_pitch,
             width, rows);
     return cudaGetLastError();
+}
+
+bool slice_copy_mask_supported(DType dt, const void* src, size_t src_pitch, const void* dst, size_t dst_pitch,
+                               int width, const void* mask) {
+    return dt == DType::BF16 && a16(src) && a16(dst) && a16(mask) && src_pitch % 8 == 0 && dst_pitch % 8 == 0 &&
+           width % 8 == 0;
+}
+
+cudaError_t slice_copy_mask(DType dt, const void* src, size_t src_pitch, void* dst, size_t dst_pitch, int width,
+                            size_t rows, const void* mask, cudaStream_t st) {
+    if (!slice_copy_mask_supported(dt, src, src_pitch, dst, dst_pitch, width, mask)) return cudaErrorInvalidValue;
+    if (rows == 0 || width == 0) return cudaSuccess;
+    const int wv = width / 8;
+    return launch_pdl(slice_copy_mask_bf16_kernel, dim3(grid_for(rows * wv, 2)), dim3(kBlock), 0, st,
+                      static_cast<const uint4*>(src), src_pitch / 8, static_cast<uint4*>(dst), dst_pitch / 8, wv,
+                      rows, static_cast<const uint4*>(mask));
 }
 
 bool avgpool2d_supported(DType dt, int c) { return c % static_cast<int>(16 / dtype_size(dt)) == 0; }

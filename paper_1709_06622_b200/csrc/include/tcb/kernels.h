@@ -174,6 +174,12 @@ cudaError_t nvls_probe(int mode, const float* grad_mc, float* grad, const float*
 // dst_pitch): concat forward / backward as channel-slice copies
 cudaError_t slice_copy(DType dt, const void* src, size_t src_pitch, void* dst, size_t dst_pitch, int width,
                        size_t rows, cudaStream_t st);
+// the same copy times [mask > 0] (bf16, 16-byte aligned rows; mask rows at dst_pitch): a concat
+// input's gradient with its producer's ReLU in one pass
+bool slice_copy_mask_supported(DType dt, const void* src, size_t src_pitch, const void* dst, size_t dst_pitch,
+                               int width, const void* mask);
+cudaError_t slice_copy_mask(DType dt, const void* src, size_t src_pitch, void* dst, size_t dst_pitch, int width,
+                            size_t rows, const void* mask, cudaStream_t st);
 // windowed average pool, padding counted (/ f*f); c % (16 B / element) == 0
 bool avgpool2d_supported(DType dt, int c);
 cudaError_t avgpool2d_fwd(DType dt, const void* x, void* y, int n, int h, int w, int c, int f, int s, int p,

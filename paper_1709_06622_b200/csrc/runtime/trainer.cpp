@@ -844,8 +844,15 @@ int backward_contribution(tcb_trainer* t, int ci, int ti, cudaStream_t st) {
         // this input's channel range of the concatenated gradient
         size_t k = 0;
         while (con.ins[k] != ti) ++k;
-        TRY_CUDA(slice_copy(t->dt, t->at<char>(con.grad) + con.coff[k] * dtype_size(t->dt), con.c, out, tgt.c,
-                            tgt.c, size_t(tgt.n) * tgt.h * tgt.w, st));
+        const void* src = t->at<char>(con.grad) + con.coff[k] * dtype_size(t->dt);
+        const size_t rows = size_t(tgt.n) * tgt.h * tgt.w;
+        if (fuse_mask && slice_copy_mask_supported(t->dt, src, con.c, out, tgt.c, tgt.c, t->at(tgt.act))) {
+            // the producer's ReLU mask in the same pass as the slice copy
+            TRY_CUDA(slice_copy_mask(t->dt, src, con.c, out, tgt.c, tgt.c, rows, t->at(tgt.act), st));
+            t->launches++;
+            return TCB_OK;
+        }
+        TRY_CUDA(slice_copy(t->dt, src, con.c, out, tgt.c, tgt.c, rows, st));
         t->launches++;
         for (const void* e : extras) {
             TRY_CUDA(add_inplace(t->dt, out, e, elems, st));
