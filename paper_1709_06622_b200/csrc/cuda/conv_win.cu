@@ -659,8 +659,17 @@ cudaError_t run_win(const ConvGeom& g, const WinPlan& q, bool dgrad, const void*
 // scripts/probes/umma_mn_probe.cu). Every CTA accumulates all M tiles of its
 // contiguous range of k-blocks in TMEM (M tiles x K columns <= 512) and writes
 // one fp32 partial [K][R][S][C]; a fixed-order split reduction sums them.
-constexpr int kWP = 256;  // positions per k-block (16 MMA K-steps)
-constexpr int kWgMaxStages = 2;
+constexpr int kWgMaxStages = 4;
+
+// positions per k-block: 256 (16 MMA K-steps, 2 stages) or 128 (8 K-steps, more stages in the
+// same shared memory); $TCB_WIN_WG_POS
+int wg_positions() {
+    static const int v = [] {
+        const char* e = getenv("TCB_WIN_WG_POS");
+        return (e && atoi(e) == 128) ? 128 : 256;
+    }();
+    return v;
+}
 
 struct WgParams {
     CUtensorMap tmap_x;   // x [N][H][W][C], box {64, Wp, WRx, 1}
@@ -676,7 +685,7 @@ struct WgParams {
     FastDiv d_wp, d_kbimg;
 };
 
-template <int BN>
+template <int BN, int kWP>
 __global__ void __launch_bounds__(kThreads, 1) conv_win_wgrad_kernel(const __grid_constant__ WgParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -804,6 +813,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_wgrad_kernel(const __gri
 struct WgPlan {
     bool use = false;
     int Wp, WRx, WRd, slices, kslices, nq, mtiles, bn, kb_img, kb_total, grid, kb_per_cta, stages, groups, per_group;
+    int wpos;
     uint32_t xwin, dywin, stage, tx;
     size_t smem, partial_bytes;
 };
@@ -829,6 +839,8 @@ WgPlan wgrad_plan(const ConvGeom& g) {
     q.groups = (q.mtiles * q.bn + 511) / 512;
     q.per_group = (q.mtiles + q.groups - 1) / q.groups;
     if (q.groups > 3) return q;
+    q.wpos = wg_positions();
+    const int kWP = q.wpos;
     q.WRx = (q.Wp - 1 + kWP - 1 + (g.r - 1) * q.Wp + g.s - 1) / q.Wp + 1;
     q.WRd = (q.Wp - 1 + kWP - 1) / q.Wp + 1;
     if (q.WRx > 256) return q;
@@ -836,8 +848,8 @@ WgPlan wgrad_plan(const ConvGeom& g) {
     q.dywin = (static_cast<uint32_t>(q.WRd) * q.Wp * 128 + 1023) / 1024 * 1024;
     q.stage = q.slices * q.xwin + q.kslices * q.dywin;
     q.tx = static_cast<uint32_t>(q.slices * q.WRx + q.kslices * q.WRd) * q.Wp * 128;
-    q.stages = kSmemCap >= 2 * size_t(q.stage) + 1024 ? 2 : 1;
     if (size_t(q.stage) + 1024 > kSmemCap) return q;
+    q.stages = static_cast<int>(std::min<size_t>(kWgMaxStages, (kSmemCap - 1024) / q.stage));
     q.smem = size_t(q.stages) * q.stage + 1024;
     q.kb_img = (Ho * q.Wp + kWP - 1) / kWP;
     q.kb_total = g.n * q.kb_img;
@@ -851,7 +863,7 @@ WgPlan wgrad_plan(const ConvGeom& g) {
 
 template <int BN>
 cudaError_t launch_wgrad(const WgParams& p, const WgPlan& q, cudaStream_t st) {
-    auto kern = conv_win_wgrad_kernel<BN>;
+    auto kern = q.wpos == 128 ? conv_win_wgrad_kernel<BN, 128> : conv_win_wgrad_kernel<BN, 256>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(q.smem));
     if (e != cudaSuccess) return e;
     return launch_pdl(kern, dim3(q.grid), dim3(kThreads), q.smem, st, p);
