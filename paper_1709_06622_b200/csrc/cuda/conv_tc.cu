@@ -839,7 +839,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                         }
                         __syncwarp();
                         if (lane == 0 && col0 < ncol) {
-                            ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * 4096, col0, row0);
+                            if (p.batch > 1) ptx::tma_store_3d(&p.tmap_out, ebuf_addr + slot * 4096, col0, row0, tc.b);
+                            else ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * 4096, col0, row0);
                             ptx::bulk_commit();
                         }
                     }
@@ -953,7 +954,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                         }
                         __syncwarp();
                         if (lane == 0) {
-                            if (col0 < ncol) ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * sstride, col0, row0);
+                            if (col0 < ncol) {
+                                if (p.batch > 1)
+                                    ptx::tma_store_3d(&p.tmap_out, ebuf_addr + slot * sstride, col0, row0, tc.b);
+                                else
+                                    ptx::tma_store_2d(&p.tmap_out, ebuf_addr + slot * sstride, col0, row0);
+                            }
                             ptx::bulk_commit();  // (an empty group keeps the read-wait counts in step)
                         }
                     }
@@ -1319,6 +1325,18 @@ bool build_maps(Params& p, const void* a_matrix, const void* b_matrix, int bn) {
 // EPI output / side-input maps: [M][Ncol] bf16, 32-row x 32-column boxes.
 bool build_epi_maps(Params& p) {
     const auto sw = CU_TENSOR_MAP_SWIZZLE_64B;
+    if (p.batch > 1) {  // batched plain GEMMs (Winograd / FFT planes): [batch][M][Ncol], no side inputs
+        if (p.residual || p.mask) return false;
+        EncodeTiledFn fn = encode_tiled_fn();
+        if (!fn) return false;
+        const cuuint64_t dims[3] = {cuuint64_t(p.s.Ncol), cuuint64_t(p.s.M), cuuint64_t(p.batch)};
+        const cuuint64_t strides[2] = {cuuint64_t(p.s.Ncol) * 2, cuuint64_t(p.s.M) * p.s.Ncol * 2};
+        const cuuint32_t box[3] = {32, 32, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        return fn(&p.tmap_out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p.out, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     if (!make_tmap_bf16_2d(&p.tmap_out, p.out, p.s.M, p.s.Ncol, 32, 32, sw)) return false;
     if (p.residual && !make_tmap_bf16_2d(&p.tmap_res, p.residual, p.s.M, p.s.Ncol, 32, 32, sw))
         return false;
@@ -1397,7 +1415,9 @@ int g_epi_kb_spatial = -1;  // ... and for spatial (im2col) layers
 // (Inception-v3's 5x5 / 1x7 / 7x1 branches).
 template <ConvMode MODE>
 bool use_epi(const Params& p) {
-    if (MODE == ConvMode::Wgrad || p.batch > 1) return false;
+    if (MODE == ConvMode::Wgrad) return false;
+    // batched plain GEMMs store through a 3-D map (no side inputs there)
+    if (p.batch > 1 && (p.residual || p.mask)) return false;
     if (MODE == ConvMode::Dgrad && (p.s.sh != 1 || p.s.sw != 1)) return false;
     if (g_epi_kb < 0) {
         const char* e = getenv("TCB_CONV_EPI_KB");

@@ -135,6 +135,13 @@ __device__ __forceinline__ void tma_store_2d(const void* desc, uint32_t src, int
                  : "memory");
 }
 
+__device__ __forceinline__ void tma_store_3d(const void* desc, uint32_t src, int32_t c0, int32_t c1,
+                                             int32_t c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];"
+                 ::"l"(desc), "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
 __device__ __forceinline__ void bulk_commit() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
