@@ -94,38 +94,58 @@ struct PoolShape {
     int n, h, w, c, ho, wo, f, s, p;
 };
 
-// one thread per (output pixel, V channels)
-template <typename T>
+// one thread per (output pixel, V channels). K3: 3x3 / stride 1 / pad 1 (the Inception branch
+// pools) with the 9 window loads issued together (raw 16-byte vectors, converted while
+// summing in the generic loop's order) instead of one dependent loop iteration each.
+template <typename T, bool K3 = false>
 __global__ void avgpool2d_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, PoolShape ps) {
     pdl_wait();
     pdl_trigger();
     constexpr int V = Vec<T>::N;
     const int cv = ps.c / V;
-    const size_t total = size_t(ps.n) * ps.ho * ps.wo * cv;
+    const uint32_t total = static_cast<uint32_t>(size_t(ps.n) * ps.ho * ps.wo * cv);  // < 2^32 (host)
     const float inv = 1.f / static_cast<float>(ps.f * ps.f);
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
-        const int cg = static_cast<int>(i % cv);
-        size_t pix = i / cv;
-        const int j = static_cast<int>(pix % ps.wo);
-        pix /= ps.wo;
-        const int oi = static_cast<int>(pix % ps.ho);
-        const int b = static_cast<int>(pix / ps.ho);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int cg = static_cast<int>(i % static_cast<uint32_t>(cv));
+        uint32_t pix = i / static_cast<uint32_t>(cv);
+        const int j = static_cast<int>(pix % static_cast<uint32_t>(ps.wo));
+        pix /= static_cast<uint32_t>(ps.wo);
+        const int oi = static_cast<int>(pix % static_cast<uint32_t>(ps.ho));
+        const int b = static_cast<int>(pix / static_cast<uint32_t>(ps.ho));
         float acc[V] = {};
-        for (int r = 0; r < ps.f; ++r) {
-            const int hh = oi * ps.s - ps.p + r;
-            if (hh < 0 || hh >= ps.h) continue;
-            for (int q = 0; q < ps.f; ++q) {
-                const int ww = j * ps.s - ps.p + q;
-                if (ww < 0 || ww >= ps.w) continue;
-                float v[V];
-                load_vec(x + ((size_t(b) * ps.h + hh) * ps.w + ww) * ps.c + cg * V, v);
+        if constexpr (K3) {
+            uint4 raw[9];
 #pragma unroll
-                for (int e = 0; e < V; ++e) acc[e] += v[e];
+            for (int t = 0; t < 9; ++t) {
+                const int hh = oi - 1 + t / 3, ww = j - 1 + t % 3;
+                raw[t] = (hh >= 0 && hh < ps.h && ww >= 0 && ww < ps.w)
+                             ? __ldg(reinterpret_cast<const uint4*>(x + ((size_t(b) * ps.h + hh) * ps.w + ww) * ps.c +
+                                                                    cg * V))
+                             : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+                const T* e8 = reinterpret_cast<const T*>(&raw[t]);
+#pragma unroll
+                for (int e = 0; e < V; ++e) acc[e] += to_f32<T>(e8[e]);
+            }
+        } else {
+            for (int r = 0; r < ps.f; ++r) {
+                const int hh = oi * ps.s - ps.p + r;
+                if (hh < 0 || hh >= ps.h) continue;
+                for (int q = 0; q < ps.f; ++q) {
+                    const int ww = j * ps.s - ps.p + q;
+                    if (ww < 0 || ww >= ps.w) continue;
+                    float v[V];
+                    load_vec(x + ((size_t(b) * ps.h + hh) * ps.w + ww) * ps.c + cg * V, v);
+#pragma unroll
+                    for (int e = 0; e < V; ++e) acc[e] += v[e];
+                }
             }
         }
 #pragma unroll
         for (int e = 0; e < V; ++e) acc[e] *= inv;
-        store_vec(y + i * V, acc);
+        store_vec(y + size_t(i) * V, acc);
     }
 }
 
@@ -172,6 +192,94 @@ __global__ void avgpool2d_bwd_kernel(const T* __restrict__ dy, T* dx, PoolShape 
             for (int e = 0; e < V; ++e) acc[e] = m[e] > 0.f ? acc[e] : 0.f;
         }
         store_vec(dx + i * V, acc);
+    }
+}
+
+// 3x3 / stride 1 / pad 1 average pool (Inception branch pools), one block per output row:
+// the block's threads sweep (column, channel vector) of that row, so the 3 input rows its 9
+// taps read stay in L1 (the flat grid-stride kernel spread a pixel's 9 readers over SMs and
+// re-read every input vector 9 times from L2). Loads issued together; the generic kernel's
+// summation order (rows, then columns).
+template <typename T>
+__global__ void __launch_bounds__(256) avgpool3_fwd_rows_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                                PoolShape ps) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int V = Vec<T>::N;
+    const int cv = ps.c / V;
+    const int b = blockIdx.x / ps.ho, oi = blockIdx.x - b * ps.ho;
+    const float inv = 1.f / 9.f;
+    const T* xb = x + size_t(b) * ps.h * ps.w * ps.c;
+    T* yr = y + size_t(blockIdx.x) * ps.wo * ps.c;
+    for (int i = threadIdx.x; i < ps.wo * cv; i += blockDim.x) {
+        const int j = i / cv, cg = i - j * cv;
+        uint4 raw[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const int hh = oi - 1 + t / 3, ww = j - 1 + t % 3;
+            raw[t] = (hh >= 0 && hh < ps.h && ww >= 0 && ww < ps.w)
+                         ? __ldg(reinterpret_cast<const uint4*>(xb + (size_t(hh) * ps.w + ww) * ps.c + cg * V))
+                         : make_uint4(0, 0, 0, 0);
+        }
+        float acc[V] = {};
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const T* e8 = reinterpret_cast<const T*>(&raw[t]);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[e] += to_f32<T>(e8[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] *= inv;
+        store_vec(yr + size_t(i) * V, acc);
+    }
+}
+
+// its backward, one block per input row: dx = [mask > 0] * (residual + sum of the 9
+// covering windows' dy / 9), windows (oi, oj) in [h - 1, h + 1] x [w - 1, w + 1]
+template <typename T>
+__global__ void __launch_bounds__(256) avgpool3_bwd_rows_kernel(const T* __restrict__ dy, T* dx, PoolShape ps,
+                                                                const T* __restrict__ mask, const T* residual) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int V = Vec<T>::N;
+    const int cv = ps.c / V;
+    const int b = blockIdx.x / ps.h, hh = blockIdx.x - b * ps.h;
+    const float inv = 1.f / 9.f;
+    const T* db = dy + size_t(b) * ps.ho * ps.wo * ps.c;
+    const size_t rbase = size_t(blockIdx.x) * ps.w * cv;  // this row's first vector
+    for (int i = threadIdx.x; i < ps.w * cv; i += blockDim.x) {
+        const int ww = i / cv, cg = i - ww * cv;
+        uint4 raw[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const int oi = hh - 1 + t / 3, oj = ww - 1 + t % 3;
+            raw[t] = (oi >= 0 && oi < ps.ho && oj >= 0 && oj < ps.wo)
+                         ? __ldg(reinterpret_cast<const uint4*>(db + (size_t(oi) * ps.wo + oj) * ps.c + cg * V))
+                         : make_uint4(0, 0, 0, 0);
+        }
+        float acc[V] = {};
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const T* e8 = reinterpret_cast<const T*>(&raw[t]);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[e] += to_f32<T>(e8[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] *= inv;
+        const size_t o = (rbase + i) * V;
+        if (residual) {  // may alias dx: read before the write below, same thread
+            float r[V];
+            load_vec(residual + o, r);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[e] += r[e];
+        }
+        if (mask) {
+            float m[V];
+            load_vec(mask + o, m);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[e] = m[e] > 0.f ? acc[e] : 0.f;
+        }
+        store_vec(dx + o, acc);
     }
 }
 
@@ -222,11 +330,22 @@ cudaError_t avgpool2d_fwd(DType dt, const void* x, void* y, int n, int h, int w,
     if (!avgpool2d_supported(dt, c) || !a16(x) || !a16(y)) return cudaErrorInvalidValue;
     PoolShape ps{n, h, w, c, (h + 2 * p - f) / s + 1, (w + 2 * p - f) / s + 1, f, s, p};
     const size_t total = size_t(n) * ps.ho * ps.wo * c / (16 / dtype_size(dt));
+    static const int env_k3 = [] { const char* e = getenv("TCB_AVGPOOL_K3"); return e ? atoi(e) : 2; }();
+    const bool k3 = env_k3 != 0 && f == 3 && s == 1 && p == 1;
+    if (k3 && env_k3 == 2) {  // one block per output row
+        if (dt == DType::F32)
+            return launch_pdl(avgpool3_fwd_rows_kernel<float>, dim3(n * ps.ho), dim3(256), 0, st,
+                              static_cast<const float*>(x), static_cast<float*>(y), ps);
+        return launch_pdl(avgpool3_fwd_rows_kernel<__nv_bfloat16>, dim3(n * ps.ho), dim3(256), 0, st,
+                          static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), ps);
+    }
     if (dt == DType::F32)
-        return launch_pdl(avgpool2d_fwd_kernel<float>, dim3(grid_for(total, 2)), dim3(kBlock), 0, st,
-                          static_cast<const float*>(x), static_cast<float*>(y), ps);
-    return launch_pdl(avgpool2d_fwd_kernel<__nv_bfloat16>, dim3(grid_for(total, 2)), dim3(kBlock), 0, st,
-                      static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), ps);
+        return launch_pdl(k3 ? avgpool2d_fwd_kernel<float, true> : avgpool2d_fwd_kernel<float>,
+                          dim3(grid_for(total, 2)), dim3(kBlock), 0, st, static_cast<const float*>(x),
+                          static_cast<float*>(y), ps);
+    return launch_pdl(k3 ? avgpool2d_fwd_kernel<__nv_bfloat16, true> : avgpool2d_fwd_kernel<__nv_bfloat16>,
+                      dim3(grid_for(total, 2)), dim3(kBlock), 0, st, static_cast<const __nv_bfloat16*>(x),
+                      static_cast<__nv_bfloat16*>(y), ps);
 }
 
 cudaError_t avgpool2d_bwd(DType dt, const void* dy, void* dx, int n, int h, int w, int c, int f, int s, int p,
@@ -235,6 +354,16 @@ cudaError_t avgpool2d_bwd(DType dt, const void* dy, void* dx, int n, int h, int 
         return cudaErrorInvalidValue;
     PoolShape ps{n, h, w, c, (h + 2 * p - f) / s + 1, (w + 2 * p - f) / s + 1, f, s, p};
     const size_t total = size_t(n) * h * w * c / (16 / dtype_size(dt));
+    static const int env_k3b = [] { const char* e = getenv("TCB_AVGPOOL_K3"); return e ? atoi(e) : 2; }();
+    if (env_k3b == 2 && f == 3 && s == 1 && p == 1) {  // one block per input row
+        if (dt == DType::F32)
+            return launch_pdl(avgpool3_bwd_rows_kernel<float>, dim3(n * h), dim3(256), 0, st,
+                              static_cast<const float*>(dy), static_cast<float*>(dx), ps,
+                              static_cast<const float*>(mask), static_cast<const float*>(residual));
+        return launch_pdl(avgpool3_bwd_rows_kernel<__nv_bfloat16>, dim3(n * h), dim3(256), 0, st,
+                          static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx), ps,
+                          static_cast<const __nv_bfloat16*>(mask), static_cast<const __nv_bfloat16*>(residual));
+    }
     if (dt == DType::F32)
         return launch_pdl(avgpool2d_bwd_kernel<float>, dim3(grid_for(total, 2)), dim3(kBlock), 0, st,
                           static_cast<const float*>(dy), static_cast<float*>(dx), ps,
