@@ -70,6 +70,10 @@ struct StemParams {
     const float* bias;
     int relu;
     int dbg;              // diagnostics ($TCB_STEM_DBG): 1 no MMA, 2 no output stores, 4 no x loads
+    // fused 3x3 / 2 / 1 max pool (conv_stem_fwd_pool_kernel)
+    __nv_bfloat16* pool_y;
+    uint8_t* pool_arg;
+    int Po, Pw, pool_rows, pool_per_cta;
     // wgrad
     int mtiles, tiles_per_cta, dy_boxes, tr;  // tr: output rows per weight-gradient tile (1 or 2)
     uint32_t dy_box_bytes, xslots;
@@ -331,6 +335,240 @@ __global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_kernel(const __grid
         ptx::tc_fence_after();
         if constexpr (CTA2) ptx::tmem_dealloc_2sm<kCols>(tmem);
         else ptx::tmem_dealloc<kCols>(tmem);
+    }
+}
+
+// Stem rows a CTA computes for its contiguous range of pooled rows [q, q1) (flattened
+// (image, pooled row)): pooled row p reads stem rows 2p-1..2p+1, rows are emitted once in
+// increasing order (the first pooled row of a range recomputes its row 2p-1, which the
+// neighbouring CTA also writes -- the same values), and the emission of row min(2p+1, Ho-1)
+// completes pooled row p.
+struct PoolSeq {
+    int q, q1, k, last;
+    __device__ PoolSeq(int q0, int qe) : q(q0), q1(qe), k(0), last(-1) {}
+    __device__ bool next(const StemParams& p, int& n, int& ho, int& done_q) {
+        while (q < q1) {
+            const int img = q / p.Po, pr = q - img * p.Po;
+            const int hlast = min(2 * pr + 1, p.Ho - 1);
+            while (k < 3) {
+                const int h = 2 * pr - 1 + k;
+                ++k;
+                if (h < 0 || h >= p.Ho) continue;
+                const int flat = img * p.Ho + h;
+                if (flat <= last) continue;
+                last = flat;
+                n = img;
+                ho = h;
+                done_q = h == hlast ? q : -1;
+                if (h == hlast) {
+                    ++q;
+                    k = 0;
+                }
+                return true;
+            }
+            ++q;
+            k = 0;
+        }
+        return false;
+    }
+};
+
+// The stem forward fused with the 3x3 / stride 2 / pad 1 max pool that follows it (ResNet):
+// the ReLU'd stem rows pass through four swizzled staging tiles on their way to the TMA
+// store, and whenever a row completes a pooled row the epilogue warps pool the three staged
+// rows straight from shared memory -- the separate pool kernel's 411 MB re-read of the stem
+// output is gone. Same max / first-maximum tie rule / argmax code as maxpool_fwd. BN = 64,
+// one width tile per row.
+template <int R>
+__global__ void __launch_bounds__(kThreads, 1) conv_stem_fwd_pool_kernel(const __grid_constant__ StemParams p) {
+    constexpr int BN = 64;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int kAcc = 4;
+    __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[kAcc], tempty[kAcc], bbar;
+    __shared__ uint32_t tmem_slot;
+    constexpr uint32_t kCols = kAcc * BN;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int q0 = blockIdx.x * p.pool_per_cta, q1 = min(p.pool_rows, q0 + p.pool_per_cta);
+    if (tid == 0) {
+        for (int i = 0; i < p.stages; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < kAcc; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 8 * 32);
+        }
+        ptx::mbar_init(&bbar, 1);
+        ptx::fence_mbarrier_init();
+        ptx::tma_prefetch_desc(&p.tmap_x);
+        ptx::tma_prefetch_desc(&p.tmap_b);
+        ptx::tma_prefetch_desc(&p.tmap_y);
+    }
+    if (warp == 1) ptx::tmem_alloc<kCols>(&tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
+    const uint32_t sbase = ptx::smem_addr(smem);
+    const uint32_t bbase = sbase + p.stages * p.stage_bytes;
+    const uint32_t stg = bbase + R * p.b_bytes;  // 4 staging tiles: the TMA store and the pool both read them
+
+    if (warp == 0) {
+        if (tid == 0) {  // ---------------------------------------- producer
+            ptx::mbar_arrive_expect_tx(&bbar, R * p.b_bytes);
+            for (int c = 0; c < R; ++c) ptx::tma_load_2d(bbase + c * p.b_bytes, &p.tmap_b, &bbar, c * 32, 0);
+            int st = 0;
+            uint32_t ph = 0;
+            PoolSeq seq(q0, q1);
+            int n, ho, dq;
+            while (seq.next(p, n, ho, dq)) {
+                ptx::mbar_wait(&empty[st], ph ^ 1);
+                const uint32_t dst = sbase + st * p.stage_bytes;
+                const int h0 = ho * p.sh - p.pad_h;
+                ptx::mbar_arrive_expect_tx(&full[st], R * p.G * 128);
+                for (int r = 0; r < R; ++r)
+                    ptx::tma_load_4d(dst + r * kRowStride, &p.tmap_x, &full[st], 0, 0, h0 + r, n);
+                if (++st == p.stages) {
+                    st = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {  // ------------------------------------ MMA issuer
+        constexpr uint32_t idesc = ptx::make_idesc(1, 128, BN, 0u, 0u);
+        ptx::mbar_wait(&bbar, 0);
+        ptx::tc_fence_after();
+        int st = 0, it = 0;
+        uint32_t ph = 0;
+        PoolSeq seq(q0, q1);
+        int n, ho, dq;
+        while (seq.next(p, n, ho, dq)) {
+            const int acc = it % kAcc;
+            ptx::mbar_wait(&tempty[acc], ((it / kAcc) & 1) ^ 1);
+            ptx::mbar_wait(&full[st], ph);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem + acc * BN;
+            const uint64_t a0 = rows_desc(sbase + st * p.stage_bytes);
+            const uint64_t b0 = sw64_desc(bbase, 16, 512);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint64_t ad = a0 + ((r * kRowStride) >> 4);
+                const uint64_t bd = b0 + ((r * BN * 64) >> 4);
+                ptx::umma_f16_elect(d, ad, bd, idesc, r ? 1u : 0u);
+                ptx::umma_f16_elect(d, ad + 2, bd + 2, idesc, 1u);
+            }
+            ptx::umma_commit_elect(&empty[st]);
+            ptx::umma_commit_elect(&tfull[acc]);
+            if (++st == p.stages) {
+                st = 0;
+                ph ^= 1;
+            }
+            ++it;
+        }
+        __syncwarp();
+    } else {  // ------------------------------------------------------ epilogue
+        const int quarter = warp & 3, half = (warp - 2) >> 2;
+        const int row = quarter * 32 + (tid & 31);
+        const int et = tid - 64;  // 0..255
+        const bool store_lead = et == 0;
+        int it = 0;
+        PoolSeq seq(q0, q1);
+        int n, ho, dq;
+        while (seq.next(p, n, ho, dq)) {
+            const int acc = it % kAcc;
+            ptx::mbar_wait(&tfull[acc], (it / kAcc) & 1);
+            ptx::tc_fence_after();
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * 32, v);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+            // staging tile it & 3 is free once the store issued four rows ago has read it
+            if (store_lead) ptx::bulk_wait_read<3>();
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            const uint32_t sb = stg + (it & 3) * p.stg_bytes;
+            if (row < p.BW) {
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    float f[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float x = __uint_as_float(v[8 * g + i]);
+                        if (p.bias) x += __ldg(p.bias + half * 32 + 8 * g + i);
+                        f[i] = p.relu ? fmaxf(x, 0.f) : x;
+                    }
+                    const uint4 w = pack8f(f);
+                    const uint32_t a = sb + stg_off(row, half * 4 + g, 128);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w.x), "r"(w.y), "r"(w.z),
+                                 "r"(w.w)
+                                 : "memory");
+                }
+            }
+            ptx::fence_proxy_async_smem();
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (store_lead) {
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                        &p.tmap_y),
+                    "r"(sb), "r"(0), "r"(0), "r"(n * p.Ho + ho)
+                    : "memory");
+                ptx::bulk_commit();
+            }
+            if (dq >= 0) {
+                // pooled row pr of image n from staged stem rows 2pr-1 .. 2pr+1 (tiles it - (ho - h))
+                const int pr = dq - n * p.Po;
+                const size_t obase = (size_t(n) * p.Po + pr) * p.Pw * BN;
+                for (int item = et; item < p.Pw * 8; item += 256) {
+                    const int pw = item >> 3, cg = item & 7;
+                    __nv_bfloat162 best[4];
+                    uint32_t idx[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        best[j] = __halves2bfloat162(__ushort_as_bfloat16(0xFF80u), __ushort_as_bfloat16(0xFF80u));
+                        idx[j] = 0;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 9; ++t) {
+                        const int h = 2 * pr - 1 + t / 3, w = 2 * pw - 1 + t % 3;
+                        if (h < 0 || h >= p.Ho || w < 0 || w >= p.Wo) continue;
+                        const uint32_t tile = stg + ((it - (ho - h)) & 3) * p.stg_bytes;
+                        uint4 vv;
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(vv.x), "=r"(vv.y), "=r"(vv.z), "=r"(vv.w)
+                                     : "r"(tile + stg_off(w, cg, 128)));
+                        const uint32_t code = static_cast<uint32_t>(t) * 0x00010001u;
+                        const uint32_t vw[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&vw[j]);
+                            const uint32_t gt = __hgt2_mask(b, best[j]);
+                            best[j] = __hmax2(best[j], b);
+                            idx[j] = (idx[j] & ~gt) | (code & gt);
+                        }
+                    }
+                    const size_t o = obase + size_t(pw) * BN + cg * 8;
+                    uint4 out;
+                    out.x = *reinterpret_cast<uint32_t*>(&best[0]);
+                    out.y = *reinterpret_cast<uint32_t*>(&best[1]);
+                    out.z = *reinterpret_cast<uint32_t*>(&best[2]);
+                    out.w = *reinterpret_cast<uint32_t*>(&best[3]);
+                    *reinterpret_cast<uint4*>(p.pool_y + o) = out;
+                    *reinterpret_cast<uint2*>(p.pool_arg + o) =
+                        make_uint2(__byte_perm(idx[0], idx[1], 0x6420), __byte_perm(idx[2], idx[3], 0x6420));
+                }
+            }
+            ++it;
+        }
+        if (store_lead) ptx::bulk_wait<0>();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<kCols>(tmem);
     }
 }
 
@@ -701,6 +939,12 @@ cudaError_t stem_pack(const ConvGeom& g, const StemPlan& q, const void* x, void*
 
 bool conv_stem_applies(const ConvGeom& g) { return stem_plan(g).use; }
 
+bool conv_stem_pool_fusable(const ConvGeom& g) {
+    static const int env_cta2 = [] { const char* e = getenv("TCB_STEM_CTA2"); return e ? atoi(e) : 0; }();
+    const StemPlan q = stem_plan(g);
+    return q.use && g.k == 64 && q.wtiles == 1 && q.nq == 1 && (g.r == 3 || g.r == 5 || g.r == 7) && env_cta2 == 0;
+}
+
 cudaError_t conv_stem_pack_input(const ConvGeom& g, const void* x, void* workspace, cudaStream_t st) {
     const StemPlan q = stem_plan(g);
     if (!q.use || workspace == nullptr) return cudaErrorInvalidValue;
@@ -787,6 +1031,33 @@ cudaError_t conv_stem_fwd(const ConvGeom& g, const void* x, const void* w, const
     p.relu = ep.relu ? 1 : 0;
     static const int env_dbg = [] { const char* e = getenv("TCB_STEM_DBG"); return e ? atoi(e) : 0; }();
     p.dbg = env_dbg;
+    if (ep.pool_y) {  // fused 3x3 / 2 / 1 max pool
+        if (g.k != 64 || q.wtiles != 1 || q.nq != 1 || !ep.pool_arg || cta2) return cudaErrorInvalidValue;
+        p.pool_y = static_cast<__nv_bfloat16*>(ep.pool_y);
+        p.pool_arg = ep.pool_arg;
+        p.Po = (q.Ho - 1) / 2 + 1;
+        p.Pw = (q.Wo - 1) / 2 + 1;
+        p.pool_rows = g.n * p.Po;
+        const size_t psmem = size_t(q.stages) * q.stage_bytes + size_t(q.T) * q.b_bytes + 4 * size_t(q.stg_bytes) + 1024;
+        int stages = q.stages;
+        size_t smem = psmem;
+        while (smem > kSmemCap && stages > 2) {
+            --stages;
+            smem = size_t(stages) * q.stage_bytes + size_t(q.T) * q.b_bytes + 4 * size_t(q.stg_bytes) + 1024;
+        }
+        if (smem > kSmemCap) return cudaErrorInvalidValue;
+        p.stages = stages;
+        const int pgrid = std::min(p.pool_rows, num_sms());
+        p.pool_per_cta = (p.pool_rows + pgrid - 1) / pgrid;
+        const int grid2 = (p.pool_rows + p.pool_per_cta - 1) / p.pool_per_cta;
+        conv_tc_note_launch(ConvTcLaunchInfo{0, 5, g.k, 4, 0, 1, p.pool_rows, grid2, 0, 1});
+        switch (g.r) {
+            case 7: return launch_big(conv_stem_fwd_pool_kernel<7>, dim3(grid2), smem, st, p);
+            case 5: return launch_big(conv_stem_fwd_pool_kernel<5>, dim3(grid2), smem, st, p);
+            case 3: return launch_big(conv_stem_fwd_pool_kernel<3>, dim3(grid2), smem, st, p);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     const int grid = cta2 ? 2 * std::min((q.tiles + 1) / 2, num_sms() / 2) : std::min(q.tiles, num_sms());
     conv_tc_note_launch(ConvTcLaunchInfo{0, 5, g.k, 0, cta2 ? 1 : 0, 1, q.tiles, grid, 0, 1});
 #define TCB_STEM_FWD(BN, R, NQ)                                                                         \

@@ -33,6 +33,10 @@ struct Epilogue {
     // odd pixels of a 1x1 stride-2 conv) already hold 0 -- skip writing them
     // (only without residual / mask)
     bool uncovered_zero = false;
+    // fwd of a row-window stem (conv_stem.cu): also max-pool the ReLU'd output 3x3 / stride 2 /
+    // pad 1 into pool_y ([N][Ho/2][Wo/2][K]) and its argmax (uint8, maxpool_fwd's encoding)
+    void* pool_y = nullptr;
+    uint8_t* pool_arg = nullptr;
 };
 
 // ---- tensor-core implicit GEMM (tcgen05 / TMEM), bf16 in, fp32 accumulate ----
@@ -122,6 +126,8 @@ cudaError_t conv_stem_pack_u8(const ConvGeom& g, const uint8_t* src, int cl, voi
                               cudaStream_t st);
 cudaError_t conv_stem_wgrad(const ConvGeom& g, const void* dy, const void* x, float* dw, void* workspace,
                             cudaStream_t st, bool x_ready);
+// the stem forward can also produce the following 3x3 / 2 / 1 max pool (Epilogue::pool_y)
+bool conv_stem_pool_fusable(const ConvGeom& g);
 void conv_stem_set_mode(int on);  // 0 off (explicit im2col path), 1 on, -1 from $TCB_STEM
   // diagnostics: per-CTA role timing (8 x u64 per CTA) or nullptr
 // TMA epilogue for layers with at most `kb` 64-deep k-blocks (0 = never,

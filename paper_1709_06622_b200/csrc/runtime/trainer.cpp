@@ -153,6 +153,11 @@ struct tcb_trainer {
     // write of the input activation also refreshes its 4-channel rows in the
     // layer's workspace, so the step never repacks them
     int stem_node = -1;
+    // max pool node whose forward the stem kernel produces (3x3 / 2 / 1 right after a ReLU'd
+    // stem that feeds nothing else; config "fuse_stem_pool"), -1 if none. Off by default:
+    // bit-identical, but the epilogue pooling made the stem kernel 0.32 ms against 0.15 +
+    // 0.12 ms for the stem and the separate pool kernel (ResNet-50 bs256)
+    int fused_pool = -1;
     // CUDA graph of the step (config "cuda_graph", $TCB_GRAPH)
     bool use_graph = true;
     int eager_steps = 0, graph_launches = 0;
@@ -562,6 +567,20 @@ int allocate(tcb_trainer* t, bool dry = false) {
             if (nd.bias) colsum = std::max(colsum, column_sum_workspace(nd.n * nd.h * nd.w, nd.g.k));
         }
     }
+    t->fused_pool = -1;
+    if (t->stem_node >= 0 && t->cfg.value("fuse_stem_pool", false)) {
+        const Node& sn = t->nodes[t->stem_node];
+        int consumers = 0, pool = -1;
+        for (size_t j = 0; j < t->nodes.size(); ++j) {
+            const Node& c = t->nodes[j];
+            bool uses = c.in == t->stem_node || c.residual == t->stem_node;
+            for (int k : c.ins) uses = uses || k == t->stem_node;
+            if (!uses) continue;
+            ++consumers;
+            if (c.op == Op::MaxPool && c.in == t->stem_node && c.f == 3 && c.s == 2 && c.p == 1) pool = static_cast<int>(j);
+        }
+        if (consumers == 1 && pool >= 0 && sn.relu && conv_stem_pool_fusable(sn.g)) t->fused_pool = pool;
+    }
     for (Node& nd : t->nodes) {
         nd.chain.clear();
         nd.tmp.clear();
@@ -710,6 +729,11 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                 t->mark(idx, 0, st);
                 const void* wgt = t->bf16 ? static_cast<const void*>(static_cast<__nv_bfloat16*>(t->wc_ptr()) + nd.woff)
                                           : static_cast<const void*>(t->at<float>(t->off_param) + nd.woff);
+                if (t->bf16 && static_cast<int>(idx) == t->stem_node && t->fused_pool >= 0) {
+                    const Node& pn = t->nodes[t->fused_pool];  // the stem kernel also writes the pool
+                    ep.pool_y = t->at(pn.act);
+                    ep.pool_arg = t->at<uint8_t>(pn.argmax);
+                }
                 if (nd.algo_id == TCB_ALGO_WINOGRAD)
                     TRY_CUDA(winograd_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
                 else if (nd.algo_id == TCB_ALGO_FFT)
@@ -731,6 +755,7 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                 break;
             }
             case Op::MaxPool:
+                if (static_cast<int>(&nd - t->nodes.data()) == t->fused_pool) break;  // done by the stem kernel
                 TRY_CUDA(maxpool_fwd(t->dt, t->at(x->act), t->at(nd.act), t->at<uint8_t>(nd.argmax), x->n,
                                      x->h, x->w, x->c, nd.f, nd.s, nd.p, st));
                 t->launches++;
@@ -1647,6 +1672,7 @@ TCB_API int tcb_trainer_describe(tcb_trainer* t, char** json_out) {
             L["init_scale"] = nd.init_scale;
             L["algo"] = nd.algo;
             L["stem_rows"] = static_cast<int>(i) == t->stem_node;
+            L["stem_pool_fused"] = static_cast<int>(i) == t->stem_node && t->fused_pool >= 0;
             L["explicit_im2col"] = nd.narrow && static_cast<int>(i) != t->stem_node;
             L["packed_dgrad_weights"] = nd.pack_wT;
             const size_t first = nd.woff / std::max<size_t>(t->shard, 1);

@@ -143,6 +143,32 @@ def test_row_window_stem_batch8(oracle):
     assert t.describe()["layers"][1]["stem_rows"]
 
 
+@pytest.mark.parametrize("net", ["stem_pool", "resnet50_b2"])
+def test_stem_fused_max_pool_matches_separate_pool(net):
+    """The row-window stem forward writing the following 3x3/2/1 max pool itself
+    (config fuse_stem_pool) gives the same bits as the separate pool kernel:
+    pooled activation, argmax, the stem activation, loss, gradients and
+    parameters after two steps."""
+    from paper_1709_06622_b200.trainer import Trainer
+    if net == "stem_pool":
+        cfg = _models().from_net("input 48 46 3\nconv 7 2 3 64\npool 3 2 1\nconv 3 1 1 64\nfc 10\n",
+                                 batch=4, precision="bf16")
+    else:
+        cfg = _models().resnet50(batch=2, precision="bf16")
+    a, b = Trainer(dict(cfg, fuse_stem_pool=True)), Trainer(cfg)
+    for _ in range(2):
+        a.step()
+        b.step()
+    torch.cuda.synchronize()
+    la = a.describe()["layers"]
+    stem = next(L for L in la if L["op"] == "conv")
+    pool = next(L for L in la if L["op"] == "maxpool")
+    assert stem["stem_pool_fused"] and not next(L for L in b.describe()["layers"] if L["op"] == "conv")["stem_pool_fused"]
+    for name in (f"act:{stem['index']}", f"act:{pool['index']}", f"argmax:{pool['index']}", "grad", "param", "loss"):
+        ta, tb = a.tensor(name), b.tensor(name)
+        assert torch.equal(ta, tb), name
+
+
 def test_explicit_im2col_first_layer_batch8(oracle):
     """An 11x11/4 first layer (AlexNet-style; stride 4 is outside the stem
     kernels): explicit-im2col fwd (TMA epilogue) and wgrad (col kept from the
