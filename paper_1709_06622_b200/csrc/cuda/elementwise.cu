@@ -285,8 +285,15 @@ __global__ void sgd4_kernel(float4* __restrict__ w, const float4* __restrict__ g
         v[i] = vi;
         w[i] = wi;
         if (wc) {
+            if constexpr (sizeof(CT) == 2) {  // the four bf16 copies as one 8-byte store
+                __align__(8) CT q[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) wc[4 * i + j] = from_f32<CT>(wp[j]);
+                for (int j = 0; j < 4; ++j) q[j] = from_f32<CT>(wp[j]);
+                reinterpret_cast<uint2*>(wc)[i] = *reinterpret_cast<const uint2*>(q);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) wc[4 * i + j] = from_f32<CT>(wp[j]);
+            }
         }
     }
 }
