@@ -1,35 +1,41 @@
 // Row-window convolution for the narrow RGB stem (sm_100a): ResNet's 7x7/2
-// conv1, Inception's 3x3/2, any even-stride first layer over <= 4 real channels.
+// conv1, Inception's 3x3/2 -- stride-2 first layers over <= 4 real channels
+// (R in {3, 5, 7, 11}, K in {32, 64, 128}).
 //
 // The explicit-im2col path (conv_tc.cu, narrow_plan) writes a 1.2 GB patch
 // matrix for the ResNet-50 bs256 stem and reads it back twice (fwd GEMM and
 // wgrad GEMM): 335 + 249 + 291 us of the 12 ms step, all HBM time. Here the
-// patch matrix is never materialised. The input is stored once as a "stem
-// row" tensor x4[n][h][u][4] (4 bf16 channels = 8 bytes per pixel, the
-// conv's left padding as zero columns u < pad_w, zero columns up to Wst on the
-// right). One output pixel (ho, wo) reads, per filter row r, the 8 stored
-// pixels u = wo*sw .. wo*sw + 7 of input row ho*sh - pad_h + r: 32 contiguous
-// bf16 = one 64-byte K-chunk holding filter columns s = 0..7 (s >= S weighted
-// by zero). Consecutive wo start stride_w pixels = 8*stride_w bytes apart, so
-// a TILED TMA map with dims {32 elements, windows, H, N} and strides
-// {8*sw, 8*Wst, 8*Wst*H} bytes (overlapping rows) delivers the GEMM A tile of
-// a whole output row in one box per filter row: {32, BW, 1, 1}, 64-byte
-// swizzle, rows out of the image (vertical padding) zero-filled. Wider
-// filters (S > 8) take nq = ceil(S/8) chunks per filter row, chunk q starting
-// 8q/sw windows further (requires sw | 8).
+// patch matrix is never materialised. The input is stored once more as a
+// "stem row" tensor x4[n][h][u][4] (4 bf16 channels = 8 bytes per pixel, the
+// conv's left padding as zero columns u < pad_w, zero columns up to Wst, a
+// multiple of 16 pixels), written by the executor's uint8 input preparation.
+// Output pixel (ho, wo) reads, per filter row r, the 8 stored pixels
+// u = 2wo .. 2wo + 7 of input row 2ho - pad_h + r: 32 contiguous bf16 = one
+// K-chunk holding filter columns s = 0..7 (s >= S weighted by zero; S > 8
+// takes nq = 2 chunks per filter row).
 //
-//   fwd   : D[wo][k] = sum_(r,q) A_(r,q)[wo][32] * Wp_(r,q)[k][32]^T, M = 128
-//           rows (BW <= 128 valid), N = K, K-major SW64 both sides, the
-//           packed weights resident in shared memory; epilogue bias / ReLU ->
-//           bf16 y[n][ho][wo][K]. Warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
-//           from double-buffered TMEM.
-//   wgrad : D[(r,q,e)][k] = sum over positions of x4-window^T * dy: the same
-//           x boxes as MN-major A operands (M = 4 chunks x 32 elements per
-//           M = 128 tile, chunks one box apart = the descriptor's leading byte
-//           offset), dy boxes {K, BW} as MN-major B, K-steps of 16 positions.
-//           Every CTA accumulates its contiguous range of output rows in TMEM
-//           and writes one fp32 partial; a fixed-order reduction sums the
-//           partials and scatters into dw[K][R][S][C] (zero on padded c, s).
+//   fwd   : per output row, the R stored rows (one TMA box of 16-pixel groups
+//           each, no swizzle). Consecutive positions start 16 bytes apart, so
+//           a no-swizzle K-major descriptor with LBO 16 / SBO 128 (8-row x
+//           16-byte core matrices overlapping each other) IS the row's im2col
+//           window: D[wo][k] = sum_r A_r * Wp_r^T, M = 128 rows (BW <= 128
+//           valid), N = K, 2 MMAs per filter row with compile-time descriptor
+//           offsets (the N = 64 MMAs are issue-bound), packed weights resident
+//           (SW64); bias / ReLU epilogue through a swizzled staging tile and a
+//           TMA store. Warp 0 TMA, warp 1 MMA, warps 2-9 epilogue from four
+//           TMEM accumulators. Variants: CTA pairs ($TCB_STEM_CTA2) and the
+//           following 3x3/2/1 max pool fused into the epilogue (config
+//           fuse_stem_pool) -- both correct and both measured slower.
+//   wgrad : D[(r, e)][k] = sum over positions of window^T * dy. The windows are
+//           overlapping-row TMA boxes {32 el, BW, 1, 1} of a map whose row
+//           stride (16 bytes) is smaller than its 64-byte inner extent, 64-byte
+//           swizzled, used as MN-major A operands (4 filter rows per M = 128
+//           tile, one box apart = the descriptor's leading byte offset); dy
+//           boxes {K, BW} are the MN-major B. Two output rows per tile share
+//           their R - 2 common input rows (9 boxes instead of 14 for 7x7).
+//           Every CTA accumulates its contiguous range of rows in TMEM and
+//           writes one fp32 partial; a fixed-order reduction sums the partials
+//           and scatters into dw[K][R][S][C] (zero on padded c, s).
 #include <algorithm>
 #include <cstdlib>
 
