@@ -515,6 +515,7 @@ WinPlan win_plan(const ConvGeom& g, int mode) {
     q.win_stride = (q.win_bytes + 1023) / 1024 * 1024;
     q.slices = q.Ca / 64;
     q.bn = q.Ncol <= 64 ? 64 : q.Ncol <= 128 ? 128 : 256;
+    if (q.rect && q.bn != 64) return q;  // rectangular tiles: validated for 64-wide single-CTA tiles only
     // Measured (scripts/win_ab2.sh, bs256): the window wins where the im2col path's
     // 64-column tiles re-read each input pixel per tap at a low MMA width (ResNet
     // stage 1: fwd 117 -> 77 us, dgrad 130 -> 78 us); with 128/256-column tiles the
@@ -530,7 +531,7 @@ WinPlan win_plan(const ConvGeom& g, int mode) {
     static const int env_wst = [] { const char* e = getenv("TCB_WIN_WSTAGES"); return e ? atoi(e) : 0; }();
     static const int env_bst = [] { const char* e = getenv("TCB_WIN_BSTAGES"); return e ? atoi(e) : 0; }();
     // CTA pairs measured slower at N = 64 (stage 1 fwd: 107 vs 77 us single)
-    q.cta2 = g.n >= 2 && q.bn >= 128 && env_cta2 != 0;
+    q.cta2 = g.n >= 2 && q.bn >= 128 && env_cta2 != 0 && !q.rect;
     q.b_bytes = static_cast<uint32_t>(q.bn) * 64 * 2 / (q.cta2 ? 2 : 1);
     const size_t b_all = size_t(q.b_bytes) * q.R * q.S * q.slices;
     q.bres = q.n_tiles == 1 && b_all <= 96 * 1024 && env_bres != 0;
@@ -836,8 +837,9 @@ WgPlan wgrad_plan(const ConvGeom& g) {
     if (q.bn > 256) return q;
     // M tiles beyond 512 TMEM columns run as tap groups: one launch per group over the same
     // windows (balanced: ceil(mtiles / groups) tiles each)
-    q.groups = (q.mtiles * q.bn + 511) / 512;
-    q.per_group = (q.mtiles + q.groups - 1) / q.groups;
+    const int fit = 512 / q.bn;  // M tiles whose accumulators fit the 512 TMEM columns
+    q.groups = (q.mtiles + fit - 1) / fit;
+    q.per_group = (q.mtiles + q.groups - 1) / q.groups;  // balanced, <= fit
     if (q.groups > 3) return q;
     q.wpos = wg_positions();
     const int kWP = q.wpos;

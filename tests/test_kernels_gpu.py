@@ -170,6 +170,8 @@ WINDOW_CASES = [  # (name, n, h, w, c, k, (r, s), (ph, pw), expected fwd / dgrad
     ("rn50_s3_3x3_k256", 2, 14, 14, 256, 256, (3, 3), (1, 1), dict(fwd=(256, 1, 0), dgrad=(256, 1, 0))),
     ("incep_5x5_48_64", 3, 35, 35, 64, 64, (5, 5), (2, 2), dict(fwd=(64, 0, 0), dgrad=(64, 0, 0))),
     ("incep_7x1_192", 2, 17, 17, 192, 192, (7, 1), (3, 0), dict(fwd=(256, 1, 0), dgrad=(256, 1, 0))),
+    # window weight gradient as tap groups: 14 tap-slices x K = 192 -> 7 M tiles, 2 per group
+    ("incep_7x1_128_192", 2, 17, 17, 128, 192, (7, 1), (3, 0), dict(fwd=(256, 1, 0), dgrad=(128, 1, 0))),
     # wide rows: rectangular window tiles (Inception Conv2d_2a / 2b, VGG conv1_2), ragged corners
     ("incep_2a_wide_valid", 2, 37, 149, 64, 64, (3, 3), (0, 0), dict(fwd=(64, 0, 1), dgrad=(64, 0, 1))),
     ("incep_2b_wide", 2, 21, 147, 64, 64, (3, 3), (1, 1), dict(fwd=(64, 0, 1), dgrad=(64, 0, 1))),
