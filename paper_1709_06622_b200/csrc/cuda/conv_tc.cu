@@ -94,6 +94,9 @@ struct Params {
     // [M x Kdim] x [Ncol x Kdim]^T problems in contiguous planes; 3-D tensor maps
     // carry the plane index, outputs (and wgrad partials) are [split][batch][M][Ncol]
     int batch;
+    // split-K forward (fc layers / K-deep plain GEMMs with few output tiles): fp32
+    // partials [split][M][Ncol]; bias / residual / ReLU applied by fwd_split_reduce
+    float* fwd_partial;
 };
 
 struct TileCoord {
@@ -289,8 +292,10 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord&
     const bool has_relu = kDyn ? p.relu != 0 : kRelu, has_mask = kDyn ? p.mask != nullptr : kMask;
     const ConvShape& s = p.s;
     if (m >= s.M || col0 >= s.Ncol) return;
-    if constexpr (MODE == ConvMode::Wgrad) {
-        float* out = static_cast<float*>(p.out) +
+    bool partial = MODE == ConvMode::Wgrad;
+    if constexpr (kDyn && MODE == ConvMode::Fwd) partial = p.fwd_partial != nullptr;
+    if (partial) {
+        float* out = (MODE == ConvMode::Wgrad ? static_cast<float*>(p.out) : p.fwd_partial) +
                      ((static_cast<size_t>(tc.split) * p.batch + tc.b) * s.M + m) * s.Ncol + col0;
         if (col0 + 32 <= s.Ncol) {
 #pragma unroll
@@ -1033,7 +1038,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             // one instantiation per side-input / ReLU combination the executor issues; bias
             // (fc layers, from_net convs) takes the run-time-checked general one
             const int f = (p.residual ? 1 : 0) | (p.relu ? 2 : 0) | (p.mask ? 4 : 0);
-            if (p.bias) run(F_{}, F_{}, F_{}, F_{}, T_{});
+            if (p.bias || p.fwd_partial) run(F_{}, F_{}, F_{}, F_{}, T_{});
             else if (f == 0) run(F_{}, F_{}, F_{}, F_{}, F_{});
             else if (f == 2) run(F_{}, F_{}, T_{}, F_{}, F_{});
             else if (f == 3) run(F_{}, T_{}, T_{}, F_{}, F_{});
@@ -1366,7 +1371,7 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
     p.n_tiles = (p.s.Ncol + BN - 1) / BN;
     p.kb_total = (p.s.Kdim + BK - 1) / BK;
     p.cta2 = CTA2 ? 1 : 0;
-    if (MODE != ConvMode::Wgrad) {
+    if (MODE != ConvMode::Wgrad && !(MODE == ConvMode::Fwd && p.fwd_partial)) {
         p.splits = 1;
         p.kb_per_split = p.kb_total;
     }
@@ -1415,7 +1420,7 @@ int g_epi_kb_spatial = -1;  // ... and for spatial (im2col) layers
 // (Inception-v3's 5x5 / 1x7 / 7x1 branches).
 template <ConvMode MODE>
 bool use_epi(const Params& p) {
-    if (MODE == ConvMode::Wgrad) return false;
+    if (MODE == ConvMode::Wgrad || p.fwd_partial) return false;
     // batched plain GEMMs store through a 3-D map (no side inputs there)
     if (p.batch > 1 && (p.residual || p.mask)) return false;
     if (MODE == ConvMode::Dgrad && (p.s.sh != 1 || p.s.sw != 1)) return false;
@@ -1472,7 +1477,7 @@ cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, c
     if constexpr (LOAD == kPlain || LOAD == kIm2col) {
         const bool pair = MODE == ConvMode::Wgrad
                               ? p.cta2 != 0
-                              : cta2_wanted(LOAD, bn, (p.s.M + BM - 1) / BM, (p.s.Kdim + BK - 1) / BK);
+                              : !p.fwd_partial && cta2_wanted(LOAD, bn, (p.s.M + BM - 1) / BM, (p.s.Kdim + BK - 1) / BK);
         if (pair && bn == 256) return launch<MODE, 256, LOAD, 0, true>(p, a_matrix, b_matrix, st);
         if (pair && bn == 128) return launch<MODE, 128, LOAD, 0, true>(p, a_matrix, b_matrix, st);
     }
@@ -1530,6 +1535,84 @@ cudaError_t dispatch(Params& p, const void* a_matrix, const void* b_matrix, cuda
     return dispatch_bn<MODE, kGather>(p, a_matrix, b_matrix, st);
 }
 
+// A fully connected layer (filter = the whole unpadded input map, 1x1 output)
+// is the 1x1 conv over a 1x1 image of H*W*C channels: same memory (NHWC rows
+// of x and KRSC rows of w are both [rows][H*W*C]), plain TMA operands.
+bool fc_geometry(const ConvGeom& g) {
+    return g.r == g.h && g.s == g.w && g.pad_h == 0 && g.pad_w == 0 && g.ho() == 1 && g.wo() == 1 &&
+           (g.h > 1 || g.w > 1);
+}
+
+ConvGeom fc_as_1x1(const ConvGeom& g) {
+    return fc_geometry(g) ? ConvGeom{g.n, 1, 1, g.h * g.w * g.c, g.k, 1, 1, 0, 0, 1, 1} : g;
+}
+
+// Split-K forward: a plain GEMM whose output tiles fill under half the SMs but
+// whose reduction is deep (VGG fc6 at batch 64: 16 tiles x 392 k-blocks) runs
+// `splits` k-ranges as separate units into fp32 partials, then one reduce pass
+// adds them in fixed split order and applies bias / residual / ReLU.
+// $TCB_FWD_SPLIT=0 disables.
+SplitPlan fwd_split_plan(const ConvGeom& g0) {
+    static const int enabled = [] {
+        const char* e = getenv("TCB_FWD_SPLIT");
+        return e ? atoi(e) : 1;
+    }();
+    const SplitPlan none{1, 0};
+    if (!enabled || force_gather()) return none;
+    const ConvGeom g = fc_as_1x1(g0);
+    const ConvShape s = make_shape(g, ConvMode::Fwd);
+    if (!plain_geometry(s) || s.Ncol % 8 != 0) return none;
+    const int bn = pick_bn(s.Ncol);
+    const int tiles = ((s.M + BM - 1) / BM) * ((s.Ncol + bn - 1) / bn);
+    const int kb = (s.Kdim + BK - 1) / BK;
+    const int slots = num_sms() - g_sm_reserve;
+    if (2 * tiles > slots || kb < 16) return none;
+    const int want = std::min({slots / tiles, kb / 4, 32});
+    if (want < 2) return none;
+    const int per = (kb + want - 1) / want;
+    return {(kb + per - 1) / per, per};
+}
+
+// y[m][n] = act(sum_k parts[k][m][n] + bias[n] + residual[m][n]), 8 columns per
+// thread (Ncol % 8 == 0), splits summed in index order (deterministic).
+__global__ void fwd_split_reduce_kernel(const float* __restrict__ parts, int splits, int rows, int cols,
+                                        const float* __restrict__ bias, const __nv_bfloat16* __restrict__ residual,
+                                        int relu, __nv_bfloat16* __restrict__ y) {
+    pdl_wait();
+    pdl_trigger();
+    const int c8 = cols / 8;
+    const size_t n8 = size_t(rows) * c8;
+    const size_t plane = size_t(rows) * cols;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n8; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t off = i * 8;
+        const int col = static_cast<int>(i % c8) * 8;
+        const float4* src = reinterpret_cast<const float4*>(parts + off);
+        float4 a = __ldcs(src), b = __ldcs(src + 1);
+        for (int k = 1; k < splits; ++k) {
+            const float4* q = reinterpret_cast<const float4*>(parts + k * plane + off);
+            const float4 u = __ldcs(q), v = __ldcs(q + 1);
+            a.x += u.x; a.y += u.y; a.z += u.z; a.w += u.w;
+            b.x += v.x; b.y += v.y; b.z += v.z; b.w += v.w;
+        }
+        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        if (bias) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] += __ldg(bias + col + j);
+        }
+        if (residual) {
+            float r[8];
+            unpack8(__ldg(reinterpret_cast<const uint4*>(residual + off)), r);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] += r[j];
+        }
+        if (relu) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = fmaxf(v[j], 0.f);
+        }
+        *reinterpret_cast<uint4*>(y + off) = pack8(v);
+    }
+}
+
 }  // namespace
 
 void conv_tc_set_force_gather(int on) { g_force_gather = on ? 1 : 0; }
@@ -1553,6 +1636,11 @@ size_t conv_tc_workspace(const ConvGeom& g, ConvMode mode) {
     if (q.use && mode == ConvMode::Wgrad)
         return align256(q.col_bytes) + align256(size_t(g.k) * q.kc * 4) +
                conv_tc_workspace(q.g1, ConvMode::Wgrad);
+    if (mode == ConvMode::Fwd) {
+        const SplitPlan fs = fwd_split_plan(g);
+        const ConvGeom g1 = fc_as_1x1(g);
+        return fs.splits > 1 ? size_t(fs.splits) * g1.n * g1.h * g1.w * g1.k * sizeof(float) : 0;
+    }
     if (mode != ConvMode::Wgrad) return 0;
     const ConvShape s = make_shape(g, mode);
     const int bn = wgrad_bn(s);
@@ -1566,7 +1654,7 @@ bool conv_tc_narrow(const ConvGeom& g) { return conv_stem_applies(g) || narrow_p
 int conv_tc_launches(const ConvGeom& g, ConvMode mode, bool cols_ready, bool counters) {
     if (mode != ConvMode::Dgrad && conv_stem_applies(g)) return conv_stem_launches(g, mode, cols_ready);
     const NarrowPlan q = narrow_plan(g);
-    if (mode == ConvMode::Fwd) return q.use ? 3 : 1;
+    if (mode == ConvMode::Fwd) return q.use ? 3 : (fwd_split_plan(g).splits > 1 ? 2 : 1);
     if (mode == ConvMode::Dgrad) return g.stride_h * g.stride_w;
     const ConvGeom& gw = q.use ? q.g1 : g;
     if (!q.use && !force_gather() && conv_win_wgrad_applies(g)) return conv_win_wgrad_launches(g);
@@ -1598,6 +1686,23 @@ cudaError_t conv_tc_fwd(const ConvGeom& g, const void* x, const void* w, const E
         a_matrix = ws;
         b_matrix = wp;
     } else {
+        const SplitPlan fs = workspace ? fwd_split_plan(g) : SplitPlan{1, 0};
+        if (fs.splits > 1) {
+            const ConvGeom g1 = fc_as_1x1(g);
+            p.s = make_shape(g1, ConvMode::Fwd);
+            p.a = static_cast<const __nv_bfloat16*>(x);
+            p.out = y;
+            p.fwd_partial = static_cast<float*>(workspace);
+            p.splits = fs.splits;
+            p.kb_per_split = fs.kb_per_split;
+            cudaError_t e = dispatch<ConvMode::Fwd>(p, x, w, st);
+            if (e != cudaSuccess) return e;
+            const int c8 = p.s.M * (g1.k / 8);
+            return launch_pdl(fwd_split_reduce_kernel, dim3(std::max(1, std::min((c8 + 255) / 256, 4 * num_sms()))),
+                              dim3(256), 0, st, static_cast<const float*>(workspace), fs.splits, p.s.M, g1.k,
+                              ep.bias, static_cast<const __nv_bfloat16*>(ep.residual), ep.relu ? 1 : 0,
+                              static_cast<__nv_bfloat16*>(y));
+        }
         if (!force_gather() && conv_win_applies(g, ConvMode::Fwd)) return conv_win_fwd(g, x, w, ep, y, st);
         p.s = make_shape(g, ConvMode::Fwd);
     }

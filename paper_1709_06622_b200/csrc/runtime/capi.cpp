@@ -54,7 +54,8 @@ ConvPlanLayout conv_plan_layout(const ConvGeom& g, int algo, int prec) {
     const size_t P = size_t(g.n) * g.ho() * g.wo();
     const DType dt = prec == TCB_PREC_BF16 ? DType::BF16 : DType::F32;
     if (algo == TCB_ALGO_GEMM) {
-        L.wgrad = prec == TCB_PREC_BF16   ? conv_tc_workspace(g, ConvMode::Wgrad)
+        L.wgrad = prec == TCB_PREC_BF16   ? std::max(conv_tc_workspace(g, ConvMode::Wgrad),
+                                                     conv_tc_workspace(g, ConvMode::Fwd))
                   : prec == TCB_PREC_TF32 ? conv_tf32_workspace(g, ConvMode::Wgrad)
                                           : conv_ffma_workspace(g, ConvMode::Wgrad);
         L.wT = prec == TCB_PREC_BF16 ? size_t(g.k) * g.r * g.s * g.c * 2 : 0;
@@ -184,7 +185,10 @@ TCB_API int tcb_conv_fwd(const tcb_conv_plan* plan, const void* x, const void* w
     switch (plan->algo) {
         case TCB_ALGO_GEMM:
             e = plan->prec == TCB_PREC_BF16 ? conv_tc_fwd(plan->g, x, w, ep, y, st,
-                                                          plan->g.c_valid > 0 ? workspace : nullptr)
+                                                          plan->g.c_valid > 0 || (!conv_tc_narrow(plan->g) &&
+                                                                                  conv_tc_workspace(plan->g, ConvMode::Fwd))
+                                                              ? workspace
+                                                              : nullptr)
                 : plan->prec == TCB_PREC_TF32
                     ? conv_tf32_fwd(plan->g, static_cast<const float*>(x),
                                     static_cast<const float*>(w), ep, static_cast<float*>(y), st)

@@ -553,7 +553,8 @@ int allocate(tcb_trainer* t, bool dry = false) {
                     t->algorithm_ws_bytes += round_up(std::max<size_t>(nb, 1), kAlign);
                 }
                 else
-                    ws = std::max(ws, t->bf16   ? conv_tc_workspace(nd.g, ConvMode::Wgrad)
+                    ws = std::max(ws, t->bf16   ? std::max(conv_tc_workspace(nd.g, ConvMode::Wgrad),
+                                                           conv_tc_workspace(nd.g, ConvMode::Fwd))
                                       : t->tf32 ? conv_tf32_workspace(nd.g, ConvMode::Wgrad)
                                                 : conv_ffma_workspace(nd.g, ConvMode::Wgrad));
                 nd.pack_wT = t->bf16 && nd.need_dgrad && conv_tc_dgrad_needs_pack(nd.g);
@@ -740,7 +741,10 @@ int forward(tcb_trainer* t, cudaStream_t st) {
                     TRY_CUDA(fft_fwd(nd.g, t->dt, t->at(x->act), wgt, ep, t->at(nd.act), t->at(t->off_ws), st));
                 else if (t->bf16)
                     TRY_CUDA(conv_tc_fwd(nd.g, t->at(x->act), static_cast<__nv_bfloat16*>(t->wc_ptr()) + nd.woff,
-                                         ep, t->at(nd.act), st, nd.narrow ? t->at(nd.nws) : nullptr,
+                                         ep, t->at(nd.act), st,
+                                         nd.narrow ? t->at(nd.nws)
+                                         : conv_tc_workspace(nd.g, ConvMode::Fwd) ? t->at(t->off_ws)
+                                                                                  : nullptr,
                                          static_cast<int>(idx) == t->stem_node));
                 else if (t->tf32)
                     TRY_CUDA(conv_tf32_fwd(nd.g, t->at<float>(x->act), t->at<float>(t->off_param) + nd.woff,

@@ -251,6 +251,36 @@ def test_wgrad_many_splits_and_cta_pairs(oracle):
     assert torch.equal(dw, plan.wgrad(_to_dev(dy, torch.bfloat16), _to_dev(x, torch.bfloat16)))
 
 
+@pytest.mark.parametrize("spec", [(8, 7, 512, 4096, 7, 16), (2, 14, 1024, 256, 1, 4), (3, 5, 2048, 1000, 1, 4)],
+                         ids=["vgg_fc6_n8", "rn50_1x1_n2", "fc_like_1x1_ragged"])
+def test_fc_forward_split_k(oracle, spec):
+    """Split-K forward of plain GEMMs with few output tiles and a deep reduction:
+    VGG fc6 at a reduced batch (7x7x512 -> 4096, depth 25,088) runs as a 1x1
+    GEMM over H*W*C channels; small-batch 1x1 layers (M = N*H*W rows) likewise.
+    k-ranges go to fp32 partials, reduced with bias + residual + ReLU in fixed
+    split order; vs the fp64 oracle, and bitwise repeatable."""
+    dev = _dev()
+    n, hw, c, k, r, tiles = spec
+    g = dev.geom(n, hw, hw, c, k, r)
+    gd = g.as_dict()
+    plan = dev.ConvPlan(g, "gemm", "bf16")
+    assert plan.workspace_bytes > 0
+    x = _rand(oracle, (n, hw, hw, c), 1, 1.0, True)
+    wt = _rand(oracle, (k, r, r, c), 2, (6.0 / (r * r * c)) ** 0.5, True)
+    bias = _rand(oracle, (k,), 3, 0.1)
+    res = _rand(oracle, (n, g.ho, g.wo, k), 4, 0.5, True)
+    xd, wd = _to_dev(x, torch.bfloat16), _to_dev(wt, torch.bfloat16)
+    bd, rd = _to_dev(bias, torch.float32), _to_dev(res, torch.bfloat16)
+    y = plan.fwd(xd, wd, bias=bd, residual=rd, relu=True)
+    info = dev.last_launch()
+    assert info["mode"] == 0 and info["splits"] >= 2 and info["units"] == tiles * info["splits"], info
+    ref = oracle.conv_fwd(gd, x, wt, bias=bias, residual=res, relu=True)
+    assert rel_err(_host(y), ref) <= 1e-2
+    assert torch.equal(y, plan.fwd(xd, wd, bias=bd, residual=rd, relu=True))
+    y0 = plan.fwd(xd, wd)
+    assert rel_err(_host(y0), oracle.conv_fwd(gd, x, wt)) <= 1e-2
+
+
 def test_fill_and_labels_bit_exact(oracle):
     dev = _dev()
     for tag, lo, hi in ((1, -1.0, 1.0), (99, -0.05, 0.05), (7, 0.0, 3.0)):
