@@ -61,7 +61,8 @@ struct Cfg {
              : EPI == 2 ? (BN == 256 ? 3 : BN == 192 ? 4 : BN == 128 ? 4 : 5)
                         : (BN == 256 ? 4 : BN == 192 ? 5 : BN == 128 ? 6 : 8);
     static constexpr int kRingBytes = kStages * kStageBytes;
-    static constexpr int kEpiWarpBytes = EPI * 2 * 2048;  // slot = {in0/out, in1}, 32x32 bf16 each
+    // EPI: slot = {in0/out, in1}, 32x32 bf16 each; register epilogue: one 32x32 bf16 staging tile
+    static constexpr int kEpiWarpBytes = EPI == 0 ? 2048 : EPI * 2 * 2048;
     static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
     static constexpr uint32_t kTmemCols = BN == 192 ? 512 : 2 * BN;  // two accumulators (pow2)
     static constexpr size_t kSmem = size_t(kRingBytes) + kEpiBytes + 1024 + 512;
@@ -97,6 +98,7 @@ struct Params {
     // split-K forward (fc layers / K-deep plain GEMMs with few output tiles): fp32
     // partials [split][M][Ncol]; bias / residual / ReLU applied by fwd_split_reduce
     float* fwd_partial;
+    int stage_epi;  // register epilogue stores through shared memory (whole sectors)
 };
 
 struct TileCoord {
@@ -287,13 +289,64 @@ __device__ __forceinline__ void load_side(const Params& p, size_t row, int col0,
 template <ConvMode MODE, bool kBias, bool kRes, bool kRelu, bool kMask, bool kDyn = false>
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const TileCoord& tc, int m,
                                                size_t row, int col0, const uint32_t (&acc)[32],
-                                               const SideIn& side) {
+                                               const SideIn& side, uint8_t* stg = nullptr) {
     const bool has_bias = kDyn ? p.bias != nullptr : kBias, has_res = kDyn ? p.residual != nullptr : kRes;
     const bool has_relu = kDyn ? p.relu != 0 : kRelu, has_mask = kDyn ? p.mask != nullptr : kMask;
     const ConvShape& s = p.s;
-    if (m >= s.M || col0 >= s.Ncol) return;
+    if (col0 >= s.Ncol) return;  // warp-uniform
     bool partial = MODE == ConvMode::Wgrad;
     if constexpr (kDyn && MODE == ConvMode::Fwd) partial = p.fwd_partial != nullptr;
+    if (MODE != ConvMode::Wgrad && !partial && stg != nullptr && col0 + 32 <= s.Ncol) {
+        // Staged store (whole warp, out-of-range rows included): the warp's 32 rows x
+        // 64 B go through shared memory (16-byte units XOR-swizzled by row pair:
+        // conflict-free both ways) and leave as 8 rows x 64 B per store instruction,
+        // i.e. whole 32-byte sectors instead of 32 half-sector writes to 32 rows.
+        const int lane = threadIdx.x & 31;
+        const size_t base = (static_cast<size_t>(tc.b) * s.M + row) * s.Ncol + col0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(acc[8 * g + i]);
+            const int c = col0 + 8 * g;
+            if (has_bias) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] += __ldg(p.bias + c + i);
+            }
+            if (has_res) {
+                float r[8];
+                unpack8(side.r[g], r);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] += r[i];
+            }
+            if (has_relu) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (has_mask) {
+                float mk[8];
+                unpack8(side.k[g], mk);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = mk[i] > 0.f ? v[i] : 0.f;
+            }
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4)) = pack8(v);
+        }
+        __syncwarp();
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+        const int part = lane & 3;
+        const int valid = m < s.M;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int r = it * 8 + (lane >> 2);
+            const unsigned long long rb = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(base), r);
+            const int ok = __shfl_sync(0xffffffffu, valid, r);
+            const uint4 val = *reinterpret_cast<const uint4*>(stg + r * 64 + ((part ^ ((r >> 1) & 3)) << 4));
+            if (ok) *reinterpret_cast<uint4*>(out + rb + part * 8) = val;
+        }
+        __syncwarp();  // the next chunk reuses the staging rows
+        return;
+    }
+    if (m >= s.M) return;
     if (partial) {
         float* out = (MODE == ConvMode::Wgrad ? static_cast<float*>(p.out) : p.fwd_partial) +
                      ((static_cast<size_t>(tc.split) * p.batch + tc.b) * s.M + m) * s.Ncol + col0;
@@ -991,6 +1044,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         constexpr int kChunks = BN / 32, kHalfChunks = kChunks / 2;
         const int c_begin = half * kHalfChunks, c_end = c_begin + kHalfChunks;
         const int row = quarter * 32 + (tid & 31);
+        uint8_t* const stg = (MODE != ConvMode::Wgrad && p.stage_epi) ? smem + C::kRingBytes + (warp - 4) * 2048
+                                                                      : nullptr;
         auto run = [&](auto bias_c, auto res_c, auto relu_c, auto mask_c, auto dyn_c) {
             constexpr bool kBias = decltype(bias_c)::value, kRes = decltype(res_c)::value;
             constexpr bool kRelu = decltype(relu_c)::value, kMask = decltype(mask_c)::value;
@@ -1019,7 +1074,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                                                 acc * BN + c * 32,
                                             v);
                     ptx::tmem_ld_wait();
-                    epilogue_chunk<MODE, kBias, kRes, kRelu, kMask, kDyn>(p, tc, m, orow, tc.nt * BN + c * 32, v, cur);
+                    epilogue_chunk<MODE, kBias, kRes, kRelu, kMask, kDyn>(p, tc, m, orow, tc.nt * BN + c * 32, v, cur,
+                                                                          stg);
                     cur = nxt;
                 }
                 ptx::tc_fence_before();
@@ -1376,6 +1432,11 @@ cudaError_t launch(Params& p, const void* a_matrix, const void* b_matrix, cudaSt
         p.kb_per_split = p.kb_total;
     }
     if (p.batch < 1) p.batch = 1;
+    static const int stage_epi = [] {
+        const char* e = getenv("TCB_EPI_STAGE");
+        return e ? atoi(e) : 1;
+    }();
+    p.stage_epi = stage_epi;
     p.num_tiles = (CTA2 ? p.m_pairs : p.m_tiles) * p.n_tiles * p.batch * p.splits;
     const int sms = std::max(2, num_sms() - g_sm_reserve);
     const int grid = CTA2 ? 2 * std::min(p.num_tiles, sms / 2) : std::min(p.num_tiles, sms);
