@@ -63,6 +63,7 @@ struct WinParams {
     int relu;
     FastDiv d_wp, d_tiles, d_ntiles;
     unsigned long long* dbg;  // optional per-CTA role timing (tcb_conv_win_debug)
+    uint32_t stg_off;         // epilogue staging tiles (8 x 2 KB) at this smem offset; 0 = direct stores
 };
 
 __device__ __forceinline__ long long clk(bool on) { return on ? clock64() : 0; }
@@ -168,6 +169,68 @@ __device__ __forceinline__ void store_chunk(const WinParams& p, size_t orow, int
             out[i] = __float2bfloat16_rn(x);
         }
     }
+}
+
+// Whole-warp variant for full 32-column chunks (out-of-range rows included,
+// `valid` masks them): the warp's 32 rows x 64 B are staged in shared memory
+// (16-byte units XOR-swizzled by row pair, conflict-free both ways) and stored
+// 8 rows x 64 B per instruction: whole 32-byte sectors instead of 32 half-sector
+// writes to 32 rows.
+template <bool kBias, bool kRes, bool kRelu, bool kMask>
+__device__ __forceinline__ void store_chunk_staged(const WinParams& p, size_t orow, int col0, const uint32_t (&acc)[32],
+                                                   bool valid, uint8_t* stg) {
+    const int lane = threadIdx.x & 31;
+    const size_t base = orow * p.Ncol + col0;
+    uint4 rv[4] = {}, mv[4] = {};
+    if (valid) {
+        if constexpr (kRes) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) rv[g] = __ldg(reinterpret_cast<const uint4*>(p.residual + base) + g);
+        }
+        if constexpr (kMask) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) mv[g] = __ldg(reinterpret_cast<const uint4*>(p.mask + base) + g);
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(acc[8 * g + i]);
+        if constexpr (kBias) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += __ldg(p.bias + col0 + 8 * g + i);
+        }
+        if constexpr (kRes) {
+            float r[8];
+            unpack8(rv[g], r);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += r[i];
+        }
+        if constexpr (kRelu) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        if constexpr (kMask) {
+            float mk[8];
+            unpack8(mv[g], mk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = mk[i] > 0.f ? v[i] : 0.f;
+        }
+        *reinterpret_cast<uint4*>(stg + lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4)) = pack8(v);
+    }
+    __syncwarp();
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+    const int part = lane & 3;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        const int r = it * 8 + (lane >> 2);
+        const unsigned long long rb = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(base), r);
+        const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
+        const uint4 val = *reinterpret_cast<const uint4*>(stg + r * 64 + ((part ^ ((r >> 1) & 3)) << 4));
+        if (ok) *reinterpret_cast<uint4*>(out + rb + part * 8) = val;
+    }
+    __syncwarp();  // the next chunk reuses the staging rows
 }
 
 template <int BN, bool CTA2, bool BRES, bool DGRAD>
@@ -409,7 +472,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_win_kernel(const __grid_cons
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, v);
                 ptx::tmem_ld_wait();
                 const int col0 = t.nt * BN + c * 32;
-                if (valid && col0 < p.Ncol) {
+                if (p.stg_off && col0 + 32 <= p.Ncol) {
+                    uint8_t* stg = smem + p.stg_off + (warp - 4) * 2048;
+                    const int f = (p.bias ? 1 : 0) | (p.residual ? 2 : 0) | (p.relu ? 4 : 0) | (p.mask ? 8 : 0);
+                    switch (f) {
+#define TCB_WIN_EPI(F) \
+    case F: store_chunk_staged<(F & 1) != 0, (F & 2) != 0, (F & 4) != 0, (F & 8) != 0>(p, orow, col0, v, valid, stg); break;
+                        TCB_WIN_EPI(0) TCB_WIN_EPI(1) TCB_WIN_EPI(2) TCB_WIN_EPI(3)
+                        TCB_WIN_EPI(4) TCB_WIN_EPI(5) TCB_WIN_EPI(6) TCB_WIN_EPI(7)
+                        TCB_WIN_EPI(8) TCB_WIN_EPI(9) TCB_WIN_EPI(10) TCB_WIN_EPI(11)
+                        TCB_WIN_EPI(12) TCB_WIN_EPI(13) TCB_WIN_EPI(14) TCB_WIN_EPI(15)
+#undef TCB_WIN_EPI
+                    }
+                } else if (valid && col0 < p.Ncol) {
                     const int f = (p.bias ? 1 : 0) | (p.residual ? 2 : 0) | (p.relu ? 4 : 0) | (p.mask ? 8 : 0);
                     switch (f) {
 #define TCB_WIN_EPI(F) \
@@ -450,6 +525,7 @@ struct WinPlan {
     uint32_t win_bytes, win_stride, b_bytes;
     int win_stages, b_stages;
     size_t smem;
+    uint32_t stg_off = 0;
 };
 
 int g_win_mode = -1;  // $TCB_WIN: 0 off, 1 on (default, N = 64 tiles), 2 every applicable geometry
@@ -538,12 +614,18 @@ WinPlan win_plan(const ConvGeom& g, int mode) {
     const size_t b_ring = q.bres ? b_all : 0;
     q.b_stages = q.bres ? 1 : 0;
     // window stages first (>= 2), then B stages (>= 3) with what is left
+    // epilogue staging tiles ($TCB_WIN_STAGE=1; off by default: the 16 KB cost a
+    // window stage and stage-1 fwd / dgrad measured 75.4 -> 77.7 / 75.9 -> 78.4 us,
+    // unlike the register epilogue of conv_tc.cu where it pays)
+    static const int env_stage = [] { const char* e = getenv("TCB_WIN_STAGE"); return e ? atoi(e) : 0; }();
+    const size_t stg = env_stage ? 8 * 2048 : 0;
+    const size_t cap = kSmemCap - stg;
     for (q.win_stages = env_wst > 1 ? std::min(env_wst, kMaxWin) : kMaxWin; q.win_stages >= 2; --q.win_stages) {
         const size_t wbytes = size_t(q.win_stages) * q.win_stride;
         if (q.bres) {
-            if (wbytes + b_ring + 1024 <= kSmemCap) break;
+            if (wbytes + b_ring + 1024 <= cap) break;
         } else {
-            const size_t left = kSmemCap - std::min(kSmemCap, wbytes + 1024);
+            const size_t left = cap - std::min(cap, wbytes + 1024);
             const int bst = static_cast<int>(std::min<size_t>(env_bst > 2 ? std::min(env_bst, kMaxB) : kMaxB,
                                                               left / q.b_bytes));
             if (bst >= 3) {
@@ -554,6 +636,8 @@ WinPlan win_plan(const ConvGeom& g, int mode) {
     }
     if (q.win_stages < 2) return q;
     q.smem = size_t(q.win_stages) * q.win_stride + (q.bres ? b_ring : size_t(q.b_stages) * q.b_bytes) + 1024;
+    q.stg_off = stg ? static_cast<uint32_t>(q.smem - 1024) : 0;
+    q.smem += stg;
     q.use = true;
     return q;
 }
@@ -629,6 +713,7 @@ cudaError_t run_win(const ConvGeom& g, const WinPlan& q, bool dgrad, const void*
     p.win_stride = q.win_stride;
     p.b_bytes = q.b_bytes;
     p.win_stages = q.win_stages;
+    p.stg_off = q.stg_off;
     p.b_stages = q.b_stages;
     p.out = out;
     p.bias = ep.bias;
