@@ -93,7 +93,10 @@ Measured measure(const ConvGeom& g, int algo, int prec, bool need_dgrad, int rep
             return conv_tf32_fwd(g, static_cast<float*>(x.p), static_cast<float*>(w.p), none,
                                  static_cast<float*>(y.p), st);
         if (algo == TCB_ALGO_GEMM)
-            return dt == DType::BF16 ? conv_tc_fwd(g, x.p, w.p, none, y.p, st)
+            // split-K forwards (fc layers) run as in the executor, through the workspace
+            return dt == DType::BF16 ? conv_tc_fwd(g, x.p, w.p, none, y.p, st,
+                                                   !conv_tc_narrow(g) && conv_tc_workspace(g, ConvMode::Fwd) ? ws.p
+                                                                                                            : nullptr)
                                      : conv_ffma_fwd(g, static_cast<float*>(x.p), static_cast<float*>(w.p),
                                                      none, static_cast<float*>(y.p), st);
         if (algo == TCB_ALGO_WINOGRAD) return winograd_fwd(g, dt, x.p, w.p, none, y.p, ws.p, st);

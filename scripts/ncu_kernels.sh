@@ -20,6 +20,7 @@ cap fwd_3x3_cta2 "conv_tc_kernel<\\(tcb::ConvMode\\)0, \\(int\\)256, \\(int\\)2,
 cap dgrad_3x3_cta2 "conv_tc_kernel<\\(tcb::ConvMode\\)1, \\(int\\)128, \\(int\\)2, \\(int\\)0, \\(bool\\)1>" 2
 cap wgrad_3x3_cta2 "conv_tc_kernel<\\(tcb::ConvMode\\)2, \\(int\\)256, \\(int\\)2, \\(int\\)0, \\(bool\\)1>" 2
 cap wgrad_1x1_cta2 "conv_tc_kernel<\\(tcb::ConvMode\\)2, \\(int\\)256, \\(int\\)1, \\(int\\)0, \\(bool\\)1>" 2
+cap dgrad_phase_staged "conv_tc_kernel<\\(tcb::ConvMode\\)1, \\(int\\)128, \\(int\\)2, \\(int\\)0, \\(bool\\)0>" 4
 cap window "conv_win_kernel|conv_win_wgrad_kernel" 2
 cap stem "conv_stem|maxpool" 3
 cap misc "split_reduce|sgd4|dgrad_empty" 4
