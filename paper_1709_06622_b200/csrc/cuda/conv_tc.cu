@@ -56,15 +56,20 @@ struct Cfg {
     static constexpr int kBBytes = BN * BK * 2 / (CTA2 ? 2 : 1);  // this CTA's share
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStages =
-        CTA2 ? (EPI == 4 ? 2 : EPI == 2 ? (BN == 256 ? 4 : 6) : (BN == 256 ? 6 : 8))
+        CTA2 ? (EPI == 4 ? 2 : EPI == 2 ? (BN == 256 ? 4 : 6) : (BN == 512 ? 4 : BN == 256 ? 6 : 8))
              : EPI == 4 ? 2
              : EPI == 2 ? (BN == 256 ? 3 : BN == 192 ? 4 : BN == 128 ? 4 : 5)
-                        : (BN == 256 ? 4 : BN == 192 ? 5 : BN == 128 ? 6 : 8);
+                        : (BN == 384 ? 3 : BN == 256 ? 4 : BN == 192 ? 5 : BN == 128 ? 6 : 8);
     static constexpr int kRingBytes = kStages * kStageBytes;
     // EPI: slot = {in0/out, in1}, 32x32 bf16 each; register epilogue: one 32x32 bf16 staging tile
     static constexpr int kEpiWarpBytes = EPI == 0 ? 2048 : EPI * 2 * 2048;
     static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
-    static constexpr uint32_t kTmemCols = BN == 192 ? 512 : 2 * BN;  // two accumulators (pow2)
+    // two accumulators (pow2); BN = 384 / 512 (wgrad double-N tiles, one unit per CTA):
+    // one accumulator, two MMAs of N = BN / 2 per k-step
+    static constexpr bool kDoubleN = BN == 384 || BN == 512;
+    static constexpr uint32_t kTmemCols = BN == 192 || kDoubleN ? 512 : 2 * BN;
+    static constexpr int kAccs = kDoubleN ? 1 : 2;
+    static constexpr int kMmaN = kDoubleN ? BN / 2 : BN;
     static constexpr size_t kSmem = size_t(kRingBytes) + kEpiBytes + 1024 + 512;
 };
 
@@ -590,6 +595,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     // B boxes of 64 N-elements: a pair's CTA takes its half
                     constexpr int kNB = CTA2 ? BN / 128 : BN / 64;
                     const int jb0 = CTA2 ? static_cast<int>(rank) * kNB : 0;
+                    // tile column of this CTA's B box j (BN = 512: boxes 0-1 feed the first
+                    // N = 256 MMA, 2-3 the second; each MMA takes 128 columns per CTA)
+                    auto bcol = [&](int j) {
+                        if constexpr (BN == 512) return (j >> 1) * 256 + static_cast<int>(rank) * 128 + (j & 1) * 64;
+                        else return (jb0 + j) * 64;
+                    };
                     if constexpr (MODE == ConvMode::Wgrad) {
                         // A = dy [P][K]: MN-major 64-channel x 64-pixel boxes (8 KB each)
                         ld2(a_smem, &p.tmap_a, tc.mt * BM, kb * BK);
@@ -597,14 +608,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                         if constexpr (LOAD == kPlain) {
 #pragma unroll
                             for (int j = 0; j < kNB; ++j)
-                                ld2(b_smem + j * 8192, &p.tmap_b, tc.nt * BN + (jb0 + j) * 64, kb * BK);
+                                ld2(b_smem + j * 8192, &p.tmap_b, tc.nt * BN + bcol(j), kb * BK);
                         } else {
                             // B = im2col(x): 64 pixels x 64 channels of one tap per box
                             const int4 px = wgrad_pixel(s, kb * BK);
                             const int pn = px.x >= 0 ? px.x / s.H : s.N;
 #pragma unroll
                             for (int j = 0; j < kNB; ++j) {
-                                int col0 = tc.nt * BN + (jb0 + j) * 64;
+                                int col0 = tc.nt * BN + bcol(j);
                                 if (col0 >= s.Ncol) col0 = 0;  // padding columns: never stored
                                 uint32_t rs, c0, r, sx;
                                 s.d_c.divmod(static_cast<uint32_t>(col0), rs, c0);
@@ -745,15 +756,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         constexpr uint32_t kMN = MODE == ConvMode::Wgrad ? 1u : 0u;
         // dgrad with TMA operands reads B (the filters) MN-major
         constexpr bool kBmn = MODE == ConvMode::Wgrad || (MODE == ConvMode::Dgrad && kTmaOnly);
-        constexpr uint32_t idesc = ptx::make_idesc(1, CTA2 ? 2 * BM : BM, BN, kMN, kBmn ? 1u : 0u);
+        constexpr uint32_t idesc = ptx::make_idesc(1, CTA2 ? 2 * BM : BM, C::kMmaN, kMN, kBmn ? 1u : 0u);
         if (!CTA2 || rank == 0) {
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
         for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
             const TileCoord tc = tile_coord<CTA2>(p, t, rank);
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
+            const int acc = it % C::kAccs;
+            const uint32_t acc_phase = (it / C::kAccs) & 1;
             ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
@@ -785,6 +796,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                             ptx::umma_f16_2sm_elect(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
                         else
                             ptx::umma_f16_elect(d_tmem, ad, bd, idesc, (kb > tc.kb_begin || k > 0) ? 1u : 0u);
+                        if constexpr (C::kDoubleN) {  // second N half: this CTA's upper B boxes
+                            constexpr uint32_t kHalfB = (CTA2 ? BN / 128 : BN / 64) / 2 * 8192;
+                            const uint64_t bd2 = ptx::sw128_desc(b_addr + kHalfB + k * 2048, 8192, 1024);
+                            if constexpr (CTA2)
+                                ptx::umma_f16_2sm_elect(d_tmem + C::kMmaN, ad, bd2, idesc,
+                                                        (kb > tc.kb_begin || k > 0) ? 1u : 0u);
+                            else
+                                ptx::umma_f16_elect(d_tmem + C::kMmaN, ad, bd2, idesc,
+                                                    (kb > tc.kb_begin || k > 0) ? 1u : 0u);
+                        }
                     }
                     if constexpr (CTA2) ptx::umma_commit_2sm_elect(&empty[stage], 3);
                     else ptx::umma_commit_elect(&empty[stage]);
@@ -854,8 +875,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 int it = 0;
                 for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
                     const TileCoord tc = tile_coord<CTA2>(p, t, rank);
-                    const int acc = it & 1;
-                    const uint32_t acc_phase = (it >> 1) & 1;
+                    const int acc = it % C::kAccs;
+                    const uint32_t acc_phase = (it / C::kAccs) & 1;
                     const int row0 = tc.mt * BM + quarter * 32;
                     ptx::mbar_wait(&tfull[acc], acc_phase);
                     ptx::tc_fence_after();
@@ -1053,8 +1074,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             int it = 0;
             for (int t = unit0; t < p.num_tiles; t += ustride, ++it) {
                 const TileCoord tc = tile_coord<CTA2>(p, t, rank);
-                const int acc = it & 1;
-                const uint32_t acc_phase = (it >> 1) & 1;
+                const int acc = it % C::kAccs;
+                const uint32_t acc_phase = (it / C::kAccs) & 1;
                 const int m = tc.mt * BM + row;
                 const bool mvalid = m < p.s.M;
                 const size_t orow = mvalid ? out_row<MODE>(p, m) : 0;
@@ -1468,7 +1489,7 @@ bool cta2_wanted(int load, int bn, int m_tiles, int kb_total) {
         const char* k = getenv("TCB_CTA2_KB");
         return k ? atoi(k) : 9;
     }();
-    return (load == kPlain || load == kIm2col) && (bn == 128 || bn == 256) && m_tiles >= 2 &&
+    return (load == kPlain || load == kIm2col) && (bn == 128 || bn == 256 || bn == 512) && m_tiles >= 2 &&
            kb_total >= min_kb;
 }
 
@@ -1496,9 +1517,12 @@ bool use_epi(const Params& p) {
     return kb <= (plain_geometry(p.s) ? g_epi_kb : g_epi_kb_spatial);
 }
 
+int wgrad_bn(const ConvShape& s);
+
 template <ConvMode MODE, int LOAD>
 cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, cudaStream_t st) {
-    const int bn = pick_bn(p.s.Ncol, !(MODE == ConvMode::Wgrad && LOAD == kGather));
+    const int bn = MODE == ConvMode::Wgrad && LOAD != kGather ? wgrad_bn(p.s)
+                                                              : pick_bn(p.s.Ncol, !(MODE == ConvMode::Wgrad && LOAD == kGather));
     if constexpr (MODE != ConvMode::Wgrad) {
         if (use_epi<MODE>(p)) {
             static const int deep_kb = [] {  // whole-share side-input prefetch up to this many k-blocks
@@ -1539,6 +1563,10 @@ cudaError_t dispatch_bn(Params& p, const void* a_matrix, const void* b_matrix, c
         const bool pair = MODE == ConvMode::Wgrad
                               ? p.cta2 != 0
                               : !p.fwd_partial && cta2_wanted(LOAD, bn, (p.s.M + BM - 1) / BM, (p.s.Kdim + BK - 1) / BK);
+        if constexpr (MODE == ConvMode::Wgrad) {
+            if (pair && bn == 512) return launch<MODE, 512, LOAD, 0, true>(p, a_matrix, b_matrix, st);
+            if (!pair && bn == 384) return launch<MODE, 384, LOAD, 0, false>(p, a_matrix, b_matrix, st);
+        }
         if (pair && bn == 256) return launch<MODE, 256, LOAD, 0, true>(p, a_matrix, b_matrix, st);
         if (pair && bn == 128) return launch<MODE, 128, LOAD, 0, true>(p, a_matrix, b_matrix, st);
     }
@@ -1573,11 +1601,29 @@ bool wgrad_pair(const ConvShape& s, int bn) {
 }
 
 // Wgrad tile width, consistent with the operand path dispatch() will pick.
+// 512-column tiles for spatial (im2col) layers (two N = 256 MMAs per k-step into
+// all of TMEM, CTA pairs only): a pair's CTA loads 16 KB of dy + 32 KB of x per
+// k-block for twice the MMA work of a 256-column tile (16 + 16 KB) -- a quarter
+// less L2 -> SM traffic per FLOP (ResNet-50 stage-4 3x3: 82.7 -> 77.3 us). 1x1
+// layers measured slower (fewer tiles -> more splits: 38.9 -> 50.9 us).
+// $TCB_WG512: 0 off, 1 when Ncol is a multiple of 512, 2 whenever Ncol >= 1024.
 int wgrad_bn(const ConvShape& s) {
     const bool tma = !force_gather() &&
                      (plain_geometry(s) || (s.C % 64 == 0 && s.R <= 16 && s.S <= 16 && s.ph <= 15 &&
                                             s.pw <= 15));
-    return pick_bn(s.Ncol, tma);
+    const int bn = pick_bn(s.Ncol, tma);
+    static const int wg512 = [] {
+        const char* e = getenv("TCB_WG512");
+        return e ? atoi(e) : 1;
+    }();
+    if (tma && !plain_geometry(s) && bn == 256 && wg512 > 0 && (wg512 == 2 ? s.Ncol >= 1024 : s.Ncol % 512 == 0) &&
+        cta2_wanted(plain_geometry(s) ? kPlain : kIm2col, 256, (s.M + BM - 1) / BM, (s.Kdim + BK - 1) / BK))
+        return 512;
+    // single-CTA spatial tiles of 2 x 192 columns where no pair forms (one 128-row M tile)
+    if (tma && !plain_geometry(s) && bn == 192 && wg512 > 0 && s.Ncol % 384 == 0 &&
+        !cta2_wanted(kIm2col, 192, (s.M + BM - 1) / BM, (s.Kdim + BK - 1) / BK))
+        return 384;
+    return bn;
 }
 
 template <ConvMode MODE>

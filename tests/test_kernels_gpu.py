@@ -281,6 +281,32 @@ def test_fc_forward_split_k(oracle, spec):
     assert rel_err(_host(y0), oracle.conv_fwd(gd, x, wt)) <= 1e-2
 
 
+@pytest.mark.parametrize("spec", [(12, 7, 512, 256, 3, 1, 512), (4, 14, 512, 512, 3, 1, 512),
+                                  (8, 9, 512, 384, 3, 1, 512), (4, 12, 128, 128, 3, 1, 384),
+                                  (3, 11, 128, 96, 3, 1, 384)],
+                         ids=["3x3_c512_k256", "3x3_c512_k512", "3x3_k384_odd_pairs", "3x3_c128_384", "3x3_k96_384"])
+def test_wgrad_double_n_tiles(oracle, spec):
+    """Spatial weight gradients on double-N tiles: N = R*S*C a multiple of 512 as
+    512-column CTA-pair tiles (two N = 256 MMAs per k-step into all of TMEM, B
+    boxes interleaved per MMA half), a multiple of 384 with one 128-row M tile
+    as 384-column single-CTA tiles (two N = 192 MMAs): vs the fp64 oracle,
+    bitwise repeatable."""
+    dev = _dev()
+    n, hw, c, k, r, pad, bn = spec
+    g = dev.geom(n, hw, hw, c, k, r, pad=pad)
+    gd = g.as_dict()
+    plan = dev.ConvPlan(g, "gemm", "bf16")
+    x = _rand(oracle, (n, hw, hw, c), 1, 1.0, True)
+    dy = _rand(oracle, (n, g.ho, g.wo, k), 5, 1.0, True)
+    xd, dyd = _to_dev(x, torch.bfloat16), _to_dev(dy, torch.bfloat16)
+    dw = plan.wgrad(dyd, xd)
+    info = dev.last_launch()
+    assert info["mode"] == 2 and info["bn"] == bn and info["cta2"] == (1 if bn == 512 else 0), info
+    refw = oracle.conv_wgrad(gd, dy, x)
+    assert rel_err(_host(dw), refw) <= 1e-3
+    assert torch.equal(dw, plan.wgrad(dyd, xd))
+
+
 def test_fill_and_labels_bit_exact(oracle):
     dev = _dev()
     for tag, lo, hi in ((1, -1.0, 1.0), (99, -0.05, 0.05), (7, 0.0, 3.0)):
