@@ -18,11 +18,14 @@ pytestmark = pytest.mark.gpu
 GUARD = 1 << 20  # bytes
 CASES = [  # n h w c k r pad stride
     (3, 56, 56, 64, 64, 3, 1, 1),     # window fwd / dgrad / wgrad
-    (2, 28, 28, 128, 128, 3, 1, 1),   # im2col TMA, CTA pairs
+    (2, 28, 28, 128, 128, 3, 1, 1),   # im2col TMA, CTA pairs, 384-column wgrad tiles
     (4, 14, 14, 256, 1024, 1, 0, 1),  # plain TMA, TMA-store epilogue, split-K wgrad
     (2, 28, 28, 256, 512, 1, 0, 2),   # strided 1x1: dgrad phases incl. empty ones
     (3, 9, 11, 40, 72, 3, 1, 2),      # gather path, ragged tails
     (2, 35, 35, 64, 64, 5, 2, 1),     # 5x5 window
+    (8, 7, 7, 512, 4096, 7, 0, 1),    # fully connected: split-K forward + reduce
+    (4, 14, 14, 512, 512, 3, 1, 1),   # 512-column CTA-pair wgrad tiles
+    (2, 28, 28, 128, 128, 3, 1, 2),   # strided 3x3 dgrad phases, staged register epilogue
 ]
 
 
