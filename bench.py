@@ -522,7 +522,7 @@ KNOB_DEFAULTS = {  # the executor's A/B switches (read once from the environment
     "TCB_GRAPH": "1 (replay the step as a CUDA graph)", "TCB_PDL": "1 (programmatic dependent launch)",
     "TCB_WIN": "1 (window conv for 64-column stride-1 tiles)", "TCB_CTA2": "1", "TCB_CTA2_KB": "9",
     "TCB_CONV_EPI_KB": "12", "TCB_CONV_EPI_KB_SPATIAL": "24", "TCB_EPI_DEEP_KB": "2",
-    "TCB_SPLIT_MIN_KB": "4", "TCB_FWD_SPLIT": "1", "TCB_EPI_STAGE": "1", "TCB_WG512": "1", "TCB_WIN_STAGE": "0", "TCB_CONV_FORCE_GATHER": "0", "TCB_FUSED_SPLIT_REDUCE": "0",
+    "TCB_SPLIT_MIN_KB": "4", "TCB_FWD_SPLIT": "1", "TCB_EPI_STAGE": "1", "TCB_WG512": "1", "TCB_BWD_CONCURRENT": "1", "TCB_DGRAD_CONCURRENT": "2", "TCB_WIN_STAGE": "0", "TCB_CONV_FORCE_GATHER": "0", "TCB_FUSED_SPLIT_REDUCE": "0",
     "TCB_NVLS_TIMEOUT_MS": "10000"}
 
 
