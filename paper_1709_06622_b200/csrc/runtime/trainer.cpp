@@ -977,8 +977,10 @@ int backward(tcb_trainer* t, cudaStream_t st) {
                 const char* e = getenv("TCB_BWD_CONCURRENT");
                 return e ? atoi(e) : 1;
             }();
+            // (per-layer timing runs keep the passes sequential so each one's events
+            // bracket that pass alone)
             const bool conc = bwd_conc > 0 && t->bf16 && nd.algo_id == TCB_ALGO_GEMM && nd.need_dgrad &&
-                              !t->overlap_active();
+                              !t->overlap_active() && !t->layer_timing;
             if (conc && !t->wg_stream) {
                 TRY_CUDA(cudaStreamCreateWithFlags(&t->wg_stream, cudaStreamNonBlocking));
                 TRY_CUDA(cudaEventCreateWithFlags(&t->wg_fork, cudaEventDisableTiming));
